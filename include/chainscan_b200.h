@@ -1,0 +1,212 @@
+/* chainscan_b200 -- C-ABI of the B200-native parallel-in-time MCMC hot path.
+ *
+ * The drop-in boundary for arXiv 2508.18413's chainscan package
+ * (/root/reference/pkg/src/chainscan).  Every entry point replaces one call
+ * the reference makes on its hot path; the replaced interface is cited as
+ * file:line beside each declaration.  Plain pointers and sizes only: device
+ * buffers are caller-owned, every call is ordered on the given CUDA stream
+ * (`stream` is a cudaStream_t, NULL = legacy default stream), and nothing is
+ * allocated except inside cs_deer_solve's caller-sized workspace.
+ *
+ * Status codes map onto the reference's exceptions in the Python host layer
+ * (paper_2508_18413_b200/_lib.py): CS_ERR_STRUCTURAL -> StructuralError
+ * (core.py:30), CS_ERR_CONFIG -> ConfigurationError (noise.py:30),
+ * CS_ERR_DIVERGED -> ChainDivergedError(step, iteration) (core.py:34-44).
+ * cs_last_error() returns a thread-local message for the last failure.
+ *
+ * dtype: CS_F32 / CS_F64 is the storage type of states and scan elements.
+ * Gate margins, noise transforms and scan carries are always computed in f64.
+ */
+#ifndef CHAINSCAN_B200_H
+#define CHAINSCAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { CS_OK = 0, CS_ERR_STRUCTURAL = 1, CS_ERR_CONFIG = 2, CS_ERR_DIVERGED = 3,
+       CS_ERR_CUDA = 4, CS_ERR_INDEX = 5 };
+enum { CS_F32 = 0, CS_F64 = 1 };
+/* noise.py:83-104 distribution kinds */
+enum { CS_NOISE_NORMAL = 0, CS_NOISE_UNIFORM = 1, CS_NOISE_CHI2 = 2, CS_NOISE_LOG_UNIFORM = 3 };
+/* targets.py:46 model kinds */
+enum { CS_TARGET_STD_NORMAL = 0, CS_TARGET_GAUSSIAN = 1, CS_TARGET_ROSENBROCK = 2,
+       CS_TARGET_MOG = 3, CS_TARGET_BLR = 4 };
+/* samplers.py kernels */
+enum { CS_SYS_MALA = 0, CS_SYS_HMC = 1, CS_SYS_LEAPFROG = 2, CS_SYS_GIBBS = 3 };
+/* core.py:27 JACOBIAN_MODES */
+enum { CS_MODE_DENSE = 0, CS_MODE_DIAG = 1, CS_MODE_BLOCK = 2 };
+/* cs_deer_result.status */
+enum { CS_RUN_MAXITERS = 0, CS_RUN_CONVERGED = 1, CS_RUN_DIVERGED = 2 };
+/* why the Newton loop stopped (deer.py:265-286) */
+enum { CS_STOP_MAXITERS = 0, CS_STOP_PICARD = 1, CS_STOP_NOFAIL = 2, CS_STOP_ERROR = 3 };
+/* divergence kinds reported in cs_deer_result.err_kind */
+enum { CS_DIV_NONE = 0, CS_DIV_PROPOSAL = 1, CS_DIV_STEP = 2, CS_DIV_JACOBIAN = 3, CS_DIV_GUARD = 4 };
+
+/* A compiled target model (targets.py:290-308, model_logp_grad_hvp).
+ * All parameter arrays are device pointers to f64. */
+typedef struct cs_target {
+  int32_t kind;
+  int32_t dim;
+  double a, b, scale1, scale2;   /* rosenbrock (targets.py:92-104)           */
+  const double *mu;              /* gaussian mean (dim)                      */
+  const double *chol;            /* gaussian L, precision = L L^T (dim x dim) */
+  const double *prec;            /* gaussian P = L L^T (dim x dim)           */
+  int32_t n_comp;                /* mog K (targets.py:107-127)               */
+  const double *means;           /* (K, dim)                                 */
+  const double *variances;       /* (K)                                      */
+  const double *logw;            /* (K) log weights                          */
+  const double *lognorm;         /* (K) -dim/2 log(2 pi var_k)               */
+  int64_t n_data;                /* blr N (targets.py:130-146)               */
+  const double *X;               /* (N, dim)                                 */
+  const double *y;               /* (N)                                      */
+  double prior_precision;
+} cs_target;
+
+/* A transition system (core.py:61-160 TransitionSystem and its subclasses in
+ * samplers.py).  Noise is the pre-drawn sequence, one row per step t = 0..T
+ * (noise.py:107-113: step t reads index t): `noise_vec` is xi (MALA) or
+ * momentum (HMC), shape (T+1, model dim), in the call's dtype; `noise_logu`
+ * is log(u) of the gate uniform, shape (T+1), f64.  Gibbs reads
+ * g_tau (T+1), xi_mu (T+1), xi_theta (T+1, S), g_sigma (T+1, S) in the
+ * call's dtype and `gibbs` = [nu0, tau0_sq, mu0, kappa0, alpha0, sigma0_sq,
+ * S, n, xbar[S], ss[S]] in f64 (samplers.py:416-461). */
+typedef struct cs_system {
+  int32_t kind;
+  int32_t dim;                   /* state dimension (leapfrog: 2 x model dim) */
+  cs_target target;
+  double eps;
+  int32_t L;                     /* leapfrog steps per HMC proposal          */
+  const double *mass;            /* (model dim) or NULL for ones             */
+  uint64_t seed;                 /* NoiseTable seed = diag Hutchinson probe seed
+                                    (deer.py:172-175 uses system.noise.seed)   */
+  uint64_t probe_seed;           /* LeapfrogSystem.probe_seed for the block
+                                    estimate (samplers.py:213-214, 290-293)     */
+  int64_t T;
+  const void *noise_vec;
+  const double *noise_logu;
+  const void *g_tau, *xi_mu, *xi_theta, *g_sigma;
+  const double *gibbs;
+} cs_system;
+
+/* DeerConfig (deer.py:55-93), validated on the host. */
+typedef struct cs_deer_config {
+  int32_t mode;
+  double atol, rtol;
+  int32_t max_iters;
+  int32_t hutchinson_samples;
+  double damping;
+  double clip;                   /* +inf = no clipping                       */
+  const double *preconditioner;  /* device (dim) or NULL                     */
+} cs_deer_config;
+
+typedef struct cs_deer_result {
+  int32_t iterations;            /* counted Newton updates (deer.py:272)     */
+  int32_t status;                /* CS_RUN_*                                 */
+  int32_t err_kind;              /* CS_DIV_*                                 */
+  int64_t err_step;              /* first offending step (1-based), -1 none  */
+  int32_t err_iteration;         /* ChainDivergedError.iteration, -1 = None  */
+  int32_t launches;              /* kernels launched by the call             */
+  double guard_dmax, guard_d0;
+  int32_t stop_reason;           /* CS_STOP_*                                */
+  int32_t grid_blocks;           /* persistent CTAs used                     */
+  int32_t steps_per_thread;      /* contiguous steps folded per thread       */
+  int32_t kept_in_registers;     /* 1 = elements kept across the grid sync   */
+} cs_deer_result;
+
+const char *cs_last_error(void);
+int cs_version(void);
+int cs_device_sm_count(int *out);
+
+/* ---- counter-based noise (noise.py:50-80, 140-156, 159-171) ------------- */
+/* out[(i*count + k)] = value k of the slot at step t0+i; f64 always except
+ * dtype-typed variants below.  CS_NOISE_LOG_UNIFORM writes log(u) (the gate's
+ * log u, samplers.py:116). */
+int cs_noise_fill(int kind, uint64_t seed, uint64_t slot_id, int64_t t0, int64_t nt,
+                  int32_t count, double df, int dtype, void *out, void *stream);
+/* z[i, d] = rademacher_probe(seed, iteration, ts[i], sample, dim)[i, d];
+ * ts == NULL means ts[i] = t0 + i. */
+int cs_rademacher_fill(uint64_t seed, int64_t iteration, const int64_t *ts, int64_t t0,
+                       int64_t n, int32_t sample, int32_t dim, int dtype, void *out,
+                       void *stream);
+
+/* ---- affine scans (pscan.py:273-354 parallel_affine_solve) -------------- */
+size_t cs_scan_workspace_bytes(int mode, int dtype, int64_t T, int32_t D);
+int cs_scan_diag(int dtype, const void *j, const void *u, const void *s0, void *out,
+                 int64_t T, int32_t D, void *ws, size_t ws_bytes, void *stream);
+int cs_scan_block(int dtype, const void *a, const void *b, const void *c, const void *d,
+                  const void *u, const void *s0, void *out, int64_t T, int32_t D,
+                  void *ws, size_t ws_bytes, void *stream);
+int cs_scan_dense(int dtype, const void *J, const void *u, const void *s0, void *out,
+                  int64_t T, int32_t D, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- Newton-update building blocks (deer.py:107-208, 273-277) ----------- */
+/* The three reductions below write into caller-owned DEVICE scalars (the host
+ * reads them once per iteration, after the stream work it needs is queued).
+ * First row (0-based) with a non-finite entry, INT64_MAX if none (deer.py:135-144). */
+int cs_first_nonfinite_row(int dtype, const void *x, int64_t n, int64_t width,
+                           int64_t *d_first, void *stream);
+/* converged(prev, next): *d_notok = #entries with !(|next-prev| <= atol + rtol|next|),
+ * *d_dmax = max |next-prev| (NaN propagates) (deer.py:107-115). */
+int cs_converged(int dtype, const void *prev, const void *next, int64_t n, double atol,
+                 double rtol, uint32_t *d_notok, double *d_dmax, void *stream);
+/* Post-update bookkeeping (deer.py:273-277): rows with any |next-guess| > atol +
+ * rtol|next| get last_fail[t] = iteration; *d_fail_rows counts them, *d_dmax as above. */
+int cs_update_bookkeeping(int dtype, const void *guess, const void *next, int64_t T, int32_t D,
+                          double atol, double rtol, int32_t iteration, int32_t *last_fail,
+                          uint32_t *d_fail_rows, double *d_dmax, void *stream);
+/* Element formation with preconditioner, damping and clip in the reference's
+ * order; u = f - Jhat prev (deer.py:161-204).  prev = [s0; guess[:-1]]. */
+int cs_form_diag(int dtype, const void *est, const void *f, const void *s0, const void *guess,
+                 int64_t T, int32_t D, const double *pre, double damping, double clip,
+                 void *j, void *u, void *stream);
+int cs_form_dense(int dtype, const void *J_in, const void *f, const void *s0, const void *guess,
+                  int64_t T, int32_t D, const double *pre, double damping, double clip,
+                  void *J, void *u, void *stream);
+int cs_form_block(int dtype, const void *a_in, const void *b_in, const void *c_in,
+                  const void *d_in, const void *f, const void *s0, const void *guess,
+                  int64_t T, int32_t D, const double *pre, double damping, double clip,
+                  void *a, void *b, void *c, void *d, void *u, void *stream);
+/* est = (first ? 0 : est) + z * jz, then est /= final_div when final_div > 0
+ * (hutchinson_diag, deer.py:127-132). */
+int cs_hutchinson_accumulate(int dtype, void *est, const void *z, const void *jz, int64_t n,
+                             int32_t first, double final_div, void *stream);
+
+/* ---- fused transition systems (samplers.py) ----------------------------- */
+/* f_t for rows ts[i] (or t0+i) at states S (n, dim) -> out (n, dim).
+ * *bad_step receives the first step whose proposal / trajectory was
+ * non-finite (samplers.py:101-105, 332-336) or -1. */
+int cs_system_step(const cs_system *sys, int dtype, const int64_t *ts, int64_t t0, int64_t n,
+                   const void *S, void *out, int64_t *bad_step, void *stream);
+/* Solver-form JVP (hard gate + sigmoid' bend), samplers.py:129-145, 353-384,
+ * 194-200, 593-627.  relaxed != 0 uses the sigmoid gate (relaxed_jvp_batch). */
+int cs_system_jvp(const cs_system *sys, int dtype, const int64_t *ts, int64_t t0, int64_t n,
+                  const void *S, const void *V, void *out, int32_t relaxed, void *stream);
+/* relaxed_step_batch (samplers.py:124-127, 348-351). */
+int cs_system_relaxed_step(const cs_system *sys, int dtype, const int64_t *ts, int64_t t0,
+                           int64_t n, const void *S, void *out, void *stream);
+/* LeapfrogSystem.block_jacobian_batch (samplers.py:202-222). */
+int cs_system_block_jacobian(const cs_system *sys, int dtype, const int64_t *ts, int64_t t0,
+                             int64_t n, const void *S, int32_t n_samples, int64_t iteration,
+                             void *a, void *b, void *c, void *d, void *stream);
+/* sequential_evaluate (core.py:163-184) as one device-resident chain walk. */
+int cs_system_sequential(const cs_system *sys, int dtype, const void *s0, int64_t T,
+                         void *out, int64_t *bad_step, void *stream);
+
+/* ---- whole-chain Newton solve (deer.py:230-328, run_deer, no window) ---- */
+/* One cooperative persistent kernel runs every Newton iteration on device:
+ * fused f_t + Jacobian estimate + element formation, block scan with grid-wide
+ * carry, convergence test and bookkeeping; one host sync at the end. */
+size_t cs_deer_workspace_bytes(const cs_system *sys, int dtype, int32_t max_iters);
+int cs_deer_supported(const cs_system *sys, int mode, int dtype);
+int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, const void *s0,
+                  void *trace, int32_t *per_step_converged_at, double *delta_history,
+                  void *ws, size_t ws_bytes, cs_deer_result *res, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

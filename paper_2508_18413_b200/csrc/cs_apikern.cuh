@@ -1,0 +1,196 @@
+// Batched TransitionSystem entry points (core.py:104-152) as one-thread-per-row
+// kernels over the fused system objects, plus the sequential chain walk
+// (core.py:163-184) and the persistent-solver launcher.
+#pragma once
+#include "cs_solver.cuh"
+
+namespace cs {
+
+constexpr int kRowThreads = 128;
+
+template <class Sys, int MD, typename ST>
+CS_D void load_row_ro(const Sys &sys, const ST *row, double (&x)[MD]) {
+#pragma unroll
+  for (int k = 0; k < MD; ++k) {
+    const int m = sys.mem_index(k);
+    x[k] = m >= 0 ? (double)row[m] : 0.0;
+  }
+}
+template <class Sys, int MD, typename ST>
+CS_D void store_row(const Sys &sys, ST *row, const double (&x)[MD]) {
+#pragma unroll
+  for (int k = 0; k < MD; ++k) {
+    const int m = sys.mem_index(k);
+    if (m >= 0) row[m] = (ST)x[k];
+  }
+}
+
+template <class Sys, int MD, typename ST>
+__global__ void __launch_bounds__(kRowThreads)
+k_sys_step(cs_system s, const int64_t *ts, int64_t t0, int64_t n, const ST *S, ST *out,
+           long long *bad, int relaxed) {
+  const int64_t i = (int64_t)blockIdx.x * kRowThreads + threadIdx.x;
+  if (i >= n) return;
+  const Sys sys = SysFactory<Sys>::make(s);
+  const int D = s.dim;
+  const int64_t t = ts ? ts[i] : t0 + i;
+  double x[MD], f[MD];
+  load_row_ro<Sys, MD, ST>(sys, S + i * D, x);
+  typename Sys::Aux aux;
+  const bool ok = sys.prepare(t, x, aux);
+  if (!ok && bad) atomicMin(bad, (long long)t);
+  if (relaxed) sys.relaxed_f(aux, f);
+  else sys.f(aux, f);
+  store_row<Sys, MD, ST>(sys, out + i * D, f);
+}
+
+template <class Sys, int MD, typename ST>
+__global__ void __launch_bounds__(kRowThreads)
+k_sys_jvp(cs_system s, const int64_t *ts, int64_t t0, int64_t n, const ST *S, const ST *V,
+          ST *out, int relaxed) {
+  const int64_t i = (int64_t)blockIdx.x * kRowThreads + threadIdx.x;
+  if (i >= n) return;
+  const Sys sys = SysFactory<Sys>::make(s);
+  const int D = s.dim;
+  const int64_t t = ts ? ts[i] : t0 + i;
+  double x[MD], v[1][MD], o[1][MD];
+  load_row_ro<Sys, MD, ST>(sys, S + i * D, x);
+  load_row_ro<Sys, MD, ST>(sys, V + i * D, v[0]);
+  typename Sys::Aux aux;
+  sys.prepare(t, x, aux);
+  sys.template jvp_many<1>(aux, v, o, 1, relaxed != 0);
+  store_row<Sys, MD, ST>(sys, out + i * D, o[0]);
+}
+
+template <class Sys, int MD, typename ST>
+__global__ void __launch_bounds__(kRowThreads)
+k_sys_block(cs_system s, const int64_t *ts, int64_t t0, int64_t n, const ST *S, int nsamp,
+            int64_t iteration, ST *a, ST *b, ST *c, ST *d) {
+  if constexpr (HasBlock<Sys>::value) {
+    const int64_t i = (int64_t)blockIdx.x * kRowThreads + threadIdx.x;
+    if (i >= n) return;
+    const Sys sys = SysFactory<Sys>::make(s);
+    constexpr int H = MD / 2;
+    const int h = s.dim / 2;
+    const int64_t t = ts ? ts[i] : t0 + i;
+    double x[MD];
+    load_row_ro<Sys, MD, ST>(sys, S + i * s.dim, x);
+    typename Sys::Aux aux;
+    sys.prepare(t, x, aux);
+    double ba[H], bb[H], bc[H], bd[H];
+    sys.block(aux, t, nsamp, iteration, ba, bb, bc, bd);
+#pragma unroll
+    for (int k = 0; k < H; ++k)
+      if (k < h) {
+        a[i * h + k] = (ST)ba[k];
+        b[i * h + k] = (ST)bb[k];
+        c[i * h + k] = (ST)bc[k];
+        d[i * h + k] = (ST)bd[k];
+      }
+  }
+}
+
+// sequential_evaluate: one thread walks the chain; stops at the first
+// non-finite proposal/state (core.py:178-182, samplers.py:101-105).
+template <class Sys, int MD, typename ST>
+__global__ void k_sys_seq(cs_system s, const ST *s0, int64_t T, ST *out, long long *bad) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const Sys sys = SysFactory<Sys>::make(s);
+  const int D = s.dim;
+  double x[MD];
+  load_row_ro<Sys, MD, ST>(sys, s0, x);
+  for (int64_t t = 1; t <= T; ++t) {
+    typename Sys::Aux aux;
+    bool ok = sys.prepare(t, x, aux);
+    sys.f(aux, x);
+#pragma unroll
+    for (int k = 0; k < MD; ++k)
+      if (sys.mem_index(k) >= 0) ok &= finite(x[k]);
+    if (!ok) { *bad = t; return; }
+    store_row<Sys, MD, ST>(sys, out + (t - 1) * D, x);
+  }
+}
+
+struct SysCall {
+  int op;  // 0 step, 1 jvp, 2 block, 3 sequential
+  const int64_t *ts;
+  int64_t t0, n;
+  const void *S, *V;
+  void *out, *out_b, *out_c, *out_d;
+  long long *bad;
+  int relaxed, nsamp;
+  int64_t iteration;
+};
+
+template <class Sys, int MD, typename ST>
+cudaError_t run_syscall(const cs_system &s, const SysCall &c, cudaStream_t st) {
+  const unsigned grid = (unsigned)((c.n + kRowThreads - 1) / kRowThreads);
+  if (c.op != 3 && c.n == 0) return cudaSuccess;
+  switch (c.op) {
+    case 0:
+      k_sys_step<Sys, MD, ST><<<grid, kRowThreads, 0, st>>>(s, c.ts, c.t0, c.n, (const ST *)c.S,
+                                                          (ST *)c.out, c.bad, c.relaxed);
+      break;
+    case 1:
+      k_sys_jvp<Sys, MD, ST><<<grid, kRowThreads, 0, st>>>(s, c.ts, c.t0, c.n, (const ST *)c.S,
+                                                         (const ST *)c.V, (ST *)c.out, c.relaxed);
+      break;
+    case 2:
+      k_sys_block<Sys, MD, ST><<<grid, kRowThreads, 0, st>>>(s, c.ts, c.t0, c.n, (const ST *)c.S,
+                                                           c.nsamp, c.iteration, (ST *)c.out,
+                                                           (ST *)c.out_b, (ST *)c.out_c, (ST *)c.out_d);
+      break;
+    default:
+      k_sys_seq<Sys, MD, ST><<<1, 1, 0, st>>>(s, (const ST *)c.S, c.n, (ST *)c.out, c.bad);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// persistent solver launch: pick register-kept vs recompute variant and the
+// co-resident grid from the occupancy calculator.
+struct SolvePick {
+  int nblocks, seg, keep;
+};
+
+template <class Sys, int MODE, int MD, typename ST>
+cudaError_t launch_solve(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *pick) {
+  // register-kept elements only pay off (and only fit) for narrow states
+  constexpr bool kKeepOK = MD <= 4;
+  auto kr = deer_persistent<Sys, MODE, MD, ST, false>;
+  int bk = 0, br = 0;
+  cudaError_t e;
+  if constexpr (kKeepOK) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, deer_persistent<Sys, MODE, MD, ST, true>,
+                                                      kSolveThreads, 0);
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, kr, kSolveThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (bk > 8) bk = 8;
+  if (br > 8) br = 8;
+  const int64_t T = A.T;
+  int64_t cap = (int64_t)bk * sms;
+  int64_t seg = cap > 0 ? (T + cap * kSolveThreads - 1) / (cap * kSolveThreads) : kSegKeep + 1;
+  bool keep = cap > 0 && seg <= kSegKeep;
+  if (!keep) {
+    cap = (int64_t)br * sms;
+    if (cap <= 0) return cudaErrorInvalidConfiguration;
+    seg = (T + cap * kSolveThreads - 1) / (cap * kSolveThreads);
+  }
+  if (seg < 1) seg = 1;
+  const int64_t nb = (T + (int64_t)kSolveThreads * seg - 1) / ((int64_t)kSolveThreads * seg);
+  A.seg = (int)seg;
+  A.nblocks = (int)(nb < 1 ? 1 : nb);
+  pick->nblocks = A.nblocks;
+  pick->seg = A.seg;
+  pick->keep = keep;
+  void *args[] = {&A};
+  void *fn = (void *)kr;
+  if constexpr (kKeepOK) {
+    if (keep) fn = (void *)deer_persistent<Sys, MODE, MD, ST, true>;
+  }
+  return cudaLaunchCooperativeKernel(fn, dim3(A.nblocks), dim3(kSolveThreads), args, 0, st);
+}
+
+}  // namespace cs

@@ -1,0 +1,74 @@
+// Shared device/host helpers for the chainscan_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+
+#include "../../include/chainscan_b200.h"
+
+#define CS_HD __host__ __device__ __forceinline__
+#define CS_D __device__ __forceinline__
+
+namespace cs {
+
+constexpr int64_t kNoStep = INT64_MAX;   // "no offending step" sentinel for atomicMin
+
+// ---- storage <-> f64 ------------------------------------------------------
+template <typename ST> CS_D double ld(const ST *p, int64_t i) { return (double)__ldg(p + i); }
+template <typename ST> CS_D void st(ST *p, int64_t i, double v) { p[i] = (ST)v; }
+// coherent (non-.nc) load for buffers written earlier in the same launch
+template <typename ST> CS_D double ldv(const ST *p, int64_t i) {
+  return (double)*((const volatile ST *)(p + i));
+}
+
+// ---- numerics mirroring numpy / scipy --------------------------------------
+CS_D double logaddexp0(double x) {  // np.logaddexp(0, x)
+  if (x != x) return x;
+  return fmax(x, 0.0) + log1p(exp(-fabs(x)));
+}
+CS_D double log_sigmoid(double z) { return -logaddexp0(-z); }            // samplers.py:53-54
+CS_D double sigmoid_prime(double z) { return exp(log_sigmoid(z) + log_sigmoid(-z)); }  // :57-59
+CS_D double expit(double x) { return 1.0 / (1.0 + exp(-x)); }             // scipy.special.expit
+CS_D double clipv(double x, double c) { return fmin(fmax(x, -c), c); }    // np.clip
+
+// ---- atomics ------------------------------------------------------------------
+// max of non-negative doubles via their bit patterns (NaN with clear sign bit
+// sorts above +inf, so a NaN gap propagates like numpy's max).
+CS_D void atomic_max_nonneg(unsigned long long *addr, double v) {
+  atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+CS_D void atomic_min_i64(long long *addr, long long v) { atomicMin(addr, v); }
+
+// ---- warp reductions -------------------------------------------------------------
+CS_D double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+CS_D unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+CS_D long long warp_min_i64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+CS_D int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+CS_D bool finite(double x) { return isfinite(x); }
+
+}  // namespace cs

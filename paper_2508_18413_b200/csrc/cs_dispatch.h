@@ -1,0 +1,8 @@
+// Dispatch declarations shared by the generated instantiation units.
+#pragma once
+#include "cs_apikern.cuh"
+
+namespace cs {
+cudaError_t syscall_gibbs(const cs_system &, int dtype, int md, const SysCall &, cudaStream_t);
+cudaError_t solve_gibbs(int dtype, int md, int mode, void *args, int sms, cudaStream_t, SolvePick *);
+}  // namespace cs

@@ -1,0 +1,655 @@
+// Affine scans s_t = J_t s_{t-1} + u_t on B200 (pscan.py:273-354).
+//
+// Three element carriers (pscan.py:100-173):
+//   diag      j,u (T,D)                       -> scan_rows<DIAG>  (D <= 64)
+//   block2x2  a,b,c,d (T,D), u (T,2D) [x|v]   -> scan_rows<BLOCK> (D <= 64)
+//   both, wide D > 64                         -> scan_cols<...>
+//   dense     J (T,D,D), u (T,D), D <= 8      -> scan_dense_small<MD>
+// All are single-pass: each tile is read from HBM once into shared memory (or
+// registers), reduced, linked to its predecessors by decoupled look-back,
+// replayed and written once -- 12 B/element (diag, f32) of algorithmic
+// traffic.  Carries and composition run in f64 regardless of storage type.
+#include "cs_lookback.cuh"
+#include "cs_scan.cuh"
+
+namespace cs {
+
+constexpr int kScanThreads = 256;
+
+// ---------------------------------------------------------------------------
+// per-column affine monoid, diag and block2x2
+template <int VAR> struct ColElem;
+
+template <> struct ColElem<SCAN_DIAG> {
+  static constexpr int W = 2;  // j, u
+  double j, u;
+  CS_D void ident() { j = 1.0; u = 0.0; }
+  // this <- e o this  (apply this first, then e)
+  CS_D void push(double ej, double eu) { u = ej * u + eu; j = ej * j; }
+  CS_D void push(const ColElem &e) { push(e.j, e.u); }
+  // this <- this o e  (apply e first)
+  CS_D void pre(const ColElem &e) { u = j * e.u + u; j = j * e.j; }
+  CS_D void apply(double &x) const { x = j * x + u; }
+  CS_D void store(double *p) const { p[0] = j; p[1] = u; }
+  CS_D void load(const double *p) { j = p[0]; u = p[1]; }
+  CS_D void load_cg(const double *p) { j = ld_cg(p); u = ld_cg(p + 1); }
+};
+
+template <> struct ColElem<SCAN_BLOCK> {
+  static constexpr int W = 6;
+  double A, B, C, E, ux, uv;
+  CS_D void ident() { A = 1.0; B = 0.0; C = 0.0; E = 1.0; ux = 0.0; uv = 0.0; }
+  CS_D void push(double a, double b, double c, double d, double px, double pv) {
+    // compose(e_t, run): (a,b;c,d) * (A,B;C,E), u = M_t u + u_t  (_scan_kernels.py:118-126)
+    double An = a * A + b * C, Bn = a * B + b * E, Cn = c * A + d * C, En = c * B + d * E;
+    double xn = a * ux + b * uv + px, vn = c * ux + d * uv + pv;
+    A = An; B = Bn; C = Cn; E = En; ux = xn; uv = vn;
+  }
+  CS_D void push(const ColElem &e) { push(e.A, e.B, e.C, e.E, e.ux, e.uv); }
+  CS_D void pre(const ColElem &e) {
+    double An = A * e.A + B * e.C, Bn = A * e.B + B * e.E, Cn = C * e.A + E * e.C,
+           En = C * e.B + E * e.E;
+    double xn = A * e.ux + B * e.uv + ux, vn = C * e.ux + E * e.uv + uv;
+    A = An; B = Bn; C = Cn; E = En; ux = xn; uv = vn;
+  }
+  CS_D void apply(double &x, double &v) const {
+    double xn = A * x + B * v + ux, vn = C * x + E * v + uv;
+    x = xn; v = vn;
+  }
+  CS_D void store(double *p) const { p[0] = A; p[1] = B; p[2] = C; p[3] = E; p[4] = ux; p[5] = uv; }
+  CS_D void load(const double *p) { A = p[0]; B = p[1]; C = p[2]; E = p[3]; ux = p[4]; uv = p[5]; }
+  CS_D void load_cg(const double *p) {
+    A = ld_cg(p); B = ld_cg(p + 1); C = ld_cg(p + 2); E = ld_cg(p + 3); ux = ld_cg(p + 4); uv = ld_cg(p + 5);
+  }
+};
+
+// look-back for column c of tile b; returns the entry state(s) of the column.
+template <int VAR, typename ST>
+CS_D void lookback_col(const LookbackWs &ws, int64_t b, int ncol, int c, int SW, const ST *s0,
+                       double &x, double &v) {
+  ColElem<VAR> acc;
+  acc.ident();
+  int64_t p = b - 1;
+  while (p >= 0) {
+    int st;
+    do { st = ld_acquire(ws.status + p); } while (st == 0);
+    if (st == 2) {
+      x = ld_cg(ws.exit + p * SW + c);
+      if (VAR == SCAN_BLOCK) v = ld_cg(ws.exit + p * SW + ncol + c);
+      break;
+    }
+    ColElem<VAR> e;
+    e.load_cg(ws.agg + (p * ncol + c) * ColElem<VAR>::W);
+    acc.pre(e);
+    --p;
+  }
+  if (p < 0) {
+    x = (double)s0[c];
+    if (VAR == SCAN_BLOCK) v = (double)s0[ncol + c];
+  }
+  if constexpr (VAR == SCAN_DIAG) acc.apply(x);
+  else acc.apply(x, v);
+}
+
+// ---------------------------------------------------------------------------
+// narrow rows: tile = R consecutive rows x all columns, staged in smem
+template <typename ST, int VAR>
+__global__ void __launch_bounds__(kScanThreads)
+scan_rows(ScanArgs<ST> a, LookbackWs ws, int R) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int NA = VAR == SCAN_DIAG ? 2 : 6;  // element arrays staged (block: a b c d + u as 2)
+  const int ncol = a.D;
+  const int SW = VAR == SCAN_DIAG ? ncol : 2 * ncol;
+  __shared__ int64_t s_tile;
+  __shared__ double s_entry[2 * 64];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ws.ticket, 1u);
+  __syncthreads();
+  const int64_t b = s_tile;
+  const int64_t row0 = b * R;
+  const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
+  const int nel = rows * ncol;
+  ST *tile = (ST *)smem_raw;                       // NA arrays of R*ncol
+  double *segagg = (double *)(smem_raw + ((sizeof(ST) * NA * R * ncol + 15) / 16) * 16);
+
+  // stage the tile (coalesced; every element read once from HBM)
+  {
+    const int64_t g0 = row0 * ncol;
+    if constexpr (VAR == SCAN_DIAG) {
+      for (int i = threadIdx.x; i < nel; i += kScanThreads) {
+        tile[i] = a.e0[g0 + i];
+        tile[R * ncol + i] = a.u[g0 + i];
+      }
+    } else {
+      for (int i = threadIdx.x; i < nel; i += kScanThreads) {
+        tile[i] = a.e0[g0 + i];
+        tile[R * ncol + i] = a.e1[g0 + i];
+        tile[2 * R * ncol + i] = a.e2[g0 + i];
+        tile[3 * R * ncol + i] = a.e3[g0 + i];
+      }
+      for (int i = threadIdx.x; i < 2 * nel; i += kScanThreads) tile[4 * R * ncol + i] = a.u[2 * g0 + i];
+    }
+  }
+  __syncthreads();
+
+  const int nseg = kScanThreads / ncol;
+  const int c = threadIdx.x % ncol, s = threadIdx.x / ncol;
+  const int seglen = (rows + nseg - 1) / nseg;
+  const int r0 = s * seglen, r1 = min(rows, r0 + seglen);
+  const bool active = s < nseg;
+  constexpr int W = ColElem<VAR>::W;
+
+  ColElem<VAR> run;
+  run.ident();
+  if (active) {
+    for (int r = r0; r < r1; ++r) {
+      const int i = r * ncol + c;
+      if constexpr (VAR == SCAN_DIAG) {
+        run.push((double)tile[i], (double)tile[R * ncol + i]);
+      } else {
+        run.push((double)tile[i], (double)tile[R * ncol + i], (double)tile[2 * R * ncol + i],
+                 (double)tile[3 * R * ncol + i], (double)tile[4 * R * ncol + 2 * r * ncol + c],
+                 (double)tile[4 * R * ncol + 2 * r * ncol + ncol + c]);
+      }
+    }
+    run.store(segagg + (s * ncol + c) * W);
+  }
+  __syncthreads();
+
+  // per-column exclusive scan over segments; publish the tile aggregate
+  if (threadIdx.x < ncol) {
+    ColElem<VAR> tot;
+    tot.ident();
+    for (int q = 0; q < nseg; ++q) {
+      ColElem<VAR> e;
+      e.load(segagg + (q * ncol + threadIdx.x) * W);
+      tot.store(segagg + (q * ncol + threadIdx.x) * W);  // exclusive prefix in place
+      tot.push(e);
+    }
+    double *g = ws.agg + (b * ncol + threadIdx.x) * W;
+    double tmp[W];
+    tot.store(tmp);
+#pragma unroll
+    for (int k = 0; k < W; ++k) g[k] = tmp[k];
+    __threadfence();
+    // keep the tile aggregate for the exit state
+    tot.store(segagg + (nseg * ncol + threadIdx.x) * W);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(ws.status + b, 1);
+
+  // look-back (first warp; lanes over columns)
+  if (threadIdx.x < 32) {
+    for (int cc = threadIdx.x; cc < ncol; cc += 32) {
+      double x = 0.0, v = 0.0;
+      lookback_col<VAR>(ws, b, ncol, cc, SW, a.s0, x, v);
+      s_entry[cc] = x;
+      if (VAR == SCAN_BLOCK) s_entry[ncol + cc] = v;
+      ColElem<VAR> tot;
+      tot.load(segagg + (nseg * ncol + cc) * W);
+      if constexpr (VAR == SCAN_DIAG) {
+        tot.apply(x);
+        ws.exit[b * SW + cc] = x;
+      } else {
+        tot.apply(x, v);
+        ws.exit[b * SW + cc] = x;
+        ws.exit[b * SW + ncol + cc] = v;
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    if (threadIdx.x == 0) st_release(ws.status + b, 2);
+  }
+  __syncthreads();
+
+  // replay from the segment entry state; results overwrite the staged tile
+  if (active && r0 < r1) {
+    ColElem<VAR> pre;
+    pre.load(segagg + (s * ncol + c) * W);
+    if constexpr (VAR == SCAN_DIAG) {
+      double x = s_entry[c];
+      pre.apply(x);
+      for (int r = r0; r < r1; ++r) {
+        const int i = r * ncol + c;
+        x = (double)tile[i] * x + (double)tile[R * ncol + i];
+        tile[i] = (ST)x;
+      }
+    } else {
+      double x = s_entry[c], v = s_entry[ncol + c];
+      pre.apply(x, v);
+      for (int r = r0; r < r1; ++r) {
+        const int i = r * ncol + c;
+        const double xa = (double)tile[i] * x + (double)tile[R * ncol + i] * v +
+                          (double)tile[4 * R * ncol + 2 * r * ncol + c];
+        const double va = (double)tile[2 * R * ncol + i] * x + (double)tile[3 * R * ncol + i] * v +
+                          (double)tile[4 * R * ncol + 2 * r * ncol + ncol + c];
+        x = xa;
+        v = va;
+        // [x | v] rows overwrite the u tile in place (same thread, same slots)
+        tile[4 * R * ncol + 2 * r * ncol + c] = (ST)x;
+        tile[4 * R * ncol + 2 * r * ncol + ncol + c] = (ST)v;
+      }
+    }
+  }
+  __syncthreads();
+  {
+    const int64_t g0 = row0 * SW;
+    const int nout = rows * SW;
+    const ST *src = VAR == SCAN_DIAG ? tile : tile + 4 * R * ncol;
+    for (int i = threadIdx.x; i < nout; i += kScanThreads) a.out[g0 + i] = src[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// wide rows (D > 64): tile = 64 rows x 32 columns, one column per lane,
+// 8 row segments of 8 rows kept in registers.
+constexpr int kWideSeg = 8;
+template <typename ST, int VAR>
+__global__ void __launch_bounds__(kScanThreads)
+scan_cols(ScanArgs<ST> a, LookbackWs ws) {
+  constexpr int W = ColElem<VAR>::W;
+  const int ncol = a.D;
+  const int SW = VAR == SCAN_DIAG ? ncol : 2 * ncol;
+  const int ncb = (ncol + 31) / 32;
+  __shared__ int64_t s_tile;
+  __shared__ double segagg[8][32][W];
+  __shared__ double s_entry[2][32];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ws.ticket, 1u);
+  __syncthreads();
+  const int64_t tk = s_tile;
+  const int64_t rb = tk / ncb;
+  const int cb = (int)(tk % ncb);
+  const int lane = threadIdx.x & 31, s = threadIdx.x >> 5;
+  const int c = cb * 32 + lane;
+  const bool colok = c < ncol;
+  const int64_t rbase = rb * 64 + s * kWideSeg;
+  double ej[kWideSeg], eu[kWideSeg], eb[kWideSeg], ec[kWideSeg], ed[kWideSeg], ev[kWideSeg];
+  ColElem<VAR> run;
+  run.ident();
+#pragma unroll
+  for (int k = 0; k < kWideSeg; ++k) {
+    const int64_t r = rbase + k;
+    const bool ok = colok && r < a.T;
+    if constexpr (VAR == SCAN_DIAG) {
+      ej[k] = ok ? (double)a.e0[r * ncol + c] : 1.0;
+      eu[k] = ok ? (double)a.u[r * ncol + c] : 0.0;
+      run.push(ej[k], eu[k]);
+    } else {
+      ej[k] = ok ? (double)a.e0[r * ncol + c] : 1.0;
+      eb[k] = ok ? (double)a.e1[r * ncol + c] : 0.0;
+      ec[k] = ok ? (double)a.e2[r * ncol + c] : 0.0;
+      ed[k] = ok ? (double)a.e3[r * ncol + c] : 1.0;
+      eu[k] = ok ? (double)a.u[r * 2 * ncol + c] : 0.0;
+      ev[k] = ok ? (double)a.u[r * 2 * ncol + ncol + c] : 0.0;
+      run.push(ej[k], eb[k], ec[k], ed[k], eu[k], ev[k]);
+    }
+  }
+  run.store(segagg[s][lane]);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    ColElem<VAR> tot;
+    tot.ident();
+    for (int q = 0; q < 8; ++q) {
+      ColElem<VAR> e;
+      e.load(segagg[q][lane]);
+      tot.store(segagg[q][lane]);
+      tot.push(e);
+    }
+    if (colok) {
+      double tmp[W];
+      tot.store(tmp);
+      double *g = ws.agg + (tk * 32 + lane) * W;
+#pragma unroll
+      for (int k = 0; k < W; ++k) g[k] = tmp[k];
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(ws.status + tk, 1);
+    // look-back along the same column block: predecessor ticket tk - ncb
+    double x = 0.0, v = 0.0;
+    {
+      ColElem<VAR> acc;
+      acc.ident();
+      int64_t p = rb - 1;
+      while (p >= 0) {
+        const int64_t pt = p * ncb + cb;
+        int st;
+        do { st = ld_acquire(ws.status + pt); } while (st == 0);
+        if (st == 2) {
+          if (colok) {
+            x = ld_cg(ws.exit + p * SW + c);
+            if (VAR == SCAN_BLOCK) v = ld_cg(ws.exit + p * SW + ncol + c);
+          }
+          break;
+        }
+        ColElem<VAR> e;
+        if (colok) e.load_cg(ws.agg + (pt * 32 + lane) * W);
+        else e.ident();
+        acc.pre(e);
+        --p;
+      }
+      if (p < 0 && colok) {
+        x = (double)a.s0[c];
+        if (VAR == SCAN_BLOCK) v = (double)a.s0[ncol + c];
+      }
+      if constexpr (VAR == SCAN_DIAG) acc.apply(x);
+      else acc.apply(x, v);
+    }
+    s_entry[0][lane] = x;
+    s_entry[1][lane] = v;
+    if constexpr (VAR == SCAN_DIAG) tot.apply(x);
+    else tot.apply(x, v);
+    if (colok) {
+      ws.exit[rb * SW + c] = x;
+      if (VAR == SCAN_BLOCK) ws.exit[rb * SW + ncol + c] = v;
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(ws.status + tk, 2);
+  }
+  __syncthreads();
+  ColElem<VAR> pre;
+  pre.load(segagg[s][lane]);
+  double x = s_entry[0][lane], v = s_entry[1][lane];
+  if constexpr (VAR == SCAN_DIAG) pre.apply(x);
+  else pre.apply(x, v);
+#pragma unroll
+  for (int k = 0; k < kWideSeg; ++k) {
+    const int64_t r = rbase + k;
+    if (!(colok && r < a.T)) continue;
+    if constexpr (VAR == SCAN_DIAG) {
+      x = ej[k] * x + eu[k];
+      a.out[r * ncol + c] = (ST)x;
+    } else {
+      const double xa = ej[k] * x + eb[k] * v + eu[k];
+      const double va = ec[k] * x + ed[k] * v + ev[k];
+      x = xa;
+      v = va;
+      a.out[r * 2 * ncol + c] = (ST)x;
+      a.out[r * 2 * ncol + ncol + c] = (ST)v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dense, D <= MD <= 8: each thread folds SEG consecutive steps into (M, w) in
+// registers; warp shuffles + smem give the block scan; look-back on the
+// D-vector exit state.
+template <int MD> struct DenseElem {
+  double M[MD][MD], w[MD];
+  CS_D void ident(int D) {
+#pragma unroll
+    for (int r = 0; r < MD; ++r) {
+      w[r] = 0.0;
+#pragma unroll
+      for (int k = 0; k < MD; ++k) M[r][k] = (r == k) ? 1.0 : 0.0;
+    }
+  }
+  // this <- e o this
+  CS_D void push(const DenseElem &e) {
+    double Mn[MD][MD], wn[MD];
+#pragma unroll
+    for (int r = 0; r < MD; ++r) {
+      double aw = e.w[r];
+#pragma unroll
+      for (int k = 0; k < MD; ++k) aw += e.M[r][k] * w[k];
+      wn[r] = aw;
+#pragma unroll
+      for (int cc = 0; cc < MD; ++cc) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < MD; ++k) acc += e.M[r][k] * M[k][cc];
+        Mn[r][cc] = acc;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < MD; ++r) {
+      w[r] = wn[r];
+#pragma unroll
+      for (int k = 0; k < MD; ++k) M[r][k] = Mn[r][k];
+    }
+  }
+  CS_D void apply(double (&x)[MD]) const {
+    double y[MD];
+#pragma unroll
+    for (int r = 0; r < MD; ++r) {
+      double acc = w[r];
+#pragma unroll
+      for (int k = 0; k < MD; ++k) acc += M[r][k] * x[k];
+      y[r] = acc;
+    }
+#pragma unroll
+    for (int r = 0; r < MD; ++r) x[r] = y[r];
+  }
+  CS_D void shfl_up(const DenseElem &src, int delta, DenseElem &dst) const {
+#pragma unroll
+    for (int r = 0; r < MD; ++r) {
+      dst.w[r] = __shfl_up_sync(0xffffffffu, src.w[r], delta);
+#pragma unroll
+      for (int k = 0; k < MD; ++k) dst.M[r][k] = __shfl_up_sync(0xffffffffu, src.M[r][k], delta);
+    }
+  }
+};
+
+template <typename ST, int MD>
+CS_D void load_dense_elem(const ScanArgs<ST> &a, int64_t t, DenseElem<MD> &e) {
+  const int D = a.D;
+#pragma unroll
+  for (int r = 0; r < MD; ++r) {
+    e.w[r] = (r < D) ? (double)a.u[t * D + r] : 0.0;
+#pragma unroll
+    for (int k = 0; k < MD; ++k)
+      e.M[r][k] = (r < D && k < D) ? (double)a.e0[(t * D + r) * D + k] : (r == k ? 1.0 : 0.0);
+  }
+}
+
+template <typename ST, int MD, int SEG>
+__global__ void __launch_bounds__(kScanThreads)
+scan_dense_small(ScanArgs<ST> a, LookbackWs ws) {
+  __shared__ int64_t s_tile;
+  __shared__ DenseElem<MD> warp_tot[kScanThreads / 32];
+  __shared__ double s_entry[MD];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ws.ticket, 1u);
+  __syncthreads();
+  const int64_t b = s_tile;
+  const int D = a.D;
+  const int64_t t0 = (b * kScanThreads + threadIdx.x) * SEG;
+  DenseElem<MD> run;
+  run.ident(D);
+  for (int k = 0; k < SEG; ++k) {
+    const int64_t t = t0 + k;
+    if (t < a.T) {
+      DenseElem<MD> e;
+      load_dense_elem(a, t, e);
+      run.push(e);
+    }
+  }
+  // inclusive warp scan: lane l gets e_l o ... o e_0
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  DenseElem<MD> inc = run;
+#pragma unroll
+  for (int dlt = 1; dlt < 32; dlt <<= 1) {
+    DenseElem<MD> o;
+    inc.shfl_up(inc, dlt, o);
+    if (lane >= dlt) {
+      DenseElem<MD> tmp = o;   // earlier part
+      tmp.push(inc);           // inc o earlier
+      inc = tmp;
+    }
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    DenseElem<MD> tot;
+    tot.ident(D);
+    for (int q = 0; q < kScanThreads / 32; ++q) {
+      DenseElem<MD> e = warp_tot[q];
+      warp_tot[q] = tot;   // exclusive warp prefix
+      tot.push(e);
+    }
+    // publish aggregate (M row-major then w)
+    double *g = ws.agg + b * (MD * MD + MD);
+#pragma unroll
+    for (int r = 0; r < MD; ++r) {
+      g[MD * MD + r] = tot.w[r];
+#pragma unroll
+      for (int k = 0; k < MD; ++k) g[r * MD + k] = tot.M[r][k];
+    }
+    __threadfence();
+    st_release(ws.status + b, 1);
+    // look-back
+    DenseElem<MD> acc;
+    acc.ident(D);
+    double x[MD];
+    int64_t p = b - 1;
+    while (p >= 0) {
+      int st;
+      do { st = ld_acquire(ws.status + p); } while (st == 0);
+      if (st == 2) {
+#pragma unroll
+        for (int r = 0; r < MD; ++r) x[r] = (r < D) ? ld_cg(ws.exit + p * MD + r) : 0.0;
+        break;
+      }
+      DenseElem<MD> e;
+      const double *q = ws.agg + p * (MD * MD + MD);
+#pragma unroll
+      for (int r = 0; r < MD; ++r) {
+        e.w[r] = ld_cg(q + MD * MD + r);
+#pragma unroll
+        for (int k = 0; k < MD; ++k) e.M[r][k] = ld_cg(q + r * MD + k);
+      }
+      // acc <- acc o e
+      DenseElem<MD> tmp = e;
+      tmp.push(acc);
+      acc = tmp;
+      --p;
+    }
+    if (p < 0) {
+#pragma unroll
+      for (int r = 0; r < MD; ++r) x[r] = (r < D) ? (double)a.s0[r] : 0.0;
+    }
+    acc.apply(x);
+#pragma unroll
+    for (int r = 0; r < MD; ++r) s_entry[r] = x[r];
+    tot.apply(x);
+#pragma unroll
+    for (int r = 0; r < MD; ++r) ws.exit[b * MD + r] = x[r];
+    __threadfence();
+    st_release(ws.status + b, 2);
+  }
+  __syncthreads();
+  // entry of this thread = (inclusive-warp-prefix of lanes < l) o warp prefix applied to tile entry
+  double x[MD];
+#pragma unroll
+  for (int r = 0; r < MD; ++r) x[r] = s_entry[r];
+  warp_tot[wid].apply(x);
+  DenseElem<MD> exl;
+  inc.shfl_up(inc, 1, exl);
+  if (lane > 0) exl.apply(x);
+  for (int k = 0; k < SEG; ++k) {
+    const int64_t t = t0 + k;
+    if (t >= a.T) break;
+    DenseElem<MD> e;
+    load_dense_elem(a, t, e);
+    e.apply(x);
+#pragma unroll
+    for (int r = 0; r < MD; ++r)
+      if (r < D) a.out[t * D + r] = (ST)x[r];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int rows_per_tile(int var, int dtype, int D) {
+  const int esz = dtype == CS_F64 ? 8 : 4;
+  const int per = (var == SCAN_DIAG ? 2 : 6) * esz;
+  int E = (64 * 1024) / per;
+  int R = E / D;
+  if (R < 1) R = 1;
+  if (R > 8192) R = 8192;
+  return R;
+}
+
+ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
+  ScanPlan p{};
+  p.var = var;
+  if (var == SCAN_DENSE) {
+    p.kind = 2;
+    p.md = D <= 1 ? 1 : D <= 2 ? 2 : D <= 4 ? 4 : 8;
+    p.seg = p.md <= 2 ? 4 : 1;
+    const int64_t per_tile = (int64_t)kScanThreads * p.seg;
+    p.ntiles = (T + per_tile - 1) / per_tile;
+    p.agg_w = p.md * p.md + p.md;
+    p.state_w = p.md;
+  } else if (D <= 64) {
+    p.kind = 0;
+    p.R = rows_per_tile(var, dtype, D);
+    p.ntiles = (T + p.R - 1) / p.R;
+    p.agg_w = D * (var == SCAN_DIAG ? 2 : 6);
+    p.state_w = var == SCAN_DIAG ? D : 2 * D;
+    const int esz = dtype == CS_F64 ? 8 : 4;
+    const int NA = var == SCAN_DIAG ? 2 : 6;
+    const int nseg = kScanThreads / D;
+    p.smem = ((size_t)esz * NA * p.R * D + 15) / 16 * 16 + sizeof(double) * (nseg + 1) * D * (var == SCAN_DIAG ? 2 : 6);
+  } else {
+    p.kind = 1;
+    const int ncb = (D + 31) / 32;
+    p.ntiles = ((T + 63) / 64) * ncb;
+    p.agg_w = 32 * (var == SCAN_DIAG ? 2 : 6);
+    p.state_w = var == SCAN_DIAG ? D : 2 * D;
+  }
+  p.ws_bytes = align_up(sizeof(unsigned)) + align_up(sizeof(int) * p.ntiles) +
+               align_up(sizeof(double) * p.ntiles * p.agg_w) +
+               align_up(sizeof(double) * (p.kind == 1 ? (p.ntiles / ((D + 31) / 32) + 1) : p.ntiles) * p.state_w);
+  return p;
+}
+
+LookbackWs carve_ws(const ScanPlan &p, void *ws, int D) {
+  unsigned char *b = (unsigned char *)ws;
+  LookbackWs w;
+  w.ticket = (unsigned *)b;
+  b += align_up(sizeof(unsigned));
+  w.status = (int *)b;
+  b += align_up(sizeof(int) * p.ntiles);
+  w.agg = (double *)b;
+  b += align_up(sizeof(double) * p.ntiles * p.agg_w);
+  w.exit = (double *)b;
+  (void)D;
+  return w;
+}
+
+template <typename ST>
+cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st) {
+  LookbackWs w = carve_ws(p, ws, a.D);
+  // ticket + status must start at zero for every launch
+  cudaError_t e = cudaMemsetAsync(ws, 0, (unsigned char *)w.agg - (unsigned char *)ws, st);
+  if (e != cudaSuccess) return e;
+  if (p.ntiles == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)p.ntiles;
+  if (p.kind == 0) {
+    if (p.var == SCAN_DIAG) {
+      cudaFuncSetAttribute(scan_rows<ST, SCAN_DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      scan_rows<ST, SCAN_DIAG><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R);
+    } else {
+      cudaFuncSetAttribute(scan_rows<ST, SCAN_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      scan_rows<ST, SCAN_BLOCK><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R);
+    }
+  } else if (p.kind == 1) {
+    if (p.var == SCAN_DIAG) scan_cols<ST, SCAN_DIAG><<<grid, kScanThreads, 0, st>>>(a, w);
+    else scan_cols<ST, SCAN_BLOCK><<<grid, kScanThreads, 0, st>>>(a, w);
+  } else {
+    switch (p.md) {
+      case 1: scan_dense_small<ST, 1, 4><<<grid, kScanThreads, 0, st>>>(a, w); break;
+      case 2: scan_dense_small<ST, 2, 4><<<grid, kScanThreads, 0, st>>>(a, w); break;
+      case 4: scan_dense_small<ST, 4, 1><<<grid, kScanThreads, 0, st>>>(a, w); break;
+      default: scan_dense_small<ST, 8, 1><<<grid, kScanThreads, 0, st>>>(a, w); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_scan_t<float>(const ScanPlan &, ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_scan_t<double>(const ScanPlan &, ScanArgs<double>, void *, cudaStream_t);
+
+}  // namespace cs

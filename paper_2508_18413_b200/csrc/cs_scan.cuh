@@ -1,0 +1,29 @@
+// Scan launch plans shared by the standalone C-ABI scans and the generic driver.
+#pragma once
+#include "cs_common.cuh"
+
+namespace cs {
+
+enum { SCAN_DIAG = 0, SCAN_BLOCK = 1, SCAN_DENSE = 2 };
+
+template <typename ST>
+struct ScanArgs {
+  const ST *e0, *e1, *e2, *e3;  // diag: j | block: a b c d | dense: J
+  const ST *u, *s0;
+  ST *out;
+  int64_t T;
+  int D;                        // diag/dense: state dim; block: half (position) dim
+};
+
+struct ScanPlan {
+  int var, kind, R, md, seg;
+  int64_t ntiles;
+  int agg_w, state_w;
+  size_t smem, ws_bytes;
+};
+
+ScanPlan scan_plan(int var, int dtype, int64_t T, int D);
+template <typename ST>
+cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st);
+
+}  // namespace cs

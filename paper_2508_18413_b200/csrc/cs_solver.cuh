@@ -1,0 +1,515 @@
+// Device-resident Newton driver: run_deer (deer.py:230-328) as ONE cooperative
+// persistent kernel.
+//
+// Grid = co-resident CTAs (cooperative launch); CTA b owns a contiguous range of
+// steps, thread i of it a contiguous segment of `seg` steps.  Per iteration:
+//
+//  phase A  for each owned step t: prev = guess[t-1] (s0 at t=1), f_t(prev) via
+//           the fused system (noise row t), finite checks, Picard residual
+//           |f - guess| <= atol + rtol|f| (deer.py:263-268), Jacobian estimate
+//           (Hutchinson probes hashed on device / D tangent columns / leapfrog
+//           block) -> element (J, u = f - J prev) with preconditioner, damping,
+//           clip in the reference's order (deer.py:161-204); fold the segment
+//           into one element (kept in registers when seg <= kSegKeep).
+//           Block scan (warp shuffles + smem) -> CTA aggregate -> global.
+//  sync     grid barrier; every CTA reads the same reduced flags and takes the
+//           same branch: proposal/step errors, Picard stop, max_iters stop,
+//           Jacobian errors (deer.py:264-271 order).
+//  phase B  carry-in = ordered fold of preceding CTA aggregates applied to s0;
+//           replay the segment, write guess', per-row fail test and
+//           last_fail[t] = iteration (deer.py:273-277), dmax.
+//  sync     history, divergence guard (deer.py:221-227, 281-283), stop if no
+//           row failed (deer.py:284-286).
+//
+// No host round trip inside the solve: the only host sync is after the launch.
+#pragma once
+#include "cs_elem.cuh"
+#include "cs_lookback.cuh"
+#include "cs_systems.cuh"
+
+namespace cs {
+
+constexpr int kSolveThreads = 256;
+constexpr int kSegKeep = 4;
+constexpr int kTanMax = 4;
+
+struct SolveSlot {
+  long long bad_prop, bad_f, bad_jac;
+  unsigned picard_fail, any_fail;
+  unsigned long long dmax_bits;
+};
+
+struct SolveCtl {
+  SolveSlot slot[2];
+  unsigned arrive, gen;
+  int iterations, status, err_kind, final_buf, stop;
+  long long err_step;
+  int err_iter, pad;
+  double guard_dmax, guard_d0;
+};
+
+template <typename ST>
+struct SolveArgs {
+  cs_system sys;
+  int mode, max_iters, nsamp;
+  double atol, rtol, damping, clip;
+  const double *pre;
+  const ST *s0;
+  ST *G0, *G1;
+  int32_t *last_fail;
+  double *hist;
+  SolveCtl *ctl;
+  double *agg;  // [2][nblocks][W]
+  int64_t T;
+  int D, seg, nblocks;
+};
+
+// ---------------------------------------------------------------------------
+template <class Sys> struct SysFactory;
+template <int MD, typename ST, int TK> struct SysFactory<Mala<MD, ST, TK>> {
+  static CS_D Mala<MD, ST, TK> make(const cs_system &s) { return make_mala<MD, ST, TK>(s); }
+};
+template <int MD, typename ST, int TK> struct SysFactory<Hmc<MD, ST, TK>> {
+  static CS_D Hmc<MD, ST, TK> make(const cs_system &s) { return make_hmc<MD, ST, TK>(s); }
+};
+template <int MD, typename ST, int TK> struct SysFactory<Leapfrog<MD, ST, TK>> {
+  static CS_D Leapfrog<MD, ST, TK> make(const cs_system &s) { return make_leapfrog<MD, ST, TK>(s); }
+};
+template <int MD, typename ST> struct SysFactory<Gibbs<MD, ST>> {
+  static CS_D Gibbs<MD, ST> make(const cs_system &s) { return make_gibbs<MD, ST>(s); }
+};
+
+template <class Sys> struct HasBlock { static constexpr bool value = false; };
+template <int MD, typename ST, int TK> struct HasBlock<Leapfrog<MD, ST, TK>> { static constexpr bool value = true; };
+
+template <class Sys, int MD, typename ST>
+CS_D void load_row(const Sys &sys, const ST *row, double (&x)[MD]) {
+#pragma unroll
+  for (int k = 0; k < MD; ++k) {
+    const int m = sys.mem_index(k);
+    x[k] = m >= 0 ? (double)__ldcg(row + m) : 0.0;
+  }
+}
+
+// Element for one step from the forward pass (deer.py:161-204).
+template <class Sys, int MODE, int MD, typename ST>
+CS_D void build_elem(const Sys &sys, const typename Sys::Aux &aux, const double (&prev)[MD],
+                     const double (&f)[MD], int64_t t, int it, const SolveArgs<ST> &A,
+                     Elem<MODE, MD> &e, bool &jac_ok) {
+  jac_ok = true;
+  if constexpr (MODE == CS_MODE_DIAG) {
+    double est[MD];
+#pragma unroll
+    for (int i = 0; i < MD; ++i) est[i] = 0.0;
+    const uint64_t h3 = hash_t(probe_prefix(A.sys.seed, it), (uint64_t)t);
+    for (int k0 = 0; k0 < A.nsamp; k0 += kTanMax) {
+      const int nk = min(kTanMax, A.nsamp - k0);
+      double V[kTanMax][MD], O[kTanMax][MD];
+#pragma unroll
+      for (int kk = 0; kk < kTanMax; ++kk)
+#pragma unroll
+        for (int i = 0; i < MD; ++i) {
+          const int m = sys.mem_index(i);
+          V[kk][i] = (kk < nk && m >= 0) ? probe_sign(h3, k0 + kk, m) : 0.0;
+        }
+      sys.template jvp_many<kTanMax>(aux, V, O, nk, false);
+#pragma unroll
+      for (int kk = 0; kk < kTanMax; ++kk)
+        if (kk < nk)
+#pragma unroll
+          for (int i = 0; i < MD; ++i) est[i] += V[kk][i] * O[kk][i];
+    }
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      const int m = sys.mem_index(i);
+      if (m < 0) { e.j(i) = 0.0; e.u(i) = 0.0; continue; }
+      double d = est[i] / (double)A.nsamp;
+      jac_ok &= finite(d);
+      if (A.pre) d = d * __ldg(A.pre + m);
+      d = d * A.damping;
+      if (isfinite(A.clip)) d = clipv(d, A.clip);
+      e.j(i) = d;
+      e.u(i) = f[i] - d * prev[i];
+    }
+  } else if constexpr (MODE == CS_MODE_DENSE) {
+#pragma unroll
+    for (int c0 = 0; c0 < MD; c0 += kTanMax) {
+      double V[kTanMax][MD], O[kTanMax][MD];
+      int nk = 0;
+#pragma unroll
+      for (int kk = 0; kk < kTanMax; ++kk) {
+        const int c = c0 + kk;
+        if (c < MD && sys.mem_index(c) >= 0) nk = kk + 1;
+#pragma unroll
+        for (int i = 0; i < MD; ++i) V[kk][i] = (c < MD && i == c && sys.mem_index(c) >= 0) ? 1.0 : 0.0;
+      }
+      if (nk > 0) sys.template jvp_many<kTanMax>(aux, V, O, nk, false);
+#pragma unroll
+      for (int kk = 0; kk < kTanMax; ++kk) {
+        const int c = c0 + kk;
+        if (c >= MD) continue;
+        const bool vc = sys.mem_index(c) >= 0;
+#pragma unroll
+        for (int a = 0; a < MD; ++a) e.M(a, c) = (vc && kk < nk) ? O[kk][a] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < MD; ++a) {
+      const int ma = sys.mem_index(a);
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < MD; ++c) {
+        const int mc = sys.mem_index(c);
+        double J = e.M(a, c);
+        if (ma >= 0 && mc >= 0) {
+          jac_ok &= finite(J);
+          if (A.pre) J = J * (__ldg(A.pre + mc) / __ldg(A.pre + ma));
+          J = J * A.damping;
+          if (isfinite(A.clip)) J = clipv(J, A.clip);
+        } else {
+          J = 0.0;
+        }
+        e.M(a, c) = J;
+        acc += J * prev[c];
+      }
+      e.u(a) = ma >= 0 ? f[a] - acc : 0.0;
+    }
+  } else {
+    if constexpr (HasBlock<Sys>::value) {
+      constexpr int H = MD / 2;
+      double ba[H], bb[H], bc[H], bd[H];
+      sys.block(aux, t, A.nsamp, it, ba, bb, bc, bd);
+      const int n = A.D / 2;
+#pragma unroll
+      for (int i = 0; i < H; ++i) {
+        if (i >= n) {
+          e.ba(i) = 0.0; e.bb(i) = 0.0; e.bc(i) = 0.0; e.bd(i) = 0.0;
+          e.u(i) = 0.0; e.u(H + i) = 0.0;
+          continue;
+        }
+        jac_ok &= finite(ba[i]) && finite(bb[i]) && finite(bc[i]) && finite(bd[i]);
+        double a = ba[i], b = bb[i], c = bc[i], d = bd[i];
+        if (A.pre) {
+          const double px = __ldg(A.pre + i), pv = __ldg(A.pre + n + i);
+          b = b * (pv / px);
+          c = c * (px / pv);
+        }
+        a = A.damping * a; b = A.damping * b; c = A.damping * c; d = A.damping * d;
+        if (isfinite(A.clip)) { a = clipv(a, A.clip); b = clipv(b, A.clip); c = clipv(c, A.clip); d = clipv(d, A.clip); }
+        e.ba(i) = a; e.bb(i) = b; e.bc(i) = c; e.bd(i) = d;
+        const double x = prev[i], v = prev[H + i];
+        e.u(i) = f[i] - (a * x + b * v);
+        e.u(H + i) = f[H + i] - (c * x + d * v);
+      }
+    }
+  }
+}
+
+// exclusive prefix (excl) and CTA total of an ordered element sequence
+template <class E>
+CS_D void block_scan(const E &x, E &excl, E &total, E *s_warp) {
+  constexpr int NW = kSolveThreads / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  E inc = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    E o;
+    inc.shfl_up(d, o);
+    if (lane >= d) {
+      o.after(inc);
+      inc = o;
+    }
+  }
+  E ex;
+  inc.shfl_up(1, ex);
+  if (lane == 0) ex.ident();
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    E tot;
+    tot.ident();
+    for (int w = 0; w < NW; ++w) {
+      E e = s_warp[w];
+      s_warp[w] = tot;
+      tot.after(e);
+    }
+    s_warp[NW] = tot;
+  }
+  __syncthreads();
+  E r = s_warp[wid];
+  r.after(ex);
+  excl = r;
+  total = s_warp[NW];
+  __syncthreads();
+}
+
+CS_D void grid_sync(SolveCtl *c, unsigned nblocks, unsigned &gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned g = gen;
+    if (atomicAdd(&c->arrive, 1u) == nblocks - 1) {
+      atomicExch(&c->arrive, 0u);
+      __threadfence();
+      st_release((int *)&c->gen, (int)(g + 1));
+    } else {
+      while ((unsigned)ld_acquire((const int *)&c->gen) == g) __nanosleep(32);
+    }
+    gen = g + 1;
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <typename T> CS_D T vload(const T *p) { return *((const volatile T *)p); }
+
+// ---------------------------------------------------------------------------
+template <class Sys, int MODE, int MD, typename ST, bool KEEP>
+__global__ void __launch_bounds__(kSolveThreads)
+deer_persistent(SolveArgs<ST> A) {
+  using E = Elem<MODE, MD>;
+  __shared__ E s_warp[kSolveThreads / 32 + 1];
+  __shared__ long long s_min[3];
+  __shared__ unsigned s_cnt[2];
+  __shared__ unsigned long long s_dm;
+
+  const Sys sys = SysFactory<Sys>::make(A.sys);
+  const int b = blockIdx.x;
+  const int D = A.D;
+  const int64_t row0 = ((int64_t)b * kSolveThreads + threadIdx.x) * A.seg;
+  double s0r[MD];
+  load_row<Sys, MD, ST>(sys, A.s0, s0r);
+  for (int k = 0; k < A.seg; ++k)
+    if (row0 + k < A.T) A.last_fail[row0 + k] = 0;
+
+  unsigned gen = 0;
+  double d0 = -1.0;
+  bool have_d0 = false;
+  int it = 0, cur = 0;
+  int status = CS_RUN_MAXITERS, err_kind = CS_DIV_NONE, err_iter = -1, stop = CS_STOP_MAXITERS;
+  long long err_step = -1;
+  double g_dmax = 0.0;
+  E keep[KEEP ? kSegKeep : 1];
+
+  for (;;) {
+    SolveSlot *S = &A.ctl->slot[it & 1];
+    const ST *Gc = cur ? A.G1 : A.G0;
+    ST *Gn = cur ? A.G0 : A.G1;
+    if (threadIdx.x == 0) {
+      s_min[0] = s_min[1] = s_min[2] = kNoStep;
+      s_cnt[0] = s_cnt[1] = 0;
+      s_dm = 0ull;
+    }
+    __syncthreads();
+
+    // ---------------- phase A: f, Picard, elements, segment fold ----------
+    E agg;
+    agg.ident();
+    long long bp = kNoStep, bf = kNoStep, bj = kNoStep;
+    unsigned pf = 0;
+    const bool want_elem = it < A.max_iters;
+    double prev[MD];
+    if (it == 0 || row0 == 0 || row0 >= A.T) {
+#pragma unroll
+      for (int i = 0; i < MD; ++i) prev[i] = s0r[i];
+    } else {
+      load_row<Sys, MD, ST>(sys, Gc + (row0 - 1) * D, prev);
+    }
+    constexpr int KB = KEEP ? kSegKeep : (1 << 30);
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const int64_t r = row0 + k;
+      if (k >= A.seg || r >= A.T) break;
+      const int64_t t = r + 1;
+      double gr[MD];
+      if (it == 0) {
+#pragma unroll
+        for (int i = 0; i < MD; ++i) gr[i] = s0r[i];
+      } else {
+        load_row<Sys, MD, ST>(sys, Gc + r * D, gr);
+      }
+      typename Sys::Aux aux;
+      if (!sys.prepare(t, prev, aux)) bp = min(bp, (long long)t);
+      double f[MD];
+      sys.f(aux, f);
+      bool fin = true, pfail = false;
+#pragma unroll
+      for (int i = 0; i < MD; ++i) {
+        if (sys.mem_index(i) < 0) continue;
+        fin &= finite(f[i]);
+        pfail |= !(fabs(f[i] - gr[i]) <= A.atol + A.rtol * fabs(f[i]));
+      }
+      if (!fin) bf = min(bf, (long long)t);
+      pf += pfail ? 1u : 0u;
+      if (want_elem) {
+        E e;
+        bool jok;
+        build_elem<Sys, MODE, MD, ST>(sys, aux, prev, f, t, it, A, e, jok);
+        if (!jok) bj = min(bj, (long long)t);
+        agg.after(e);
+        if constexpr (KEEP) keep[k] = e;
+      }
+#pragma unroll
+      for (int i = 0; i < MD; ++i) prev[i] = gr[i];
+    }
+    E excl, total;
+    block_scan(agg, excl, total, s_warp);
+    if (threadIdx.x == 0) {
+      double *g = A.agg + ((size_t)(it & 1) * A.nblocks + b) * E::W;
+#pragma unroll
+      for (int q = 0; q < E::W; ++q) g[q] = total.v[q];
+    }
+    bp = warp_min_i64(bp);
+    bf = warp_min_i64(bf);
+    bj = warp_min_i64(bj);
+    pf = (unsigned)warp_sum_i((int)pf);
+    if ((threadIdx.x & 31) == 0) {
+      if (bp != kNoStep) atomicMin(&s_min[0], bp);
+      if (bf != kNoStep) atomicMin(&s_min[1], bf);
+      if (bj != kNoStep) atomicMin(&s_min[2], bj);
+      if (pf) atomicAdd(&s_cnt[0], pf);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_min[0] != kNoStep) atomicMin(&S->bad_prop, s_min[0]);
+      if (s_min[1] != kNoStep) atomicMin(&S->bad_f, s_min[1]);
+      if (s_min[2] != kNoStep) atomicMin(&S->bad_jac, s_min[2]);
+      if (s_cnt[0]) atomicAdd(&S->picard_fail, s_cnt[0]);
+    }
+    grid_sync(A.ctl, (unsigned)A.nblocks, gen);
+
+    // ---------------- decision (identical in every CTA) --------------------
+    {
+      const long long gbp = vload(&S->bad_prop), gbf = vload(&S->bad_f), gbj = vload(&S->bad_jac);
+      const unsigned gpf = vload(&S->picard_fail);
+      if (gbp != kNoStep) { status = CS_RUN_DIVERGED; stop = CS_STOP_ERROR; err_kind = CS_DIV_PROPOSAL; err_step = gbp; err_iter = -1; break; }
+      if (gbf != kNoStep) { status = CS_RUN_DIVERGED; stop = CS_STOP_ERROR; err_kind = CS_DIV_STEP; err_step = gbf; err_iter = it + 1; break; }
+      if (gpf == 0) { status = CS_RUN_CONVERGED; stop = CS_STOP_PICARD; break; }
+      if (it >= A.max_iters) { status = CS_RUN_MAXITERS; stop = CS_STOP_MAXITERS; break; }
+      if (gbj != kNoStep) { status = CS_RUN_DIVERGED; stop = CS_STOP_ERROR; err_kind = CS_DIV_JACOBIAN; err_step = gbj; err_iter = it + 1; break; }
+    }
+    if (b == 0 && threadIdx.x == 0) {
+      SolveSlot *O = &A.ctl->slot[(it + 1) & 1];
+      O->bad_prop = O->bad_f = O->bad_jac = kNoStep;
+      O->picard_fail = O->any_fail = 0;
+      O->dmax_bits = 0ull;
+    }
+
+    // ---------------- phase B: carry-in, replay, bookkeeping -------------
+    {
+      const double *ag = A.agg + (size_t)(it & 1) * A.nblocks * E::W;
+      const int per = (b + kSolveThreads - 1) / kSolveThreads;
+      const int lo = threadIdx.x * per, hi = min(b, lo + per);
+      E fold;
+      fold.ident();
+      for (int q = lo; q < hi; ++q) {
+        E e;
+#pragma unroll
+        for (int w = 0; w < E::W; ++w) e.v[w] = __ldcg(ag + (size_t)q * E::W + w);
+        fold.after(e);
+      }
+      E fex, ftot;
+      block_scan(fold, fex, ftot, s_warp);
+      double x[MD];
+#pragma unroll
+      for (int i = 0; i < MD; ++i) x[i] = s0r[i];
+      ftot.apply(x);      // state entering this CTA
+      excl.apply(x);      // state entering this thread's segment
+      unsigned af = 0;
+      unsigned long long dmb = 0ull;
+      double pv[MD];
+      if (!KEEP) {
+        if (it == 0 || row0 == 0 || row0 >= A.T) {
+#pragma unroll
+          for (int i = 0; i < MD; ++i) pv[i] = s0r[i];
+        } else {
+          load_row<Sys, MD, ST>(sys, Gc + (row0 - 1) * D, pv);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const int64_t r = row0 + k;
+        if (k >= A.seg || r >= A.T) break;
+        double gr[MD];
+        if (it == 0) {
+#pragma unroll
+          for (int i = 0; i < MD; ++i) gr[i] = s0r[i];
+        } else {
+          load_row<Sys, MD, ST>(sys, Gc + r * D, gr);
+        }
+        E e;
+        if constexpr (KEEP) {
+          e = keep[k];
+        } else {
+          const int64_t t = r + 1;
+          typename Sys::Aux aux;
+          sys.prepare(t, pv, aux);
+          double f[MD];
+          sys.f(aux, f);
+          bool jok;
+          build_elem<Sys, MODE, MD, ST>(sys, aux, pv, f, t, it, A, e, jok);
+#pragma unroll
+          for (int i = 0; i < MD; ++i) pv[i] = gr[i];
+        }
+        e.apply(x);
+        bool fail = false;
+#pragma unroll
+        for (int i = 0; i < MD; ++i) {
+          const int m = sys.mem_index(i);
+          if (m < 0) continue;
+          const ST xs = (ST)x[i];
+          Gn[r * D + m] = xs;
+          const double xd = (double)xs;
+          const double gap = fabs(xd - gr[i]);
+          fail |= gap > A.atol + A.rtol * fabs(xd);
+          const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
+          dmb = gb > dmb ? gb : dmb;
+        }
+        if (fail) {
+          A.last_fail[r] = it + 1;
+          ++af;
+        }
+      }
+      af = (unsigned)warp_sum_i((int)af);
+      dmb = warp_max_u64(dmb);
+      if ((threadIdx.x & 31) == 0) {
+        if (af) atomicAdd(&s_cnt[1], af);
+        atomicMax(&s_dm, dmb);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (s_cnt[1]) atomicAdd(&S->any_fail, s_cnt[1]);
+        atomicMax(&S->dmax_bits, s_dm);
+      }
+    }
+    grid_sync(A.ctl, (unsigned)A.nblocks, gen);
+
+    ++it;
+    const unsigned gaf = vload(&S->any_fail);
+    const double dmax = __longlong_as_double((long long)vload(&S->dmax_bits));
+    if (b == 0 && threadIdx.x == 0) A.hist[it - 1] = dmax;
+    if (!have_d0) { d0 = dmax; have_d0 = true; }
+    cur ^= 1;
+    g_dmax = dmax;
+    if (d0 > 0.0 && dmax > 1e6 * d0) {
+      status = CS_RUN_DIVERGED; stop = CS_STOP_ERROR; err_kind = CS_DIV_GUARD; err_step = -1; err_iter = it;
+      break;
+    }
+    if (gaf == 0) { status = CS_RUN_CONVERGED; stop = CS_STOP_NOFAIL; break; }
+  }
+
+  if (b == 0 && threadIdx.x == 0) {
+    SolveCtl *c = A.ctl;
+    c->iterations = it;
+    c->status = status;
+    c->stop = stop;
+    c->err_kind = err_kind;
+    c->err_step = err_step;
+    c->err_iter = err_iter;
+    c->final_buf = it == 0 ? -1 : cur;
+    c->guard_dmax = g_dmax;
+    c->guard_d0 = d0;
+  }
+}
+
+}  // namespace cs

@@ -1,0 +1,466 @@
+// Transition systems f_t and their solver-form tangents, one thread per step.
+//
+// Each system exposes
+//   prepare(t, s, aux)          forward pass; false if the proposal / trajectory
+//                               is non-finite (samplers.py:101-105, 332-336)
+//   f(aux, out)                 the hard-gated step (samplers.py:120-122, 344-346)
+//   relaxed_f(aux, out)         sigmoid-gated step (124-127, 348-351)
+//   jvp_many<NT>(aux, V, out, n, relaxed)   n <= NT tangents J v at the same s
+// with the reference's arithmetic order, all in f64 registers.  Noise rows are
+// read from the pre-drawn sequence (noise.py:107-113: step t reads row t).
+#pragma once
+#include "cs_rng.cuh"
+#include "cs_targets.cuh"
+
+namespace cs {
+
+// ---------------------------------------------------------------------------
+// MALA (samplers.py:71-148)
+template <int MD, typename ST, int TK = -1>
+struct Mala {
+  Target<MD, TK> tg;
+  double eps, sq2eps;
+  const ST *xi;
+  const double *logu;
+
+  struct Aux {
+    double S[MD], prop[MD], g0[MD], g1[MD], back[MD];
+    double delta, margin;
+  };
+
+  CS_D int dim() const { return tg.p.dim; }
+  CS_D int mem_index(int k) const { return k < tg.p.dim ? k : -1; }
+
+  CS_D bool prepare(int64_t t, const double (&s)[MD], Aux &a) const {
+    const int D = dim();
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) a.S[i] = s[i];
+    tg.grad(s, a.g0);
+    double xx = 0.0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      double z = (i < D) ? ld(xi, t * D + i) : 0.0;
+      a.prop[i] = (i < D) ? (s[i] + eps * a.g0[i]) + sq2eps * z : 0.0;
+      ok &= (i >= D) || finite(a.prop[i]);
+      xx += z * z;
+    }
+    tg.grad(a.prop, a.g1);
+    double rr = 0.0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      a.back[i] = (i < D) ? (s[i] - a.prop[i]) - eps * a.g1[i] : 0.0;
+      rr += a.back[i] * a.back[i];
+    }
+    a.delta = ((tg.logp(a.prop) - tg.logp(s)) - rr / (4.0 * eps)) + 0.5 * xx;
+    a.margin = fmin(0.0, a.delta) - __ldg(logu + t);
+    return ok;
+  }
+
+  CS_D void f(const Aux &a, double (&o)[MD]) const {
+    const bool acc = a.margin > 0.0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) o[i] = acc ? a.prop[i] : a.S[i];
+  }
+
+  CS_D void relaxed_f(const Aux &a, double (&o)[MD]) const {
+    const double w = expit(a.margin);
+#pragma unroll
+    for (int i = 0; i < MD; ++i) o[i] = w * a.prop[i] + (1.0 - w) * a.S[i];
+  }
+
+  CS_D void jvp1(const Aux &a, const double (&V)[MD], double (&o)[MD], bool relaxed) const {
+    double hv[MD], dprop[MD], hd[MD];
+    tg.hvp(a.S, V, hv);
+#pragma unroll
+    for (int i = 0; i < MD; ++i) dprop[i] = V[i] + eps * hv[i];
+    tg.hvp(a.prop, dprop, hd);
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      double dback = (V[i] - dprop[i]) - eps * hd[i];
+      s1 += a.g1[i] * dprop[i];
+      s2 += a.g0[i] * V[i];
+      s3 += a.back[i] * dback;
+    }
+    const double ddelta = (s1 - s2) - s3 / (2.0 * eps);
+    const double gate = relaxed ? expit(a.margin) : (a.margin > 0.0 ? 1.0 : 0.0);
+    const double bend = sigmoid_prime(a.margin) * (ddelta * (a.delta < 0.0 ? 1.0 : 0.0));
+#pragma unroll
+    for (int i = 0; i < MD; ++i)
+      o[i] = (gate * dprop[i] + (1.0 - gate) * V[i]) + (a.prop[i] - a.S[i]) * bend;
+  }
+
+  template <int NT>
+  CS_D void jvp_many(const Aux &a, const double (&V)[NT][MD], double (&o)[NT][MD], int n,
+                     bool relaxed) const {
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+      if (k < n) jvp1(a, V[k], o[k], relaxed);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// chain-level HMC (samplers.py:253-387); the L-step leapfrog runs in registers
+template <int MD, typename ST, int TK = -1>
+struct Hmc {
+  Target<MD, TK> tg;
+  double eps;
+  int L;
+  const double *mass;  // nullable
+  const ST *mom;
+  const double *logu;
+
+  struct Aux {
+    double S[MD], vh0[MD], g0[MD], xl[MD], vl[MD], gl[MD];
+    double delta, margin;
+  };
+
+  CS_D int dim() const { return tg.p.dim; }
+  CS_D int mem_index(int k) const { return k < tg.p.dim ? k : -1; }
+  CS_D double m(int i) const { return (mass && i < tg.p.dim) ? __ldg(mass + i) : 1.0; }
+
+  CS_D bool prepare(int64_t t, const double (&s)[MD], Aux &a) const {
+    const int D = dim();
+    double xx = 0.0;
+    tg.grad(s, a.g0);
+    double x[MD], v[MD], g[MD];
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      double z = (i < D) ? ld(mom, t * D + i) : 0.0;
+      xx += z * z;
+      a.S[i] = s[i];
+      a.vh0[i] = (i < D) ? sqrt(m(i)) * z + (0.5 * eps) * a.g0[i] : 0.0;
+      x[i] = s[i];
+      v[i] = a.vh0[i];
+    }
+    const double h0 = 0.5 * xx - tg.logp(s);
+    for (int l = 0; l < L; ++l) {
+#pragma unroll
+      for (int i = 0; i < MD; ++i) x[i] = x[i] + (eps * v[i]) / m(i);
+      tg.grad(x, g);
+#pragma unroll
+      for (int i = 0; i < MD; ++i) v[i] = v[i] + eps * g[i];
+    }
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) ok &= (i >= D) || finite(x[i]);
+    tg.grad(x, a.gl);
+    double kin = 0.0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      a.xl[i] = x[i];
+      a.vl[i] = v[i] - (0.5 * eps) * a.gl[i];
+      if (i < D) kin += (a.vl[i] * a.vl[i]) / m(i);
+    }
+    const double hl = 0.5 * kin - tg.logp(x);
+    a.delta = h0 - hl;
+    a.margin = fmin(0.0, a.delta) - __ldg(logu + t);
+    return ok;
+  }
+
+  CS_D void f(const Aux &a, double (&o)[MD]) const {
+    const bool acc = a.margin > 0.0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) o[i] = acc ? a.xl[i] : a.S[i];
+  }
+
+  CS_D void relaxed_f(const Aux &a, double (&o)[MD]) const {
+    const double w = expit(a.margin);
+#pragma unroll
+    for (int i = 0; i < MD; ++i) o[i] = w * a.xl[i] + (1.0 - w) * a.S[i];
+  }
+
+  // tangents ride the forward integrator (samplers.py:353-381), all n at once
+  template <int NT>
+  CS_D void jvp_many(const Aux &a, const double (&V)[NT][MD], double (&o)[NT][MD], int n,
+                     bool relaxed) const {
+    const int D = dim();
+    double dx[NT][MD], dv[NT][MD], dh0[NT];
+    double x[MD], v[MD], g[MD], h[MD];
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      if (k >= n) continue;
+      tg.hvp(a.S, V[k], h);
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < MD; ++i) {
+        dx[k][i] = V[k][i];
+        dv[k][i] = (0.5 * eps) * h[i];
+        s += a.g0[i] * V[k][i];
+      }
+      dh0[k] = -s;
+    }
+#pragma unroll
+    for (int i = 0; i < MD; ++i) { x[i] = a.S[i]; v[i] = a.vh0[i]; }
+    for (int l = 0; l < L; ++l) {
+#pragma unroll
+      for (int i = 0; i < MD; ++i) x[i] = x[i] + (eps * v[i]) / m(i);
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        if (k >= n) continue;
+#pragma unroll
+        for (int i = 0; i < MD; ++i) dx[k][i] = dx[k][i] + (eps * dv[k][i]) / m(i);
+        tg.hvp(x, dx[k], h);
+#pragma unroll
+        for (int i = 0; i < MD; ++i) dv[k][i] = dv[k][i] + eps * h[i];
+      }
+      tg.grad(x, g);
+#pragma unroll
+      for (int i = 0; i < MD; ++i) v[i] = v[i] + eps * g[i];
+    }
+    const double gate = relaxed ? expit(a.margin) : (a.margin > 0.0 ? 1.0 : 0.0);
+    const double sp = sigmoid_prime(a.margin);
+    const double neg = a.delta < 0.0 ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      if (k >= n) continue;
+      tg.hvp(x, dx[k], h);
+      double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < MD; ++i) {
+        double dvl = dv[k][i] - (0.5 * eps) * h[i];
+        if (i < D) s1 += (a.vl[i] * dvl) / m(i);
+        s2 += a.gl[i] * dx[k][i];
+      }
+      const double ddelta = dh0[k] - (s1 - s2);
+      const double bend = sp * (ddelta * neg);
+#pragma unroll
+      for (int i = 0; i < MD; ++i)
+        o[k][i] = (gate * dx[k][i] + (1.0 - gate) * V[k][i]) + (a.xl[i] - a.S[i]) * bend;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// leapfrog integrator as a system over [x, v] (samplers.py:165-222).  MD is
+// the (even) register width; x lives in slots [0, n), v in [H, H + n) with
+// H = MD/2, so block elements stay compile-time indexed (see mem_index).
+template <int MD, typename ST, int TK = -1>
+struct Leapfrog {
+  static constexpr int H = MD / 2;
+  Target<H, TK> tg;
+  double eps;
+  const double *mass;
+  uint64_t probe_seed;
+
+  struct Aux {
+    double S[MD], xn[H], vn[H];
+  };
+
+  CS_D int dim() const { return 2 * tg.p.dim; }
+  CS_D int mem_index(int k) const {
+    const int n = tg.p.dim;
+    return k < H ? (k < n ? k : -1) : (k - H < n ? n + k - H : -1);
+  }
+  CS_D double m(int i) const { return (mass && i < tg.p.dim) ? __ldg(mass + i) : 1.0; }
+
+  CS_D bool prepare(int64_t, const double (&s)[MD], Aux &a) const {
+    const int n = tg.p.dim;
+    double g[H];
+#pragma unroll
+    for (int i = 0; i < MD; ++i) a.S[i] = s[i];
+#pragma unroll
+    for (int i = 0; i < H; ++i) a.xn[i] = (i < n) ? s[i] + (eps * s[H + i]) / m(i) : 0.0;
+    tg.grad(a.xn, g);
+#pragma unroll
+    for (int i = 0; i < H; ++i) a.vn[i] = (i < n) ? s[H + i] + eps * g[i] : 0.0;
+    return true;
+  }
+
+  CS_D void f(const Aux &a, double (&o)[MD]) const {
+#pragma unroll
+    for (int i = 0; i < H; ++i) { o[i] = a.xn[i]; o[H + i] = a.vn[i]; }
+  }
+  CS_D void relaxed_f(const Aux &a, double (&o)[MD]) const { f(a, o); }
+
+  CS_D void jvp1(const Aux &a, const double (&V)[MD], double (&o)[MD]) const {
+    const int n = tg.p.dim;
+    double dxn[H], h[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) dxn[i] = (i < n) ? V[i] + (eps * V[H + i]) / m(i) : 0.0;
+    tg.hvp(a.xn, dxn, h);
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      o[i] = dxn[i];
+      o[H + i] = (i < n) ? V[H + i] + eps * h[i] : 0.0;
+    }
+  }
+
+  template <int NT>
+  CS_D void jvp_many(const Aux &a, const double (&V)[NT][MD], double (&o)[NT][MD], int n,
+                     bool) const {
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+      if (k < n) jvp1(a, V[k], o[k]);
+  }
+
+  // block estimate (samplers.py:202-222): a=1, b=eps/m, c=eps dhat, d=1+eps^2 dhat/m
+  CS_D void block(const Aux &a, int64_t t, int nsamp, int64_t iteration, double (&ba)[H],
+                  double (&bb)[H], double (&bc)[H], double (&bd)[H]) const {
+    const int n = tg.p.dim;
+    const uint64_t h3 = hash_t(probe_prefix(probe_seed, iteration), (uint64_t)t);
+    double dhat[H], z[H], hz[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) dhat[i] = 0.0;
+    for (int k = 0; k < nsamp; ++k) {
+#pragma unroll
+      for (int i = 0; i < H; ++i) z[i] = (i < n) ? probe_sign(h3, k, i) : 0.0;
+      tg.hvp(a.xn, z, hz);
+#pragma unroll
+      for (int i = 0; i < H; ++i) dhat[i] += z[i] * hz[i];
+    }
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      dhat[i] = dhat[i] / (double)nsamp;
+      ba[i] = (i < n) ? 1.0 : 0.0;
+      bb[i] = (i < n) ? eps / m(i) : 0.0;
+      bc[i] = eps * dhat[i];
+      bd[i] = (i < n) ? 1.0 + ((eps * eps) * dhat[i]) / m(i) : 0.0;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// eight-schools systematic Gibbs sweep (samplers.py:464-627); MD = 2S + 2
+template <int MD, typename ST>
+struct Gibbs {
+  static constexpr int S = (MD - 2) / 2;
+  static constexpr double kFloor = 1e-8;   // VARIANCE_FLOOR, samplers.py:549
+  int D;
+  const ST *g_tau, *xi_mu, *xi_theta, *g_sigma;
+  const double *prm;  // nu0 tau0_sq mu0 kappa0 alpha0 sigma0_sq S n xbar[S] ss[S]
+
+  struct Aux {
+    double mu, th[S], sg[S], raw_ok[S];
+    double gt, xm, xt[S], gs[S];
+    double tau2n, mun, prec[S], mean[S], thn[S], sgn[S];
+  };
+
+  CS_D int dim() const { return D; }
+  CS_D int mem_index(int k) const { return k < D ? k : -1; }
+
+  CS_D bool prepare(int64_t t, const double (&s)[MD], Aux &a) const {
+    const double nu0 = __ldg(prm + 0), tau0_sq = __ldg(prm + 1), mu0 = __ldg(prm + 2);
+    const double kappa0 = __ldg(prm + 3), alpha0 = __ldg(prm + 4), sigma0_sq = __ldg(prm + 5);
+    const double n = __ldg(prm + 7);
+    a.mu = s[1];
+    a.gt = ld(g_tau, t);
+    a.xm = ld(xi_mu, t);
+    double sth = 0.0, q = 0.0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      a.th[i] = s[2 + i];
+      a.raw_ok[i] = s[2 + S + i] > kFloor ? 1.0 : 0.0;
+      a.sg[i] = fmax(s[2 + S + i], kFloor);
+      a.xt[i] = ld(xi_theta, t * S + i);
+      a.gs[i] = ld(g_sigma, t * S + i);
+      double dm = a.th[i] - a.mu;
+      q += dm * dm;
+      sth += a.th[i];
+    }
+    const double dmu0 = a.mu - mu0;
+    const double q_tau = (nu0 * tau0_sq + kappa0 * (dmu0 * dmu0)) + q;
+    a.tau2n = q_tau / a.gt;
+    const double kS = kappa0 + (double)S;
+    a.mun = (kappa0 * mu0 + sth) / kS + sqrt(a.tau2n / kS) * a.xm;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const double xbar = __ldg(prm + 8 + i), ss = __ldg(prm + 8 + S + i);
+      a.prec[i] = 1.0 / a.tau2n + n / a.sg[i];
+      a.mean[i] = (a.mun / a.tau2n + (n * xbar) / a.sg[i]) / a.prec[i];
+      a.thn[i] = a.mean[i] + a.xt[i] / sqrt(a.prec[i]);
+      const double r = xbar - a.thn[i];
+      a.sgn[i] = ((alpha0 * sigma0_sq + ss) + n * (r * r)) / a.gs[i];
+    }
+    return true;
+  }
+
+  CS_D void f(const Aux &a, double (&o)[MD]) const {
+    o[0] = a.tau2n;
+    o[1] = a.mun;
+#pragma unroll
+    for (int i = 0; i < S; ++i) { o[2 + i] = a.thn[i]; o[2 + S + i] = a.sgn[i]; }
+  }
+  CS_D void relaxed_f(const Aux &a, double (&o)[MD]) const { f(a, o); }
+
+  CS_D void jvp1(const Aux &a, const double (&V)[MD], double (&o)[MD]) const {
+    const double mu0 = __ldg(prm + 2), kappa0 = __ldg(prm + 3), n = __ldg(prm + 7);
+    const double dmu_in = V[1];
+    double q = 0.0, sdth = 0.0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      q += 2.0 * (a.th[i] - a.mu) * (V[2 + i] - dmu_in);
+      sdth += V[2 + i];
+    }
+    const double dq = 2.0 * kappa0 * (a.mu - mu0) * dmu_in + q;
+    const double dtau2 = dq / a.gt;
+    const double kS = kappa0 + (double)S;
+    const double dmu = sdth / kS + a.xm * dtau2 / (2.0 * sqrt(a.tau2n * kS));
+    const double t2sq = a.tau2n * a.tau2n;
+    o[0] = dtau2;
+    o[1] = dmu;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const double xbar = __ldg(prm + 8 + i);
+      const double dsg = a.raw_ok[i] != 0.0 ? V[2 + S + i] : 0.0;
+      const double sg2 = a.sg[i] * a.sg[i];
+      const double dprec = -dtau2 / t2sq - n * dsg / sg2;
+      const double damean = (dmu / a.tau2n - a.mun * dtau2 / t2sq) - n * xbar * dsg / sg2;
+      const double dmean = (damean - a.mean[i] * dprec) / a.prec[i];
+      const double dth = dmean - 0.5 * a.xt[i] * dprec / pow(a.prec[i], 1.5);
+      o[2 + i] = dth;
+      o[2 + S + i] = (-2.0 * n * (xbar - a.thn[i]) * dth) / a.gs[i];
+    }
+  }
+
+  template <int NT>
+  CS_D void jvp_many(const Aux &a, const double (&V)[NT][MD], double (&o)[NT][MD], int n,
+                     bool) const {
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+      if (k < n) jvp1(a, V[k], o[k]);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// build a device system object from the C-ABI descriptor
+template <int MD, typename ST, int TK> CS_D Mala<MD, ST, TK> make_mala(const cs_system &s) {
+  Mala<MD, ST, TK> m;
+  m.tg.p = s.target;
+  m.eps = s.eps;
+  m.sq2eps = sqrt(2.0 * s.eps);
+  m.xi = (const ST *)s.noise_vec;
+  m.logu = s.noise_logu;
+  return m;
+}
+template <int MD, typename ST, int TK> CS_D Hmc<MD, ST, TK> make_hmc(const cs_system &s) {
+  Hmc<MD, ST, TK> h;
+  h.tg.p = s.target;
+  h.eps = s.eps;
+  h.L = s.L;
+  h.mass = s.mass;
+  h.mom = (const ST *)s.noise_vec;
+  h.logu = s.noise_logu;
+  return h;
+}
+template <int MD, typename ST, int TK> CS_D Leapfrog<MD, ST, TK> make_leapfrog(const cs_system &s) {
+  Leapfrog<MD, ST, TK> l;
+  l.tg.p = s.target;
+  l.eps = s.eps;
+  l.mass = s.mass;
+  l.probe_seed = s.probe_seed;
+  return l;
+}
+template <int MD, typename ST> CS_D Gibbs<MD, ST> make_gibbs(const cs_system &s) {
+  Gibbs<MD, ST> g;
+  g.D = s.dim;
+  g.g_tau = (const ST *)s.g_tau;
+  g.xi_mu = (const ST *)s.xi_mu;
+  g.xi_theta = (const ST *)s.xi_theta;
+  g.g_sigma = (const ST *)s.g_sigma;
+  g.prm = s.gibbs;
+  return g;
+}
+
+}  // namespace cs

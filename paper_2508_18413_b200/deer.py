@@ -1,0 +1,396 @@
+"""Newton fixed-point drivers for evaluating chains in parallel on B200
+(mirror of chainscan/deer.py).
+
+``run_deer`` has two realisations with identical semantics:
+
+* fused: built-in systems (MALA / HMC on register-resident targets, Gibbs)
+  without a sliding window or full trace run the WHOLE solve as one
+  cooperative persistent CUDA kernel (cs_deer_solve): f_t, the Jacobian
+  estimate, element formation, the scan, the convergence test and all
+  bookkeeping stay on device; one host sync at the end.
+* host-driven: any TransitionSystem (user systems written with torch,
+  windowed solves, full traces).  Each iteration queues CUDA kernels for the
+  finite checks, Picard test, Hutchinson accumulation, element formation,
+  scan and bookkeeping, and reads back a few scalars to branch exactly like
+  deer.py:261-319.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import JACOBIAN_MODES, ChainDivergedError, StructuralError, TransitionSystem, as_steps
+from .errors import ConfigurationError
+from .noise import rademacher_probe
+from .pscan import Block2x2Elements, DenseElements, DiagElements, parallel_affine_solve
+
+__all__ = ["DeerConfig", "DeerResult", "default_max_iters", "converged", "hutchinson_diag",
+           "deer_iterate", "run_deer"]
+
+_DIVERGENCE_FACTOR = 1e6
+_NO_STEP = 2 ** 63 - 1
+_MODE_CODE = {"dense": _lib.CS_MODE_DENSE, "diag-stochastic": _lib.CS_MODE_DIAG,
+              "block2x2-stochastic": _lib.CS_MODE_BLOCK}
+
+
+def default_max_iters(T: int) -> int:
+    return math.ceil(50 + 5 * T * 1e-4)
+
+
+@dataclass
+class DeerConfig:
+    """Solver knobs (deer.py:55-93).  ``workers``/``chunk`` are accepted for API
+    compatibility; ``fused`` = False forces the host-driven path."""
+
+    mode: str = "dense"
+    atol: float = 1e-4
+    rtol: float = 1e-3
+    max_iters: int | None = None
+    hutchinson_samples: int = 1
+    damping: float = 1.0
+    clip: float = math.inf
+    window_len: int | None = None
+    full_trace: bool = False
+    preconditioner: np.ndarray | None = None
+    workers: int | None = None
+    chunk: int | None = None
+    fused: bool = True
+
+    def __post_init__(self):
+        if self.mode not in JACOBIAN_MODES:
+            raise ConfigurationError(f"unknown mode {self.mode!r}; expected one of {JACOBIAN_MODES}")
+        if self.atol <= 0 or self.rtol < 0:
+            raise ConfigurationError("need atol > 0 and rtol >= 0")
+        if self.max_iters is not None and self.max_iters < 1:
+            raise ConfigurationError("max_iters must be >= 1")
+        if self.hutchinson_samples < 1:
+            raise ConfigurationError("hutchinson_samples must be >= 1")
+        if not 0.0 < self.damping <= 1.0:
+            raise ConfigurationError("damping must lie in (0, 1]")
+        if self.clip <= 0:
+            raise ConfigurationError("clip must be positive")
+        if self.window_len is not None and self.window_len < 1:
+            raise ConfigurationError("window_len must be >= 1")
+        if self.preconditioner is not None:
+            p = np.asarray(self.preconditioner.cpu() if torch.is_tensor(self.preconditioner)
+                           else self.preconditioner, float)
+            if p.ndim != 1 or np.any(p <= 0):
+                raise ConfigurationError("preconditioner must be a positive vector")
+            self.preconditioner = p
+
+
+@dataclass
+class DeerResult:
+    trace: torch.Tensor
+    iterations: int
+    delta_history: np.ndarray
+    converged: bool
+    per_step_converged_at: torch.Tensor
+    full_trace: list | None = None
+    stats: dict = field(default_factory=dict)
+
+
+class _Scratch:
+    """Small device scalars read back once per host-driven iteration."""
+
+    def __init__(self, device):
+        self.i64 = torch.empty(1, dtype=torch.int64, device=device)
+        self.u32 = torch.empty(1, dtype=torch.int32, device=device)
+        self.f64 = torch.empty(1, dtype=torch.float64, device=device)
+
+
+def _scratch(device):
+    return _Scratch(device)
+
+
+def converged(prev, next_, atol: float, rtol: float):
+    """(all |next-prev| <= atol + rtol|next|, max |next-prev|) (deer.py:107-115)."""
+    prev = torch.as_tensor(prev)
+    next_ = torch.as_tensor(next_, dtype=prev.dtype, device=prev.device)
+    if prev.shape != next_.shape:
+        raise StructuralError(f"shape mismatch: {tuple(prev.shape)} vs {tuple(next_.shape)}")
+    if not prev.is_cuda:
+        prev, next_ = prev.cuda(), next_.cuda()
+    sc = _scratch(prev.device)
+    rc = _lib.load().cs_converged(_lib.dtype_code(prev.dtype), _lib.ptr(prev.contiguous()),
+                                  _lib.ptr(next_.contiguous()), prev.numel(), float(atol), float(rtol),
+                                  _lib.ptr(sc.u32), _lib.ptr(sc.f64), _lib.stream_ptr())
+    _lib.check(rc)
+    vals = torch.cat([sc.u32.to(torch.float64), sc.f64]).cpu().numpy()
+    return bool(vals[0] == 0), float(vals[1])
+
+
+def hutchinson_diag(jvp_batch, ts, S, n_samples: int, probe_seed: int, iteration: int):
+    """mean_k z_k * (J z_k) with device Rademacher probes (deer.py:118-132)."""
+    S = torch.as_tensor(S)
+    est = torch.empty_like(S)
+    lib = _lib.load()
+    dt = _lib.dtype_code(S.dtype)
+    tt = as_steps(ts, S.device)
+    for k in range(n_samples):
+        z = rademacher_probe(probe_seed, iteration, tt, k, S.shape[-1], dtype=S.dtype, device=S.device)
+        jz = torch.as_tensor(jvp_batch(tt, S, z), dtype=S.dtype, device=S.device).contiguous()
+        rc = lib.cs_hutchinson_accumulate(dt, _lib.ptr(est), _lib.ptr(z), _lib.ptr(jz), est.numel(),
+                                          int(k == 0), float(n_samples) if k == n_samples - 1 else 0.0,
+                                          _lib.stream_ptr())
+        _lib.check(rc)
+    return est
+
+
+def _first_nonfinite(arr):
+    arr = arr.contiguous()
+    sc = _scratch(arr.device)
+    width = arr[0].numel() if arr.shape[0] else 1
+    rc = _lib.load().cs_first_nonfinite_row(_lib.dtype_code(arr.dtype), _lib.ptr(arr), arr.shape[0], width,
+                                            _lib.ptr(sc.i64), _lib.stream_ptr())
+    _lib.check(rc)
+    return int(sc.i64.item())
+
+
+def _check_finite(arr, what, ts, iteration):
+    row = _first_nonfinite(arr)
+    if row != _NO_STEP:
+        t = int(ts[row])
+        raise ChainDivergedError(f"non-finite {what} at step {t} (iteration {iteration + 1})",
+                                 step=t, iteration=iteration + 1)
+
+
+def _pre_tensor(cfg, device):
+    if cfg.preconditioner is None:
+        return None
+    return torch.as_tensor(cfg.preconditioner, dtype=torch.float64, device=device)
+
+
+def _iterate_range(system, ts, guess, s0_local, cfg, iteration, f=None):
+    """One Newton update on the steps ts seeded from s0_local (deer.py:147-208)."""
+    lib = _lib.load()
+    dt = _lib.dtype_code(guess.dtype)
+    st = _lib.stream_ptr()
+    guess = guess.contiguous()
+    s0_local = s0_local.contiguous()
+    prev = torch.cat([s0_local[None], guess[:-1]], dim=0)
+    if f is None:
+        f = system.step_batch(ts, prev)
+        _check_finite(f, "step value", ts, iteration)
+    f = f.to(guess.dtype).contiguous()
+    T, W = guess.shape
+    pre = _pre_tensor(cfg, guess.device)
+    clip = float(cfg.clip)
+    if cfg.mode == "dense":
+        Jin = torch.as_tensor(system.dense_jacobian_batch(ts, prev), dtype=guess.dtype).contiguous()
+        _check_finite(Jin, "jacobian", ts, iteration)
+        J = torch.empty_like(Jin)
+        u = torch.empty_like(f)
+        rc = lib.cs_form_dense(dt, _lib.ptr(Jin), _lib.ptr(f), _lib.ptr(s0_local), _lib.ptr(guess), T, W,
+                               _lib.ptr(pre), float(cfg.damping), clip, _lib.ptr(J), _lib.ptr(u), st)
+        _lib.check(rc)
+        elements = DenseElements(J, u)
+    elif cfg.mode == "diag-stochastic":
+        d = hutchinson_diag(system.jvp_batch, ts, prev, cfg.hutchinson_samples, system.noise.seed, iteration)
+        _check_finite(d, "jacobian diagonal", ts, iteration)
+        j = torch.empty_like(d)
+        u = torch.empty_like(f)
+        rc = lib.cs_form_diag(dt, _lib.ptr(d.contiguous()), _lib.ptr(f), _lib.ptr(s0_local), _lib.ptr(guess), T,
+                              W, _lib.ptr(pre), float(cfg.damping), clip, _lib.ptr(j), _lib.ptr(u), st)
+        _lib.check(rc)
+        elements = DiagElements(j, u)
+    else:
+        a, b, c, dd = (torch.as_tensor(x, dtype=guess.dtype).contiguous() for x in
+                       system.block_jacobian_batch(ts, prev, cfg.hutchinson_samples, iteration))
+        _check_finite(torch.cat([a, b, c, dd], dim=-1), "block jacobian", ts, iteration)
+        half = a.shape[-1]
+        outs = [torch.empty_like(a) for _ in range(4)]
+        u = torch.empty_like(f)
+        rc = lib.cs_form_block(dt, _lib.ptr(a), _lib.ptr(b), _lib.ptr(c), _lib.ptr(dd), _lib.ptr(f),
+                               _lib.ptr(s0_local), _lib.ptr(guess), T, half, _lib.ptr(pre), float(cfg.damping), clip,
+                               *[_lib.ptr(o) for o in outs], _lib.ptr(u), st)
+        _lib.check(rc)
+        elements = Block2x2Elements(*outs, u)
+    return parallel_affine_solve(elements, s0_local)
+
+
+def deer_iterate(system: TransitionSystem, guess, s0, cfg: DeerConfig, iteration: int = 0):
+    """One full-sequence Newton update from ``guess`` (deer.py:211-218)."""
+    guess = torch.as_tensor(guess, dtype=system.dtype, device=system.device)
+    s0 = torch.as_tensor(s0, dtype=system.dtype, device=system.device)
+    ts = torch.arange(1, guess.shape[0] + 1, device=system.device)
+    return _iterate_range(system, ts, guess, s0, cfg, iteration)
+
+
+def _guard(dmax, d0, iteration):
+    if d0 > 0 and dmax > _DIVERGENCE_FACTOR * d0:
+        raise ChainDivergedError(
+            f"fixed-point iteration diverging: delta_max {dmax:.3e} exceeds "
+            f"{_DIVERGENCE_FACTOR:.0e} x initial {d0:.3e}", iteration=iteration)
+
+
+def _bookkeeping(guess, nxt, atol, rtol, iteration, last_fail, sc):
+    T, W = guess.shape
+    rc = _lib.load().cs_update_bookkeeping(_lib.dtype_code(guess.dtype), _lib.ptr(guess), _lib.ptr(nxt), T, W,
+                                           float(atol), float(rtol), int(iteration), _lib.ptr(last_fail),
+                                           _lib.ptr(sc.u32), _lib.ptr(sc.f64), _lib.stream_ptr())
+    _lib.check(rc)
+    vals = torch.cat([sc.u32.to(torch.float64), sc.f64]).cpu().numpy()
+    return int(vals[0]), float(vals[1])
+
+
+def _fused_ok(system, cfg):
+    desc_fn = getattr(system, "desc", None)
+    if not cfg.fused or desc_fn is None or cfg.full_trace:
+        return False
+    if cfg.window_len is not None and cfg.window_len < system.T:
+        return False
+    if getattr(system, "_blr", False) or getattr(system, "leapfrog_mode", "sequential") == "parallel":
+        return False
+    d = desc_fn()
+    return bool(_lib.load().cs_deer_supported(ctypes.byref(d), _MODE_CODE[cfg.mode],
+                                              _lib.dtype_code(system.dtype)))
+
+
+def _run_fused(system, s0, cfg, max_iters):
+    lib = _lib.load()
+    T, D = system.T, system.dim
+    dev, dtype = system.device, system.dtype
+    d = system.desc()
+    trace = torch.empty((T, D), dtype=dtype, device=dev)
+    psca = torch.empty(T, dtype=torch.int32, device=dev)
+    hist = torch.empty(max_iters, dtype=torch.float64, device=dev)
+    ws_bytes = lib.cs_deer_workspace_bytes(ctypes.byref(d), _lib.dtype_code(dtype), max_iters)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    pre = _pre_tensor(cfg, dev)
+    if pre is not None and pre.shape != (D,):
+        raise StructuralError(f"preconditioner must have shape ({D},)")
+    c = _lib.cs_deer_config()
+    c.mode = _MODE_CODE[cfg.mode]
+    c.atol, c.rtol = float(cfg.atol), float(cfg.rtol)
+    c.max_iters = int(max_iters)
+    c.hutchinson_samples = int(cfg.hutchinson_samples)
+    c.damping, c.clip = float(cfg.damping), float(cfg.clip)
+    c.preconditioner = 0 if pre is None else pre.data_ptr()
+    res = _lib.cs_deer_result()
+    rc = lib.cs_deer_solve(ctypes.byref(d), ctypes.byref(c), _lib.dtype_code(dtype), _lib.ptr(s0.contiguous()),
+                           _lib.ptr(trace), _lib.ptr(psca), _lib.ptr(hist), _lib.ptr(ws), ws_bytes,
+                           ctypes.byref(res), _lib.stream_ptr())
+    it = int(res.iterations)
+    # work counters as the reference would have accumulated them
+    passes = it + (0 if res.stop_reason in (_lib.CS_STOP_NOFAIL,) or res.err_kind == _lib.CS_DIV_GUARD else 1)
+    updates = it + (1 if res.err_kind == _lib.CS_DIV_JACOBIAN else 0)
+    system.n_step_evals += T * passes
+    if cfg.mode == "diag-stochastic":
+        system.n_jvp_evals += T * cfg.hutchinson_samples * updates
+    elif cfg.mode == "dense":
+        system.n_jvp_evals += T * D * updates
+    else:
+        system.n_hvp_evals += T * cfg.hutchinson_samples * updates
+    if rc == _lib.CS_ERR_DIVERGED:
+        step = None if res.err_step < 0 else int(res.err_step)
+        iteration = None if res.err_iteration < 0 else int(res.err_iteration)
+        kind = {_lib.CS_DIV_PROPOSAL: f"non-finite {getattr(system, '_what', 'proposal')} at step {step}",
+                _lib.CS_DIV_STEP: f"non-finite step value at step {step} (iteration {iteration})",
+                _lib.CS_DIV_JACOBIAN: f"non-finite jacobian at step {step} (iteration {iteration})",
+                _lib.CS_DIV_GUARD: (f"fixed-point iteration diverging: delta_max {res.guard_dmax:.3e} exceeds "
+                                    f"{_DIVERGENCE_FACTOR:.0e} x initial {res.guard_d0:.3e}")}[res.err_kind]
+        raise ChainDivergedError(kind, step=step, iteration=iteration)
+    _lib.check(rc)
+    stats = {"path": "fused", "grid_blocks": int(res.grid_blocks), "steps_per_thread": int(res.steps_per_thread),
+             "kept_in_registers": bool(res.kept_in_registers), "launches": int(res.launches),
+             "stop_reason": int(res.stop_reason)}
+    return DeerResult(trace=trace, iterations=it, delta_history=hist[:it].cpu().numpy(),
+                      converged=res.status == _lib.CS_RUN_CONVERGED, per_step_converged_at=psca,
+                      full_trace=None, stats=stats)
+
+
+def run_deer(system: TransitionSystem, s0, cfg: DeerConfig) -> DeerResult:
+    """Drive Newton iterations to convergence or max_iters (deer.py:230-328)."""
+    s0 = torch.as_tensor(s0, dtype=system.dtype, device=system.device).contiguous()
+    if tuple(s0.shape) != (system.dim,):
+        raise StructuralError(f"s0 must have shape ({system.dim},), got {tuple(s0.shape)}")
+    T = system.T
+    max_iters = cfg.max_iters if cfg.max_iters is not None else default_max_iters(T)
+    if _fused_ok(system, cfg):
+        return _run_fused(system, s0, cfg, max_iters)
+    return _run_host(system, s0, cfg, max_iters)
+
+
+def _run_host(system, s0, cfg, max_iters):
+    T = system.T
+    dev = system.device
+    atol, rtol = cfg.atol, cfg.rtol
+    guess = s0.expand(T, -1).clone()
+    history: list[float] = []
+    full = [] if cfg.full_trace else None
+    last_fail = torch.zeros(T, dtype=torch.int32, device=dev)
+    sc = _scratch(dev)
+    d0 = None
+    done = False
+    iterations = 0
+
+    if cfg.window_len is None or cfg.window_len >= T:
+        ts = torch.arange(1, T + 1, device=dev)
+        while True:
+            prev = torch.cat([s0[None], guess[:-1]], dim=0)
+            f = system.step_batch(ts, prev).to(guess.dtype)
+            _check_finite(f, "step value", ts, iterations)
+            ok, _ = converged(guess, f, atol, rtol)
+            if ok:
+                done = True
+                break
+            if iterations >= max_iters:
+                break
+            nxt = _iterate_range(system, ts, guess, s0, cfg, iterations, f=f)
+            iterations += 1
+            nfail, dmax = _bookkeeping(guess, nxt, atol, rtol, iterations, last_fail, sc)
+            history.append(dmax)
+            if full is not None:
+                full.append(nxt.clone())
+            guess = nxt
+            if d0 is None:
+                d0 = dmax
+            _guard(dmax, d0, iterations)
+            if nfail == 0:
+                done = True
+                break
+    else:
+        win = cfg.window_len
+        w = 0
+        while w < T:
+            lo, hi = w, min(w + win, T)
+            ts = torch.arange(lo + 1, hi + 1, device=dev)
+            seed_state = s0 if lo == 0 else guess[lo - 1]
+            prev = torch.cat([seed_state[None], guess[lo:hi - 1]], dim=0)
+            f = system.step_batch(ts, prev).to(guess.dtype)
+            _check_finite(f, "step value", ts, iterations)
+            ok, _ = converged(guess[lo:hi], f, atol, rtol)
+            if ok:
+                w = hi
+                continue
+            if iterations >= max_iters:
+                break
+            nxt = _iterate_range(system, ts, guess[lo:hi], seed_state.clone(), cfg, iterations, f=f)
+            iterations += 1
+            win_fail = torch.zeros(hi - lo, dtype=torch.int32, device=dev)
+            nfail, dmax = _bookkeeping(guess[lo:hi].contiguous(), nxt, atol, rtol, 1, win_fail, sc)
+            history.append(dmax)
+            failmask = win_fail > 0
+            last_fail[lo:hi][failmask] = iterations
+            guess[lo:hi] = nxt
+            if full is not None:
+                full.append(guess.clone())
+            if d0 is None:
+                d0 = dmax
+            _guard(dmax, d0, iterations)
+            if nfail:
+                first = int(torch.nonzero(failmask)[0, 0])
+                w = lo + first
+            else:
+                w = hi
+        done = w >= T
+
+    return DeerResult(trace=guess, iterations=iterations, delta_history=np.array(history), converged=done,
+                      per_step_converged_at=last_fail + 1, full_trace=full, stats={"path": "host"})

@@ -1,0 +1,300 @@
+"""CUDA path vs the reference (golden fixtures) and the CPU oracle.
+
+Bar (stated here, per north_star): f64 runs match the reference's f64 run_deer
+traces to 1e-8 with the SAME Newton iteration count and per-step convergence
+record; f32 runs (states/elements in fp32, gate margins in f64) match within
+the reference's own convergence envelope |gpu - ref| <= 1e-4 + 1e-3|ref|,
+iterations within +-1, identical accept/reject pattern.  Integer/bit work
+(counter hash, uniforms, Rademacher probes) is bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+cs = pytest.importorskip("paper_2508_18413_b200")
+
+F32_ATOL, F32_RTOL = 1e-4, 1e-3
+
+
+def np_(t):
+    return t.detach().cpu().numpy() if torch.is_tensor(t) else np.asarray(t)
+
+
+def envelope(a, ref, atol=F32_ATOL, rtol=F32_RTOL):
+    return bool(np.all(np.abs(np_(a) - ref) <= atol + rtol * np.abs(ref)))
+
+
+# ---------------------------------------------------------------------------
+# noise (noise.py:50-171)
+
+
+def test_noise_tables_match_reference(cuda_device):
+    g = golden("noise")
+    layout = {"xi": cs.SlotSpec(3, "standard-normal"), "u": cs.SlotSpec(1, "uniform-0-1"),
+              "g": cs.SlotSpec(2, "chi-squared", df=9.1), "g_small": cs.SlotSpec(2, "chi-squared", df=0.1),
+              "g_big": cs.SlotSpec(8, "chi-squared", df=20.1)}
+    tab = cs.NoiseTable(7, layout, 300)
+    np.testing.assert_array_equal(np_(tab.block("u", np.arange(301))), g["u"])          # bit-exact
+    np.testing.assert_allclose(np_(tab.block("xi", np.arange(301))), g["xi"], rtol=1e-14, atol=1e-14)
+    for k in ("g", "g_small", "g_big"):
+        np.testing.assert_allclose(np_(tab.block(k, np.arange(301))), g[k], rtol=1e-11, atol=1e-300)
+    big = cs.NoiseTable(2**63 + 12345, {"xi": cs.SlotSpec(2, "standard-normal")}, 10)
+    np.testing.assert_allclose(np_(big.block("xi", np.arange(11))), g["xi_bigseed"], rtol=1e-14, atol=1e-14)
+    probes = [np_(cs.rademacher_probe(9, it, np.arange(1, 65), k, 6)) for it in range(3) for k in range(3)]
+    np.testing.assert_array_equal(np.stack(probes), g["probes"])
+
+
+def test_chi_squared_inverts_the_gamma_cdf(cuda_device):
+    from scipy.special import gammainc
+
+    for df in (0.1, 9.1, 20.1):
+        t = cs.NoiseTable(13, {"g": cs.SlotSpec(1, "chi-squared", df=df)}, T=2000)
+        u = cs.NoiseTable(13, {"g": cs.SlotSpec(1, "uniform-0-1")}, T=2000)
+        x = np_(t.block("g", np.arange(2000)))[:, 0]
+        uu = np_(u.block("g", np.arange(2000)))[:, 0]
+        assert np.all(x > 0)
+        assert np.max(np.abs(gammainc(df / 2.0, x / 2.0) - uu)) < 1e-12   # test_noise.py:72-80
+
+
+# ---------------------------------------------------------------------------
+# scans (pscan.py:273-354)
+
+
+@pytest.mark.parametrize("T", [1, 257, 1024])
+def test_scans_match_reference_golden(cuda_device, T):
+    g = golden("scan")
+    dev = cuda_device
+    t = lambda k: torch.as_tensor(g[k], device=dev)
+    out = cs.parallel_affine_solve(cs.DiagElements(t(f"diag_{T}_j"), t(f"diag_{T}_u")), t(f"diag_{T}_s0"))
+    np.testing.assert_allclose(np_(out), g[f"diag_{T}_out"], atol=1e-12, rtol=1e-12)
+    out = cs.parallel_affine_solve(cs.DenseElements(t(f"dense_{T}_J"), t(f"dense_{T}_u")), t(f"dense_{T}_s0"))
+    np.testing.assert_allclose(np_(out), g[f"dense_{T}_out"], atol=1e-12, rtol=1e-12)
+    el = cs.Block2x2Elements(*(t(f"block_{T}_{k}") for k in "abcdu"))
+    out = cs.parallel_affine_solve(el, t(f"block_{T}_s0"))
+    np.testing.assert_allclose(np_(out), g[f"block_{T}_out"], atol=1e-12, rtol=1e-12)
+
+
+def test_scan_kats(cuda_device):
+    e = cs.DiagElements(torch.tensor([[2.0], [3.0], [4.0]], device=cuda_device),
+                        torch.ones((3, 1), dtype=torch.float64, device=cuda_device))
+    np.testing.assert_array_equal(np_(cs.parallel_affine_solve(e, torch.tensor([1.0], device=cuda_device)))[:, 0],
+                                  [3.0, 10.0, 41.0])
+    T, D = 64, 3
+    e = cs.DiagElements(torch.ones((T, D), dtype=torch.float64, device=cuda_device),
+                        torch.zeros((T, D), dtype=torch.float64, device=cuda_device))
+    s0 = torch.tensor([4.0, -1.0, 0.25], dtype=torch.float64, device=cuda_device)
+    assert bool((cs.parallel_affine_solve(e, s0) == s0).all())
+
+
+@pytest.mark.parametrize("D", [1, 2, 5, 18, 64, 65, 100, 300])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_diag_and_block_scans_vs_oracle(cuda_device, D, dtype):
+    rng = np.random.default_rng(D)
+    T = 20_011
+    j = rng.uniform(-0.95, 0.95, (T, D))
+    u = rng.normal(size=(T, D))
+    s0 = rng.normal(size=D)
+    want = O.parallel_affine_solve(O.DiagElements(j, u), s0, workers=8)
+    tt = lambda x: torch.as_tensor(x, dtype=dtype, device=cuda_device)
+    got = np_(cs.parallel_affine_solve(cs.DiagElements(tt(j), tt(u)), tt(s0)))
+    tol = 1e-11 if dtype == torch.float64 else 2e-5
+    np.testing.assert_allclose(got, want, atol=tol * 10, rtol=tol)
+    a, b, c, d = (rng.uniform(-0.65, 0.65, (T, D)) for _ in range(4))
+    ub = rng.normal(size=(T, 2 * D))
+    s0b = rng.normal(size=2 * D)
+    want = O.parallel_affine_solve(O.Block2x2Elements(a, b, c, d, ub), s0b, workers=8)
+    got = np_(cs.parallel_affine_solve(cs.Block2x2Elements(tt(a), tt(b), tt(c), tt(d), tt(ub)), tt(s0b)))
+    np.testing.assert_allclose(got, want, atol=tol * 10, rtol=tol)
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 4, 6, 8])
+def test_dense_scan_vs_oracle(cuda_device, D):
+    rng = np.random.default_rng(40 + D)
+    T = 5003
+    J = rng.normal(size=(T, D, D))
+    J *= (0.9 / np.abs(np.linalg.eigvals(J)).max(axis=-1))[:, None, None]
+    u = rng.normal(size=(T, D))
+    s0 = rng.normal(size=D)
+    want = O.parallel_affine_solve(O.DenseElements(J, u), s0, workers=8)
+    tt = lambda x: torch.as_tensor(x, device=cuda_device)
+    got = np_(cs.parallel_affine_solve(cs.DenseElements(tt(J), tt(u)), tt(s0)))
+    np.testing.assert_allclose(got, want, atol=1e-10, rtol=1e-10)
+
+
+# ---------------------------------------------------------------------------
+# systems: batched f_t and JVPs vs the oracle (samplers.py)
+
+
+def _pair(kind, dtype=torch.float64, T=64):
+    if kind == "mala_gauss":
+        mu, L = [1.0, -1.0], [[1.0, 0.0], [-0.6, 1.2]]
+        return (cs.MalaKernel(cs.model_logp_grad_hvp(cs.gaussian(mu, L)), 0.4, seed=3, T=T, dtype=dtype),
+                O.MalaKernel(O.gaussian(mu, L), 0.4, seed=3, T=T))
+    if kind == "mala_mog":
+        return (cs.MalaKernel(cs.model_logp_grad_hvp(cs.mog()), 0.1, seed=5, T=T, dtype=dtype),
+                O.MalaKernel(O.mog(), 0.1, seed=5, T=T))
+    if kind == "mala_std5":
+        return (cs.MalaKernel(cs.model_logp_grad_hvp(cs.std_normal(5)), 0.3, seed=1, T=T, dtype=dtype),
+                O.MalaKernel(O.std_normal(5), 0.3, seed=1, T=T))
+    if kind == "hmc_rosen":
+        return (cs.HmcKernel(cs.model_logp_grad_hvp(cs.rosenbrock(b=0.1, scale2=1.0)), 0.5, 8, seed=0, T=T,
+                             dtype=dtype),
+                O.HmcKernel(O.rosenbrock(b=0.1, scale2=1.0), 0.5, 8, seed=0, T=T))
+    if kind == "hmc_gauss_mass":
+        mu, L = [0.5, 0.0, -0.5], [[1.0, 0, 0], [0.3, 1.1, 0], [0.0, -0.2, 0.9]]
+        return (cs.HmcKernel(cs.model_logp_grad_hvp(cs.gaussian(mu, L)), 0.2, 5, seed=2, T=T,
+                             mass=[1.0, 2.0, 0.5], dtype=dtype),
+                O.HmcKernel(O.gaussian(mu, L), 0.2, 5, seed=2, T=T, mass=[1.0, 2.0, 0.5]))
+    if kind == "leapfrog_rosen":
+        return (cs.LeapfrogSystem(cs.model_logp_grad_hvp(cs.rosenbrock()), 0.05, 16, probe_seed=4, dtype=dtype),
+                O.LeapfrogSystem(O.rosenbrock(), 0.05, 16, probe_seed=4))
+    if kind == "gibbs":
+        data_c = cs.generate_eight_schools()
+        data_o = O.generate_eight_schools()
+        return cs.GibbsKernel(data_c, seed=0, T=T, dtype=dtype), O.GibbsKernel(data_o, seed=0, T=T)
+    raise KeyError(kind)
+
+
+SYSTEMS = ["mala_gauss", "mala_mog", "mala_std5", "hmc_rosen", "hmc_gauss_mass", "leapfrog_rosen", "gibbs"]
+
+
+@pytest.mark.parametrize("kind", SYSTEMS)
+def test_system_step_and_jvp_vs_oracle(cuda_device, kind):
+    gs, os_ = _pair(kind)
+    rng = np.random.default_rng(11)
+    n = os_.T if kind != "leapfrog_rosen" else 16
+    D = os_.dim
+    S = rng.normal(size=(n, D)) * 0.7
+    if kind == "gibbs":
+        S[:, 0] = np.abs(S[:, 0]) + 1.0
+        S[:, 10:] = np.abs(S[:, 10:]) * 50 + 1.0
+    V = rng.normal(size=(n, D))
+    ts = np.arange(1, n + 1)
+    np.testing.assert_allclose(np_(gs.step_batch(ts, S)), os_.step_batch(ts, S), rtol=1e-11, atol=1e-11)
+    np.testing.assert_allclose(np_(gs.jvp_batch(ts, S, V)), os_.jvp_batch(ts, S, V), rtol=1e-9, atol=1e-9)
+    if hasattr(os_, "relaxed_jvp_batch"):
+        np.testing.assert_allclose(np_(gs.relaxed_jvp_batch(ts, S, V)), os_.relaxed_jvp_batch(ts, S, V),
+                                   rtol=1e-9, atol=1e-9)
+    if kind == "leapfrog_rosen":
+        for it in (0, 3):
+            got = gs.block_jacobian_batch(ts, S, 2, it)
+            want = os_.block_jacobian_batch(ts, S, 2, it)
+            for g_, w_ in zip(got, want):
+                np.testing.assert_allclose(np_(g_), w_, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["mala_gauss", "mala_mog", "hmc_rosen", "gibbs", "leapfrog_rosen"])
+def test_sequential_evaluate_vs_oracle(cuda_device, kind):
+    gs, os_ = _pair(kind, T=500)
+    if kind == "gibbs":
+        s0 = os_.initial_state()
+        np.testing.assert_allclose(np_(gs.initial_state()), s0, rtol=1e-11)
+    elif kind == "leapfrog_rosen":
+        s0 = np.array([0.4, -0.3, 0.6, 0.1])
+    else:
+        s0 = np.zeros(os_.dim)
+    T = os_.T
+    want = O.sequential_evaluate(os_, s0, T)
+    got = np_(cs.sequential_evaluate(gs, s0, T))
+    np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-9)
+
+
+# ---------------------------------------------------------------------------
+# whole-chain solves vs the reference's own run_deer (golden)
+
+
+def _deer_cmp(res, g, prefix, dtype, exact_iters=True):
+    it_ref = int(g[prefix + "iterations"])
+    if dtype == torch.float64:
+        assert res.iterations == it_ref
+        np.testing.assert_allclose(np_(res.trace), g[prefix + "trace"], atol=1e-8, rtol=1e-8)
+        np.testing.assert_array_equal(np_(res.per_step_converged_at), g[prefix + "psca"])
+        np.testing.assert_allclose(res.delta_history, g[prefix + "delta_history"], rtol=1e-6, atol=1e-12)
+    else:
+        assert abs(res.iterations - it_ref) <= 1
+        assert envelope(res.trace, g[prefix + "trace"])
+    assert res.converged == bool(g[prefix + "converged"])
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_run_deer_mala_gauss2d(cuda_device, dtype):
+    g = golden("mala_gauss2d")
+    m = cs.model_logp_grad_hvp(cs.gaussian([1.0, -1.0], [[1.0, 0.0], [-0.6, 1.2]]))
+    k = cs.MalaKernel(m, 0.4, seed=0, T=2000, dtype=dtype)
+    np.testing.assert_allclose(np_(cs.sequential_evaluate(k, np.zeros(2))), g["seq"], atol=1e-6 if dtype == torch.float32 else 1e-10)
+    r = cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="dense"))
+    assert r.stats["path"] == "fused"
+    _deer_cmp(r, g, "dense_", dtype)
+    _deer_cmp(cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="diag-stochastic")), g, "diag_", dtype)
+    _deer_cmp(cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="dense", atol=1e-6, rtol=1e-5)), g, "tight_", dtype)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_run_deer_mala_rosen2d(cuda_device, dtype):
+    g = golden("mala_rosen2d")
+    k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.rosenbrock(b=0.1, scale2=1.0)), 0.5, seed=0, T=2000, dtype=dtype)
+    _deer_cmp(cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="dense")), g, "dense_", dtype)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_run_deer_hmc_rosen2d(cuda_device, dtype):
+    g = golden("hmc_rosen2d")
+    m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
+    k = cs.HmcKernel(m, 0.5, 8, seed=0, T=5000, dtype=dtype)
+    np.testing.assert_allclose(np_(cs.sequential_evaluate(k, np.zeros(2))), g["seq"],
+                               atol=1e-5 if dtype == torch.float32 else 1e-9)
+    _deer_cmp(cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="diag-stochastic", clip=1.0)), g, "diagclip_", dtype)
+    _deer_cmp(cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="dense", damping=0.5, clip=1.0, atol=1e-6, rtol=1e-5)),
+              g, "dense_", dtype)
+
+
+def test_run_deer_mog_damped(cuda_device):
+    g = golden("mala_mog2d")
+    k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.mog()), 0.1, seed=3, T=1000)
+    _deer_cmp(cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="diag-stochastic", damping=0.5, max_iters=300)),
+              g, "damped_", torch.float64)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_run_deer_gibbs(cuda_device, dtype):
+    g = golden("gibbs_schools")
+    k = cs.GibbsKernel(cs.generate_eight_schools(), seed=0, T=3000, dtype=dtype)
+    s0 = k.initial_state()
+    np.testing.assert_allclose(np_(s0), g["s0"], rtol=1e-10)
+    cfg = cs.DeerConfig(mode="diag-stochastic", hutchinson_samples=3, preconditioner=k.recommended_preconditioner(),
+                        max_iters=400)
+    r = cs.run_deer(k, g["s0"], cfg)
+    _deer_cmp(r, g, "diag3_", dtype)
+
+
+def test_run_deer_host_path_matches_fused(cuda_device):
+    m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
+    k = cs.HmcKernel(m, 0.5, 8, seed=0, T=3000)
+    a = cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="diag-stochastic", clip=1.0))
+    b = cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="diag-stochastic", clip=1.0, fused=False))
+    assert a.stats["path"] == "fused" and b.stats["path"] == "host"
+    assert a.iterations == b.iterations
+    np.testing.assert_allclose(np_(a.trace), np_(b.trace), atol=1e-10)
+    np.testing.assert_array_equal(np_(a.per_step_converged_at), np_(b.per_step_converged_at))
+
+
+def test_run_deer_leapfrog_block_and_window(cuda_device):
+    g = golden("mala_window")
+    k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.std_normal(2)), 0.3, seed=6, T=512)
+    _deer_cmp(cs.run_deer(k, np.array([1.0, 0.0]), cs.DeerConfig(mode="dense", window_len=64, max_iters=2000)),
+              g, "win64_", torch.float64)
+    k1 = cs.MalaKernel(cs.model_logp_grad_hvp(cs.std_normal(2)), 0.3, seed=6, T=40)
+    _deer_cmp(cs.run_deer(k1, np.array([1.0, 0.0]), cs.DeerConfig(mode="dense", window_len=1, max_iters=500)),
+              g, "win1_", torch.float64)
+    # block one-shot on a Gaussian leapfrog (test_deer.py:250-261)
+    lf = cs.LeapfrogSystem(cs.model_logp_grad_hvp(cs.std_normal(2)), 0.1, 64)
+    s0 = np.array([1.0, -0.5, 0.3, 0.8])
+    r = cs.run_deer(lf, s0, cs.DeerConfig(mode="block2x2-stochastic"))
+    assert r.converged and r.iterations == 1
+    np.testing.assert_allclose(np_(r.trace), np_(cs.sequential_evaluate(lf, s0)), atol=1e-9)

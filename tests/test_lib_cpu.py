@@ -1,0 +1,104 @@
+"""CPU-side checks of the boundary: the C-ABI library loads, exports every
+symbol include/chainscan_b200.h declares, and the host layer validates
+configurations exactly like the reference (no GPU needed)."""
+
+import math
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "chainscan_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(cs_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declarations_are_bound():
+    from paper_2508_18413_b200 import _lib
+
+    assert declared_symbols() == _lib.exported_symbols()
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    from paper_2508_18413_b200 import _lib
+
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("library not built here (run __graft_entry__.build())")
+    lib = _lib.load()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (cs_[a-z0-9_]+)", out))
+    assert set(declared_symbols()) <= exported
+    assert lib.cs_version() == 1
+
+
+def test_struct_layouts_match_header_sizes():
+    from paper_2508_18413_b200 import _lib
+    import ctypes
+
+    # natural alignment: pointers 8, doubles 8 -> sizes fixed by the field lists
+    assert ctypes.sizeof(_lib.cs_target) == 4 + 4 + 4 * 8 + 3 * 8 + 8 + 4 * 8 + 8 + 2 * 8 + 8
+    assert ctypes.sizeof(_lib.cs_deer_config) == 8 + 8 + 8 + 4 + 4 + 8 + 8 + 8
+    assert ctypes.sizeof(_lib.cs_deer_result) == 4 + 4 + 4 + 4 + 8 + 4 + 4 + 8 + 8 + 16
+
+
+@pytest.mark.parametrize("kwargs", [
+    {"mode": "cubic"}, {"atol": 0.0}, {"rtol": -1e-3}, {"max_iters": 0}, {"hutchinson_samples": 0},
+    {"damping": 0.0}, {"damping": 1.5}, {"clip": 0.0}, {"window_len": 0},
+    {"preconditioner": np.array([1.0, -1.0])},
+])
+def test_config_rejects_bad_values(kwargs):
+    # deer.py:72-93 / test_deer.py:503-520
+    from paper_2508_18413_b200 import ConfigurationError, DeerConfig
+
+    with pytest.raises(ConfigurationError):
+        DeerConfig(**kwargs)
+
+
+def test_default_max_iters_and_chunk_policy():
+    from paper_2508_18413_b200 import default_chunk, default_max_iters
+
+    assert default_max_iters(256) == 51
+    assert default_max_iters(10_000) == 55
+    assert default_max_iters(1_000_000) == 550
+    assert default_chunk(100, 4) == 100
+    assert default_chunk(10_000, 4) == 313
+    assert default_chunk(1_000_000, 8) == 15625
+
+
+def test_slot_spec_validation():
+    from paper_2508_18413_b200 import ConfigurationError, SlotSpec
+
+    for args in ((0, "uniform-0-1"), (1, "gaussian"), (1, "chi-squared"), (1, "uniform-0-1", 3.0)):
+        with pytest.raises(ConfigurationError):
+            SlotSpec(*args)
+
+
+def test_fnv_slot_ids_match_oracle():
+    import oracle as O
+    from paper_2508_18413_b200.noise import fnv1a64
+
+    for name in ("xi", "u", "momentum", "g_tau", "xi_theta_prior", "z"):
+        assert fnv1a64(name) == int(O.fnv1a64(name))
+
+
+def test_model_spec_validation():
+    from paper_2508_18413_b200 import ConfigurationError, blr, gaussian, mog, rosenbrock
+
+    with pytest.raises(ConfigurationError):
+        gaussian([0.0, 0.0], [[1.0, 0.0], [0.0, -1.0]])
+    with pytest.raises(ConfigurationError):
+        rosenbrock(scale1=0.0)
+    with pytest.raises(ConfigurationError):
+        mog(weights=[0.5, 0.6], means=[(0, 0), (1, 1)])
+    with pytest.raises(ConfigurationError):
+        blr(np.zeros((3, 2)), np.array([0.0, 2.0, 1.0]))
+    assert math.isinf(float("inf"))
