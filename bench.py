@@ -1,0 +1,328 @@
+"""Benchmark: converged samples/s of a 100K-step HMC chain solved in parallel
+across its length (BASELINE.json configs[1]: HMC on the 2D Rosenbrock,
+eps=0.5, L=8, T=100,000, diagonal quasi-Newton with clip=1 -- the only setting
+the reference itself converges on).
+
+A "step" is one complete run_deer solve of the chain (all Newton iterations to
+convergence) from pre-drawn noise.  ``value`` times the solve with the noise
+already resident in HBM; ``e2e`` goes through the public API from pinned host
+noise (H2D of the noise tables, solve, D2H of the trace) every step.  L2 is
+flushed (256 MiB write) between timed steps, outside the timed region.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "converged samples/s, 100K-step HMC chain solved in parallel (Newton iterations to convergence)"
+T_DEFAULT = 100_000
+EPS, LSTEPS = 0.5, 8
+ROSEN = dict(a=0.0, b=0.1, scale1=1.0, scale2=1.0)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """SM clocks and throttle reasons sampled (NVML, ~1 kHz) during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = None
+
+    def __enter__(self):
+        import threading
+
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return self
+        self._stop = threading.Event()
+
+        def poll():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for name, bit in self.REASONS.items():
+                        if bits & bit:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+                time.sleep(0.001)
+
+        self._t = threading.Thread(target=poll, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle port on the host cores
+
+
+def cpu_solve(T, seed=0):
+    import oracle as O
+
+    k = O.HmcKernel(O.rosenbrock(**ROSEN), EPS, LSTEPS, seed=seed, T=T)
+    t0 = time.perf_counter()
+    res = O.run_deer(k, np.zeros(2), O.DeerConfig(mode="diag-stochastic", clip=1.0))
+    return time.perf_counter() - t0, res
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle.scan import build_lib, workers_default
+
+    build_lib()
+    cores = workers_default()
+    T = args.T
+    for _ in range(args.warmup):
+        cpu_solve(T)
+    times, iters = [], []
+    for _ in range(args.steps):
+        dt, res = cpu_solve(T)
+        times.append(dt)
+        iters.append(res.iterations)
+    tot = float(np.sum(times))
+    value = args.steps * T / tot
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-RNG noise)",
+            "impl": "reference",
+            "config": {"workload": f"HMC Rosenbrock(b=0.1,s2=1) eps={EPS} L={LSTEPS} T={T}, diag quasi-Newton clip=1",
+                       "T": T, "newton_iterations": int(np.median(iters))},
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
+                             "sample": f"full T={T} chain solve per step (oracle/: numpy f_t + pthread C scan)"},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_18413_b200 as cs
+    from paper_2508_18413_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dtype = torch.float32 if args.dtype == "f32" else torch.float64
+    T = args.T
+    seed = rank  # replicas: each rank solves its own chain (weak scaling)
+    model = cs.model_logp_grad_hvp(cs.rosenbrock(**ROSEN))
+    kern = cs.HmcKernel(model, EPS, LSTEPS, seed=seed, T=T, dtype=dtype)
+    cfg = cs.DeerConfig(mode="diag-stochastic", clip=1.0)
+    s0 = torch.zeros(2, dtype=dtype, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    # pinned host copies of the pre-drawn noise (the e2e inputs)
+    mom_dev = kern.noise.table("momentum", dtype)
+    logu_dev = kern.noise.table("u", torch.float64, log_uniform=True)
+    mom_host = mom_dev.cpu().pin_memory()
+    logu_host = logu_dev.cpu().pin_memory()
+    trace_host = torch.empty((T, 2), dtype=dtype).pin_memory()
+    h2d = mom_host.numel() * mom_host.element_size() + logu_host.numel() * logu_host.element_size()
+    d2h = trace_host.numel() * trace_host.element_size()
+
+    def solve():
+        return cs.run_deer(kern, s0, cfg)
+
+    for _ in range(args.warmup):
+        res = solve()
+    torch.cuda.synchronize()
+    iters = res.iterations
+
+    def timed(fn):
+        evs = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record()
+            out = fn()
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs), out
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms_dev, res = timed(solve)
+
+        def e2e_step():
+            kern.noise.load("momentum", mom_host, dtype=dtype)
+            kern.noise.load("u", logu_host, dtype=torch.float64, log_uniform=True)
+            r = solve()
+            trace_host.copy_(r.trace, non_blocking=True)
+            return r
+
+        ms_e2e, _ = timed(e2e_step)
+    torch.cuda.synchronize()
+    if world > 1:
+        t = torch.tensor([ms_dev, ms_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_dev, ms_e2e = t.tolist()
+        dist.barrier()
+
+    value = world * args.steps * T / (ms_dev / 1e3)
+    e2e_value = world * args.steps * T / (ms_e2e / 1e3)
+    # dominant kernel: the persistent solver (one launch per solve); its
+    # algorithmic bytes per Newton pass: read guess rows + noise rows, write the
+    # next guess (+ int32 fail stamps), i.e. T*(2 D s + D s + 8) + T*D*s
+    es = 4 if dtype == torch.float32 else 8
+    passes = iters + 1 if res.stats.get("stop_reason") != _lib.CS_STOP_NOFAIL else iters
+    bytes_per_launch = T * (2 * es + 2 * es + 8) * passes + T * 2 * es * iters + T * 4
+    per_launch_s = ms_dev / 1e3 / args.steps
+    hbm, src = peaks()
+    achieved = bytes_per_launch / per_launch_s / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": None, "kernel": "cs::deer_persistent<Hmc<2,f,Rosenbrock>,DIAG> (whole solve)",
+            "peak_source": src, "algorithmic_bytes_per_launch": bytes_per_launch}
+
+    scan_roof = None
+    cpu_base = None
+    if rank == 0 and not args.no_extras:
+        scan_roof = scan_roofline(cs, dev, hbm, src)
+        cpu_base = cpu_baseline_sample(args)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+                "data": "synthetic (counter-RNG noise, reference seed 0 per rank)",
+                "config": {"workload": f"HMC Rosenbrock(b=0.1,s2=1) eps={EPS} L={LSTEPS} T={T}, "
+                                       f"diag quasi-Newton clip=1, s0=0",
+                           "T": T, "newton_iterations": iters, "parallelism": f"replicas x{world}",
+                           "l2": "flushed (256 MiB write) between timed steps",
+                           "solver": res.stats},
+                "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps},
+                "gpu_launches": args.steps * int(res.stats.get("launches", 3)),
+                "roofline": roof, "scan_roofline": scan_roof, "cpu_baseline": cpu_base,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def scan_roofline(cs, dev, hbm, src):
+    """The standalone diagonal scan at an HBM-sized problem (north_star: the
+    diag/block scans are HBM-bound; 12 B per element in fp32)."""
+    import torch
+
+    T, D = 1 << 22, 18
+    g = torch.Generator(device=dev).manual_seed(0)
+    j = (torch.rand((T, D), generator=g, device=dev) * 1.8 - 0.9).float()
+    u = torch.randn((T, D), generator=g, device=dev).float()
+    s0 = torch.zeros(D, device=dev)
+    out = torch.empty_like(u)
+    el = cs.DiagElements(j, u)
+    for _ in range(3):
+        cs.parallel_affine_solve(el, s0, out=out)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    times = []
+    for _ in range(10):
+        flush.fill_(0.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        cs.parallel_affine_solve(el, s0, out=out)
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = float(np.median(times))
+    byts = 12 * T * D
+    ach = byts / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+            "kernel": "cs::scan_rows<float,DIAG>", "T": T, "D": D, "ms": ms, "peak_source": src,
+            "algorithmic_bytes": byts}
+
+
+def cpu_baseline_sample(args):
+    try:
+        from oracle.scan import build_lib, workers_default
+
+        build_lib()
+        dt, res = cpu_solve(args.T)
+        return {"value": args.T / dt, "unit": "samples/s", "cores": workers_default(), "kind": "port",
+                "sample": f"one full T={args.T} solve ({res.iterations} Newton iterations), oracle/ numpy+C"}
+    except Exception as e:  # the CPU baseline is reported, never required
+        return {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+                "sample": f"unavailable: {e}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--T", type=int, default=T_DEFAULT)
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -143,6 +143,14 @@ int cs_scan_block(int dtype, const void *a, const void *b, const void *c, const 
 int cs_scan_dense(int dtype, const void *J, const void *u, const void *s0, void *out,
                   int64_t T, int32_t D, void *ws, size_t ws_bytes, void *stream);
 
+/* Composed affine map of the whole sequence (the shard carry exchanged by the
+ * T-sharded driver): agg_out f64 = diag [j|u] (2D), block
+ * [A|B|C|E|ux|uv] (6D), dense [M row-major | w] (D*D + D).  Same workspace as
+ * the scan of that mode. */
+int cs_scan_aggregate(int mode, int dtype, const void *e0, const void *e1, const void *e2,
+                      const void *e3, const void *u, int64_t T, int32_t D, double *agg_out,
+                      void *ws, size_t ws_bytes, void *stream);
+
 /* ---- Newton-update building blocks (deer.py:107-208, 273-277) ----------- */
 /* The three reductions below write into caller-owned DEVICE scalars (the host
  * reads them once per iteration, after the stream work it needs is queued).

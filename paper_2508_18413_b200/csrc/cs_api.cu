@@ -336,6 +336,28 @@ int cs_scan_dense(int dtype, const void *J, const void *u, const void *s0, void 
   return do_scan(SCAN_DENSE, dtype, J, nullptr, nullptr, nullptr, u, s0, out, T, D, ws, ws_bytes, stream);
 }
 
+int cs_scan_aggregate(int mode, int dtype, const void *e0, const void *e1, const void *e2, const void *e3,
+                      const void *u, int64_t T, int32_t D, double *agg_out, void *ws, size_t ws_bytes,
+                      void *stream) {
+  if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
+  if (T < 1 || D < 1) return fail(CS_ERR_STRUCTURAL, "bad aggregate shape");
+  const int var = mode == CS_MODE_DIAG ? SCAN_DIAG : mode == CS_MODE_BLOCK ? SCAN_BLOCK : SCAN_DENSE;
+  if (var == SCAN_DENSE && D > 8) return fail(CS_ERR_CONFIG, "dense aggregate supports D <= 8");
+  const ScanPlan p = scan_plan(var, dtype, T, D);
+  if (ws_bytes < p.ws_bytes) return fail(CS_ERR_CONFIG, "scan workspace too small");
+  cudaError_t e;
+  if (dtype == CS_F64) {
+    ScanArgs<double> a{(const double *)e0, (const double *)e1, (const double *)e2, (const double *)e3,
+                       (const double *)u, nullptr, nullptr, T, D};
+    e = launch_aggregate_t<double>(p, a, ws, agg_out, S(stream));
+  } else {
+    ScanArgs<float> a{(const float *)e0, (const float *)e1, (const float *)e2, (const float *)e3,
+                      (const float *)u, nullptr, nullptr, T, D};
+    e = launch_aggregate_t<float>(p, a, ws, agg_out, S(stream));
+  }
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "aggregate launch");
+}
+
 // ---- building blocks -------------------------------------------------------------
 int cs_first_nonfinite_row(int dtype, const void *x, int64_t n, int64_t width, int64_t *d_first,
                            void *stream) {

@@ -158,11 +158,15 @@ cudaError_t launch_solve(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *p
   // register-kept elements only pay off (and only fit) for narrow states
   constexpr bool kKeepOK = MD <= 4;
   auto kr = deer_persistent<Sys, MODE, MD, ST, false>;
+  const size_t keep_smem = sizeof(double) * kSegKeep * Elem<MODE, MD>::W * kSolveThreads;
   int bk = 0, br = 0;
   cudaError_t e;
   if constexpr (kKeepOK) {
+    e = cudaFuncSetAttribute(deer_persistent<Sys, MODE, MD, ST, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)keep_smem);
+    if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, deer_persistent<Sys, MODE, MD, ST, true>,
-                                                      kSolveThreads, 0);
+                                                      kSolveThreads, keep_smem);
     if (e != cudaSuccess) return e;
   }
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, kr, kSolveThreads, 0);
@@ -187,10 +191,14 @@ cudaError_t launch_solve(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *p
   pick->keep = keep;
   void *args[] = {&A};
   void *fn = (void *)kr;
+  size_t smem = 0;
   if constexpr (kKeepOK) {
-    if (keep) fn = (void *)deer_persistent<Sys, MODE, MD, ST, true>;
+    if (keep) {
+      fn = (void *)deer_persistent<Sys, MODE, MD, ST, true>;
+      smem = keep_smem;
+    }
   }
-  return cudaLaunchCooperativeKernel(fn, dim3(A.nblocks), dim3(kSolveThreads), args, 0, st);
+  return cudaLaunchCooperativeKernel(fn, dim3(A.nblocks), dim3(kSolveThreads), args, smem, st);
 }
 
 }  // namespace cs

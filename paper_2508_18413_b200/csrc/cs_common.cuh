@@ -29,7 +29,13 @@ CS_D double logaddexp0(double x) {  // np.logaddexp(0, x)
   return fmax(x, 0.0) + log1p(exp(-fabs(x)));
 }
 CS_D double log_sigmoid(double z) { return -logaddexp0(-z); }            // samplers.py:53-54
-CS_D double sigmoid_prime(double z) { return exp(log_sigmoid(z) + log_sigmoid(-z)); }  // :57-59
+// sigma'(z) = sigma(z) sigma(-z) = e^-|z| / (1 + e^-|z|)^2: the saturation-safe value of
+// samplers.py:57-59 with one exp instead of three transcendental calls
+CS_D double sigmoid_prime(double z) {
+  const double e = exp(-fabs(z));
+  const double q = 1.0 + e;
+  return e / (q * q);
+}
 CS_D double expit(double x) { return 1.0 / (1.0 + exp(-x)); }             // scipy.special.expit
 CS_D double clipv(double x, double c) { return fmin(fmax(x, -c), c); }    // np.clip
 

@@ -93,7 +93,7 @@ CS_D void lookback_col(const LookbackWs &ws, int64_t b, int ncol, int c, int SW,
 
 // ---------------------------------------------------------------------------
 // narrow rows: tile = R consecutive rows x all columns, staged in smem
-template <typename ST, int VAR>
+template <typename ST, int VAR, bool AGG_ONLY = false>
 __global__ void __launch_bounds__(kScanThreads)
 scan_rows(ScanArgs<ST> a, LookbackWs ws, int R) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -176,6 +176,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R) {
   }
   __syncthreads();
   if (threadIdx.x == 0) st_release(ws.status + b, 1);
+  if constexpr (AGG_ONLY) return;
 
   // look-back (first warp; lanes over columns)
   if (threadIdx.x < 32) {
@@ -243,7 +244,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R) {
 // wide rows (D > 64): tile = 64 rows x 32 columns, one column per lane,
 // 8 row segments of 8 rows kept in registers.
 constexpr int kWideSeg = 8;
-template <typename ST, int VAR>
+template <typename ST, int VAR, bool AGG_ONLY = false>
 __global__ void __launch_bounds__(kScanThreads)
 scan_cols(ScanArgs<ST> a, LookbackWs ws) {
   constexpr int W = ColElem<VAR>::W;
@@ -304,6 +305,7 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release(ws.status + tk, 1);
+    if constexpr (AGG_ONLY) return;
     // look-back along the same column block: predecessor ticket tk - ncb
     double x = 0.0, v = 0.0;
     {
@@ -346,6 +348,7 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
     __syncwarp();
     if (lane == 0) st_release(ws.status + tk, 2);
   }
+  if constexpr (AGG_ONLY) return;
   __syncthreads();
   ColElem<VAR> pre;
   pre.load(segagg[s][lane]);
@@ -442,7 +445,7 @@ CS_D void load_dense_elem(const ScanArgs<ST> &a, int64_t t, DenseElem<MD> &e) {
   }
 }
 
-template <typename ST, int MD, int SEG>
+template <typename ST, int MD, int SEG, bool AGG_ONLY = false>
 __global__ void __launch_bounds__(kScanThreads)
 scan_dense_small(ScanArgs<ST> a, LookbackWs ws) {
   __shared__ int64_t s_tile;
@@ -496,6 +499,18 @@ scan_dense_small(ScanArgs<ST> a, LookbackWs ws) {
     }
     __threadfence();
     st_release(ws.status + b, 1);
+  }
+  if constexpr (AGG_ONLY) return;
+  if (threadIdx.x == 0) {
+    // the tile total, as just published by this thread
+    DenseElem<MD> tot;
+    const double *g = ws.agg + b * (MD * MD + MD);
+#pragma unroll
+    for (int r = 0; r < MD; ++r) {
+      tot.w[r] = g[MD * MD + r];
+#pragma unroll
+      for (int k = 0; k < MD; ++k) tot.M[r][k] = g[r * MD + k];
+    }
     // look-back
     DenseElem<MD> acc;
     acc.ident(D);
@@ -554,6 +569,72 @@ scan_dense_small(ScanArgs<ST> a, LookbackWs ws) {
 #pragma unroll
     for (int r = 0; r < MD; ++r)
       if (r < D) a.out[t * D + r] = (ST)x[r];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// whole-sequence aggregate (the composed affine map of all T elements), used
+// by the T-sharded driver to exchange one carry per shard: tile aggregates
+// from the AGG_ONLY scans, then an ordered fold here.  Output layout (f64):
+//   diag  [j(D) | u(D)]   block [A|B|C|E|ux|uv] each (D)   dense [M (DxD) | w(D)]
+template <int VAR>
+__global__ void __launch_bounds__(kScanThreads)
+k_agg_compose_cols(const double *agg, int64_t nrt, int ncol, int ncb, double *out) {
+  constexpr int W = ColElem<VAR>::W;
+  __shared__ double part[kScanThreads][W];
+  const int per_pass = ncol < kScanThreads ? ncol : kScanThreads;
+  for (int c0 = 0; c0 < ncol; c0 += per_pass) {
+    const int nc = min(per_pass, ncol - c0);
+    const int nparts = kScanThreads / nc;
+    const int t = threadIdx.x, c = c0 + t % nc, p = t / nc;
+    if (p < nparts) {
+      ColElem<VAR> run;
+      run.ident();
+      const int64_t per = (nrt + nparts - 1) / nparts;
+      const int64_t lo = p * per, hi = lo + per < nrt ? lo + per : nrt;
+      for (int64_t r = lo; r < hi; ++r) {
+        const int64_t idx = ncb ? ((r * ncb + c / 32) * 32 + (c % 32)) : (r * ncol + c);
+        ColElem<VAR> e;
+        e.load(agg + idx * W);
+        run.push(e);
+      }
+      run.store(part[t]);
+    }
+    __syncthreads();
+    if (t < nc) {
+      ColElem<VAR> tot;
+      tot.ident();
+      for (int q = 0; q < nparts; ++q) {
+        ColElem<VAR> e;
+        e.load(part[q * nc + t]);
+        tot.push(e);
+      }
+      double v[W];
+      tot.store(v);
+#pragma unroll
+      for (int k = 0; k < W; ++k) out[k * ncol + c0 + t] = v[k];
+    }
+    __syncthreads();
+  }
+}
+
+template <int MD>
+__global__ void k_agg_compose_dense(const double *agg, int64_t ntiles, int D, double *out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  DenseElem<MD> tot;
+  tot.ident(D);
+  for (int64_t q = 0; q < ntiles; ++q) {
+    DenseElem<MD> e;
+    const double *g = agg + q * (MD * MD + MD);
+    for (int r = 0; r < MD; ++r) {
+      e.w[r] = g[MD * MD + r];
+      for (int k = 0; k < MD; ++k) e.M[r][k] = g[r * MD + k];
+    }
+    tot.push(e);
+  }
+  for (int r = 0; r < D; ++r) {
+    out[D * D + r] = tot.w[r];
+    for (int k = 0; k < D; ++k) out[r * D + k] = tot.M[r][k];
   }
 }
 
@@ -649,7 +730,49 @@ cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStrea
   return cudaGetLastError();
 }
 
+template <typename ST>
+cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, double *out, cudaStream_t st) {
+  LookbackWs w = carve_ws(p, ws, a.D);
+  cudaError_t e = cudaMemsetAsync(ws, 0, (unsigned char *)w.agg - (unsigned char *)ws, st);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)p.ntiles;
+  if (p.kind == 0) {
+    if (p.var == SCAN_DIAG) {
+      cudaFuncSetAttribute(scan_rows<ST, SCAN_DIAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      scan_rows<ST, SCAN_DIAG, true><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R);
+      k_agg_compose_cols<SCAN_DIAG><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
+    } else {
+      cudaFuncSetAttribute(scan_rows<ST, SCAN_BLOCK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      scan_rows<ST, SCAN_BLOCK, true><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R);
+      k_agg_compose_cols<SCAN_BLOCK><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
+    }
+  } else if (p.kind == 1) {
+    const int ncb = (a.D + 31) / 32;
+    if (p.var == SCAN_DIAG) {
+      scan_cols<ST, SCAN_DIAG, true><<<grid, kScanThreads, 0, st>>>(a, w);
+      k_agg_compose_cols<SCAN_DIAG><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles / ncb, a.D, ncb, out);
+    } else {
+      scan_cols<ST, SCAN_BLOCK, true><<<grid, kScanThreads, 0, st>>>(a, w);
+      k_agg_compose_cols<SCAN_BLOCK><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles / ncb, a.D, ncb, out);
+    }
+  } else {
+    switch (p.md) {
+      case 1: scan_dense_small<ST, 1, 4, true><<<grid, kScanThreads, 0, st>>>(a, w);
+              k_agg_compose_dense<1><<<1, 32, 0, st>>>(w.agg, p.ntiles, a.D, out); break;
+      case 2: scan_dense_small<ST, 2, 4, true><<<grid, kScanThreads, 0, st>>>(a, w);
+              k_agg_compose_dense<2><<<1, 32, 0, st>>>(w.agg, p.ntiles, a.D, out); break;
+      case 4: scan_dense_small<ST, 4, 1, true><<<grid, kScanThreads, 0, st>>>(a, w);
+              k_agg_compose_dense<4><<<1, 32, 0, st>>>(w.agg, p.ntiles, a.D, out); break;
+      default: scan_dense_small<ST, 8, 1, true><<<grid, kScanThreads, 0, st>>>(a, w);
+               k_agg_compose_dense<8><<<1, 32, 0, st>>>(w.agg, p.ntiles, a.D, out); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
 template cudaError_t launch_scan_t<float>(const ScanPlan &, ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_aggregate_t<float>(const ScanPlan &, ScanArgs<float>, void *, double *, cudaStream_t);
+template cudaError_t launch_aggregate_t<double>(const ScanPlan &, ScanArgs<double>, void *, double *, cudaStream_t);
 template cudaError_t launch_scan_t<double>(const ScanPlan &, ScanArgs<double>, void *, cudaStream_t);
 
 }  // namespace cs

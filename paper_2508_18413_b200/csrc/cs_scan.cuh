@@ -25,5 +25,7 @@ struct ScanPlan {
 ScanPlan scan_plan(int var, int dtype, int64_t T, int D);
 template <typename ST>
 cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st);
+template <typename ST>
+cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, double *out, cudaStream_t st);
 
 }  // namespace cs

@@ -98,26 +98,22 @@ CS_D void build_elem(const Sys &sys, const typename Sys::Aux &aux, const double 
                      Elem<MODE, MD> &e, bool &jac_ok) {
   jac_ok = true;
   if constexpr (MODE == CS_MODE_DIAG) {
+    // Hutchinson: one probe at a time (deer.py:128-131), probes hashed on device
     double est[MD];
 #pragma unroll
     for (int i = 0; i < MD; ++i) est[i] = 0.0;
     const uint64_t h3 = hash_t(probe_prefix(A.sys.seed, it), (uint64_t)t);
-    for (int k0 = 0; k0 < A.nsamp; k0 += kTanMax) {
-      const int nk = min(kTanMax, A.nsamp - k0);
-      double V[kTanMax][MD], O[kTanMax][MD];
+#pragma unroll 1
+    for (int k = 0; k < A.nsamp; ++k) {
+      double V[1][MD], O[1][MD];
 #pragma unroll
-      for (int kk = 0; kk < kTanMax; ++kk)
+      for (int i = 0; i < MD; ++i) {
+        const int m = sys.mem_index(i);
+        V[0][i] = m >= 0 ? probe_sign(h3, k, m) : 0.0;
+      }
+      sys.template jvp_many<1>(aux, V, O, 1, false);
 #pragma unroll
-        for (int i = 0; i < MD; ++i) {
-          const int m = sys.mem_index(i);
-          V[kk][i] = (kk < nk && m >= 0) ? probe_sign(h3, k0 + kk, m) : 0.0;
-        }
-      sys.template jvp_many<kTanMax>(aux, V, O, nk, false);
-#pragma unroll
-      for (int kk = 0; kk < kTanMax; ++kk)
-        if (kk < nk)
-#pragma unroll
-          for (int i = 0; i < MD; ++i) est[i] += V[kk][i] * O[kk][i];
+      for (int i = 0; i < MD; ++i) est[i] += V[0][i] * O[0][i];
     }
 #pragma unroll
     for (int i = 0; i < MD; ++i) {
@@ -132,27 +128,16 @@ CS_D void build_elem(const Sys &sys, const typename Sys::Aux &aux, const double 
       e.u(i) = f[i] - d * prev[i];
     }
   } else if constexpr (MODE == CS_MODE_DENSE) {
+    // D unit tangents in one pass (core.py:125-134: column d = J e_d)
+    double V[MD][MD], O[MD][MD];
+    int nk = 0;
 #pragma unroll
-    for (int c0 = 0; c0 < MD; c0 += kTanMax) {
-      double V[kTanMax][MD], O[kTanMax][MD];
-      int nk = 0;
+    for (int c = 0; c < MD; ++c) {
+      if (sys.mem_index(c) >= 0) nk = c + 1;
 #pragma unroll
-      for (int kk = 0; kk < kTanMax; ++kk) {
-        const int c = c0 + kk;
-        if (c < MD && sys.mem_index(c) >= 0) nk = kk + 1;
-#pragma unroll
-        for (int i = 0; i < MD; ++i) V[kk][i] = (c < MD && i == c && sys.mem_index(c) >= 0) ? 1.0 : 0.0;
-      }
-      if (nk > 0) sys.template jvp_many<kTanMax>(aux, V, O, nk, false);
-#pragma unroll
-      for (int kk = 0; kk < kTanMax; ++kk) {
-        const int c = c0 + kk;
-        if (c >= MD) continue;
-        const bool vc = sys.mem_index(c) >= 0;
-#pragma unroll
-        for (int a = 0; a < MD; ++a) e.M(a, c) = (vc && kk < nk) ? O[kk][a] : 0.0;
-      }
+      for (int i = 0; i < MD; ++i) V[c][i] = (i == c && sys.mem_index(c) >= 0) ? 1.0 : 0.0;
     }
+    sys.template jvp_many<MD>(aux, V, O, nk, false);
 #pragma unroll
     for (int a = 0; a < MD; ++a) {
       const int ma = sys.mem_index(a);
@@ -160,7 +145,7 @@ CS_D void build_elem(const Sys &sys, const typename Sys::Aux &aux, const double 
 #pragma unroll
       for (int c = 0; c < MD; ++c) {
         const int mc = sys.mem_index(c);
-        double J = e.M(a, c);
+        double J = O[c][a];
         if (ma >= 0 && mc >= 0) {
           jac_ok &= finite(J);
           if (A.pre) J = J * (__ldg(A.pre + mc) / __ldg(A.pre + ma));
@@ -268,6 +253,9 @@ template <class Sys, int MODE, int MD, typename ST, bool KEEP>
 __global__ void __launch_bounds__(kSolveThreads)
 deer_persistent(SolveArgs<ST> A) {
   using E = Elem<MODE, MD>;
+  // KEEP: the segment's elements wait in shared memory across the grid sync,
+  // laid out [k][w][thread] so every access is bank-conflict free
+  extern __shared__ double s_keep[];
   __shared__ E s_warp[kSolveThreads / 32 + 1];
   __shared__ long long s_min[3];
   __shared__ unsigned s_cnt[2];
@@ -289,7 +277,6 @@ deer_persistent(SolveArgs<ST> A) {
   int status = CS_RUN_MAXITERS, err_kind = CS_DIV_NONE, err_iter = -1, stop = CS_STOP_MAXITERS;
   long long err_step = -1;
   double g_dmax = 0.0;
-  E keep[KEEP ? kSegKeep : 1];
 
   for (;;) {
     SolveSlot *S = &A.ctl->slot[it & 1];
@@ -315,11 +302,10 @@ deer_persistent(SolveArgs<ST> A) {
     } else {
       load_row<Sys, MD, ST>(sys, Gc + (row0 - 1) * D, prev);
     }
-    constexpr int KB = KEEP ? kSegKeep : (1 << 30);
-#pragma unroll
-    for (int k = 0; k < KB; ++k) {
+#pragma unroll 1
+    for (int k = 0; k < A.seg; ++k) {
       const int64_t r = row0 + k;
-      if (k >= A.seg || r >= A.T) break;
+      if (r >= A.T) break;
       const int64_t t = r + 1;
       double gr[MD];
       if (it == 0) {
@@ -347,7 +333,10 @@ deer_persistent(SolveArgs<ST> A) {
         build_elem<Sys, MODE, MD, ST>(sys, aux, prev, f, t, it, A, e, jok);
         if (!jok) bj = min(bj, (long long)t);
         agg.after(e);
-        if constexpr (KEEP) keep[k] = e;
+        if constexpr (KEEP) {
+#pragma unroll
+          for (int w = 0; w < E::W; ++w) s_keep[(k * E::W + w) * kSolveThreads + threadIdx.x] = e.v[w];
+        }
       }
 #pragma unroll
       for (int i = 0; i < MD; ++i) prev[i] = gr[i];
@@ -426,10 +415,10 @@ deer_persistent(SolveArgs<ST> A) {
           load_row<Sys, MD, ST>(sys, Gc + (row0 - 1) * D, pv);
         }
       }
-#pragma unroll
-      for (int k = 0; k < KB; ++k) {
+#pragma unroll 1
+      for (int k = 0; k < A.seg; ++k) {
         const int64_t r = row0 + k;
-        if (k >= A.seg || r >= A.T) break;
+        if (r >= A.T) break;
         double gr[MD];
         if (it == 0) {
 #pragma unroll
@@ -439,7 +428,8 @@ deer_persistent(SolveArgs<ST> A) {
         }
         E e;
         if constexpr (KEEP) {
-          e = keep[k];
+#pragma unroll
+          for (int w = 0; w < E::W; ++w) e.v[w] = s_keep[(k * E::W + w) * kSolveThreads + threadIdx.x];
         } else {
           const int64_t t = r + 1;
           typename Sys::Aux aux;

@@ -19,7 +19,7 @@ namespace cs {
 template <int MD, typename ST, int TK = -1>
 struct Mala {
   Target<MD, TK> tg;
-  double eps, sq2eps;
+  double eps, sq2eps, inv4eps, inv2eps;
   const ST *xi;
   const double *logu;
 
@@ -52,7 +52,7 @@ struct Mala {
       a.back[i] = (i < D) ? (s[i] - a.prop[i]) - eps * a.g1[i] : 0.0;
       rr += a.back[i] * a.back[i];
     }
-    a.delta = ((tg.logp(a.prop) - tg.logp(s)) - rr / (4.0 * eps)) + 0.5 * xx;
+    a.delta = ((tg.logp(a.prop) - tg.logp(s)) - rr * inv4eps) + 0.5 * xx;
     a.margin = fmin(0.0, a.delta) - __ldg(logu + t);
     return ok;
   }
@@ -83,7 +83,7 @@ struct Mala {
       s2 += a.g0[i] * V[i];
       s3 += a.back[i] * dback;
     }
-    const double ddelta = (s1 - s2) - s3 / (2.0 * eps);
+    const double ddelta = (s1 - s2) - s3 * inv2eps;
     const double gate = relaxed ? expit(a.margin) : (a.margin > 0.0 ? 1.0 : 0.0);
     const double bend = sigmoid_prime(a.margin) * (ddelta * (a.delta < 0.0 ? 1.0 : 0.0));
 #pragma unroll
@@ -119,6 +119,7 @@ struct Hmc {
   CS_D int dim() const { return tg.p.dim; }
   CS_D int mem_index(int k) const { return k < tg.p.dim ? k : -1; }
   CS_D double m(int i) const { return (mass && i < tg.p.dim) ? __ldg(mass + i) : 1.0; }
+  CS_D double divm(double x, int i) const { return (mass && i < tg.p.dim) ? x / __ldg(mass + i) : x; }
 
   CS_D bool prepare(int64_t t, const double (&s)[MD], Aux &a) const {
     const int D = dim();
@@ -137,7 +138,7 @@ struct Hmc {
     const double h0 = 0.5 * xx - tg.logp(s);
     for (int l = 0; l < L; ++l) {
 #pragma unroll
-      for (int i = 0; i < MD; ++i) x[i] = x[i] + (eps * v[i]) / m(i);
+      for (int i = 0; i < MD; ++i) x[i] = x[i] + divm(eps * v[i], i);
       tg.grad(x, g);
 #pragma unroll
       for (int i = 0; i < MD; ++i) v[i] = v[i] + eps * g[i];
@@ -151,7 +152,7 @@ struct Hmc {
     for (int i = 0; i < MD; ++i) {
       a.xl[i] = x[i];
       a.vl[i] = v[i] - (0.5 * eps) * a.gl[i];
-      if (i < D) kin += (a.vl[i] * a.vl[i]) / m(i);
+      if (i < D) kin += divm(a.vl[i] * a.vl[i], i);
     }
     const double hl = 0.5 * kin - tg.logp(x);
     a.delta = h0 - hl;
@@ -195,12 +196,12 @@ struct Hmc {
     for (int i = 0; i < MD; ++i) { x[i] = a.S[i]; v[i] = a.vh0[i]; }
     for (int l = 0; l < L; ++l) {
 #pragma unroll
-      for (int i = 0; i < MD; ++i) x[i] = x[i] + (eps * v[i]) / m(i);
+      for (int i = 0; i < MD; ++i) x[i] = x[i] + divm(eps * v[i], i);
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
         if (k >= n) continue;
 #pragma unroll
-        for (int i = 0; i < MD; ++i) dx[k][i] = dx[k][i] + (eps * dv[k][i]) / m(i);
+        for (int i = 0; i < MD; ++i) dx[k][i] = dx[k][i] + divm(eps * dv[k][i], i);
         tg.hvp(x, dx[k], h);
 #pragma unroll
         for (int i = 0; i < MD; ++i) dv[k][i] = dv[k][i] + eps * h[i];
@@ -220,7 +221,7 @@ struct Hmc {
 #pragma unroll
       for (int i = 0; i < MD; ++i) {
         double dvl = dv[k][i] - (0.5 * eps) * h[i];
-        if (i < D) s1 += (a.vl[i] * dvl) / m(i);
+        if (i < D) s1 += divm(a.vl[i] * dvl, i);
         s2 += a.gl[i] * dx[k][i];
       }
       const double ddelta = dh0[k] - (s1 - s2);
@@ -254,6 +255,7 @@ struct Leapfrog {
     return k < H ? (k < n ? k : -1) : (k - H < n ? n + k - H : -1);
   }
   CS_D double m(int i) const { return (mass && i < tg.p.dim) ? __ldg(mass + i) : 1.0; }
+  CS_D double divm(double x, int i) const { return (mass && i < tg.p.dim) ? x / __ldg(mass + i) : x; }
 
   CS_D bool prepare(int64_t, const double (&s)[MD], Aux &a) const {
     const int n = tg.p.dim;
@@ -261,7 +263,7 @@ struct Leapfrog {
 #pragma unroll
     for (int i = 0; i < MD; ++i) a.S[i] = s[i];
 #pragma unroll
-    for (int i = 0; i < H; ++i) a.xn[i] = (i < n) ? s[i] + (eps * s[H + i]) / m(i) : 0.0;
+    for (int i = 0; i < H; ++i) a.xn[i] = (i < n) ? s[i] + divm(eps * s[H + i], i) : 0.0;
     tg.grad(a.xn, g);
 #pragma unroll
     for (int i = 0; i < H; ++i) a.vn[i] = (i < n) ? s[H + i] + eps * g[i] : 0.0;
@@ -278,7 +280,7 @@ struct Leapfrog {
     const int n = tg.p.dim;
     double dxn[H], h[H];
 #pragma unroll
-    for (int i = 0; i < H; ++i) dxn[i] = (i < n) ? V[i] + (eps * V[H + i]) / m(i) : 0.0;
+    for (int i = 0; i < H; ++i) dxn[i] = (i < n) ? V[i] + divm(eps * V[H + i], i) : 0.0;
     tg.hvp(a.xn, dxn, h);
 #pragma unroll
     for (int i = 0; i < H; ++i) {
@@ -314,9 +316,9 @@ struct Leapfrog {
     for (int i = 0; i < H; ++i) {
       dhat[i] = dhat[i] / (double)nsamp;
       ba[i] = (i < n) ? 1.0 : 0.0;
-      bb[i] = (i < n) ? eps / m(i) : 0.0;
+      bb[i] = (i < n) ? divm(eps, i) : 0.0;
       bc[i] = eps * dhat[i];
-      bd[i] = (i < n) ? 1.0 + ((eps * eps) * dhat[i]) / m(i) : 0.0;
+      bd[i] = (i < n) ? 1.0 + divm((eps * eps) * dhat[i], i) : 0.0;
     }
   }
 };
@@ -430,6 +432,9 @@ template <int MD, typename ST, int TK> CS_D Mala<MD, ST, TK> make_mala(const cs_
   m.tg.p = s.target;
   m.eps = s.eps;
   m.sq2eps = sqrt(2.0 * s.eps);
+  m.inv4eps = 1.0 / (4.0 * s.eps);
+  m.inv2eps = 1.0 / (2.0 * s.eps);
+  m.tg.init();
   m.xi = (const ST *)s.noise_vec;
   m.logu = s.noise_logu;
   return m;
@@ -437,6 +442,7 @@ template <int MD, typename ST, int TK> CS_D Mala<MD, ST, TK> make_mala(const cs_
 template <int MD, typename ST, int TK> CS_D Hmc<MD, ST, TK> make_hmc(const cs_system &s) {
   Hmc<MD, ST, TK> h;
   h.tg.p = s.target;
+  h.tg.init();
   h.eps = s.eps;
   h.L = s.L;
   h.mass = s.mass;
@@ -447,6 +453,7 @@ template <int MD, typename ST, int TK> CS_D Hmc<MD, ST, TK> make_hmc(const cs_sy
 template <int MD, typename ST, int TK> CS_D Leapfrog<MD, ST, TK> make_leapfrog(const cs_system &s) {
   Leapfrog<MD, ST, TK> l;
   l.tg.p = s.target;
+  l.tg.init();
   l.eps = s.eps;
   l.mass = s.mass;
   l.probe_seed = s.probe_seed;

@@ -15,6 +15,12 @@ namespace cs {
 template <int MD, int TK = -1>
 struct Target {
   cs_target p;
+  double is1, is2;  // 1/scale1, 1/scale2 (rosenbrock), hoisted out of the hot loops
+
+  CS_D void init() {
+    is1 = 1.0 / p.scale1;
+    is2 = 1.0 / p.scale2;
+  }
 
   CS_D int dim() const { return p.dim; }
   CS_D int kind() const { return TK >= 0 ? TK : p.kind; }
@@ -45,7 +51,7 @@ struct Target {
         double x1 = x[0], x2 = x[MD > 1 ? 1 : 0];
         double r = x2 - p.b * x1 * x1;
         double q = x1 - p.a;
-        return -(q * q) / (2.0 * p.scale1) - r * r / (2.0 * p.scale2);
+        return -(q * q) * (0.5 * is1) - (r * r) * (0.5 * is2);
       }
       default: {  // mog: log-sum-exp over components (no per-component arrays)
         double top = -INFINITY;
@@ -98,8 +104,8 @@ struct Target {
       case CS_TARGET_ROSENBROCK: {
         double x1 = x[0], x2 = x[MD > 1 ? 1 : 0];
         double r = x2 - p.b * x1 * x1;
-        g[0] = -(x1 - p.a) / p.scale1 + 2.0 * p.b * x1 * r / p.scale2;
-        if (MD > 1) g[MD > 1 ? 1 : 0] = -r / p.scale2;
+        g[0] = -(x1 - p.a) * is1 + 2.0 * p.b * x1 * r * is2;
+        if (MD > 1) g[MD > 1 ? 1 : 0] = -r * is2;
 #pragma unroll
         for (int i = 2; i < MD; ++i) g[i] = 0.0;
         return;
@@ -141,14 +147,14 @@ struct Target {
         }
         return;
       case CS_TARGET_ROSENBROCK: {
-        const double b = p.b, s1 = p.scale1, s2 = p.scale2;
+        const double b = p.b;
         double x1 = x[0], x2 = x[MD > 1 ? 1 : 0];
         double r = x2 - b * x1 * x1;
-        double h11 = -1.0 / s1 + (2.0 * b * r - 4.0 * b * b * x1 * x1) / s2;
-        double h12 = 2.0 * b * x1 / s2;
+        double h11 = -is1 + (2.0 * b * r - 4.0 * b * b * x1 * x1) * is2;
+        double h12 = 2.0 * b * x1 * is2;
         double v0 = v[0], v1 = v[MD > 1 ? 1 : 0];
         o[0] = h11 * v0 + h12 * v1;
-        if (MD > 1) o[MD > 1 ? 1 : 0] = h12 * v0 - v1 / s2;
+        if (MD > 1) o[MD > 1 ? 1 : 0] = h12 * v0 - v1 * is2;
 #pragma unroll
         for (int i = 2; i < MD; ++i) o[i] = 0.0;
         return;

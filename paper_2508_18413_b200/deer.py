@@ -167,51 +167,73 @@ def _pre_tensor(cfg, device):
     return torch.as_tensor(cfg.preconditioner, dtype=torch.float64, device=device)
 
 
-def _iterate_range(system, ts, guess, s0_local, cfg, iteration, f=None):
-    """One Newton update on the steps ts seeded from s0_local (deer.py:147-208)."""
+def _build_elements(system, ts, guess, s0_local, cfg, iteration, f, on_bad=None):
+    """Jacobian estimate -> affine elements with preconditioner, damping and clip
+    in the reference's order, u = f - Jhat prev (deer.py:157-204).
+
+    A non-finite Jacobian raises ChainDivergedError, or, with ``on_bad`` given,
+    is reported as on_bad(step) so a sharded caller can agree on it first.
+    """
     lib = _lib.load()
     dt = _lib.dtype_code(guess.dtype)
     st = _lib.stream_ptr()
-    guess = guess.contiguous()
-    s0_local = s0_local.contiguous()
     prev = torch.cat([s0_local[None], guess[:-1]], dim=0)
-    if f is None:
-        f = system.step_batch(ts, prev)
-        _check_finite(f, "step value", ts, iteration)
     f = f.to(guess.dtype).contiguous()
     T, W = guess.shape
     pre = _pre_tensor(cfg, guess.device)
     clip = float(cfg.clip)
+
+    def finite_or(arr, what):
+        row = _first_nonfinite(arr)
+        if row == _NO_STEP:
+            return
+        t = int(ts[row])
+        if on_bad is not None:
+            on_bad(t)
+            return
+        raise ChainDivergedError(f"non-finite {what} at step {t} (iteration {iteration + 1})",
+                                 step=t, iteration=iteration + 1)
+
     if cfg.mode == "dense":
         Jin = torch.as_tensor(system.dense_jacobian_batch(ts, prev), dtype=guess.dtype).contiguous()
-        _check_finite(Jin, "jacobian", ts, iteration)
+        finite_or(Jin, "jacobian")
         J = torch.empty_like(Jin)
         u = torch.empty_like(f)
         rc = lib.cs_form_dense(dt, _lib.ptr(Jin), _lib.ptr(f), _lib.ptr(s0_local), _lib.ptr(guess), T, W,
                                _lib.ptr(pre), float(cfg.damping), clip, _lib.ptr(J), _lib.ptr(u), st)
         _lib.check(rc)
-        elements = DenseElements(J, u)
-    elif cfg.mode == "diag-stochastic":
+        return DenseElements(J, u)
+    if cfg.mode == "diag-stochastic":
         d = hutchinson_diag(system.jvp_batch, ts, prev, cfg.hutchinson_samples, system.noise.seed, iteration)
-        _check_finite(d, "jacobian diagonal", ts, iteration)
+        finite_or(d, "jacobian diagonal")
         j = torch.empty_like(d)
         u = torch.empty_like(f)
         rc = lib.cs_form_diag(dt, _lib.ptr(d.contiguous()), _lib.ptr(f), _lib.ptr(s0_local), _lib.ptr(guess), T,
                               W, _lib.ptr(pre), float(cfg.damping), clip, _lib.ptr(j), _lib.ptr(u), st)
         _lib.check(rc)
-        elements = DiagElements(j, u)
-    else:
-        a, b, c, dd = (torch.as_tensor(x, dtype=guess.dtype).contiguous() for x in
-                       system.block_jacobian_batch(ts, prev, cfg.hutchinson_samples, iteration))
-        _check_finite(torch.cat([a, b, c, dd], dim=-1), "block jacobian", ts, iteration)
-        half = a.shape[-1]
-        outs = [torch.empty_like(a) for _ in range(4)]
-        u = torch.empty_like(f)
-        rc = lib.cs_form_block(dt, _lib.ptr(a), _lib.ptr(b), _lib.ptr(c), _lib.ptr(dd), _lib.ptr(f),
-                               _lib.ptr(s0_local), _lib.ptr(guess), T, half, _lib.ptr(pre), float(cfg.damping), clip,
-                               *[_lib.ptr(o) for o in outs], _lib.ptr(u), st)
-        _lib.check(rc)
-        elements = Block2x2Elements(*outs, u)
+        return DiagElements(j, u)
+    a, b, c, dd = (torch.as_tensor(x, dtype=guess.dtype).contiguous() for x in
+                   system.block_jacobian_batch(ts, prev, cfg.hutchinson_samples, iteration))
+    finite_or(torch.cat([a, b, c, dd], dim=-1), "block jacobian")
+    half = a.shape[-1]
+    outs = [torch.empty_like(a) for _ in range(4)]
+    u = torch.empty_like(f)
+    rc = lib.cs_form_block(dt, _lib.ptr(a), _lib.ptr(b), _lib.ptr(c), _lib.ptr(dd), _lib.ptr(f),
+                           _lib.ptr(s0_local), _lib.ptr(guess), T, half, _lib.ptr(pre), float(cfg.damping), clip,
+                           *[_lib.ptr(o) for o in outs], _lib.ptr(u), st)
+    _lib.check(rc)
+    return Block2x2Elements(*outs, u)
+
+
+def _iterate_range(system, ts, guess, s0_local, cfg, iteration, f=None):
+    """One Newton update on the steps ts seeded from s0_local (deer.py:147-208)."""
+    guess = guess.contiguous()
+    s0_local = s0_local.contiguous()
+    if f is None:
+        prev = torch.cat([s0_local[None], guess[:-1]], dim=0)
+        f = system.step_batch(ts, prev)
+        _check_finite(f, "step value", ts, iteration)
+    elements = _build_elements(system, ts, guess, s0_local, cfg, iteration, f)
     return parallel_affine_solve(elements, s0_local)
 
 

@@ -73,6 +73,13 @@ def _tensor(x, like=None):
     return torch.as_tensor(x, dtype=dt, device=dev)
 
 
+def _unify(*ts):
+    """Common floating dtype (f64 wins, like the reference's np.asarray(float))."""
+    dt = torch.float64 if any(t.dtype == torch.float64 for t in ts) else torch.float32
+    dev = ts[0].device
+    return [t.to(device=dev, dtype=dt) for t in ts]
+
+
 def _same(a, b, what):
     if tuple(a.shape) != tuple(b.shape):
         raise StructuralError(f"{what}: shapes {tuple(a.shape)} and {tuple(b.shape)} differ")
@@ -84,8 +91,7 @@ class DiagElements:
     u: torch.Tensor
 
     def __post_init__(self):
-        self.j = _tensor(self.j)
-        self.u = _tensor(self.u, self.j)
+        self.j, self.u = _unify(_tensor(self.j), _tensor(self.u))
         _same(self.j, self.u, "Diag j/u")
 
     @property
@@ -102,8 +108,7 @@ class DenseElements:
     u: torch.Tensor
 
     def __post_init__(self):
-        self.J = _tensor(self.J)
-        self.u = _tensor(self.u, self.J)
+        self.J, self.u = _unify(_tensor(self.J), _tensor(self.u))
         if self.J.shape[-1] != self.J.shape[-2]:
             raise StructuralError(f"Dense J must be square, got {tuple(self.J.shape)}")
         _same(self.J[..., 0], self.u, "Dense J/u")
@@ -125,9 +130,8 @@ class Block2x2Elements:
     u: torch.Tensor
 
     def __post_init__(self):
-        self.a = _tensor(self.a)
-        for name in ("b", "c", "d", "u"):
-            setattr(self, name, _tensor(getattr(self, name), self.a))
+        self.a, self.b, self.c, self.d, self.u = _unify(
+            *(_tensor(getattr(self, n)) for n in ("a", "b", "c", "d", "u")))
         for name in ("b", "c", "d"):
             _same(self.a, getattr(self, name), f"Block2x2 a/{name}")
         want = tuple(self.a.shape[:-1]) + (2 * self.a.shape[-1],)

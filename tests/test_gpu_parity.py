@@ -266,7 +266,7 @@ def test_run_deer_gibbs(cuda_device, dtype):
     g = golden("gibbs_schools")
     k = cs.GibbsKernel(cs.generate_eight_schools(), seed=0, T=3000, dtype=dtype)
     s0 = k.initial_state()
-    np.testing.assert_allclose(np_(s0), g["s0"], rtol=1e-10)
+    np.testing.assert_allclose(np_(s0), g["s0"], rtol=1e-10 if dtype == torch.float64 else 1e-6)
     cfg = cs.DeerConfig(mode="diag-stochastic", hutchinson_samples=3, preconditioner=k.recommended_preconditioner(),
                         max_iters=400)
     r = cs.run_deer(k, g["s0"], cfg)
