@@ -184,6 +184,10 @@ int cs_hutchinson_accumulate(int dtype, void *est, const void *z, const void *jz
                              int32_t first, double final_div, void *stream);
 
 /* ---- fused transition systems (samplers.py) ----------------------------- */
+/* 1 if the register-resident fused kernels below cover this system (small
+ * state dimension, non-GEMM target), else 0 (the host layer then evaluates
+ * the system with cuBLAS GEMMs, e.g. logistic regression, D = 1000 Gaussians). */
+int cs_system_supported(const cs_system *sys, int dtype);
 /* f_t for rows ts[i] (or t0+i) at states S (n, dim) -> out (n, dim).
  * *bad_step receives the first step whose proposal / trajectory was
  * non-finite (samplers.py:101-105, 332-336) or -1. */

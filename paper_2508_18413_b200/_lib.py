@@ -79,6 +79,7 @@ _SIGS = {
     "cs_form_block": ([ctypes.c_int, P, P, P, P, P, P, P, i64, i32, P, f64, f64, P, P, P, P, P, P],
                       ctypes.c_int),
     "cs_hutchinson_accumulate": ([ctypes.c_int, P, P, P, i64, i32, f64, P], ctypes.c_int),
+    "cs_system_supported": ([SP, ctypes.c_int], ctypes.c_int),
     "cs_system_step": ([SP, ctypes.c_int, P, i64, i64, P, P, P, P], ctypes.c_int),
     "cs_system_jvp": ([SP, ctypes.c_int, P, i64, i64, P, P, P, i32, P], ctypes.c_int),
     "cs_system_relaxed_step": ([SP, ctypes.c_int, P, i64, i64, P, P, P], ctypes.c_int),

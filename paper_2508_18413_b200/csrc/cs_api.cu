@@ -477,6 +477,13 @@ static int check_sys(const cs_system *sys, int dtype, int *md_out) {
   return CS_OK;
 }
 
+int cs_system_supported(const cs_system *sys, int dtype) {
+  if (!sys || !dtype_ok(dtype)) return 0;
+  if (sys->kind == CS_SYS_GIBBS) return sys->dim == 18 ? 1 : 0;
+  if (sys->target.kind == CS_TARGET_BLR) return 0;
+  return api_md(sys->kind, sys->target.kind, sys->dim) ? 1 : 0;
+}
+
 static int syscall(const cs_system *sys, int dtype, SysCall c, void *stream, const char *what) {
   int md = 0;
   int rc = check_sys(sys, dtype, &md);

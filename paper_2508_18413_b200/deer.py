@@ -268,7 +268,7 @@ def _fused_ok(system, cfg):
         return False
     if cfg.window_len is not None and cfg.window_len < system.T:
         return False
-    if getattr(system, "_blr", False) or getattr(system, "leapfrog_mode", "sequential") == "parallel":
+    if getattr(system, "leapfrog_mode", "sequential") == "parallel":
         return False
     d = desc_fn()
     return bool(_lib.load().cs_deer_supported(ctypes.byref(d), _MODE_CODE[cfg.mode],

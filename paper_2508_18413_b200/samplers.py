@@ -93,19 +93,42 @@ class _Fused(TransitionSystem):
         _lib.check(rc)
         return out
 
+    # register-resident CUDA kernels when the C-ABI covers the system, else the
+    # GEMM (cuBLAS) evaluation of the same arithmetic in _torch_* below
+    @property
+    def kernels(self) -> bool:
+        if getattr(self, "_kernels", None) is None:
+            d = self.desc()
+            self._kernels = bool(_lib.load().cs_system_supported(ctypes.byref(d), _lib.dtype_code(self.dtype)))
+        return self._kernels
+
     def _step_batch(self, ts, S):
-        return self._call_step(ts, S)
+        if self.kernels:
+            return self._call_step(ts, S)
+        return self._torch_step(ts, S, relaxed=False).to(self.dtype)
 
     def _jvp_batch(self, ts, S, V):
-        return self._call_jvp(ts, S, V)
+        if self.kernels:
+            return self._call_jvp(ts, S, V)
+        return self._torch_jvp(ts, S, V, relaxed=False).to(self.dtype)
 
     def relaxed_step_batch(self, ts, S):
-        return self._call_step(as_steps(ts, self.device), self._state(S), relaxed=True)
+        ts, S = as_steps(ts, self.device), self._state(S)
+        if self.kernels:
+            return self._call_step(ts, S, relaxed=True)
+        return self._torch_step(ts, S, relaxed=True).to(self.dtype)
 
     def relaxed_jvp_batch(self, ts, S, V):
-        return self._call_jvp(as_steps(ts, self.device), self._state(S), self._state(V), relaxed=True)
+        ts, S, V = as_steps(ts, self.device), self._state(S), self._state(V)
+        if self.kernels:
+            return self._call_jvp(ts, S, V, relaxed=True)
+        return self._torch_jvp(ts, S, V, relaxed=True).to(self.dtype)
 
-    def _sequential(self, s0, T):
+    @property
+    def _sequential(self):
+        return self._sequential_kernel if self.kernels else None
+
+    def _sequential_kernel(self, s0, T):
         out = torch.empty((T, self.dim), dtype=self.dtype, device=self.device)
         bad = torch.empty(1, dtype=torch.int64, device=self.device)
         d = self.desc()
@@ -152,7 +175,6 @@ class MalaKernel(_Fused):
         super().__init__(model.dim, noise, dtype)
         self.model = model
         self.eps = float(eps)
-        self._blr = model.spec is not None and model.spec.kind == "blr"
 
     def desc(self):
         d = _base_desc(self._kind, self.dim, self.model, self.eps, self.noise.seed, self.noise.T)
@@ -162,7 +184,7 @@ class MalaKernel(_Fused):
         d.noise_logu = self._logu.data_ptr()
         return d
 
-    # -- logistic regression: GEMM-based evaluation of the same arithmetic --
+    # -- GEMM evaluation (logistic regression, wide Gaussians): samplers.py:95-145 --
     def _gate(self, ts, S):
         eps, m = self.eps, self.model
         xi = _noise_table(self.noise, "xi", self.noise.T, torch.float64)[ts]
@@ -180,7 +202,15 @@ class MalaKernel(_Fused):
         gtilde = torch.minimum(torch.zeros_like(delta), delta) - logu
         return xprop, gx, gprop, r_back, delta, gtilde
 
-    def _jvp_core(self, ts, S, V, hard):
+    def _torch_step(self, ts, S, relaxed):
+        xprop, *_, gtilde = self._gate(ts, S)
+        S = S.to(torch.float64)
+        if relaxed:
+            w = torch.sigmoid(gtilde)[:, None]
+            return w * xprop + (1.0 - w) * S
+        return torch.where((gtilde > 0.0)[:, None], xprop, S)
+
+    def _torch_jvp(self, ts, S, V, relaxed):
         eps, m = self.eps, self.model
         xprop, gx, gprop, r_back, delta, gtilde = self._gate(ts, S)
         S, V = S.to(torch.float64), V.to(torch.float64)
@@ -189,38 +219,9 @@ class MalaKernel(_Fused):
         ddelta = (torch.sum(gprop * dxprop, dim=-1) - torch.sum(gx * V, dim=-1)
                   - torch.sum(r_back * dr_back, dim=-1) / (2.0 * eps))
         dgate = ddelta * (delta < 0.0)
-        gate = (gtilde > 0.0).to(torch.float64) if hard else torch.sigmoid(gtilde)
+        gate = torch.sigmoid(gtilde) if relaxed else (gtilde > 0.0).to(torch.float64)
         bend = (_sigmoid_prime(gtilde) * dgate)[:, None]
-        out = gate[:, None] * dxprop + (1.0 - gate)[:, None] * V + (xprop - S) * bend
-        return out.to(self.dtype)
-
-    def _step_batch(self, ts, S):
-        if self._blr:
-            xprop, *_, gtilde = self._gate(ts, S)
-            return torch.where((gtilde > 0.0)[:, None], xprop, S.to(torch.float64)).to(self.dtype)
-        return self._call_step(ts, S)
-
-    def _jvp_batch(self, ts, S, V):
-        if self._blr:
-            return self._jvp_core(ts, S, V, True)
-        return self._call_jvp(ts, S, V)
-
-    def relaxed_step_batch(self, ts, S):
-        if self._blr:
-            ts, S = as_steps(ts, self.device), self._state(S)
-            xprop, *_, gtilde = self._gate(ts, S)
-            w = torch.sigmoid(gtilde)[:, None]
-            return (w * xprop + (1.0 - w) * S.to(torch.float64)).to(self.dtype)
-        return super().relaxed_step_batch(ts, S)
-
-    def relaxed_jvp_batch(self, ts, S, V):
-        if self._blr:
-            return self._jvp_core(as_steps(ts, self.device), self._state(S), self._state(V), False)
-        return super().relaxed_jvp_batch(ts, S, V)
-
-    @property
-    def _sequential(self):
-        return None if self._blr else _Fused._sequential.__get__(self)
+        return gate[:, None] * dxprop + (1.0 - gate)[:, None] * V + (xprop - S) * bend
 
 
 def mala_step(x, t, kernel: MalaKernel):
@@ -268,12 +269,47 @@ class LeapfrogSystem(_Fused):
         d.probe_seed = self.probe_seed & 0xFFFFFFFFFFFFFFFF
         return d
 
+    def _mass_t(self):
+        return torch.as_tensor(self.mass, dtype=torch.float64, device=self.device)
+
+    def _torch_step(self, ts, S, relaxed):
+        h = self.model.dim
+        S = S.to(torch.float64)
+        x, v = S[:, :h], S[:, h:]
+        xn = x + self.eps * v / self._mass_t()
+        return torch.cat([xn, v + self.eps * self.model.grad(xn)], dim=-1)
+
+    def _torch_jvp(self, ts, S, V, relaxed):
+        h = self.model.dim
+        S, V = S.to(torch.float64), V.to(torch.float64)
+        m = self._mass_t()
+        xn = S[:, :h] + self.eps * S[:, h:] / m
+        dxn = V[:, :h] + self.eps * V[:, h:] / m
+        return torch.cat([dxn, V[:, h:] + self.eps * self.model.hvp(xn, dxn)], dim=-1)
+
+    def _torch_block(self, ts, S, n_samples, iteration):
+        h = self.model.dim
+        S = S.to(torch.float64)
+        m = self._mass_t()
+        xn = S[:, :h] + self.eps * S[:, h:] / m
+        dhat = torch.zeros_like(xn)
+        for k in range(n_samples):
+            z = rademacher_probe(self.probe_seed, iteration, ts, k, h, device=self.device)
+            dhat += z * self.model.hvp(xn, z)
+        dhat /= n_samples
+        a = torch.ones_like(dhat)
+        b = (self.eps / m).expand(dhat.shape).clone()
+        return a, b, self.eps * dhat, 1.0 + self.eps * self.eps * dhat / m
+
     def block_jacobian_batch(self, ts, S, n_samples: int, iteration: int):
         """Stochastic 2x2 block-diagonal Jacobian (samplers.py:202-222)."""
         ts = as_steps(ts, self.device)
         S = self._state(S).contiguous()
         n = S.shape[0]
         h = self.model.dim
+        if not self.kernels:
+            self.n_hvp_evals += int(n_samples) * n
+            return tuple(x.to(self.dtype) for x in self._torch_block(ts, S, int(n_samples), int(iteration)))
         outs = [torch.empty((n, h), dtype=self.dtype, device=self.device) for _ in range(4)]
         d = self.desc()
         rc = _lib.load().cs_system_block_jacobian(ctypes.byref(d), _lib.dtype_code(self.dtype),
@@ -374,9 +410,67 @@ class HmcKernel(_Fused):
                 xs[b], vs[b] = final[:h], final[h:]
         return xs, vs
 
+    def _torch_step(self, ts, S, relaxed):
+        xl, delta, gtilde = self._gate_torch(ts, S, parallel=False)
+        S = S.to(torch.float64)
+        if relaxed:
+            w = torch.sigmoid(gtilde)[:, None]
+            return w * xl + (1.0 - w) * S
+        return torch.where((gtilde > 0.0)[:, None], xl, S)
+
+    def _gate_torch(self, ts, S, parallel):
+        eps, m = self.eps, self.model
+        S64 = S.to(torch.float64)
+        xi = _noise_table(self.noise, "momentum", self.noise.T, torch.float64)[ts]
+        mass = self._mass_t()
+        h0 = 0.5 * torch.sum(xi * xi, dim=-1) - m.logp(S64)
+        v_half = torch.sqrt(mass) * xi + 0.5 * eps * m.grad(S64)
+        if parallel:
+            xl, v_lhalf = self._integrate_parallel(ts, S64, v_half)
+        else:
+            xl, v_lhalf = self._integrate_sequential(S64, v_half)
+        if not bool(torch.isfinite(xl).all()):
+            b = _first_bad(ts, xl)
+            raise ChainDivergedError(f"non-finite HMC trajectory at step {b}", step=b)
+        vl = v_lhalf - 0.5 * eps * m.grad(xl)
+        hl = 0.5 * torch.sum(vl * vl / mass, dim=-1) - m.logp(xl)
+        delta = h0 - hl
+        logu = _noise_table(self.noise, "u", self.noise.T, torch.float64, log_uniform=True)[ts, 0]
+        gtilde = torch.minimum(torch.zeros_like(delta), delta) - logu
+        return xl, delta, gtilde
+
+    def _torch_jvp(self, ts, S, V, relaxed):
+        """Tangents ride the sequential integrator (samplers.py:353-381)."""
+        eps, m = self.eps, self.model
+        S, V = S.to(torch.float64), V.to(torch.float64)
+        mass = self._mass_t()
+        xi = _noise_table(self.noise, "momentum", self.noise.T, torch.float64)[ts]
+        g0 = m.grad(S)
+        dh0 = -torch.sum(g0 * V, dim=-1)
+        h0 = 0.5 * torch.sum(xi * xi, dim=-1) - m.logp(S)
+        x, v = S, torch.sqrt(mass) * xi + 0.5 * eps * g0
+        dx, dv = V, 0.5 * eps * m.hvp(S, V)
+        for _ in range(self.L):
+            x = x + eps * v / mass
+            dx = dx + eps * dv / mass
+            dv = dv + eps * m.hvp(x, dx)
+            v = v + eps * m.grad(x)
+        gl = m.grad(x)
+        vl = v - 0.5 * eps * gl
+        dvl = dv - 0.5 * eps * m.hvp(x, dx)
+        hl = 0.5 * torch.sum(vl * vl / mass, dim=-1) - m.logp(x)
+        dhl = torch.sum(vl * dvl / mass, dim=-1) - torch.sum(gl * dx, dim=-1)
+        delta, ddelta = h0 - hl, dh0 - dhl
+        logu = _noise_table(self.noise, "u", self.noise.T, torch.float64, log_uniform=True)[ts, 0]
+        gtilde = torch.minimum(torch.zeros_like(delta), delta) - logu
+        dgate = ddelta * (delta < 0.0)
+        gate = torch.sigmoid(gtilde) if relaxed else (gtilde > 0.0).to(torch.float64)
+        bend = (_sigmoid_prime(gtilde) * dgate)[:, None]
+        return gate[:, None] * dx + (1.0 - gate)[:, None] * V + (x - S) * bend
+
     def _step_batch(self, ts, S):
         if self.leapfrog_mode != "parallel":
-            return self._call_step(ts, S)
+            return super()._step_batch(ts, S)
         eps, m = self.eps, self.model
         S64 = S.to(torch.float64)
         xi = _noise_table(self.noise, "momentum", self.noise.T, torch.float64)[ts]
@@ -396,7 +490,7 @@ class HmcKernel(_Fused):
 
     @property
     def _sequential(self):
-        return None if self.leapfrog_mode == "parallel" else _Fused._sequential.__get__(self)
+        return self._sequential_kernel if (self.kernels and self.leapfrog_mode != "parallel") else None
 
 
 def hmc_step(x, t, kernel: HmcKernel, leapfrog_mode: str | None = None):

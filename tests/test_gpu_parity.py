@@ -298,3 +298,61 @@ def test_run_deer_leapfrog_block_and_window(cuda_device):
     r = cs.run_deer(lf, s0, cs.DeerConfig(mode="block2x2-stochastic"))
     assert r.converged and r.iterations == 1
     np.testing.assert_allclose(np_(r.trace), np_(cs.sequential_evaluate(lf, s0)), atol=1e-9)
+
+
+# ---------------------------------------------------------------------------
+# GEMM-evaluated systems: logistic-regression MALA (cfg 3) and the wide
+# Gaussian leapfrog (cfg 4)
+
+
+def test_synthetic_credit_like_matches_reference(cuda_device):
+    g = golden("mala_blr100")
+    X, y, beta = cs.synthetic_credit_like(seed=20250819, n=1000, dim=100)
+    np.testing.assert_allclose(X, g["X"], rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(beta, g["beta_star"], rtol=1e-13, atol=1e-13)
+    np.testing.assert_array_equal(y, g["y"])
+
+
+def test_run_deer_blr_gemm_path(cuda_device):
+    g = golden("mala_blr100")
+    m = cs.model_logp_grad_hvp(cs.blr(g["X"], g["y"], 1.0))
+    k = cs.MalaKernel(m, 0.003, seed=4, T=300)
+    assert not k.kernels
+    np.testing.assert_allclose(np_(cs.sequential_evaluate(k, np.zeros(100))), g["seq"], atol=1e-9, rtol=1e-9)
+    r = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="diag-stochastic"))
+    assert r.stats["path"] == "host"
+    _deer_cmp(r, g, "diag_", torch.float64)
+
+
+def test_run_deer_leapfrog_gauss200(cuda_device):
+    g = golden("leapfrog_gauss200")
+    m = cs.model_logp_grad_hvp(cs.gaussian(np.zeros(200), g["chol"]))
+    lf = cs.LeapfrogSystem(m, 0.05, 100, probe_seed=0)
+    assert not lf.kernels
+    np.testing.assert_allclose(np_(cs.sequential_evaluate(lf, g["s0"])), g["seq"], atol=1e-9, rtol=1e-9)
+    _deer_cmp(cs.run_deer(lf, g["s0"], cs.DeerConfig(mode="block2x2-stochastic")), g, "block_", torch.float64)
+    _deer_cmp(cs.run_deer(lf, g["s0"], cs.DeerConfig(mode="diag-stochastic")), g, "diag_", torch.float64)
+
+
+def _cfg4_gaussian(D=1000):
+    rng = np.random.default_rng(0)
+    Q, _ = np.linalg.qr(rng.normal(size=(D, D)))
+    lam = np.exp(rng.uniform(np.log(0.1), np.log(10.0), D))
+    P = (Q * lam) @ Q.T
+    return np.linalg.cholesky(P)
+
+
+def test_leapfrog_block_cfg4_full_size_vs_oracle(cuda_device):
+    # BASELINE cfg 4: HMC proposal of L=100 leapfrog steps, Gaussian D=1000, block quasi-Newton
+    D, eps, L = 1000, 0.05, 100
+    Lc = _cfg4_gaussian(D)
+    om = O.gaussian(np.zeros(D), Lc)
+    x0 = np.random.default_rng(1).normal(size=D)
+    v0 = np.random.default_rng(2).normal(size=D)
+    s0 = np.concatenate([x0, v0 + 0.5 * eps * om.grad(x0)])
+    ref = O.run_deer(O.LeapfrogSystem(om, eps, L, probe_seed=0), s0, O.DeerConfig(mode="block2x2-stochastic"))
+    lf = cs.LeapfrogSystem(cs.model_logp_grad_hvp(cs.gaussian(np.zeros(D), Lc)), eps, L, probe_seed=0)
+    r = cs.run_deer(lf, s0, cs.DeerConfig(mode="block2x2-stochastic"))
+    assert r.iterations == ref.iterations
+    np.testing.assert_allclose(np_(r.trace), ref.trace, atol=1e-8, rtol=1e-8)
+    np.testing.assert_array_equal(np_(r.per_step_converged_at), ref.per_step_converged_at)
