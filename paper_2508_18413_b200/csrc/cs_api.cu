@@ -217,8 +217,10 @@ __global__ void k_hutch(ST *est, const ST *z, const ST *jz, int64_t n, int first
 
 __global__ void k_set_i64(long long *p, long long v) { *p = v; }
 
-__global__ void k_init_ctl(SolveCtl *c) {
-  for (int s = 0; s < 2; ++s) {
+__global__ void k_init_ctl(SolveCtl *c, int *ready, int nready) {
+  for (int i = threadIdx.x; i < nready; i += blockDim.x) ready[i] = 0;
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < 4; ++s) {
     c->slot[s].bad_prop = c->slot[s].bad_f = c->slot[s].bad_jac = kNoStep;
     c->slot[s].picard_fail = c->slot[s].any_fail = 0;
     c->slot[s].dmax_bits = 0ull;
@@ -545,7 +547,8 @@ size_t cs_deer_workspace_bytes(const cs_system *sys, int dtype, int32_t max_iter
   const int md = solver_width(sys);
   const int W = md * md + md;
   const size_t T = (size_t)sys->T, D = (size_t)sys->dim;
-  return al(T * D * esize(dtype)) + al(sizeof(SolveCtl)) + al(sizeof(double) * 2 * 8 * (size_t)sm_count() * (W > 0 ? W : 1));
+  return al(T * D * esize(dtype)) + al(sizeof(SolveCtl)) + al(sizeof(double) * 2 * 8 * (size_t)sm_count() * (W > 0 ? W : 1)) +
+         al(sizeof(int) * 8 * (size_t)sm_count());
 }
 
 int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, const void *s0, void *trace,
@@ -573,9 +576,11 @@ int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, co
   SolveCtl *ctl = (SolveCtl *)w;
   w += al(sizeof(SolveCtl));
   double *agg = (double *)w;
-  cudaStream_t st = S(stream);
   const int sms = sm_count();
-  k_init_ctl<<<1, 1, 0, st>>>(ctl);
+  w += al(sizeof(double) * 2 * 8 * (size_t)sms * (md * md + md));
+  int *ready = (int *)w;
+  cudaStream_t st = S(stream);
+  k_init_ctl<<<1, 256, 0, st>>>(ctl, ready, 8 * sms);
   SolvePick pick{};
   cudaError_t e;
   if (dtype == CS_F64) {
@@ -583,14 +588,14 @@ int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, co
     A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;
     A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
     A.pre = cfg->preconditioner; A.s0 = (const double *)s0; A.G0 = (double *)trace; A.G1 = (double *)G1;
-    A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ctl; A.agg = agg; A.T = T; A.D = D;
+    A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ctl; A.agg = agg; A.ready = ready; A.T = T; A.D = D;
     e = solve_dispatch(*sys, dtype, md, cfg->mode, &A, sms, st, &pick);
   } else {
     SolveArgs<float> A{};
     A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;
     A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
     A.pre = cfg->preconditioner; A.s0 = (const float *)s0; A.G0 = (float *)trace; A.G1 = (float *)G1;
-    A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ctl; A.agg = agg; A.T = T; A.D = D;
+    A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ctl; A.agg = agg; A.ready = ready; A.T = T; A.D = D;
     e = solve_dispatch(*sys, dtype, md, cfg->mode, &A, sms, st, &pick);
   }
   if (e == cudaErrorNotSupported) return fail(CS_ERR_CONFIG, "fused solver not instantiated for this system");

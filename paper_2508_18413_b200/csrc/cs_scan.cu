@@ -11,6 +11,7 @@
 // traffic.  Carries and composition run in f64 regardless of storage type.
 #include "cs_lookback.cuh"
 #include "cs_scan.cuh"
+#include "cs_tma.cuh"
 
 namespace cs {
 
@@ -33,6 +34,12 @@ template <> struct ColElem<SCAN_DIAG> {
   CS_D void store(double *p) const { p[0] = j; p[1] = u; }
   CS_D void load(const double *p) { j = p[0]; u = p[1]; }
   CS_D void load_cg(const double *p) { j = ld_cg(p); u = ld_cg(p + 1); }
+  CS_D ColElem down(int off) const {
+    ColElem o;
+    o.j = __shfl_down_sync(0xffffffffu, j, off);
+    o.u = __shfl_down_sync(0xffffffffu, u, off);
+    return o;
+  }
 };
 
 template <> struct ColElem<SCAN_BLOCK> {
@@ -61,82 +68,162 @@ template <> struct ColElem<SCAN_BLOCK> {
   CS_D void load_cg(const double *p) {
     A = ld_cg(p); B = ld_cg(p + 1); C = ld_cg(p + 2); E = ld_cg(p + 3); ux = ld_cg(p + 4); uv = ld_cg(p + 5);
   }
+  CS_D ColElem down(int off) const {
+    ColElem o;
+    o.A = __shfl_down_sync(0xffffffffu, A, off);
+    o.B = __shfl_down_sync(0xffffffffu, B, off);
+    o.C = __shfl_down_sync(0xffffffffu, C, off);
+    o.E = __shfl_down_sync(0xffffffffu, E, off);
+    o.ux = __shfl_down_sync(0xffffffffu, ux, off);
+    o.uv = __shfl_down_sync(0xffffffffu, uv, off);
+    return o;
+  }
 };
 
-// look-back for column c of tile b; returns the entry state(s) of the column.
-template <int VAR, typename ST>
-CS_D void lookback_col(const LookbackWs &ws, int64_t b, int ncol, int c, int SW, const ST *s0,
-                       double &x, double &v) {
-  ColElem<VAR> acc;
-  acc.ident();
-  int64_t p = b - 1;
-  while (p >= 0) {
-    int st;
-    do { st = ld_acquire(ws.status + p); } while (st == 0);
-    if (st == 2) {
-      x = ld_cg(ws.exit + p * SW + c);
-      if (VAR == SCAN_BLOCK) v = ld_cg(ws.exit + p * SW + ncol + c);
-      break;
+// CTA-wide decoupled look-back over a window of 32 predecessors at a time:
+// warp 0 waits until every predecessor in the window has published at least
+// its aggregate and finds the nearest exit state; then the 8 warps fold the
+// window's aggregates column by column (lane = tile, ordered tree reduction)
+// into the running prefix s_acc.  One L2 round trip covers 32 tiles.
+//   status(p) -> const int*     agg(p, c) -> const double*
+//   exit_x(p, c), exit_v(p, c)  the published exit state of tile p
+//   s0x(c), s0v(c)              the chain's initial state
+template <int VAR, class StatusF, class AggF, class ExitF, class ExitVF, class S0F, class S0VF>
+CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF exit_x, ExitVF exit_v,
+                       S0F s0x, S0VF s0v, double *s_acc, double *s_entry, int *s_ctl) {
+  constexpr int W = ColElem<VAR>::W;
+  constexpr int NW = kScanThreads / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c = threadIdx.x; c < ncol; c += kScanThreads) {
+    ColElem<VAR> id;
+    id.ident();
+    id.store(s_acc + c * W);
+  }
+  int64_t hi = pos - 1;
+  for (;;) {
+    __syncthreads();
+    if (wid == 0) {
+      const int64_t p = hi - lane;
+      int st = 2;
+      if (p >= 0) {
+        do { st = ld_acquire(status(p)); } while (st == 0);
+      }
+      const unsigned m2 = __ballot_sync(0xffffffffu, st == 2);
+      if (lane == 0) s_ctl[0] = m2 ? __ffs(m2) - 1 : 32;
     }
-    ColElem<VAR> e;
-    e.load_cg(ws.agg + (p * ncol + c) * ColElem<VAR>::W);
-    acc.pre(e);
-    --p;
+    __syncthreads();
+    const int stop = s_ctl[0];
+    const int64_t p = hi - lane;
+    for (int c = wid; c < ncol; c += NW) {
+      ColElem<VAR> e;
+      if (lane < stop) e.load_cg(agg(p, c));
+      else e.ident();
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        ColElem<VAR> o = e.down(off);
+        if (lane + off < 32) e.pre(o);  // later tile (lower lane) applied after the earlier one
+      }
+      if (lane == 0) {
+        ColElem<VAR> acc;
+        acc.load(s_acc + c * W);
+        acc.pre(e);
+        acc.store(s_acc + c * W);
+      }
+    }
+    if (stop < 32) {
+      __syncthreads();
+      const int64_t pe = hi - stop;
+      for (int c = threadIdx.x; c < ncol; c += kScanThreads) {
+        double x = pe < 0 ? s0x(c) : exit_x(pe, c);
+        double v = 0.0;
+        if (VAR == SCAN_BLOCK) v = pe < 0 ? s0v(c) : exit_v(pe, c);
+        ColElem<VAR> acc;
+        acc.load(s_acc + c * W);
+        if constexpr (VAR == SCAN_DIAG) acc.apply(x);
+        else acc.apply(x, v);
+        s_entry[c] = x;
+        if (VAR == SCAN_BLOCK) s_entry[ncol + c] = v;
+      }
+      __syncthreads();
+      return;
+    }
+    hi -= 32;
   }
-  if (p < 0) {
-    x = (double)s0[c];
-    if (VAR == SCAN_BLOCK) v = (double)s0[ncol + c];
-  }
-  if constexpr (VAR == SCAN_DIAG) acc.apply(x);
-  else acc.apply(x, v);
 }
 
 // ---------------------------------------------------------------------------
 // narrow rows: tile = R consecutive rows x all columns, staged in smem
 template <typename ST, int VAR, bool AGG_ONLY = false>
 __global__ void __launch_bounds__(kScanThreads)
-scan_rows(ScanArgs<ST> a, LookbackWs ws, int R) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int NA = VAR == SCAN_DIAG ? 2 : 6;  // element arrays staged (block: a b c d + u as 2)
+scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int win) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int NA = VAR == SCAN_DIAG ? 2 : 6;  // staged arrays (block: a b c d + u counted as 2)
+  constexpr int W = ColElem<VAR>::W;
   const int ncol = a.D;
   const int SW = VAR == SCAN_DIAG ? ncol : 2 * ncol;
   __shared__ int64_t s_tile;
   __shared__ double s_entry[2 * 64];
-  if (threadIdx.x == 0) s_tile = atomicAdd(ws.ticket, 1u);
+  __shared__ double s_acc[64 * W];
+  __shared__ int s_ctl[1];
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(ws.ticket, 1u);
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
   __syncthreads();
   const int64_t b = s_tile;
   const int64_t row0 = b * R;
   const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
   const int nel = rows * ncol;
-  ST *tile = (ST *)smem_raw;                       // NA arrays of R*ncol
+  ST *tile = (ST *)smem_raw;  // NA arrays of R*ncol
   double *segagg = (double *)(smem_raw + ((sizeof(ST) * NA * R * ncol + 15) / 16) * 16);
+  const ST *u_src = a.u + 2 * row0 * ncol * (VAR == SCAN_BLOCK) + row0 * ncol * (VAR == SCAN_DIAG);
 
-  // stage the tile (coalesced; every element read once from HBM)
-  {
-    const int64_t g0 = row0 * ncol;
-    if constexpr (VAR == SCAN_DIAG) {
-      for (int i = threadIdx.x; i < nel; i += kScanThreads) {
-        tile[i] = a.e0[g0 + i];
-        tile[R * ncol + i] = a.u[g0 + i];
+  // ---- stage the tile: one bulk (TMA) copy per array when aligned, else LDG loop
+  const unsigned bytes = (unsigned)(sizeof(ST) * nel);
+  const bool tma = (bytes % 16 == 0) && aligned16(a.e0 + row0 * ncol) && aligned16(u_src) &&
+                   (VAR == SCAN_DIAG || (aligned16(a.e1 + row0 * ncol) && aligned16(a.e2 + row0 * ncol) &&
+                                         aligned16(a.e3 + row0 * ncol)));
+  if (tma) {
+    if (threadIdx.x == 0) {
+      const int64_t g0 = row0 * ncol;
+      if constexpr (VAR == SCAN_DIAG) {
+        mbar_expect_tx(&s_bar, 2 * bytes);
+        bulk_g2s(tile, a.e0 + g0, bytes, &s_bar);
+        bulk_g2s(tile + R * ncol, u_src, bytes, &s_bar);
+      } else {
+        mbar_expect_tx(&s_bar, 6 * bytes);
+        bulk_g2s(tile, a.e0 + g0, bytes, &s_bar);
+        bulk_g2s(tile + R * ncol, a.e1 + g0, bytes, &s_bar);
+        bulk_g2s(tile + 2 * R * ncol, a.e2 + g0, bytes, &s_bar);
+        bulk_g2s(tile + 3 * R * ncol, a.e3 + g0, bytes, &s_bar);
+        bulk_g2s(tile + 4 * R * ncol, u_src, 2 * bytes, &s_bar);
       }
-    } else {
-      for (int i = threadIdx.x; i < nel; i += kScanThreads) {
-        tile[i] = a.e0[g0 + i];
+    }
+    mbar_wait(&s_bar, 0);
+  } else {
+    const int64_t g0 = row0 * ncol;
+    for (int i = threadIdx.x; i < nel; i += kScanThreads) {
+      tile[i] = a.e0[g0 + i];
+      if constexpr (VAR == SCAN_DIAG) {
+        tile[R * ncol + i] = u_src[i];
+      } else {
         tile[R * ncol + i] = a.e1[g0 + i];
         tile[2 * R * ncol + i] = a.e2[g0 + i];
         tile[3 * R * ncol + i] = a.e3[g0 + i];
       }
-      for (int i = threadIdx.x; i < 2 * nel; i += kScanThreads) tile[4 * R * ncol + i] = a.u[2 * g0 + i];
     }
+    if constexpr (VAR == SCAN_BLOCK)
+      for (int i = threadIdx.x; i < 2 * nel; i += kScanThreads) tile[4 * R * ncol + i] = u_src[i];
+    __syncthreads();
   }
-  __syncthreads();
 
   const int nseg = kScanThreads / ncol;
-  const int c = threadIdx.x % ncol, s = threadIdx.x / ncol;
+  const int c = threadIdx.x % ncol, sg = threadIdx.x / ncol;
   const int seglen = (rows + nseg - 1) / nseg;
-  const int r0 = s * seglen, r1 = min(rows, r0 + seglen);
-  const bool active = s < nseg;
-  constexpr int W = ColElem<VAR>::W;
+  const int r0 = sg * seglen, r1 = min(rows, r0 + seglen);
+  const bool active = sg < nseg;
 
   ColElem<VAR> run;
   run.ident();
@@ -151,7 +238,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R) {
                  (double)tile[4 * R * ncol + 2 * r * ncol + ncol + c]);
       }
     }
-    run.store(segagg + (s * ncol + c) * W);
+    run.store(segagg + (sg * ncol + c) * W);
   }
   __syncthreads();
 
@@ -170,42 +257,43 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R) {
     tot.store(tmp);
 #pragma unroll
     for (int k = 0; k < W; ++k) g[k] = tmp[k];
-    __threadfence();
-    // keep the tile aggregate for the exit state
     tot.store(segagg + (nseg * ncol + threadIdx.x) * W);
+    __threadfence();
   }
   __syncthreads();
   if (threadIdx.x == 0) st_release(ws.status + b, 1);
   if constexpr (AGG_ONLY) return;
 
-  // look-back (first warp; lanes over columns)
-  if (threadIdx.x < 32) {
-    for (int cc = threadIdx.x; cc < ncol; cc += 32) {
-      double x = 0.0, v = 0.0;
-      lookback_col<VAR>(ws, b, ncol, cc, SW, a.s0, x, v);
-      s_entry[cc] = x;
-      if (VAR == SCAN_BLOCK) s_entry[ncol + cc] = v;
-      ColElem<VAR> tot;
-      tot.load(segagg + (nseg * ncol + cc) * W);
-      if constexpr (VAR == SCAN_DIAG) {
-        tot.apply(x);
-        ws.exit[b * SW + cc] = x;
-      } else {
-        tot.apply(x, v);
-        ws.exit[b * SW + cc] = x;
-        ws.exit[b * SW + ncol + cc] = v;
-      }
+  lookback_cta<VAR>(
+      b, ncol, [&](int64_t p) { return ws.status + p; },
+      [&](int64_t p, int cc) { return ws.agg + (p * ncol + cc) * W; },
+      [&](int64_t p, int cc) { return ld_cg(ws.exit + p * SW + cc); },
+      [&](int64_t p, int cc) { return ld_cg(ws.exit + p * SW + ncol + cc); },
+      [&](int cc) { return (double)a.s0[cc]; }, [&](int cc) { return (double)a.s0[ncol + cc]; }, s_acc,
+      s_entry, s_ctl);
+
+  // exit state of this tile, published before the replay
+  if (threadIdx.x < ncol) {
+    ColElem<VAR> tot;
+    tot.load(segagg + (nseg * ncol + threadIdx.x) * W);
+    double x = s_entry[threadIdx.x], v = VAR == SCAN_BLOCK ? s_entry[ncol + threadIdx.x] : 0.0;
+    if constexpr (VAR == SCAN_DIAG) {
+      tot.apply(x);
+      ws.exit[b * SW + threadIdx.x] = x;
+    } else {
+      tot.apply(x, v);
+      ws.exit[b * SW + threadIdx.x] = x;
+      ws.exit[b * SW + ncol + threadIdx.x] = v;
     }
     __threadfence();
-    __syncwarp();
-    if (threadIdx.x == 0) st_release(ws.status + b, 2);
   }
   __syncthreads();
+  if (threadIdx.x == 0) st_release(ws.status + b, 2);
 
   // replay from the segment entry state; results overwrite the staged tile
   if (active && r0 < r1) {
     ColElem<VAR> pre;
-    pre.load(segagg + (s * ncol + c) * W);
+    pre.load(segagg + (sg * ncol + c) * W);
     if constexpr (VAR == SCAN_DIAG) {
       double x = s_entry[c];
       pre.apply(x);
@@ -231,11 +319,20 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R) {
       }
     }
   }
-  __syncthreads();
-  {
-    const int64_t g0 = row0 * SW;
+  const ST *src = VAR == SCAN_DIAG ? tile : tile + 4 * R * ncol;
+  const int64_t g0 = row0 * SW;
+  const unsigned obytes = (unsigned)(sizeof(ST) * rows * SW);
+  if (tma && aligned16(a.out + g0) && obytes % 16 == 0) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(a.out + g0, src, obytes);
+      bulk_commit();
+      bulk_wait_read();
+    }
+  } else {
+    __syncthreads();
     const int nout = rows * SW;
-    const ST *src = VAR == SCAN_DIAG ? tile : tile + 4 * R * ncol;
     for (int i = threadIdx.x; i < nout; i += kScanThreads) a.out[g0 + i] = src[i];
   }
 }
@@ -252,8 +349,10 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
   const int SW = VAR == SCAN_DIAG ? ncol : 2 * ncol;
   const int ncb = (ncol + 31) / 32;
   __shared__ int64_t s_tile;
-  __shared__ double segagg[8][32][W];
-  __shared__ double s_entry[2][32];
+  __shared__ double segagg[9][32][W];
+  __shared__ double s_entry[2 * 32];
+  __shared__ double s_acc[32 * W];
+  __shared__ int s_ctl[1];
   if (threadIdx.x == 0) s_tile = atomicAdd(ws.ticket, 1u);
   __syncthreads();
   const int64_t tk = s_tile;
@@ -295,49 +394,31 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
       tot.store(segagg[q][lane]);
       tot.push(e);
     }
-    if (colok) {
-      double tmp[W];
-      tot.store(tmp);
-      double *g = ws.agg + (tk * 32 + lane) * W;
+    tot.store(segagg[8][lane]);
+    double tmp[W];
+    tot.store(tmp);
+    double *g = ws.agg + (tk * 32 + lane) * W;
 #pragma unroll
-      for (int k = 0; k < W; ++k) g[k] = tmp[k];
-    }
+    for (int k = 0; k < W; ++k) g[k] = tmp[k];
     __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(ws.status + tk, 1);
-    if constexpr (AGG_ONLY) return;
-    // look-back along the same column block: predecessor ticket tk - ncb
-    double x = 0.0, v = 0.0;
-    {
-      ColElem<VAR> acc;
-      acc.ident();
-      int64_t p = rb - 1;
-      while (p >= 0) {
-        const int64_t pt = p * ncb + cb;
-        int st;
-        do { st = ld_acquire(ws.status + pt); } while (st == 0);
-        if (st == 2) {
-          if (colok) {
-            x = ld_cg(ws.exit + p * SW + c);
-            if (VAR == SCAN_BLOCK) v = ld_cg(ws.exit + p * SW + ncol + c);
-          }
-          break;
-        }
-        ColElem<VAR> e;
-        if (colok) e.load_cg(ws.agg + (pt * 32 + lane) * W);
-        else e.ident();
-        acc.pre(e);
-        --p;
-      }
-      if (p < 0 && colok) {
-        x = (double)a.s0[c];
-        if (VAR == SCAN_BLOCK) v = (double)a.s0[ncol + c];
-      }
-      if constexpr (VAR == SCAN_DIAG) acc.apply(x);
-      else acc.apply(x, v);
-    }
-    s_entry[0][lane] = x;
-    s_entry[1][lane] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(ws.status + tk, 1);
+  if constexpr (AGG_ONLY) return;
+
+  lookback_cta<VAR>(
+      rb, 32, [&](int64_t p) { return ws.status + p * ncb + cb; },
+      [&](int64_t p, int cc) { return ws.agg + ((p * ncb + cb) * 32 + cc) * W; },
+      [&](int64_t p, int cc) { return cb * 32 + cc < ncol ? ld_cg(ws.exit + p * SW + cb * 32 + cc) : 0.0; },
+      [&](int64_t p, int cc) { return cb * 32 + cc < ncol ? ld_cg(ws.exit + p * SW + ncol + cb * 32 + cc) : 0.0; },
+      [&](int cc) { return cb * 32 + cc < ncol ? (double)a.s0[cb * 32 + cc] : 0.0; },
+      [&](int cc) { return cb * 32 + cc < ncol ? (double)a.s0[ncol + cb * 32 + cc] : 0.0; }, s_acc, s_entry,
+      s_ctl);
+
+  if (threadIdx.x < 32) {
+    ColElem<VAR> tot;
+    tot.load(segagg[8][lane]);
+    double x = s_entry[lane], v = VAR == SCAN_BLOCK ? s_entry[32 + lane] : 0.0;
     if constexpr (VAR == SCAN_DIAG) tot.apply(x);
     else tot.apply(x, v);
     if (colok) {
@@ -345,14 +426,13 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
       if (VAR == SCAN_BLOCK) ws.exit[rb * SW + ncol + c] = v;
     }
     __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(ws.status + tk, 2);
   }
-  if constexpr (AGG_ONLY) return;
   __syncthreads();
+  if (threadIdx.x == 0) st_release(ws.status + tk, 2);
+
   ColElem<VAR> pre;
   pre.load(segagg[s][lane]);
-  double x = s_entry[0][lane], v = s_entry[1][lane];
+  double x = s_entry[lane], v = VAR == SCAN_BLOCK ? s_entry[32 + lane] : 0.0;
   if constexpr (VAR == SCAN_DIAG) pre.apply(x);
   else pre.apply(x, v);
 #pragma unroll
@@ -647,8 +727,10 @@ static int rows_per_tile(int var, int dtype, int D) {
   const int per = (var == SCAN_DIAG ? 2 : 6) * esz;
   int E = (64 * 1024) / per;
   int R = E / D;
-  if (R < 1) R = 1;
   if (R > 8192) R = 8192;
+  const int q = dtype == CS_F64 ? 2 : 4;  // R*D*esize % 16 == 0 for any D
+  R = (R / q) * q;
+  if (R < q) R = q;
   return R;
 }
 
@@ -672,7 +754,14 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
     const int esz = dtype == CS_F64 ? 8 : 4;
     const int NA = var == SCAN_DIAG ? 2 : 6;
     const int nseg = kScanThreads / D;
-    p.smem = ((size_t)esz * NA * p.R * D + 15) / 16 * 16 + sizeof(double) * (nseg + 1) * D * (var == SCAN_DIAG ? 2 : 6);
+    const int W = var == SCAN_DIAG ? 2 : 6;
+    p.smem = ((size_t)esz * NA * p.R * D + 15) / 16 * 16 + sizeof(double) * (nseg + 1) * D * W;
+    // walker window: aggregates [win][D][W] + chunk scratch [nseg][D][W] within the same smem
+    const size_t chunk_bytes = sizeof(double) * (size_t)nseg * D * W;
+    int win = (int)((p.smem - chunk_bytes) / (sizeof(double) * D * W));
+    if (win > 256) win = 256;
+    if (win < 1) win = 1;
+    p.win = win;
   } else {
     p.kind = 1;
     const int ncb = (D + 31) / 32;
@@ -711,10 +800,10 @@ cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStrea
   if (p.kind == 0) {
     if (p.var == SCAN_DIAG) {
       cudaFuncSetAttribute(scan_rows<ST, SCAN_DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      scan_rows<ST, SCAN_DIAG><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R);
+      scan_rows<ST, SCAN_DIAG><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
     } else {
       cudaFuncSetAttribute(scan_rows<ST, SCAN_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      scan_rows<ST, SCAN_BLOCK><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R);
+      scan_rows<ST, SCAN_BLOCK><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
     }
   } else if (p.kind == 1) {
     if (p.var == SCAN_DIAG) scan_cols<ST, SCAN_DIAG><<<grid, kScanThreads, 0, st>>>(a, w);
@@ -739,11 +828,11 @@ cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, doub
   if (p.kind == 0) {
     if (p.var == SCAN_DIAG) {
       cudaFuncSetAttribute(scan_rows<ST, SCAN_DIAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      scan_rows<ST, SCAN_DIAG, true><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R);
+      scan_rows<ST, SCAN_DIAG, true><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
       k_agg_compose_cols<SCAN_DIAG><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
     } else {
       cudaFuncSetAttribute(scan_rows<ST, SCAN_BLOCK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      scan_rows<ST, SCAN_BLOCK, true><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R);
+      scan_rows<ST, SCAN_BLOCK, true><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
       k_agg_compose_cols<SCAN_BLOCK><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
     }
   } else if (p.kind == 1) {

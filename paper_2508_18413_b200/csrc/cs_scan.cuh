@@ -16,7 +16,7 @@ struct ScanArgs {
 };
 
 struct ScanPlan {
-  int var, kind, R, md, seg;
+  int var, kind, R, md, seg, win;
   int64_t ntiles;
   int agg_w, state_w;
   size_t smem, ws_bytes;

@@ -40,7 +40,7 @@ struct SolveSlot {
 };
 
 struct SolveCtl {
-  SolveSlot slot[2];
+  SolveSlot slot[4];
   unsigned arrive, gen;
   int iterations, status, err_kind, final_buf, stop;
   long long err_step;
@@ -60,6 +60,7 @@ struct SolveArgs {
   double *hist;
   SolveCtl *ctl;
   double *agg;  // [2][nblocks][W]
+  int *ready;   // [nblocks] iterate stamp: rows of guess_it written by CTA b
   int64_t T;
   int D, seg, nblocks;
 };
@@ -228,20 +229,18 @@ CS_D void block_scan(const E &x, E &excl, E &total, E *s_warp) {
   __syncthreads();
 }
 
-CS_D void grid_sync(SolveCtl *c, unsigned nblocks, unsigned &gen) {
+// Grid barrier on a monotone arrival counter: every CTA adds 1 with release
+// semantics and waits (acquire) until the counter reaches nblocks * generation.
+// No reset and no last-arriver hand-off, so one L2 round trip per barrier.
+CS_D void grid_sync(SolveCtl *c, unsigned nblocks, unsigned &target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned g = gen;
-    if (atomicAdd(&c->arrive, 1u) == nblocks - 1) {
-      atomicExch(&c->arrive, 0u);
-      __threadfence();
-      st_release((int *)&c->gen, (int)(g + 1));
-    } else {
-      while ((unsigned)ld_acquire((const int *)&c->gen) == g) __nanosleep(32);
-    }
-    gen = g + 1;
-    __threadfence();
+    target += nblocks;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&c->arrive) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&c->arrive) : "memory");
+    } while (v < target);
   }
   __syncthreads();
 }
@@ -270,26 +269,31 @@ deer_persistent(SolveArgs<ST> A) {
   for (int k = 0; k < A.seg; ++k)
     if (row0 + k < A.T) A.last_fail[row0 + k] = 0;
 
-  unsigned gen = 0;
+  unsigned target = 0;
   double d0 = -1.0;
   bool have_d0 = false;
   int it = 0, cur = 0;
   int status = CS_RUN_MAXITERS, err_kind = CS_DIV_NONE, err_iter = -1, stop = CS_STOP_MAXITERS;
   long long err_step = -1;
   double g_dmax = 0.0;
+  E excl;  // this thread's exclusive in-CTA prefix of the current pass
 
   for (;;) {
-    SolveSlot *S = &A.ctl->slot[it & 1];
+    SolveSlot *S = &A.ctl->slot[it & 3];
     const ST *Gc = cur ? A.G1 : A.G0;
-    ST *Gn = cur ? A.G0 : A.G1;
     if (threadIdx.x == 0) {
       s_min[0] = s_min[1] = s_min[2] = kNoStep;
       s_cnt[0] = s_cnt[1] = 0;
       s_dm = 0ull;
     }
+    // ---------------- phase A(it): f, Picard, elements, segment fold -------
+    // the halo row guess_it[row0-1] of CTA b's first thread was written by CTA b-1
+    if (it > 0 && threadIdx.x == 0 && b > 0) {
+      const int *rd = A.ready + (b - 1);
+      while (ld_acquire(rd) < it) {
+      }
+    }
     __syncthreads();
-
-    // ---------------- phase A: f, Picard, elements, segment fold ----------
     E agg;
     agg.ident();
     long long bp = kNoStep, bf = kNoStep, bj = kNoStep;
@@ -341,7 +345,7 @@ deer_persistent(SolveArgs<ST> A) {
 #pragma unroll
       for (int i = 0; i < MD; ++i) prev[i] = gr[i];
     }
-    E excl, total;
+    E total;
     block_scan(agg, excl, total, s_warp);
     if (threadIdx.x == 0) {
       double *g = A.agg + ((size_t)(it & 1) * A.nblocks + b) * E::W;
@@ -365,9 +369,30 @@ deer_persistent(SolveArgs<ST> A) {
       if (s_min[2] != kNoStep) atomicMin(&S->bad_jac, s_min[2]);
       if (s_cnt[0]) atomicAdd(&S->picard_fail, s_cnt[0]);
     }
-    grid_sync(A.ctl, (unsigned)A.nblocks, gen);
+    // the ONE grid barrier of the iteration: it publishes pass it's aggregates
+    // and flags together with update it-1's fail count and delta_max
+    grid_sync(A.ctl, (unsigned)A.nblocks, target);
+    if (b == 0 && threadIdx.x == 0) {
+      SolveSlot *O = &A.ctl->slot[(it + 2) & 3];
+      O->bad_prop = O->bad_f = O->bad_jac = kNoStep;
+      O->picard_fail = O->any_fail = 0;
+      O->dmax_bits = 0ull;
+    }
 
-    // ---------------- decision (identical in every CTA) --------------------
+    // ---------------- decisions (identical in every CTA) ------------------
+    if (it > 0) {  // the update that produced guess_it (deer.py:273-286)
+      const SolveSlot *P = &A.ctl->slot[(it - 1) & 3];
+      const unsigned gaf = vload(&P->any_fail);
+      const double dmax = __longlong_as_double((long long)vload(&P->dmax_bits));
+      if (b == 0 && threadIdx.x == 0) A.hist[it - 1] = dmax;
+      if (!have_d0) { d0 = dmax; have_d0 = true; }
+      g_dmax = dmax;
+      if (d0 > 0.0 && dmax > 1e6 * d0) {
+        status = CS_RUN_DIVERGED; stop = CS_STOP_ERROR; err_kind = CS_DIV_GUARD; err_step = -1; err_iter = it;
+        break;
+      }
+      if (gaf == 0) { status = CS_RUN_CONVERGED; stop = CS_STOP_NOFAIL; break; }
+    }
     {
       const long long gbp = vload(&S->bad_prop), gbf = vload(&S->bad_f), gbj = vload(&S->bad_jac);
       const unsigned gpf = vload(&S->picard_fail);
@@ -377,14 +402,9 @@ deer_persistent(SolveArgs<ST> A) {
       if (it >= A.max_iters) { status = CS_RUN_MAXITERS; stop = CS_STOP_MAXITERS; break; }
       if (gbj != kNoStep) { status = CS_RUN_DIVERGED; stop = CS_STOP_ERROR; err_kind = CS_DIV_JACOBIAN; err_step = gbj; err_iter = it + 1; break; }
     }
-    if (b == 0 && threadIdx.x == 0) {
-      SolveSlot *O = &A.ctl->slot[(it + 1) & 1];
-      O->bad_prop = O->bad_f = O->bad_jac = kNoStep;
-      O->picard_fail = O->any_fail = 0;
-      O->dmax_bits = 0ull;
-    }
 
-    // ---------------- phase B: carry-in, replay, bookkeeping -------------
+    // ---------------- phase B(it): carry-in, replay, bookkeeping ----------
+    ST *Gn = cur ? A.G0 : A.G1;
     {
       const double *ag = A.agg + (size_t)(it & 1) * A.nblocks * E::W;
       const int per = (b + kSolveThreads - 1) / kSolveThreads;
@@ -466,26 +486,16 @@ deer_persistent(SolveArgs<ST> A) {
         if (af) atomicAdd(&s_cnt[1], af);
         atomicMax(&s_dm, dmb);
       }
+      __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) {
         if (s_cnt[1]) atomicAdd(&S->any_fail, s_cnt[1]);
         atomicMax(&S->dmax_bits, s_dm);
+        st_release(A.ready + b, it + 1);  // rows of guess_{it+1} from this CTA are visible
       }
     }
-    grid_sync(A.ctl, (unsigned)A.nblocks, gen);
-
     ++it;
-    const unsigned gaf = vload(&S->any_fail);
-    const double dmax = __longlong_as_double((long long)vload(&S->dmax_bits));
-    if (b == 0 && threadIdx.x == 0) A.hist[it - 1] = dmax;
-    if (!have_d0) { d0 = dmax; have_d0 = true; }
     cur ^= 1;
-    g_dmax = dmax;
-    if (d0 > 0.0 && dmax > 1e6 * d0) {
-      status = CS_RUN_DIVERGED; stop = CS_STOP_ERROR; err_kind = CS_DIV_GUARD; err_step = -1; err_iter = it;
-      break;
-    }
-    if (gaf == 0) { status = CS_RUN_CONVERGED; stop = CS_STOP_NOFAIL; break; }
   }
 
   if (b == 0 && threadIdx.x == 0) {
