@@ -119,6 +119,9 @@ typedef struct cs_deer_result {
 
 const char *cs_last_error(void);
 int cs_version(void);
+/* Development timing hook: the persistent solver stamps %globaltimer (ns) at
+ * 8 phase boundaries of each of its first n/8 iterations into dev_buf (NULL off). */
+int cs_debug_probe(unsigned long long *dev_buf, int n);
 int cs_device_sm_count(int *out);
 
 /* ---- counter-based noise (noise.py:50-80, 140-156, 159-171) ------------- */
@@ -207,6 +210,36 @@ int cs_system_block_jacobian(const cs_system *sys, int dtype, const int64_t *ts,
 /* sequential_evaluate (core.py:163-184) as one device-resident chain walk. */
 int cs_system_sequential(const cs_system *sys, int dtype, const void *s0, int64_t T,
                          void *out, int64_t *bad_step, void *stream);
+
+/* Per-iteration flags of the fused element builder (device struct). */
+typedef struct cs_elem_stats {
+  int64_t bad_proposal;          /* first step with a non-finite proposal, INT64_MAX none */
+  int64_t bad_step;              /* first step with non-finite f_t                       */
+  int64_t bad_jacobian;          /* first step with a non-finite Jacobian estimate        */
+  uint32_t picard_fail;          /* rows failing |f - guess| <= atol + rtol|f|             */
+  uint32_t fail_rows;            /* filled by cs_scan_*_update                             */
+  double dmax;                   /* filled by cs_scan_*_update (max |next - guess|)        */
+} cs_elem_stats;
+
+/* One fused pass over all T steps (deer.py:262-271 + 157-204): f_t at
+ * prev = [s0; guess[:-1]], finite checks, the Picard residual against guess,
+ * the Jacobian estimate for cfg->mode at `iteration` (Hutchinson probes hashed
+ * in-kernel), preconditioner / damping / clip and u = f - Jhat prev.  Writes
+ * the elements (diag: e0 = j; dense: e0 = J; block: e0..e3 = a,b,c,d; u) and
+ * resets/fills *d_stats (device). */
+int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtype, int64_t iteration,
+                       const void *s0, const void *guess, void *e0, void *e1, void *e2, void *e3,
+                       void *u, cs_elem_stats *d_stats, void *stream);
+/* Scans with the post-update bookkeeping fused into the replay (deer.py:273-277):
+ * rows of `out` that moved more than atol + rtol|out| from `guess` get
+ * last_fail[t] = iteration; d_stats->fail_rows / dmax are accumulated. */
+int cs_scan_diag_update(int dtype, const void *j, const void *u, const void *s0, void *out, int64_t T,
+                        int32_t D, void *ws, size_t ws_bytes, const void *guess, double atol, double rtol,
+                        int32_t iteration, int32_t *last_fail, cs_elem_stats *d_stats, void *stream);
+int cs_scan_block_update(int dtype, const void *a, const void *b, const void *c, const void *d,
+                         const void *u, const void *s0, void *out, int64_t T, int32_t D, void *ws,
+                         size_t ws_bytes, const void *guess, double atol, double rtol, int32_t iteration,
+                         int32_t *last_fail, cs_elem_stats *d_stats, void *stream);
 
 /* ---- whole-chain Newton solve (deer.py:230-328, run_deer, no window) ---- */
 /* One cooperative persistent kernel runs every Newton iteration on device:

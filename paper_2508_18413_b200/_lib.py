@@ -59,10 +59,17 @@ class cs_deer_result(ctypes.Structure):
                 ("steps_per_thread", i32), ("kept_in_registers", i32)]
 
 
+class cs_elem_stats(ctypes.Structure):
+    _fields_ = [("bad_proposal", i64), ("bad_step", i64), ("bad_jacobian", i64), ("picard_fail", ctypes.c_uint32),
+                ("fail_rows", ctypes.c_uint32), ("dmax", f64)]
+
+
 SP = ctypes.POINTER(cs_system)
+CP = ctypes.POINTER(cs_deer_config)
 _SIGS = {
     "cs_last_error": ([], ctypes.c_char_p),
     "cs_version": ([], ctypes.c_int),
+    "cs_debug_probe": ([P, ctypes.c_int], ctypes.c_int),
     "cs_device_sm_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "cs_noise_fill": ([ctypes.c_int, u64, u64, i64, i64, i32, f64, ctypes.c_int, P, P], ctypes.c_int),
     "cs_rademacher_fill": ([u64, i64, P, i64, i64, i32, i32, ctypes.c_int, P, P], ctypes.c_int),
@@ -86,6 +93,10 @@ _SIGS = {
     "cs_system_block_jacobian": ([SP, ctypes.c_int, P, i64, i64, P, i32, i64, P, P, P, P, P],
                                  ctypes.c_int),
     "cs_system_sequential": ([SP, ctypes.c_int, P, i64, P, P, P], ctypes.c_int),
+    "cs_system_elements": ([SP, CP, ctypes.c_int, i64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
+    "cs_scan_diag_update": ([ctypes.c_int, P, P, P, P, i64, i32, P, szt, P, f64, f64, i32, P, P, P], ctypes.c_int),
+    "cs_scan_block_update": ([ctypes.c_int, P, P, P, P, P, P, P, i64, i32, P, szt, P, f64, f64, i32, P, P, P],
+                             ctypes.c_int),
     "cs_deer_workspace_bytes": ([SP, ctypes.c_int, i32], szt),
     "cs_deer_supported": ([SP, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "cs_deer_solve": ([SP, ctypes.POINTER(cs_deer_config), ctypes.c_int, P, P, P, P, P, szt,

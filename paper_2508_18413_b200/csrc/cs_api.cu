@@ -217,6 +217,13 @@ __global__ void k_hutch(ST *est, const ST *z, const ST *jz, int64_t n, int first
 
 __global__ void k_set_i64(long long *p, long long v) { *p = v; }
 
+__global__ void k_init_stats(cs_elem_stats *s) {
+  s->bad_proposal = s->bad_step = s->bad_jacobian = kNoStep;
+  s->picard_fail = 0;
+  s->fail_rows = 0;
+  s->dmax = 0.0;
+}
+
 __global__ void k_init_ctl(SolveCtl *c, int *ready, int nready) {
   for (int i = threadIdx.x; i < nready; i += blockDim.x) ready[i] = 0;
   if (threadIdx.x != 0) return;
@@ -257,6 +264,14 @@ __global__ void k_finalize(const SolveCtl *c, ST *trace, const ST *G1, const ST 
 extern "C" {
 
 const char *cs_last_error(void) { return g_err.c_str(); }
+
+static unsigned long long *h_probe = nullptr;
+static int h_probe_n = 0;
+int cs_debug_probe(unsigned long long *dev_buf, int n) {
+  h_probe = dev_buf;
+  h_probe_n = dev_buf ? n : 0;
+  return CS_OK;
+}
 int cs_version(void) { return 1; }
 
 int cs_device_sm_count(int *out) {
@@ -526,6 +541,81 @@ int cs_system_sequential(const cs_system *sys, int dtype, const void *s0, int64_
   return syscall(sys, dtype, c, stream, "cs_system_sequential");
 }
 
+// ---- fused element builder + update scans (the streamed solver path) ---------------
+static int elem_width(const cs_system *sys) {
+  if (sys->kind == CS_SYS_GIBBS) return sys->dim == 18 ? 18 : 0;
+  if (sys->target.kind == CS_TARGET_BLR) return 0;
+  return elem_md(sys->kind, sys->target.kind, sys->dim);
+}
+
+int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtype, int64_t iteration,
+                       const void *s0, const void *guess, void *e0, void *e1, void *e2, void *e3, void *u,
+                       cs_elem_stats *d_stats, void *stream) {
+  if (!sys || !cfg || !d_stats) return fail(CS_ERR_CONFIG, "null argument");
+  if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
+  const int md = elem_width(sys);
+  if (!md) return fail(CS_ERR_CONFIG, "no fused element builder for this system");
+  if (cfg->mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG)
+    return fail(CS_ERR_CONFIG, "system does not provide a block2x2 Jacobian estimate");
+  cudaStream_t st = S(stream);
+  k_init_stats<<<1, 1, 0, st>>>(d_stats);
+  if (sys->T < 1) return CS_OK;
+  cudaError_t e;
+  if (dtype == CS_F64) {
+    SolveArgs<double> A{};
+    A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;
+    A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
+    A.pre = cfg->preconditioner; A.s0 = (const double *)s0; A.T = sys->T; A.D = sys->dim;
+    e = elements_dispatch(*sys, dtype, md, cfg->mode, &A, (int)iteration, guess, e0, e1, e2, e3, u, d_stats, st);
+  } else {
+    SolveArgs<float> A{};
+    A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;
+    A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
+    A.pre = cfg->preconditioner; A.s0 = (const float *)s0; A.T = sys->T; A.D = sys->dim;
+    e = elements_dispatch(*sys, dtype, md, cfg->mode, &A, (int)iteration, guess, e0, e1, e2, e3, u, d_stats, st);
+  }
+  if (e == cudaErrorNotSupported) return fail(CS_ERR_CONFIG, "element builder not instantiated for this system/mode");
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements");
+}
+
+static int do_scan_update(int var, int dtype, const void *e0, const void *e1, const void *e2, const void *e3,
+                          const void *u, const void *s0, void *out, int64_t T, int D, void *ws, size_t ws_bytes,
+                          const void *guess, double atol, double rtol, int it, int32_t *last_fail,
+                          cs_elem_stats *stats, void *stream) {
+  if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
+  if (T < 0 || D < 1 || D > 4096) return fail(CS_ERR_STRUCTURAL, "bad scan shape");
+  const ScanPlan p = scan_plan(var, dtype, T, D);
+  if (ws_bytes < p.ws_bytes) return fail(CS_ERR_CONFIG, "scan workspace too small");
+  if (T == 0) return CS_OK;
+  cudaError_t e;
+  if (dtype == CS_F64) {
+    ScanArgs<double> a{(const double *)e0, (const double *)e1, (const double *)e2, (const double *)e3,
+                       (const double *)u, (const double *)s0, (double *)out, T, D, (const double *)guess,
+                       atol, rtol, it, last_fail, stats};
+    e = launch_scan_t<double>(p, a, ws, S(stream), true);
+  } else {
+    ScanArgs<float> a{(const float *)e0, (const float *)e1, (const float *)e2, (const float *)e3,
+                      (const float *)u, (const float *)s0, (float *)out, T, D, (const float *)guess,
+                      atol, rtol, it, last_fail, stats};
+    e = launch_scan_t<float>(p, a, ws, S(stream), true);
+  }
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "scan update launch");
+}
+
+int cs_scan_diag_update(int dtype, const void *j, const void *u, const void *s0, void *out, int64_t T, int32_t D,
+                        void *ws, size_t ws_bytes, const void *guess, double atol, double rtol, int32_t iteration,
+                        int32_t *last_fail, cs_elem_stats *d_stats, void *stream) {
+  return do_scan_update(SCAN_DIAG, dtype, j, nullptr, nullptr, nullptr, u, s0, out, T, D, ws, ws_bytes, guess, atol,
+                        rtol, iteration, last_fail, d_stats, stream);
+}
+int cs_scan_block_update(int dtype, const void *a, const void *b, const void *c, const void *d, const void *u,
+                         const void *s0, void *out, int64_t T, int32_t D, void *ws, size_t ws_bytes,
+                         const void *guess, double atol, double rtol, int32_t iteration, int32_t *last_fail,
+                         cs_elem_stats *d_stats, void *stream) {
+  return do_scan_update(SCAN_BLOCK, dtype, a, b, c, d, u, s0, out, T, D, ws, ws_bytes, guess, atol, rtol,
+                        iteration, last_fail, d_stats, stream);
+}
+
 // ---- whole-chain solve ------------------------------------------------------------
 static int solver_width(const cs_system *sys) {
   if (sys->kind == CS_SYS_GIBBS) return sys->dim == 18 ? 18 : 0;
@@ -588,14 +678,14 @@ int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, co
     A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;
     A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
     A.pre = cfg->preconditioner; A.s0 = (const double *)s0; A.G0 = (double *)trace; A.G1 = (double *)G1;
-    A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ctl; A.agg = agg; A.ready = ready; A.T = T; A.D = D;
+    A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ctl; A.agg = agg; A.ready = ready; A.probe = h_probe; A.probe_n = h_probe_n; A.T = T; A.D = D;
     e = solve_dispatch(*sys, dtype, md, cfg->mode, &A, sms, st, &pick);
   } else {
     SolveArgs<float> A{};
     A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;
     A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
     A.pre = cfg->preconditioner; A.s0 = (const float *)s0; A.G0 = (float *)trace; A.G1 = (float *)G1;
-    A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ctl; A.agg = agg; A.ready = ready; A.T = T; A.D = D;
+    A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ctl; A.agg = agg; A.ready = ready; A.probe = h_probe; A.probe_n = h_probe_n; A.T = T; A.D = D;
     e = solve_dispatch(*sys, dtype, md, cfg->mode, &A, sms, st, &pick);
   }
   if (e == cudaErrorNotSupported) return fail(CS_ERR_CONFIG, "fused solver not instantiated for this system");

@@ -111,6 +111,108 @@ __global__ void k_sys_seq(cs_system s, const ST *s0, int64_t T, ST *out, long lo
   }
 }
 
+// One fused pass over all steps: f_t, finite checks, Picard residual, the
+// Jacobian estimate and the element (cs_system_elements).
+template <class Sys, int MODE, int MD, typename ST>
+__global__ void __launch_bounds__(kRowThreads)
+k_sys_elements(SolveArgs<ST> A, int iteration, const ST *guess, ST *e0, ST *e1, ST *e2, ST *e3, ST *u,
+               cs_elem_stats *stats) {
+  using E = Elem<MODE, MD>;
+  __shared__ long long smin[3];
+  __shared__ unsigned scnt;
+  if (threadIdx.x == 0) {
+    smin[0] = smin[1] = smin[2] = kNoStep;
+    scnt = 0;
+  }
+  __syncthreads();
+  const Sys sys = SysFactory<Sys>::make(A.sys);
+  const int D = A.D;
+  const int64_t r = (int64_t)blockIdx.x * kRowThreads + threadIdx.x;
+  long long bp = kNoStep, bf = kNoStep, bj = kNoStep;
+  unsigned pf = 0;
+  if (r < A.T) {
+    const int64_t t = r + 1;
+    double prev[MD], gr[MD];
+    load_row_ro<Sys, MD, ST>(sys, r == 0 ? A.s0 : guess + (r - 1) * D, prev);
+    load_row_ro<Sys, MD, ST>(sys, guess + r * D, gr);
+    typename Sys::Aux aux;
+    if (!sys.prepare(t, prev, aux)) bp = t;
+    double f[MD];
+    sys.f(aux, f);
+    bool fin = true, pfail = false;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      if (sys.mem_index(i) < 0) continue;
+      fin &= finite(f[i]);
+      pfail |= !(fabs(f[i] - gr[i]) <= A.atol + A.rtol * fabs(f[i]));
+    }
+    if (!fin) bf = t;
+    pf = pfail ? 1u : 0u;
+    E e;
+    bool jok;
+    build_elem<Sys, MODE, MD, ST>(sys, aux, prev, f, t, iteration, A, e, jok);
+    if (!jok) bj = t;
+    if constexpr (MODE == CS_MODE_DIAG) {
+#pragma unroll
+      for (int k = 0; k < MD; ++k) {
+        const int m = sys.mem_index(k);
+        if (m >= 0) { e0[r * D + m] = (ST)e.j(k); u[r * D + m] = (ST)e.u(k); }
+      }
+    } else if constexpr (MODE == CS_MODE_DENSE) {
+#pragma unroll
+      for (int a = 0; a < MD; ++a) {
+        const int ma = sys.mem_index(a);
+        if (ma < 0) continue;
+        u[r * D + ma] = (ST)e.u(a);
+#pragma unroll
+        for (int c = 0; c < MD; ++c) {
+          const int mc = sys.mem_index(c);
+          if (mc >= 0) e0[(r * D + ma) * D + mc] = (ST)e.M(a, c);
+        }
+      }
+    } else {
+      constexpr int H = MD / 2;
+      const int n = D / 2;
+#pragma unroll
+      for (int i = 0; i < H; ++i)
+        if (i < n) {
+          e0[r * n + i] = (ST)e.ba(i);
+          e1[r * n + i] = (ST)e.bb(i);
+          e2[r * n + i] = (ST)e.bc(i);
+          e3[r * n + i] = (ST)e.bd(i);
+          u[r * D + i] = (ST)e.u(i);
+          u[r * D + n + i] = (ST)e.u(H + i);
+        }
+    }
+  }
+  bp = warp_min_i64(bp);
+  bf = warp_min_i64(bf);
+  bj = warp_min_i64(bj);
+  pf = (unsigned)warp_sum_i((int)pf);
+  if ((threadIdx.x & 31) == 0) {
+    if (bp != kNoStep) atomicMin(&smin[0], bp);
+    if (bf != kNoStep) atomicMin(&smin[1], bf);
+    if (bj != kNoStep) atomicMin(&smin[2], bj);
+    if (pf) atomicAdd(&scnt, pf);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (smin[0] != kNoStep) atomicMin((long long *)&stats->bad_proposal, smin[0]);
+    if (smin[1] != kNoStep) atomicMin((long long *)&stats->bad_step, smin[1]);
+    if (smin[2] != kNoStep) atomicMin((long long *)&stats->bad_jacobian, smin[2]);
+    if (scnt) atomicAdd(&stats->picard_fail, scnt);
+  }
+}
+
+template <class Sys, int MODE, int MD, typename ST>
+cudaError_t launch_elements(SolveArgs<ST> A, int iteration, const void *guess, void *e0, void *e1, void *e2,
+                            void *e3, void *u, cs_elem_stats *stats, cudaStream_t st) {
+  const unsigned grid = (unsigned)((A.T + kRowThreads - 1) / kRowThreads);
+  k_sys_elements<Sys, MODE, MD, ST><<<grid, kRowThreads, 0, st>>>(A, iteration, (const ST *)guess, (ST *)e0,
+                                                                    (ST *)e1, (ST *)e2, (ST *)e3, (ST *)u, stats);
+  return cudaGetLastError();
+}
+
 struct SysCall {
   int op;  // 0 step, 1 jvp, 2 block, 3 sequential
   const int64_t *ts;

@@ -5,4 +5,6 @@
 namespace cs {
 cudaError_t syscall_gibbs(const cs_system &, int dtype, int md, const SysCall &, cudaStream_t);
 cudaError_t solve_gibbs(int dtype, int md, int mode, void *args, int sms, cudaStream_t, SolvePick *);
+cudaError_t elements_gibbs(int dtype, int md, int mode, void *args, int it, const void *g, void *e0, void *e1,
+                           void *e2, void *e3, void *u, cs_elem_stats *stats, cudaStream_t st);
 }  // namespace cs

@@ -153,7 +153,7 @@ CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF ex
 
 // ---------------------------------------------------------------------------
 // narrow rows: tile = R consecutive rows x all columns, staged in smem
-template <typename ST, int VAR, bool AGG_ONLY = false>
+template <typename ST, int VAR, bool AGG_ONLY = false, bool UPDATE = false>
 __global__ void __launch_bounds__(kScanThreads)
 scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int win) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -178,6 +178,8 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int win) {
   const int nel = rows * ncol;
   ST *tile = (ST *)smem_raw;  // NA arrays of R*ncol
   double *segagg = (double *)(smem_raw + ((sizeof(ST) * NA * R * ncol + 15) / 16) * 16);
+  // UPDATE: one fail flag per row, after the segment aggregates
+  int *s_fail = (int *)(segagg + (kScanThreads / ncol + 1) * ncol * W);
   const ST *u_src = a.u + 2 * row0 * ncol * (VAR == SCAN_BLOCK) + row0 * ncol * (VAR == SCAN_DIAG);
 
   // ---- stage the tile: one bulk (TMA) copy per array when aligned, else LDG loop
@@ -291,6 +293,20 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int win) {
   if (threadIdx.x == 0) st_release(ws.status + b, 2);
 
   // replay from the segment entry state; results overwrite the staged tile
+  unsigned long long dmb = 0ull;
+  if constexpr (UPDATE) {
+    for (int r = threadIdx.x; r < rows; r += kScanThreads) s_fail[r] = 0;
+    __syncthreads();
+  }
+  auto check = [&](int r, int col, double xv) {  // deer.py:273-275 on the stored value
+    if constexpr (UPDATE) {
+      const double xd = (double)(ST)xv;
+      const double gap = fabs(xd - (double)a.guess[(row0 + r) * SW + col]);
+      if (gap > a.atol + a.rtol * fabs(xd)) s_fail[r] = 1;
+      const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
+      dmb = gb > dmb ? gb : dmb;
+    }
+  };
   if (active && r0 < r1) {
     ColElem<VAR> pre;
     pre.load(segagg + (sg * ncol + c) * W);
@@ -301,6 +317,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int win) {
         const int i = r * ncol + c;
         x = (double)tile[i] * x + (double)tile[R * ncol + i];
         tile[i] = (ST)x;
+        check(r, c, x);
       }
     } else {
       double x = s_entry[c], v = s_entry[ncol + c];
@@ -316,7 +333,32 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int win) {
         // [x | v] rows overwrite the u tile in place (same thread, same slots)
         tile[4 * R * ncol + 2 * r * ncol + c] = (ST)x;
         tile[4 * R * ncol + 2 * r * ncol + ncol + c] = (ST)v;
+        check(r, c, x);
+        check(r, ncol + c, v);
       }
+    }
+  }
+  if constexpr (UPDATE) {
+    __shared__ unsigned s_nf;
+    __shared__ unsigned long long s_dm;
+    if (threadIdx.x == 0) { s_nf = 0; s_dm = 0ull; }
+    __syncthreads();
+    unsigned nf = 0;
+    for (int r = threadIdx.x; r < rows; r += kScanThreads)
+      if (s_fail[r]) {
+        a.last_fail[row0 + r] = a.it;
+        ++nf;
+      }
+    nf = (unsigned)warp_sum_i((int)nf);
+    dmb = warp_max_u64(dmb);
+    if ((threadIdx.x & 31) == 0) {
+      if (nf) atomicAdd(&s_nf, nf);
+      atomicMax(&s_dm, dmb);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_nf) atomicAdd(&a.stats->fail_rows, s_nf);
+      atomicMax((unsigned long long *)&a.stats->dmax, s_dm);
     }
   }
   const ST *src = VAR == SCAN_DIAG ? tile : tile + 4 * R * ncol;
@@ -341,7 +383,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int win) {
 // wide rows (D > 64): tile = 64 rows x 32 columns, one column per lane,
 // 8 row segments of 8 rows kept in registers.
 constexpr int kWideSeg = 8;
-template <typename ST, int VAR, bool AGG_ONLY = false>
+template <typename ST, int VAR, bool AGG_ONLY = false, bool UPDATE = false>
 __global__ void __launch_bounds__(kScanThreads)
 scan_cols(ScanArgs<ST> a, LookbackWs ws) {
   constexpr int W = ColElem<VAR>::W;
@@ -430,6 +472,21 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
   __syncthreads();
   if (threadIdx.x == 0) st_release(ws.status + tk, 2);
 
+  __shared__ int s_fail[64];
+  if constexpr (UPDATE) {
+    if (threadIdx.x < 64) s_fail[threadIdx.x] = 0;
+    __syncthreads();
+  }
+  unsigned long long dmb = 0ull;
+  auto check = [&](int k, int64_t r, int64_t idx, double xv) {
+    if constexpr (UPDATE) {
+      const double xd = (double)(ST)xv;
+      const double gap = fabs(xd - (double)a.guess[idx]);
+      if (gap > a.atol + a.rtol * fabs(xd)) s_fail[s * kWideSeg + k] = 1;
+      const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
+      dmb = gb > dmb ? gb : dmb;
+    }
+  };
   ColElem<VAR> pre;
   pre.load(segagg[s][lane]);
   double x = s_entry[lane], v = VAR == SCAN_BLOCK ? s_entry[32 + lane] : 0.0;
@@ -442,6 +499,7 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
     if constexpr (VAR == SCAN_DIAG) {
       x = ej[k] * x + eu[k];
       a.out[r * ncol + c] = (ST)x;
+      check(k, r, r * ncol + c, x);
     } else {
       const double xa = ej[k] * x + eb[k] * v + eu[k];
       const double va = ec[k] * x + ed[k] * v + ev[k];
@@ -449,6 +507,28 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
       v = va;
       a.out[r * 2 * ncol + c] = (ST)x;
       a.out[r * 2 * ncol + ncol + c] = (ST)v;
+      check(k, r, r * 2 * ncol + c, x);
+      check(k, r, r * 2 * ncol + ncol + c, v);
+    }
+  }
+  if constexpr (UPDATE) {
+    __shared__ unsigned s_nf;
+    __shared__ unsigned long long s_dm;
+    if (threadIdx.x == 0) { s_nf = 0; s_dm = 0ull; }
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      const int64_t r = rb * 64 + threadIdx.x;
+      if (r < a.T && s_fail[threadIdx.x]) {
+        a.last_fail[r] = a.it;
+        atomicAdd(&s_nf, 1u);
+      }
+    }
+    dmb = warp_max_u64(dmb);
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_dm, dmb);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_nf) atomicAdd(&a.stats->fail_rows, s_nf);
+      atomicMax((unsigned long long *)&a.stats->dmax, s_dm);
     }
   }
 }
@@ -755,7 +835,7 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
     const int NA = var == SCAN_DIAG ? 2 : 6;
     const int nseg = kScanThreads / D;
     const int W = var == SCAN_DIAG ? 2 : 6;
-    p.smem = ((size_t)esz * NA * p.R * D + 15) / 16 * 16 + sizeof(double) * (nseg + 1) * D * W;
+    p.smem = ((size_t)esz * NA * p.R * D + 15) / 16 * 16 + sizeof(double) * (nseg + 1) * D * W + sizeof(int) * p.R;
     // walker window: aggregates [win][D][W] + chunk scratch [nseg][D][W] within the same smem
     const size_t chunk_bytes = sizeof(double) * (size_t)nseg * D * W;
     int win = (int)((p.smem - chunk_bytes) / (sizeof(double) * D * W));
@@ -789,8 +869,15 @@ LookbackWs carve_ws(const ScanPlan &p, void *ws, int D) {
   return w;
 }
 
+template <typename ST, int VAR, bool UPD>
+static void launch_rows(const ScanPlan &p, const ScanArgs<ST> &a, LookbackWs w, cudaStream_t st) {
+  auto k = scan_rows<ST, VAR, false, UPD>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  k<<<(unsigned)p.ntiles, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
+}
+
 template <typename ST>
-cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st) {
+cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update) {
   LookbackWs w = carve_ws(p, ws, a.D);
   // ticket + status must start at zero for every launch
   cudaError_t e = cudaMemsetAsync(ws, 0, (unsigned char *)w.agg - (unsigned char *)ws, st);
@@ -799,15 +886,20 @@ cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStrea
   const unsigned grid = (unsigned)p.ntiles;
   if (p.kind == 0) {
     if (p.var == SCAN_DIAG) {
-      cudaFuncSetAttribute(scan_rows<ST, SCAN_DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      scan_rows<ST, SCAN_DIAG><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
+      if (update) launch_rows<ST, SCAN_DIAG, true>(p, a, w, st);
+      else launch_rows<ST, SCAN_DIAG, false>(p, a, w, st);
     } else {
-      cudaFuncSetAttribute(scan_rows<ST, SCAN_BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      scan_rows<ST, SCAN_BLOCK><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
+      if (update) launch_rows<ST, SCAN_BLOCK, true>(p, a, w, st);
+      else launch_rows<ST, SCAN_BLOCK, false>(p, a, w, st);
     }
   } else if (p.kind == 1) {
-    if (p.var == SCAN_DIAG) scan_cols<ST, SCAN_DIAG><<<grid, kScanThreads, 0, st>>>(a, w);
-    else scan_cols<ST, SCAN_BLOCK><<<grid, kScanThreads, 0, st>>>(a, w);
+    if (p.var == SCAN_DIAG) {
+      if (update) scan_cols<ST, SCAN_DIAG, false, true><<<grid, kScanThreads, 0, st>>>(a, w);
+      else scan_cols<ST, SCAN_DIAG><<<grid, kScanThreads, 0, st>>>(a, w);
+    } else {
+      if (update) scan_cols<ST, SCAN_BLOCK, false, true><<<grid, kScanThreads, 0, st>>>(a, w);
+      else scan_cols<ST, SCAN_BLOCK><<<grid, kScanThreads, 0, st>>>(a, w);
+    }
   } else {
     switch (p.md) {
       case 1: scan_dense_small<ST, 1, 4><<<grid, kScanThreads, 0, st>>>(a, w); break;
@@ -859,9 +951,9 @@ cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, doub
   return cudaGetLastError();
 }
 
-template cudaError_t launch_scan_t<float>(const ScanPlan &, ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_scan_t<float>(const ScanPlan &, ScanArgs<float>, void *, cudaStream_t, bool);
 template cudaError_t launch_aggregate_t<float>(const ScanPlan &, ScanArgs<float>, void *, double *, cudaStream_t);
 template cudaError_t launch_aggregate_t<double>(const ScanPlan &, ScanArgs<double>, void *, double *, cudaStream_t);
-template cudaError_t launch_scan_t<double>(const ScanPlan &, ScanArgs<double>, void *, cudaStream_t);
+template cudaError_t launch_scan_t<double>(const ScanPlan &, ScanArgs<double>, void *, cudaStream_t, bool);
 
 }  // namespace cs

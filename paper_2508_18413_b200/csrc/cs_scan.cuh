@@ -13,6 +13,12 @@ struct ScanArgs {
   ST *out;
   int64_t T;
   int D;                        // diag/dense: state dim; block: half (position) dim
+  // fused post-update bookkeeping (deer.py:273-277), used by the *_update scans
+  const ST *guess;
+  double atol, rtol;
+  int it;
+  int32_t *last_fail;
+  cs_elem_stats *stats;
 };
 
 struct ScanPlan {
@@ -24,7 +30,7 @@ struct ScanPlan {
 
 ScanPlan scan_plan(int var, int dtype, int64_t T, int D);
 template <typename ST>
-cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st);
+cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update = false);
 template <typename ST>
 cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, double *out, cudaStream_t st);
 

@@ -61,6 +61,8 @@ struct SolveArgs {
   SolveCtl *ctl;
   double *agg;  // [2][nblocks][W]
   int *ready;   // [nblocks] iterate stamp: rows of guess_it written by CTA b
+  unsigned long long *probe;  // cs_debug_probe buffer or null
+  int probe_n;
   int64_t T;
   int D, seg, nblocks;
 };
@@ -247,6 +249,16 @@ CS_D void grid_sync(SolveCtl *c, unsigned nblocks, unsigned &target) {
 
 template <typename T> CS_D T vload(const T *p) { return *((const volatile T *)p); }
 
+// timing probe (cs_debug_probe): CTA 0 / thread 0 stamps %globaltimer at the
+// phase boundaries of the first iterations; null = off
+CS_D void probe_stamp(unsigned long long *buf, int n, int it, int k) {
+  if (buf && blockIdx.x == 0 && threadIdx.x == 0 && it * 8 + k < n) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    buf[it * 8 + k] = t;
+  }
+}
+
 // ---------------------------------------------------------------------------
 template <class Sys, int MODE, int MD, typename ST, bool KEEP>
 __global__ void __launch_bounds__(kSolveThreads)
@@ -288,12 +300,14 @@ deer_persistent(SolveArgs<ST> A) {
     }
     // ---------------- phase A(it): f, Picard, elements, segment fold -------
     // the halo row guess_it[row0-1] of CTA b's first thread was written by CTA b-1
+    probe_stamp(A.probe, A.probe_n, it, 0);
     if (it > 0 && threadIdx.x == 0 && b > 0) {
       const int *rd = A.ready + (b - 1);
       while (ld_acquire(rd) < it) {
       }
     }
     __syncthreads();
+    probe_stamp(A.probe, A.probe_n, it, 1);
     E agg;
     agg.ident();
     long long bp = kNoStep, bf = kNoStep, bj = kNoStep;
@@ -345,6 +359,7 @@ deer_persistent(SolveArgs<ST> A) {
 #pragma unroll
       for (int i = 0; i < MD; ++i) prev[i] = gr[i];
     }
+    probe_stamp(A.probe, A.probe_n, it, 2);
     E total;
     block_scan(agg, excl, total, s_warp);
     if (threadIdx.x == 0) {
@@ -371,7 +386,9 @@ deer_persistent(SolveArgs<ST> A) {
     }
     // the ONE grid barrier of the iteration: it publishes pass it's aggregates
     // and flags together with update it-1's fail count and delta_max
+    probe_stamp(A.probe, A.probe_n, it, 3);
     grid_sync(A.ctl, (unsigned)A.nblocks, target);
+    probe_stamp(A.probe, A.probe_n, it, 4);
     if (b == 0 && threadIdx.x == 0) {
       SolveSlot *O = &A.ctl->slot[(it + 2) & 3];
       O->bad_prop = O->bad_f = O->bad_jac = kNoStep;
@@ -419,6 +436,7 @@ deer_persistent(SolveArgs<ST> A) {
       }
       E fex, ftot;
       block_scan(fold, fex, ftot, s_warp);
+      probe_stamp(A.probe, A.probe_n, it, 5);
       double x[MD];
 #pragma unroll
       for (int i = 0; i < MD; ++i) x[i] = s0r[i];
@@ -494,6 +512,7 @@ deer_persistent(SolveArgs<ST> A) {
         st_release(A.ready + b, it + 1);  // rows of guess_{it+1} from this CTA are visible
       }
     }
+    probe_stamp(A.probe, A.probe_n, it, 6);
     ++it;
     cur ^= 1;
   }

@@ -46,7 +46,9 @@ def default_max_iters(T: int) -> int:
 @dataclass
 class DeerConfig:
     """Solver knobs (deer.py:55-93).  ``workers``/``chunk`` are accepted for API
-    compatibility; ``fused`` = False forces the host-driven path."""
+    compatibility.  ``engine`` picks the realisation: "fused" (one persistent
+    kernel), "streamed" (fused element builder + update scan per iteration),
+    "host" (generic host-driven loop) or "auto"."""
 
     mode: str = "dense"
     atol: float = 1e-4
@@ -60,7 +62,7 @@ class DeerConfig:
     preconditioner: np.ndarray | None = None
     workers: int | None = None
     chunk: int | None = None
-    fused: bool = True
+    engine: str = "auto"
 
     def __post_init__(self):
         if self.mode not in JACOBIAN_MODES:
@@ -77,6 +79,8 @@ class DeerConfig:
             raise ConfigurationError("clip must be positive")
         if self.window_len is not None and self.window_len < 1:
             raise ConfigurationError("window_len must be >= 1")
+        if self.engine not in ("auto", "fused", "streamed", "host"):
+            raise ConfigurationError(f"unknown engine {self.engine!r}")
         if self.preconditioner is not None:
             p = np.asarray(self.preconditioner.cpu() if torch.is_tensor(self.preconditioner)
                            else self.preconditioner, float)
@@ -262,17 +266,41 @@ def _bookkeeping(guess, nxt, atol, rtol, iteration, last_fail, sc):
     return int(vals[0]), float(vals[1])
 
 
-def _fused_ok(system, cfg):
-    desc_fn = getattr(system, "desc", None)
-    if not cfg.fused or desc_fn is None or cfg.full_trace:
+def _builtin_ok(system, cfg):
+    """Built-in system on the register kernels, no window / full trace."""
+    if getattr(system, "desc", None) is None or cfg.full_trace or not getattr(system, "kernels", False):
         return False
     if cfg.window_len is not None and cfg.window_len < system.T:
         return False
-    if getattr(system, "leapfrog_mode", "sequential") == "parallel":
+    return getattr(system, "leapfrog_mode", "sequential") != "parallel"
+
+
+def _fused_ok(system, cfg):
+    if not _builtin_ok(system, cfg):
         return False
-    d = desc_fn()
+    d = system.desc()
     return bool(_lib.load().cs_deer_supported(ctypes.byref(d), _MODE_CODE[cfg.mode],
                                               _lib.dtype_code(system.dtype)))
+
+
+# persistent kernel while a thread's steps stay few (elements kept in shared
+# memory); beyond that the streamed engine keeps every thread on one step
+_FUSED_MAX_T = 1 << 18
+
+
+def _pick_engine(system, cfg):
+    if cfg.engine == "host":
+        return "host"
+    fused, builtin = _fused_ok(system, cfg), _builtin_ok(system, cfg)
+    if cfg.engine == "fused":
+        return "fused" if fused else ("streamed" if builtin else "host")
+    if cfg.engine == "streamed":
+        return "streamed" if builtin else "host"
+    if fused and system.T <= _FUSED_MAX_T and getattr(system, "_kind", -1) != _lib.CS_SYS_GIBBS:
+        return "fused"
+    if builtin:
+        return "streamed"
+    return "host"
 
 
 def _run_fused(system, s0, cfg, max_iters):
@@ -335,9 +363,136 @@ def run_deer(system: TransitionSystem, s0, cfg: DeerConfig) -> DeerResult:
         raise StructuralError(f"s0 must have shape ({system.dim},), got {tuple(s0.shape)}")
     T = system.T
     max_iters = cfg.max_iters if cfg.max_iters is not None else default_max_iters(T)
-    if _fused_ok(system, cfg):
+    engine = _pick_engine(system, cfg)
+    if engine == "fused":
         return _run_fused(system, s0, cfg, max_iters)
+    if engine == "streamed":
+        try:
+            return _run_streamed(system, s0, cfg, max_iters)
+        except _NotInstantiated:
+            pass
     return _run_host(system, s0, cfg, max_iters)
+
+
+class _NotInstantiated(Exception):
+    pass
+
+
+_STATS_BYTES = 40
+
+
+def _parse_stats(buf):
+    raw = buf.cpu().numpy().tobytes()
+    bad_prop, bad_step, bad_jac = np.frombuffer(raw[:24], dtype=np.int64)
+    picard, fail_rows = np.frombuffer(raw[24:32], dtype=np.uint32)
+    dmax = float(np.frombuffer(raw[32:40], dtype=np.float64)[0])
+    return int(bad_prop), int(bad_step), int(bad_jac), int(picard), int(fail_rows), dmax
+
+
+def _run_streamed(system, s0, cfg, max_iters):
+    """Per iteration: the fused element builder (f, checks, Picard, Jacobian
+    estimate, elements in one pass), the scan with the bookkeeping fused into its
+    replay, and ONE 40-byte read-back that decides the branch (deer.py:261-286)."""
+    lib = _lib.load()
+    T, D = system.T, system.dim
+    dev, dtype = system.device, system.dtype
+    dt = _lib.dtype_code(dtype)
+    st = _lib.stream_ptr()
+    d = system.desc()
+    c = _lib.cs_deer_config()
+    c.mode = _MODE_CODE[cfg.mode]
+    c.atol, c.rtol = float(cfg.atol), float(cfg.rtol)
+    c.max_iters = int(max_iters)
+    c.hutchinson_samples = int(cfg.hutchinson_samples)
+    c.damping, c.clip = float(cfg.damping), float(cfg.clip)
+    pre = _pre_tensor(cfg, dev)
+    c.preconditioner = 0 if pre is None else pre.data_ptr()
+    mode = cfg.mode
+    if mode == "diag-stochastic":
+        E = [torch.empty((T, D), dtype=dtype, device=dev)]
+    elif mode == "dense":
+        E = [torch.empty((T, D, D), dtype=dtype, device=dev)]
+    else:
+        E = [torch.empty((T, D // 2), dtype=dtype, device=dev) for _ in range(4)]
+    u = torch.empty((T, D), dtype=dtype, device=dev)
+    eptr = [_lib.ptr(x) for x in E] + [_lib.ptr(None)] * (4 - len(E))
+    half = D // 2 if mode == "block2x2-stochastic" else D
+    ws_bytes = lib.cs_scan_workspace_bytes(c.mode, dt, T, half)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    stats = torch.zeros(_STATS_BYTES, dtype=torch.uint8, device=dev)
+    sptr = _lib.ptr(stats)
+    guess = s0.expand(T, D).clone()
+    nxt = torch.empty_like(guess)
+    last_fail = torch.zeros(T, dtype=torch.int32, device=dev)
+    backup = torch.empty_like(last_fail)
+    hist, d0, it, done = [], None, 0, False
+    launches = 0
+    nfail, picard = 1, 1
+    while True:
+        rc = lib.cs_system_elements(ctypes.byref(d), ctypes.byref(c), dt, it, _lib.ptr(s0), _lib.ptr(guess),
+                                    *eptr, _lib.ptr(u), sptr, st)
+        if rc == _lib.CS_ERR_CONFIG and it == 0:
+            raise _NotInstantiated()
+        _lib.check(rc)
+        launches += 2
+        counted = it < max_iters
+        if counted:
+            backup.copy_(last_fail)
+            if mode == "diag-stochastic":
+                rc = lib.cs_scan_diag_update(dt, eptr[0], _lib.ptr(u), _lib.ptr(s0), _lib.ptr(nxt), T, D,
+                                             _lib.ptr(ws), ws_bytes, _lib.ptr(guess), c.atol, c.rtol, it + 1,
+                                             _lib.ptr(last_fail), sptr, st)
+            elif mode == "block2x2-stochastic":
+                rc = lib.cs_scan_block_update(dt, *eptr, _lib.ptr(u), _lib.ptr(s0), _lib.ptr(nxt), T, half,
+                                              _lib.ptr(ws), ws_bytes, _lib.ptr(guess), c.atol, c.rtol, it + 1,
+                                              _lib.ptr(last_fail), sptr, st)
+            else:
+                rc = lib.cs_scan_dense(dt, eptr[0], _lib.ptr(u), _lib.ptr(s0), _lib.ptr(nxt), T, D, _lib.ptr(ws),
+                                       ws_bytes, st)
+                _lib.check(rc)
+                base = stats.data_ptr()
+                rc = lib.cs_update_bookkeeping(dt, _lib.ptr(guess), _lib.ptr(nxt), T, D, c.atol, c.rtol, it + 1,
+                                               _lib.ptr(last_fail), ctypes.c_void_p(base + 28),
+                                               ctypes.c_void_p(base + 32), st)
+            _lib.check(rc)
+            launches += 2
+        bad_prop, bad_step, bad_jac, picard, nfail, dmax = _parse_stats(stats)
+        if bad_prop != _NO_STEP:
+            raise ChainDivergedError(f"non-finite {getattr(system, '_what', 'proposal')} at step {bad_prop}",
+                                     step=bad_prop)
+        if bad_step != _NO_STEP:
+            raise ChainDivergedError(f"non-finite step value at step {bad_step} (iteration {it + 1})",
+                                     step=bad_step, iteration=it + 1)
+        if picard == 0:
+            done = True
+            if counted:
+                last_fail.copy_(backup)
+            break
+        if not counted:
+            break
+        if bad_jac != _NO_STEP:
+            raise ChainDivergedError(f"non-finite jacobian at step {bad_jac} (iteration {it + 1})",
+                                     step=bad_jac, iteration=it + 1)
+        it += 1
+        hist.append(dmax)
+        guess, nxt = nxt, guess
+        if d0 is None:
+            d0 = dmax
+        _guard(dmax, d0, it)
+        if nfail == 0:
+            done = True
+            break
+    nofail_stop = done and picard != 0 and nfail == 0
+    system.n_step_evals += T * (it if nofail_stop else it + 1)
+    if mode == "diag-stochastic":
+        system.n_jvp_evals += T * cfg.hutchinson_samples * it
+    elif mode == "dense":
+        system.n_jvp_evals += T * D * it
+    else:
+        system.n_hvp_evals += T * cfg.hutchinson_samples * it
+    return DeerResult(trace=guess, iterations=it, delta_history=np.array(hist), converged=done,
+                      per_step_converged_at=last_fail + 1, full_trace=None,
+                      stats={"path": "streamed", "launches": launches})
 
 
 def _run_host(system, s0, cfg, max_iters):

@@ -273,15 +273,43 @@ def test_run_deer_gibbs(cuda_device, dtype):
     _deer_cmp(r, g, "diag3_", dtype)
 
 
-def test_run_deer_host_path_matches_fused(cuda_device):
+@pytest.mark.parametrize("mode,kw", [("diag-stochastic", dict(clip=1.0)), ("dense", dict(damping=0.5, clip=1.0))])
+def test_engines_agree(cuda_device, mode, kw):
     m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
     k = cs.HmcKernel(m, 0.5, 8, seed=0, T=3000)
-    a = cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="diag-stochastic", clip=1.0))
-    b = cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="diag-stochastic", clip=1.0, fused=False))
-    assert a.stats["path"] == "fused" and b.stats["path"] == "host"
-    assert a.iterations == b.iterations
-    np.testing.assert_allclose(np_(a.trace), np_(b.trace), atol=1e-10)
-    np.testing.assert_array_equal(np_(a.per_step_converged_at), np_(b.per_step_converged_at))
+    runs = {e: cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode=mode, engine=e, **kw))
+            for e in ("fused", "streamed", "host")}
+    for e, r in runs.items():
+        assert r.stats["path"] == e
+    a = runs["fused"]
+    for e in ("streamed", "host"):
+        b = runs[e]
+        assert a.iterations == b.iterations and a.converged == b.converged
+        np.testing.assert_allclose(np_(a.trace), np_(b.trace), atol=1e-10)
+        np.testing.assert_array_equal(np_(a.per_step_converged_at), np_(b.per_step_converged_at))
+        np.testing.assert_allclose(a.delta_history, b.delta_history, rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_streamed_engine_golden(cuda_device, dtype):
+    g = golden("gibbs_schools")
+    k = cs.GibbsKernel(cs.generate_eight_schools(), seed=0, T=3000, dtype=dtype)
+    cfg = cs.DeerConfig(mode="diag-stochastic", hutchinson_samples=3, preconditioner=k.recommended_preconditioner(),
+                        max_iters=400, engine="streamed")
+    r = cs.run_deer(k, g["s0"], cfg)
+    assert r.stats["path"] == "streamed"
+    _deer_cmp(r, g, "diag3_", dtype)
+    g = golden("hmc_rosen2d")
+    m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
+    k = cs.HmcKernel(m, 0.5, 8, seed=0, T=5000, dtype=dtype)
+    _deer_cmp(cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="diag-stochastic", clip=1.0, engine="streamed")),
+              g, "diagclip_", dtype)
+    _deer_cmp(cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode="dense", damping=0.5, clip=1.0, atol=1e-6, rtol=1e-5,
+                                                        engine="streamed")), g, "dense_", dtype)
+    # leapfrog block elements through the streamed engine (test_deer.py:250-261 one-shot)
+    lf = cs.LeapfrogSystem(cs.model_logp_grad_hvp(cs.std_normal(2)), 0.1, 64, dtype=dtype)
+    r = cs.run_deer(lf, np.array([1.0, -0.5, 0.3, 0.8]), cs.DeerConfig(mode="block2x2-stochastic", engine="streamed"))
+    assert r.stats["path"] == "streamed" and r.converged and r.iterations == 1
 
 
 def test_run_deer_leapfrog_block_and_window(cuda_device):

@@ -31,12 +31,12 @@ def main():
     ap.add_argument("--T", type=int, nargs="+", default=[100_000])
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--host", action="store_true")
+    ap.add_argument("--engine", default="auto")
     a = ap.parse_args()
     dtype = torch.float32 if a.dtype == "f32" else torch.float64
     for T in a.T:
         k, s0, cfg = make(a.cfg, T, dtype)
-        cfg.fused = not a.host
+        cfg.engine = a.engine
         r = cs.run_deer(k, s0, cfg)
         torch.cuda.synchronize()
         ts = []
