@@ -285,7 +285,9 @@ cudaError_t launch_solve(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *p
     seg = (T + cap * kSolveThreads - 1) / (cap * kSolveThreads);
   }
   if (seg < 1) seg = 1;
-  const int64_t nb = (T + (int64_t)kSolveThreads * seg - 1) / ((int64_t)kSolveThreads * seg);
+  // every co-resident CTA gets an equal contiguous share (at most seg steps per thread)
+  int64_t nb = (T + kSolveThreads - 1) / kSolveThreads;
+  if (nb > cap) nb = cap;
   A.seg = (int)seg;
   A.nblocks = (int)(nb < 1 ? 1 : nb);
   pick->nblocks = A.nblocks;

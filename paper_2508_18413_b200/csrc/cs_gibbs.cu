@@ -2,6 +2,151 @@
 #include "cs_dispatch.h"
 
 namespace cs {
+
+// ---------------------------------------------------------------------------
+// The eight-schools element builder with one 8-lane team per chain step
+// (lane = school).  The sweep (samplers.py:551-587) and its JVP (593-627) couple
+// schools only through sums over schools, which become 3-level xor butterflies
+// -- the same pairwise order numpy uses for 8 terms.  Each lane holds one
+// school's state, so 8x more threads carry the f64 dependency chains than in the
+// one-thread-per-step kernel, at a fraction of the registers.
+CS_D double team_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  return v;
+}
+
+template <typename ST>
+__global__ void __launch_bounds__(256)
+k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout, ST *uout, cs_elem_stats *stats) {
+  constexpr int S = 8, D = 18;
+  constexpr double kFloor = 1e-8;
+  __shared__ long long smin[3];
+  __shared__ unsigned scnt;
+  if (threadIdx.x == 0) {
+    smin[0] = smin[1] = smin[2] = kNoStep;
+    scnt = 0;
+  }
+  __syncthreads();
+  const double *prm = A.sys.gibbs;
+  const double nu0 = __ldg(prm + 0), tau0_sq = __ldg(prm + 1), mu0 = __ldg(prm + 2);
+  const double kappa0 = __ldg(prm + 3), alpha0 = __ldg(prm + 4), sigma0_sq = __ldg(prm + 5), n = __ldg(prm + 7);
+  const int sub = threadIdx.x & 7;
+  const int64_t r = ((int64_t)blockIdx.x * 256 + threadIdx.x) >> 3;
+  const bool valid = r < A.T;
+  const int64_t rr = valid ? r : 0;
+  const int64_t t = rr + 1;
+  const ST *prow = rr == 0 ? A.s0 : guess + (rr - 1) * D;
+  const ST *grow = guess + rr * D;
+  const ST *g_tau = (const ST *)A.sys.g_tau, *xi_mu = (const ST *)A.sys.xi_mu;
+  const ST *xi_theta = (const ST *)A.sys.xi_theta, *g_sigma = (const ST *)A.sys.g_sigma;
+  const double xbar = __ldg(prm + 8 + sub), ss = __ldg(prm + 8 + S + sub);
+  // prev state (tau^2 is never read by the sweep, samplers.py:543-548)
+  const double mu = (double)prow[1], th = (double)prow[2 + sub], sgraw = (double)prow[2 + S + sub];
+  const double gt = (double)g_tau[t], xm = (double)xi_mu[t];
+  const double xt = (double)xi_theta[t * S + sub], gs = (double)g_sigma[t * S + sub];
+  const bool raw_ok = sgraw > kFloor;
+  const double sg = fmax(sgraw, kFloor);
+  // ---- forward sweep
+  const double dm = th - mu;
+  const double q = team_sum(dm * dm);
+  const double sth = team_sum(th);
+  const double dmu0 = mu - mu0;
+  const double q_tau = (nu0 * tau0_sq + kappa0 * (dmu0 * dmu0)) + q;
+  const double tau2n = q_tau / gt;
+  const double kS = kappa0 + (double)S;
+  const double mun = (kappa0 * mu0 + sth) / kS + sqrt(tau2n / kS) * xm;
+  const double prec = 1.0 / tau2n + n / sg;
+  const double mean = (mun / tau2n + (n * xbar) / sg) / prec;
+  const double rsq = sqrt(prec);
+  const double thn = mean + xt / rsq;
+  const double res = xbar - thn;
+  const double sgn = ((alpha0 * sigma0_sq + ss) + n * (res * res)) / gs;
+  // finite / Picard on the coordinates this lane owns (lane 0 also tau^2, mu)
+  auto tol_fail = [&](double f, double g) { return !(fabs(f - g) <= A.atol + A.rtol * fabs(f)); };
+  bool fin = isfinite(thn) && isfinite(sgn);
+  bool pfail = tol_fail(thn, (double)grow[2 + sub]) || tol_fail(sgn, (double)grow[2 + S + sub]);
+  if (sub == 0) {
+    fin &= isfinite(tau2n) && isfinite(mun);
+    pfail |= tol_fail(tau2n, (double)grow[0]) || tol_fail(mun, (double)grow[1]);
+  }
+  // ---- Hutchinson over nsamp probes (deer.py:118-132).  The tangent map is
+  // linear in the probe, so every per-step quotient is hoisted into a
+  // reciprocal once; the tangents run in the storage precision TT (the estimate
+  // only steers convergence, the step values above stay f64).
+  using TT = ST;
+  const uint64_t h3 = hash_t(probe_prefix(A.sys.seed, iteration), (uint64_t)t);
+  const TT inv_gt = (TT)(1.0 / gt), inv_kS = (TT)(1.0 / kS), inv_tau2n = (TT)(1.0 / tau2n);
+  const TT inv_t2sq = (TT)(1.0 / (tau2n * tau2n)), n_sg2 = (TT)(n / (sg * sg)), inv_prec = (TT)(1.0 / prec);
+  const TT c_mu = (TT)(xm / (2.0 * sqrt(tau2n * kS))), c_th = (TT)(0.5 * xt / (prec * rsq));
+  const TT c_sg = (TT)((-2.0 * n * (xbar - thn)) / gs), mun_t = (TT)mun, mean_t = (TT)mean;
+  const TT xbar_t = (TT)xbar, two_dm = (TT)(2.0 * (th - mu)), mu_c = (TT)(2.0 * kappa0 * (mu - mu0));
+  TT e_tau = 0, e_mu = 0, e_th = 0, e_sg = 0;
+  for (int k = 0; k < A.nsamp; ++k) {
+    // z_tau / z_mu are shared by the team: lanes 0 and 1 hash them
+    const double zs = probe_sign(h3, k, sub == 0 ? 0 : (sub == 1 ? 1 : 2 + sub));
+    const TT z_tau = (TT)__shfl_sync(0xffffffffu, zs, (threadIdx.x & 31) & ~7);
+    const TT z_mu = (TT)__shfl_sync(0xffffffffu, zs, ((threadIdx.x & 31) & ~7) + 1);
+    const TT z_th = (TT)probe_sign(h3, k, 2 + sub), z_sg = (TT)probe_sign(h3, k, 2 + S + sub);
+    const TT dsg = raw_ok ? z_sg : (TT)0;
+    const TT dq = mu_c * z_mu + (TT)team_sum((double)(two_dm * (z_th - z_mu)));
+    const TT dtau2 = dq * inv_gt;
+    const TT dmu = (TT)team_sum((double)z_th) * inv_kS + c_mu * dtau2;
+    const TT dprec = -dtau2 * inv_t2sq - n_sg2 * dsg;
+    const TT damean = (dmu * inv_tau2n - mun_t * dtau2 * inv_t2sq) - xbar_t * n_sg2 * dsg;
+    const TT dmean = (damean - mean_t * dprec) * inv_prec;
+    const TT dth = dmean - c_th * dprec;
+    const TT dsgo = c_sg * dth;
+    e_tau += z_tau * dtau2;
+    e_mu += z_mu * dmu;
+    e_th += z_th * dth;
+    e_sg += z_sg * dsgo;
+  }
+  const double ns = (double)A.nsamp;
+  bool jok = true;
+  auto elem = [&](int d, double est, double f, double p, int64_t off) {
+    double v = est / ns;  // est / n_samples as deer.py:131
+    jok &= isfinite(v);
+    if (A.pre) v = v * __ldg(A.pre + d);
+    v = v * A.damping;
+    if (isfinite(A.clip)) v = clipv(v, A.clip);
+    if (valid) {
+      jout[off] = (ST)v;
+      uout[off] = (ST)(f - v * p);
+    }
+  };
+  elem(2 + sub, (double)e_th, thn, th, rr * D + 2 + sub);
+  elem(2 + S + sub, (double)e_sg, sgn, sgraw, rr * D + 2 + S + sub);
+  if (sub == 0) {
+    elem(0, (double)e_tau, tau2n, (double)prow[0], rr * D);
+    elem(1, (double)e_mu, mun, mu, rr * D + 1);
+  }
+  // team flags -> block -> stats
+  const unsigned bad_fin = __ballot_sync(0xffffffffu, valid && !fin);
+  const unsigned bad_jac = __ballot_sync(0xffffffffu, valid && !jok);
+  const unsigned pf = __ballot_sync(0xffffffffu, valid && pfail);
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    const int64_t r0 = ((int64_t)blockIdx.x * 256 + (threadIdx.x & ~31)) >> 3;
+    unsigned cnt = 0;
+    for (int tm = 0; tm < 4; ++tm) {
+      const unsigned m = 0xFFu << (8 * tm);
+      const long long step = r0 + tm + 1;
+      if (bad_fin & m) atomicMin(&smin[1], step);
+      if (bad_jac & m) atomicMin(&smin[2], step);
+      if (pf & m) ++cnt;
+    }
+    if (cnt) atomicAdd(&scnt, cnt);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (smin[1] != kNoStep) atomicMin((long long *)&stats->bad_step, smin[1]);
+    if (smin[2] != kNoStep) atomicMin((long long *)&stats->bad_jacobian, smin[2]);
+    if (scnt) atomicAdd(&stats->picard_fail, scnt);
+  }
+}
+
 cudaError_t syscall_gibbs(const cs_system &s, int dtype, int md, const SysCall &c, cudaStream_t st) {
   if (md != 18) return cudaErrorNotSupported;
   return dtype == CS_F64 ? run_syscall<Gibbs<18, double>, 18, double>(s, c, st)
@@ -16,10 +161,17 @@ cudaError_t solve_gibbs(int dtype, int md, int mode, void *args, int sms, cudaSt
 }
 cudaError_t elements_gibbs(int dtype, int md, int mode, void *args, int it, const void *g, void *e0, void *e1,
                            void *e2, void *e3, void *u, cs_elem_stats *stats, cudaStream_t st) {
-  if (md != 18) return cudaErrorNotSupported;
-  if (mode == CS_MODE_DIAG)
-    return dtype == CS_F64 ? launch_elements<Gibbs<18, double>, CS_MODE_DIAG, 18, double>(*(SolveArgs<double> *)args, it, g, e0, e1, e2, e3, u, stats, st)
-                           : launch_elements<Gibbs<18, float>, CS_MODE_DIAG, 18, float>(*(SolveArgs<float> *)args, it, g, e0, e1, e2, e3, u, stats, st);
-  return cudaErrorNotSupported;
+  if (md != 18 || mode != CS_MODE_DIAG) return cudaErrorNotSupported;
+  (void)e1; (void)e2; (void)e3;
+  if (dtype == CS_F64) {
+    const SolveArgs<double> &A = *(SolveArgs<double> *)args;
+    const unsigned grid = (unsigned)((A.T * 8 + 255) / 256);
+    k_gibbs_elements_team<double><<<grid, 256, 0, st>>>(A, it, (const double *)g, (double *)e0, (double *)u, stats);
+  } else {
+    const SolveArgs<float> &A = *(SolveArgs<float> *)args;
+    const unsigned grid = (unsigned)((A.T * 8 + 255) / 256);
+    k_gibbs_elements_team<float><<<grid, 256, 0, st>>>(A, it, (const float *)g, (float *)e0, (float *)u, stats);
+  }
+  return cudaGetLastError();
 }
 }  // namespace cs

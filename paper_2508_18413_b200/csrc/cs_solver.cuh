@@ -275,11 +275,16 @@ deer_persistent(SolveArgs<ST> A) {
   const Sys sys = SysFactory<Sys>::make(A.sys);
   const int b = blockIdx.x;
   const int D = A.D;
-  const int64_t row0 = ((int64_t)b * kSolveThreads + threadIdx.x) * A.seg;
+  // balanced contiguous ranges: CTA b owns rows [lo_b, hi_b), thread i the
+  // segment starting at lo_b + i * seg (every SM gets the same share of steps)
+  const int64_t lo_b = (int64_t)b * A.T / A.nblocks, hi_b = (int64_t)(b + 1) * A.T / A.nblocks;
+  const int seg = (int)((hi_b - lo_b + kSolveThreads - 1) / kSolveThreads);
+  const int64_t row0 = lo_b + (int64_t)threadIdx.x * seg;
+  const int64_t row_end = hi_b;
   double s0r[MD];
   load_row<Sys, MD, ST>(sys, A.s0, s0r);
-  for (int k = 0; k < A.seg; ++k)
-    if (row0 + k < A.T) A.last_fail[row0 + k] = 0;
+  for (int k = 0; k < seg; ++k)
+    if (row0 + k < row_end) A.last_fail[row0 + k] = 0;
 
   unsigned target = 0;
   double d0 = -1.0;
@@ -314,16 +319,16 @@ deer_persistent(SolveArgs<ST> A) {
     unsigned pf = 0;
     const bool want_elem = it < A.max_iters;
     double prev[MD];
-    if (it == 0 || row0 == 0 || row0 >= A.T) {
+    if (it == 0 || row0 == 0 || row0 >= row_end) {
 #pragma unroll
       for (int i = 0; i < MD; ++i) prev[i] = s0r[i];
     } else {
       load_row<Sys, MD, ST>(sys, Gc + (row0 - 1) * D, prev);
     }
 #pragma unroll 1
-    for (int k = 0; k < A.seg; ++k) {
+    for (int k = 0; k < seg; ++k) {
       const int64_t r = row0 + k;
-      if (r >= A.T) break;
+      if (r >= row_end) break;
       const int64_t t = r + 1;
       double gr[MD];
       if (it == 0) {
@@ -446,7 +451,7 @@ deer_persistent(SolveArgs<ST> A) {
       unsigned long long dmb = 0ull;
       double pv[MD];
       if (!KEEP) {
-        if (it == 0 || row0 == 0 || row0 >= A.T) {
+        if (it == 0 || row0 == 0 || row0 >= row_end) {
 #pragma unroll
           for (int i = 0; i < MD; ++i) pv[i] = s0r[i];
         } else {
@@ -454,9 +459,9 @@ deer_persistent(SolveArgs<ST> A) {
         }
       }
 #pragma unroll 1
-      for (int k = 0; k < A.seg; ++k) {
+      for (int k = 0; k < seg; ++k) {
         const int64_t r = row0 + k;
-        if (r >= A.T) break;
+        if (r >= row_end) break;
         double gr[MD];
         if (it == 0) {
 #pragma unroll

@@ -384,3 +384,49 @@ def test_leapfrog_block_cfg4_full_size_vs_oracle(cuda_device):
     assert r.iterations == ref.iterations
     np.testing.assert_allclose(np_(r.trace), ref.trace, atol=1e-8, rtol=1e-8)
     np.testing.assert_array_equal(np_(r.per_step_converged_at), ref.per_step_converged_at)
+
+
+# ---------------------------------------------------------------------------
+# the sharded driver's CUDA shard ops (world size 1 here; the multi-rank
+# exchange is covered with gloo in test_sharded_gloo.py)
+
+
+@pytest.mark.parametrize("mode,kw", [("diag-stochastic", dict(clip=1.0)), ("dense", dict(damping=0.5, clip=1.0))])
+def test_sharded_driver_cuda_ops_single_rank(cuda_device, mode, kw):
+    from paper_2508_18413_b200.sharded import run_deer_sharded
+
+    m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
+    k = cs.HmcKernel(m, 0.5, 8, seed=0, T=3000)
+    ref = cs.run_deer(k, np.zeros(2), cs.DeerConfig(mode=mode, **kw))
+    r = run_deer_sharded(k, np.zeros(2), cs.DeerConfig(mode=mode, **kw))
+    assert r.iterations == ref.iterations and r.converged == ref.converged
+    np.testing.assert_allclose(np_(r.trace), np_(ref.trace), atol=1e-10)
+    np.testing.assert_array_equal(np_(r.per_step_converged_at), np_(ref.per_step_converged_at))
+
+
+@pytest.mark.parametrize("mode", ["diag", "block", "dense"])
+def test_scan_aggregate_matches_fold(cuda_device, mode):
+    # cs_scan_aggregate = the composed map of the whole sequence (the shard carry)
+    from paper_2508_18413_b200.sharded import CudaShardOps, apply_agg
+
+    rng = np.random.default_rng(5)
+    T, D = 7001, (4 if mode != "dense" else 3)
+    tt = lambda x: torch.as_tensor(x, device=cuda_device)
+    if mode == "diag":
+        el = cs.DiagElements(tt(rng.uniform(-0.9, 0.9, (T, D))), tt(rng.normal(size=(T, D))))
+        W, key, s0 = D, "diag-stochastic", rng.normal(size=D)
+    elif mode == "block":
+        el = cs.Block2x2Elements(*(tt(rng.uniform(-0.6, 0.6, (T, D))) for _ in range(4)), tt(rng.normal(size=(T, 2 * D))))
+        W, key, s0 = 2 * D, "block2x2-stochastic", rng.normal(size=2 * D)
+    else:
+        J = rng.normal(size=(T, D, D))
+        J *= (0.9 / np.abs(np.linalg.eigvals(J)).max(axis=-1))[:, None, None]
+        el = cs.DenseElements(tt(J), tt(rng.normal(size=(T, D))))
+        W, key, s0 = D, "dense", rng.normal(size=D)
+    agg = CudaShardOps.__new__(CudaShardOps)
+    from paper_2508_18413_b200 import _lib
+
+    agg.lib = _lib
+    a = agg.aggregate(el)
+    last = cs.parallel_affine_solve(el, tt(s0))[-1]
+    np.testing.assert_allclose(np_(apply_agg(key, a, tt(s0))), np_(last), rtol=1e-10, atol=1e-10)
