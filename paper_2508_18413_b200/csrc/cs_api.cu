@@ -331,10 +331,14 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
   if (dtype == CS_F64) {
     ScanArgs<double> a{(const double *)e0, (const double *)e1, (const double *)e2, (const double *)e3,
                        (const double *)u, (const double *)s0, (double *)out, T, D};
+    a.probe = h_probe;
+    a.probe_n = h_probe_n;
     e = launch_scan_t<double>(p, a, ws, S(stream));
   } else {
     ScanArgs<float> a{(const float *)e0, (const float *)e1, (const float *)e2, (const float *)e3,
                       (const float *)u, (const float *)s0, (float *)out, T, D};
+    a.probe = h_probe;
+    a.probe_n = h_probe_n;
     e = launch_scan_t<float>(p, a, ws, S(stream));
   }
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "scan launch");

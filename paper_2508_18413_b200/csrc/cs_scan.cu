@@ -9,6 +9,8 @@
 // registers), reduced, linked to its predecessors by decoupled look-back,
 // replayed and written once -- 12 B/element (diag, f32) of algorithmic
 // traffic.  Carries and composition run in f64 regardless of storage type.
+#include <cstdlib>
+
 #include "cs_lookback.cuh"
 #include "cs_scan.cuh"
 #include "cs_tma.cuh"
@@ -16,6 +18,20 @@
 namespace cs {
 
 constexpr int kScanThreads = 256;
+constexpr int kHalf = kScanThreads / 2;
+
+// A thread group that cooperates on one phase: the whole CTA, or one half of
+// a warp-specialised CTA synchronised with a named barrier.
+template <int BASE, int NT, int BAR>
+struct Grp {
+  static constexpr int kN = NT;
+  CS_D static int tid() { return (int)threadIdx.x - BASE; }
+  CS_D static void sync() {
+    if constexpr (BAR == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+  }
+};
+using CtaGrp = Grp<0, kScanThreads, 0>;
 
 // ---------------------------------------------------------------------------
 // per-column affine monoid, diag and block2x2
@@ -38,6 +54,12 @@ template <> struct ColElem<SCAN_DIAG> {
     ColElem o;
     o.j = __shfl_down_sync(0xffffffffu, j, off);
     o.u = __shfl_down_sync(0xffffffffu, u, off);
+    return o;
+  }
+  CS_D ColElem up(int off) const {
+    ColElem o;
+    o.j = __shfl_up_sync(0xffffffffu, j, off);
+    o.u = __shfl_up_sync(0xffffffffu, u, off);
     return o;
   }
 };
@@ -78,50 +100,82 @@ template <> struct ColElem<SCAN_BLOCK> {
     o.uv = __shfl_down_sync(0xffffffffu, uv, off);
     return o;
   }
+  CS_D ColElem up(int off) const {
+    ColElem o;
+    o.A = __shfl_up_sync(0xffffffffu, A, off);
+    o.B = __shfl_up_sync(0xffffffffu, B, off);
+    o.C = __shfl_up_sync(0xffffffffu, C, off);
+    o.E = __shfl_up_sync(0xffffffffu, E, off);
+    o.ux = __shfl_up_sync(0xffffffffu, ux, off);
+    o.uv = __shfl_up_sync(0xffffffffu, uv, off);
+    return o;
+  }
 };
 
 // CTA-wide decoupled look-back over a window of 32 predecessors at a time:
 // warp 0 waits until every predecessor in the window has published at least
 // its aggregate and finds the nearest exit state; then the 8 warps fold the
 // window's aggregates column by column (lane = tile, ordered tree reduction)
-// into the running prefix s_acc.  One L2 round trip covers 32 tiles.
+// into the running prefix s_acc.  One L2 round trip covers kLbWindow tiles.
 //   status(p) -> const int*     agg(p, c) -> const double*
 //   exit_x(p, c), exit_v(p, c)  the published exit state of tile p
 //   s0x(c), s0v(c)              the chain's initial state
-template <int VAR, class StatusF, class AggF, class ExitF, class ExitVF, class S0F, class S0VF>
+constexpr int kLbPerLane = 4;                    // tiles per lane in a look-back window
+constexpr int kLbWindow = 32 * kLbPerLane;          // 128 predecessors per round trip
+
+template <int VAR, class G = CtaGrp, class StatusF, class AggF, class ExitF, class ExitVF, class S0F, class S0VF>
 CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF exit_x, ExitVF exit_v,
                        S0F s0x, S0VF s0v, double *s_acc, double *s_entry, int *s_ctl) {
   constexpr int W = ColElem<VAR>::W;
-  constexpr int NW = kScanThreads / 32;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int c = threadIdx.x; c < ncol; c += kScanThreads) {
+  constexpr int NW = G::kN / 32;
+  const int tid = G::tid(), lane = tid & 31, wid = tid >> 5;
+  for (int c = tid; c < ncol; c += G::kN) {
     ColElem<VAR> id;
     id.ident();
     id.store(s_acc + c * W);
   }
   int64_t hi = pos - 1;
   for (;;) {
-    __syncthreads();
+    G::sync();
     if (wid == 0) {
-      const int64_t p = hi - lane;
-      int st = 2;
-      if (p >= 0) {
-        do { st = ld_acquire(status(p)); } while (st == 0);
+      // lane l watches tiles hi - l*K - j, j < K (lane 0 holds the latest)
+      int st[kLbPerLane];
+#pragma unroll
+      for (int j = 0; j < kLbPerLane; ++j) {  // K independent loads: one round trip
+        const int64_t p = hi - lane * kLbPerLane - j;
+        st[j] = p >= 0 ? ld_acquire(status(p)) : 2;  // p < 0: the chain start (s0) acts as an exit
       }
-      const unsigned m2 = __ballot_sync(0xffffffffu, st == 2);
-      if (lane == 0) s_ctl[0] = m2 ? __ffs(m2) - 1 : 32;
+      int first = kLbWindow;
+#pragma unroll
+      for (int j = 0; j < kLbPerLane; ++j) {
+        const int64_t p = hi - lane * kLbPerLane - j;
+        while (st[j] == 0) st[j] = ld_acquire(status(p));
+        if (st[j] == 2 && first == kLbWindow) first = lane * kLbPerLane + j;
+      }
+      // nearest exit in the window = the smallest index over lanes
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, off));
+      if (lane == 0) s_ctl[0] = first;
     }
-    __syncthreads();
+    G::sync();
     const int stop = s_ctl[0];
-    const int64_t p = hi - lane;
     for (int c = wid; c < ncol; c += NW) {
+      // each lane folds its K tiles (latest applied last), then an ordered tree
       ColElem<VAR> e;
-      if (lane < stop) e.load_cg(agg(p, c));
-      else e.ident();
+      e.ident();
+#pragma unroll
+      for (int j = kLbPerLane - 1; j >= 0; --j) {
+        const int idx = lane * kLbPerLane + j;
+        if (idx < stop) {
+          ColElem<VAR> a;
+          a.load_cg(agg(hi - idx, c));
+          e.push(a);  // e <- a o e: tile hi-idx is later than hi-idx-1
+        }
+      }
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         ColElem<VAR> o = e.down(off);
-        if (lane + off < 32) e.pre(o);  // later tile (lower lane) applied after the earlier one
+        if (lane + off < 32) e.pre(o);  // later lanes hold earlier tiles
       }
       if (lane == 0) {
         ColElem<VAR> acc;
@@ -130,10 +184,10 @@ CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF ex
         acc.store(s_acc + c * W);
       }
     }
-    if (stop < 32) {
-      __syncthreads();
+    if (stop < kLbWindow) {
+      G::sync();
       const int64_t pe = hi - stop;
-      for (int c = threadIdx.x; c < ncol; c += kScanThreads) {
+      for (int c = tid; c < ncol; c += G::kN) {
         double x = pe < 0 ? s0x(c) : exit_x(pe, c);
         double v = 0.0;
         if (VAR == SCAN_BLOCK) v = pe < 0 ? s0v(c) : exit_v(pe, c);
@@ -144,238 +198,512 @@ CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF ex
         s_entry[c] = x;
         if (VAR == SCAN_BLOCK) s_entry[ncol + c] = v;
       }
-      __syncthreads();
+      G::sync();
       return;
     }
-    hi -= 32;
+    hi -= kLbWindow;
   }
 }
 
+// Two-level look-back for row tiles (see cs_lookback.cuh).  On return
+// s_entry holds the chain state entering tile b.
+template <int VAR, class G = CtaGrp, class S0F, class S0VF, class StampF>
+CS_D void lookback_grouped(int64_t b, int ncol, const LookbackWs &ws, S0F s0x, S0VF s0v, double *s_acc,
+                           double *s_acc2, double *s_entry, double *s_gentry, int *s_ctl, StampF stamp) {
+  constexpr int W = ColElem<VAR>::W;
+  const int SW = VAR == SCAN_DIAG ? ncol : 2 * ncol;
+  const int tid = G::tid();
+  const int64_t g = b / kGroupTiles;
+  const int i = (int)(b % kGroupTiles);
+  const int64_t t0 = g * kGroupTiles;
+  // The two levels are independent: the first half of the group folds the
+  // in-group prefix while the second half looks back over groups.
+  using H0 = Grp<G::kN == kScanThreads ? 0 : kHalf, G::kN / 2, 3>;
+  using H1 = Grp<(G::kN == kScanThreads ? 0 : kHalf) + G::kN / 2, G::kN / 2, 4>;
+  static_assert(G::kN == kHalf, "two-level look-back runs on one half of a warp-specialised CTA");
+  if (tid < G::kN / 2) {
+    // (1) in-group exclusive prefix over tiles t0 .. b-1 (lane l <-> tile t0+l)
+    const int ht = H0::tid(), lane = ht & 31, wid = ht >> 5;
+    if (wid == 0 && lane < i)
+      while (ld_acquire(ws.status + t0 + lane) == 0) {
+      }
+    H0::sync();
+    for (int c = wid; c < ncol; c += H0::kN / 32) {
+      ColElem<VAR> e;
+      e.ident();
+      if (lane < i) e.load_cg(ws.agg + ((t0 + lane) * ncol + c) * W);
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        ColElem<VAR> o = e.down(off);
+        if (lane + off < 32) e.push(o);  // later lanes hold later tiles
+      }
+      if (lane == 0) e.store(s_acc + c * W);
+    }
+    H0::sync();
+    if (ht == 0) stamp(6);
+  } else {
+    // (2) state entering the group: decoupled look-back over group aggregates
+    lookback_cta<VAR, H1>(
+        g, ncol, [&](int64_t p) { return ws.gstatus + p; },
+        [&](int64_t p, int cc) { return ws.gagg + (p * ncol + cc) * W; },
+        [&](int64_t p, int cc) { return ld_cg(ws.exit + p * SW + cc); },
+        [&](int64_t p, int cc) { return ld_cg(ws.exit + p * SW + ncol + cc); }, s0x, s0v, s_acc2, s_gentry,
+        s_ctl);
+    if (H1::tid() == 0) stamp(7);
+  }
+  G::sync();
+  // (3) tile entry = in-group prefix applied to the group entry
+  for (int c = tid; c < ncol; c += G::kN) {
+    ColElem<VAR> acc;
+    acc.load(s_acc + c * W);
+    double x = s_gentry[c], v = VAR == SCAN_BLOCK ? s_gentry[ncol + c] : 0.0;
+    if constexpr (VAR == SCAN_DIAG) acc.apply(x);
+    else acc.apply(x, v);
+    s_entry[c] = x;
+    if (VAR == SCAN_BLOCK) s_entry[ncol + c] = v;
+  }
+  G::sync();
+  // the first tile of a group publishes the group's entry as the previous
+  // group's exit (second half only; the first half goes on to the replay)
+  if (i == 0 && g > 0 && tid >= G::kN / 2) {
+    const int ht = H1::tid();
+    for (int c = ht; c < SW; c += H1::kN) ws.exit[(g - 1) * SW + c] = s_gentry[c];
+    __threadfence();
+    H1::sync();
+    if (ht == 0) st_release(ws.gstatus + g - 1, 2);
+  }
+}
+
+// Producer side of the two-level scheme: count this tile's aggregate into its
+// group; the producer completing the group folds and publishes the group
+// aggregate (status 1).
+template <int VAR, class G>
+CS_D void group_aggregate_publish(int64_t b, int ncol, const LookbackWs &ws, int *s_flag) {
+  constexpr int W = ColElem<VAR>::W;
+  constexpr int NW = G::kN / 32;
+  const int tid = G::tid(), lane = tid & 31, wid = tid >> 5;
+  const int64_t g = b / kGroupTiles;
+  if (tid == 0) {
+    __threadfence();
+    const int old = atomicAdd(ws.gcount + g, 1);
+    __threadfence();
+    *s_flag = old == kGroupTiles - 1;
+  }
+  G::sync();
+  if (!*s_flag) return;
+  const int64_t t0 = g * kGroupTiles;
+  for (int c = wid; c < ncol; c += NW) {
+    ColElem<VAR> e;
+    e.load_cg(ws.agg + ((t0 + lane) * ncol + c) * W);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      ColElem<VAR> o = e.down(off);
+      if (lane + off < 32) e.push(o);
+    }
+    if (lane == 0) {
+      double tmp[W];
+      e.store(tmp);
+#pragma unroll
+      for (int q = 0; q < W; ++q) ws.gagg[(g * ncol + c) * W + q] = tmp[q];
+      __threadfence();
+    }
+  }
+  G::sync();
+  if (tid == 0) st_release(ws.gstatus + g, 1);
+}
+
 // ---------------------------------------------------------------------------
-// narrow rows: tile = R consecutive rows x all columns, staged in smem
+// narrow rows: tile = R consecutive rows x all columns, staged in smem.
+// Persistent CTAs (grid = resident capacity) claim tiles in ticket order and
+// double-buffer them: the bulk (TMA) load of the next tile is in flight while
+// the current one is reduced, linked and replayed, so HBM never idles behind
+// a wave of CTAs that all sit in look-back at the same time.
+template <typename ST, int VAR>
+CS_D bool rows_tile_tma(const ScanArgs<ST> &a, int64_t b, int R) {
+  const int ncol = a.D;
+  const int64_t row0 = b * R;
+  const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
+  const unsigned bytes = (unsigned)(sizeof(ST) * rows * ncol);
+  const ST *u_src = a.u + (VAR == SCAN_BLOCK ? 2 : 1) * row0 * ncol;
+  return (bytes % 16 == 0) && aligned16(a.e0 + row0 * ncol) && aligned16(u_src) &&
+         (VAR == SCAN_DIAG || (aligned16(a.e1 + row0 * ncol) && aligned16(a.e2 + row0 * ncol) &&
+                               aligned16(a.e3 + row0 * ncol)));
+}
+
+template <typename ST, int VAR>
+CS_D void rows_tile_issue(const ScanArgs<ST> &a, int64_t b, int R, ST *tile, uint64_t *bar) {
+  const int ncol = a.D;
+  const int64_t row0 = b * R;
+  const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
+  const unsigned bytes = (unsigned)(sizeof(ST) * rows * ncol);
+  const int64_t g0 = row0 * ncol;
+  if constexpr (VAR == SCAN_DIAG) {
+    mbar_expect_tx(bar, 2 * bytes);
+    bulk_g2s(tile, a.e0 + g0, bytes, bar);
+    bulk_g2s(tile + R * ncol, a.u + g0, bytes, bar);
+  } else {
+    mbar_expect_tx(bar, 6 * bytes);
+    bulk_g2s(tile, a.e0 + g0, bytes, bar);
+    bulk_g2s(tile + R * ncol, a.e1 + g0, bytes, bar);
+    bulk_g2s(tile + 2 * R * ncol, a.e2 + g0, bytes, bar);
+    bulk_g2s(tile + 3 * R * ncol, a.e3 + g0, bytes, bar);
+    bulk_g2s(tile + 4 * R * ncol, a.u + 2 * g0, 2 * bytes, bar);
+  }
+}
+
+CS_D unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+CS_D unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+template <typename ST>
+CS_D void scan_stamp(const ScanArgs<ST> &a, int64_t b, int k) {
+  if (a.probe && b * 16 + 16 <= a.probe_n) a.probe[b * 16 + k] = k == 0 ? smid() : gtimer();
+}
+
+// Warp-specialised persistent CTA: warps 0-3 produce (claim a tile, bulk-load
+// it, reduce, publish its aggregate), warps 4-7 consume (look back, replay,
+// bulk-store).  Tiles live in a ring of kRowsBufs shared-memory slots.  A
+// claimed tile's aggregate never waits on any look-back -- the producer only
+// claims into a free slot -- so successors that look back into it see it one
+// load + one reduction after the claim.
+constexpr int kRowsBufs = 3;
+using ProdGrp = Grp<0, kHalf, 1>;
+using ConsGrp = Grp<kHalf, kHalf, 2>;
+
+CS_D bool mbar_test(uint64_t *bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+CS_D void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <typename ST, int VAR, bool AGG_ONLY = false, bool UPDATE = false>
 __global__ void __launch_bounds__(kScanThreads)
-scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int win) {
+scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int tile_stride) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int NA = VAR == SCAN_DIAG ? 2 : 6;  // staged arrays (block: a b c d + u counted as 2)
   constexpr int W = ColElem<VAR>::W;
+  constexpr int NB = kRowsBufs;
+  using CT = ST;  // in-segment arithmetic type; everything crossing segments is f64
   const int ncol = a.D;
   const int SW = VAR == SCAN_DIAG ? ncol : 2 * ncol;
-  __shared__ int64_t s_tile;
+  const int nseg = kHalf / ncol;
+  const int segw = (nseg + 1) * ncol * W;  // doubles per segment-aggregate slot
+  __shared__ int64_t s_tile[NB];
+  __shared__ int s_kc, s_done, s_gflag;
   __shared__ double s_entry[2 * 64];
   __shared__ double s_acc[64 * W];
+  __shared__ double s_acc2[64 * W];
+  __shared__ double s_gentry[2 * 64];
   __shared__ int s_ctl[1];
-  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ unsigned s_nf;
+  __shared__ unsigned long long s_dm;
+  __shared__ __align__(8) uint64_t s_ld[NB], s_full[NB], s_empty[NB];
+  double *segagg0 = (double *)(smem_raw + NB * (size_t)tile_stride);
+  int *s_fail = (int *)(segagg0 + NB * segw);  // UPDATE: one flag per row (consumer)
+  auto buf = [&](int slot) { return (ST *)(smem_raw + (size_t)slot * tile_stride); };
+
   if (threadIdx.x == 0) {
-    s_tile = atomicAdd(ws.ticket, 1u);
-    mbar_init(&s_bar, 1);
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(&s_ld[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  const int64_t b = s_tile;
-  const int64_t row0 = b * R;
-  const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
-  const int nel = rows * ncol;
-  ST *tile = (ST *)smem_raw;  // NA arrays of R*ncol
-  double *segagg = (double *)(smem_raw + ((sizeof(ST) * NA * R * ncol + 15) / 16) * 16);
-  // UPDATE: one fail flag per row, after the segment aggregates
-  int *s_fail = (int *)(segagg + (kScanThreads / ncol + 1) * ncol * W);
-  const ST *u_src = a.u + 2 * row0 * ncol * (VAR == SCAN_BLOCK) + row0 * ncol * (VAR == SCAN_DIAG);
 
-  // ---- stage the tile: one bulk (TMA) copy per array when aligned, else LDG loop
-  const unsigned bytes = (unsigned)(sizeof(ST) * nel);
-  const bool tma = (bytes % 16 == 0) && aligned16(a.e0 + row0 * ncol) && aligned16(u_src) &&
-                   (VAR == SCAN_DIAG || (aligned16(a.e1 + row0 * ncol) && aligned16(a.e2 + row0 * ncol) &&
-                                         aligned16(a.e3 + row0 * ncol)));
-  if (tma) {
-    if (threadIdx.x == 0) {
-      const int64_t g0 = row0 * ncol;
-      if constexpr (VAR == SCAN_DIAG) {
-        mbar_expect_tx(&s_bar, 2 * bytes);
-        bulk_g2s(tile, a.e0 + g0, bytes, &s_bar);
-        bulk_g2s(tile + R * ncol, u_src, bytes, &s_bar);
-      } else {
-        mbar_expect_tx(&s_bar, 6 * bytes);
-        bulk_g2s(tile, a.e0 + g0, bytes, &s_bar);
-        bulk_g2s(tile + R * ncol, a.e1 + g0, bytes, &s_bar);
-        bulk_g2s(tile + 2 * R * ncol, a.e2 + g0, bytes, &s_bar);
-        bulk_g2s(tile + 3 * R * ncol, a.e3 + g0, bytes, &s_bar);
-        bulk_g2s(tile + 4 * R * ncol, u_src, 2 * bytes, &s_bar);
+  if (threadIdx.x < kHalf) {
+    // ======================= producer =======================
+    const int tid = ProdGrp::tid();
+    const int c = tid % ncol, sg = tid / ncol;
+    const bool active = sg < nseg;
+    int kc = 0, kr = 0;  // tiles claimed / reduced by this CTA
+    bool done = false;
+    unsigned ldph = 0;   // bit i: parity of the next bulk-load completion on slot i
+    for (;;) {
+      if (tid == 0 && !done) {
+        while (kc < kr + NB) {
+          const int slot = kc % NB;
+          if (kc >= NB && !mbar_test(&s_empty[slot], ((kc / NB) - 1) & 1)) break;  // slot still busy
+          const int64_t t = atomicAdd(ws.ticket, 1u);
+          if (t >= ntiles) {
+            s_tile[slot] = -1;
+            mbar_arrive(&s_full[slot]);  // end marker for the consumer
+            done = true;
+            break;
+          }
+          s_tile[slot] = t;
+          scan_stamp(a, t, 1);
+          if (rows_tile_tma<ST, VAR>(a, t, R)) rows_tile_issue<ST, VAR>(a, t, R, buf(slot), &s_ld[slot]);
+          ++kc;
+        }
+        s_kc = kc;
+        s_done = done;
       }
-    }
-    mbar_wait(&s_bar, 0);
-  } else {
-    const int64_t g0 = row0 * ncol;
-    for (int i = threadIdx.x; i < nel; i += kScanThreads) {
-      tile[i] = a.e0[g0 + i];
-      if constexpr (VAR == SCAN_DIAG) {
-        tile[R * ncol + i] = u_src[i];
-      } else {
-        tile[R * ncol + i] = a.e1[g0 + i];
-        tile[2 * R * ncol + i] = a.e2[g0 + i];
-        tile[3 * R * ncol + i] = a.e3[g0 + i];
+      ProdGrp::sync();
+      kc = s_kc;
+      done = s_done;
+      ProdGrp::sync();
+      if (kr == kc) {
+        if (done) break;
+        // nothing loaded: block until the consumer frees the next slot
+        if (tid == 0) mbar_wait(&s_empty[kc % NB], ((kc / NB) - 1) & 1);
+        ProdGrp::sync();
+        continue;
       }
-    }
-    if constexpr (VAR == SCAN_BLOCK)
-      for (int i = threadIdx.x; i < 2 * nel; i += kScanThreads) tile[4 * R * ncol + i] = u_src[i];
-    __syncthreads();
-  }
-
-  const int nseg = kScanThreads / ncol;
-  const int c = threadIdx.x % ncol, sg = threadIdx.x / ncol;
-  const int seglen = (rows + nseg - 1) / nseg;
-  const int r0 = sg * seglen, r1 = min(rows, r0 + seglen);
-  const bool active = sg < nseg;
-
-  ColElem<VAR> run;
-  run.ident();
-  if (active) {
-    for (int r = r0; r < r1; ++r) {
-      const int i = r * ncol + c;
-      if constexpr (VAR == SCAN_DIAG) {
-        run.push((double)tile[i], (double)tile[R * ncol + i]);
+      const int slot = kr % NB;
+      const int64_t b = s_tile[slot];
+      ST *tile = buf(slot);
+      double *segagg = segagg0 + slot * segw;
+      const int64_t row0 = b * R;
+      const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
+      if (rows_tile_tma<ST, VAR>(a, b, R)) {
+        mbar_wait(&s_ld[slot], (ldph >> slot) & 1u);
+        ldph ^= 1u << slot;
       } else {
-        run.push((double)tile[i], (double)tile[R * ncol + i], (double)tile[2 * R * ncol + i],
-                 (double)tile[3 * R * ncol + i], (double)tile[4 * R * ncol + 2 * r * ncol + c],
-                 (double)tile[4 * R * ncol + 2 * r * ncol + ncol + c]);
+        const int nel = rows * ncol;
+        const int64_t g0 = row0 * ncol;
+        const ST *u_src = a.u + (VAR == SCAN_BLOCK ? 2 : 1) * g0;
+        for (int i = tid; i < nel; i += kHalf) {
+          tile[i] = a.e0[g0 + i];
+          if constexpr (VAR == SCAN_DIAG) {
+            tile[R * ncol + i] = u_src[i];
+          } else {
+            tile[R * ncol + i] = a.e1[g0 + i];
+            tile[2 * R * ncol + i] = a.e2[g0 + i];
+            tile[3 * R * ncol + i] = a.e3[g0 + i];
+          }
+        }
+        if constexpr (VAR == SCAN_BLOCK)
+          for (int i = tid; i < 2 * nel; i += kHalf) tile[4 * R * ncol + i] = u_src[i];
+        ProdGrp::sync();
       }
-    }
-    run.store(segagg + (sg * ncol + c) * W);
-  }
-  __syncthreads();
-
-  // per-column exclusive scan over segments; publish the tile aggregate
-  if (threadIdx.x < ncol) {
-    ColElem<VAR> tot;
-    tot.ident();
-    for (int q = 0; q < nseg; ++q) {
-      ColElem<VAR> e;
-      e.load(segagg + (q * ncol + threadIdx.x) * W);
-      tot.store(segagg + (q * ncol + threadIdx.x) * W);  // exclusive prefix in place
-      tot.push(e);
-    }
-    double *g = ws.agg + (b * ncol + threadIdx.x) * W;
-    double tmp[W];
-    tot.store(tmp);
+      if (tid == 0) {
+        scan_stamp(a, b, 0);
+        scan_stamp(a, b, 2);
+      }
+      const int seglen = (rows + nseg - 1) / nseg;
+      const int r0 = sg * seglen, r1 = min(rows, r0 + seglen);
+      if (active) {
+        ColElem<VAR> run;
+        if constexpr (VAR == SCAN_DIAG) {
+          CT rj = 1, ru = 0;
+          for (int r = r0; r < r1; ++r) {
+            const int i = r * ncol + c;
+            const CT ej = (CT)tile[i];
+            ru = ej * ru + (CT)tile[R * ncol + i];
+            rj = ej * rj;
+          }
+          run.j = (double)rj;
+          run.u = (double)ru;
+        } else {
+          CT A = 1, B = 0, C = 0, E = 1, ux = 0, uv = 0;
+          for (int r = r0; r < r1; ++r) {
+            const int i = r * ncol + c;
+            const CT ea = (CT)tile[i], eb = (CT)tile[R * ncol + i], ec = (CT)tile[2 * R * ncol + i],
+                     ed = (CT)tile[3 * R * ncol + i];
+            const CT px = (CT)tile[4 * R * ncol + 2 * r * ncol + c],
+                     pv = (CT)tile[4 * R * ncol + 2 * r * ncol + ncol + c];
+            const CT An = ea * A + eb * C, Bn = ea * B + eb * E, Cn = ec * A + ed * C, En = ec * B + ed * E;
+            const CT xn = ea * ux + eb * uv + px, vn = ec * ux + ed * uv + pv;
+            A = An; B = Bn; C = Cn; E = En; ux = xn; uv = vn;
+          }
+          run.A = A; run.B = B; run.C = C; run.E = E; run.ux = ux; run.uv = uv;
+        }
+        run.store(segagg + (sg * ncol + c) * W);
+      }
+      ProdGrp::sync();
+      if (tid == 0) scan_stamp(a, b, 3);
+      // per-column exclusive scan over segments (warp per column, lane q holds
+      // segments [q*K, q*K+K)); publish the tile aggregate
+      {
+        const int lane = tid & 31, wid = tid >> 5;
+        const int K = (nseg + 31) / 32;
+        for (int cc = wid; cc < ncol; cc += kHalf / 32) {
+          ColElem<VAR> e;
+          e.ident();
+          for (int q = lane * K; q < lane * K + K && q < nseg; ++q) {
+            ColElem<VAR> x;
+            x.load(segagg + (q * ncol + cc) * W);
+            e.push(x);
+          }
 #pragma unroll
-    for (int k = 0; k < W; ++k) g[k] = tmp[k];
-    tot.store(segagg + (nseg * ncol + threadIdx.x) * W);
-    __threadfence();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) st_release(ws.status + b, 1);
-  if constexpr (AGG_ONLY) return;
-
-  lookback_cta<VAR>(
-      b, ncol, [&](int64_t p) { return ws.status + p; },
-      [&](int64_t p, int cc) { return ws.agg + (p * ncol + cc) * W; },
-      [&](int64_t p, int cc) { return ld_cg(ws.exit + p * SW + cc); },
-      [&](int64_t p, int cc) { return ld_cg(ws.exit + p * SW + ncol + cc); },
-      [&](int cc) { return (double)a.s0[cc]; }, [&](int cc) { return (double)a.s0[ncol + cc]; }, s_acc,
-      s_entry, s_ctl);
-
-  // exit state of this tile, published before the replay
-  if (threadIdx.x < ncol) {
-    ColElem<VAR> tot;
-    tot.load(segagg + (nseg * ncol + threadIdx.x) * W);
-    double x = s_entry[threadIdx.x], v = VAR == SCAN_BLOCK ? s_entry[ncol + threadIdx.x] : 0.0;
-    if constexpr (VAR == SCAN_DIAG) {
-      tot.apply(x);
-      ws.exit[b * SW + threadIdx.x] = x;
-    } else {
-      tot.apply(x, v);
-      ws.exit[b * SW + threadIdx.x] = x;
-      ws.exit[b * SW + ncol + threadIdx.x] = v;
-    }
-    __threadfence();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) st_release(ws.status + b, 2);
-
-  // replay from the segment entry state; results overwrite the staged tile
-  unsigned long long dmb = 0ull;
-  if constexpr (UPDATE) {
-    for (int r = threadIdx.x; r < rows; r += kScanThreads) s_fail[r] = 0;
-    __syncthreads();
-  }
-  auto check = [&](int r, int col, double xv) {  // deer.py:273-275 on the stored value
-    if constexpr (UPDATE) {
-      const double xd = (double)(ST)xv;
-      const double gap = fabs(xd - (double)a.guess[(row0 + r) * SW + col]);
-      if (gap > a.atol + a.rtol * fabs(xd)) s_fail[r] = 1;
-      const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
-      dmb = gb > dmb ? gb : dmb;
-    }
-  };
-  if (active && r0 < r1) {
-    ColElem<VAR> pre;
-    pre.load(segagg + (sg * ncol + c) * W);
-    if constexpr (VAR == SCAN_DIAG) {
-      double x = s_entry[c];
-      pre.apply(x);
-      for (int r = r0; r < r1; ++r) {
-        const int i = r * ncol + c;
-        x = (double)tile[i] * x + (double)tile[R * ncol + i];
-        tile[i] = (ST)x;
-        check(r, c, x);
+          for (int off = 1; off < 32; off <<= 1) {
+            ColElem<VAR> o = e.up(off);
+            if (lane >= off) e.pre(o);  // earlier lanes hold earlier segments
+          }
+          ColElem<VAR> ex = e.up(1);
+          if (lane == 0) ex.ident();
+          if (lane == 31) {
+            double tmp[W];
+            e.store(tmp);
+            double *g = ws.agg + (b * ncol + cc) * W;
+#pragma unroll
+            for (int q = 0; q < W; ++q) g[q] = tmp[q];
+            e.store(segagg + (nseg * ncol + cc) * W);
+          }
+          for (int q = lane * K; q < lane * K + K && q < nseg; ++q) {  // exclusive prefixes in place
+            ColElem<VAR> x;
+            x.load(segagg + (q * ncol + cc) * W);
+            ex.store(segagg + (q * ncol + cc) * W);
+            ex.push(x);
+          }
+        }
+        __threadfence();
       }
-    } else {
-      double x = s_entry[c], v = s_entry[ncol + c];
-      pre.apply(x, v);
-      for (int r = r0; r < r1; ++r) {
-        const int i = r * ncol + c;
-        const double xa = (double)tile[i] * x + (double)tile[R * ncol + i] * v +
-                          (double)tile[4 * R * ncol + 2 * r * ncol + c];
-        const double va = (double)tile[2 * R * ncol + i] * x + (double)tile[3 * R * ncol + i] * v +
-                          (double)tile[4 * R * ncol + 2 * r * ncol + ncol + c];
-        x = xa;
-        v = va;
-        // [x | v] rows overwrite the u tile in place (same thread, same slots)
-        tile[4 * R * ncol + 2 * r * ncol + c] = (ST)x;
-        tile[4 * R * ncol + 2 * r * ncol + ncol + c] = (ST)v;
-        check(r, c, x);
-        check(r, ncol + c, v);
+      ProdGrp::sync();
+      if (tid == 0) {
+        st_release(ws.status + b, 1);
+        scan_stamp(a, b, 4);
+        mbar_arrive(&s_full[slot]);
       }
-    }
-  }
-  if constexpr (UPDATE) {
-    __shared__ unsigned s_nf;
-    __shared__ unsigned long long s_dm;
-    if (threadIdx.x == 0) { s_nf = 0; s_dm = 0ull; }
-    __syncthreads();
-    unsigned nf = 0;
-    for (int r = threadIdx.x; r < rows; r += kScanThreads)
-      if (s_fail[r]) {
-        a.last_fail[row0 + r] = a.it;
-        ++nf;
-      }
-    nf = (unsigned)warp_sum_i((int)nf);
-    dmb = warp_max_u64(dmb);
-    if ((threadIdx.x & 31) == 0) {
-      if (nf) atomicAdd(&s_nf, nf);
-      atomicMax(&s_dm, dmb);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (s_nf) atomicAdd(&a.stats->fail_rows, s_nf);
-      atomicMax((unsigned long long *)&a.stats->dmax, s_dm);
-    }
-  }
-  const ST *src = VAR == SCAN_DIAG ? tile : tile + 4 * R * ncol;
-  const int64_t g0 = row0 * SW;
-  const unsigned obytes = (unsigned)(sizeof(ST) * rows * SW);
-  if (tma && aligned16(a.out + g0) && obytes % 16 == 0) {
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      bulk_s2g(a.out + g0, src, obytes);
-      bulk_commit();
-      bulk_wait_read();
+      if constexpr (!AGG_ONLY) group_aggregate_publish<VAR, ProdGrp>(b, ncol, ws, &s_gflag);
+      ++kr;
     }
   } else {
-    __syncthreads();
-    const int nout = rows * SW;
-    for (int i = threadIdx.x; i < nout; i += kScanThreads) a.out[g0 + i] = src[i];
+    // ======================= consumer =======================
+    const int tid = ConsGrp::tid();
+    const int c = tid % ncol, sg = tid / ncol;
+    const bool active = sg < nseg;
+    int pend = -1;  // slot whose bulk store has not yet been confirmed read
+    for (int k = 0;; ++k) {
+      const int slot = k % NB;
+      mbar_wait(&s_full[slot], (k / NB) & 1);
+      const int64_t b = s_tile[slot];
+      if (b < 0) break;
+      if (tid == 0) scan_stamp(a, b, 5);
+      ST *tile = buf(slot);
+      const double *segagg = segagg0 + slot * segw;
+      if constexpr (AGG_ONLY) {
+        ConsGrp::sync();  // all consumers have read s_tile before the slot is recycled
+        if (tid == 0) mbar_arrive(&s_empty[slot]);
+        continue;
+      }
+      const int64_t row0 = b * R;
+      const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
+      lookback_grouped<VAR, ConsGrp>(
+          b, ncol, ws, [&](int cc) { return (double)a.s0[cc]; }, [&](int cc) { return (double)a.s0[ncol + cc]; }, s_acc,
+          s_acc2, s_entry, s_gentry, s_ctl, [&](int k) { scan_stamp(a, b, k); });
+      if (tid == 0) scan_stamp(a, b, 8);
+
+      unsigned long long dmb = 0ull;
+      if constexpr (UPDATE) {
+        for (int r = tid; r < rows; r += kHalf) s_fail[r] = 0;
+        if (tid == 0) { s_nf = 0; s_dm = 0ull; }
+        ConsGrp::sync();
+      }
+      auto check = [&](int r, int col, double xv) {  // deer.py:273-275 on the stored value
+        if constexpr (UPDATE) {
+          const double gap = fabs(xv - (double)a.guess[(row0 + r) * SW + col]);
+          if (gap > a.atol + a.rtol * fabs(xv)) s_fail[r] = 1;
+          const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
+          dmb = gb > dmb ? gb : dmb;
+        }
+      };
+      const int seglen = (rows + nseg - 1) / nseg;
+      const int r0 = sg * seglen, r1 = min(rows, r0 + seglen);
+      if (active && r0 < r1) {
+        ColElem<VAR> pre;
+        pre.load(segagg + (sg * ncol + c) * W);
+        if constexpr (VAR == SCAN_DIAG) {
+          double xe = s_entry[c];
+          pre.apply(xe);
+          CT x = (CT)xe;
+          for (int r = r0; r < r1; ++r) {
+            const int i = r * ncol + c;
+            x = (CT)tile[i] * x + (CT)tile[R * ncol + i];
+            tile[i] = (ST)x;
+            check(r, c, (double)x);
+          }
+        } else {
+          double xe = s_entry[c], ve = s_entry[ncol + c];
+          pre.apply(xe, ve);
+          CT x = (CT)xe, v = (CT)ve;
+          for (int r = r0; r < r1; ++r) {
+            const int i = r * ncol + c;
+            const CT xa = (CT)tile[i] * x + (CT)tile[R * ncol + i] * v + (CT)tile[4 * R * ncol + 2 * r * ncol + c];
+            const CT va = (CT)tile[2 * R * ncol + i] * x + (CT)tile[3 * R * ncol + i] * v +
+                          (CT)tile[4 * R * ncol + 2 * r * ncol + ncol + c];
+            x = xa;
+            v = va;
+            // [x | v] rows overwrite the u tile in place (same thread, same slots)
+            tile[4 * R * ncol + 2 * r * ncol + c] = (ST)x;
+            tile[4 * R * ncol + 2 * r * ncol + ncol + c] = (ST)v;
+            check(r, c, (double)x);
+            check(r, ncol + c, (double)v);
+          }
+        }
+      }
+      if constexpr (UPDATE) {
+        ConsGrp::sync();
+        unsigned nf = 0;
+        for (int r = tid; r < rows; r += kHalf)
+          if (s_fail[r]) {
+            a.last_fail[row0 + r] = a.it;
+            ++nf;
+          }
+        nf = (unsigned)warp_sum_i((int)nf);
+        dmb = warp_max_u64(dmb);
+        if ((tid & 31) == 0) {
+          if (nf) atomicAdd(&s_nf, nf);
+          atomicMax(&s_dm, dmb);
+        }
+        ConsGrp::sync();
+        if (tid == 0) {
+          if (s_nf) atomicAdd(&a.stats->fail_rows, s_nf);
+          atomicMax((unsigned long long *)&a.stats->dmax, s_dm);
+        }
+      }
+      const ST *src = VAR == SCAN_DIAG ? tile : tile + 4 * R * ncol;
+      const int64_t g0 = row0 * SW;
+      const unsigned obytes = (unsigned)(sizeof(ST) * rows * SW);
+      if (rows_tile_tma<ST, VAR>(a, b, R) && aligned16(a.out + g0) && obytes % 16 == 0) {
+        fence_proxy_async_smem();
+        ConsGrp::sync();
+        if (tid == 0) {
+          scan_stamp(a, b, 9);
+          bulk_s2g(a.out + g0, src, obytes);
+          bulk_commit();
+          // free the previous slot once its store has been read out of smem
+          if (pend >= 0) {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            mbar_arrive(&s_empty[pend]);
+          }
+        }
+        pend = slot;
+      } else {
+        ConsGrp::sync();
+        const int nout = rows * SW;
+        for (int i = tid; i < nout; i += kHalf) a.out[g0 + i] = src[i];
+        ConsGrp::sync();
+        if (tid == 0) {
+          if (pend >= 0) {
+            bulk_wait_read();
+            mbar_arrive(&s_empty[pend]);
+          }
+          mbar_arrive(&s_empty[slot]);
+        }
+        pend = -1;
+      }
+    }
+    if (tid == 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      if (pend >= 0) mbar_arrive(&s_empty[pend]);
+    }
   }
 }
 
@@ -805,7 +1133,12 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 static int rows_per_tile(int var, int dtype, int D) {
   const int esz = dtype == CS_F64 ? 8 : 4;
   const int per = (var == SCAN_DIAG ? 2 : 6) * esz;
-  int E = (64 * 1024) / per;
+  static const int tile_kb = [] {  // tuning override for experiments
+    const char *e = getenv("CS_SCAN_TILE_KB");
+    const int v = e ? atoi(e) : 0;
+    return v >= 4 && v <= 96 ? v : 32;
+  }();
+  int E = (tile_kb * 1024) / per;
   int R = E / D;
   if (R > 8192) R = 8192;
   const int q = dtype == CS_F64 ? 2 : 4;  // R*D*esize % 16 == 0 for any D
@@ -835,13 +1168,11 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
     const int NA = var == SCAN_DIAG ? 2 : 6;
     const int nseg = kScanThreads / D;
     const int W = var == SCAN_DIAG ? 2 : 6;
-    p.smem = ((size_t)esz * NA * p.R * D + 15) / 16 * 16 + sizeof(double) * (nseg + 1) * D * W + sizeof(int) * p.R;
-    // walker window: aggregates [win][D][W] + chunk scratch [nseg][D][W] within the same smem
-    const size_t chunk_bytes = sizeof(double) * (size_t)nseg * D * W;
-    int win = (int)((p.smem - chunk_bytes) / (sizeof(double) * D * W));
-    if (win > 256) win = 256;
-    if (win < 1) win = 1;
-    p.win = win;
+    // ring of tile slots, one segment-aggregate slot per tile slot, row flags
+    const int nseg_h = kHalf / D;
+    p.win = (int)(((size_t)esz * NA * p.R * D + 127) / 128 * 128);  // tile slot stride
+    p.smem = kRowsBufs * (size_t)p.win + sizeof(double) * kRowsBufs * (nseg_h + 1) * D * W + sizeof(int) * p.R;
+    (void)nseg;
   } else {
     p.kind = 1;
     const int ncb = (D + 31) / 32;
@@ -849,8 +1180,9 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
     p.agg_w = 32 * (var == SCAN_DIAG ? 2 : 6);
     p.state_w = var == SCAN_DIAG ? D : 2 * D;
   }
-  p.ws_bytes = align_up(sizeof(unsigned)) + align_up(sizeof(int) * p.ntiles) +
-               align_up(sizeof(double) * p.ntiles * p.agg_w) +
+  const int64_t ngroups = p.kind == 0 ? (p.ntiles + kGroupTiles - 1) / kGroupTiles : 0;
+  p.ws_bytes = align_up(sizeof(unsigned)) + align_up(sizeof(int) * (p.ntiles + 2 * ngroups)) +
+               align_up(sizeof(double) * (p.ntiles + ngroups) * p.agg_w) +
                align_up(sizeof(double) * (p.kind == 1 ? (p.ntiles / ((D + 31) / 32) + 1) : p.ntiles) * p.state_w);
   return p;
 }
@@ -860,20 +1192,36 @@ LookbackWs carve_ws(const ScanPlan &p, void *ws, int D) {
   LookbackWs w;
   w.ticket = (unsigned *)b;
   b += align_up(sizeof(unsigned));
+  const int64_t ngroups = p.kind == 0 ? (p.ntiles + kGroupTiles - 1) / kGroupTiles : 0;
   w.status = (int *)b;
-  b += align_up(sizeof(int) * p.ntiles);
+  w.gstatus = w.status + p.ntiles;
+  w.gcount = w.gstatus + ngroups;
+  b += align_up(sizeof(int) * (p.ntiles + 2 * ngroups));
   w.agg = (double *)b;
-  b += align_up(sizeof(double) * p.ntiles * p.agg_w);
+  w.gagg = w.agg + p.ntiles * p.agg_w;
+  b += align_up(sizeof(double) * (p.ntiles + ngroups) * p.agg_w);
   w.exit = (double *)b;
   (void)D;
   return w;
 }
 
+// persistent grid for scan_rows: every CTA must be co-resident (look-back
+// waits on tiles held by other CTAs), so never launch more than fit at once
+static unsigned rows_grid(const ScanPlan &p, const void *k) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kScanThreads, p.smem);
+  if (occ < 1) occ = 1;
+  const int64_t cap = (int64_t)occ * sms;
+  return (unsigned)(p.ntiles < cap ? p.ntiles : cap);
+}
+
 template <typename ST, int VAR, bool UPD>
 static void launch_rows(const ScanPlan &p, const ScanArgs<ST> &a, LookbackWs w, cudaStream_t st) {
   auto k = scan_rows<ST, VAR, false, UPD>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-  k<<<(unsigned)p.ntiles, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
+  k<<<rows_grid(p, (const void *)k), kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
 }
 
 template <typename ST>
@@ -919,12 +1267,12 @@ cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, doub
   const unsigned grid = (unsigned)p.ntiles;
   if (p.kind == 0) {
     if (p.var == SCAN_DIAG) {
-      cudaFuncSetAttribute(scan_rows<ST, SCAN_DIAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      scan_rows<ST, SCAN_DIAG, true><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
+      const void *kf = (const void *)scan_rows<ST, SCAN_DIAG, true>;
+      scan_rows<ST, SCAN_DIAG, true><<<rows_grid(p, kf), kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
       k_agg_compose_cols<SCAN_DIAG><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
     } else {
-      cudaFuncSetAttribute(scan_rows<ST, SCAN_BLOCK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      scan_rows<ST, SCAN_BLOCK, true><<<grid, kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
+      const void *kf = (const void *)scan_rows<ST, SCAN_BLOCK, true>;
+      scan_rows<ST, SCAN_BLOCK, true><<<rows_grid(p, kf), kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
       k_agg_compose_cols<SCAN_BLOCK><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
     }
   } else if (p.kind == 1) {

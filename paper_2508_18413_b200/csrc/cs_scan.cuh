@@ -19,6 +19,10 @@ struct ScanArgs {
   int it;
   int32_t *last_fail;
   cs_elem_stats *stats;
+  // debug timeline (cs_debug_probe): per tile 8 x u64 {sm, claim, data, agg,
+  // linked, replayed, -, -} globaltimer stamps; null in production
+  unsigned long long *probe;
+  int64_t probe_n;
 };
 
 struct ScanPlan {

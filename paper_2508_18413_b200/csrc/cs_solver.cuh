@@ -114,7 +114,7 @@ CS_D void build_elem(const Sys &sys, const typename Sys::Aux &aux, const double 
         const int m = sys.mem_index(i);
         V[0][i] = m >= 0 ? probe_sign(h3, k, m) : 0.0;
       }
-      sys.template jvp_many<1>(aux, V, O, 1, false);
+      sys.template jvp_many<1, ST>(aux, V, O, 1, false);
 #pragma unroll
       for (int i = 0; i < MD; ++i) est[i] += V[0][i] * O[0][i];
     }
@@ -140,7 +140,7 @@ CS_D void build_elem(const Sys &sys, const typename Sys::Aux &aux, const double 
 #pragma unroll
       for (int i = 0; i < MD; ++i) V[c][i] = (i == c && sys.mem_index(c) >= 0) ? 1.0 : 0.0;
     }
-    sys.template jvp_many<MD>(aux, V, O, nk, false);
+    sys.template jvp_many<MD, ST>(aux, V, O, nk, false);
 #pragma unroll
     for (int a = 0; a < MD; ++a) {
       const int ma = sys.mem_index(a);

@@ -69,34 +69,38 @@ struct Mala {
     for (int i = 0; i < MD; ++i) o[i] = w * a.prop[i] + (1.0 - w) * a.S[i];
   }
 
-  CS_D void jvp1(const Aux &a, const double (&V)[MD], double (&o)[MD], bool relaxed) const {
-    double hv[MD], dprop[MD], hd[MD];
-    tg.hvp(a.S, V, hv);
+  template <typename TT = double>
+  CS_D void jvp1(const Aux &a, const double (&Vd)[MD], double (&o)[MD], bool relaxed) const {
+    TT V[MD], hv[MD], dprop[MD], hd[MD];
 #pragma unroll
-    for (int i = 0; i < MD; ++i) dprop[i] = V[i] + eps * hv[i];
-    tg.hvp(a.prop, dprop, hd);
-    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int i = 0; i < MD; ++i) V[i] = (TT)Vd[i];
+    tg.hvpT(a.S, V, hv);
+    const TT e = (TT)eps;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) dprop[i] = V[i] + e * hv[i];
+    tg.hvpT(a.prop, dprop, hd);
+    TT s1 = 0, s2 = 0, s3 = 0;
 #pragma unroll
     for (int i = 0; i < MD; ++i) {
-      double dback = (V[i] - dprop[i]) - eps * hd[i];
-      s1 += a.g1[i] * dprop[i];
-      s2 += a.g0[i] * V[i];
-      s3 += a.back[i] * dback;
+      const TT dback = (V[i] - dprop[i]) - e * hd[i];
+      s1 += (TT)a.g1[i] * dprop[i];
+      s2 += (TT)a.g0[i] * V[i];
+      s3 += (TT)a.back[i] * dback;
     }
-    const double ddelta = (s1 - s2) - s3 * inv2eps;
-    const double gate = relaxed ? expit(a.margin) : (a.margin > 0.0 ? 1.0 : 0.0);
-    const double bend = sigmoid_prime(a.margin) * (ddelta * (a.delta < 0.0 ? 1.0 : 0.0));
+    const TT ddelta = (s1 - s2) - s3 * (TT)inv2eps;
+    const TT gate = (TT)(relaxed ? expit(a.margin) : (a.margin > 0.0 ? 1.0 : 0.0));
+    const TT bend = (TT)sigmoid_prime(a.margin) * (ddelta * (TT)(a.delta < 0.0 ? 1.0 : 0.0));
 #pragma unroll
     for (int i = 0; i < MD; ++i)
-      o[i] = (gate * dprop[i] + (1.0 - gate) * V[i]) + (a.prop[i] - a.S[i]) * bend;
+      o[i] = (double)((gate * dprop[i] + ((TT)1 - gate) * V[i]) + (TT)(a.prop[i] - a.S[i]) * bend);
   }
 
-  template <int NT>
+  template <int NT, typename TT = double>
   CS_D void jvp_many(const Aux &a, const double (&V)[NT][MD], double (&o)[NT][MD], int n,
                      bool relaxed) const {
 #pragma unroll
     for (int k = 0; k < NT; ++k)
-      if (k < n) jvp1(a, V[k], o[k], relaxed);
+      if (k < n) jvp1<TT>(a, V[k], o[k], relaxed);
   }
 };
 
@@ -172,23 +176,28 @@ struct Hmc {
     for (int i = 0; i < MD; ++i) o[i] = w * a.xl[i] + (1.0 - w) * a.S[i];
   }
 
-  // tangents ride the forward integrator (samplers.py:353-381), all n at once
-  template <int NT>
+  // tangents ride the forward integrator (samplers.py:353-381), all n at once,
+  // in tangent precision TT; the positions they are linearised at stay f64
+  template <int NT, typename TT = double>
   CS_D void jvp_many(const Aux &a, const double (&V)[NT][MD], double (&o)[NT][MD], int n,
                      bool relaxed) const {
     const int D = dim();
-    double dx[NT][MD], dv[NT][MD], dh0[NT];
-    double x[MD], v[MD], g[MD], h[MD];
+    TT dx[NT][MD], dv[NT][MD], dh0[NT], h[MD];
+    double x[MD], v[MD], g[MD];
+    const TT e = (TT)eps, he = (TT)(0.5 * eps);
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       if (k >= n) continue;
-      tg.hvp(a.S, V[k], h);
-      double s = 0.0;
+      TT Vk[MD];
+#pragma unroll
+      for (int i = 0; i < MD; ++i) Vk[i] = (TT)V[k][i];
+      tg.hvpT(a.S, Vk, h);
+      TT s = 0;
 #pragma unroll
       for (int i = 0; i < MD; ++i) {
-        dx[k][i] = V[k][i];
-        dv[k][i] = (0.5 * eps) * h[i];
-        s += a.g0[i] * V[k][i];
+        dx[k][i] = Vk[i];
+        dv[k][i] = he * h[i];
+        s += (TT)a.g0[i] * Vk[i];
       }
       dh0[k] = -s;
     }
@@ -201,34 +210,34 @@ struct Hmc {
       for (int k = 0; k < NT; ++k) {
         if (k >= n) continue;
 #pragma unroll
-        for (int i = 0; i < MD; ++i) dx[k][i] = dx[k][i] + divm(eps * dv[k][i], i);
-        tg.hvp(x, dx[k], h);
+        for (int i = 0; i < MD; ++i) dx[k][i] = dx[k][i] + (TT)divm((double)(e * dv[k][i]), i);
+        tg.hvpT(x, dx[k], h);
 #pragma unroll
-        for (int i = 0; i < MD; ++i) dv[k][i] = dv[k][i] + eps * h[i];
+        for (int i = 0; i < MD; ++i) dv[k][i] = dv[k][i] + e * h[i];
       }
       tg.grad(x, g);
 #pragma unroll
       for (int i = 0; i < MD; ++i) v[i] = v[i] + eps * g[i];
     }
-    const double gate = relaxed ? expit(a.margin) : (a.margin > 0.0 ? 1.0 : 0.0);
-    const double sp = sigmoid_prime(a.margin);
-    const double neg = a.delta < 0.0 ? 1.0 : 0.0;
+    const TT gate = (TT)(relaxed ? expit(a.margin) : (a.margin > 0.0 ? 1.0 : 0.0));
+    const TT sp = (TT)sigmoid_prime(a.margin);
+    const TT neg = (TT)(a.delta < 0.0 ? 1.0 : 0.0);
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       if (k >= n) continue;
-      tg.hvp(x, dx[k], h);
-      double s1 = 0.0, s2 = 0.0;
+      tg.hvpT(x, dx[k], h);
+      TT s1 = 0, s2 = 0;
 #pragma unroll
       for (int i = 0; i < MD; ++i) {
-        double dvl = dv[k][i] - (0.5 * eps) * h[i];
-        if (i < D) s1 += divm(a.vl[i] * dvl, i);
-        s2 += a.gl[i] * dx[k][i];
+        const TT dvl = dv[k][i] - he * h[i];
+        if (i < D) s1 += (TT)divm((double)((TT)a.vl[i] * dvl), i);
+        s2 += (TT)a.gl[i] * dx[k][i];
       }
-      const double ddelta = dh0[k] - (s1 - s2);
-      const double bend = sp * (ddelta * neg);
+      const TT ddelta = dh0[k] - (s1 - s2);
+      const TT bend = sp * (ddelta * neg);
 #pragma unroll
       for (int i = 0; i < MD; ++i)
-        o[k][i] = (gate * dx[k][i] + (1.0 - gate) * V[k][i]) + (a.xl[i] - a.S[i]) * bend;
+        o[k][i] = (double)((gate * dx[k][i] + ((TT)1 - gate) * (TT)V[k][i]) + (TT)(a.xl[i] - a.S[i]) * bend);
     }
   }
 };
@@ -289,7 +298,7 @@ struct Leapfrog {
     }
   }
 
-  template <int NT>
+  template <int NT, typename TT = double>
   CS_D void jvp_many(const Aux &a, const double (&V)[NT][MD], double (&o)[NT][MD], int n,
                      bool) const {
 #pragma unroll
@@ -416,7 +425,7 @@ struct Gibbs {
     }
   }
 
-  template <int NT>
+  template <int NT, typename TT = double>
   CS_D void jvp_many(const Aux &a, const double (&V)[NT][MD], double (&o)[NT][MD], int n,
                      bool) const {
 #pragma unroll

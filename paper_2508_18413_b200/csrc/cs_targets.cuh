@@ -129,6 +129,55 @@ struct Target {
     }
   }
 
+  // tangent-precision Hessian-vector product: the curvature is formed from the
+  // f64 state, the product runs in TT (float tangents in fp32 storage mode)
+  template <typename TT>
+  CS_D void hvpT(const double (&x)[MD], const TT (&v)[MD], TT (&o)[MD]) const {
+    if constexpr (sizeof(TT) == sizeof(double)) {
+      hvp(x, v, o);
+    } else {
+      const int D = p.dim;
+      switch (kind()) {
+        case CS_TARGET_STD_NORMAL:
+#pragma unroll
+          for (int i = 0; i < MD; ++i) o[i] = -v[i];
+          return;
+        case CS_TARGET_GAUSSIAN:
+#pragma unroll
+          for (int j = 0; j < MD; ++j) {
+            TT s = 0;
+            if (j < D)
+#pragma unroll
+              for (int i = 0; i < MD; ++i) if (i < D) s += v[i] * (TT)__ldg(p.prec + i * D + j);
+            o[j] = -s;
+          }
+          return;
+        case CS_TARGET_ROSENBROCK: {
+          const double b = p.b;
+          const double x1 = x[0], x2 = x[MD > 1 ? 1 : 0];
+          const double r = x2 - b * x1 * x1;
+          const TT h11 = (TT)(-is1 + (2.0 * b * r - 4.0 * b * b * x1 * x1) * is2);
+          const TT h12 = (TT)(2.0 * b * x1 * is2), h22 = (TT)is2;
+          const TT v0 = v[0], v1 = v[MD > 1 ? 1 : 0];
+          o[0] = h11 * v0 + h12 * v1;
+          if (MD > 1) o[MD > 1 ? 1 : 0] = h12 * v0 - v1 * h22;
+#pragma unroll
+          for (int i = 2; i < MD; ++i) o[i] = 0;
+          return;
+        }
+        default: {
+          double vd[MD], od[MD];
+#pragma unroll
+          for (int i = 0; i < MD; ++i) vd[i] = (double)v[i];
+          hvp(x, vd, od);
+#pragma unroll
+          for (int i = 0; i < MD; ++i) o[i] = (TT)od[i];
+          return;
+        }
+      }
+    }
+  }
+
   CS_D void hvp(const double (&x)[MD], const double (&v)[MD], double (&o)[MD]) const {
     const int D = p.dim;
     switch (kind()) {

@@ -157,6 +157,15 @@ def _first_nonfinite(arr):
     return int(sc.i64.item())
 
 
+def _first_nonfinite_into(arr, out):
+    """Device-side first non-finite row (INT64_MAX if none) into out (1-elem i64)."""
+    arr = arr.contiguous()
+    width = arr[0].numel() if arr.shape[0] else 1
+    rc = _lib.load().cs_first_nonfinite_row(_lib.dtype_code(arr.dtype), _lib.ptr(arr), arr.shape[0], width,
+                                            _lib.ptr(out), _lib.stream_ptr())
+    _lib.check(rc)
+
+
 def _check_finite(arr, what, ts, iteration):
     row = _first_nonfinite(arr)
     if row != _NO_STEP:
@@ -171,7 +180,7 @@ def _pre_tensor(cfg, device):
     return torch.as_tensor(cfg.preconditioner, dtype=torch.float64, device=device)
 
 
-def _build_elements(system, ts, guess, s0_local, cfg, iteration, f, on_bad=None):
+def _build_elements(system, ts, guess, s0_local, cfg, iteration, f, on_bad=None, prev=None):
     """Jacobian estimate -> affine elements with preconditioner, damping and clip
     in the reference's order, u = f - Jhat prev (deer.py:157-204).
 
@@ -181,13 +190,17 @@ def _build_elements(system, ts, guess, s0_local, cfg, iteration, f, on_bad=None)
     lib = _lib.load()
     dt = _lib.dtype_code(guess.dtype)
     st = _lib.stream_ptr()
-    prev = torch.cat([s0_local[None], guess[:-1]], dim=0)
+    if prev is None:  # the caller's prev (same tensor as step_batch saw) keeps system caches warm
+        prev = torch.cat([s0_local[None], guess[:-1]], dim=0)
     f = f.to(guess.dtype).contiguous()
     T, W = guess.shape
     pre = _pre_tensor(cfg, guess.device)
     clip = float(cfg.clip)
 
     def finite_or(arr, what):
+        if isinstance(on_bad, torch.Tensor):  # deferred: first bad row lands on device
+            _first_nonfinite_into(arr, on_bad)
+            return
         row = _first_nonfinite(arr)
         if row == _NO_STEP:
             return
@@ -229,7 +242,7 @@ def _build_elements(system, ts, guess, s0_local, cfg, iteration, f, on_bad=None)
     return Block2x2Elements(*outs, u)
 
 
-def _iterate_range(system, ts, guess, s0_local, cfg, iteration, f=None):
+def _iterate_range(system, ts, guess, s0_local, cfg, iteration, f=None, prev=None):
     """One Newton update on the steps ts seeded from s0_local (deer.py:147-208)."""
     guess = guess.contiguous()
     s0_local = s0_local.contiguous()
@@ -237,7 +250,7 @@ def _iterate_range(system, ts, guess, s0_local, cfg, iteration, f=None):
         prev = torch.cat([s0_local[None], guess[:-1]], dim=0)
         f = system.step_batch(ts, prev)
         _check_finite(f, "step value", ts, iteration)
-    elements = _build_elements(system, ts, guess, s0_local, cfg, iteration, f)
+    elements = _build_elements(system, ts, guess, s0_local, cfg, iteration, f, prev=prev)
     return parallel_affine_solve(elements, s0_local)
 
 
@@ -509,20 +522,56 @@ def _run_host(system, s0, cfg, max_iters):
     iterations = 0
 
     if cfg.window_len is None or cfg.window_len >= T:
+        # one device->host read per iteration: the finite check of f, the Picard
+        # test, the Jacobian check and the post-update bookkeeping all land in a
+        # small device buffer, and the branch below replays deer.py:263-286 in order
         ts = torch.arange(1, T + 1, device=dev)
+        # 48-byte read-back: [0] bad-f row i64, [8] bad-jac row i64, [16] Picard fails u32,
+        # [24] Picard dmax f64, [32] fail rows u32, [40] update dmax f64
+        buf = torch.empty(48, dtype=torch.uint8, device=dev)
+        base = buf.data_ptr()
+        at = lambda off: ctypes.c_void_p(base + off)  # noqa: E731
+        backup = torch.empty_like(last_fail)
+        lib = _lib.load()
+        dt = _lib.dtype_code(guess.dtype)
         while True:
             prev = torch.cat([s0[None], guess[:-1]], dim=0)
-            f = system.step_batch(ts, prev).to(guess.dtype)
-            _check_finite(f, "step value", ts, iterations)
-            ok, _ = converged(guess, f, atol, rtol)
-            if ok:
+            f = system.step_batch(ts, prev).to(guess.dtype).contiguous()
+            _lib.check(lib.cs_first_nonfinite_row(dt, _lib.ptr(f), T, f.shape[1], at(0), _lib.stream_ptr()))
+            _lib.check(lib.cs_converged(dt, _lib.ptr(guess), _lib.ptr(f), guess.numel(), float(atol), float(rtol),
+                                        at(16), at(24), _lib.stream_ptr()))
+            update = iterations < max_iters
+            nxt = None
+            if update:
+                badj = buf[8:16].view(torch.int64)
+                badj.fill_(_NO_STEP)
+                el = _build_elements(system, ts, guess, s0, cfg, iterations, f, on_bad=badj, prev=prev)
+                nxt = parallel_affine_solve(el, s0)
+                backup.copy_(last_fail)
+                _lib.check(lib.cs_update_bookkeeping(dt, _lib.ptr(guess), _lib.ptr(nxt), T, guess.shape[1],
+                                                     float(atol), float(rtol), int(iterations + 1),
+                                                     _lib.ptr(last_fail), at(32), at(40), _lib.stream_ptr()))
+            raw = buf.cpu().numpy().tobytes()
+            bad_f, bad_j = (int(v) for v in np.frombuffer(raw[0:16], dtype=np.int64))
+            pic = int(np.frombuffer(raw[16:20], dtype=np.uint32)[0])
+            if bad_f != _NO_STEP:
+                t = int(ts[bad_f])
+                raise ChainDivergedError(f"non-finite step value at step {t} (iteration {iterations + 1})",
+                                         step=t, iteration=iterations + 1)
+            if pic == 0:
+                if update:
+                    last_fail.copy_(backup)
                 done = True
                 break
-            if iterations >= max_iters:
+            if not update:
                 break
-            nxt = _iterate_range(system, ts, guess, s0, cfg, iterations, f=f)
+            if bad_j != _NO_STEP:
+                t = int(ts[bad_j])
+                raise ChainDivergedError(f"non-finite jacobian at step {t} (iteration {iterations + 1})",
+                                         step=t, iteration=iterations + 1)
+            nfail = int(np.frombuffer(raw[32:36], dtype=np.uint32)[0])
+            dmax = float(np.frombuffer(raw[40:48], dtype=np.float64)[0])
             iterations += 1
-            nfail, dmax = _bookkeeping(guess, nxt, atol, rtol, iterations, last_fail, sc)
             history.append(dmax)
             if full is not None:
                 full.append(nxt.clone())
@@ -549,7 +598,7 @@ def _run_host(system, s0, cfg, max_iters):
                 continue
             if iterations >= max_iters:
                 break
-            nxt = _iterate_range(system, ts, guess[lo:hi], seed_state.clone(), cfg, iterations, f=f)
+            nxt = _iterate_range(system, ts, guess[lo:hi], seed_state.clone(), cfg, iterations, f=f, prev=prev)
             iterations += 1
             win_fail = torch.zeros(hi - lo, dtype=torch.int32, device=dev)
             nfail, dmax = _bookkeeping(guess[lo:hi].contiguous(), nxt, atol, rtol, 1, win_fail, sc)

@@ -13,6 +13,7 @@ contractions with cuBLAS GEMMs.
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -185,7 +186,19 @@ class MalaKernel(_Fused):
         return d
 
     # -- GEMM evaluation (logistic regression, wide Gaussians): samplers.py:95-145 --
+    # run_deer evaluates f_t(prev) and then the Hutchinson JVPs at the SAME prev;
+    # the gate terms (two gradient and two log-density GEMM passes) are cached
+    # for that batch so each JVP costs only its own two hvp GEMM pairs.
     def _gate(self, ts, S):
+        # identity (weakref) + version: a recycled allocation never hits
+        hit = getattr(self, "_gate_cache", None)
+        if (hit is not None and hit[0]() is S and hit[1]() is ts and hit[2] == (S._version, ts._version)):
+            return hit[3]
+        out = self._gate_eval(ts, S)
+        self._gate_cache = (weakref.ref(S), weakref.ref(ts), (S._version, ts._version), out)
+        return out
+
+    def _gate_eval(self, ts, S):
         eps, m = self.eps, self.model
         xi = _noise_table(self.noise, "xi", self.noise.T, torch.float64)[ts]
         S = S.to(torch.float64)

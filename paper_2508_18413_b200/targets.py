@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import weakref
 from dataclasses import dataclass, field
 from typing import Any
 
@@ -212,31 +213,48 @@ def model_logp_grad_hvp(spec: ModelSpec) -> TargetModel:
             term = torch.sum((r * gv)[..., None] * gk, dim=-2)
             curv = torch.sum(r / var, dim=-1)
             return term - curv[..., None] * v - gbar * torch.sum(gbar * v, dim=-1)[..., None]
-    else:  # blr: eta = beta X^T as a cuBLAS GEMM
+    else:  # blr: eta = beta X^T as a cuBLAS GEMM, shared by logp / grad / hvp
         X, y, prec = _t(p["X"], dev), _t(p["y"], dev), p["prior_precision"]
         keep.update(X=X, y=y)
         desc.n_data = X.shape[0]
         desc.X, desc.y, desc.prior_precision = X.data_ptr(), y.data_ptr(), prec
         dim = spec.dim
+        etas = []  # [(weakref(beta), version, eta, sigmoid(eta))], two most recent batches
+
+        def eta_of(beta, flat):
+            # MALA evaluates logp, grad and hvp at the current states and at the
+            # proposals; each batch's logits are formed once (weakref identity +
+            # version key, so a recycled allocation never hits)
+            for ref, ver, eta, pr in etas:
+                if ref() is beta and ver == beta._version:
+                    return eta, pr
+            eta = flat @ X.T
+            pr = torch.sigmoid(eta)
+            etas.insert(0, (weakref.ref(beta), beta._version, eta, pr))
+            del etas[2:]
+            return eta, pr
 
         def logp(beta):
-            flat, lead = _flat(f64(beta), dim)
-            eta = flat @ X.T
+            beta = f64(beta)
+            flat, lead = _flat(beta, dim)
+            eta, _ = eta_of(beta, flat)
             out = eta @ y - torch.logaddexp(torch.zeros((), dtype=eta.dtype, device=dev), eta).sum(dim=-1)
             out = out - 0.5 * prec * torch.sum(flat * flat, dim=-1)
             return out.reshape(lead)
 
         def grad(beta):
-            flat, lead = _flat(f64(beta), dim)
-            out = (y - torch.sigmoid(flat @ X.T)) @ X - prec * flat
+            beta = f64(beta)
+            flat, lead = _flat(beta, dim)
+            _, pr = eta_of(beta, flat)
+            out = (y - pr) @ X - prec * flat
             return out.reshape(lead + (dim,))
 
         def hvp(beta, v):
             beta = f64(beta)
             flat, lead = _flat(beta, dim)
             vflat, _ = _flat(f64(v).expand(beta.shape), dim)
-            pr = torch.sigmoid(flat @ X.T)
-            out = -((pr * (1.0 - pr) * (vflat @ X.T)) @ X) - prec * vflat
+            _, pr = eta_of(beta, flat)
+            out = -(((pr * (1.0 - pr)) * (vflat @ X.T)) @ X) - prec * vflat
             return out.reshape(lead + (dim,))
 
     tm = DeviceTarget(dim=spec.dim, logp=logp, grad=grad, hvp=hvp, spec=spec)
