@@ -25,6 +25,7 @@ constexpr int kHalf = kScanThreads / 2;
 template <int BASE, int NT, int BAR>
 struct Grp {
   static constexpr int kN = NT;
+  static constexpr int kBase = BASE;
   CS_D static int tid() { return (int)threadIdx.x - BASE; }
   CS_D static void sync() {
     if constexpr (BAR == 0) __syncthreads();
@@ -102,6 +103,56 @@ template <> struct ColElem<SCAN_BLOCK> {
   }
   CS_D ColElem up(int off) const {
     ColElem o;
+    o.A = __shfl_up_sync(0xffffffffu, A, off);
+    o.B = __shfl_up_sync(0xffffffffu, B, off);
+    o.C = __shfl_up_sync(0xffffffffu, C, off);
+    o.E = __shfl_up_sync(0xffffffffu, E, off);
+    o.ux = __shfl_up_sync(0xffffffffu, ux, off);
+    o.uv = __shfl_up_sync(0xffffffffu, uv, off);
+    return o;
+  }
+};
+
+// The same monoid in the storage precision T, for in-stage segment work.
+template <int VAR, typename T> struct SegE;
+template <typename T> struct SegE<SCAN_DIAG, T> {
+  static constexpr int W = 2;
+  T j, u;
+  CS_D void ident() { j = 1; u = 0; }
+  CS_D void push(const SegE &e) { u = e.j * u + e.u; j = e.j * j; }  // this <- e o this
+  CS_D void store(T *p) const { p[0] = j; p[1] = u; }
+  CS_D void load(const T *p) { j = p[0]; u = p[1]; }
+  CS_D void apply(double &x) const { x = (double)j * x + (double)u; }
+  CS_D ColElem<SCAN_DIAG> wide() const { ColElem<SCAN_DIAG> o; o.j = (double)j; o.u = (double)u; return o; }
+  CS_D SegE up(int off) const {
+    SegE o;
+    o.j = __shfl_up_sync(0xffffffffu, j, off);
+    o.u = __shfl_up_sync(0xffffffffu, u, off);
+    return o;
+  }
+};
+template <typename T> struct SegE<SCAN_BLOCK, T> {
+  static constexpr int W = 6;
+  T A, B, C, E, ux, uv;
+  CS_D void ident() { A = 1; B = 0; C = 0; E = 1; ux = 0; uv = 0; }
+  CS_D void push(const SegE &e) {
+    const T An = e.A * A + e.B * C, Bn = e.A * B + e.B * E, Cn = e.C * A + e.E * C, En = e.C * B + e.E * E;
+    const T xn = e.A * ux + e.B * uv + e.ux, vn = e.C * ux + e.E * uv + e.uv;
+    A = An; B = Bn; C = Cn; E = En; ux = xn; uv = vn;
+  }
+  CS_D void store(T *p) const { p[0] = A; p[1] = B; p[2] = C; p[3] = E; p[4] = ux; p[5] = uv; }
+  CS_D void load(const T *p) { A = p[0]; B = p[1]; C = p[2]; E = p[3]; ux = p[4]; uv = p[5]; }
+  CS_D void apply(double &x, double &v) const {
+    const double xn = (double)A * x + (double)B * v + (double)ux, vn = (double)C * x + (double)E * v + (double)uv;
+    x = xn; v = vn;
+  }
+  CS_D ColElem<SCAN_BLOCK> wide() const {
+    ColElem<SCAN_BLOCK> o;
+    o.A = A; o.B = B; o.C = C; o.E = E; o.ux = ux; o.uv = uv;
+    return o;
+  }
+  CS_D SegE up(int off) const {
+    SegE o;
     o.A = __shfl_up_sync(0xffffffffu, A, off);
     o.B = __shfl_up_sync(0xffffffffu, B, off);
     o.C = __shfl_up_sync(0xffffffffu, C, off);
@@ -218,9 +269,8 @@ CS_D void lookback_grouped(int64_t b, int ncol, const LookbackWs &ws, S0F s0x, S
   const int64_t t0 = g * kGroupTiles;
   // The two levels are independent: the first half of the group folds the
   // in-group prefix while the second half looks back over groups.
-  using H0 = Grp<G::kN == kScanThreads ? 0 : kHalf, G::kN / 2, 3>;
-  using H1 = Grp<(G::kN == kScanThreads ? 0 : kHalf) + G::kN / 2, G::kN / 2, 4>;
-  static_assert(G::kN == kHalf, "two-level look-back runs on one half of a warp-specialised CTA");
+  using H0 = Grp<G::kBase, G::kN / 2, 3>;
+  using H1 = Grp<G::kBase + G::kN / 2, G::kN / 2, 4>;
   if (tid < G::kN / 2) {
     // (1) in-group exclusive prefix over tiles t0 .. b-1 (lane l <-> tile t0+l)
     const int ht = H0::tid(), lane = ht & 31, wid = ht >> 5;
@@ -331,7 +381,7 @@ CS_D bool rows_tile_tma(const ScanArgs<ST> &a, int64_t b, int R) {
 }
 
 template <typename ST, int VAR>
-CS_D void rows_tile_issue(const ScanArgs<ST> &a, int64_t b, int R, ST *tile, uint64_t *bar) {
+CS_D void rows_tile_issue(const ScanArgs<ST> &a, int64_t b, int R, ST *tile, uint64_t *bar, uint64_t pol) {
   const int ncol = a.D;
   const int64_t row0 = b * R;
   const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
@@ -339,15 +389,15 @@ CS_D void rows_tile_issue(const ScanArgs<ST> &a, int64_t b, int R, ST *tile, uin
   const int64_t g0 = row0 * ncol;
   if constexpr (VAR == SCAN_DIAG) {
     mbar_expect_tx(bar, 2 * bytes);
-    bulk_g2s(tile, a.e0 + g0, bytes, bar);
-    bulk_g2s(tile + R * ncol, a.u + g0, bytes, bar);
+    bulk_g2s_hint(tile, a.e0 + g0, bytes, bar, pol);
+    bulk_g2s_hint(tile + R * ncol, a.u + g0, bytes, bar, pol);
   } else {
     mbar_expect_tx(bar, 6 * bytes);
-    bulk_g2s(tile, a.e0 + g0, bytes, bar);
-    bulk_g2s(tile + R * ncol, a.e1 + g0, bytes, bar);
-    bulk_g2s(tile + 2 * R * ncol, a.e2 + g0, bytes, bar);
-    bulk_g2s(tile + 3 * R * ncol, a.e3 + g0, bytes, bar);
-    bulk_g2s(tile + 4 * R * ncol, a.u + 2 * g0, 2 * bytes, bar);
+    bulk_g2s_hint(tile, a.e0 + g0, bytes, bar, pol);
+    bulk_g2s_hint(tile + R * ncol, a.e1 + g0, bytes, bar, pol);
+    bulk_g2s_hint(tile + 2 * R * ncol, a.e2 + g0, bytes, bar, pol);
+    bulk_g2s_hint(tile + 3 * R * ncol, a.e3 + g0, bytes, bar, pol);
+    bulk_g2s_hint(tile + 4 * R * ncol, a.u + 2 * g0, 2 * bytes, bar, pol);
   }
 }
 
@@ -366,246 +416,305 @@ CS_D void scan_stamp(const ScanArgs<ST> &a, int64_t b, int k) {
   if (a.probe && b * 16 + 16 <= a.probe_n) a.probe[b * 16 + k] = k == 0 ? smid() : gtimer();
 }
 
-// Warp-specialised persistent CTA: warps 0-3 produce (claim a tile, bulk-load
-// it, reduce, publish its aggregate), warps 4-7 consume (look back, replay,
-// bulk-store).  Tiles live in a ring of kRowsBufs shared-memory slots.  A
-// claimed tile's aggregate never waits on any look-back -- the producer only
-// claims into a free slot -- so successors that look back into it see it one
-// load + one reduction after the claim.
-constexpr int kRowsBufs = 3;
-using ProdGrp = Grp<0, kHalf, 1>;
-using ConsGrp = Grp<kHalf, kHalf, 2>;
+// Chained-chunk row scan.  A persistent grid of G CTAs (3 per SM) walks the
+// sequence in rounds: chunk q = r*G + j (CS stages of R rows) belongs to CTA
+// j.  Each CTA alternates two passes over its chunks, stage by stage, with
+// every thread loading its own column segment of the stage straight into
+// registers (all of a stage's loads in flight before the FMA chain starts):
+//   A(r)    read chunk (r, j), reduce it, publish its aggregate
+//   C(r-1)  look back for chunk (r-1, j)'s entry state, re-read the chunk,
+//           replay it and stream the states out
+// The look-back for a chunk runs a full round after its predecessors
+// published, so it resolves in a few L2 round trips instead of waiting on a
+// chain of in-flight tiles.  Loads carry L2 eviction hints (A: evict_last,
+// C: evict_first) so the re-read hits L2 when a round fits in it.  Chunks are
+// linked with the two-level (group) look-back.  HBM traffic is 20 B/element
+// (diag f32: j,u read twice, s written once) against 12 B/element for a
+// single pass; see DESIGN.md for why the single-pass variants lost.
+constexpr int kRowsMaxSlots = 8;
 
-CS_D bool mbar_test(uint64_t *bar, unsigned parity) {
-  unsigned ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-CS_D void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+struct RowsJob {  // position in a CTA's job stream: A(0) A(1) C(0) A(2) C(1) ... C(nr-1)
+  int64_t r;
+  int ph;  // 0: A(r), 1: C(r-1)
+  int s, ns;
+  int64_t q;
+};
+
+struct RowsGeom {
+  int64_t T, nchunks, nr;
+  int R, CS, G, j;
+  bool agg_only;
+  CS_D int stages_in(int64_t q) const {
+    const int64_t rows = T - q * (int64_t)CS * R;
+    const int64_t st = (rows + R - 1) / R;
+    return (int)(st < CS ? st : CS);
+  }
+  CS_D void settle(RowsJob &it) const {
+    while (it.r <= nr) {
+      const int64_t rr = it.ph == 0 ? it.r : it.r - 1;
+      const bool ok = (it.ph == 0 ? it.r < nr : (it.r >= 1 && !agg_only)) && rr * G + j < nchunks;
+      if (ok) {
+        it.q = rr * G + j;
+        it.ns = stages_in(it.q);
+        it.s = 0;
+        return;
+      }
+      if (it.ph == 0) it.ph = 1;
+      else { it.ph = 0; ++it.r; }
+    }
+  }
+  CS_D RowsJob first() const {
+    RowsJob it{0, 0, 0, 0, 0};
+    settle(it);
+    return it;
+  }
+  CS_D void next(RowsJob &it) const {
+    if (++it.s < it.ns) return;
+    if (it.ph == 0) it.ph = 1;
+    else { it.ph = 0; ++it.r; }
+    settle(it);
+  }
+  CS_D bool valid(const RowsJob &it) const { return it.r <= nr; }
+};
+
+// rows per thread segment per stage: the thread's loads for a stage are all
+// issued before its FMA chain starts (registers: NA * kSegRows values)
+template <typename ST, int VAR>
+struct RowsSeg {
+  static constexpr int kRows = VAR == SCAN_DIAG ? (sizeof(ST) == 4 ? 16 : 8) : (sizeof(ST) == 4 ? 4 : 2);
+};
+
+template <typename T>
+CS_D T ld_hint(const T *p, uint64_t pol) {
+  if constexpr (sizeof(T) == 4) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+  } else {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+  }
 }
 
 template <typename ST, int VAR, bool AGG_ONLY = false, bool UPDATE = false>
-__global__ void __launch_bounds__(kScanThreads)
-scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int tile_stride) {
+__global__ void __launch_bounds__(kScanThreads, 3)
+scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int stride, int NS) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = ColElem<VAR>::W;
-  constexpr int NB = kRowsBufs;
+  constexpr int KR = RowsSeg<ST, VAR>::kRows;
   using CT = ST;  // in-segment arithmetic type; everything crossing segments is f64
   const int ncol = a.D;
   const int SW = VAR == SCAN_DIAG ? ncol : 2 * ncol;
-  const int nseg = kHalf / ncol;
-  const int segw = (nseg + 1) * ncol * W;  // doubles per segment-aggregate slot
-  __shared__ int64_t s_tile[NB];
-  __shared__ int s_kc, s_done, s_gflag;
+  const int nseg = kScanThreads / ncol;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int c = tid % ncol, sg = tid / ncol;
+  const bool active = sg < nseg;
+  __shared__ double s_chunk[64 * W];    // A: running chunk aggregate
+  __shared__ double s_run[2 * 2 * 64];  // C: running chain state, double-buffered by stage parity
   __shared__ double s_entry[2 * 64];
   __shared__ double s_acc[64 * W];
   __shared__ double s_acc2[64 * W];
   __shared__ double s_gentry[2 * 64];
   __shared__ int s_ctl[1];
-  __shared__ unsigned s_nf;
+  __shared__ int s_gflag;
   __shared__ unsigned long long s_dm;
-  __shared__ __align__(8) uint64_t s_ld[NB], s_full[NB], s_empty[NB];
-  double *segagg0 = (double *)(smem_raw + NB * (size_t)tile_stride);
-  int *s_fail = (int *)(segagg0 + NB * segw);  // UPDATE: one flag per row (consumer)
-  auto buf = [&](int slot) { return (ST *)(smem_raw + (size_t)slot * tile_stride); };
+  CT *segagg = (CT *)smem_raw;                                // [2][nseg+1][ncol][W], by stage parity
+  int *s_fail = (int *)(segagg + 2 * (nseg + 1) * ncol * W);  // UPDATE: one flag per stage row
+  (void)stride;
+  (void)NS;
+  if constexpr (UPDATE)
+    for (int r = tid; r < R; r += kScanThreads) s_fail[r] = 0;
 
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NB; ++i) {
-      mbar_init(&s_ld[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 1);
-    }
-    fence_mbar_init();
-  }
+  RowsGeom geo;
+  geo.T = a.T;
+  geo.nchunks = nchunks;
+  geo.G = gridDim.x;
+  geo.j = blockIdx.x;
+  geo.R = R;
+  geo.CS = CS;
+  geo.nr = (nchunks + geo.G - 1) / geo.G;
+  geo.agg_only = AGG_ONLY;
+  // A keeps what it reads in L2 for C (one round later); C's reads are the last use
+  const uint64_t pol_a = l2_policy_evict_last(), pol_c = l2_policy_evict_first();
   __syncthreads();
 
-  if (threadIdx.x < kHalf) {
-    // ======================= producer =======================
-    const int tid = ProdGrp::tid();
-    const int c = tid % ncol, sg = tid / ncol;
-    const bool active = sg < nseg;
-    int kc = 0, kr = 0;  // tiles claimed / reduced by this CTA
-    bool done = false;
-    unsigned ldph = 0;   // bit i: parity of the next bulk-load completion on slot i
-    for (;;) {
-      if (tid == 0 && !done) {
-        while (kc < kr + NB) {
-          const int slot = kc % NB;
-          if (kc >= NB && !mbar_test(&s_empty[slot], ((kc / NB) - 1) & 1)) break;  // slot still busy
-          const int64_t t = atomicAdd(ws.ticket, 1u);
-          if (t >= ntiles) {
-            s_tile[slot] = -1;
-            mbar_arrive(&s_full[slot]);  // end marker for the consumer
-            done = true;
-            break;
-          }
-          s_tile[slot] = t;
-          scan_stamp(a, t, 1);
-          if (rows_tile_tma<ST, VAR>(a, t, R)) rows_tile_issue<ST, VAR>(a, t, R, buf(slot), &s_ld[slot]);
-          ++kc;
+  int64_t n = 0;
+  for (RowsJob cur = geo.first(); geo.valid(cur); geo.next(cur), ++n) {
+    const int64_t q = cur.q;
+    const int64_t stg = q * CS + cur.s;
+    const int64_t row0 = stg * R;
+    const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
+    if (cur.s == 0) {
+      if (cur.ph == 0) {
+        for (int cc = tid; cc < ncol; cc += kScanThreads) {
+          ColElem<VAR> id;
+          id.ident();
+          id.store(s_chunk + cc * W);
         }
-        s_kc = kc;
-        s_done = done;
-      }
-      ProdGrp::sync();
-      kc = s_kc;
-      done = s_done;
-      ProdGrp::sync();
-      if (kr == kc) {
-        if (done) break;
-        // nothing loaded: block until the consumer frees the next slot
-        if (tid == 0) mbar_wait(&s_empty[kc % NB], ((kc / NB) - 1) & 1);
-        ProdGrp::sync();
-        continue;
-      }
-      const int slot = kr % NB;
-      const int64_t b = s_tile[slot];
-      ST *tile = buf(slot);
-      double *segagg = segagg0 + slot * segw;
-      const int64_t row0 = b * R;
-      const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
-      if (rows_tile_tma<ST, VAR>(a, b, R)) {
-        mbar_wait(&s_ld[slot], (ldph >> slot) & 1u);
-        ldph ^= 1u << slot;
       } else {
-        const int nel = rows * ncol;
-        const int64_t g0 = row0 * ncol;
-        const ST *u_src = a.u + (VAR == SCAN_BLOCK ? 2 : 1) * g0;
-        for (int i = tid; i < nel; i += kHalf) {
-          tile[i] = a.e0[g0 + i];
-          if constexpr (VAR == SCAN_DIAG) {
-            tile[R * ncol + i] = u_src[i];
-          } else {
-            tile[R * ncol + i] = a.e1[g0 + i];
-            tile[2 * R * ncol + i] = a.e2[g0 + i];
-            tile[3 * R * ncol + i] = a.e3[g0 + i];
-          }
+        if (tid == 0) {
+          scan_stamp(a, q, 5);
+          s_dm = 0ull;
         }
-        if constexpr (VAR == SCAN_BLOCK)
-          for (int i = tid; i < 2 * nel; i += kHalf) tile[4 * R * ncol + i] = u_src[i];
-        ProdGrp::sync();
+        lookback_grouped<VAR, CtaGrp>(
+            q, ncol, ws, [&](int cc) { return (double)a.s0[cc]; },
+            [&](int cc) { return (double)a.s0[ncol + cc]; }, s_acc, s_acc2, s_entry, s_gentry, s_ctl,
+            [&](int k) { scan_stamp(a, q, k); });
+        for (int cc = tid; cc < SW; cc += kScanThreads) s_run[(n & 1) * 2 * 64 + cc] = s_entry[cc];
+        if (tid == 0) scan_stamp(a, q, 8);
       }
-      if (tid == 0) {
-        scan_stamp(a, b, 0);
-        scan_stamp(a, b, 2);
-      }
-      const int seglen = (rows + nseg - 1) / nseg;
-      const int r0 = sg * seglen, r1 = min(rows, r0 + seglen);
-      if (active) {
-        ColElem<VAR> run;
-        if constexpr (VAR == SCAN_DIAG) {
-          CT rj = 1, ru = 0;
-          for (int r = r0; r < r1; ++r) {
-            const int i = r * ncol + c;
-            const CT ej = (CT)tile[i];
-            ru = ej * ru + (CT)tile[R * ncol + i];
-            rj = ej * rj;
-          }
-          run.j = (double)rj;
-          run.u = (double)ru;
-        } else {
-          CT A = 1, B = 0, C = 0, E = 1, ux = 0, uv = 0;
-          for (int r = r0; r < r1; ++r) {
-            const int i = r * ncol + c;
-            const CT ea = (CT)tile[i], eb = (CT)tile[R * ncol + i], ec = (CT)tile[2 * R * ncol + i],
-                     ed = (CT)tile[3 * R * ncol + i];
-            const CT px = (CT)tile[4 * R * ncol + 2 * r * ncol + c],
-                     pv = (CT)tile[4 * R * ncol + 2 * r * ncol + ncol + c];
-            const CT An = ea * A + eb * C, Bn = ea * B + eb * E, Cn = ec * A + ed * C, En = ec * B + ed * E;
-            const CT xn = ea * ux + eb * uv + px, vn = ec * ux + ed * uv + pv;
-            A = An; B = Bn; C = Cn; E = En; ux = xn; uv = vn;
-          }
-          run.A = A; run.B = B; run.C = C; run.E = E; run.ux = ux; run.uv = uv;
-        }
-        run.store(segagg + (sg * ncol + c) * W);
-      }
-      ProdGrp::sync();
-      if (tid == 0) scan_stamp(a, b, 3);
-      // per-column exclusive scan over segments (warp per column, lane q holds
-      // segments [q*K, q*K+K)); publish the tile aggregate
-      {
-        const int lane = tid & 31, wid = tid >> 5;
-        const int K = (nseg + 31) / 32;
-        for (int cc = wid; cc < ncol; cc += kHalf / 32) {
-          ColElem<VAR> e;
-          e.ident();
-          for (int q = lane * K; q < lane * K + K && q < nseg; ++q) {
-            ColElem<VAR> x;
-            x.load(segagg + (q * ncol + cc) * W);
-            e.push(x);
-          }
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            ColElem<VAR> o = e.up(off);
-            if (lane >= off) e.pre(o);  // earlier lanes hold earlier segments
-          }
-          ColElem<VAR> ex = e.up(1);
-          if (lane == 0) ex.ident();
-          if (lane == 31) {
-            double tmp[W];
-            e.store(tmp);
-            double *g = ws.agg + (b * ncol + cc) * W;
-#pragma unroll
-            for (int q = 0; q < W; ++q) g[q] = tmp[q];
-            e.store(segagg + (nseg * ncol + cc) * W);
-          }
-          for (int q = lane * K; q < lane * K + K && q < nseg; ++q) {  // exclusive prefixes in place
-            ColElem<VAR> x;
-            x.load(segagg + (q * ncol + cc) * W);
-            ex.store(segagg + (q * ncol + cc) * W);
-            ex.push(x);
-          }
-        }
-        __threadfence();
-      }
-      ProdGrp::sync();
-      if (tid == 0) {
-        st_release(ws.status + b, 1);
-        scan_stamp(a, b, 4);
-        mbar_arrive(&s_full[slot]);
-      }
-      if constexpr (!AGG_ONLY) group_aggregate_publish<VAR, ProdGrp>(b, ncol, ws, &s_gflag);
-      ++kr;
     }
-  } else {
-    // ======================= consumer =======================
-    const int tid = ConsGrp::tid();
-    const int c = tid % ncol, sg = tid / ncol;
-    const bool active = sg < nseg;
-    int pend = -1;  // slot whose bulk store has not yet been confirmed read
-    for (int k = 0;; ++k) {
-      const int slot = k % NB;
-      mbar_wait(&s_full[slot], (k / NB) & 1);
-      const int64_t b = s_tile[slot];
-      if (b < 0) break;
-      if (tid == 0) scan_stamp(a, b, 5);
-      ST *tile = buf(slot);
-      const double *segagg = segagg0 + slot * segw;
-      if constexpr (AGG_ONLY) {
-        ConsGrp::sync();  // all consumers have read s_tile before the slot is recycled
-        if (tid == 0) mbar_arrive(&s_empty[slot]);
-        continue;
-      }
-      const int64_t row0 = b * R;
-      const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
-      lookback_grouped<VAR, ConsGrp>(
-          b, ncol, ws, [&](int cc) { return (double)a.s0[cc]; }, [&](int cc) { return (double)a.s0[ncol + cc]; }, s_acc,
-          s_acc2, s_entry, s_gentry, s_ctl, [&](int k) { scan_stamp(a, b, k); });
-      if (tid == 0) scan_stamp(a, b, 8);
+    const uint64_t pol = cur.ph == 0 ? pol_a : pol_c;
 
-      unsigned long long dmb = 0ull;
-      if constexpr (UPDATE) {
-        for (int r = tid; r < rows; r += kHalf) s_fail[r] = 0;
-        if (tid == 0) { s_nf = 0; s_dm = 0ull; }
-        ConsGrp::sync();
+    // ---- this thread's rows of the stage, straight from global into registers
+    const int r0 = sg * KR, r1 = min(rows, r0 + KR);
+    CT ev[VAR == SCAN_DIAG ? 2 : 6][KR];
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int r = r0 + k;
+        if (r < r1) {
+          const int64_t i = (row0 + r) * ncol + c;
+          if constexpr (VAR == SCAN_DIAG) {
+            ev[0][k] = (CT)ld_hint(a.e0 + i, pol);
+            ev[1][k] = (CT)ld_hint(a.u + i, pol);
+          } else {
+            ev[0][k] = (CT)ld_hint(a.e0 + i, pol);
+            ev[1][k] = (CT)ld_hint(a.e1 + i, pol);
+            ev[2][k] = (CT)ld_hint(a.e2 + i, pol);
+            ev[3][k] = (CT)ld_hint(a.e3 + i, pol);
+            ev[4][k] = (CT)ld_hint(a.u + 2 * (row0 + r) * ncol + c, pol);
+            ev[5][k] = (CT)ld_hint(a.u + 2 * (row0 + r) * ncol + ncol + c, pol);
+          }
+        } else {  // identity rows
+          if constexpr (VAR == SCAN_DIAG) {
+            ev[0][k] = 1;
+            ev[1][k] = 0;
+          } else {
+            ev[0][k] = 1; ev[1][k] = 0; ev[2][k] = 0; ev[3][k] = 1; ev[4][k] = 0; ev[5][k] = 0;
+          }
+        }
       }
+    }
+    // ---- segment aggregate (CT) -> segagg[par]
+    CT *sa = segagg + (n & 1) * (nseg + 1) * ncol * W;
+    if (active) {
+      SegE<VAR, CT> run;
+      run.ident();
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        SegE<VAR, CT> e;
+        if constexpr (VAR == SCAN_DIAG) {
+          e.j = ev[0][k];
+          e.u = ev[1][k];
+        } else {
+          e.A = ev[0][k]; e.B = ev[1][k]; e.C = ev[2][k]; e.E = ev[3][k]; e.ux = ev[4][k]; e.uv = ev[5][k];
+        }
+        run.push(e);
+      }
+      run.store(sa + (sg * ncol + c) * W);
+    }
+    __syncthreads();
+    if (nseg > 32) {
+      // narrow D: many segments per column -- warp scan per column (lane q
+      // holds segments [q*K, q*K+K)), exclusive prefixes in place, total in slot nseg
+      const int K = (nseg + 31) / 32;
+      for (int cc = wid; cc < ncol; cc += kScanThreads / 32) {
+        SegE<VAR, CT> e;
+        e.ident();
+        for (int qq = lane * K; qq < lane * K + K && qq < nseg; ++qq) {
+          SegE<VAR, CT> x;
+          x.load(sa + (qq * ncol + cc) * W);
+          e.push(x);
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          SegE<VAR, CT> o = e.up(off);
+          if (lane >= off) { o.push(e); e = o; }  // earlier lanes hold earlier segments
+        }
+        SegE<VAR, CT> ex = e.up(1);
+        if (lane == 0) ex.ident();
+        if (lane == 31) e.store(sa + (nseg * ncol + cc) * W);
+        for (int qq = lane * K; qq < lane * K + K && qq < nseg; ++qq) {
+          SegE<VAR, CT> x;
+          x.load(sa + (qq * ncol + cc) * W);
+          ex.store(sa + (qq * ncol + cc) * W);
+          ex.push(x);
+        }
+      }
+      __syncthreads();
+    }
+
+    if (cur.ph == 0) {
+      // ---- A: fold the stage into the chunk aggregate (f64); segagg is
+      // double-buffered, so the next stage does not wait for this
+      for (int cc = tid; cc < ncol; cc += kScanThreads) {
+        ColElem<VAR> ch;
+        ch.load(s_chunk + cc * W);
+        if (nseg > 32) {
+          SegE<VAR, CT> x;
+          x.load(sa + (nseg * ncol + cc) * W);
+          ch.push(x.wide());
+        } else {
+          for (int qq = 0; qq < nseg; ++qq) {
+            SegE<VAR, CT> x;
+            x.load(sa + (qq * ncol + cc) * W);
+            ch.push(x.wide());
+          }
+        }
+        ch.store(s_chunk + cc * W);
+      }
+      if (cur.s == cur.ns - 1) {  // publish the chunk aggregate after its last stage
+        __syncthreads();
+        for (int cc = tid; cc < ncol * W; cc += kScanThreads) ws.agg[q * ncol * W + cc] = s_chunk[cc];
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+          st_release(ws.status + q, 1);
+          scan_stamp(a, q, 4);
+        }
+        if constexpr (!AGG_ONLY) group_aggregate_publish<VAR, CtaGrp>(q, ncol, ws, &s_gflag);
+      }
+      continue;
+    }
+
+    // ---- C: entry state of each segment = (segments before it) o running state
+    double *run_in = s_run + (n & 1) * 2 * 64, *run_out = s_run + ((n + 1) & 1) * 2 * 64;
+    if (active) {
+      SegE<VAR, CT> pre;
+      pre.ident();
+      if (nseg <= 32) {
+        for (int qq = 0; qq < sg; ++qq) {
+          SegE<VAR, CT> x;
+          x.load(sa + (qq * ncol + c) * W);
+          pre.push(x);
+        }
+      } else {
+        pre.load(sa + (sg * ncol + c) * W);  // exclusive prefix from the warp scan
+      }
+      double xe = run_in[c], ve = VAR == SCAN_BLOCK ? run_in[ncol + c] : 0.0;
+      if (sg == nseg - 1) {  // the last segment carries the running state to the next stage
+        SegE<VAR, CT> tot = pre;
+        if (nseg <= 32) {
+          SegE<VAR, CT> own;
+          own.load(sa + (sg * ncol + c) * W);
+          tot.push(own);
+        } else {
+          tot.load(sa + (nseg * ncol + c) * W);
+        }
+        double xo = xe, vo = ve;
+        if constexpr (VAR == SCAN_DIAG) tot.apply(xo);
+        else tot.apply(xo, vo);
+        run_out[c] = xo;
+        if constexpr (VAR == SCAN_BLOCK) run_out[ncol + c] = vo;
+      }
+      if constexpr (VAR == SCAN_DIAG) pre.apply(xe);
+      else pre.apply(xe, ve);
+
+      // ---- replay from registers; states stream straight out (lanes of a warp
+      // cover whole rows, so each store instruction writes contiguous runs)
+      unsigned long long dmb = 0ull;
       auto check = [&](int r, int col, double xv) {  // deer.py:273-275 on the stored value
         if constexpr (UPDATE) {
           const double gap = fabs(xv - (double)a.guess[(row0 + r) * SW + col]);
@@ -614,96 +723,55 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles, int tile_stride)
           dmb = gb > dmb ? gb : dmb;
         }
       };
-      const int seglen = (rows + nseg - 1) / nseg;
-      const int r0 = sg * seglen, r1 = min(rows, r0 + seglen);
-      if (active && r0 < r1) {
-        ColElem<VAR> pre;
-        pre.load(segagg + (sg * ncol + c) * W);
-        if constexpr (VAR == SCAN_DIAG) {
-          double xe = s_entry[c];
-          pre.apply(xe);
-          CT x = (CT)xe;
-          for (int r = r0; r < r1; ++r) {
-            const int i = r * ncol + c;
-            x = (CT)tile[i] * x + (CT)tile[R * ncol + i];
-            tile[i] = (ST)x;
-            check(r, c, (double)x);
+      ST *o = a.out + row0 * SW + c;
+      if constexpr (VAR == SCAN_DIAG) {
+        CT x = (CT)xe;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          x = ev[0][k] * x + ev[1][k];
+          if (r0 + k < r1) {
+            __stcs(o + (int64_t)(r0 + k) * SW, (ST)x);
+            check(r0 + k, c, (double)x);
           }
-        } else {
-          double xe = s_entry[c], ve = s_entry[ncol + c];
-          pre.apply(xe, ve);
-          CT x = (CT)xe, v = (CT)ve;
-          for (int r = r0; r < r1; ++r) {
-            const int i = r * ncol + c;
-            const CT xa = (CT)tile[i] * x + (CT)tile[R * ncol + i] * v + (CT)tile[4 * R * ncol + 2 * r * ncol + c];
-            const CT va = (CT)tile[2 * R * ncol + i] * x + (CT)tile[3 * R * ncol + i] * v +
-                          (CT)tile[4 * R * ncol + 2 * r * ncol + ncol + c];
-            x = xa;
-            v = va;
-            // [x | v] rows overwrite the u tile in place (same thread, same slots)
-            tile[4 * R * ncol + 2 * r * ncol + c] = (ST)x;
-            tile[4 * R * ncol + 2 * r * ncol + ncol + c] = (ST)v;
-            check(r, c, (double)x);
-            check(r, ncol + c, (double)v);
+        }
+      } else {
+        CT x = (CT)xe, v = (CT)ve;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          const CT xa = ev[0][k] * x + ev[1][k] * v + ev[4][k];
+          const CT va = ev[2][k] * x + ev[3][k] * v + ev[5][k];
+          x = xa;
+          v = va;
+          if (r0 + k < r1) {
+            __stcs(o + (int64_t)(r0 + k) * SW, (ST)x);
+            __stcs(o + (int64_t)(r0 + k) * SW + ncol, (ST)v);
+            check(r0 + k, c, (double)x);
+            check(r0 + k, ncol + c, (double)v);
           }
         }
       }
       if constexpr (UPDATE) {
-        ConsGrp::sync();
-        unsigned nf = 0;
-        for (int r = tid; r < rows; r += kHalf)
-          if (s_fail[r]) {
-            a.last_fail[row0 + r] = a.it;
-            ++nf;
-          }
-        nf = (unsigned)warp_sum_i((int)nf);
         dmb = warp_max_u64(dmb);
-        if ((tid & 31) == 0) {
-          if (nf) atomicAdd(&s_nf, nf);
-          atomicMax(&s_dm, dmb);
-        }
-        ConsGrp::sync();
-        if (tid == 0) {
-          if (s_nf) atomicAdd(&a.stats->fail_rows, s_nf);
-          atomicMax((unsigned long long *)&a.stats->dmax, s_dm);
-        }
+        if (lane == 0) atomicMax(&s_dm, dmb);
       }
-      const ST *src = VAR == SCAN_DIAG ? tile : tile + 4 * R * ncol;
-      const int64_t g0 = row0 * SW;
-      const unsigned obytes = (unsigned)(sizeof(ST) * rows * SW);
-      if (rows_tile_tma<ST, VAR>(a, b, R) && aligned16(a.out + g0) && obytes % 16 == 0) {
-        fence_proxy_async_smem();
-        ConsGrp::sync();
-        if (tid == 0) {
-          scan_stamp(a, b, 9);
-          bulk_s2g(a.out + g0, src, obytes);
-          bulk_commit();
-          // free the previous slot once its store has been read out of smem
-          if (pend >= 0) {
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            mbar_arrive(&s_empty[pend]);
-          }
-        }
-        pend = slot;
-      } else {
-        ConsGrp::sync();
-        const int nout = rows * SW;
-        for (int i = tid; i < nout; i += kHalf) a.out[g0 + i] = src[i];
-        ConsGrp::sync();
-        if (tid == 0) {
-          if (pend >= 0) {
-            bulk_wait_read();
-            mbar_arrive(&s_empty[pend]);
-          }
-          mbar_arrive(&s_empty[slot]);
-        }
-        pend = -1;
-      }
+    } else if constexpr (UPDATE) {
+      const unsigned long long z = warp_max_u64(0ull);
+      if (lane == 0) atomicMax(&s_dm, z);
     }
-    if (tid == 0) {
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      if (pend >= 0) mbar_arrive(&s_empty[pend]);
+    if constexpr (UPDATE) {
+      __syncthreads();  // every row's flag is final
+      unsigned nf = 0;
+      for (int r = tid; r < rows; r += kScanThreads)
+        if (s_fail[r]) {
+          a.last_fail[row0 + r] = a.it;
+          s_fail[r] = 0;
+          ++nf;
+        }
+      nf = (unsigned)warp_sum_i((int)nf);
+      if (lane == 0 && nf) atomicAdd(&a.stats->fail_rows, nf);
+      if (tid == 0 && cur.s == cur.ns - 1) atomicMax((unsigned long long *)&a.stats->dmax, s_dm);
     }
+    if (tid == 0 && cur.s == cur.ns - 1) scan_stamp(a, q, 9);
   }
 }
 
@@ -1130,14 +1198,24 @@ __global__ void k_agg_compose_dense(const double *agg, int64_t ntiles, int D, do
 // host launchers
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+static int env_int(const char *name, int lo, int hi, int dflt) {
+  const char *e = getenv(name);
+  const int v = e ? atoi(e) : 0;
+  return v >= lo && v <= hi ? v : dflt;
+}
+static int rows_chunk_stages() {  // tuning override for experiments
+  static const int v = env_int("CS_SCAN_CHUNK_STAGES", 1, 256, 16);
+  return v;
+}
+static int rows_slots() {
+  static const int v = env_int("CS_SCAN_SLOTS", 3, kRowsMaxSlots, 6);
+  return v;
+}
+
 static int rows_per_tile(int var, int dtype, int D) {
   const int esz = dtype == CS_F64 ? 8 : 4;
   const int per = (var == SCAN_DIAG ? 2 : 6) * esz;
-  static const int tile_kb = [] {  // tuning override for experiments
-    const char *e = getenv("CS_SCAN_TILE_KB");
-    const int v = e ? atoi(e) : 0;
-    return v >= 4 && v <= 96 ? v : 32;
-  }();
+  static const int tile_kb = env_int("CS_SCAN_TILE_KB", 4, 96, 16);
   int E = (tile_kb * 1024) / per;
   int R = E / D;
   if (R > 8192) R = 8192;
@@ -1160,19 +1238,18 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
     p.state_w = p.md;
   } else if (D <= 64) {
     p.kind = 0;
-    p.R = rows_per_tile(var, dtype, D);
-    p.ntiles = (T + p.R - 1) / p.R;
+    const int nseg = kScanThreads / D;
+    const int kr = var == SCAN_DIAG ? (dtype == CS_F64 ? 8 : 16) : (dtype == CS_F64 ? 2 : 4);  // RowsSeg
+    p.R = nseg * kr;                      // rows per stage
+    p.seg = rows_chunk_stages();          // stages per chunk
+    p.ntiles = (T + (int64_t)p.R * p.seg - 1) / ((int64_t)p.R * p.seg);  // chunks
     p.agg_w = D * (var == SCAN_DIAG ? 2 : 6);
     p.state_w = var == SCAN_DIAG ? D : 2 * D;
     const int esz = dtype == CS_F64 ? 8 : 4;
-    const int NA = var == SCAN_DIAG ? 2 : 6;
-    const int nseg = kScanThreads / D;
     const int W = var == SCAN_DIAG ? 2 : 6;
-    // ring of tile slots, one segment-aggregate slot per tile slot, row flags
-    const int nseg_h = kHalf / D;
-    p.win = (int)(((size_t)esz * NA * p.R * D + 127) / 128 * 128);  // tile slot stride
-    p.smem = kRowsBufs * (size_t)p.win + sizeof(double) * kRowsBufs * (nseg_h + 1) * D * W + sizeof(int) * p.R;
-    (void)nseg;
+    p.win = 0;
+    p.md = 0;
+    p.smem = (size_t)esz * 2 * (nseg + 1) * D * W + sizeof(int) * p.R + 16;
   } else {
     p.kind = 1;
     const int ncb = (D + 31) / 32;
@@ -1221,7 +1298,7 @@ static unsigned rows_grid(const ScanPlan &p, const void *k) {
 template <typename ST, int VAR, bool UPD>
 static void launch_rows(const ScanPlan &p, const ScanArgs<ST> &a, LookbackWs w, cudaStream_t st) {
   auto k = scan_rows<ST, VAR, false, UPD>;
-  k<<<rows_grid(p, (const void *)k), kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
+  k<<<rows_grid(p, (const void *)k), kScanThreads, p.smem, st>>>(a, w, p.R, p.seg, p.ntiles, p.win, p.md);
 }
 
 template <typename ST>
@@ -1268,11 +1345,11 @@ cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, doub
   if (p.kind == 0) {
     if (p.var == SCAN_DIAG) {
       const void *kf = (const void *)scan_rows<ST, SCAN_DIAG, true>;
-      scan_rows<ST, SCAN_DIAG, true><<<rows_grid(p, kf), kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
+      scan_rows<ST, SCAN_DIAG, true><<<rows_grid(p, kf), kScanThreads, p.smem, st>>>(a, w, p.R, p.seg, p.ntiles, p.win, p.md);
       k_agg_compose_cols<SCAN_DIAG><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
     } else {
       const void *kf = (const void *)scan_rows<ST, SCAN_BLOCK, true>;
-      scan_rows<ST, SCAN_BLOCK, true><<<rows_grid(p, kf), kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles, p.win);
+      scan_rows<ST, SCAN_BLOCK, true><<<rows_grid(p, kf), kScanThreads, p.smem, st>>>(a, w, p.R, p.seg, p.ntiles, p.win, p.md);
       k_agg_compose_cols<SCAN_BLOCK><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
     }
   } else if (p.kind == 1) {

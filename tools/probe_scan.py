@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--trace", action="store_true", help="per-tile phase timeline (cs_debug_probe)")
+    ap.add_argument("--agg", action="store_true", help="also time the aggregate-only (reduce) pass")
     a = ap.parse_args()
     dt = torch.float32 if a.dtype == "f32" else torch.float64
     dev = torch.device("cuda")
@@ -48,6 +49,26 @@ def main():
         ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
     print(f"{a.mode} T={T} D={D} {a.dtype}: {ms:.3f} ms  {byts / ms / 1e6:.1f} GB/s (algorithmic {byts / 1e6:.0f} MB)")
+    if a.agg and a.mode == "diag":
+        from paper_2508_18413_b200 import _lib
+        lib = _lib.load()
+        dtc = 1 if dt == torch.float64 else 0
+        wsb = lib.cs_scan_workspace_bytes(1, dtc, T, D)
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+        agg = torch.empty(2 * D, dtype=torch.float64, device=dev)
+        ta = []
+        for _ in range(a.reps):
+            flush.fill_(0.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            lib.cs_scan_aggregate(1, dtc, el.j.data_ptr(), None, None, None, el.u.data_ptr(), T, D, agg.data_ptr(),
+                                  ws.data_ptr(), wsb, None)
+            e1.record()
+            torch.cuda.synchronize()
+            ta.append(e0.elapsed_time(e1))
+        ma = float(np.median(ta))
+        print(f"  aggregate-only: {ma:.3f} ms  {2 * T * D * es / ma / 1e6:.1f} GB/s read")
     if a.trace:
         from paper_2508_18413_b200 import _lib
         n = min(T, 1 << 20)
@@ -59,21 +80,17 @@ def main():
         torch.cuda.synchronize()
         _lib.load().cs_debug_probe(None, 0)
         tr = buf.view(-1, 16).cpu().numpy().astype(np.int64)
-        idx = np.nonzero(tr[:, 1] > 0)[0]
+        idx = np.nonzero(tr[:, 4] > 0)[0]
         tr = tr[idx]
         nt = len(tr)
-        t0 = tr[:, 1].min()
-        st = {k: tr[:, k] - t0 for k in range(1, 10)}
+        t0 = tr[:, 4].min()
+        st = {k: tr[:, k] - t0 for k in range(4, 10)}
         span = st[9].max()
         q = lambda x: " ".join(f"{v / 1e3:7.2f}" for v in np.percentile(x, [10, 50, 90, 99]))
-        print(f"tiles={nt} span={span / 1e3:.1f}us; steady state = tiles claimed in the middle half (us, p10/50/90/99)")
-        inflight = [int(np.sum((st[1] <= t) & (st[9] > t))) for t in np.linspace(span * 0.2, span * 0.8, 7)]
-        print(f"  tiles in flight: {inflight}; SMs used: {np.unique(tr[:, 0]).size}")
-        m = (st[1] > 0.25 * span) & (st[1] < 0.75 * span)
-        print(f"  claims per us (steady): {m.sum() / (0.5 * span / 1e3):.1f}")
-        names = {1: "claim", 2: "p.start", 3: "p.reduced", 4: "p.published", 5: "c.start", 6: "c.ingroup",
-                 7: "c.groups", 8: "c.entry", 9: "c.store"}
-        for k0, k1 in ((1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (5, 7), (7, 8), (8, 9), (1, 9)):
+        print(f"chunks={nt} span={span / 1e3:.1f}us (us, p10/50/90/99 over the middle half)")
+        m = (st[4] > 0.25 * span) & (st[4] < 0.75 * span)
+        names = {4: "A.published", 5: "C.start", 6: "C.ingroup", 7: "C.groups", 8: "C.entry", 9: "C.laststore"}
+        for k0, k1 in ((4, 5), (5, 6), (5, 7), (7, 8), (5, 8), (8, 9)):
             print(f"  {names[k0]:>11s}->{names[k1]:<11s} {q((st[k1] - st[k0])[m])}")
 
 
