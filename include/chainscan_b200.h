@@ -230,6 +230,11 @@ typedef struct cs_elem_stats {
 int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtype, int64_t iteration,
                        const void *s0, const void *guess, void *e0, void *e1, void *e2, void *e3,
                        void *u, cs_elem_stats *d_stats, void *stream);
+/* 1 when cs_system_elements can build elements for (sys, mode, dtype): the
+ * register builders (narrow built-in systems) or, for a leapfrog system on a
+ * dense Gaussian target in block2x2 mode at any dimension, the GEMM-backed
+ * builder (samplers.py:165-222; one cuBLAS DGEMM per iteration). */
+int cs_system_elements_supported(const cs_system *sys, int32_t mode, int dtype);
 /* Scans with the post-update bookkeeping fused into the replay (deer.py:273-277):
  * rows of `out` that moved more than atol + rtol|out| from `guess` get
  * last_fail[t] = iteration; d_stats->fail_rows / dmax are accumulated. */

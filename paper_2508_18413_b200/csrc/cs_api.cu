@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <string>
 
+#include "cs_dispatch.h"
 #include "cs_gen_tables.h"
 #include "cs_noise.cuh"
 #include "cs_scan.cuh"
@@ -127,6 +128,37 @@ __global__ void k_bookkeeping(const ST *guess, const ST *next, int64_t T, int D,
   cnt = (unsigned)warp_sum_i((int)cnt);
   dm = warp_max_u64(dm);
   if ((threadIdx.x & 31) == 0) {
+    if (cnt) atomicAdd(nfail, cnt);
+    atomicMax(dmax, dm);
+  }
+}
+
+// wide rows (D >= 32): one warp per row, lanes across the state
+template <typename ST>
+__global__ void k_bookkeeping_wide(const ST *guess, const ST *next, int64_t T, int D, double atol,
+                                   double rtol, int iteration, int32_t *last_fail, unsigned *nfail,
+                                   unsigned long long *dmax) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned cnt = 0;
+  unsigned long long dm = 0ull;
+  for (int64_t r = w0; r < T; r += nw) {
+    int f = 0;
+    for (int d = lane; d < D; d += 32) {
+      const double nx = (double)next[r * D + d];
+      const double gap = fabs(nx - (double)guess[r * D + d]);
+      f |= gap > atol + rtol * fabs(nx);
+      const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
+      dm = gb > dm ? gb : dm;
+    }
+    if (__any_sync(0xffffffffu, f)) {
+      if (lane == 0) { last_fail[r] = iteration; ++cnt; }
+    }
+  }
+  cnt = (unsigned)warp_sum_i((int)cnt);
+  dm = warp_max_u64(dm);
+  if (lane == 0) {
     if (cnt) atomicAdd(nfail, cnt);
     atomicMax(dmax, dm);
   }
@@ -415,7 +447,13 @@ int cs_update_bookkeeping(int dtype, const void *guess, const void *next, int64_
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   cudaMemsetAsync(d_fail_rows, 0, sizeof(uint32_t), S(stream));
   cudaMemsetAsync(d_dmax, 0, sizeof(double), S(stream));
-  if (T > 0) {
+  if (T > 0 && D >= 32) {
+    const int64_t threads = T * 32;
+    if (dtype == CS_F64)
+      k_bookkeeping_wide<double><<<grid_for(threads, 256), 256, 0, S(stream)>>>((const double *)guess, (const double *)next, T, D, atol, rtol, iteration, last_fail, d_fail_rows, (unsigned long long *)d_dmax);
+    else
+      k_bookkeeping_wide<float><<<grid_for(threads, 256), 256, 0, S(stream)>>>((const float *)guess, (const float *)next, T, D, atol, rtol, iteration, last_fail, d_fail_rows, (unsigned long long *)d_dmax);
+  } else if (T > 0) {
     if (dtype == CS_F64)
       k_bookkeeping<double><<<grid_for(T, 256), 256, 0, S(stream)>>>((const double *)guess, (const double *)next, T, D, atol, rtol, iteration, last_fail, d_fail_rows, (unsigned long long *)d_dmax);
     else
@@ -546,6 +584,15 @@ int cs_system_sequential(const cs_system *sys, int dtype, const void *s0, int64_
 }
 
 // ---- fused element builder + update scans (the streamed solver path) ---------------
+int cs_system_elements_supported(const cs_system *sys, int32_t mode, int dtype) {
+  if (!sys || !dtype_ok(dtype)) return 0;
+  if (mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG) return 0;
+  int md = 0;
+  if (sys->kind == CS_SYS_GIBBS) md = (sys->dim == 18 && mode == CS_MODE_DIAG) ? 18 : 0;
+  else if (sys->target.kind != CS_TARGET_BLR) md = elem_md(sys->kind, sys->target.kind, sys->dim);
+  return md > 0 || wide_leapfrog_ok(*sys, mode) ? 1 : 0;
+}
+
 static int elem_width(const cs_system *sys) {
   if (sys->kind == CS_SYS_GIBBS) return sys->dim == 18 ? 18 : 0;
   if (sys->target.kind == CS_TARGET_BLR) return 0;
@@ -558,13 +605,18 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
   if (!sys || !cfg || !d_stats) return fail(CS_ERR_CONFIG, "null argument");
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   const int md = elem_width(sys);
-  if (!md) return fail(CS_ERR_CONFIG, "no fused element builder for this system");
+  const bool wide = !md && wide_leapfrog_ok(*sys, cfg->mode);
+  if (!md && !wide) return fail(CS_ERR_CONFIG, "no fused element builder for this system");
   if (cfg->mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG)
     return fail(CS_ERR_CONFIG, "system does not provide a block2x2 Jacobian estimate");
   cudaStream_t st = S(stream);
   k_init_stats<<<1, 1, 0, st>>>(d_stats);
   if (sys->T < 1) return CS_OK;
   cudaError_t e;
+  if (wide) {
+    e = elements_wide(*sys, *cfg, dtype, iteration, s0, guess, e0, e1, e2, e3, u, d_stats, st);
+    return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements (wide leapfrog, cuBLAS)");
+  }
   if (dtype == CS_F64) {
     SolveArgs<double> A{};
     A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;

@@ -7,4 +7,8 @@ cudaError_t syscall_gibbs(const cs_system &, int dtype, int md, const SysCall &,
 cudaError_t solve_gibbs(int dtype, int md, int mode, void *args, int sms, cudaStream_t, SolvePick *);
 cudaError_t elements_gibbs(int dtype, int md, int mode, void *args, int it, const void *g, void *e0, void *e1,
                            void *e2, void *e3, void *u, cs_elem_stats *stats, cudaStream_t st);
+bool wide_leapfrog_ok(const cs_system &s, int mode);
+cudaError_t elements_wide(const cs_system &sys, const cs_deer_config &cfg, int dtype, int64_t iteration,
+                          const void *s0, const void *guess, void *e0, void *e1, void *e2, void *e3, void *u,
+                          cs_elem_stats *stats, cudaStream_t st);
 }  // namespace cs

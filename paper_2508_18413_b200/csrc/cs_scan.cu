@@ -1207,6 +1207,14 @@ static int rows_chunk_stages() {  // tuning override for experiments
   static const int v = env_int("CS_SCAN_CHUNK_STAGES", 1, 256, 16);
   return v;
 }
+static int rows_resident_ctas() {  // persistent grid of scan_rows: 3 CTAs per SM (launch bounds)
+  static const int v = [] {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return 3 * (sms > 0 ? sms : 148);
+  }();
+  return v;
+}
 static int rows_slots() {
   static const int v = env_int("CS_SCAN_SLOTS", 3, kRowsMaxSlots, 6);
   return v;
@@ -1241,7 +1249,17 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
     const int nseg = kScanThreads / D;
     const int kr = var == SCAN_DIAG ? (dtype == CS_F64 ? 8 : 16) : (dtype == CS_F64 ? 2 : 4);  // RowsSeg
     p.R = nseg * kr;                      // rows per stage
-    p.seg = rows_chunk_stages();          // stages per chunk
+    // stages per chunk: large chunks amortise the per-chunk look-back, but
+    // every resident CTA needs chunks -- aim for >= 2 rounds of the grid
+    {
+      const int64_t stages = (T + p.R - 1) / p.R;
+      const int64_t g = (int64_t)rows_resident_ctas();
+      int64_t cs = stages / (2 * g);
+      const int cmax = rows_chunk_stages();
+      if (cs > cmax) cs = cmax;
+      if (cs < 1) cs = 1;
+      p.seg = (int)cs;
+    }
     p.ntiles = (T + (int64_t)p.R * p.seg - 1) / ((int64_t)p.R * p.seg);  // chunks
     p.agg_w = D * (var == SCAN_DIAG ? 2 : 6);
     p.state_w = var == SCAN_DIAG ? D : 2 * D;

@@ -260,8 +260,11 @@ CS_D void probe_stamp(unsigned long long *buf, int n, int it, int k) {
 }
 
 // ---------------------------------------------------------------------------
+#ifndef CS_SOLVE_MIN_BLOCKS
+#define CS_SOLVE_MIN_BLOCKS 2
+#endif
 template <class Sys, int MODE, int MD, typename ST, bool KEEP>
-__global__ void __launch_bounds__(kSolveThreads)
+__global__ void __launch_bounds__(kSolveThreads, CS_SOLVE_MIN_BLOCKS)
 deer_persistent(SolveArgs<ST> A) {
   using E = Elem<MODE, MD>;
   // KEEP: the segment's elements wait in shared memory across the grid sync,

@@ -280,9 +280,15 @@ def _bookkeeping(guess, nxt, atol, rtol, iteration, last_fail, sc):
 
 
 def _builtin_ok(system, cfg):
-    """Built-in system on the register kernels, no window / full trace."""
-    if getattr(system, "desc", None) is None or cfg.full_trace or not getattr(system, "kernels", False):
+    """Built-in system whose elements the library builds (register kernels, or
+    the GEMM-backed wide leapfrog builder), no window / full trace."""
+    if getattr(system, "desc", None) is None or cfg.full_trace:
         return False
+    if not getattr(system, "kernels", False):
+        d = system.desc()
+        if not _lib.load().cs_system_elements_supported(ctypes.byref(d), _MODE_CODE[cfg.mode],
+                                                        _lib.dtype_code(system.dtype)):
+            return False
     if cfg.window_len is not None and cfg.window_len < system.T:
         return False
     return getattr(system, "leapfrog_mode", "sequential") != "parallel"

@@ -362,6 +362,21 @@ def test_run_deer_leapfrog_gauss200(cuda_device):
     _deer_cmp(cs.run_deer(lf, g["s0"], cs.DeerConfig(mode="diag-stochastic")), g, "diag_", torch.float64)
 
 
+def test_wide_leapfrog_builder_matches_host_engine(cuda_device):
+    # the GEMM-backed element builder (cuBLAS DGEMM + fused epilogue) against the
+    # host engine's torch evaluation of the same LeapfrogSystem (samplers.py:165-222)
+    g = golden("leapfrog_gauss200")
+    m = cs.model_logp_grad_hvp(cs.gaussian(np.zeros(200), g["chol"]))
+    for dt, tol in ((torch.float64, 1e-10), (torch.float32, 2e-4)):
+        lf = cs.LeapfrogSystem(m, 0.05, 100, probe_seed=0, dtype=dt)
+        cfg = dict(mode="block2x2-stochastic", damping=0.9)
+        a = cs.run_deer(lf, g["s0"], cs.DeerConfig(engine="streamed", **cfg))
+        b = cs.run_deer(lf, g["s0"], cs.DeerConfig(engine="host", **cfg))
+        assert a.stats["path"] == "streamed" and b.stats["path"] == "host"
+        assert abs(a.iterations - b.iterations) <= (0 if dt == torch.float64 else 1)
+        np.testing.assert_allclose(np_(a.trace), np_(b.trace), atol=tol, rtol=tol)
+
+
 def _cfg4_gaussian(D=1000):
     rng = np.random.default_rng(0)
     Q, _ = np.linalg.qr(rng.normal(size=(D, D)))
