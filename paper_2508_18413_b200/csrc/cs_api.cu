@@ -750,10 +750,20 @@ int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, co
     k_finalize<double><<<grid_for(T, 256), 256, 0, st>>>(ctl, (double *)trace, (const double *)G1, (const double *)s0, T, D, per_step_converged_at);
   else
     k_finalize<float><<<grid_for(T, 256), 256, 0, st>>>(ctl, (float *)trace, (const float *)G1, (const float *)s0, T, D, per_step_converged_at);
-  SolveCtl h;
-  e = cudaMemcpyAsync(&h, ctl, sizeof(SolveCtl), cudaMemcpyDeviceToHost, st);
+  // control block read back through a pinned staging buffer (one per device)
+  static SolveCtl *s_hctl[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SolveCtl *hp = s_hctl[dev & 15];
+  if (!hp) {
+    e = cudaMallocHost(&hp, sizeof(SolveCtl));
+    if (e != cudaSuccess) return cuda_fail(e, "pinned control buffer");
+    s_hctl[dev & 15] = hp;
+  }
+  e = cudaMemcpyAsync(hp, ctl, sizeof(SolveCtl), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "solve");
+  const SolveCtl h = *hp;
   res->iterations = h.iterations;
   res->status = h.status;
   res->err_kind = h.err_kind;

@@ -261,18 +261,30 @@ cudaError_t launch_solve(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *p
   constexpr bool kKeepOK = MD <= 4;
   auto kr = deer_persistent<Sys, MODE, MD, ST, false>;
   const size_t keep_smem = sizeof(double) * kSegKeep * Elem<MODE, MD>::W * kSolveThreads;
-  int bk = 0, br = 0;
+  // occupancy is a property of the instantiation: query once per device
+  static int s_bk[16], s_br[16];
+  static bool s_done[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 15;
   cudaError_t e;
-  if constexpr (kKeepOK) {
-    e = cudaFuncSetAttribute(deer_persistent<Sys, MODE, MD, ST, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)keep_smem);
+  if (!s_done[dev]) {
+    int bk = 0, br = 0;
+    if constexpr (kKeepOK) {
+      e = cudaFuncSetAttribute(deer_persistent<Sys, MODE, MD, ST, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)keep_smem);
+      if (e != cudaSuccess) return e;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, deer_persistent<Sys, MODE, MD, ST, true>,
+                                                        kSolveThreads, keep_smem);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, kr, kSolveThreads, 0);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, deer_persistent<Sys, MODE, MD, ST, true>,
-                                                      kSolveThreads, keep_smem);
-    if (e != cudaSuccess) return e;
+    s_bk[dev] = bk;
+    s_br[dev] = br;
+    s_done[dev] = true;
   }
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, kr, kSolveThreads, 0);
-  if (e != cudaSuccess) return e;
+  int bk = s_bk[dev], br = s_br[dev];
   if (bk > 8) bk = 8;
   if (br > 8) br = 8;
   const int64_t T = A.T;

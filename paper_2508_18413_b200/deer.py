@@ -297,9 +297,14 @@ def _builtin_ok(system, cfg):
 def _fused_ok(system, cfg):
     if not _builtin_ok(system, cfg):
         return False
-    d = system.desc()
-    return bool(_lib.load().cs_deer_supported(ctypes.byref(d), _MODE_CODE[cfg.mode],
-                                              _lib.dtype_code(system.dtype)))
+    # a property of (system kind, target, width, mode, dtype): asked once per system
+    cache = system.__dict__.setdefault("_fused_support", {})
+    key = (cfg.mode, system.dtype)
+    if key not in cache:
+        d = system.desc()
+        cache[key] = bool(_lib.load().cs_deer_supported(ctypes.byref(d), _MODE_CODE[cfg.mode],
+                                                        _lib.dtype_code(system.dtype)))
+    return cache[key]
 
 
 # persistent kernel while a thread's steps stay few (elements kept in shared
@@ -329,7 +334,9 @@ def _run_fused(system, s0, cfg, max_iters):
     d = system.desc()
     trace = torch.empty((T, D), dtype=dtype, device=dev)
     psca = torch.empty(T, dtype=torch.int32, device=dev)
-    hist = torch.empty(max_iters, dtype=torch.float64, device=dev)
+    # delta history straight into pinned host memory (UVA: the kernel's one
+    # store per iteration lands on the host; no second read-back after the solve)
+    hist = _pinned_hist(max_iters)
     ws_bytes = lib.cs_deer_workspace_bytes(ctypes.byref(d), _lib.dtype_code(dtype), max_iters)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     pre = _pre_tensor(cfg, dev)
@@ -370,9 +377,22 @@ def _run_fused(system, s0, cfg, max_iters):
     stats = {"path": "fused", "grid_blocks": int(res.grid_blocks), "steps_per_thread": int(res.steps_per_thread),
              "kept_in_registers": bool(res.kept_in_registers), "launches": int(res.launches),
              "stop_reason": int(res.stop_reason)}
-    return DeerResult(trace=trace, iterations=it, delta_history=hist[:it].cpu().numpy(),
+    return DeerResult(trace=trace, iterations=it, delta_history=hist[:it].numpy().copy(),
                       converged=res.status == _lib.CS_RUN_CONVERGED, per_step_converged_at=psca,
                       full_trace=None, stats=stats)
+
+
+_PINNED_HIST: dict = {}
+
+
+def _pinned_hist(n):
+    # reused across solves on this thread's stream: cs_deer_solve synchronises
+    # before returning, and the result copies out of it
+    buf = _PINNED_HIST.get(n)
+    if buf is None:
+        buf = torch.empty(n, dtype=torch.float64).pin_memory()
+        _PINNED_HIST[n] = buf
+    return buf
 
 
 def run_deer(system: TransitionSystem, s0, cfg: DeerConfig) -> DeerResult:
