@@ -444,9 +444,9 @@ struct RowsGeom {
   int64_t T, nchunks, nr;
   int R, CS, G, j;
   bool agg_only;
+  int64_t nstages;  // ceil(T / R), so stages_in needs no division
   CS_D int stages_in(int64_t q) const {
-    const int64_t rows = T - q * (int64_t)CS * R;
-    const int64_t st = (rows + R - 1) / R;
+    const int64_t st = nstages - q * CS;
     return (int)(st < CS ? st : CS);
   }
   CS_D void settle(RowsJob &it) const {
@@ -479,9 +479,19 @@ struct RowsGeom {
 
 // rows per thread segment per stage: the thread's loads for a stage are all
 // issued before its FMA chain starts (registers: NA * kSegRows values)
+#ifndef CS_ROWS_KR
+#define CS_ROWS_KR 16  // diag fp32 rows per thread segment per stage
+#endif
+#ifndef CS_ROWS_MINB
+#define CS_ROWS_MINB 3  // resident CTAs per SM the register budget is cut for
+#endif
+#ifndef CS_ROWS_PREFETCH
+#define CS_ROWS_PREFETCH 0  // software-pipelined stage loads (needs 2x registers)
+#endif
 template <typename ST, int VAR>
 struct RowsSeg {
-  static constexpr int kRows = VAR == SCAN_DIAG ? (sizeof(ST) == 4 ? 16 : 8) : (sizeof(ST) == 4 ? 4 : 2);
+  static constexpr int kRows = VAR == SCAN_DIAG ? (sizeof(ST) == 4 ? CS_ROWS_KR : CS_ROWS_KR / 2)
+                                                : (sizeof(ST) == 4 ? CS_ROWS_KR / 4 : CS_ROWS_KR / 8 > 0 ? CS_ROWS_KR / 8 : 1);
 };
 
 template <typename T>
@@ -498,7 +508,7 @@ CS_D T ld_hint(const T *p, uint64_t pol) {
 }
 
 template <typename ST, int VAR, bool AGG_ONLY = false, bool UPDATE = false>
-__global__ void __launch_bounds__(kScanThreads, 3)
+__global__ void __launch_bounds__(kScanThreads, CS_ROWS_MINB)
 scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int stride, int NS) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = ColElem<VAR>::W;
@@ -534,13 +544,55 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
   geo.R = R;
   geo.CS = CS;
   geo.nr = (nchunks + geo.G - 1) / geo.G;
+  geo.nstages = (a.T + R - 1) / R;
   geo.agg_only = AGG_ONLY;
   // A keeps what it reads in L2 for C (one round later); C's reads are the last use
   const uint64_t pol_a = l2_policy_evict_last(), pol_c = l2_policy_evict_first();
   __syncthreads();
 
-  int64_t n = 0;
-  for (RowsJob cur = geo.first(); geo.valid(cur); geo.next(cur), ++n) {
+  constexpr int NA = VAR == SCAN_DIAG ? 2 : 6;
+  // issue one stage's loads (this thread's KR rows of its column) into ev
+  auto load_stage = [&](const RowsJob &job, CT (&ev)[NA][KR]) {
+    const int64_t row0 = (job.q * CS + job.s) * R;
+    const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
+    const uint64_t pol = job.ph == 0 ? pol_a : pol_c;
+    const int r0 = sg * KR, r1 = min(rows, r0 + KR);
+    if (!active) return;
+    // per-stage 64-bit bases, 32-bit offsets inside the stage
+    const int64_t g0 = row0 * ncol;
+    const ST *p0 = a.e0 + g0 + c, *pu = a.u + (VAR == SCAN_BLOCK ? 2 : 1) * g0 + c;
+    const ST *p1 = VAR == SCAN_BLOCK ? a.e1 + g0 + c : nullptr, *p2 = VAR == SCAN_BLOCK ? a.e2 + g0 + c : nullptr;
+    const ST *p3 = VAR == SCAN_BLOCK ? a.e3 + g0 + c : nullptr;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int r = r0 + k;
+      if (r < r1) {
+        const int i = r * ncol;
+        if constexpr (VAR == SCAN_DIAG) {
+          ev[0][k] = (CT)ld_hint(p0 + i, pol);
+          ev[1][k] = (CT)ld_hint(pu + i, pol);
+        } else {
+          ev[0][k] = (CT)ld_hint(p0 + i, pol);
+          ev[1][k] = (CT)ld_hint(p1 + i, pol);
+          ev[2][k] = (CT)ld_hint(p2 + i, pol);
+          ev[3][k] = (CT)ld_hint(p3 + i, pol);
+          ev[4][k] = (CT)ld_hint(pu + 2 * i, pol);
+          ev[5][k] = (CT)ld_hint(pu + 2 * i + ncol, pol);
+        }
+      } else {  // identity rows
+        if constexpr (VAR == SCAN_DIAG) {
+          ev[0][k] = 1;
+          ev[1][k] = 0;
+        } else {
+          ev[0][k] = 1; ev[1][k] = 0; ev[2][k] = 0; ev[3][k] = 1; ev[4][k] = 0; ev[5][k] = 0;
+        }
+      }
+    }
+  };
+
+  // process one stage whose loads are in ev (the next stage's loads are
+  // already in flight in the other register set)
+  auto body = [&](const RowsJob &cur, int64_t n, const CT (&ev)[NA][KR]) {
     const int64_t q = cur.q;
     const int64_t stg = q * CS + cur.s;
     const int64_t row0 = stg * R;
@@ -565,38 +617,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
         if (tid == 0) scan_stamp(a, q, 8);
       }
     }
-    const uint64_t pol = cur.ph == 0 ? pol_a : pol_c;
-
-    // ---- this thread's rows of the stage, straight from global into registers
     const int r0 = sg * KR, r1 = min(rows, r0 + KR);
-    CT ev[VAR == SCAN_DIAG ? 2 : 6][KR];
-    if (active) {
-#pragma unroll
-      for (int k = 0; k < KR; ++k) {
-        const int r = r0 + k;
-        if (r < r1) {
-          const int64_t i = (row0 + r) * ncol + c;
-          if constexpr (VAR == SCAN_DIAG) {
-            ev[0][k] = (CT)ld_hint(a.e0 + i, pol);
-            ev[1][k] = (CT)ld_hint(a.u + i, pol);
-          } else {
-            ev[0][k] = (CT)ld_hint(a.e0 + i, pol);
-            ev[1][k] = (CT)ld_hint(a.e1 + i, pol);
-            ev[2][k] = (CT)ld_hint(a.e2 + i, pol);
-            ev[3][k] = (CT)ld_hint(a.e3 + i, pol);
-            ev[4][k] = (CT)ld_hint(a.u + 2 * (row0 + r) * ncol + c, pol);
-            ev[5][k] = (CT)ld_hint(a.u + 2 * (row0 + r) * ncol + ncol + c, pol);
-          }
-        } else {  // identity rows
-          if constexpr (VAR == SCAN_DIAG) {
-            ev[0][k] = 1;
-            ev[1][k] = 0;
-          } else {
-            ev[0][k] = 1; ev[1][k] = 0; ev[2][k] = 0; ev[3][k] = 1; ev[4][k] = 0; ev[5][k] = 0;
-          }
-        }
-      }
-    }
     // ---- segment aggregate (CT) -> segagg[par]
     CT *sa = segagg + (n & 1) * (nseg + 1) * ncol * W;
     if (active) {
@@ -676,7 +697,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
         }
         if constexpr (!AGG_ONLY) group_aggregate_publish<VAR, CtaGrp>(q, ncol, ws, &s_gflag);
       }
-      continue;
+      return;
     }
 
     // ---- C: entry state of each segment = (segments before it) o running state
@@ -715,9 +736,10 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
       // ---- replay from registers; states stream straight out (lanes of a warp
       // cover whole rows, so each store instruction writes contiguous runs)
       unsigned long long dmb = 0ull;
+      const ST *gbase = UPDATE ? a.guess + row0 * SW : nullptr;
       auto check = [&](int r, int col, double xv) {  // deer.py:273-275 on the stored value
         if constexpr (UPDATE) {
-          const double gap = fabs(xv - (double)a.guess[(row0 + r) * SW + col]);
+          const double gap = fabs(xv - (double)gbase[r * SW + col]);
           if (gap > a.atol + a.rtol * fabs(xv)) s_fail[r] = 1;
           const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
           dmb = gb > dmb ? gb : dmb;
@@ -730,7 +752,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
         for (int k = 0; k < KR; ++k) {
           x = ev[0][k] * x + ev[1][k];
           if (r0 + k < r1) {
-            __stcs(o + (int64_t)(r0 + k) * SW, (ST)x);
+            __stcs(o + (r0 + k) * SW, (ST)x);
             check(r0 + k, c, (double)x);
           }
         }
@@ -743,8 +765,8 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
           x = xa;
           v = va;
           if (r0 + k < r1) {
-            __stcs(o + (int64_t)(r0 + k) * SW, (ST)x);
-            __stcs(o + (int64_t)(r0 + k) * SW + ncol, (ST)v);
+            __stcs(o + (r0 + k) * SW, (ST)x);
+            __stcs(o + (r0 + k) * SW + ncol, (ST)v);
             check(r0 + k, c, (double)x);
             check(r0 + k, ncol + c, (double)v);
           }
@@ -772,7 +794,37 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
       if (tid == 0 && cur.s == cur.ns - 1) atomicMax((unsigned long long *)&a.stats->dmax, s_dm);
     }
     if (tid == 0 && cur.s == cur.ns - 1) scan_stamp(a, q, 9);
+  };
+
+#if CS_ROWS_PREFETCH
+  // two register sets, swapped by unrolling the stage loop by two
+  CT evA[NA][KR], evB[NA][KR];
+  RowsJob cur = geo.first();
+  if (geo.valid(cur)) load_stage(cur, evA);
+  int64_t n = 0;
+  while (geo.valid(cur)) {
+    RowsJob nx = cur;
+    geo.next(nx);
+    if (geo.valid(nx)) load_stage(nx, evB);
+    body(cur, n++, evA);
+    cur = nx;
+    if (!geo.valid(cur)) break;
+    nx = cur;
+    geo.next(nx);
+    if (geo.valid(nx)) load_stage(nx, evA);
+    body(cur, n++, evB);
+    cur = nx;
   }
+#else
+  // one register set: occupancy (3 CTAs per SM) hides the load latency better
+  // than a second set would (measured)
+  CT ev[NA][KR];
+  int64_t n = 0;
+  for (RowsJob cur = geo.first(); geo.valid(cur); geo.next(cur)) {
+    load_stage(cur, ev);
+    body(cur, n++, ev);
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1207,11 +1259,11 @@ static int rows_chunk_stages() {  // tuning override for experiments
   static const int v = env_int("CS_SCAN_CHUNK_STAGES", 1, 256, 16);
   return v;
 }
-static int rows_resident_ctas() {  // persistent grid of scan_rows: 3 CTAs per SM (launch bounds)
+static int rows_resident_ctas() {  // persistent grid of scan_rows (launch bounds: CS_ROWS_MINB per SM)
   static const int v = [] {
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return 3 * (sms > 0 ? sms : 148);
+    return CS_ROWS_MINB * (sms > 0 ? sms : 148);
   }();
   return v;
 }
@@ -1247,7 +1299,8 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
   } else if (D <= 64) {
     p.kind = 0;
     const int nseg = kScanThreads / D;
-    const int kr = var == SCAN_DIAG ? (dtype == CS_F64 ? 8 : 16) : (dtype == CS_F64 ? 2 : 4);  // RowsSeg
+    const int kr = dtype == CS_F64 ? (var == SCAN_DIAG ? RowsSeg<double, SCAN_DIAG>::kRows : RowsSeg<double, SCAN_BLOCK>::kRows)
+                                   : (var == SCAN_DIAG ? RowsSeg<float, SCAN_DIAG>::kRows : RowsSeg<float, SCAN_BLOCK>::kRows);
     p.R = nseg * kr;                      // rows per stage
     // stages per chunk: large chunks amortise the per-chunk look-back, but
     // every resident CTA needs chunks -- aim for >= 2 rounds of the grid
