@@ -252,10 +252,13 @@ template <typename T> CS_D T vload(const T *p) { return *((const volatile T *)p)
 // timing probe (cs_debug_probe): CTA 0 / thread 0 stamps %globaltimer at the
 // phase boundaries of the first iterations; null = off
 CS_D void probe_stamp(unsigned long long *buf, int n, int it, int k) {
-  if (buf && blockIdx.x == 0 && threadIdx.x == 0 && it * 8 + k < n) {
+  if (buf && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    buf[it * 8 + k] = t;
+    if (blockIdx.x == 0 && it * 8 + k < n) buf[it * 8 + k] = t;
+    // every CTA's phase stamps of iteration 4 (skew across the grid)
+    const int slot = 1024 + blockIdx.x * 8 + k;
+    if (it == 4 && slot < n) buf[slot] = t;
   }
 }
 
@@ -512,11 +515,13 @@ deer_persistent(SolveArgs<ST> A) {
         if (af) atomicAdd(&s_cnt[1], af);
         atomicMax(&s_dm, dmb);
       }
-      __threadfence();
+      // the CTA barrier orders every thread's stores before thread 0's fence +
+      // release (cumulativity), so one fence per CTA publishes the whole segment
       __syncthreads();
       if (threadIdx.x == 0) {
         if (s_cnt[1]) atomicAdd(&S->any_fail, s_cnt[1]);
         atomicMax(&S->dmax_bits, s_dm);
+        __threadfence();
         st_release(A.ready + b, it + 1);  // rows of guess_{it+1} from this CTA are visible
       }
     }
