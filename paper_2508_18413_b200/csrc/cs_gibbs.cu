@@ -77,10 +77,27 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
   // only steers convergence, the step values above stay f64).
   using TT = ST;
   const uint64_t h3 = hash_t(probe_prefix(A.sys.seed, iteration), (uint64_t)t);
-  const TT inv_gt = (TT)(1.0 / gt), inv_kS = (TT)(1.0 / kS), inv_tau2n = (TT)(1.0 / tau2n);
-  const TT inv_t2sq = (TT)(1.0 / (tau2n * tau2n)), n_sg2 = (TT)(n / (sg * sg)), inv_prec = (TT)(1.0 / prec);
-  const TT c_mu = (TT)(xm / (2.0 * sqrt(tau2n * kS))), c_th = (TT)(0.5 * xt / (prec * rsq));
-  const TT c_sg = (TT)((-2.0 * n * (xbar - thn)) / gs), mun_t = (TT)mun, mean_t = (TT)mean;
+  // coefficients of the tangent map, formed in TT: in fp32 storage mode these
+  // are fp32 reciprocals (the f64 forward values above are only rounded once)
+  TT inv_gt, inv_kS, inv_tau2n, inv_t2sq, n_sg2, inv_prec, c_mu, c_th, c_sg;
+  if constexpr (sizeof(TT) == 4) {
+    const float gt_t = (float)gt, kS_t = (float)kS, t2_t = (float)tau2n, sg_t = (float)sg, n_t = (float)n;
+    inv_gt = 1.0f / gt_t;
+    inv_kS = 1.0f / kS_t;
+    inv_tau2n = 1.0f / t2_t;
+    inv_t2sq = inv_tau2n * inv_tau2n;
+    n_sg2 = n_t / (sg_t * sg_t);
+    inv_prec = 1.0f / (float)prec;
+    c_mu = (float)xm / (2.0f * sqrtf(t2_t * kS_t));
+    c_th = 0.5f * (float)xt * inv_prec / (float)rsq;
+    c_sg = (-2.0f * n_t * (float)(xbar - thn)) / (float)gs;
+  } else {
+    inv_gt = 1.0 / gt; inv_kS = 1.0 / kS; inv_tau2n = 1.0 / tau2n;
+    inv_t2sq = 1.0 / (tau2n * tau2n); n_sg2 = n / (sg * sg); inv_prec = 1.0 / prec;
+    c_mu = xm / (2.0 * sqrt(tau2n * kS)); c_th = 0.5 * xt / (prec * rsq);
+    c_sg = (-2.0 * n * (xbar - thn)) / gs;
+  }
+  const TT mun_t = (TT)mun, mean_t = (TT)mean;
   const TT xbar_t = (TT)xbar, two_dm = (TT)(2.0 * (th - mu)), mu_c = (TT)(2.0 * kappa0 * (mu - mu0));
   TT e_tau = 0, e_mu = 0, e_th = 0, e_sg = 0;
   for (int k = 0; k < A.nsamp; ++k) {
