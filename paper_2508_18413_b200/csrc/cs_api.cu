@@ -590,7 +590,7 @@ int cs_system_elements_supported(const cs_system *sys, int32_t mode, int dtype) 
   int md = 0;
   if (sys->kind == CS_SYS_GIBBS) md = (sys->dim == 18 && mode == CS_MODE_DIAG) ? 18 : 0;
   else if (sys->target.kind != CS_TARGET_BLR) md = elem_md(sys->kind, sys->target.kind, sys->dim);
-  return md > 0 || wide_leapfrog_ok(*sys, mode) ? 1 : 0;
+  return md > 0 || wide_leapfrog_ok(*sys, mode) || blr_mala_ok(*sys, mode) ? 1 : 0;
 }
 
 static int elem_width(const cs_system *sys) {
@@ -606,7 +606,8 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   const int md = elem_width(sys);
   const bool wide = !md && wide_leapfrog_ok(*sys, cfg->mode);
-  if (!md && !wide) return fail(CS_ERR_CONFIG, "no fused element builder for this system");
+  const bool blr = !md && !wide && blr_mala_ok(*sys, cfg->mode);
+  if (!md && !wide && !blr) return fail(CS_ERR_CONFIG, "no fused element builder for this system");
   if (cfg->mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG)
     return fail(CS_ERR_CONFIG, "system does not provide a block2x2 Jacobian estimate");
   cudaStream_t st = S(stream);
@@ -616,6 +617,10 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
   if (wide) {
     e = elements_wide(*sys, *cfg, dtype, iteration, s0, guess, e0, e1, e2, e3, u, d_stats, st);
     return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements (wide leapfrog, cuBLAS)");
+  }
+  if (blr) {
+    e = elements_blr(*sys, *cfg, dtype, iteration, s0, guess, e0, u, d_stats, st);
+    return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements (logistic-regression MALA, cuBLAS)");
   }
   if (dtype == CS_F64) {
     SolveArgs<double> A{};

@@ -48,6 +48,11 @@ CS_D void atomic_max_nonneg(unsigned long long *addr, double v) {
 CS_D void atomic_min_i64(long long *addr, long long v) { atomicMin(addr, v); }
 
 // ---- warp reductions -------------------------------------------------------------
+CS_D double warp_sum(double v) {  // butterfly: every lane ends with the full sum
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
 CS_D double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -11,4 +11,8 @@ bool wide_leapfrog_ok(const cs_system &s, int mode);
 cudaError_t elements_wide(const cs_system &sys, const cs_deer_config &cfg, int dtype, int64_t iteration,
                           const void *s0, const void *guess, void *e0, void *e1, void *e2, void *e3, void *u,
                           cs_elem_stats *stats, cudaStream_t st);
+bool blr_mala_ok(const cs_system &s, int mode);
+cudaError_t elements_blr(const cs_system &sys, const cs_deer_config &cfg, int dtype, int64_t iteration,
+                         const void *s0, const void *guess, void *e0, void *u, cs_elem_stats *stats,
+                         cudaStream_t st);
 }  // namespace cs

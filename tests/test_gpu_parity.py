@@ -347,9 +347,14 @@ def test_run_deer_blr_gemm_path(cuda_device):
     k = cs.MalaKernel(m, 0.003, seed=4, T=300)
     assert not k.kernels
     np.testing.assert_allclose(np_(cs.sequential_evaluate(k, np.zeros(100))), g["seq"], atol=1e-9, rtol=1e-9)
+    # GEMM-backed element builder on the streamed engine (cs_blr.cu) and the
+    # host engine's torch evaluation: both must reproduce the reference run
     r = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="diag-stochastic"))
-    assert r.stats["path"] == "host"
+    assert r.stats["path"] == "streamed"
     _deer_cmp(r, g, "diag_", torch.float64)
+    h = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="diag-stochastic", engine="host"))
+    assert h.stats["path"] == "host"
+    _deer_cmp(h, g, "diag_", torch.float64)
 
 
 def test_run_deer_leapfrog_gauss200(cuda_device):
