@@ -450,3 +450,69 @@ def test_scan_aggregate_matches_fold(cuda_device, mode):
     a = agg.aggregate(el)
     last = cs.parallel_affine_solve(el, tt(s0))[-1]
     np.testing.assert_allclose(np_(apply_agg(key, a, tt(s0))), np_(last), rtol=1e-10, atol=1e-10)
+
+
+# ---------------------------------------------------------------------------
+# full-size row scans: the chained-chunk kernel only walks several rounds, group
+# boundaries and partial last chunks at large T (a 444-CTA grid and 224-row stages)
+
+
+@pytest.mark.parametrize("mode,D,T,dtype", [
+    ("diag", 18, 2_000_003, torch.float32),
+    ("diag", 1, 8_000_017, torch.float64),
+    ("diag", 2, 4_000_037, torch.float32),
+    ("diag", 64, 500_009, torch.float32),
+    ("block", 7, 1_000_003, torch.float64),
+])
+def test_row_scan_multi_round_vs_oracle(cuda_device, mode, D, T, dtype):
+    rng = np.random.default_rng(T)
+    tt = lambda x: torch.as_tensor(x, dtype=dtype, device=cuda_device)
+    if mode == "diag":
+        j = rng.uniform(-0.95, 0.95, (T, D))
+        u = rng.normal(size=(T, D))
+        s0 = rng.normal(size=D)
+        want = O.parallel_affine_solve(O.DiagElements(j, u), s0, workers=16)
+        got = np_(cs.parallel_affine_solve(cs.DiagElements(tt(j), tt(u)), tt(s0)))
+    else:
+        a, b, c, d = (rng.uniform(-0.65, 0.65, (T, D)) for _ in range(4))
+        u = rng.normal(size=(T, 2 * D))
+        s0 = rng.normal(size=2 * D)
+        want = O.parallel_affine_solve(O.Block2x2Elements(a, b, c, d, u), s0, workers=16)
+        got = np_(cs.parallel_affine_solve(cs.Block2x2Elements(tt(a), tt(b), tt(c), tt(d), tt(u)), tt(s0)))
+    tol = 1e-11 if dtype == torch.float64 else 2e-5
+    np.testing.assert_allclose(got, want, atol=tol * 10, rtol=tol)
+
+
+def test_update_scan_bookkeeping_multi_round(cuda_device):
+    # the replay's fused bookkeeping (deer.py:273-277) at a multi-round size:
+    # last_fail stamps, fail_rows and dmax against a direct evaluation
+    from paper_2508_18413_b200 import _lib
+
+    lib = _lib.load()
+    T, D, it = 3_000_001, 18, 7
+    g = torch.Generator(device=cuda_device).manual_seed(3)
+    j = (torch.rand((T, D), generator=g, device=cuda_device) * 1.9 - 0.95).float()
+    u = torch.randn((T, D), generator=g, device=cuda_device).float()
+    s0 = torch.zeros(D, device=cuda_device)
+    ref = cs.parallel_affine_solve(cs.DiagElements(j, u), s0)
+    guess = ref + torch.randn((T, D), generator=g, device=cuda_device) * 1e-4 * (torch.rand((T, 1), generator=g, device=cuda_device) < 0.3)
+    out = torch.empty_like(ref)
+    last_fail = torch.full((T,), 2, dtype=torch.int32, device=cuda_device)
+    stats = torch.zeros(40, dtype=torch.uint8, device=cuda_device)
+    wsb = lib.cs_scan_workspace_bytes(_lib.CS_MODE_DIAG, _lib.CS_F32, T, D)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=cuda_device)
+    atol, rtol = 1e-5, 1e-5
+    _lib.check(lib.cs_scan_diag_update(_lib.CS_F32, _lib.ptr(j), _lib.ptr(u), _lib.ptr(s0), _lib.ptr(out), T, D,
+                                       _lib.ptr(ws), wsb, _lib.ptr(guess), atol, rtol, it, _lib.ptr(last_fail),
+                                       _lib.ptr(stats), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out, ref, atol=1e-5, rtol=1e-5)  # look-back fold order may differ run to run
+    gap = (out.double() - guess.double()).abs()
+    fail = (gap > atol + rtol * out.double().abs()).any(dim=1)
+    want_lf = torch.where(fail, torch.tensor(it, dtype=torch.int32, device=cuda_device), torch.tensor(2, dtype=torch.int32, device=cuda_device))
+    assert torch.equal(last_fail, want_lf)
+    raw = stats.cpu().numpy().tobytes()
+    fail_rows = int(np.frombuffer(raw[28:32], dtype=np.uint32)[0])
+    dmax = float(np.frombuffer(raw[32:40], dtype=np.float64)[0])
+    assert fail_rows == int(fail.sum())
+    assert dmax == float(gap.max())
