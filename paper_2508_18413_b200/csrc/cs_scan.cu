@@ -363,6 +363,164 @@ CS_D void group_aggregate_publish(int64_t b, int ncol, const LookbackWs &ws, int
 }
 
 // ---------------------------------------------------------------------------
+// One-warp look-back (the dedicated look-back warp of scan_rows).  The same
+// two-level scheme as lookback_grouped, arranged so a lookup costs a handful
+// of L2 round trips whatever D is: statuses are polled one per lane, and the
+// aggregate records a fold needs are contiguous in the workspace, so they are
+// staged into shared memory with every 16-byte copy in flight at once
+// (cp.async), then folded lane-per-column from shared memory.
+constexpr int kLbwStage = 2048;     // doubles of look-back staging buffer (16 KB)
+constexpr int kLbwPubStage = 1024;  // doubles of the publisher's staging buffer (8 KB)
+
+// acc(c) <- acc(c) o (rec[n-1] o ... o rec[0]) for every column c, where
+// rec[p] = src + p * ncol * W (earliest record first).
+template <int VAR>
+CS_D void lbw_fold_records(const double *src, int n, int ncol, double *stage, double *s_acc, int cap = kLbwStage) {
+  constexpr int W = ColElem<VAR>::W;
+  constexpr int U = W / 2;  // 16-byte units per (record, column)
+  const int lane = threadIdx.x & 31;
+  if (n <= 0) return;
+  const int nbmax = min(32, cap / (32 * W));
+  for (int c0 = 0; c0 < ncol; c0 += nbmax) {
+    const int nb = min(nbmax, ncol - c0);
+    const int units = n * nb * U;
+    for (int k = lane; k < units; k += 32) {
+      const int p = k / (nb * U), rem = k - p * nb * U;  // rem = column-in-batch * U + unit
+      cp_async16(stage + (p * nb) * W + rem * 2, src + ((int64_t)p * ncol + c0) * W + rem * 2);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    if (lane < nb) {
+      ColElem<VAR> e;
+      e.ident();
+      for (int p = 0; p < n; ++p) {
+        ColElem<VAR> r;
+        r.load(stage + (p * nb + lane) * W);
+        e.push(r);
+      }
+      ColElem<VAR> acc;
+      acc.load(s_acc + (c0 + lane) * W);
+      acc.pre(e);
+      acc.store(s_acc + (c0 + lane) * W);
+    }
+    __syncwarp();
+  }
+}
+
+// Entry state of chunk b into s_entry (SW doubles).  s_acc, s_acc2: ncol*W
+// doubles each; stage: kLbwStage doubles.  Publishes the previous group's exit
+// when b opens a group.
+template <int VAR, class S0F, class S0VF, class StampF>
+CS_D void lookback_warp(int64_t b, int ncol, const LookbackWs &ws, S0F s0x, S0VF s0v, double *s_acc,
+                        double *s_acc2, double *stage, double *s_entry, StampF stamp) {
+  constexpr int W = ColElem<VAR>::W;
+  const int SW = VAR == SCAN_DIAG ? ncol : 2 * ncol;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = b / kGroupTiles;
+  const int i = (int)(b % kGroupTiles);
+  const int64_t t0 = g * kGroupTiles;
+  for (int c = lane; c < ncol; c += 32) {
+    ColElem<VAR> id;
+    id.ident();
+    id.store(s_acc + c * W);
+    id.store(s_acc2 + c * W);
+  }
+  // (1) state entering the group: look back over group aggregates, one
+  // window of 32 groups per round trip (lane l watches group hi - l)
+  int64_t hi = g - 1;
+  for (;;) {
+    const int64_t p = hi - lane;
+    int st = p >= 0 ? ld_acquire(ws.gstatus + p) : 2;  // p < 0: the chain start acts as an exit
+    unsigned exits = __ballot_sync(0xffffffffu, st == 2);
+    int stop = exits ? __ffs(exits) - 1 : 32;
+    for (;;) {  // every group nearer than the exit must have its aggregate
+      const unsigned below = stop == 32 ? 0xffffffffu : ((1u << stop) - 1u);
+      if (!(__ballot_sync(0xffffffffu, st == 0) & below)) break;
+      __nanosleep(200);  // a spinning warp would steal issue slots from the streaming warps
+      if (st == 0) st = ld_acquire(ws.gstatus + p);
+      exits = __ballot_sync(0xffffffffu, st == 2);
+      stop = exits ? __ffs(exits) - 1 : 32;
+    }
+    if (lane == 0) stamp(10);
+    // groups hi-stop+1 .. hi, earliest first, folded after what is already in s_acc2
+    lbw_fold_records<VAR>(ws.gagg + (hi - stop + 1) * ncol * W, stop, ncol, stage, s_acc2);
+    if (lane == 0) stamp(11);
+    if (stop < 32) {
+      const int64_t pe = hi - stop;
+      for (int c = lane; c < ncol; c += 32) {
+        double x = pe < 0 ? s0x(c) : ld_cg(ws.exit + pe * SW + c);
+        double v = 0.0;
+        if (VAR == SCAN_BLOCK) v = pe < 0 ? s0v(c) : ld_cg(ws.exit + pe * SW + ncol + c);
+        ColElem<VAR> acc;
+        acc.load(s_acc2 + c * W);
+        if constexpr (VAR == SCAN_DIAG) acc.apply(x);
+        else acc.apply(x, v);
+        s_entry[c] = x;
+        if (VAR == SCAN_BLOCK) s_entry[ncol + c] = v;
+      }
+      break;
+    }
+    hi -= 32;
+  }
+  __syncwarp();
+  // the first chunk of a group publishes the group's entry as the previous group's exit
+  if (i == 0 && g > 0) {
+    for (int c = lane; c < SW; c += 32) ws.exit[(g - 1) * SW + c] = s_entry[c];
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(ws.gstatus + g - 1, 2);
+  }
+  // (2) in-group prefix over chunks t0 .. b-1, applied to the group entry
+  if (i > 0) {
+    if (lane == 0) stamp(12);
+    if (lane < i)
+      while (ld_acquire(ws.status + t0 + lane) == 0) __nanosleep(200);
+    __syncwarp();
+    if (lane == 0) stamp(13);
+    lbw_fold_records<VAR>(ws.agg + t0 * ncol * W, i, ncol, stage, s_acc);
+    if (lane == 0) stamp(14);
+    for (int c = lane; c < ncol; c += 32) {
+      ColElem<VAR> acc;
+      acc.load(s_acc + c * W);
+      double x = s_entry[c], v = VAR == SCAN_BLOCK ? s_entry[ncol + c] : 0.0;
+      if constexpr (VAR == SCAN_DIAG) acc.apply(x);
+      else acc.apply(x, v);
+      s_entry[c] = x;
+      if (VAR == SCAN_BLOCK) s_entry[ncol + c] = v;
+    }
+  }
+  __syncwarp();
+}
+
+// One-warp group publication (the publisher warp of scan_rows): count chunk
+// b's aggregate into its group; the chunk completing the group folds the 32
+// aggregates (staged, one round trip) and publishes the group aggregate.
+template <int VAR>
+CS_D void group_publish_warp(int64_t b, int ncol, const LookbackWs &ws, double *stage, double *s_acc) {
+  constexpr int W = ColElem<VAR>::W;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = b / kGroupTiles;
+  int last = 0;
+  if (lane == 0) {
+    const int old = atomicAdd(ws.gcount + g, 1);
+    __threadfence();
+    last = old == kGroupTiles - 1;
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  for (int c = lane; c < ncol; c += 32) {
+    ColElem<VAR> id;
+    id.ident();
+    id.store(s_acc + c * W);
+  }
+  __syncwarp();
+  lbw_fold_records<VAR>(ws.agg + g * kGroupTiles * ncol * W, kGroupTiles, ncol, stage, s_acc, kLbwPubStage);
+  for (int k = lane; k < ncol * W; k += 32) ws.gagg[g * ncol * W + k] = s_acc[k];
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) st_release(ws.gstatus + g, 1);
+}
+
+// ---------------------------------------------------------------------------
 // narrow rows: tile = R consecutive rows x all columns, staged in smem.
 // Persistent CTAs (grid = resident capacity) claim tiles in ticket order and
 // double-buffer them: the bulk (TMA) load of the next tile is in flight while
@@ -431,11 +589,10 @@ CS_D void scan_stamp(const ScanArgs<ST> &a, int64_t b, int k) {
 // linked with the two-level (group) look-back.  HBM traffic is 20 B/element
 // (diag f32: j,u read twice, s written once) against 12 B/element for a
 // single pass; see DESIGN.md for why the single-pass variants lost.
-constexpr int kRowsMaxSlots = 8;
 
-struct RowsJob {  // position in a CTA's job stream: A(0) A(1) C(0) A(2) C(1) ... C(nr-1)
+struct RowsJob {  // position in a CTA's job stream: A(0) .. A(L-1) A(L) C(0) A(L+1) C(1) ... C(nr-1)
   int64_t r;
-  int ph;  // 0: A(r), 1: C(r-1)
+  int ph;  // 0: A(r), 1: C(r-L)
   int s, ns;
   int64_t q;
 };
@@ -443,6 +600,7 @@ struct RowsJob {  // position in a CTA's job stream: A(0) A(1) C(0) A(2) C(1) ..
 struct RowsGeom {
   int64_t T, nchunks, nr;
   int R, CS, G, j;
+  int L;  // rounds between a chunk's A pass and its C pass
   bool agg_only;
   int64_t nstages;  // ceil(T / R), so stages_in needs no division
   CS_D int stages_in(int64_t q) const {
@@ -450,9 +608,9 @@ struct RowsGeom {
     return (int)(st < CS ? st : CS);
   }
   CS_D void settle(RowsJob &it) const {
-    while (it.r <= nr) {
-      const int64_t rr = it.ph == 0 ? it.r : it.r - 1;
-      const bool ok = (it.ph == 0 ? it.r < nr : (it.r >= 1 && !agg_only)) && rr * G + j < nchunks;
+    while (it.r < nr + L) {
+      const int64_t rr = it.ph == 0 ? it.r : it.r - L;
+      const bool ok = (it.ph == 0 ? it.r < nr : (it.r >= L && !agg_only)) && rr * G + j < nchunks;
       if (ok) {
         it.q = rr * G + j;
         it.ns = stages_in(it.q);
@@ -474,7 +632,7 @@ struct RowsGeom {
     else { it.ph = 0; ++it.r; }
     settle(it);
   }
-  CS_D bool valid(const RowsJob &it) const { return it.r <= nr; }
+  CS_D bool valid(const RowsJob &it) const { return it.r < nr + L; }
 };
 
 // rows per thread segment per stage: the thread's loads for a stage are all
@@ -507,9 +665,20 @@ CS_D T ld_hint(const T *p, uint64_t pol) {
   }
 }
 
-template <typename ST, int VAR, bool AGG_ONLY = false, bool UPDATE = false>
-__global__ void __launch_bounds__(kScanThreads, CS_ROWS_MINB)
-scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int stride, int NS) {
+template <typename ST, int VAR, bool AGG_ONLY = false, bool UPDATE = false, bool LBW = false>
+#ifndef CS_ROWS_LBW_MINB
+#define CS_ROWS_LBW_MINB 2
+#endif
+__global__ void __launch_bounds__(kScanThreads + (LBW ? 64 : 0), LBW ? CS_ROWS_LBW_MINB : CS_ROWS_MINB)
+scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag, int NS) {
+  (void)NS;
+  // LBW: two helper warps take every global hand-off off the eight streaming
+  // warps.  Warp 8 computes the entry state of each of the CTA's C chunks
+  // while the main warps stream the A pass before it (lookback_warp); warp 9
+  // publishes each chunk aggregate and its group's (group_publish_warp), so
+  // the memory fences a publication needs never wait on the main warps'
+  // in-flight state stores.
+  using MG = Grp<0, kScanThreads, LBW ? 1 : 0>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = ColElem<VAR>::W;
   constexpr int KR = RowsSeg<ST, VAR>::kRows;
@@ -520,21 +689,38 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int c = tid % ncol, sg = tid / ncol;
   const bool active = sg < nseg;
-  __shared__ double s_chunk[64 * W];    // A: running chunk aggregate
+  __shared__ double s_chunk2[(LBW ? 2 : 1) * 64 * W];  // A: running chunk aggregate (LBW: two slots)
   __shared__ double s_run[2 * 2 * 64];  // C: running chain state, double-buffered by stage parity
   __shared__ double s_entry[2 * 64];
   __shared__ double s_acc[64 * W];
   __shared__ double s_acc2[64 * W];
+  __shared__ double s_acc3[LBW ? 64 * W : 1];
   __shared__ double s_gentry[2 * 64];
   __shared__ int s_ctl[1];
   __shared__ int s_gflag;
   __shared__ unsigned long long s_dm;
   CT *segagg = (CT *)smem_raw;                                // [2][nseg+1][ncol][W], by stage parity
   int *s_fail = (int *)(segagg + 2 * (nseg + 1) * ncol * W);  // UPDATE: one flag per stage row
-  (void)stride;
-  (void)NS;
+  // LBW: look-back staging buffer and the two-slot entry hand-off
+  double *lb_stage = (double *)(((uintptr_t)(s_fail + R) + 15) & ~(uintptr_t)15);
+  __shared__ double s_lbe[2 * 128];
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], s_aggfull[2], s_aggempty[2];
+  double *pub_stage = lb_stage + kLbwStage;  // kLbwPubStage doubles
   if constexpr (UPDATE)
     for (int r = tid; r < R; r += kScanThreads) s_fail[r] = 0;
+  if constexpr (LBW) {
+    if (tid == 0) {
+      mbar_init(&s_full[0], 1);
+      mbar_init(&s_full[1], 1);
+      mbar_init(&s_empty[0], 1);
+      mbar_init(&s_empty[1], 1);
+      mbar_init(&s_aggfull[0], 1);
+      mbar_init(&s_aggfull[1], 1);
+      mbar_init(&s_aggempty[0], 1);
+      mbar_init(&s_aggempty[1], 1);
+      fence_mbar_init();
+    }
+  }
 
   RowsGeom geo;
   geo.T = a.T;
@@ -546,9 +732,49 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
   geo.nr = (nchunks + geo.G - 1) / geo.G;
   geo.nstages = (a.T + R - 1) / R;
   geo.agg_only = AGG_ONLY;
+  geo.L = LBW ? (lag > 0 ? lag : 1) : 1;
   // A keeps what it reads in L2 for C (one round later); C's reads are the last use
   const uint64_t pol_a = l2_policy_evict_last(), pol_c = l2_policy_evict_first();
   __syncthreads();
+  if constexpr (LBW) {
+    if (wid == kScanThreads / 32) {  // the look-back warp: one entry per C chunk, in job order
+      int64_t k = 0;
+      for (int64_t q = geo.j; q < nchunks; q += geo.G, ++k) {
+        const int slot = (int)(k & 1);
+        if (k >= 2) mbar_wait(&s_empty[slot], (unsigned)(((k >> 1) - 1) & 1));
+        if (lane == 0) scan_stamp(a, q, 6);
+        lookback_warp<VAR>(
+            q, ncol, ws, [&](int cc) { return (double)a.s0[cc]; }, [&](int cc) { return (double)a.s0[ncol + cc]; },
+            s_acc, s_acc2, lb_stage, s_lbe + slot * 128, [&](int kk) { scan_stamp(a, q, kk); });
+        if (lane == 0) {
+          scan_stamp(a, q, 7);
+          mbar_arrive(&s_full[slot]);
+        }
+      }
+      return;
+    }
+    if (wid == kScanThreads / 32 + 1) {  // the publisher warp: chunk and group aggregates, in job order
+      int64_t k = 0;
+      for (int64_t q = geo.j; q < nchunks; q += geo.G, ++k) {
+        const int slot = (int)(k & 1);
+        mbar_wait(&s_aggfull[slot], (unsigned)((k >> 1) & 1));
+        const double *src = s_chunk2 + slot * 64 * W;
+        for (int cc = lane; cc < ncol * W; cc += 32) ws.agg[q * ncol * W + cc] = src[cc];
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          st_release(ws.status + q, 1);
+          scan_stamp(a, q, 4);
+          mbar_arrive(&s_aggempty[slot]);
+        }
+        group_publish_warp<VAR>(q, ncol, ws, pub_stage, s_acc3);
+        if (lane == 0) scan_stamp(a, q, 3);
+      }
+      return;
+    }
+  }
+  int64_t kc = 0;  // C jobs started (LBW hand-off slot/parity)
+  int64_t ka = 0;  // A jobs started (LBW publication slot/parity)
 
   constexpr int NA = VAR == SCAN_DIAG ? 2 : 6;
   // issue one stage's loads (this thread's KR rows of its column) into ev
@@ -597,8 +823,12 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
     const int64_t stg = q * CS + cur.s;
     const int64_t row0 = stg * R;
     const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
+    double *s_chunk = s_chunk2 + (LBW ? (ka & 1) * 64 * W : 0);
     if (cur.s == 0) {
       if (cur.ph == 0) {
+        if constexpr (LBW)
+          if (ka >= 2) mbar_wait(&s_aggempty[ka & 1], (unsigned)(((ka >> 1) - 1) & 1));
+        if (tid == 0) scan_stamp(a, q, 1);
         for (int cc = tid; cc < ncol; cc += kScanThreads) {
           ColElem<VAR> id;
           id.ident();
@@ -609,11 +839,16 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
           scan_stamp(a, q, 5);
           s_dm = 0ull;
         }
-        lookback_grouped<VAR, CtaGrp>(
-            q, ncol, ws, [&](int cc) { return (double)a.s0[cc]; },
-            [&](int cc) { return (double)a.s0[ncol + cc]; }, s_acc, s_acc2, s_entry, s_gentry, s_ctl,
-            [&](int k) { scan_stamp(a, q, k); });
-        for (int cc = tid; cc < SW; cc += kScanThreads) s_run[(n & 1) * 2 * 64 + cc] = s_entry[cc];
+        if constexpr (LBW) {
+          mbar_wait(&s_full[kc & 1], (unsigned)((kc >> 1) & 1));
+          for (int cc = tid; cc < SW; cc += kScanThreads) s_run[(n & 1) * 2 * 64 + cc] = s_lbe[(kc & 1) * 128 + cc];
+        } else {
+          lookback_grouped<VAR, CtaGrp>(
+              q, ncol, ws, [&](int cc) { return (double)a.s0[cc]; },
+              [&](int cc) { return (double)a.s0[ncol + cc]; }, s_acc, s_acc2, s_entry, s_gentry, s_ctl,
+              [&](int k) { scan_stamp(a, q, k); });
+          for (int cc = tid; cc < SW; cc += kScanThreads) s_run[(n & 1) * 2 * 64 + cc] = s_entry[cc];
+        }
         if (tid == 0) scan_stamp(a, q, 8);
       }
     }
@@ -636,7 +871,13 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
       }
       run.store(sa + (sg * ncol + c) * W);
     }
-    __syncthreads();
+    MG::sync();
+    if constexpr (LBW) {
+      if (cur.ph == 1 && cur.s == 0) {
+        if (tid == 0) mbar_arrive(&s_empty[kc & 1]);  // every main thread has copied the entry
+        ++kc;
+      }
+    }
     if (nseg > 32) {
       // narrow D: many segments per column -- warp scan per column (lane q
       // holds segments [q*K, q*K+K)), exclusive prefixes in place, total in slot nseg
@@ -664,7 +905,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
           ex.push(x);
         }
       }
-      __syncthreads();
+      MG::sync();
     }
 
     if (cur.ph == 0) {
@@ -687,15 +928,23 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
         ch.store(s_chunk + cc * W);
       }
       if (cur.s == cur.ns - 1) {  // publish the chunk aggregate after its last stage
-        __syncthreads();
+        MG::sync();
+        if constexpr (LBW) {  // hand it to the publisher warp
+          if (tid == 0) {
+            scan_stamp(a, q, 2);
+            mbar_arrive(&s_aggfull[ka & 1]);
+          }
+          ++ka;
+          return;
+        }
         for (int cc = tid; cc < ncol * W; cc += kScanThreads) ws.agg[q * ncol * W + cc] = s_chunk[cc];
         __threadfence();
-        __syncthreads();
+        MG::sync();
         if (tid == 0) {
           st_release(ws.status + q, 1);
           scan_stamp(a, q, 4);
         }
-        if constexpr (!AGG_ONLY) group_aggregate_publish<VAR, CtaGrp>(q, ncol, ws, &s_gflag);
+        if constexpr (!AGG_ONLY) group_aggregate_publish<VAR, MG>(q, ncol, ws, &s_gflag);
       }
       return;
     }
@@ -781,7 +1030,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
       if (lane == 0) atomicMax(&s_dm, z);
     }
     if constexpr (UPDATE) {
-      __syncthreads();  // every row's flag is final
+      MG::sync();  // every row's flag is final
       unsigned nf = 0;
       for (int r = tid; r < rows; r += kScanThreads)
         if (s_fail[r]) {
@@ -816,8 +1065,9 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int str
     cur = nx;
   }
 #else
-  // one register set: occupancy (3 CTAs per SM) hides the load latency better
-  // than a second set would (measured)
+  // one register set: occupancy hides the load latency better than a second
+  // set would (measured); a bulk-copy (TMA) ring of stage slots measured
+  // 0.8-1.4 TB/s here against 2.3-2.4 TB/s for register-streamed loads
   CT ev[NA][KR];
   int64_t n = 0;
   for (RowsJob cur = geo.first(); geo.valid(cur); geo.next(cur)) {
@@ -1267,8 +1517,19 @@ static int rows_resident_ctas() {  // persistent grid of scan_rows (launch bound
   }();
   return v;
 }
-static int rows_slots() {
-  static const int v = env_int("CS_SCAN_SLOTS", 3, kRowsMaxSlots, 6);
+static bool rows_lbw() {  // dedicated look-back warp (CS_SCAN_LBW=0 selects the in-line look-back)
+  static const bool v = [] {
+    const char *e = getenv("CS_SCAN_LBW");
+    return e ? atoi(e) != 0 : false;
+  }();
+  return v;
+}
+static int rows_round_kb() {  // LBW: input bytes per round of the grid, sized so the C pass re-reads from L2
+  static const int v = env_int("CS_SCAN_ROUND_KB", 1024, 1 << 20, 24 * 1024);
+  return v;
+}
+static int rows_lag() {  // LBW: rounds between a chunk's A and C passes
+  static const int v = env_int("CS_SCAN_LAG", 1, 8, 2);
   return v;
 }
 
@@ -1310,6 +1571,15 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
       int64_t cs = stages / (2 * g);
       const int cmax = rows_chunk_stages();
       if (cs > cmax) cs = cmax;
+      if (rows_lbw()) {
+        // the look-back is off the critical path, so chunks only need to be
+        // large enough to amortise the per-chunk fold: size a round of the
+        // grid to stay L2-resident until its C pass (one round later)
+        const int esz0 = dtype == CS_F64 ? 8 : 4;
+        const int64_t stage_bytes = (int64_t)p.R * D * (var == SCAN_DIAG ? 2 : 6) * esz0;
+        const int64_t cl = ((int64_t)rows_round_kb() * 1024) / (g * stage_bytes);
+        if (cs > cl) cs = cl;
+      }
       if (cs < 1) cs = 1;
       p.seg = (int)cs;
     }
@@ -1318,9 +1588,12 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
     p.state_w = var == SCAN_DIAG ? D : 2 * D;
     const int esz = dtype == CS_F64 ? 8 : 4;
     const int W = var == SCAN_DIAG ? 2 : 6;
-    p.win = 0;
+    p.win = rows_lbw() ? rows_lag() : 1;
     p.md = 0;
     p.smem = (size_t)esz * 2 * (nseg + 1) * D * W + sizeof(int) * p.R + 16;
+    if (rows_lbw()) {
+      p.smem += 16 + sizeof(double) * (kLbwStage + kLbwPubStage);
+    }
   } else {
     p.kind = 1;
     const int ncb = (D + 31) / 32;
@@ -1355,12 +1628,12 @@ LookbackWs carve_ws(const ScanPlan &p, void *ws, int D) {
 
 // persistent grid for scan_rows: every CTA must be co-resident (look-back
 // waits on tiles held by other CTAs), so never launch more than fit at once
-static unsigned rows_grid(const ScanPlan &p, const void *k) {
+static unsigned rows_grid(const ScanPlan &p, const void *k, int threads = kScanThreads) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kScanThreads, p.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, p.smem);
   if (occ < 1) occ = 1;
   const int64_t cap = (int64_t)occ * sms;
   return (unsigned)(p.ntiles < cap ? p.ntiles : cap);
@@ -1368,8 +1641,14 @@ static unsigned rows_grid(const ScanPlan &p, const void *k) {
 
 template <typename ST, int VAR, bool UPD>
 static void launch_rows(const ScanPlan &p, const ScanArgs<ST> &a, LookbackWs w, cudaStream_t st) {
-  auto k = scan_rows<ST, VAR, false, UPD>;
-  k<<<rows_grid(p, (const void *)k), kScanThreads, p.smem, st>>>(a, w, p.R, p.seg, p.ntiles, p.win, p.md);
+  if (rows_lbw()) {
+    auto k = scan_rows<ST, VAR, false, UPD, true>;
+    k<<<rows_grid(p, (const void *)k, kScanThreads + 64), kScanThreads + 64, p.smem, st>>>(a, w, p.R, p.seg,
+                                                                                            p.ntiles, p.win, 0);
+  } else {
+    auto k = scan_rows<ST, VAR, false, UPD>;
+    k<<<rows_grid(p, (const void *)k), kScanThreads, p.smem, st>>>(a, w, p.R, p.seg, p.ntiles, p.win, p.md);
+  }
 }
 
 template <typename ST>

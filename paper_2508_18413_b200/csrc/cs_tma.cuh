@@ -68,4 +68,19 @@ CS_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta
 
 CS_D bool aligned16(const void *p) { return (((uintptr_t)p) & 15u) == 0; }
 
+// plain arrive (release at CTA scope): producer/consumer hand-offs inside a CTA
+CS_D void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 16-byte global -> shared copies that bypass L1 (reads are served by L2, so
+// data published by other SMs is seen); all of a thread's copies stay in
+// flight until cp_async_wait_all
+CS_D void cp_async16(void *dst_smem, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+CS_D void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 }  // namespace cs

@@ -516,3 +516,20 @@ def test_update_scan_bookkeeping_multi_round(cuda_device):
     dmax = float(np.frombuffer(raw[32:40], dtype=np.float64)[0])
     assert fail_rows == int(fail.sum())
     assert dmax == float(gap.max())
+
+
+@pytest.mark.skipif(bool(__import__("os").environ.get("CS_SCAN_LBW")), reason="already the variant run")
+@pytest.mark.parametrize("lag,round_kb", [(1, 4096), (2, 16384)])
+def test_row_scan_lookback_warp_variant(cuda_device, lag, round_kb):
+    # the opt-in row-scan variant with dedicated look-back and publisher warps
+    # (CS_SCAN_LBW=1; the switch is read once per process, hence a subprocess):
+    # the multi-round parity and fused-bookkeeping cases above, many small rounds
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, CS_SCAN_LBW="1", CS_SCAN_LAG=str(lag), CS_SCAN_ROUND_KB=str(round_kb))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-x", "-q", "-m", "gpu", "-p",
+                        "no:cacheprovider", "-k", "multi_round or update_scan_bookkeeping or scan_kats or diag_and_block"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

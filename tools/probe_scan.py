@@ -84,13 +84,35 @@ def main():
         tr = tr[idx]
         nt = len(tr)
         t0 = tr[:, 4].min()
-        st = {k: tr[:, k] - t0 for k in range(4, 10)}
+        st = {k: tr[:, k] - t0 for k in range(1, 15)}
         span = st[9].max()
         q = lambda x: " ".join(f"{v / 1e3:7.2f}" for v in np.percentile(x, [10, 50, 90, 99]))
         print(f"chunks={nt} span={span / 1e3:.1f}us (us, p10/50/90/99 over the middle half)")
         m = (st[4] > 0.25 * span) & (st[4] < 0.75 * span)
-        names = {4: "A.published", 5: "C.start", 6: "C.ingroup", 7: "C.groups", 8: "C.entry", 9: "C.laststore"}
-        for k0, k1 in ((4, 5), (5, 6), (5, 7), (7, 8), (5, 8), (8, 9)):
+        lbw = os.environ.get("CS_SCAN_LBW", "1") != "0"
+        if lbw:  # look-back warp: 6/7 = its lookup start/end
+            names = {4: "A.published", 5: "C.start", 6: "LB.start", 7: "LB.end", 8: "C.entry", 9: "C.laststore"}
+            names.update({10: "LB.gpoll", 11: "LB.gfold", 12: "LB.exit", 13: "LB.ipoll", 14: "LB.ifold",
+                          1: "A.start", 2: "A.end", 3: "P.groupdone"})
+            pairs = ((1, 2), (2, 4), (4, 3), (2, 5), (4, 5), (4, 6), (6, 7), (6, 10), (10, 11), (11, 12), (12, 13), (13, 14), (14, 7), (7, 8),
+                     (5, 8), (8, 9))
+        else:
+            names = {4: "A.published", 5: "C.start", 6: "C.ingroup", 7: "C.groups", 8: "C.entry", 9: "C.laststore"}
+            pairs = ((4, 5), (5, 6), (5, 7), (7, 8), (5, 8), (8, 9))
+        if lbw and os.environ.get("CS_TRACE_CTA"):
+            # one CTA's event sequence (chunks j, j+G, ...; G = grid size)
+            G = int(os.environ.get("CS_TRACE_G", "444"))
+            j = int(os.environ["CS_TRACE_CTA"])
+            ev = []
+            full = buf.view(-1, 16).cpu().numpy().astype(np.int64)
+            for q in range(j, min(len(full), j + 12 * G), G):
+                for k in (1, 2, 4, 3, 6, 10, 11, 13, 14, 7, 5, 8, 9):
+                    if full[q, k] > 0:
+                        ev.append((full[q, k], q // G, names.get(k, str(k))))
+            ev.sort()
+            e0 = ev[0][0]
+            print("  ".join(f"{(t - e0) / 1e3:.1f}:{nm}@{r}" for t, r, nm in ev))
+        for k0, k1 in pairs:
             print(f"  {names[k0]:>11s}->{names[k1]:<11s} {q((st[k1] - st[k0])[m])}")
 
 
