@@ -345,6 +345,7 @@ int cs_rademacher_fill(uint64_t seed, int64_t iteration, const int64_t *ts, int6
 // ---- scans -----------------------------------------------------------------
 size_t cs_scan_workspace_bytes(int mode, int dtype, int64_t T, int32_t D) {
   const int var = mode == CS_MODE_DIAG ? SCAN_DIAG : mode == CS_MODE_BLOCK ? SCAN_BLOCK : SCAN_DENSE;
+  if (var == SCAN_DENSE && D > 8) return dense_wide_ws_bytes(T, D);
   return scan_plan(var, dtype, T, D).ws_bytes;
 }
 
@@ -353,9 +354,22 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
                    void *stream) {
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   if (T < 0 || D < 1) return fail(CS_ERR_STRUCTURAL, "bad scan shape");
-  if (var == SCAN_DENSE && D > 8)
-    return fail(CS_ERR_CONFIG, "dense scan in this build supports D <= 8 (larger D: see DESIGN.md)");
+  if (var == SCAN_DENSE && D > 128) return fail(CS_ERR_CONFIG, "dense scan supports D <= 128");
   if (var != SCAN_DENSE && D > 4096) return fail(CS_ERR_CONFIG, "scan D too large");
+  if (var == SCAN_DENSE && D > 8) {  // wide dense: chunked reduce / carry / replay (cs_dense.cu)
+    if (ws_bytes < dense_wide_ws_bytes(T, D)) return fail(CS_ERR_CONFIG, "scan workspace too small");
+    cudaError_t e;
+    if (dtype == CS_F64) {
+      ScanArgs<double> a{(const double *)e0, nullptr, nullptr, nullptr, (const double *)u, (const double *)s0,
+                         (double *)out, T, D};
+      e = launch_dense_wide_t<double>(a, ws, S(stream));
+    } else {
+      ScanArgs<float> a{(const float *)e0, nullptr, nullptr, nullptr, (const float *)u, (const float *)s0,
+                        (float *)out, T, D};
+      e = launch_dense_wide_t<float>(a, ws, S(stream));
+    }
+    return e == cudaSuccess ? CS_OK : cuda_fail(e, "dense scan launch");
+  }
   const ScanPlan p = scan_plan(var, dtype, T, D);
   if (ws_bytes < p.ws_bytes) return fail(CS_ERR_CONFIG, "scan workspace too small");
   if (T == 0) return CS_OK;

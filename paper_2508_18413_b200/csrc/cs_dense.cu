@@ -1,0 +1,238 @@
+// Dense affine scan for wide states, 8 < D <= 128 (pscan.py:196-213 and
+// _scan_kernels.py:47-99; SURVEY.md 8a row A12 at BASELINE cfg 3, D = 100).
+//
+// The recurrence s_t = J_t s_{t-1} + u_t with full D x D Jacobians is split in
+// chunks of c steps and solved in three launches:
+//   k_dense_reduce  one CTA per chunk composes (M, w) = (J_last...J_first,
+//                   the chunk's affine part) -- the 2 T D^3 flop of the scan,
+//                   a register-tiled product chain with J streamed through
+//                   shared memory in 16-column slices
+//   k_dense_carry   one CTA walks the chunk aggregates in order (f64) and
+//                   writes every chunk's entry state (D^2 per chunk)
+//   k_dense_replay  one CTA per chunk replays s_t = J_t s_{t-1} + u_t from
+//                   its entry, warp-per-row dot products with f64 sums; the
+//                   J_t reads (4 D^2 bytes per step) make it HBM-bound
+// Aggregates and carries are f64 whatever the storage type.
+#include <cstdlib>
+
+#include "cs_common.cuh"
+#include "cs_scan.cuh"
+
+namespace cs {
+
+constexpr int kDwSlice = 16;     // columns of J_t per shared-memory slice
+constexpr int kDwReduceThr = 256;
+constexpr int kDwThr = 512;      // carry / replay
+
+template <typename ST, int DP>
+__global__ void __launch_bounds__(kDwReduceThr)
+k_dense_reduce(const ST *__restrict__ J, const ST *__restrict__ u, int64_t T, int D, int c, double *aggM,
+               double *aggw) {
+  constexpr int NA = DP / 16;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  ST *Ms = (ST *)dsm;              // DP x DP running product (zero padded)
+  ST *Js = Ms + DP * DP;           // DP x kDwSlice slice of J_t
+  ST *wv = Js + DP * kDwSlice;     // DP running affine part
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t q = blockIdx.x, t0 = q * (int64_t)c;
+  const int64_t t1 = t0 + c < T ? t0 + c : T;
+  const int64_t DD = (int64_t)D * D;
+  {
+    const ST *J0 = J + t0 * DD;
+    for (int idx = tid; idx < DP * DP; idx += kDwReduceThr) {
+      const int i = idx / DP, k = idx - i * DP;
+      Ms[idx] = (i < D && k < D) ? J0[i * D + k] : ST(0);
+    }
+    for (int i = tid; i < DP; i += kDwReduceThr) wv[i] = i < D ? u[t0 * D + i] : ST(0);
+  }
+  __syncthreads();
+  for (int64_t t = t0 + 1; t < t1; ++t) {
+    const ST *Jt = J + t * DD;
+    ST acc[NA][NA];
+#pragma unroll
+    for (int x = 0; x < NA; ++x)
+#pragma unroll
+      for (int y = 0; y < NA; ++y) acc[x][y] = ST(0);
+    double wacc = 0.0;  // thread i < D: row i of J_t w
+    for (int k0 = 0; k0 < DP; k0 += kDwSlice) {
+      for (int idx = tid; idx < DP * kDwSlice; idx += kDwReduceThr) {
+        const int i = idx / kDwSlice, k = k0 + (idx - i * kDwSlice);
+        Js[idx] = (i < D && k < D) ? Jt[i * D + k] : ST(0);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kDwSlice; ++kk) {
+        ST a[NA], b[NA];
+#pragma unroll
+        for (int x = 0; x < NA; ++x) a[x] = Js[(ty + 16 * x) * kDwSlice + kk];
+#pragma unroll
+        for (int y = 0; y < NA; ++y) b[y] = Ms[(k0 + kk) * DP + tx + 16 * y];
+#pragma unroll
+        for (int x = 0; x < NA; ++x)
+#pragma unroll
+          for (int y = 0; y < NA; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+      }
+      if (tid < DP)
+#pragma unroll
+        for (int kk = 0; kk < kDwSlice; ++kk) wacc += (double)Js[tid * kDwSlice + kk] * (double)wv[k0 + kk];
+      __syncthreads();
+    }
+#pragma unroll
+    for (int x = 0; x < NA; ++x)
+#pragma unroll
+      for (int y = 0; y < NA; ++y) Ms[(ty + 16 * x) * DP + tx + 16 * y] = acc[x][y];
+    if (tid < DP) wv[tid] = tid < D ? (ST)(wacc + (double)u[t * D + tid]) : ST(0);
+    __syncthreads();
+  }
+  double *M = aggM + q * DD;
+  for (int idx = tid; idx < D * D; idx += kDwReduceThr) {
+    const int i = idx / D, k = idx - i * D;
+    M[idx] = (double)Ms[i * DP + k];
+  }
+  for (int i = tid; i < D; i += kDwReduceThr) aggw[q * D + i] = (double)wv[i];
+}
+
+// entries[q] = state entering chunk q; e_{q+1} = M_q e_q + w_q.  Four threads
+// per row; the next chunk's matrix rows are loaded while this one is applied.
+template <typename ST>
+__global__ void __launch_bounds__(kDwThr)
+k_dense_carry(const double *aggM, const double *aggw, const ST *s0, int64_t nch, int D, double *entries) {
+  constexpr int KP = 32;  // columns per thread (D <= 128)
+  __shared__ double e[2][128];
+  const int tid = threadIdx.x, i = tid >> 2, part = tid & 3;
+  const bool row = i < D;
+  const int kb = part * KP;
+  const int64_t DD = (int64_t)D * D;
+  if (tid < D) e[0][tid] = (double)s0[tid];
+  double m[KP];
+  auto load = [&](int64_t q) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) m[k] = (row && kb + k < D) ? aggM[q * DD + (int64_t)i * D + kb + k] : 0.0;
+  };
+  if (nch > 0) load(0);
+  __syncthreads();
+  for (int64_t q = 0; q < nch; ++q) {
+    const double *cur = e[q & 1];
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < KP; ++k) acc = fma(m[k], kb + k < D ? cur[kb + k] : 0.0, acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (q + 1 < nch) load(q + 1);
+    if (row && part == 0) {
+      entries[q * D + i] = cur[i];
+      e[(q + 1) & 1][i] = acc + aggw[q * D + i];
+    }
+    __syncthreads();
+  }
+}
+
+// replay chunk q from its entry: warp w owns rows w, w + 16, ...; lanes
+// stride the columns, f64 sums, one barrier per step
+template <typename ST>
+__global__ void __launch_bounds__(kDwThr)
+k_dense_replay(const ST *__restrict__ J, const ST *__restrict__ u, const double *entries, int64_t T, int D, int c,
+               ST *out) {
+  constexpr int NW = kDwThr / 32, RPW = (128 + NW - 1) / NW, KL = 4;  // rows per warp, columns per lane
+  __shared__ double s[2][128];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t q = blockIdx.x, t0 = q * (int64_t)c;
+  const int64_t t1 = t0 + c < T ? t0 + c : T;
+  const int64_t DD = (int64_t)D * D;
+  if (tid < D) s[0][tid] = entries[q * D + tid];
+  __syncthreads();
+  int par = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const ST *Jt = J + t * DD;
+    ST jv[RPW][KL];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int i = w + NW * r;
+#pragma unroll
+      for (int m = 0; m < KL; ++m) {
+        const int k = lane + 32 * m;
+        jv[r][m] = (i < D && k < D) ? __ldg(Jt + (int64_t)i * D + k) : ST(0);
+      }
+    }
+    const double *cur = s[par];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int i = w + NW * r;
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < KL; ++m) {
+        const int k = lane + 32 * m;
+        acc = fma((double)jv[r][m], k < D ? cur[k] : 0.0, acc);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0 && i < D) {
+        const ST v = (ST)(acc + (double)u[t * D + i]);
+        s[par ^ 1][i] = (double)v;
+        out[t * D + i] = v;
+      }
+    }
+    par ^= 1;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+int dense_wide_chunk(int64_t T) {
+  const char *e = getenv("CS_DENSE_CHUNK");
+  if (e && atoi(e) > 0) return atoi(e);
+  // enough chunks to fill the machine with reduce CTAs, few enough that the
+  // serial carry stays short: ~128 steps per chunk at T = 1e5
+  int64_t c = T / 768;
+  if (c < 8) c = 8;
+  if (c > 512) c = 512;
+  return (int)c;
+}
+
+size_t dense_wide_ws_bytes(int64_t T, int D) {
+  const int c = dense_wide_chunk(T);
+  const int64_t nch = (T + c - 1) / c;
+  return (size_t)nch * ((size_t)D * D + 2 * D) * sizeof(double) + 256;
+}
+
+static int dense_dp(int D) { return D <= 16 ? 16 : D <= 32 ? 32 : D <= 64 ? 64 : D <= 112 ? 112 : 128; }
+
+template <typename ST, int DP>
+static cudaError_t launch_reduce(const ScanArgs<ST> &a, int c, int64_t nch, double *aggM, double *aggw,
+                                 cudaStream_t st) {
+  const size_t smem = sizeof(ST) * ((size_t)DP * DP + (size_t)DP * kDwSlice + DP);
+  auto k = k_dense_reduce<ST, DP>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)nch, kDwReduceThr, smem, st>>>(a.e0, a.u, a.T, a.D, c, aggM, aggw);
+  return cudaGetLastError();
+}
+
+template <typename ST>
+cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
+  const int64_t T = a.T;
+  const int D = a.D;
+  if (T == 0) return cudaSuccess;
+  const int c = dense_wide_chunk(T);
+  const int64_t nch = (T + c - 1) / c;
+  double *aggM = (double *)ws;
+  double *aggw = aggM + nch * (int64_t)D * D;
+  double *entries = aggw + nch * (int64_t)D;
+  cudaError_t e;
+  switch (dense_dp(D)) {
+    case 16: e = launch_reduce<ST, 16>(a, c, nch, aggM, aggw, st); break;
+    case 32: e = launch_reduce<ST, 32>(a, c, nch, aggM, aggw, st); break;
+    case 64: e = launch_reduce<ST, 64>(a, c, nch, aggM, aggw, st); break;
+    case 112: e = launch_reduce<ST, 112>(a, c, nch, aggM, aggw, st); break;
+    default: e = launch_reduce<ST, 128>(a, c, nch, aggM, aggw, st); break;
+  }
+  if (e != cudaSuccess) return e;
+  k_dense_carry<ST><<<1, kDwThr, 0, st>>>(aggM, aggw, a.s0, nch, D, entries);
+  k_dense_replay<ST><<<(unsigned)nch, kDwThr, 0, st>>>(a.e0, a.u, entries, T, D, c, a.out);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_dense_wide_t<float>(ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_dense_wide_t<double>(ScanArgs<double>, void *, cudaStream_t);
+
+}  // namespace cs

@@ -35,6 +35,10 @@ struct ScanPlan {
 ScanPlan scan_plan(int var, int dtype, int64_t T, int D);
 template <typename ST>
 cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update = false);
+// wide dense scans, 8 < D <= 128 (cs_dense.cu)
+size_t dense_wide_ws_bytes(int64_t T, int D);
+template <typename ST>
+cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st);
 template <typename ST>
 cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, double *out, cudaStream_t st);
 

@@ -207,7 +207,22 @@ def chain_fixtures():
     save("mala_window", **out)
 
 
+def blr_dense_fixture():
+    # cfg3 "full" (reduced T): the same BLR MALA chain as mala_blr100, solved
+    # with dense (full-Jacobian) Newton -- D = 100, the wide dense scan
+    out = {}
+    X, y, _ = synthetic_credit_like(seed=20250819, n=1000, dim=100)
+    m = model_logp_grad_hvp(blr(X, y, 1.0))
+    k = MalaKernel(m, eps=0.003, seed=4, T=300)
+    deer_record("dense_", run_deer(k, np.zeros(100), DeerConfig(mode="dense", workers=WORKERS)), out)
+    save("mala_blr100_dense", **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["blr_dense"]:
+        blr_dense_fixture()
+        sys.exit(0)
     noise_fixtures()
     scan_fixtures()
     chain_fixtures()
+    blr_dense_fixture()

@@ -127,6 +127,36 @@ def test_dense_scan_vs_oracle(cuda_device, D):
     np.testing.assert_allclose(got, want, atol=1e-10, rtol=1e-10)
 
 
+@pytest.mark.parametrize("D,T", [(9, 1), (9, 3001), (16, 2000), (33, 777), (100, 1), (100, 2049), (128, 1500)])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_wide_dense_scan_vs_oracle(cuda_device, D, T, dtype):
+    # chunked reduce / carry / replay for 8 < D <= 128 (cs_dense.cu; A12 at cfg 3's D = 100)
+    rng = np.random.default_rng(7 * D + T)
+    J = rng.normal(size=(T, D, D)) * (0.9 / (2.0 * np.sqrt(D)))  # spectral radius ~0.45
+    u = rng.normal(size=(T, D))
+    s0 = rng.normal(size=D)
+    tt = lambda x: torch.as_tensor(x, dtype=dtype, device=cuda_device)
+    Jd, ud, s0d = (np_(tt(x)).astype(np.float64) for x in (J, u, s0))  # the inputs the kernel sees
+    want = O.parallel_affine_solve(O.DenseElements(Jd, ud), s0d, workers=8)
+    got = np_(cs.parallel_affine_solve(cs.DenseElements(tt(J), tt(u)), tt(s0)))
+    tol = 1e-10 if dtype == torch.float64 else 2e-5
+    np.testing.assert_allclose(got, want, atol=tol * 10, rtol=tol)
+
+
+def test_wide_dense_scan_kat_and_errors(cuda_device):
+    # J = 0.5 I for every step: s_t = 0.5 s_{t-1} + 1 -> 2 - 2^-t (s0 = 1 gives 2 - 2^-t)
+    T, D = 700, 40
+    J = torch.eye(D, dtype=torch.float64, device=cuda_device).expand(T, D, D).contiguous() * 0.5
+    u = torch.ones((T, D), dtype=torch.float64, device=cuda_device)
+    got = np_(cs.parallel_affine_solve(cs.DenseElements(J, u), torch.ones(D, dtype=torch.float64, device=cuda_device)))
+    want = 2.0 - 0.5 ** np.arange(1, T + 1)
+    np.testing.assert_allclose(got, np.repeat(want[:, None], D, axis=1), rtol=1e-13, atol=1e-13)
+    with pytest.raises(Exception):
+        big = torch.zeros((2, 129, 129), device=cuda_device)
+        cs.parallel_affine_solve(cs.DenseElements(big, torch.zeros((2, 129), device=cuda_device)),
+                                 torch.zeros(129, device=cuda_device))
+
+
 # ---------------------------------------------------------------------------
 # systems: batched f_t and JVPs vs the oracle (samplers.py)
 
@@ -355,6 +385,17 @@ def test_run_deer_blr_gemm_path(cuda_device):
     h = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="diag-stochastic", engine="host"))
     assert h.stats["path"] == "host"
     _deer_cmp(h, g, "diag_", torch.float64)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_run_deer_blr_dense_wide(cuda_device, dtype):
+    # cfg3 "full vs diagonal": dense Newton at D = 100 -- Jacobians from the
+    # system's jvps, the wide dense scan (cs_dense.cu) -- against the reference
+    g0, g = golden("mala_blr100"), golden("mala_blr100_dense")
+    m = cs.model_logp_grad_hvp(cs.blr(g0["X"], g0["y"], 1.0))
+    k = cs.MalaKernel(m, 0.003, seed=4, T=300, dtype=dtype)
+    r = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="dense"))
+    _deer_cmp(r, g, "dense_", dtype)
 
 
 def test_run_deer_leapfrog_gauss200(cuda_device):

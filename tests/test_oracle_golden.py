@@ -131,6 +131,13 @@ def test_blr_golden():
                 exact=False)
 
 
+def test_blr_dense_golden():
+    # cfg3 "full": dense Newton at D = 100 (the reference's D-jvp Jacobian)
+    g0, g = golden("mala_blr100"), golden("mala_blr100_dense")
+    k = O.MalaKernel(O.blr(g0["X"], g0["y"], 1.0), 0.003, seed=4, T=300)
+    _check_deer(O.run_deer(k, np.zeros(100), O.DeerConfig(mode="dense", workers=W)), g, "dense_", exact=False)
+
+
 def test_leapfrog_gauss_golden():
     g = golden("leapfrog_gauss200")
     D = 200

@@ -30,6 +30,12 @@ def main():
                              torch.randn((T, D), generator=g, device=dev).to(dt))
         s0 = torch.zeros(D, device=dev, dtype=dt)
         byts = 3 * T * D * es
+    elif a.mode == "dense":
+        el = cs.DenseElements((torch.randn((T, D, D), generator=g, device=dev) * (0.45 / D ** 0.5)).to(dt),
+                              torch.randn((T, D), generator=g, device=dev).to(dt))
+        s0 = torch.zeros(D, device=dev, dtype=dt)
+        byts = T * (D * D + 2 * D) * es
+        print(f"  dense: {2 * T * D ** 3 / 1e9:.1f} GFLOP of composition")
     else:
         el = cs.Block2x2Elements(*[(torch.rand((T, D), generator=g, device=dev) * 1.2 - 0.6).to(dt) for _ in range(4)],
                                  torch.randn((T, 2 * D), generator=g, device=dev).to(dt))
