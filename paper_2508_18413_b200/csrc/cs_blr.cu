@@ -15,6 +15,7 @@
 // formation (deer.py:171-183) are our kernels, one warp per step.
 #include <cublas_v2.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "cs_apikern.cuh"
@@ -56,7 +57,7 @@ __global__ void k_blr_prologue(cs_system sys, const ST *s0, const ST *guess, int
 // sums eta.y and sum logaddexp(0, eta).  exp(-eta) serves both the sigmoid and,
 // for eta >= 0, logaddexp's exp(-|eta|).
 __global__ void __launch_bounds__(256) k_blr_epilogue(double *E, const double *y, int64_t T, int K, int N,
-                                                       double *rowsum) {
+                                                       double *rowsum, double *wout = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < T; r += nw) {
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(256) k_blr_epilogue(double *E, const double *y
       b += eta != eta ? eta : fmax(eta, 0.0) + log1p(eta >= 0.0 ? em : exp(eta));  // logaddexp(0, eta)
       er[n] = yn - p;
       const double w = p * (1.0 - p);
+      if (wout) wout[r * N + n] = w;
       for (int k = 0; k < K; ++k) E[((int64_t)(k + 1) * T + r) * N + n] *= w;
     }
     a = warp_sum(a);
@@ -228,10 +230,306 @@ __global__ void k_blr_final(cs_system sys, cs_deer_config cfg, int64_t iteration
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dense (full-Jacobian) Newton for BLR MALA (BASELINE cfg 3 "full").  The
+// reference assembles J column by column from D jvps (core.py:125-134); the
+// jvp is linear in V, so J has the closed form
+//   A = I + eps H(S),  r = S - x~ - eps g(x~)
+//   w = A g(x~) - g(S) + (H(S) r + A H(x~) r) / 2
+//   J = gate A + (1 - gate) I + c (x~ - S) w^T,  c = sigma'(margin) 1(delta < 0)
+// with H(x) = -X^T diag(p(1-p)) X - prec I.  H(x~) r is one GEMM pair against
+// X; H(S) is formed explicitly per step (it is J's main term) by k_bd_final,
+// which then forms the vectors, the gate and the element (preconditioner,
+// damping, clip, u = f - J prev; deer.py:161-170) in the same CTA.
+
+// g~ = G - prec x~ and r = S - x~ - eps g~ (T x D)
+template <typename ST>
+__global__ void k_bd_resid(cs_system sys, const ST *s0, const ST *guess, const double *A2, const double *G,
+                           double *GX, double *R) {
+  const int D = sys.dim;
+  const int64_t total = sys.T * D;
+  const double prec = sys.target.prior_precision, eps = sys.eps;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / D;
+    const int i = (int)(idx - r * D);
+    const double s = (double)(r == 0 ? s0[i] : guess[(r - 1) * D + i]);
+    const double xt = A2[idx], gt = G[idx] - prec * xt;
+    GX[idx] = gt;
+    R[idx] = (s - xt) - eps * gt;
+  }
+}
+
+__global__ void k_bd_scale(double *E, const double *W, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    E[i] *= W[i];
+}
+
+constexpr int kBdThr = 256;
+
+// one CTA per step r: H_raw = X^T diag(w_S) X (register-tiled, X streamed
+// through shared memory in 16-row slices, the next slice prefetched into
+// registers), then the closed-form J and the dense element
+CS_D unsigned tf32_of(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+CS_D void mma_tf32(float (&c)[4], unsigned a0, unsigned a1, unsigned a2, unsigned a3, unsigned b0, unsigned b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+CS_D void cp_async16_zfill(void *dst, const void *src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+// X as f32 rows padded to 128 columns (the tensor-core Hessian's operand)
+__global__ void k_bd_xf(const double *X, int N, int D, float *Xf) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N * 128; i += gridDim.x * blockDim.x) {
+    const int n = i >> 7, d = i & 127;
+    Xf[i] = d < D ? (float)X[(int64_t)n * D + d] : 0.0f;
+  }
+}
+
+constexpr int kTcKB = 32, kTcLD = 136;  // n rows per staged block; padded row stride (conflict-free fragments)
+
+template <typename ST, int DP, bool TC>
+__global__ void __launch_bounds__(kBdThr)
+k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, const double *A2, const double *GX,
+           const double *gS, const double *R, const double *HR, const double *WS, const double *rsS,
+           const double *rsX, const float *Xf, ST *Jout, ST *uout, cs_elem_stats *stats) {
+  using CT = ST;
+  constexpr int NA = DP / 16, SL = 16, PER = SL * DP / kBdThr;
+  constexpr int XS = TC ? 2 * kTcKB * kTcLD + 2 * kTcKB : 2 * SL * DP;  // staging elements
+  const int D = sys.dim, N = (int)sys.target.n_data;
+  const double prec = sys.target.prior_precision, eps = sys.eps;
+  const double *X = sys.target.X;
+  const ST *xi = (const ST *)sys.noise_vec;
+  extern __shared__ __align__(16) unsigned char bsm[];
+  CT *Hs = (CT *)bsm;                      // DP x DP
+  CT *Xs = Hs + DP * DP;                   // SIMT: 2 x SL x DP; TC: 2 x kTcKB x kTcLD + 2 x kTcKB weights
+  double *vS = (double *)(Xs + XS + ((XS & 1) ? 1 : 0));
+  double *vX = vS + DP, *vG = vX + DP, *vR = vG + DP, *vW = vR + DP, *vH = vW + DP;
+  __shared__ double red[4][kBdThr / 32];
+  __shared__ int flags[3];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4, lane = tid & 31, wid = tid >> 5;
+  const bool do_clip = isfinite(cfg.clip);
+  for (int64_t r = blockIdx.x; r < sys.T; r += gridDim.x) {
+    const int64_t t = r + 1;
+    const double *w = WS + r * N;
+    if constexpr (TC) {
+      // H_raw on the tensor cores (mma.sync m16n8k8 TF32, f32 accumulate):
+      // warp wid owns output rows 16 wid .. 16 wid + 15, all 16 column blocks
+      // of 8; A[d][n] = w_n X[n][d], B[n][e] = X[n][e], K = the N data rows
+      // in blocks of 32 staged by cp.async (double-buffered)
+      static_assert(!TC || (DP == 128 && sizeof(ST) == 4), "tensor-core Hessian: f32, 128 padded columns");
+      float *xs = (float *)Xs, *wsl = xs + 2 * kTcKB * kTcLD;
+      const int g = lane >> 2, tq = lane & 3;
+      float acc[16][4];
+#pragma unroll
+      for (int cb = 0; cb < 16; ++cb) acc[cb][0] = acc[cb][1] = acc[cb][2] = acc[cb][3] = 0.0f;
+      const int nkb = (N + kTcKB - 1) / kTcKB;
+      auto stage = [&](int kb, int buf) {
+#pragma unroll
+        for (int p = 0; p < kTcKB * 32 / kBdThr; ++p) {
+          const int idx = tid + p * kBdThr, row = idx >> 5, c16 = idx & 31, n = kb * kTcKB + row;
+          cp_async16_zfill(xs + buf * kTcKB * kTcLD + row * kTcLD + c16 * 4, Xf + (int64_t)(n < N ? n : 0) * 128 + c16 * 4,
+                           n < N);
+        }
+        if (tid < kTcKB) {
+          const int n = kb * kTcKB + tid;
+          wsl[buf * kTcKB + tid] = n < N ? (float)__ldg(w + n) : 0.0f;
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      stage(0, 0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        if (kb + 1 < nkb) {
+          stage(kb + 1, (kb + 1) & 1);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const float *xb = xs + (kb & 1) * kTcKB * kTcLD, *wb = wsl + (kb & 1) * kTcKB;
+#pragma unroll
+        for (int ks = 0; ks < kTcKB / 8; ++ks) {
+          const int n0 = ks * 8;
+          const float w0 = wb[n0 + tq], w1 = wb[n0 + tq + 4];
+          const float *r0 = xb + (n0 + tq) * kTcLD, *r1 = xb + (n0 + tq + 4) * kTcLD;
+          const int d0 = 16 * wid + g;
+          const unsigned a0 = tf32_of(w0 * r0[d0]), a1 = tf32_of(w0 * r0[d0 + 8]);
+          const unsigned a2 = tf32_of(w1 * r1[d0]), a3 = tf32_of(w1 * r1[d0 + 8]);
+#pragma unroll
+          for (int cb = 0; cb < 16; ++cb)
+            mma_tf32(acc[cb], a0, a1, a2, a3, tf32_of(r0[8 * cb + g]), tf32_of(r1[8 * cb + g]));
+        }
+        __syncthreads();  // the buffer is restaged two blocks on
+      }
+#pragma unroll
+      for (int cb = 0; cb < 16; ++cb) {
+        const int row = 16 * wid + g, col = 8 * cb + 2 * tq;
+        Hs[row * DP + col] = acc[cb][0];
+        Hs[row * DP + col + 1] = acc[cb][1];
+        Hs[(row + 8) * DP + col] = acc[cb][2];
+        Hs[(row + 8) * DP + col + 1] = acc[cb][3];
+      }
+    } else {
+    CT pf[PER];
+    auto fetch = [&](int n0) {
+#pragma unroll
+      for (int p = 0; p < PER; ++p) {
+        const int idx = tid + p * kBdThr, nn = idx / DP, d = idx - nn * DP, n = n0 + nn;
+        pf[p] = (n < N && d < D) ? (CT)(__ldg(X + (int64_t)n * D + d) * __ldg(w + n)) : CT(0);
+      }
+    };
+    auto stash = [&](int buf) {
+#pragma unroll
+      for (int p = 0; p < PER; ++p) Xs[buf * SL * DP + tid + p * kBdThr] = pf[p];
+    };
+    // the unweighted operand X[n][e] is read straight from the L2-resident X
+    CT acc[NA][NA];
+#pragma unroll
+    for (int x = 0; x < NA; ++x)
+#pragma unroll
+      for (int y = 0; y < NA; ++y) acc[x][y] = CT(0);
+    const int nsl = (N + SL - 1) / SL;
+    fetch(0);
+    stash(0);
+    __syncthreads();
+    for (int sl = 0; sl < nsl; ++sl) {
+      if (sl + 1 < nsl) fetch((sl + 1) * SL);
+      const CT *Xc = Xs + (sl & 1) * SL * DP;
+#pragma unroll 4
+      for (int nn = 0; nn < SL; ++nn) {
+        const int n = sl * SL + nn;
+        CT a[NA], b[NA];
+#pragma unroll
+        for (int x = 0; x < NA; ++x) a[x] = Xc[nn * DP + ty + 16 * x];  // w_n X[n][i]
+        const double *xr = X + (int64_t)(n < N ? n : 0) * D;
+#pragma unroll
+        for (int y = 0; y < NA; ++y) {
+          const int e = tx + 16 * y;
+          b[y] = (n < N && e < D) ? (CT)__ldg(xr + e) : CT(0);
+        }
+#pragma unroll
+        for (int x = 0; x < NA; ++x)
+#pragma unroll
+          for (int y = 0; y < NA; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+      }
+      if (sl + 1 < nsl) stash((sl + 1) & 1);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int x = 0; x < NA; ++x)
+#pragma unroll
+      for (int y = 0; y < NA; ++y) Hs[(ty + 16 * x) * DP + tx + 16 * y] = acc[x][y];
+    }
+    // vectors
+    double ss = 0.0, sx = 0.0, sr = 0.0, sxi = 0.0, hxr = 0.0;
+    const ST *pr = r == 0 ? s0 : guess + (r - 1) * D;
+    if (tid < D) {
+      const double S = (double)pr[tid], xt = A2[r * D + tid], rr = R[r * D + tid], z = (double)xi[t * D + tid];
+      vS[tid] = S;
+      vX[tid] = xt;
+      vG[tid] = GX[r * D + tid];
+      vR[tid] = rr;
+      hxr = -HR[r * D + tid] - prec * rr;  // H(x~) r
+      vH[tid] = hxr;
+      ss = S * S;
+      sx = xt * xt;
+      sr = rr * rr;
+      sxi = z * z;
+    }
+    ss = warp_sum(ss);
+    sx = warp_sum(sx);
+    sr = warp_sum(sr);
+    sxi = warp_sum(sxi);
+    if (lane == 0) {
+      red[0][wid] = ss;
+      red[1][wid] = sx;
+      red[2][wid] = sr;
+      red[3][wid] = sxi;
+    }
+    if (tid < 3) flags[tid] = 0;
+    __syncthreads();  // Hs, vectors, partial sums
+    ss = sx = sr = sxi = 0.0;
+#pragma unroll
+    for (int k = 0; k < kBdThr / 32; ++k) {
+      ss += red[0][k];
+      sx += red[1][k];
+      sr += red[2][k];
+      sxi += red[3][k];
+    }
+    const double lpX = (rsX[2 * r] - rsX[2 * r + 1]) - 0.5 * prec * sx;
+    const double lpS = (rsS[2 * r] - rsS[2 * r + 1]) - 0.5 * prec * ss;
+    const double delta = lpX - lpS - sr / (4.0 * eps) + 0.5 * sxi;  // samplers.py:111-116
+    const double margin = fmin(0.0, delta) - __ldg(sys.noise_logu + t);
+    const double gate = margin > 0.0 ? 1.0 : 0.0;
+    const double cb = sigmoid_prime(margin) * (delta < 0.0 ? 1.0 : 0.0);
+    // w_i = A g~ - g(S) + (H(S) r + A H(x~) r)/2, H(S) v = -(H_raw v) - prec v
+    if (tid < D) {
+      double hg = 0.0, hr = 0.0, hh = 0.0;
+      const CT *hrow = Hs + tid * DP;
+      for (int j = 0; j < D; ++j) {
+        const double h = (double)hrow[j];
+        hg = fma(h, vG[j], hg);
+        hr = fma(h, vR[j], hr);
+        hh = fma(h, vH[j], hh);
+      }
+      hg = -hg - prec * vG[tid];
+      hr = -hr - prec * vR[tid];
+      hh = -hh - prec * vH[tid];
+      vW[tid] = (vG[tid] + eps * hg) - gS[r * D + tid] + 0.5 * (hr + (hxr + eps * hh));
+    }
+    __syncthreads();
+    // element: J_ij = gate (d_ij + eps H_ij) + (1 - gate) d_ij + cb (x~_i - S_i) w_j, then the
+    // preconditioner ratio p_j / p_i, damping and clip (deer.py:161-170)
+    auto Jij = [&](int i, int j) {
+      const double hij = -(double)Hs[i * DP + j] - (i == j ? prec : 0.0);
+      const double dij = i == j ? 1.0 : 0.0;
+      double v = gate * (dij + eps * hij) + (1.0 - gate) * dij + cb * (vX[i] - vS[i]) * vW[j];
+      if (cfg.preconditioner) v = v * (__ldg(cfg.preconditioner + j) / __ldg(cfg.preconditioner + i));
+      v = v * cfg.damping;
+      if (do_clip) v = clipv(v, cfg.clip);
+      return v;
+    };
+    ST *Jr = Jout + r * (int64_t)D * D;
+    bool jok = true;
+    for (int idx = tid; idx < D * D; idx += kBdThr) {
+      const int i = idx / D, j = idx - i * D;
+      const double v = Jij(i, j);
+      jok &= isfinite(v);
+      Jr[idx] = (ST)v;
+    }
+    if (!jok) flags[1] = 1;
+    if (tid < D) {
+      const double f = gate > 0.0 ? vX[tid] : vS[tid];
+      double jp = 0.0;
+      for (int j = 0; j < D; ++j) jp = fma(Jij(tid, j), vS[j], jp);
+      uout[r * D + tid] = (ST)(f - jp);
+      if (!isfinite(f)) flags[0] = 1;
+      if (!(fabs(f - (double)guess[r * D + tid]) <= cfg.atol + cfg.rtol * fabs(f))) flags[2] = 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (flags[0]) atomicMin((long long *)&stats->bad_step, (long long)t);
+      if (flags[1]) atomicMin((long long *)&stats->bad_jacobian, (long long)t);
+      if (flags[2]) atomicAdd(&stats->picard_fail, 1u);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 bool blr_mala_ok(const cs_system &s, int mode) {
-  return s.kind == CS_SYS_MALA && s.target.kind == CS_TARGET_BLR && mode == CS_MODE_DIAG && s.dim >= 1 &&
+  return s.kind == CS_SYS_MALA && s.target.kind == CS_TARGET_BLR && (mode == CS_MODE_DIAG || mode == CS_MODE_DENSE) &&
+         s.dim >= 1 &&
          s.dim <= kBlrMaxD && s.target.dim == s.dim && s.target.X && s.target.y && s.target.n_data > 0 &&
          s.noise_vec && s.noise_logu;
 }
@@ -283,9 +581,104 @@ static cudaError_t blr_run(const cs_system &sys, const cs_deer_config &cfg, int6
   return cudaGetLastError();
 }
 
+static bool bd_tensor_cores() {  // CS_BLR_DENSE_TC=0 keeps the f32 Hessian on the FP32 pipes
+  static const bool v = [] {
+    const char *e = getenv("CS_BLR_DENSE_TC");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
+template <typename ST, int DP, bool TC = false>
+static cudaError_t bd_final_launch(const cs_system &sys, const cs_deer_config &cfg, const ST *s0, const ST *guess,
+                                   const double *A2, const double *GX, const double *gS, const double *R,
+                                   const double *HR, const double *WS, const double *rsS, const double *rsX,
+                                   const float *Xf, ST *J, ST *u, cs_elem_stats *stats, cudaStream_t st) {
+  const size_t xs = TC ? 2 * kTcKB * kTcLD + 2 * kTcKB : 2 * 16 * DP;
+  const size_t smem = sizeof(ST) * ((size_t)DP * DP + xs) + 8 + 6 * DP * sizeof(double);
+  auto k = k_bd_final<ST, DP, TC>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = sys.T < 148 * 16 ? sys.T : 148 * 16;
+  k<<<(unsigned)grid, kBdThr, smem, st>>>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, u, stats);
+  return cudaGetLastError();
+}
+
+template <typename ST>
+static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg, int64_t iteration, const ST *s0,
+                                 const ST *guess, ST *J, ST *uout, cs_elem_stats *stats, cudaStream_t st) {
+  const int D = sys.dim, N = (int)sys.target.n_data;
+  const int64_t T = sys.T;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  BlrCtx &ctx = g_blr[dev & 15];
+  std::lock_guard<std::mutex> lock(ctx.mu);
+  if (!ctx.h && cublasCreate(&ctx.h) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  // A, A2, G, gS, GX, R, HR (T x D); E, WS, WX (T x N); row sums 2 x (2T)
+  const size_t need = (size_t)7 * T * D + (size_t)3 * T * N + (size_t)4 * T + (size_t)64 * N;  // + Xf (N x 128 f32)
+  if (ctx.cap < need) {
+    if (ctx.buf) cudaFree(ctx.buf);
+    ctx.buf = nullptr;
+    ctx.cap = 0;
+    cudaError_t e = cudaMalloc(&ctx.buf, need * sizeof(double));
+    if (e != cudaSuccess) return e;
+    ctx.cap = need;
+  }
+  double *A = ctx.buf, *A2 = A + (size_t)T * D, *G = A2 + (size_t)T * D, *gS = G + (size_t)T * D;
+  double *GX = gS + (size_t)T * D, *R = GX + (size_t)T * D, *HR = R + (size_t)T * D;
+  double *E = HR + (size_t)T * D, *WS = E + (size_t)T * N, *WX = WS + (size_t)T * N;
+  double *rsS = WX + (size_t)T * N, *rsX = rsS + 2 * T;
+  float *Xf = (float *)(rsX + 2 * T);
+  const double *X = sys.target.X, *y = sys.target.y;
+  const double one = 1.0, zero = 0.0;
+  if (cublasSetStream(ctx.h, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  auto gemm_xt = [&](const double *Ain, double *Cout) {  // row-major C (T x N) = A (T x D) X^T
+    return cublasDgemm(ctx.h, CUBLAS_OP_T, CUBLAS_OP_N, N, (int)T, D, &one, X, D, Ain, D, &zero, Cout, N);
+  };
+  auto gemm_x = [&](const double *Bin, double *Cout) {  // row-major C (T x D) = B (T x N) X
+    return cublasDgemm(ctx.h, CUBLAS_OP_N, CUBLAS_OP_N, D, (int)T, N, &one, X, D, Bin, N, &zero, Cout, D);
+  };
+  const unsigned ge = (unsigned)((T * D + 255) / 256 < 148 * 32 ? (T * D + 255) / 256 : 148 * 32);
+  const unsigned gw = (unsigned)((T * 32 + 255) / 256);
+  k_blr_prologue<ST><<<ge, 256, 0, st>>>(sys, s0, guess, iteration, 0, A);
+  if (gemm_xt(A, E) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsS, WS);
+  if (gemm_x(E, G) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  k_blr_propose<ST><<<gw, 256, 0, st>>>(sys, s0, guess, A, G, 0, A2, gS, stats);
+  if (gemm_xt(A2, E) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsX, WX);
+  if (gemm_x(E, G) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  k_bd_resid<ST><<<ge, 256, 0, st>>>(sys, s0, guess, A2, G, GX, R);
+  if (gemm_xt(R, E) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  k_bd_scale<<<148 * 32, 256, 0, st>>>(E, WX, T * N);
+  if (gemm_x(E, HR) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if constexpr (sizeof(ST) == 4) {
+    if (bd_tensor_cores()) {  // f32 storage: H(S) on the tensor cores (TF32 in, f32 accumulate)
+      k_bd_xf<<<(N * 128 + 255) / 256, 256, 0, st>>>(X, N, D, Xf);
+      return bd_final_launch<ST, 128, true>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout,
+                                            stats, st);
+    }
+  }
+  const int dp = D <= 16 ? 16 : D <= 32 ? 32 : D <= 64 ? 64 : D <= 112 ? 112 : 128;
+  switch (dp) {
+    case 16: return bd_final_launch<ST, 16>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout, stats, st);
+    case 32: return bd_final_launch<ST, 32>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout, stats, st);
+    case 64: return bd_final_launch<ST, 64>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout, stats, st);
+    case 112: return bd_final_launch<ST, 112>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout, stats, st);
+    default: return bd_final_launch<ST, 128>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout, stats, st);
+  }
+}
+
 cudaError_t elements_blr(const cs_system &sys, const cs_deer_config &cfg, int dtype, int64_t iteration,
                          const void *s0, const void *guess, void *e0, void *u, cs_elem_stats *stats,
                          cudaStream_t st) {
+  if (cfg.mode == CS_MODE_DENSE) {
+    if (dtype == CS_F64)
+      return blr_dense_run<double>(sys, cfg, iteration, (const double *)s0, (const double *)guess, (double *)e0,
+                                   (double *)u, stats, st);
+    return blr_dense_run<float>(sys, cfg, iteration, (const float *)s0, (const float *)guess, (float *)e0,
+                                (float *)u, stats, st);
+  }
   if (dtype == CS_F64)
     return blr_run<double>(sys, cfg, iteration, (const double *)s0, (const double *)guess, (double *)e0,
                            (double *)u, stats, st);

@@ -29,10 +29,12 @@ __global__ void __launch_bounds__(kDwReduceThr)
 k_dense_reduce(const ST *__restrict__ J, const ST *__restrict__ u, int64_t T, int D, int c, double *aggM,
                double *aggw) {
   constexpr int NA = DP / 16;
+  constexpr int NS = DP / kDwSlice;                          // slices per step
+  constexpr int PER = DP * kDwSlice / kDwReduceThr;          // slice elements per thread (DP*16/256)
   extern __shared__ __align__(16) unsigned char dsm[];
   ST *Ms = (ST *)dsm;              // DP x DP running product (zero padded)
-  ST *Js = Ms + DP * DP;           // DP x kDwSlice slice of J_t
-  ST *wv = Js + DP * kDwSlice;     // DP running affine part
+  ST *Js = Ms + DP * DP;           // 2 x (DP x kDwSlice) slices of J_t, double-buffered
+  ST *wv = Js + 2 * DP * kDwSlice; // DP running affine part
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t q = blockIdx.x, t0 = q * (int64_t)c;
   const int64_t t1 = t0 + c < T ? t0 + c : T;
@@ -45,26 +47,49 @@ k_dense_reduce(const ST *__restrict__ J, const ST *__restrict__ u, int64_t T, in
     }
     for (int i = tid; i < DP; i += kDwReduceThr) wv[i] = i < D ? u[t0 * D + i] : ST(0);
   }
-  __syncthreads();
-  for (int64_t t = t0 + 1; t < t1; ++t) {
+  // slice n of the chunk's stream (step t0+1+n/NS, columns (n%NS)*16..): each
+  // thread owns PER fixed (row, column) positions of it; the next slice is
+  // loaded into registers while the current one is multiplied
+  ST pf[PER];
+  auto fetch = [&](int64_t n) {
+    const int64_t t = t0 + 1 + n / NS;
+    const int k0 = (int)(n % NS) * kDwSlice;
     const ST *Jt = J + t * DD;
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int idx = tid + p * kDwReduceThr;
+      const int i = idx / kDwSlice, k = k0 + (idx - i * kDwSlice);
+      pf[p] = (t < t1 && i < D && k < D) ? __ldg(Jt + i * D + k) : ST(0);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int p = 0; p < PER; ++p) Js[buf * DP * kDwSlice + tid + p * kDwReduceThr] = pf[p];
+  };
+  const int64_t nslices = (t1 - t0 - 1) * NS;
+  if (nslices > 0) {
+    fetch(0);
+    stash(0);
+  }
+  __syncthreads();
+  int64_t n = 0;
+  for (int64_t t = t0 + 1; t < t1; ++t) {
     ST acc[NA][NA];
 #pragma unroll
     for (int x = 0; x < NA; ++x)
 #pragma unroll
       for (int y = 0; y < NA; ++y) acc[x][y] = ST(0);
     double wacc = 0.0;  // thread i < D: row i of J_t w
-    for (int k0 = 0; k0 < DP; k0 += kDwSlice) {
-      for (int idx = tid; idx < DP * kDwSlice; idx += kDwReduceThr) {
-        const int i = idx / kDwSlice, k = k0 + (idx - i * kDwSlice);
-        Js[idx] = (i < D && k < D) ? Jt[i * D + k] : ST(0);
-      }
-      __syncthreads();
+#pragma unroll 1
+    for (int sl = 0; sl < NS; ++sl, ++n) {
+      const int k0 = sl * kDwSlice;
+      if (n + 1 < nslices) fetch(n + 1);
+      const ST *Jc = Js + (n & 1) * DP * kDwSlice;
 #pragma unroll
       for (int kk = 0; kk < kDwSlice; ++kk) {
         ST a[NA], b[NA];
 #pragma unroll
-        for (int x = 0; x < NA; ++x) a[x] = Js[(ty + 16 * x) * kDwSlice + kk];
+        for (int x = 0; x < NA; ++x) a[x] = Jc[(ty + 16 * x) * kDwSlice + kk];
 #pragma unroll
         for (int y = 0; y < NA; ++y) b[y] = Ms[(k0 + kk) * DP + tx + 16 * y];
 #pragma unroll
@@ -74,9 +99,11 @@ k_dense_reduce(const ST *__restrict__ J, const ST *__restrict__ u, int64_t T, in
       }
       if (tid < DP)
 #pragma unroll
-        for (int kk = 0; kk < kDwSlice; ++kk) wacc += (double)Js[tid * kDwSlice + kk] * (double)wv[k0 + kk];
-      __syncthreads();
+        for (int kk = 0; kk < kDwSlice; ++kk) wacc += (double)Jc[tid * kDwSlice + kk] * (double)wv[k0 + kk];
+      if (n + 1 < nslices) stash((int)((n + 1) & 1));  // the other buffer: last read a slice ago
+      if (sl + 1 < NS) __syncthreads();
     }
+    __syncthreads();  // every product read of Ms done
 #pragma unroll
     for (int x = 0; x < NA; ++x)
 #pragma unroll
@@ -92,88 +119,131 @@ k_dense_reduce(const ST *__restrict__ J, const ST *__restrict__ u, int64_t T, in
   for (int i = tid; i < D; i += kDwReduceThr) aggw[q * D + i] = (double)wv[i];
 }
 
-// entries[q] = state entering chunk q; e_{q+1} = M_q e_q + w_q.  Four threads
-// per row; the next chunk's matrix rows are loaded while this one is applied.
-template <typename ST>
+// entries[q] = state entering chunk q; e_{q+1} = M_q e_q + w_q.  Warp w owns
+// rows w, w + 16, ...; lanes stride the columns (coalesced row reads), and
+// the next chunk's matrix is loaded into registers while this one is applied.
+template <typename ST, int DP>
 __global__ void __launch_bounds__(kDwThr)
 k_dense_carry(const double *aggM, const double *aggw, const ST *s0, int64_t nch, int D, double *entries) {
-  constexpr int KP = 32;  // columns per thread (D <= 128)
+  constexpr int NW = kDwThr / 32, RPW = DP / NW, KL = (DP + 31) / 32;
   __shared__ double e[2][128];
-  const int tid = threadIdx.x, i = tid >> 2, part = tid & 3;
-  const bool row = i < D;
-  const int kb = part * KP;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t DD = (int64_t)D * D;
   if (tid < D) e[0][tid] = (double)s0[tid];
-  double m[KP];
+  double m[RPW][KL];
   auto load = [&](int64_t q) {
 #pragma unroll
-    for (int k = 0; k < KP; ++k) m[k] = (row && kb + k < D) ? aggM[q * DD + (int64_t)i * D + kb + k] : 0.0;
+    for (int r = 0; r < RPW; ++r) {
+      const int i = w + NW * r;
+#pragma unroll
+      for (int k = 0; k < KL; ++k) {
+        const int col = lane + 32 * k;
+        m[r][k] = (i < D && col < D) ? __ldcg(aggM + q * DD + (int64_t)i * D + col) : 0.0;
+      }
+    }
   };
   if (nch > 0) load(0);
   __syncthreads();
   for (int64_t q = 0; q < nch; ++q) {
     const double *cur = e[q & 1];
-    double acc = 0.0;
+    double acc[RPW];
 #pragma unroll
-    for (int k = 0; k < KP; ++k) acc = fma(m[k], kb + k < D ? cur[kb + k] : 0.0, acc);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    for (int r = 0; r < RPW; ++r) {
+      acc[r] = 0.0;
+#pragma unroll
+      for (int k = 0; k < KL; ++k) {
+        const int col = lane + 32 * k;
+        acc[r] = fma(m[r][k], col < D ? cur[col] : 0.0, acc[r]);
+      }
+    }
     if (q + 1 < nch) load(q + 1);
-    if (row && part == 0) {
-      entries[q * D + i] = cur[i];
-      e[(q + 1) & 1][i] = acc + aggw[q * D + i];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
+      const int i = w + NW * r;
+      if (lane == 0 && i < D) {
+        entries[q * D + i] = cur[i];
+        e[(q + 1) & 1][i] = acc[r] + __ldcg(aggw + q * D + i);
+      }
     }
     __syncthreads();
   }
 }
 
 // replay chunk q from its entry: warp w owns rows w, w + 16, ...; lanes
-// stride the columns, f64 sums, one barrier per step
-template <typename ST>
+// stride the columns, f64 sums, one barrier per step; J_{t+1} is loaded into
+// a second register set while step t is applied
+template <typename ST, int DP>
 __global__ void __launch_bounds__(kDwThr)
 k_dense_replay(const ST *__restrict__ J, const ST *__restrict__ u, const double *entries, int64_t T, int D, int c,
                ST *out) {
-  constexpr int NW = kDwThr / 32, RPW = (128 + NW - 1) / NW, KL = 4;  // rows per warp, columns per lane
+  constexpr int NW = kDwThr / 32, RPW = DP / NW, KL = (DP + 31) / 32;
   __shared__ double s[2][128];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t q = blockIdx.x, t0 = q * (int64_t)c;
   const int64_t t1 = t0 + c < T ? t0 + c : T;
   const int64_t DD = (int64_t)D * D;
   if (tid < D) s[0][tid] = entries[q * D + tid];
-  __syncthreads();
-  int par = 0;
-  for (int64_t t = t0; t < t1; ++t) {
+  ST ja[RPW][KL];
+  ST jb[sizeof(ST) == 4 ? RPW : 1][sizeof(ST) == 4 ? KL : 1];  // f64: one set (registers)
+  auto load = [&](int64_t t, ST (&jv)[RPW][KL]) {
     const ST *Jt = J + t * DD;
-    ST jv[RPW][KL];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
       const int i = w + NW * r;
 #pragma unroll
       for (int m = 0; m < KL; ++m) {
         const int k = lane + 32 * m;
-        jv[r][m] = (i < D && k < D) ? __ldg(Jt + (int64_t)i * D + k) : ST(0);
+        jv[r][m] = (t < t1 && i < D && k < D) ? __ldcs(Jt + (int64_t)i * D + k) : ST(0);
       }
     }
+  };
+  auto step = [&](int64_t t, const ST (&jv)[RPW][KL], int par) {
     const double *cur = s[par];
+    double acc[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
-      const int i = w + NW * r;
-      double acc = 0.0;
+      acc[r] = 0.0;
 #pragma unroll
       for (int m = 0; m < KL; ++m) {
         const int k = lane + 32 * m;
-        acc = fma((double)jv[r][m], k < D ? cur[k] : 0.0, acc);
+        acc[r] = fma((double)jv[r][m], k < D ? cur[k] : 0.0, acc[r]);
       }
+    }
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
+      const int i = w + NW * r;
       if (lane == 0 && i < D) {
-        const ST v = (ST)(acc + (double)u[t * D + i]);
+        const ST v = (ST)(acc[r] + (double)u[t * D + i]);
         s[par ^ 1][i] = (double)v;
         out[t * D + i] = v;
       }
     }
-    par ^= 1;
     __syncthreads();
+  };
+  __syncthreads();
+  int par = 0;
+  if constexpr (sizeof(ST) == 8) {
+    for (int64_t t = t0; t < t1; ++t) {
+      load(t, ja);
+      step(t, ja, par);
+      par ^= 1;
+    }
+    return;
+  } else {
+  load(t0, ja);
+  for (int64_t t = t0; t < t1; t += 2) {
+    load(t + 1, jb);
+    step(t, ja, par);
+    par ^= 1;
+    if (t + 1 >= t1) break;
+    load(t + 2, ja);
+    step(t + 1, jb, par);
+    par ^= 1;
+  }
   }
 }
 
@@ -200,12 +270,19 @@ static int dense_dp(int D) { return D <= 16 ? 16 : D <= 32 ? 32 : D <= 64 ? 64 :
 template <typename ST, int DP>
 static cudaError_t launch_reduce(const ScanArgs<ST> &a, int c, int64_t nch, double *aggM, double *aggw,
                                  cudaStream_t st) {
-  const size_t smem = sizeof(ST) * ((size_t)DP * DP + (size_t)DP * kDwSlice + DP);
+  const size_t smem = sizeof(ST) * ((size_t)DP * DP + 2 * (size_t)DP * kDwSlice + DP);
   auto k = k_dense_reduce<ST, DP>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<(unsigned)nch, kDwReduceThr, smem, st>>>(a.e0, a.u, a.T, a.D, c, aggM, aggw);
   return cudaGetLastError();
+}
+
+template <typename ST, int DP>
+static void launch_tail(const ScanArgs<ST> &a, int c, int64_t nch, const double *aggM, const double *aggw,
+                        double *entries, cudaStream_t st) {
+  k_dense_carry<ST, DP><<<1, kDwThr, 0, st>>>(aggM, aggw, a.s0, nch, a.D, entries);
+  k_dense_replay<ST, DP><<<(unsigned)nch, kDwThr, 0, st>>>(a.e0, a.u, entries, a.T, a.D, c, a.out);
 }
 
 template <typename ST>
@@ -227,8 +304,13 @@ cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
     default: e = launch_reduce<ST, 128>(a, c, nch, aggM, aggw, st); break;
   }
   if (e != cudaSuccess) return e;
-  k_dense_carry<ST><<<1, kDwThr, 0, st>>>(aggM, aggw, a.s0, nch, D, entries);
-  k_dense_replay<ST><<<(unsigned)nch, kDwThr, 0, st>>>(a.e0, a.u, entries, T, D, c, a.out);
+  switch (dense_dp(D)) {
+    case 16: launch_tail<ST, 16>(a, c, nch, aggM, aggw, entries, st); break;
+    case 32: launch_tail<ST, 32>(a, c, nch, aggM, aggw, entries, st); break;
+    case 64: launch_tail<ST, 64>(a, c, nch, aggM, aggw, entries, st); break;
+    case 112: launch_tail<ST, 112>(a, c, nch, aggM, aggw, entries, st); break;
+    default: launch_tail<ST, 128>(a, c, nch, aggM, aggw, entries, st); break;
+  }
   return cudaGetLastError();
 }
 

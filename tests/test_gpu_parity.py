@@ -394,8 +394,14 @@ def test_run_deer_blr_dense_wide(cuda_device, dtype):
     g0, g = golden("mala_blr100"), golden("mala_blr100_dense")
     m = cs.model_logp_grad_hvp(cs.blr(g0["X"], g0["y"], 1.0))
     k = cs.MalaKernel(m, 0.003, seed=4, T=300, dtype=dtype)
+    # closed-form element builder on the streamed engine (cs_blr.cu, k_bd_final)
     r = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="dense"))
+    assert r.stats["path"] == "streamed"
     _deer_cmp(r, g, "dense_", dtype)
+    # and the reference's own construction: J column by column from D jvps (host engine)
+    h = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="dense", engine="host"))
+    assert h.stats["path"] == "host"
+    _deer_cmp(h, g, "dense_", dtype)
 
 
 def test_run_deer_leapfrog_gauss200(cuda_device):

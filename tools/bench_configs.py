@@ -17,7 +17,14 @@ import paper_2508_18413_b200 as cs  # noqa: E402
 
 
 def timed(fn, reps):
-    fn()
+    if reps == 0:  # one cold run, timed (long solves are their own warm-up)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b), r
+    r = fn()
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
@@ -62,6 +69,17 @@ def main():
         k = cs.MalaKernel(m, 0.003, seed=4, T=100_000, dtype=torch.float64)
         ms, r = timed(lambda: cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="diag-stochastic")), 1)
         rows.append(("cfg3 MALA BLR D=100 T=100K diag (f64)", ms, r, 100_000, None))
+    for key, T3 in (("3d10k", 10_000), ("3d", 100_000)):
+        if key not in which:
+            continue
+        # cfg3 "full": dense Newton (Jacobians from the system's jvps, wide dense scan)
+        X, y, _ = cs.synthetic_credit_like(seed=20250819, n=1000, dim=100)
+        m = cs.model_logp_grad_hvp(cs.blr(X, y, 1.0))
+        k = cs.MalaKernel(m, 0.003, seed=4, T=T3, dtype=dt)
+        t0 = time.perf_counter()
+        ms, r = timed(lambda: cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="dense")), 0)
+        print(f"  cfg3 dense T={T3}: {time.perf_counter() - t0:.1f} s incl. warm-up", flush=True)
+        rows.append((f"cfg3 MALA BLR D=100 T={T3} dense (f32)", ms, r, T3, None))
     if "4" in which:
         D, eps, L = 1000, 0.05, 100
         Lc = cfg4_chol(D)

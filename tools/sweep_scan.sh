@@ -1,4 +1,6 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
-for c in 64 128 256; do CS_DENSE_CHUNK=$c timeout 120 python tools/probe_scan.py --mode dense --D 100 --T 100000 --reps 3; done
-timeout 120 python tools/probe_scan.py --mode dense --D 100 --T 100000 --reps 3 --dtype f64
-timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_dense -c 6 python tools/probe_scan.py --mode dense --D 100 --T 100000 --reps 1 2>&1 | grep -E "k_dense|gpu__time"
+timeout 600 python -m pytest tests -m gpu -x -q -k "blr or dense" 2>&1 | tail -5
+timeout 900 python tools/bench_configs.py 3d 2>&1 | tail -2
+CS_BLR_DENSE_TC=0 timeout 600 python tools/bench_configs.py 3d10k 2>&1 | tail -1
+timeout 600 python tools/bench_configs.py 3d10k 2>&1 | tail -1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/cfg3d_launches_tc.csv python tools/bench_configs.py 3d > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/cfg3d_launches_tc.csv | head -12
