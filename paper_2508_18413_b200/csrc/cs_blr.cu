@@ -328,6 +328,9 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
       // in blocks of 32 staged by cp.async (double-buffered)
       static_assert(!TC || (DP == 128 && sizeof(ST) == 4), "tensor-core Hessian: f32, 128 padded columns");
       float *xs = (float *)Xs, *wsl = xs + 2 * kTcKB * kTcLD;
+      // warp wid owns output rows 16 wid .. 16 wid + 15, all 16 column blocks
+      // (multiplying only the upper-triangle blocks measured slower: the
+      // per-block operand selection costs more than the saved MMAs)
       const int g = lane >> 2, tq = lane & 3;
       float acc[16][4];
 #pragma unroll
@@ -373,10 +376,14 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
 #pragma unroll
       for (int cb = 0; cb < 16; ++cb) {
         const int row = 16 * wid + g, col = 8 * cb + 2 * tq;
-        Hs[row * DP + col] = acc[cb][0];
-        Hs[row * DP + col + 1] = acc[cb][1];
-        Hs[(row + 8) * DP + col] = acc[cb][2];
-        Hs[(row + 8) * DP + col + 1] = acc[cb][3];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {  // upper triangle, mirrored: Hs is exactly symmetric
+          const int ri = row + (e >> 1) * 8, ci = col + (e & 1);
+          if (ci >= ri) {
+            Hs[ri * DP + ci] = acc[cb][e];
+            Hs[ci * DP + ri] = acc[cb][e];
+          }
+        }
       }
     } else {
     CT pf[PER];
@@ -427,7 +434,13 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
 #pragma unroll
     for (int x = 0; x < NA; ++x)
 #pragma unroll
-      for (int y = 0; y < NA; ++y) Hs[(ty + 16 * x) * DP + tx + 16 * y] = acc[x][y];
+      for (int y = 0; y < NA; ++y) {  // upper triangle, mirrored: Hs is exactly symmetric
+        const int ri = ty + 16 * x, ci = tx + 16 * y;
+        if (ci >= ri) {
+          Hs[ri * DP + ci] = acc[x][y];
+          Hs[ci * DP + ri] = acc[x][y];
+        }
+      }
     }
     // vectors
     double ss = 0.0, sx = 0.0, sr = 0.0, sxi = 0.0, hxr = 0.0;
@@ -474,9 +487,8 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     // w_i = A g~ - g(S) + (H(S) r + A H(x~) r)/2, H(S) v = -(H_raw v) - prec v
     if (tid < D) {
       double hg = 0.0, hr = 0.0, hh = 0.0;
-      const CT *hrow = Hs + tid * DP;
       for (int j = 0; j < D; ++j) {
-        const double h = (double)hrow[j];
+        const double h = (double)Hs[j * DP + tid];  // = H[tid][j] (symmetric), bank-conflict free
         hg = fma(h, vG[j], hg);
         hr = fma(h, vR[j], hr);
         hh = fma(h, vH[j], hh);
@@ -489,8 +501,8 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     __syncthreads();
     // element: J_ij = gate (d_ij + eps H_ij) + (1 - gate) d_ij + cb (x~_i - S_i) w_j, then the
     // preconditioner ratio p_j / p_i, damping and clip (deer.py:161-170)
-    auto Jij = [&](int i, int j) {
-      const double hij = -(double)Hs[i * DP + j] - (i == j ? prec : 0.0);
+    auto Jij = [&](int i, int j, double hraw) {  // hraw = H_raw[i][j]
+      const double hij = -hraw - (i == j ? prec : 0.0);
       const double dij = i == j ? 1.0 : 0.0;
       double v = gate * (dij + eps * hij) + (1.0 - gate) * dij + cb * (vX[i] - vS[i]) * vW[j];
       if (cfg.preconditioner) v = v * (__ldg(cfg.preconditioner + j) / __ldg(cfg.preconditioner + i));
@@ -502,7 +514,7 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     bool jok = true;
     for (int idx = tid; idx < D * D; idx += kBdThr) {
       const int i = idx / D, j = idx - i * D;
-      const double v = Jij(i, j);
+      const double v = Jij(i, j, (double)Hs[i * DP + j]);
       jok &= isfinite(v);
       Jr[idx] = (ST)v;
     }
@@ -510,7 +522,7 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     if (tid < D) {
       const double f = gate > 0.0 ? vX[tid] : vS[tid];
       double jp = 0.0;
-      for (int j = 0; j < D; ++j) jp = fma(Jij(tid, j), vS[j], jp);
+      for (int j = 0; j < D; ++j) jp = fma(Jij(tid, j, (double)Hs[j * DP + tid]), vS[j], jp);
       uout[r * D + tid] = (ST)(f - jp);
       if (!isfinite(f)) flags[0] = 1;
       if (!(fabs(f - (double)guess[r * D + tid]) <= cfg.atol + cfg.rtol * fabs(f))) flags[2] = 1;

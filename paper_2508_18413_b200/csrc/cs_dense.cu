@@ -122,14 +122,22 @@ k_dense_reduce(const ST *__restrict__ J, const ST *__restrict__ u, int64_t T, in
 // entries[q] = state entering chunk q; e_{q+1} = M_q e_q + w_q.  Warp w owns
 // rows w, w + 16, ...; lanes stride the columns (coalesced row reads), and
 // the next chunk's matrix is loaded into registers while this one is applied.
+// CTA g walks chunks [g per, g per + per) from its entry: gent[g] when given,
+// else s0 (one CTA over everything).
 template <typename ST, int DP>
 __global__ void __launch_bounds__(kDwThr)
-k_dense_carry(const double *aggM, const double *aggw, const ST *s0, int64_t nch, int D, double *entries) {
+k_dense_carry(const double *aggM, const double *aggw, const ST *s0, const double *gent, int64_t nch_all, int D,
+              int64_t per, double *entries) {
   constexpr int NW = kDwThr / 32, RPW = DP / NW, KL = (DP + 31) / 32;
   __shared__ double e[2][128];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t DD = (int64_t)D * D;
-  if (tid < D) e[0][tid] = (double)s0[tid];
+  const int64_t q0 = (int64_t)blockIdx.x * per;
+  const int64_t nch = q0 + per < nch_all ? per : nch_all - q0;
+  aggM += q0 * DD;
+  aggw += q0 * D;
+  entries += q0 * D;
+  if (tid < D) e[0][tid] = gent ? gent[(int64_t)blockIdx.x * D + tid] : (double)s0[tid];
   double m[RPW][KL];
   auto load = [&](int64_t q) {
 #pragma unroll
@@ -262,7 +270,8 @@ int dense_wide_chunk(int64_t T) {
 size_t dense_wide_ws_bytes(int64_t T, int D) {
   const int c = dense_wide_chunk(T);
   const int64_t nch = (T + c - 1) / c;
-  return (size_t)nch * ((size_t)D * D + 2 * D) * sizeof(double) + 256;
+  const int64_t ng = (nch + 15) / 16;
+  return (size_t)(nch + ng) * ((size_t)D * D + 2 * D) * sizeof(double) + 256;
 }
 
 static int dense_dp(int D) { return D <= 16 ? 16 : D <= 32 ? 32 : D <= 64 ? 64 : D <= 112 ? 112 : 128; }
@@ -278,11 +287,29 @@ static cudaError_t launch_reduce(const ScanArgs<ST> &a, int c, int64_t nch, doub
   return cudaGetLastError();
 }
 
+// Chunk entries: one serial walk over the chunk aggregates when they are few;
+// otherwise two levels -- groups of kDwGroup chunk aggregates are composed in
+// parallel (the reduce kernel again, on f64 aggregates), one CTA walks the
+// group aggregates, and every group then walks its own chunks from its entry.
+constexpr int kDwGroup = 16;
+
 template <typename ST, int DP>
-static void launch_tail(const ScanArgs<ST> &a, int c, int64_t nch, const double *aggM, const double *aggw,
-                        double *entries, cudaStream_t st) {
-  k_dense_carry<ST, DP><<<1, kDwThr, 0, st>>>(aggM, aggw, a.s0, nch, a.D, entries);
-  k_dense_replay<ST, DP><<<(unsigned)nch, kDwThr, 0, st>>>(a.e0, a.u, entries, a.T, a.D, c, a.out);
+static cudaError_t launch_tail(const ScanArgs<ST> &a, int c, int64_t nch, const double *aggM, const double *aggw,
+                               double *entries, double *gM, cudaStream_t st) {
+  const int D = a.D;
+  if (nch <= 4 * kDwGroup) {
+    k_dense_carry<ST, DP><<<1, kDwThr, 0, st>>>(aggM, aggw, a.s0, nullptr, nch, D, nch, entries);
+  } else {
+    const int64_t ng = (nch + kDwGroup - 1) / kDwGroup;
+    double *gw = gM + ng * (int64_t)D * D, *gent = gw + ng * (int64_t)D;
+    ScanArgs<double> g{aggM, nullptr, nullptr, nullptr, aggw, nullptr, nullptr, nch, D};
+    cudaError_t e = launch_reduce<double, DP>(g, kDwGroup, ng, gM, gw, st);
+    if (e != cudaSuccess) return e;
+    k_dense_carry<ST, DP><<<1, kDwThr, 0, st>>>(gM, gw, a.s0, nullptr, ng, D, ng, gent);
+    k_dense_carry<ST, DP><<<(unsigned)ng, kDwThr, 0, st>>>(aggM, aggw, a.s0, gent, nch, D, kDwGroup, entries);
+  }
+  k_dense_replay<ST, DP><<<(unsigned)nch, kDwThr, 0, st>>>(a.e0, a.u, entries, a.T, D, c, a.out);
+  return cudaGetLastError();
 }
 
 template <typename ST>
@@ -295,6 +322,7 @@ cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
   double *aggM = (double *)ws;
   double *aggw = aggM + nch * (int64_t)D * D;
   double *entries = aggw + nch * (int64_t)D;
+  double *gM = entries + nch * (int64_t)D;  // group level: ng x (D*D + 2D)
   cudaError_t e;
   switch (dense_dp(D)) {
     case 16: e = launch_reduce<ST, 16>(a, c, nch, aggM, aggw, st); break;
@@ -305,13 +333,13 @@ cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
   }
   if (e != cudaSuccess) return e;
   switch (dense_dp(D)) {
-    case 16: launch_tail<ST, 16>(a, c, nch, aggM, aggw, entries, st); break;
-    case 32: launch_tail<ST, 32>(a, c, nch, aggM, aggw, entries, st); break;
-    case 64: launch_tail<ST, 64>(a, c, nch, aggM, aggw, entries, st); break;
-    case 112: launch_tail<ST, 112>(a, c, nch, aggM, aggw, entries, st); break;
-    default: launch_tail<ST, 128>(a, c, nch, aggM, aggw, entries, st); break;
+    case 16: e = launch_tail<ST, 16>(a, c, nch, aggM, aggw, entries, gM, st); break;
+    case 32: e = launch_tail<ST, 32>(a, c, nch, aggM, aggw, entries, gM, st); break;
+    case 64: e = launch_tail<ST, 64>(a, c, nch, aggM, aggw, entries, gM, st); break;
+    case 112: e = launch_tail<ST, 112>(a, c, nch, aggM, aggw, entries, gM, st); break;
+    default: e = launch_tail<ST, 128>(a, c, nch, aggM, aggw, entries, gM, st); break;
   }
-  return cudaGetLastError();
+  return e;
 }
 
 template cudaError_t launch_dense_wide_t<float>(ScanArgs<float>, void *, cudaStream_t);
