@@ -143,6 +143,8 @@ int cs_scan_diag(int dtype, const void *j, const void *u, const void *s0, void *
 int cs_scan_block(int dtype, const void *a, const void *b, const void *c, const void *d,
                   const void *u, const void *s0, void *out, int64_t T, int32_t D,
                   void *ws, size_t ws_bytes, void *stream);
+/* dense: D <= 8 single-pass register kernel; 8 < D <= 128 chunked reduce /
+ * two-level f64 carry / replay (pscan.py:196-213, _scan_kernels.py:47-99). */
 int cs_scan_dense(int dtype, const void *J, const void *u, const void *s0, void *out,
                   int64_t T, int32_t D, void *ws, size_t ws_bytes, void *stream);
 
@@ -231,9 +233,13 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
                        const void *s0, const void *guess, void *e0, void *e1, void *e2, void *e3,
                        void *u, cs_elem_stats *d_stats, void *stream);
 /* 1 when cs_system_elements can build elements for (sys, mode, dtype): the
- * register builders (narrow built-in systems) or, for a leapfrog system on a
+ * register builders (narrow built-in systems); for a leapfrog system on a
  * dense Gaussian target in block2x2 mode at any dimension, the GEMM-backed
- * builder (samplers.py:165-222; one cuBLAS DGEMM per iteration). */
+ * builder (samplers.py:165-222; one cuBLAS DGEMM per iteration); for MALA on
+ * the logistic-regression target (D <= 128) in diag mode the four-GEMM
+ * Hutchinson builder, and in dense mode the closed-form Jacobian builder
+ * (samplers.py:129-145 collapsed: A = I + eps H(S), per-step Hessian on the
+ * tensor cores for f32 storage). */
 int cs_system_elements_supported(const cs_system *sys, int32_t mode, int dtype);
 /* Scans with the post-update bookkeeping fused into the replay (deer.py:273-277):
  * rows of `out` that moved more than atol + rtol|out| from `guess` get
