@@ -122,6 +122,11 @@ int cs_version(void);
 /* Development timing hook: the persistent solver stamps %globaltimer (ns) at
  * 8 phase boundaries of each of its first n/8 iterations into dev_buf (NULL off). */
 int cs_debug_probe(unsigned long long *dev_buf, int n);
+/* Test hook for the tcgen05 weighted Gram kernel: H_out[t] (128 x 128 f32,
+ * zero padded) = X^T diag(W[t]) X for X (N x D, D <= 128) and W (T x N), f64
+ * device inputs.  The Hessian term of the dense logistic-regression builder. */
+int cs_debug_gram(const double *X, int32_t N, int32_t D, const double *W, int64_t T, float *H_out,
+                  void *stream);
 int cs_device_sm_count(int *out);
 
 /* ---- counter-based noise (noise.py:50-80, 140-156, 159-171) ------------- */

@@ -19,6 +19,7 @@
 #include <mutex>
 
 #include "cs_apikern.cuh"
+#include "cs_umma.cuh"
 
 namespace cs {
 
@@ -297,31 +298,51 @@ __global__ void k_bd_xf(const double *X, int N, int D, float *Xf) {
 
 constexpr int kTcKB = 32, kTcLD = 136;  // n rows per staged block; padded row stride (conflict-free fragments)
 
-template <typename ST, int DP, bool TC>
+// TCM: 0 = FP32/FP64 pipes, 1 = mma.sync TF32, 2 = tcgen05 (UMMA, TMEM accumulator)
+template <typename ST, int DP, int TCM>
 __global__ void __launch_bounds__(kBdThr)
 k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, const double *A2, const double *GX,
            const double *gS, const double *R, const double *HR, const double *WS, const double *rsS,
-           const double *rsX, const float *Xf, ST *Jout, ST *uout, cs_elem_stats *stats) {
+           const double *rsX, const float *Xf, int ldx, ST *Jout, ST *uout, cs_elem_stats *stats) {
   using CT = ST;
+  constexpr bool TC = TCM == 1;
   constexpr int NA = DP / 16, SL = 16, PER = SL * DP / kBdThr;
-  constexpr int XS = TC ? 2 * kTcKB * kTcLD + 2 * kTcKB : 2 * SL * DP;  // staging elements
+  constexpr int XS = TCM == 1 ? 2 * kTcKB * kTcLD + 2 * kTcKB : 2 * SL * DP;  // staging elements
   const int D = sys.dim, N = (int)sys.target.n_data;
   const double prec = sys.target.prior_precision, eps = sys.eps;
   const double *X = sys.target.X;
   const ST *xi = (const ST *)sys.noise_vec;
   extern __shared__ __align__(16) unsigned char bsm[];
-  CT *Hs = (CT *)bsm;                      // DP x DP
-  CT *Xs = Hs + DP * DP;                   // SIMT: 2 x SL x DP; TC: 2 x kTcKB x kTcLD + 2 x kTcKB weights
-  double *vS = (double *)(Xs + XS + ((XS & 1) ? 1 : 0));
+  // TCM 2: the UMMA operand stages (64 KB, 1024-aligned) alias the Hessian tile
+  CT *Hs = TCM == 2 ? (CT *)(((uintptr_t)bsm + 1023) & ~(uintptr_t)1023) : (CT *)bsm;  // DP x DP
+  CT *Xs = Hs + DP * DP;  // SIMT: 2 x SL x DP; mma.sync: 2 x kTcKB x kTcLD + 2 x kTcKB weights; tcgen05: ldx weights
+  double *vS = TCM == 2 ? (double *)(((uintptr_t)(Xs + ldx) + 15) & ~(uintptr_t)15)
+                        : (double *)(Xs + XS + ((XS & 1) ? 1 : 0));
   double *vX = vS + DP, *vG = vX + DP, *vR = vG + DP, *vW = vR + DP, *vH = vW + DP;
   __shared__ double red[4][kBdThr / 32];
   __shared__ int flags[3];
+  __shared__ __align__(8) uint64_t s_ubar[2 * kUmmaStages + 1];
+  __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4, lane = tid & 31, wid = tid >> 5;
   const bool do_clip = isfinite(cfg.clip);
+  UmmaPipe pipe;
+  if constexpr (TCM == 2) {
+    static_assert(TCM != 2 || (DP == 128 && sizeof(ST) == 4), "tcgen05 Hessian: f32, 128 padded columns");
+    pipe.full = s_ubar;
+    pipe.empty = s_ubar + kUmmaStages;
+    pipe.done = s_ubar + 2 * kUmmaStages;
+    umma_pipe_init(pipe);
+    pipe.tmem = tmem_alloc128(&s_tmem);  // its barrier also publishes the mbarrier inits
+  }
   for (int64_t r = blockIdx.x; r < sys.T; r += gridDim.x) {
     const int64_t t = r + 1;
     const double *w = WS + r * N;
-    if constexpr (TC) {
+    if constexpr (TCM == 2) {
+      float *wbuf = (float *)Xs;
+      for (int n = tid; n < ldx; n += kBdThr) wbuf[n] = n < N ? (float)__ldg(w + n) : 0.0f;
+      __syncthreads();
+      gram_tcgen05(pipe, Xf, ldx, N, wbuf, (float *)Hs, (float *)Hs);
+    } else if constexpr (TC) {
       // H_raw on the tensor cores (mma.sync m16n8k8 TF32, f32 accumulate):
       // warp wid owns output rows 16 wid .. 16 wid + 15, all 16 column blocks
       // of 8; A[d][n] = w_n X[n][d], B[n][e] = X[n][e], K = the N data rows
@@ -535,9 +556,42 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     }
     __syncthreads();
   }
+  if constexpr (TCM == 2) tmem_free128(pipe.tmem);
+}
+
+// X^T as f32 [128][ldx] (rows >= D and columns >= N zero): the UMMA operand source
+__global__ void k_bd_xt(const double *X, int N, int D, int ldx, float *XT) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 128 * ldx; i += gridDim.x * blockDim.x) {
+    const int d = i / ldx, n = i - d * ldx;
+    XT[i] = (d < D && n < N) ? (float)X[(int64_t)n * D + d] : 0.0f;
+  }
 }
 
 }  // namespace
+
+// test hook: H_t = X^T diag(W_t) X through the tcgen05 path, one CTA per t
+__global__ void __launch_bounds__(kBdThr) k_gram_debug(const float *XT, int ldx, int N, const double *W, int64_t T,
+                                                       float *Hout) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  float *tiles = (float *)(((uintptr_t)gsm + 1023) & ~(uintptr_t)1023);
+  float *wbuf = tiles + 2 * kUmmaStages * kUmmaTile;
+  __shared__ __align__(8) uint64_t bars[2 * kUmmaStages + 1];
+  __shared__ uint32_t s_tmem;
+  UmmaPipe pipe;
+  pipe.full = bars;
+  pipe.empty = bars + kUmmaStages;
+  pipe.done = bars + 2 * kUmmaStages;
+  umma_pipe_init(pipe);
+  pipe.tmem = tmem_alloc128(&s_tmem);
+  for (int64_t r = blockIdx.x; r < T; r += gridDim.x) {
+    for (int n = threadIdx.x; n < ldx; n += blockDim.x) wbuf[n] = n < N ? (float)W[r * N + n] : 0.0f;
+    __syncthreads();
+    gram_tcgen05(pipe, XT, ldx, N, wbuf, tiles, tiles);
+    for (int i = threadIdx.x; i < 128 * 128; i += blockDim.x) Hout[r * 128 * 128 + i] = tiles[i];
+    __syncthreads();
+  }
+  tmem_free128(pipe.tmem);
+}
 
 bool blr_mala_ok(const cs_system &s, int mode) {
   return s.kind == CS_SYS_MALA && s.target.kind == CS_TARGET_BLR && (mode == CS_MODE_DIAG || mode == CS_MODE_DENSE) &&
@@ -593,26 +647,28 @@ static cudaError_t blr_run(const cs_system &sys, const cs_deer_config &cfg, int6
   return cudaGetLastError();
 }
 
-static bool bd_tensor_cores() {  // CS_BLR_DENSE_TC=0 keeps the f32 Hessian on the FP32 pipes
-  static const bool v = [] {
+static int bd_tensor_cores() {  // f32 Hessian: 2 tcgen05 (default), 1 mma.sync, 0 FP32 pipes (CS_BLR_DENSE_TC)
+  static const int v = [] {
     const char *e = getenv("CS_BLR_DENSE_TC");
-    return e ? atoi(e) != 0 : true;
+    return e ? atoi(e) : 2;
   }();
   return v;
 }
 
-template <typename ST, int DP, bool TC = false>
+template <typename ST, int DP, int TCM = 0>
 static cudaError_t bd_final_launch(const cs_system &sys, const cs_deer_config &cfg, const ST *s0, const ST *guess,
                                    const double *A2, const double *GX, const double *gS, const double *R,
                                    const double *HR, const double *WS, const double *rsS, const double *rsX,
-                                   const float *Xf, ST *J, ST *u, cs_elem_stats *stats, cudaStream_t st) {
-  const size_t xs = TC ? 2 * kTcKB * kTcLD + 2 * kTcKB : 2 * 16 * DP;
-  const size_t smem = sizeof(ST) * ((size_t)DP * DP + xs) + 8 + 6 * DP * sizeof(double);
-  auto k = k_bd_final<ST, DP, TC>;
+                                   const float *Xf, ST *J, ST *u, cs_elem_stats *stats, cudaStream_t st,
+                                   int ldx = 0) {
+  const size_t xs = TCM == 1 ? 2 * kTcKB * kTcLD + 2 * kTcKB : TCM == 2 ? (size_t)ldx + 4 : 2 * 16 * DP;
+  const size_t smem = sizeof(ST) * ((size_t)DP * DP + xs) + 8 + 6 * DP * sizeof(double) + (TCM == 2 ? 1024 : 0);
+  auto k = k_bd_final<ST, DP, TCM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t grid = sys.T < 148 * 16 ? sys.T : 148 * 16;
-  k<<<(unsigned)grid, kBdThr, smem, st>>>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, u, stats);
+  k<<<(unsigned)grid, kBdThr, smem, st>>>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, ldx, J, u,
+                                          stats);
   return cudaGetLastError();
 }
 
@@ -627,7 +683,8 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   std::lock_guard<std::mutex> lock(ctx.mu);
   if (!ctx.h && cublasCreate(&ctx.h) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   // A, A2, G, gS, GX, R, HR (T x D); E, WS, WX (T x N); row sums 2 x (2T)
-  const size_t need = (size_t)7 * T * D + (size_t)3 * T * N + (size_t)4 * T + (size_t)64 * N;  // + Xf (N x 128 f32)
+  // + Xf: X as f32 (N x 128, or its transpose 128 x ldx for tcgen05)
+  const size_t need = (size_t)7 * T * D + (size_t)3 * T * N + (size_t)4 * T + (size_t)64 * (N + 32);
   if (ctx.cap < need) {
     if (ctx.buf) cudaFree(ctx.buf);
     ctx.buf = nullptr;
@@ -665,10 +722,16 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   k_bd_scale<<<148 * 32, 256, 0, st>>>(E, WX, T * N);
   if (gemm_x(E, HR) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   if constexpr (sizeof(ST) == 4) {
-    if (bd_tensor_cores()) {  // f32 storage: H(S) on the tensor cores (TF32 in, f32 accumulate)
+    if (bd_tensor_cores() == 2) {  // f32 storage: H(S) on the 5th-gen tensor cores (tcgen05, TMEM accumulator)
+      const int ldx = (N + 31) / 32 * 32;
+      k_bd_xt<<<(128 * ldx + 255) / 256, 256, 0, st>>>(X, N, D, ldx, Xf);
+      return bd_final_launch<ST, 128, 2>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout,
+                                         stats, st, ldx);
+    }
+    if (bd_tensor_cores() == 1) {  // mma.sync TF32
       k_bd_xf<<<(N * 128 + 255) / 256, 256, 0, st>>>(X, N, D, Xf);
-      return bd_final_launch<ST, 128, true>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout,
-                                            stats, st);
+      return bd_final_launch<ST, 128, 1>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout,
+                                         stats, st);
     }
   }
   const int dp = D <= 16 ? 16 : D <= 32 ? 32 : D <= 64 ? 64 : D <= 112 ? 112 : 128;
@@ -679,6 +742,20 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
     case 112: return bd_final_launch<ST, 112>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout, stats, st);
     default: return bd_final_launch<ST, 128>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Xf, J, uout, stats, st);
   }
+}
+
+cudaError_t debug_gram(const double *X, int N, int D, const double *W, int64_t T, float *H, cudaStream_t st) {
+  const int ldx = (N + 31) / 32 * 32;
+  float *XT = nullptr;
+  cudaError_t e = cudaMallocAsync(&XT, sizeof(float) * 128 * ldx, st);
+  if (e != cudaSuccess) return e;
+  k_bd_xt<<<(128 * ldx + 255) / 256, 256, 0, st>>>(X, N, D, ldx, XT);
+  const size_t smem = 1024 + sizeof(float) * (2 * kUmmaStages * kUmmaTile + ldx + 4);
+  cudaFuncSetAttribute(k_gram_debug, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_gram_debug<<<(unsigned)(T < 148 ? T : 148), kBdThr, smem, st>>>(XT, ldx, N, W, T, H);
+  e = cudaGetLastError();
+  cudaFreeAsync(XT, st);
+  return e;
 }
 
 cudaError_t elements_blr(const cs_system &sys, const cs_deer_config &cfg, int dtype, int64_t iteration,
