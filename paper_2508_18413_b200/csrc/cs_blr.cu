@@ -313,13 +313,16 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
   const double *X = sys.target.X;
   const ST *xi = (const ST *)sys.noise_vec;
   extern __shared__ __align__(16) unsigned char bsm[];
-  // TCM 2: the UMMA operand stages (64 KB, 1024-aligned) alias the Hessian tile
+  // TCM 2: the UMMA operand stages (1024-aligned) alias the Hessian tile
   CT *Hs = TCM == 2 ? (CT *)(((uintptr_t)bsm + 1023) & ~(uintptr_t)1023) : (CT *)bsm;  // DP x DP
-  CT *Xs = Hs + DP * DP;  // SIMT: 2 x SL x DP; mma.sync: 2 x kTcKB x kTcLD + 2 x kTcKB weights; tcgen05: ldx weights
+  constexpr int HLD = DP + 1;  // Hessian tile row stride: row and column walks are both bank-conflict free
+  constexpr int HS = TCM == 2 && 2 * kUmmaStages * kUmmaTile > DP * HLD ? 2 * kUmmaStages * kUmmaTile : DP * HLD;
+  CT *Xs = Hs + HS;  // SIMT: 2 x SL x DP; mma.sync: 2 x kTcKB x kTcLD + 2 x kTcKB weights; tcgen05: ldx weights
   double *vS = TCM == 2 ? (double *)(((uintptr_t)(Xs + ldx) + 15) & ~(uintptr_t)15)
                         : (double *)(Xs + XS + ((XS & 1) ? 1 : 0));
-  double *vX = vS + DP, *vG = vX + DP, *vR = vG + DP, *vW = vR + DP, *vH = vW + DP;
+  double *vX = vS + DP, *vG = vX + DP, *vR = vG + DP, *vW = vR + DP, *vH = vW + DP, *vP = vH + DP;
   __shared__ double red[4][kBdThr / 32];
+  __shared__ double mpart[4][2][128];
   __shared__ int flags[3];
   __shared__ __align__(8) uint64_t s_ubar[2 * kUmmaStages + 1];
   __shared__ uint32_t s_tmem;
@@ -341,7 +344,7 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
       float *wbuf = (float *)Xs;
       for (int n = tid; n < ldx; n += kBdThr) wbuf[n] = n < N ? (float)__ldg(w + n) : 0.0f;
       __syncthreads();
-      gram_tcgen05(pipe, Xf, ldx, N, wbuf, (float *)Hs, (float *)Hs);
+      gram_tcgen05<kBdThr>(pipe, Xf, ldx, N, wbuf, (float *)Hs, (float *)Hs, HLD);
     } else if constexpr (TC) {
       // H_raw on the tensor cores (mma.sync m16n8k8 TF32, f32 accumulate):
       // warp wid owns output rows 16 wid .. 16 wid + 15, all 16 column blocks
@@ -401,8 +404,8 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
         for (int e = 0; e < 4; ++e) {  // upper triangle, mirrored: Hs is exactly symmetric
           const int ri = row + (e >> 1) * 8, ci = col + (e & 1);
           if (ci >= ri) {
-            Hs[ri * DP + ci] = acc[cb][e];
-            Hs[ci * DP + ri] = acc[cb][e];
+            Hs[ri * HLD + ci] = acc[cb][e];
+            Hs[ci * HLD + ri] = acc[cb][e];
           }
         }
       }
@@ -458,8 +461,8 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
       for (int y = 0; y < NA; ++y) {  // upper triangle, mirrored: Hs is exactly symmetric
         const int ri = ty + 16 * x, ci = tx + 16 * y;
         if (ci >= ri) {
-          Hs[ri * DP + ci] = acc[x][y];
-          Hs[ci * DP + ri] = acc[x][y];
+          Hs[ri * HLD + ci] = acc[x][y];
+          Hs[ci * HLD + ri] = acc[x][y];
         }
       }
     }
@@ -474,6 +477,7 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
       vR[tid] = rr;
       hxr = -HR[r * D + tid] - prec * rr;  // H(x~) r
       vH[tid] = hxr;
+      vP[tid] = cfg.preconditioner ? S * __ldg(cfg.preconditioner + tid) : S;  // p . S
       ss = S * S;
       sx = xt * xt;
       sr = rr * rr;
@@ -505,20 +509,38 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     const double margin = fmin(0.0, delta) - __ldg(sys.noise_logu + t);
     const double gate = margin > 0.0 ? 1.0 : 0.0;
     const double cb = sigmoid_prime(margin) * (delta < 0.0 ? 1.0 : 0.0);
-    // w_i = A g~ - g(S) + (H(S) r + A H(x~) r)/2, H(S) v = -(H_raw v) - prec v
-    if (tid < D) {
-      double hg = 0.0, hr = 0.0, hh = 0.0;
-      for (int j = 0; j < D; ++j) {
-        const double h = (double)Hs[j * DP + tid];  // = H[tid][j] (symmetric), bank-conflict free
-        hg = fma(h, vG[j], hg);
-        hr = fma(h, vR[j], hr);
-        hh = fma(h, vH[j], hh);
+    // w_i = A g~ - g(S) + (H(S) r + A H(x~) r)/2, H(S) v = -(H_raw v) - prec v; also
+    // H(S) (p.S) for the closed-form u.  Two threads per row (column halves).
+    {
+      const int i = tid & 127, hf = tid >> 7;
+      if (i < D) {
+        const int jm = (D + 1) / 2, j0 = hf ? jm : 0, j1 = hf ? D : jm;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int j = j0; j < j1; ++j) {
+          const double h = (double)Hs[j * HLD + i];  // = H[i][j] (symmetric), bank-conflict free
+          a0 = fma(h, vG[j], a0);
+          a1 = fma(h, vR[j], a1);
+          a2 = fma(h, vH[j], a2);
+          a3 = fma(h, vP[j], a3);
+        }
+        mpart[0][hf][i] = a0;
+        mpart[1][hf][i] = a1;
+        mpart[2][hf][i] = a2;
+        mpart[3][hf][i] = a3;
       }
-      hg = -hg - prec * vG[tid];
-      hr = -hr - prec * vR[tid];
-      hh = -hh - prec * vH[tid];
-      vW[tid] = (vG[tid] + eps * hg) - gS[r * D + tid] + 0.5 * (hr + (hxr + eps * hh));
     }
+    __syncthreads();
+    double wps = 0.0;
+    if (tid < D) {
+      const double hg = -(mpart[0][0][tid] + mpart[0][1][tid]) - prec * vG[tid];
+      const double hr = -(mpart[1][0][tid] + mpart[1][1][tid]) - prec * vR[tid];
+      const double hh = -(mpart[2][0][tid] + mpart[2][1][tid]) - prec * vH[tid];
+      const double wv = (vG[tid] + eps * hg) - gS[r * D + tid] + 0.5 * (hr + (hxr + eps * hh));
+      vW[tid] = wv;
+      wps = wv * vP[tid];
+    }
+    wps = warp_sum(wps);
+    if (lane == 0) red[0][wid] = wps;
     __syncthreads();
     // element: J_ij = gate (d_ij + eps H_ij) + (1 - gate) d_ij + cb (x~_i - S_i) w_j, then the
     // preconditioner ratio p_j / p_i, damping and clip (deer.py:161-170)
@@ -535,7 +557,7 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     bool jok = true;
     for (int idx = tid; idx < D * D; idx += kBdThr) {
       const int i = idx / D, j = idx - i * D;
-      const double v = Jij(i, j, (double)Hs[i * DP + j]);
+      const double v = Jij(i, j, (double)Hs[i * HLD + j]);
       jok &= isfinite(v);
       Jr[idx] = (ST)v;
     }
@@ -543,7 +565,19 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     if (tid < D) {
       const double f = gate > 0.0 ? vX[tid] : vS[tid];
       double jp = 0.0;
-      for (int j = 0; j < D; ++j) jp = fma(Jij(tid, j, (double)Hs[j * DP + tid]), vS[j], jp);
+      if (do_clip) {  // clipped entries: the elementwise row sum
+        for (int j = 0; j < D; ++j) jp = fma(Jij(tid, j, (double)Hs[j * HLD + tid]), vS[j], jp);
+      } else {
+        // (J prev)_i = (damping / p_i) [gate (pS_i + eps (H pS)_i) + (1 - gate) pS_i + cb dx_i (w . pS)]
+        double wp = 0.0;
+#pragma unroll
+        for (int k = 0; k < kBdThr / 32; ++k) wp += red[0][k];
+        const double ps = vP[tid];
+        const double hp = -(mpart[3][0][tid] + mpart[3][1][tid]) - prec * ps;
+        const double pi = cfg.preconditioner ? __ldg(cfg.preconditioner + tid) : 1.0;
+        jp = (cfg.damping / pi) *
+             (gate * (ps + eps * hp) + (1.0 - gate) * ps + cb * (vX[tid] - vS[tid]) * wp);
+      }
       uout[r * D + tid] = (ST)(f - jp);
       if (!isfinite(f)) flags[0] = 1;
       if (!(fabs(f - (double)guess[r * D + tid]) <= cfg.atol + cfg.rtol * fabs(f))) flags[2] = 1;
@@ -574,7 +608,8 @@ __global__ void __launch_bounds__(kBdThr) k_gram_debug(const float *XT, int ldx,
                                                        float *Hout) {
   extern __shared__ __align__(16) unsigned char gsm[];
   float *tiles = (float *)(((uintptr_t)gsm + 1023) & ~(uintptr_t)1023);
-  float *wbuf = tiles + 2 * kUmmaStages * kUmmaTile;
+  constexpr int kHs = 2 * kUmmaStages * kUmmaTile > 128 * 129 ? 2 * kUmmaStages * kUmmaTile : 128 * 129;
+  float *wbuf = tiles + kHs;  // after the operand stages / the (aliased) Hessian tile
   __shared__ __align__(8) uint64_t bars[2 * kUmmaStages + 1];
   __shared__ uint32_t s_tmem;
   UmmaPipe pipe;
@@ -586,8 +621,8 @@ __global__ void __launch_bounds__(kBdThr) k_gram_debug(const float *XT, int ldx,
   for (int64_t r = blockIdx.x; r < T; r += gridDim.x) {
     for (int n = threadIdx.x; n < ldx; n += blockDim.x) wbuf[n] = n < N ? (float)W[r * N + n] : 0.0f;
     __syncthreads();
-    gram_tcgen05(pipe, XT, ldx, N, wbuf, tiles, tiles);
-    for (int i = threadIdx.x; i < 128 * 128; i += blockDim.x) Hout[r * 128 * 128 + i] = tiles[i];
+    gram_tcgen05<kBdThr>(pipe, XT, ldx, N, wbuf, tiles, tiles, 129);
+    for (int i = threadIdx.x; i < 128 * 128; i += blockDim.x) Hout[r * 128 * 128 + i] = tiles[(i >> 7) * 129 + (i & 127)];
     __syncthreads();
   }
   tmem_free128(pipe.tmem);
@@ -662,7 +697,8 @@ static cudaError_t bd_final_launch(const cs_system &sys, const cs_deer_config &c
                                    const float *Xf, ST *J, ST *u, cs_elem_stats *stats, cudaStream_t st,
                                    int ldx = 0) {
   const size_t xs = TCM == 1 ? 2 * kTcKB * kTcLD + 2 * kTcKB : TCM == 2 ? (size_t)ldx + 4 : 2 * 16 * DP;
-  const size_t smem = sizeof(ST) * ((size_t)DP * DP + xs) + 8 + 6 * DP * sizeof(double) + (TCM == 2 ? 1024 : 0);
+  const size_t hs = TCM == 2 && 2 * kUmmaStages * kUmmaTile > DP * (DP + 1) ? 2 * kUmmaStages * kUmmaTile : DP * (DP + 1);
+  const size_t smem = sizeof(ST) * (hs + xs) + 8 + 7 * DP * sizeof(double) + (TCM == 2 ? 1024 : 0);
   auto k = k_bd_final<ST, DP, TCM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -750,7 +786,8 @@ cudaError_t debug_gram(const double *X, int N, int D, const double *W, int64_t T
   cudaError_t e = cudaMallocAsync(&XT, sizeof(float) * 128 * ldx, st);
   if (e != cudaSuccess) return e;
   k_bd_xt<<<(128 * ldx + 255) / 256, 256, 0, st>>>(X, N, D, ldx, XT);
-  const size_t smem = 1024 + sizeof(float) * (2 * kUmmaStages * kUmmaTile + ldx + 4);
+  const size_t hs = 2 * kUmmaStages * kUmmaTile > 128 * 129 ? 2 * kUmmaStages * kUmmaTile : 128 * 129;
+  const size_t smem = 1024 + sizeof(float) * (hs + ldx + 4);
   cudaFuncSetAttribute(k_gram_debug, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_gram_debug<<<(unsigned)(T < 148 ? T : 148), kBdThr, smem, st>>>(XT, ldx, N, W, T, H);
   e = cudaGetLastError();

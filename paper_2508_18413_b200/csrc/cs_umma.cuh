@@ -78,7 +78,7 @@ CS_D void tmem_free128(uint32_t base) {
 
 // Pipeline state carried across the steps a persistent CTA processes.
 struct UmmaPipe {
-  uint64_t *full;   // [kUmmaStages] count = blockDim.x (every thread staged its share)
+  uint64_t *full;   // [kUmmaStages] count = staging threads (every one stored its share)
   uint64_t *empty;  // [kUmmaStages] count 1 (tcgen05.commit)
   uint64_t *done;   // [1] count 1: the accumulator of this step is complete
   uint32_t tmem;
@@ -89,7 +89,7 @@ struct UmmaPipe {
 CS_D void umma_pipe_init(UmmaPipe &p) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kUmmaStages; ++s) {
-      mbar_init(&p.full[s], blockDim.x);
+      mbar_init(&p.full[s], blockDim.x - 32);  // the staging threads (warps 1..)
       mbar_init(&p.empty[s], 1);
     }
     mbar_init(p.done, 1);
@@ -99,42 +99,76 @@ CS_D void umma_pipe_init(UmmaPipe &p) {
   p.steps = 0;
 }
 
-// Hs[i][j] (row stride 128, f32) = sum_n w[n] X[n][i] X[n][j] for i, j < 128,
+// Hs[i][j] (row stride ldh, f32) = sum_n w[n] X[n][i] X[n][j] for i, j < 128,
 // exactly symmetric (upper triangle mirrored).  XT: f32 [128][ldx] (rows >= D
 // and columns >= N zero), w: N weights in shared memory, tiles: 1024-aligned
 // smem of kUmmaStages * 2 * kUmmaTile floats (may alias Hs: the epilogue
 // starts after every MMA has completed).  Called by all threads of the CTA.
+template <int NTHR>
 CS_D void gram_tcgen05(UmmaPipe &p, const float *__restrict__ XT, int ldx, int N, const float *w, float *tiles,
-                       float *Hs) {
-  const int tid = threadIdx.x, nthr = blockDim.x;
+                       float *Hs, int ldh) {
+  // warp 0 only issues (lane 0: wait for a staged block, 4 MMAs, commit);
+  // warps 1.. stage, running up to kUmmaStages blocks ahead of the MMAs
+  constexpr int NS = NTHR - 32;                       // staging threads
+  constexpr int PER = (128 * 8 + NS - 1) / NS;        // 16-byte chunks per staging thread per operand
+  const int tid = threadIdx.x;
   const int nkb = (N + kUmmaKB - 1) / kUmmaKB;
-  for (int kb = 0; kb < nkb; ++kb, ++p.kb) {
-    const int s = (int)(p.kb % kUmmaStages);
-    const uint32_t use = p.kb / kUmmaStages;
-    if (use > 0) mbar_wait(&p.empty[s], (use - 1) & 1);  // the MMAs that read this stage are done
-    float *A = tiles + s * 2 * kUmmaTile, *B = A + kUmmaTile;
-    // 128 rows x 8 chunks of 16 B per operand; chunk c of row r lands at c ^ (r & 7)
-    for (int q = tid; q < 128 * 8; q += nthr) {
-      const int r = q >> 3, c = q & 7, n0 = kb * kUmmaKB + 4 * c;
-      const float4 x = *(const float4 *)(XT + (int64_t)r * ldx + n0);
-      const float4 ww = *(const float4 *)(w + n0);
-      const int off = r * 32 + ((c ^ (r & 7)) << 2);
-      *(float4 *)(B + off) = x;
-      *(float4 *)(A + off) = make_float4(x.x * ww.x, x.y * ww.y, x.z * ww.z, x.w * ww.w);
-    }
-    fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p.full[s])) : "memory");
+  if (tid < 32) {
     if (tid == 0) {
-      mbar_wait(&p.full[s], use & 1);
-      tc_fence_after();
-      const uint64_t da = umma_desc_sw128(A), db = umma_desc_sw128(B);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const uint32_t g = p.kb + kb;
+        const int s = (int)(g % kUmmaStages);
+        mbar_wait(&p.full[s], (g / kUmmaStages) & 1);
+        tc_fence_after();
+        float *A = tiles + s * 2 * kUmmaTile, *B = A + kUmmaTile;
+        const uint64_t da = umma_desc_sw128(A), db = umma_desc_sw128(B);
 #pragma unroll
-      for (int k = 0; k < kUmmaKB / 8; ++k)  // K = 8 tf32 = 32 B per MMA: advance the start address by 2 (x16 B)
-        umma_tf32(p.tmem, da + 2 * k, db + 2 * k, kIdescTf32_128x128, (kb | k) != 0);
-      umma_commit(&p.empty[s]);
-      if (kb == nkb - 1) umma_commit(p.done);
+        for (int k = 0; k < kUmmaKB / 8; ++k)  // K = 8 tf32 = 32 B per MMA: advance the start address by 2 (x16 B)
+          umma_tf32(p.tmem, da + 2 * k, db + 2 * k, kIdescTf32_128x128, (kb | k) != 0);
+        umma_commit(&p.empty[s]);
+      }
+      umma_commit(p.done);
+    }
+    __syncwarp();
+  } else {
+    const int st = tid - 32;
+    // X^T chunks are loaded into registers two K-blocks ahead of their store
+    float4 xr[2][PER];
+    auto load = [&](int kb, float4 (&dst)[PER]) {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int q = st + i * NS, r = q >> 3, c = q & 7;
+        dst[i] = (kb < nkb && q < 128 * 8) ? __ldg((const float4 *)(XT + (int64_t)r * ldx + kb * kUmmaKB + 4 * c))
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    load(0, xr[0]);
+    load(1, xr[1]);
+#pragma unroll 2
+    for (int kb = 0; kb < nkb; ++kb) {
+      const uint32_t g = p.kb + kb;
+      const int s = (int)(g % kUmmaStages);
+      const uint32_t use = g / kUmmaStages;
+      if (use > 0) mbar_wait(&p.empty[s], (use - 1) & 1);  // the MMAs that read this stage are done
+      float *A = tiles + s * 2 * kUmmaTile, *B = A + kUmmaTile;
+      // 128 rows x 8 chunks of 16 B per operand; chunk c of row r lands at c ^ (r & 7)
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int q = st + i * NS, r = q >> 3, c = q & 7, n0 = kb * kUmmaKB + 4 * c;
+        if (q < 128 * 8) {
+          const float4 x = xr[kb & 1][i];
+          const float4 ww = *(const float4 *)(w + n0);
+          const int off = r * 32 + ((c ^ (r & 7)) << 2);
+          *(float4 *)(B + off) = x;
+          *(float4 *)(A + off) = make_float4(x.x * ww.x, x.y * ww.y, x.z * ww.z, x.w * ww.w);
+        }
+      }
+      if (kb + 2 < nkb) load(kb + 2, xr[kb & 1]);
+      fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core (async proxy)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p.full[s])) : "memory");
     }
   }
+  p.kb += nkb;
   // epilogue: TMEM -> registers -> Hs (warp w: lanes 32 (w % 4) .., column half w / 4)
   mbar_wait(p.done, p.steps & 1);
   ++p.steps;
@@ -150,8 +184,8 @@ CS_D void gram_tcgen05(UmmaPipe &p, const float *__restrict__ XT, int ldx, int N
       for (int i = 0; i < 16; ++i) {
         const int col = c0 + cc + i;
         if (col >= row) {
-          Hs[row * 128 + col] = v[i];
-          Hs[col * 128 + row] = v[i];
+          Hs[row * ldh + col] = v[i];
+          Hs[col * ldh + row] = v[i];
         }
       }
     }

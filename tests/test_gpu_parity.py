@@ -424,6 +424,27 @@ def test_run_deer_blr_dense_wide(cuda_device, dtype):
     _deer_cmp(h, g, "dense_", dtype)
 
 
+@pytest.mark.parametrize("kw", [dict(damping=0.7), dict(preconditioner="ramp"), dict(clip=0.5),
+                                dict(damping=0.8, preconditioner="ramp", clip=2.0)])
+def test_blr_dense_builder_options_match_host_engine(cuda_device, kw):
+    # the closed-form element (u from J prev in closed form when unclipped) against
+    # the host engine's jvp-built J + elementwise formation, with preconditioner /
+    # damping / clip (deer.py:161-170)
+    g0 = golden("mala_blr100")
+    kw = dict(kw)
+    if kw.get("preconditioner") == "ramp":
+        kw["preconditioner"] = np.linspace(0.5, 2.0, 100)
+    m = cs.model_logp_grad_hvp(cs.blr(g0["X"], g0["y"], 1.0))
+    k = cs.MalaKernel(m, 0.003, seed=4, T=150)
+    cfg = cs.DeerConfig(mode="dense", max_iters=60, **kw)
+    r = cs.run_deer(k, np.zeros(100), cfg)
+    h = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="dense", max_iters=60, engine="host", **kw))
+    assert r.stats["path"] == "streamed" and h.stats["path"] == "host"
+    assert r.iterations == h.iterations and r.converged == h.converged
+    np.testing.assert_allclose(np_(r.trace), np_(h.trace), atol=1e-9, rtol=1e-9)
+    np.testing.assert_array_equal(np_(r.per_step_converged_at), np_(h.per_step_converged_at))
+
+
 def test_run_deer_leapfrog_gauss200(cuda_device):
     g = golden("leapfrog_gauss200")
     m = cs.model_logp_grad_hvp(cs.gaussian(np.zeros(200), g["chol"]))
