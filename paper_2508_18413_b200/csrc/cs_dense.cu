@@ -17,6 +17,7 @@
 
 #include "cs_common.cuh"
 #include "cs_scan.cuh"
+#include "cs_umma.cuh"
 
 namespace cs {
 
@@ -274,6 +275,14 @@ size_t dense_wide_ws_bytes(int64_t T, int D) {
   return (size_t)(nch + ng) * ((size_t)D * D + 2 * D) * sizeof(double) + 256;
 }
 
+static bool dense_tc() {  // CS_DENSE_TC=0 keeps the f32 composition on the FP32 pipes
+  static const bool v = [] {
+    const char *e = getenv("CS_DENSE_TC");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 static int dense_dp(int D) { return D <= 16 ? 16 : D <= 32 ? 32 : D <= 64 ? 64 : D <= 112 ? 112 : 128; }
 
 template <typename ST, int DP>
@@ -285,6 +294,180 @@ static cudaError_t launch_reduce(const ScanArgs<ST> &a, int c, int64_t nch, doub
   if (e != cudaSuccess) return e;
   k<<<(unsigned)nch, kDwReduceThr, smem, st>>>(a.e0, a.u, a.T, a.D, c, aggM, aggw);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core composition (f32 storage, D < 128, D % 4 == 0): the chunk's
+// product chain M <- J_t M on the 5th-gen tensor cores.  The chain needs f32
+// accuracy (the carry applies M to the entry state), so every operand is
+// split x = hi + lo in TF32 and each product is hi.hi + hi.lo + lo.hi (3xTF32,
+// error ~2^-21 per product against f32's 2^-24).  The affine part rides along
+// as column D of the B operand, M_aug = [M | w]: J_t M_aug = [J_t M | J_t w],
+// and u_t is added to that column in the epilogue.  Per step: J_t streams in
+// four 32-column K-blocks (staging warps 1..7, two blocks ahead in registers),
+// warp 0 lane 0 issues 4 x 3 kind::tf32 MMAs per block into a 128 x 128 f32
+// TMEM accumulator, then all warps read it back (tcgen05.ld) and write the new
+// M_aug^T, split, as the next step's B operand (K-major, SWIZZLE_128B).
+constexpr int kDrtThr = 256;
+
+CS_D void tf32_split(float x, float &hi, float &lo) {
+  unsigned h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  unsigned l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
+  lo = __uint_as_float(l);
+}
+// float offset of element (row, k) in a K-major SW128 operand of 128 rows whose
+// K extent is split into 32-column atoms of 128 x 32 floats
+CS_D int sw128_off(int row, int k) {
+  return (k >> 5) * kUmmaTile + row * 32 + ((((k & 31) >> 2) ^ (row & 7)) << 2) + (k & 3);
+}
+
+__global__ void __launch_bounds__(kDrtThr, 1)
+k_dense_reduce_tc(const float *__restrict__ J, const float *__restrict__ u, int64_t T, int D, int c, double *aggM,
+                  double *aggw) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float *Bh = (float *)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);  // 4 atoms: M_aug^T hi
+  float *Bl = Bh + 4 * kUmmaTile;                                      // lo
+  float *As = Bl + 4 * kUmmaTile;                                      // 2 stages x (hi, lo) of J_t K-blocks
+  __shared__ __align__(8) uint64_t bars[2 * kUmmaStages + 1];
+  __shared__ uint32_t s_tmem;
+  UmmaPipe pipe;
+  pipe.full = bars;
+  pipe.empty = bars + kUmmaStages;
+  pipe.done = bars + 2 * kUmmaStages;
+  umma_pipe_init(pipe);  // full barriers count blockDim.x - 32: the staging warps
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t q = blockIdx.x, t0 = q * (int64_t)c;
+  const int64_t t1 = t0 + c < T ? t0 + c : T;
+  const int64_t DD = (int64_t)D * D;
+  // initial B = M_aug^T with M_aug = [J_t0 | u_t0]
+  {
+    const float *J0 = J + t0 * DD;
+    for (int idx = tid; idx < 128 * 128; idx += kDrtThr) {
+      const int k = idx >> 7, j = idx & 127;  // coalesced over j (row k of M_aug)
+      float v = 0.0f;
+      if (k < D) v = j < D ? J0[k * D + j] : (j == D ? u[t0 * D + k] : 0.0f);
+      float hi, lo;
+      tf32_split(v, hi, lo);
+      Bh[sw128_off(j, k)] = hi;
+      Bl[sw128_off(j, k)] = lo;
+    }
+  }
+  pipe.tmem = tmem_alloc128(&s_tmem);  // its barrier also publishes the B writes and barrier inits
+  if (t1 - t0 == 1) {
+    for (int idx = tid; idx < D * D; idx += kDrtThr) aggM[q * DD + idx] = (double)J[t0 * DD + idx];
+    for (int i = tid; i < D; i += kDrtThr) aggw[q * D + i] = (double)u[t0 * D + i];
+    tmem_free128(pipe.tmem);
+    return;
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  const int nblk = (int)(t1 - t0 - 1) * 4;  // K-blocks of the chunk's stream: step t0 + 1 + b / 4, columns 32 (b % 4)
+  constexpr int NS = kDrtThr - 32, PER = (128 * 8 + NS - 1) / NS;
+  const int st = tid - 32;
+  float4 xr[2][PER];
+  auto load = [&](int b, float4 (&dst)[PER]) {
+    const int64_t t = t0 + 1 + b / 4;
+    const float *Jt = J + t * DD;
+    const int kb = b & 3;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int qq = st + i * NS, r = qq >> 3, ch = qq & 7, k0 = 32 * kb + 4 * ch;
+      dst[i] = (b < nblk && qq < 1024 && r < D && k0 < D) ? __ldg((const float4 *)(Jt + r * D + k0))
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  if (wid > 0) {
+    load(0, xr[0]);
+    load(1, xr[1]);
+  }
+  int b = 0;
+  for (int64_t t = t0 + 1; t < t1; ++t) {
+    if (wid == 0) {
+      if (lane == 0) {
+        for (int kb = 0; kb < 4; ++kb) {
+          const uint32_t g = pipe.kb + kb;
+          const int s = (int)(g % kUmmaStages);
+          mbar_wait(&pipe.full[s], (g / kUmmaStages) & 1);
+          tc_fence_after();
+          const float *Ah = As + s * 2 * kUmmaTile, *Al = Ah + kUmmaTile;
+          const uint64_t dah = umma_desc_sw128(Ah), dal = umma_desc_sw128(Al);
+          const uint64_t dbh = umma_desc_sw128(Bh + kb * kUmmaTile), dbl = umma_desc_sw128(Bl + kb * kUmmaTile);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            umma_tf32(pipe.tmem, dah + 2 * k, dbh + 2 * k, kIdescTf32_128x128, (kb | k) != 0);
+            umma_tf32(pipe.tmem, dah + 2 * k, dbl + 2 * k, kIdescTf32_128x128, 1);
+            umma_tf32(pipe.tmem, dal + 2 * k, dbh + 2 * k, kIdescTf32_128x128, 1);
+          }
+          umma_commit(&pipe.empty[s]);
+        }
+        umma_commit(pipe.done);
+      }
+      __syncwarp();
+    } else {
+      for (int kb = 0; kb < 4; ++kb, ++b) {
+        const uint32_t g = pipe.kb + kb;
+        const int s = (int)(g % kUmmaStages);
+        const uint32_t use = g / kUmmaStages;
+        if (use > 0) mbar_wait(&pipe.empty[s], (use - 1) & 1);
+        float *Ah = As + s * 2 * kUmmaTile, *Al = Ah + kUmmaTile;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const int qq = st + i * NS, r = qq >> 3, ch = qq & 7;
+          if (qq < 1024) {
+            const float4 x = xr[b & 1][i];
+            float4 h, l;
+            tf32_split(x.x, h.x, l.x);
+            tf32_split(x.y, h.y, l.y);
+            tf32_split(x.z, h.z, l.z);
+            tf32_split(x.w, h.w, l.w);
+            const int off = r * 32 + ((ch ^ (r & 7)) << 2);
+            *(float4 *)(Ah + off) = h;
+            *(float4 *)(Al + off) = l;
+          }
+        }
+        if (b + 2 < nblk) load(b + 2, xr[b & 1]);
+        fence_proxy_async_smem();
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&pipe.full[s])) : "memory");
+      }
+    }
+    pipe.kb += 4;
+    // epilogue: the new M_aug = J_t M_aug (+ u_t in column D) back into B, or the aggregate
+    mbar_wait(pipe.done, pipe.steps & 1);
+    ++pipe.steps;
+    tc_fence_after();
+    const bool last = t + 1 == t1;
+    const int row = 32 * (wid & 3) + lane, c0 = 64 * (wid >> 2);
+    const float ut = row < D ? __ldg(u + t * D + row) : 0.0f;
+#pragma unroll
+    for (int cc = 0; cc < 64; cc += 16) {
+      float v[16];
+      tmem_ld16(pipe.tmem + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(c0 + cc), v);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int j = c0 + cc + e;
+        float val = v[e];
+        if (j == D) val += ut;
+        if (last) {
+          if (row < D) {
+            if (j < D) aggM[q * DD + (int64_t)row * D + j] = (double)val;
+            else if (j == D) aggw[q * D + row] = (double)val;
+          }
+        } else {
+          float hi, lo;
+          tf32_split(val, hi, lo);
+          Bh[sw128_off(j, row)] = hi;
+          Bl[sw128_off(j, row)] = lo;
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+  }
+  tmem_free128(pipe.tmem);
 }
 
 // Chunk entries: one serial walk over the chunk aggregates when they are few;
@@ -324,6 +507,14 @@ cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
   double *entries = aggw + nch * (int64_t)D;
   double *gM = entries + nch * (int64_t)D;  // group level: ng x (D*D + 2D)
   cudaError_t e;
+  if (sizeof(ST) == 4 && dense_tc() && D % 4 == 0 && D < 128) {
+    const size_t smem = 1024 + sizeof(float) * 12 * kUmmaTile;
+    e = cudaFuncSetAttribute(k_dense_reduce_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_dense_reduce_tc<<<(unsigned)nch, kDrtThr, smem, st>>>((const float *)a.e0, (const float *)a.u, T, D, c, aggM,
+                                                            aggw);
+    e = cudaGetLastError();
+  } else
   switch (dense_dp(D)) {
     case 16: e = launch_reduce<ST, 16>(a, c, nch, aggM, aggw, st); break;
     case 32: e = launch_reduce<ST, 32>(a, c, nch, aggM, aggw, st); break;
