@@ -112,6 +112,10 @@ def load():
     """Load the CUDA library; raise loudly if it is missing (no fallback)."""
     global _lib
     if _lib is None:
+        # tuning experiments only: a variant build of the same library
+        LIB_PATH_ = os.environ.get("CS_LIB_PATH", LIB_PATH)
+        if LIB_PATH_ != LIB_PATH:
+            return _load_path(LIB_PATH_)
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(
                 f"libchainscan_b200.so not found at {LIB_PATH}; build it with "
@@ -122,6 +126,17 @@ def load():
             fn.argtypes = args
             fn.restype = res
         _lib = lib
+    return _lib
+
+
+def _load_path(path):
+    global _lib
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
     return _lib
 
 

@@ -352,7 +352,7 @@ int cs_rademacher_fill(uint64_t seed, int64_t iteration, const int64_t *ts, int6
 size_t cs_scan_workspace_bytes(int mode, int dtype, int64_t T, int32_t D) {
   const int var = mode == CS_MODE_DIAG ? SCAN_DIAG : mode == CS_MODE_BLOCK ? SCAN_BLOCK : SCAN_DENSE;
   if (var == SCAN_DENSE && D > 8) return dense_wide_ws_bytes(T, D);
-  return scan_plan(var, dtype, T, D).ws_bytes;
+  return scan_ws_bytes(var, dtype, T, D);
 }
 
 static int do_scan(int var, int dtype, const void *e0, const void *e1, const void *e2, const void *e3,
@@ -665,7 +665,7 @@ static int do_scan_update(int var, int dtype, const void *e0, const void *e1, co
                           cs_elem_stats *stats, void *stream) {
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   if (T < 0 || D < 1 || D > 4096) return fail(CS_ERR_STRUCTURAL, "bad scan shape");
-  const ScanPlan p = scan_plan(var, dtype, T, D);
+  const ScanPlan p = scan_plan(var, dtype, T, D, true);
   if (ws_bytes < p.ws_bytes) return fail(CS_ERR_CONFIG, "scan workspace too small");
   if (T == 0) return CS_OK;
   cudaError_t e;

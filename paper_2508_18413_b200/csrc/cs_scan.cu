@@ -637,20 +637,28 @@ struct RowsGeom {
 
 // rows per thread segment per stage: the thread's loads for a stage are all
 // issued before its FMA chain starts (registers: NA * kSegRows values)
-#ifndef CS_ROWS_KR
-#define CS_ROWS_KR 16  // diag fp32 rows per thread segment per stage
-#endif
-#ifndef CS_ROWS_MINB
-#define CS_ROWS_MINB 3  // resident CTAs per SM the register budget is cut for
-#endif
+// Per-thread rows per stage and resident CTAs per SM, by scan kind (measured,
+// tools/build_scan_variants.sh, T = 4M, D = 18 fp32): the plain diag scan runs
+// best at 24 rows x 2 CTAs/SM (2.29 -> 2.50 TB/s against 16 x 3; 2.58 -> 2.83
+// at T = 16M), block2x2 at 6 rows x 3 CTAs/SM (1.90 -> 2.39 TB/s), and the
+// diag scan with the fused Newton bookkeeping (UPDATE: it also reads the
+// previous iterate) at 16 x 3 -- 24 x 2 made it 30% slower at cfg 5's T = 1M.
 #ifndef CS_ROWS_PREFETCH
 #define CS_ROWS_PREFETCH 0  // software-pipelined stage loads (needs 2x registers)
 #endif
-template <typename ST, int VAR>
-struct RowsSeg {
-  static constexpr int kRows = VAR == SCAN_DIAG ? (sizeof(ST) == 4 ? CS_ROWS_KR : CS_ROWS_KR / 2)
-                                                : (sizeof(ST) == 4 ? CS_ROWS_KR / 4 : CS_ROWS_KR / 8 > 0 ? CS_ROWS_KR / 8 : 1);
+template <int VAR, bool UPD>
+struct RowsTune {
+  static constexpr int kRows32 = VAR == SCAN_DIAG ? (UPD ? 16 : 24) : 6;  // fp32 rows per thread per stage
+  static constexpr int kMinBlocks = VAR == SCAN_DIAG && !UPD ? 2 : 3;
 };
+template <typename ST, int VAR, bool UPD = false>
+struct RowsSeg {
+  static constexpr int kRows = sizeof(ST) == 4 ? RowsTune<VAR, UPD>::kRows32
+                                               : (RowsTune<VAR, UPD>::kRows32 / 2 > 0 ? RowsTune<VAR, UPD>::kRows32 / 2 : 1);
+};
+#ifndef CS_ROWS_LBW_MINB
+#define CS_ROWS_LBW_MINB 2
+#endif
 
 template <typename T>
 CS_D T ld_hint(const T *p, uint64_t pol) {
@@ -666,10 +674,8 @@ CS_D T ld_hint(const T *p, uint64_t pol) {
 }
 
 template <typename ST, int VAR, bool AGG_ONLY = false, bool UPDATE = false, bool LBW = false>
-#ifndef CS_ROWS_LBW_MINB
-#define CS_ROWS_LBW_MINB 2
-#endif
-__global__ void __launch_bounds__(kScanThreads + (LBW ? 64 : 0), LBW ? CS_ROWS_LBW_MINB : CS_ROWS_MINB)
+__global__ void __launch_bounds__(kScanThreads + (LBW ? 64 : 0),
+                                  LBW ? CS_ROWS_LBW_MINB : RowsTune<VAR, UPDATE>::kMinBlocks)
 scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag, int NS) {
   (void)NS;
   // LBW: two helper warps take every global hand-off off the eight streaming
@@ -681,7 +687,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
   using MG = Grp<0, kScanThreads, LBW ? 1 : 0>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = ColElem<VAR>::W;
-  constexpr int KR = RowsSeg<ST, VAR>::kRows;
+  constexpr int KR = RowsSeg<ST, VAR, UPDATE>::kRows;
   using CT = ST;  // in-segment arithmetic type; everything crossing segments is f64
   const int ncol = a.D;
   const int SW = VAR == SCAN_DIAG ? ncol : 2 * ncol;
@@ -1509,13 +1515,13 @@ static int rows_chunk_stages() {  // tuning override for experiments
   static const int v = env_int("CS_SCAN_CHUNK_STAGES", 1, 256, 16);
   return v;
 }
-static int rows_resident_ctas() {  // persistent grid of scan_rows (launch bounds: CS_ROWS_MINB per SM)
-  static const int v = [] {
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return CS_ROWS_MINB * (sms > 0 ? sms : 148);
+static int rows_resident_ctas(int minb) {  // persistent grid of scan_rows (launch bounds: minb CTAs per SM)
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
   }();
-  return v;
+  return minb * sms;
 }
 static bool rows_lbw() {  // dedicated look-back warp (CS_SCAN_LBW=0 selects the in-line look-back)
   static const bool v = [] {
@@ -1546,7 +1552,12 @@ static int rows_per_tile(int var, int dtype, int D) {
   return R;
 }
 
-ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
+size_t scan_ws_bytes(int var, int dtype, int64_t T, int D) {
+  const size_t a = scan_plan(var, dtype, T, D, false).ws_bytes, b = scan_plan(var, dtype, T, D, true).ws_bytes;
+  return a > b ? a : b;
+}
+
+ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update) {
   ScanPlan p{};
   p.var = var;
   if (var == SCAN_DENSE) {
@@ -1560,14 +1571,21 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D) {
   } else if (D <= 64) {
     p.kind = 0;
     const int nseg = kScanThreads / D;
-    const int kr = dtype == CS_F64 ? (var == SCAN_DIAG ? RowsSeg<double, SCAN_DIAG>::kRows : RowsSeg<double, SCAN_BLOCK>::kRows)
-                                   : (var == SCAN_DIAG ? RowsSeg<float, SCAN_DIAG>::kRows : RowsSeg<float, SCAN_BLOCK>::kRows);
+    const bool u = update;
+    const int kr = dtype == CS_F64
+                       ? (var == SCAN_DIAG ? (u ? RowsSeg<double, SCAN_DIAG, true>::kRows : RowsSeg<double, SCAN_DIAG>::kRows)
+                                           : (u ? RowsSeg<double, SCAN_BLOCK, true>::kRows : RowsSeg<double, SCAN_BLOCK>::kRows))
+                       : (var == SCAN_DIAG ? (u ? RowsSeg<float, SCAN_DIAG, true>::kRows : RowsSeg<float, SCAN_DIAG>::kRows)
+                                           : (u ? RowsSeg<float, SCAN_BLOCK, true>::kRows : RowsSeg<float, SCAN_BLOCK>::kRows));
+    const int minb = rows_lbw() ? CS_ROWS_LBW_MINB
+                                : var == SCAN_DIAG ? (u ? RowsTune<SCAN_DIAG, true>::kMinBlocks : RowsTune<SCAN_DIAG, false>::kMinBlocks)
+                                                   : RowsTune<SCAN_BLOCK, false>::kMinBlocks;
     p.R = nseg * kr;                      // rows per stage
     // stages per chunk: large chunks amortise the per-chunk look-back, but
     // every resident CTA needs chunks -- aim for >= 2 rounds of the grid
     {
       const int64_t stages = (T + p.R - 1) / p.R;
-      const int64_t g = (int64_t)rows_resident_ctas();
+      const int64_t g = (int64_t)rows_resident_ctas(minb);
       int64_t cs = stages / (2 * g);
       const int cmax = rows_chunk_stages();
       if (cs > cmax) cs = cmax;

@@ -32,7 +32,9 @@ struct ScanPlan {
   size_t smem, ws_bytes;
 };
 
-ScanPlan scan_plan(int var, int dtype, int64_t T, int D);
+ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update = false);
+// workspace for either the plain or the bookkeeping (update) scan of a shape
+size_t scan_ws_bytes(int var, int dtype, int64_t T, int D);
 template <typename ST>
 cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update = false);
 // wide dense scans, 8 < D <= 128 (cs_dense.cu)
