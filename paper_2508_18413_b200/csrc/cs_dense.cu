@@ -384,7 +384,9 @@ k_dense_reduce_tc(const float *__restrict__ J, const float *__restrict__ u, int6
     load(1, xr[1]);
   }
   int b = 0;
+  const int erow = 32 * (wid & 3) + lane;  // this thread's accumulator row in the epilogue
   for (int64_t t = t0 + 1; t < t1; ++t) {
+    const float ut = erow < D ? __ldg(u + t * D + erow) : 0.0f;  // issued now, used after the MMAs
     if (wid == 0) {
       if (lane == 0) {
         for (int kb = 0; kb < 4; ++kb) {
@@ -439,8 +441,7 @@ k_dense_reduce_tc(const float *__restrict__ J, const float *__restrict__ u, int6
     ++pipe.steps;
     tc_fence_after();
     const bool last = t + 1 == t1;
-    const int row = 32 * (wid & 3) + lane, c0 = 64 * (wid >> 2);
-    const float ut = row < D ? __ldg(u + t * D + row) : 0.0f;
+    const int row = erow, c0 = 64 * (wid >> 2);
 #pragma unroll
     for (int cc = 0; cc < 64; cc += 16) {
       float v[16];
