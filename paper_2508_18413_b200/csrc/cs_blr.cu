@@ -322,7 +322,9 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
                         : (double *)(Xs + XS + ((XS & 1) ? 1 : 0));
   double *vX = vS + DP, *vG = vX + DP, *vR = vG + DP, *vW = vR + DP, *vH = vW + DP, *vP = vH + DP;
   __shared__ double red[4][kBdThr / 32];
-  __shared__ double mpart[4][2][128];
+  // matvec partials [4][2][128]: for TCM 2 in the stage region past the Hessian tile
+  __shared__ double mpart_s[TCM == 2 ? 1 : 4 * 2 * 128];
+  double(*mpart)[2][128] = (double(*)[2][128])(TCM == 2 ? (double *)(Hs + ((DP * HLD + 1) & ~1)) : mpart_s);
   __shared__ int flags[3];
   __shared__ __align__(8) uint64_t s_ubar[2 * kUmmaStages + 1];
   __shared__ uint32_t s_tmem;
@@ -555,11 +557,27 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     };
     ST *Jr = Jout + r * (int64_t)D * D;
     bool jok = true;
-    for (int idx = tid; idx < D * D; idx += kBdThr) {
-      const int i = idx / D, j = idx - i * D;
-      const double v = Jij(i, j, (double)Hs[i * HLD + j]);
-      jok &= isfinite(v);
-      Jr[idx] = (ST)v;
+    {
+      // warp per row, lanes across the row (coalesced stores, no index division);
+      // the entries are formed in the storage precision, the f64 parts hoisted
+      const CT g1 = (CT)gate, g0 = (CT)(1.0 - gate), ce = (CT)(gate * eps), lam = (CT)cfg.damping;
+      const CT cl = (CT)cfg.clip;
+      const CT pdiag = (CT)prec;
+      for (int i = wid; i < D; i += kBdThr / 32) {
+        const CT ci = (CT)(cb * (vX[i] - vS[i]));
+        const CT pinv = cfg.preconditioner ? (CT)(1.0 / __ldg(cfg.preconditioner + i)) : CT(1);
+        const CT *hrow = Hs + i * HLD;
+        ST *jrow = Jr + (int64_t)i * D;
+        for (int j = lane; j < D; j += 32) {
+          const CT hij = -hrow[j] - (i == j ? pdiag : CT(0));
+          CT v = ce * hij + ci * (CT)vW[j] + (i == j ? g1 + g0 : CT(0));
+          if (cfg.preconditioner) v = v * ((CT)__ldg(cfg.preconditioner + j) * pinv);
+          v = v * lam;
+          if (do_clip) v = v < -cl ? -cl : (v > cl ? cl : v);
+          jok &= isfinite((double)v);
+          jrow[j] = (ST)v;
+        }
+      }
     }
     if (!jok) flags[1] = 1;
     if (tid < D) {

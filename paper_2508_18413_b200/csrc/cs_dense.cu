@@ -509,7 +509,7 @@ cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
   double *gM = entries + nch * (int64_t)D;  // group level: ng x (D*D + 2D)
   cudaError_t e;
   if (sizeof(ST) == 4 && dense_tc() && D % 4 == 0 && D < 128) {
-    const size_t smem = 1024 + sizeof(float) * 12 * kUmmaTile;
+    const size_t smem = 1024 + sizeof(float) * (8 + 2 * kUmmaStages) * kUmmaTile;  // B hi/lo + A stages
     e = cudaFuncSetAttribute(k_dense_reduce_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_dense_reduce_tc<<<(unsigned)nch, kDrtThr, smem, st>>>((const float *)a.e0, (const float *)a.u, T, D, c, aggM,

@@ -16,7 +16,7 @@
 namespace cs {
 
 constexpr int kUmmaTile = 128 * 32;          // f32 elements of one operand tile (16 KB)
-constexpr int kUmmaStages = 2;
+constexpr int kUmmaStages = 3;
 constexpr int kUmmaKB = 32;                  // K (data rows) per stage
 
 // K-major, SWIZZLE_128B shared-memory matrix descriptor (sm100 layout:
