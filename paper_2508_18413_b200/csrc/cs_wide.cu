@@ -9,7 +9,7 @@
 //                    written as the GEMM's row-major A operand
 //   k_wide_epilogue  v'_t, the finite / Picard checks, d_hat, the block
 //                    (a, b, c, d) with preconditioner, damping and clip, and
-//                    u = f - M prev (deer.py:184-204) -- one warp per step
+//                    u = f - M prev (deer.py:184-204) -- one CTA per step
 // The result feeds cs_scan_block_update exactly like the register builders.
 #include <cublas_v2.h>
 
@@ -56,18 +56,15 @@ __global__ void k_wide_epilogue(cs_system sys, const ST *s0, const ST *guess, co
                                 ST *ea, ST *eb, ST *ec, ST *ed, ST *u, cs_elem_stats *stats) {
   const int n = sys.dim / 2;
   const int64_t T = sys.T;
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const bool do_clip = isfinite(clip);
   long long bf = kNoStep, bj = kNoStep;
   unsigned pf = 0;
-  for (int64_t r = w0; r < T; r += nw) {
+  for (int64_t r = blockIdx.x; r < T; r += gridDim.x) {  // one CTA per step: the n columns across its threads
     const int64_t t = r + 1;
     const ST *pr = r == 0 ? s0 : guess + (r - 1) * sys.dim;
     const ST *gr = guess + r * sys.dim;
     bool fin = true, jok = true, pfail = false;
-    for (int i = lane; i < n; i += 32) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const double x = (double)pr[i], v = (double)pr[n + i];
       const double ev = sys.eps * v;
       const double xn = x + (sys.mass ? ev / __ldg(sys.mass + i) : ev);  // as in the prologue
@@ -100,16 +97,16 @@ __global__ void k_wide_epilogue(cs_system sys, const ST *s0, const ST *guess, co
       u[r * sys.dim + i] = (ST)(xn - (a * x + b * v));
       u[r * sys.dim + n + i] = (ST)(vn - (c * x + d * v));
     }
-    fin = __all_sync(0xffffffffu, fin);
-    jok = __all_sync(0xffffffffu, jok);
-    pfail = __any_sync(0xffffffffu, pfail);
-    if (lane == 0) {
+    fin = __syncthreads_and(fin);
+    jok = __syncthreads_and(jok);
+    pfail = __syncthreads_or(pfail);
+    if (threadIdx.x == 0) {
       if (!fin && t < bf) bf = t;
       if (!jok && t < bj) bj = t;
       pf += pfail ? 1u : 0u;
     }
   }
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     if (bf != kNoStep) atomicMin((long long *)&stats->bad_step, bf);
     if (bj != kNoStep) atomicMin((long long *)&stats->bad_jacobian, bj);
     if (pf) atomicAdd(&stats->picard_fail, pf);
@@ -157,8 +154,7 @@ static cudaError_t wide_run(const cs_system &sys, const cs_deer_config &cfg, int
   if (cublasDgemm(ctx.h, CUBLAS_OP_N, CUBLAS_OP_N, n, (int)M, n, &one, sys.target.prec, n, A, n, &zero, C, n) !=
       CUBLAS_STATUS_SUCCESS)
     return cudaErrorUnknown;
-  const int64_t warps = T;
-  const unsigned g2 = (unsigned)((warps * 32 + 255) / 256);
+  const unsigned g2 = (unsigned)(T < 148 * 8 ? T : 148 * 8);
   k_wide_epilogue<ST><<<g2 < 1 ? 1 : g2, 256, 0, st>>>(sys, s0, guess, A, C, K, cfg.atol, cfg.rtol,
                                                         cfg.preconditioner, cfg.damping, cfg.clip, e0, e1, e2, e3, u,
                                                         stats);
