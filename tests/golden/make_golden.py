@@ -218,11 +218,29 @@ def blr_dense_fixture():
     save("mala_blr100_dense", **out)
 
 
+def trace_fixture():
+    # the reference's own trace artifact (tracefile.py): payload + sidecar + CSV
+    from chainscan.tracefile import export_csv, write_trace
+
+    rng = np.random.default_rng(17)
+    tr = rng.normal(size=(2, 5, 3))
+    tr[0, 0, 0], tr[1, 4, 2] = 1e-300, -np.inf
+    base = os.path.join(OUT, "trace_ref.bin")
+    write_trace(base, tr, "hmc", 123, {"eps": 0.5, "L": 8, "method": "quasi-deer"})
+    export_csv(os.path.join(OUT, "trace_ref.csv"), tr)
+    np.save(os.path.join(OUT, "trace_ref_array.npy"), tr)
+    print("wrote trace_ref")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["blr_dense"]:
         blr_dense_fixture()
+        sys.exit(0)
+    if sys.argv[1:] == ["trace"]:
+        trace_fixture()
         sys.exit(0)
     noise_fixtures()
     scan_fixtures()
     chain_fixtures()
     blr_dense_fixture()
+    trace_fixture()
