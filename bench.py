@@ -32,6 +32,16 @@ EPS, LSTEPS = 0.5, 8
 ROSEN = dict(a=0.0, b=0.1, scale1=1.0, scale2=1.0)
 
 
+def traffic(key):
+    """DRAM bytes per launch of a kernel at a bench workload, from its committed
+    ncu capture (profiles/r01_traffic.json); None when not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            return int(json.load(fh)[key]["bytes"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -183,7 +193,10 @@ def run_gpu(args):
     def solve():
         return cs.run_deer(kern, s0, cfg)
 
+    res = None
     for _ in range(args.warmup):
+        res = solve()
+    if res is None:  # --warmup 0: one untimed solve still fixes the iteration count
         res = solve()
     torch.cuda.synchronize()
     iters = res.iterations
@@ -234,7 +247,8 @@ def run_gpu(args):
     hbm, src = peaks()
     achieved = bytes_per_launch / per_launch_s / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": None, "kernel": "cs::deer_persistent<Hmc<2,f,Rosenbrock>,DIAG> (whole solve)",
+            "traffic": traffic(f"deer_persistent_hmc_rosen_T{T}") if dtype == torch.float32 else None,
+            "kernel": "cs::deer_persistent<Hmc<2,f,Rosenbrock>,DIAG> (whole solve)",
             "peak_source": src, "algorithmic_bytes_per_launch": bytes_per_launch}
 
     scan_roof = None
@@ -291,7 +305,8 @@ def scan_roofline(cs, dev, hbm, src):
     ms = float(np.median(times))
     byts = 12 * T * D
     ach = byts / (ms / 1e3) / 1e9
-    return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+    return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "traffic": traffic(f"scan_rows_diag_f32_T{T}_D{D}"),
             "kernel": "cs::scan_rows<float,DIAG>", "T": T, "D": D, "ms": ms, "peak_source": src,
             "algorithmic_bytes": byts}
 
