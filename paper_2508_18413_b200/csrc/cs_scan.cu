@@ -1238,6 +1238,110 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
 }
 
 // ---------------------------------------------------------------------------
+// wide rows, short sequences (D > 64, T <= 128; e.g. the leapfrog inside one HMC
+// proposal, L = 100, state 2 x 1000): one CTA per 32 columns holds the whole
+// sequence -- 16 warps x up to 8 rows in registers -- so there is no look-back
+// between row tiles at all: segment aggregates meet in shared memory, each
+// warp folds its predecessors' and replays.  Same arithmetic (f64) and the same
+// bookkeeping as scan_cols.
+constexpr int kSmallWarps = 16, kSmallRows = 8, kSmallT = kSmallWarps * kSmallRows;
+
+template <typename ST, int VAR, bool UPDATE>
+__global__ void __launch_bounds__(kSmallWarps * 32)
+scan_cols_small(ScanArgs<ST> a) {
+  constexpr int W = ColElem<VAR>::W;
+  const int ncol = a.D;
+  const int lane = threadIdx.x & 31, s = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  const bool colok = c < ncol;
+  const int rpt = (int)((a.T + kSmallWarps - 1) / kSmallWarps);
+  const int64_t rbase = (int64_t)s * rpt;
+  __shared__ double segagg[kSmallWarps][32][W];
+  __shared__ int s_fail[kSmallT];
+  __shared__ unsigned s_nf;
+  __shared__ unsigned long long s_dm;
+  double ej[kSmallRows], eu[kSmallRows], eb[kSmallRows], ec[kSmallRows], ed[kSmallRows], ev[kSmallRows];
+  ColElem<VAR> run;
+  run.ident();
+#pragma unroll
+  for (int k = 0; k < kSmallRows; ++k) {
+    const int64_t r = rbase + k;
+    const bool ok = colok && k < rpt && r < a.T;
+    if constexpr (VAR == SCAN_DIAG) {
+      ej[k] = ok ? (double)a.e0[r * ncol + c] : 1.0;
+      eu[k] = ok ? (double)a.u[r * ncol + c] : 0.0;
+      run.push(ej[k], eu[k]);
+    } else {
+      ej[k] = ok ? (double)a.e0[r * ncol + c] : 1.0;
+      eb[k] = ok ? (double)a.e1[r * ncol + c] : 0.0;
+      ec[k] = ok ? (double)a.e2[r * ncol + c] : 0.0;
+      ed[k] = ok ? (double)a.e3[r * ncol + c] : 1.0;
+      eu[k] = ok ? (double)a.u[r * 2 * ncol + c] : 0.0;
+      ev[k] = ok ? (double)a.u[r * 2 * ncol + ncol + c] : 0.0;
+      run.push(ej[k], eb[k], ec[k], ed[k], eu[k], ev[k]);
+    }
+  }
+  run.store(segagg[s][lane]);
+  if constexpr (UPDATE) {
+    for (int i = threadIdx.x; i < kSmallT; i += blockDim.x) s_fail[i] = 0;
+    if (threadIdx.x == 0) { s_nf = 0; s_dm = 0ull; }
+  }
+  __syncthreads();
+  // state entering this warp's rows: s0, then the earlier warps' segments
+  double x = colok ? (double)a.s0[c] : 0.0, v = (VAR == SCAN_BLOCK && colok) ? (double)a.s0[ncol + c] : 0.0;
+  for (int q = 0; q < s; ++q) {
+    ColElem<VAR> e;
+    e.load(segagg[q][lane]);
+    if constexpr (VAR == SCAN_DIAG) e.apply(x);
+    else e.apply(x, v);
+  }
+  unsigned long long dmb = 0ull;
+  auto check = [&](int k, int64_t idx, double xv) {
+    if constexpr (UPDATE) {
+      const double xd = (double)(ST)xv;
+      const double gap = fabs(xd - (double)a.guess[idx]);
+      if (gap > a.atol + a.rtol * fabs(xd)) s_fail[s * rpt + k] = 1;
+      const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
+      dmb = gb > dmb ? gb : dmb;
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < kSmallRows; ++k) {
+    const int64_t r = rbase + k;
+    if (!(colok && k < rpt && r < a.T)) continue;
+    if constexpr (VAR == SCAN_DIAG) {
+      x = ej[k] * x + eu[k];
+      a.out[r * ncol + c] = (ST)x;
+      check(k, r * ncol + c, x);
+    } else {
+      const double xa = ej[k] * x + eb[k] * v + eu[k];
+      const double va = ec[k] * x + ed[k] * v + ev[k];
+      x = xa;
+      v = va;
+      a.out[r * 2 * ncol + c] = (ST)x;
+      a.out[r * 2 * ncol + ncol + c] = (ST)v;
+      check(k, r * 2 * ncol + c, x);
+      check(k, r * 2 * ncol + ncol + c, v);
+    }
+  }
+  if constexpr (UPDATE) {
+    dmb = warp_max_u64(dmb);
+    if (lane == 0) atomicMax(&s_dm, dmb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.T; i += blockDim.x)
+      if (s_fail[i]) {
+        a.last_fail[i] = a.it;
+        atomicAdd(&s_nf, 1u);  // per column block, like scan_cols: only "any row failed" is used
+      }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_nf) atomicAdd(&a.stats->fail_rows, s_nf);
+      atomicMax((unsigned long long *)&a.stats->dmax, s_dm);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // dense, D <= MD <= 8: each thread folds SEG consecutive steps into (M, w) in
 // registers; warp shuffles + smem give the block scan; look-back on the
 // D-vector exit state.
@@ -1684,6 +1788,15 @@ cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStrea
     } else {
       if (update) launch_rows<ST, SCAN_BLOCK, true>(p, a, w, st);
       else launch_rows<ST, SCAN_BLOCK, false>(p, a, w, st);
+    }
+  } else if (p.kind == 1 && a.T <= kSmallT) {  // the whole sequence fits one CTA per column block
+    const unsigned g = (unsigned)((a.D + 31) / 32);
+    if (p.var == SCAN_DIAG) {
+      if (update) scan_cols_small<ST, SCAN_DIAG, true><<<g, kSmallWarps * 32, 0, st>>>(a);
+      else scan_cols_small<ST, SCAN_DIAG, false><<<g, kSmallWarps * 32, 0, st>>>(a);
+    } else {
+      if (update) scan_cols_small<ST, SCAN_BLOCK, true><<<g, kSmallWarps * 32, 0, st>>>(a);
+      else scan_cols_small<ST, SCAN_BLOCK, false><<<g, kSmallWarps * 32, 0, st>>>(a);
     }
   } else if (p.kind == 1) {
     if (p.var == SCAN_DIAG) {

@@ -621,3 +621,58 @@ def test_row_scan_lookback_warp_variant(cuda_device, lag, round_kb):
                         "no:cacheprovider", "-k", "multi_round or update_scan_bookkeeping or scan_kats or diag_and_block"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("T", [1, 2, 17, 100, 127, 128, 129])
+@pytest.mark.parametrize("D", [65, 300])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_wide_short_scans_vs_oracle(cuda_device, T, D, dtype):
+    # scan_cols_small (D > 64, T <= 128: one CTA per column block, no look-back) and
+    # scan_cols just above the switch, diag and block2x2
+    rng = np.random.default_rng(1000 * T + D)
+    tt = lambda x: torch.as_tensor(x, dtype=dtype, device=cuda_device)
+    tol = 1e-12 if dtype == torch.float64 else 2e-5
+    j, u, s0 = rng.uniform(-0.95, 0.95, (T, D)), rng.normal(size=(T, D)), rng.normal(size=D)
+    want = O.parallel_affine_solve(O.DiagElements(j, u), s0, workers=4)
+    got = np_(cs.parallel_affine_solve(cs.DiagElements(tt(j), tt(u)), tt(s0)))
+    np.testing.assert_allclose(got, want, atol=tol * 10, rtol=tol)
+    a, b, c, d = (rng.uniform(-0.65, 0.65, (T, D)) for _ in range(4))
+    ub, s0b = rng.normal(size=(T, 2 * D)), rng.normal(size=2 * D)
+    want = O.parallel_affine_solve(O.Block2x2Elements(a, b, c, d, ub), s0b, workers=4)
+    got = np_(cs.parallel_affine_solve(cs.Block2x2Elements(tt(a), tt(b), tt(c), tt(d), tt(ub)), tt(s0b)))
+    np.testing.assert_allclose(got, want, atol=tol * 10, rtol=tol)
+
+
+def test_wide_short_update_scan_bookkeeping(cuda_device):
+    # the small-T kernel's fused bookkeeping against a direct evaluation
+    from paper_2508_18413_b200 import _lib
+
+    lib = _lib.load()
+    T, D, it = 100, 1000, 5
+    g = torch.Generator(device=cuda_device).manual_seed(9)
+    a, b, c, d = ((torch.rand((T, D), generator=g, device=cuda_device, dtype=torch.float64) * 1.3 - 0.65)
+                  for _ in range(4))
+    u = torch.randn((T, 2 * D), generator=g, device=cuda_device, dtype=torch.float64)
+    s0 = torch.zeros(2 * D, device=cuda_device, dtype=torch.float64)
+    ref = cs.parallel_affine_solve(cs.Block2x2Elements(a, b, c, d, u), s0)
+    guess = ref + torch.randn((T, 2 * D), generator=g, device=cuda_device, dtype=torch.float64) * 1e-3 * (
+        torch.rand((T, 1), generator=g, device=cuda_device) < 0.4)
+    out = torch.empty_like(ref)
+    last_fail = torch.full((T,), 3, dtype=torch.int32, device=cuda_device)
+    stats = torch.zeros(40, dtype=torch.uint8, device=cuda_device)
+    wsb = lib.cs_scan_workspace_bytes(_lib.CS_MODE_BLOCK, _lib.CS_F64, T, D)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=cuda_device)
+    atol, rtol = 1e-6, 1e-6
+    _lib.check(lib.cs_scan_block_update(_lib.CS_F64, *[_lib.ptr(x) for x in (a, b, c, d, u, s0, out)], T, D,
+                                        _lib.ptr(ws), wsb, _lib.ptr(guess), atol, rtol, it, _lib.ptr(last_fail),
+                                        _lib.ptr(stats), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out, ref, atol=1e-12, rtol=1e-12)
+    gap = (out - guess).abs()
+    fail = (gap > atol + rtol * out.abs()).any(dim=1)
+    want_lf = torch.where(fail, torch.tensor(it, dtype=torch.int32, device=cuda_device),
+                          torch.tensor(3, dtype=torch.int32, device=cuda_device))
+    assert torch.equal(last_fail, want_lf)
+    raw = stats.cpu().numpy().tobytes()
+    assert (int(np.frombuffer(raw[28:32], dtype=np.uint32)[0]) > 0) == bool(fail.any())
+    assert float(np.frombuffer(raw[32:40], dtype=np.float64)[0]) == float(gap.max())

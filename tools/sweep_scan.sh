@@ -1,1 +1,2 @@
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:deer_persistent -c 1 -o gpurun_out/prof_hmc_bench -f python bench.py --steps 1 --warmup 1 --no-extras > /dev/null 2>&1; echo ncu=$?
+timeout 900 python -m pytest tests -m gpu -x -q -k "wide_short or leapfrog or wide or scan" 2>&1 | tail -3
+timeout 600 python tools/bench_configs.py 4 2>&1 | tail -1 | cut -c1-160
