@@ -420,8 +420,19 @@ class _NotInstantiated(Exception):
 _STATS_BYTES = 40
 
 
+_PINNED_STATS: dict = {}
+
+
 def _parse_stats(buf):
-    raw = buf.cpu().numpy().tobytes()
+    # one 40-byte read-back per iteration into a reused pinned buffer (no
+    # pageable allocation, one stream sync)
+    host = _PINNED_STATS.get(buf.numel())
+    if host is None:
+        host = torch.empty(buf.numel(), dtype=torch.uint8).pin_memory()
+        _PINNED_STATS[buf.numel()] = host
+    host.copy_(buf, non_blocking=True)
+    torch.cuda.current_stream(buf.device).synchronize()
+    raw = host.numpy().tobytes()
     bad_prop, bad_step, bad_jac = np.frombuffer(raw[:24], dtype=np.int64)
     picard, fail_rows = np.frombuffer(raw[24:32], dtype=np.uint32)
     dmax = float(np.frombuffer(raw[32:40], dtype=np.float64)[0])
