@@ -339,14 +339,45 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     umma_pipe_init(pipe);
     pipe.tmem = tmem_alloc128(&s_tmem);  // its barrier also publishes the mbarrier inits
   }
+  // TCM 2: the next step's weight row is loaded into registers behind this
+  // step's Hessian, so the weights never cost an exposed round trip
+  constexpr int WP = 8;  // weights per thread held in registers (N <= 2048; beyond: direct loads)
+  float wpre[WP];
+  auto wload = [&](int64_t rr) {
+#pragma unroll
+    for (int p = 0; p < WP; ++p) {
+      const int n = tid + p * kBdThr;
+      wpre[p] = (rr < sys.T && n < N) ? (float)__ldg(WS + rr * N + n) : 0.0f;
+    }
+  };
+  if constexpr (TCM == 2) wload(blockIdx.x);
   for (int64_t r = blockIdx.x; r < sys.T; r += gridDim.x) {
     const int64_t t = r + 1;
     const double *w = WS + r * N;
+    // this step's vectors are requested now and used after the Hessian
+    const ST *pr = r == 0 ? s0 : guess + (r - 1) * D;
+    double pS = 0.0, pX = 0.0, pR = 0.0, pZ = 0.0, pG = 0.0, pH = 0.0, pgS = 0.0, pgu = 0.0;
+    if (tid < D) {
+      pS = (double)pr[tid];
+      pX = A2[r * D + tid];
+      pR = R[r * D + tid];
+      pZ = (double)xi[t * D + tid];
+      pG = GX[r * D + tid];
+      pH = HR[r * D + tid];
+      pgS = gS[r * D + tid];
+      pgu = (double)guess[r * D + tid];
+    }
     if constexpr (TCM == 2) {
       float *wbuf = (float *)Xs;
-      for (int n = tid; n < ldx; n += kBdThr) wbuf[n] = n < N ? (float)__ldg(w + n) : 0.0f;
+#pragma unroll
+      for (int p = 0; p < WP; ++p) {
+        const int n = tid + p * kBdThr;
+        if (n < ldx) wbuf[n] = wpre[p];
+      }
+      for (int n = tid + WP * kBdThr; n < ldx; n += kBdThr) wbuf[n] = n < N ? (float)__ldg(w + n) : 0.0f;
       __syncthreads();
       gram_tcgen05<kBdThr>(pipe, Xf, ldx, N, wbuf, (float *)Hs, (float *)Hs, HLD);
+      wload(r + gridDim.x);
     } else if constexpr (TC) {
       // H_raw on the tensor cores (mma.sync m16n8k8 TF32, f32 accumulate):
       // warp wid owns output rows 16 wid .. 16 wid + 15, all 16 column blocks
@@ -470,14 +501,13 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     }
     // vectors
     double ss = 0.0, sx = 0.0, sr = 0.0, sxi = 0.0, hxr = 0.0;
-    const ST *pr = r == 0 ? s0 : guess + (r - 1) * D;
     if (tid < D) {
-      const double S = (double)pr[tid], xt = A2[r * D + tid], rr = R[r * D + tid], z = (double)xi[t * D + tid];
+      const double S = pS, xt = pX, rr = pR, z = pZ;
       vS[tid] = S;
       vX[tid] = xt;
-      vG[tid] = GX[r * D + tid];
+      vG[tid] = pG;
       vR[tid] = rr;
-      hxr = -HR[r * D + tid] - prec * rr;  // H(x~) r
+      hxr = -pH - prec * rr;  // H(x~) r
       vH[tid] = hxr;
       vP[tid] = cfg.preconditioner ? S * __ldg(cfg.preconditioner + tid) : S;  // p . S
       ss = S * S;
@@ -537,7 +567,7 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
       const double hg = -(mpart[0][0][tid] + mpart[0][1][tid]) - prec * vG[tid];
       const double hr = -(mpart[1][0][tid] + mpart[1][1][tid]) - prec * vR[tid];
       const double hh = -(mpart[2][0][tid] + mpart[2][1][tid]) - prec * vH[tid];
-      const double wv = (vG[tid] + eps * hg) - gS[r * D + tid] + 0.5 * (hr + (hxr + eps * hh));
+      const double wv = (vG[tid] + eps * hg) - pgS + 0.5 * (hr + (hxr + eps * hh));
       vW[tid] = wv;
       wps = wv * vP[tid];
     }
@@ -598,7 +628,7 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
       }
       uout[r * D + tid] = (ST)(f - jp);
       if (!isfinite(f)) flags[0] = 1;
-      if (!(fabs(f - (double)guess[r * D + tid]) <= cfg.atol + cfg.rtol * fabs(f))) flags[2] = 1;
+      if (!(fabs(f - pgu) <= cfg.atol + cfg.rtol * fabs(f))) flags[2] = 1;
     }
     __syncthreads();
     if (tid == 0) {

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q -k "streamed or leapfrog or gibbs or blr or engines" 2>&1 | tail -2
-timeout 600 python tools/bench_configs.py 4 5 3 2>&1 | grep config | cut -c1-140
+for i in 1 2 3; do timeout 900 python tools/bench_configs.py 3d 2>&1 | tail -1 | cut -c1-110; done
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv
