@@ -579,6 +579,10 @@ def _run_host(system, s0, cfg, max_iters):
                                         at(16), at(24), _lib.stream_ptr()))
             update = iterations < max_iters
             nxt = None
+            # the update is built before the Picard test is read back (one sync per
+            # iteration); if the test stops the run the update is discarded, and so
+            # are the jvp/hvp counts it made (deer.py:265-271 never evaluates them)
+            counts = (system.n_jvp_evals, system.n_hvp_evals)
             if update:
                 badj = buf[8:16].view(torch.int64)
                 badj.fill_(_NO_STEP)
@@ -598,6 +602,7 @@ def _run_host(system, s0, cfg, max_iters):
             if pic == 0:
                 if update:
                     last_fail.copy_(backup)
+                    system.n_jvp_evals, system.n_hvp_evals = counts
                 done = True
                 break
             if not update:
