@@ -51,8 +51,13 @@ def peaks():
         return 6650.0, "fallback"
 
 
+POLL_S = float(os.environ.get("CS_BENCH_POLL_MS", "5")) / 1e3
+
+
 class ClockSampler:
-    """SM clocks and throttle reasons sampled (NVML, ~1 kHz) during the timed region."""
+    """SM clocks and throttle reasons sampled (NVML, every POLL_S) during the timed
+    region.  NVML calls take driver locks, so a 1 kHz poller measurably delays the
+    solve's launches and read-back; 5 ms still yields ~10 samples per leg."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
@@ -87,7 +92,7 @@ class ClockSampler:
                             self.reasons.add(name)
                 except Exception:
                     pass
-                time.sleep(0.001)
+                time.sleep(POLL_S)
 
         self._t = threading.Thread(target=poll, daemon=True)
         self._t.start()
