@@ -1,1 +1,1 @@
-for ms in 1 5 1 5 1 5; do CS_BENCH_POLL_MS=$ms timeout 300 python bench.py --no-extras | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('poll', $ms, round(d['ms_per_step'],4), round(d['e2e']['ms_per_step'],4), d['clocks']['samples'])"; done
+timeout 900 python -m pytest tests/test_samplers_api.py -m gpu -q 2>&1 | tail -3
