@@ -246,6 +246,18 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
  * (samplers.py:129-145 collapsed: A = I + eps H(S), per-step Hessian on the
  * tensor cores for f32 storage). */
 int cs_system_elements_supported(const cs_system *sys, int32_t mode, int dtype);
+/* B independent inner leapfrog solves at once (samplers.py:301-320: the
+ * parallel-leapfrog HMC proposal, one run_deer per chain row in the reference):
+ * one CTA per proposal runs the whole Newton loop of deer.py:259-286 for its
+ * L-step trajectory in block2x2 mode.  s0s / finals: (B, dim) device rows in the
+ * call's dtype (finals = the last trajectory state); info (B, 4) int32 =
+ * {CS_RUN_* status, Newton iterations, CS_DIV_* kind, error iteration};
+ * err_step (B) = offending step or -1.  Supported for leapfrog systems on the
+ * register targets with L <= 256 and dim <= 4. */
+int cs_leapfrog_batch_supported(const cs_system *sys, int32_t mode, int dtype);
+int cs_leapfrog_batch_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, int32_t B,
+                            const void *s0s, void *finals, int32_t *info, int64_t *err_step,
+                            void *stream);
 /* Scans with the post-update bookkeeping fused into the replay (deer.py:273-277):
  * rows of `out` that moved more than atol + rtol|out| from `guess` get
  * last_fail[t] = iteration; d_stats->fail_rows / dmax are accumulated. */

@@ -100,6 +100,8 @@ _SIGS = {
     "cs_scan_block_update": ([ctypes.c_int, P, P, P, P, P, P, P, i64, i32, P, szt, P, f64, f64, i32, P, P, P],
                              ctypes.c_int),
     "cs_deer_workspace_bytes": ([SP, ctypes.c_int, i32], szt),
+    "cs_leapfrog_batch_supported": ([SP, i32, ctypes.c_int], ctypes.c_int),
+    "cs_leapfrog_batch_solve": ([SP, ctypes.POINTER(cs_deer_config), ctypes.c_int, i32, P, P, P, P, P], ctypes.c_int),
     "cs_deer_supported": ([SP, ctypes.c_int, ctypes.c_int], ctypes.c_int),
     "cs_deer_solve": ([SP, ctypes.POINTER(cs_deer_config), ctypes.c_int, P, P, P, P, P, szt,
                        ctypes.POINTER(cs_deer_result), P], ctypes.c_int),

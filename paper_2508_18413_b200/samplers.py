@@ -409,6 +409,9 @@ class HmcKernel(_Fused):
 
         cfg = self.leapfrog_cfg if self.leapfrog_cfg is not None else DeerConfig(mode="block2x2-stochastic")
         system = self.leapfrog_system()
+        batched = self._integrate_parallel_batched(ts, x, v, system, cfg)
+        if batched is not None:
+            return batched
         xs, vs = torch.empty_like(x), torch.empty_like(v)
         h = self.model.dim
         for b in range(x.shape[0]):
@@ -421,6 +424,57 @@ class HmcKernel(_Fused):
             else:
                 final = res.trace[-1].to(torch.float64)
                 xs[b], vs[b] = final[:h], final[h:]
+        return xs, vs
+
+    def _integrate_parallel_batched(self, ts, x, v, system, cfg):
+        """Every row's inner solve in one launch (cs_leapfrog_batch_solve: one CTA
+        per proposal runs its own Newton loop); rows are then taken in order with
+        the reference's semantics -- the first diverged row raises, rows that did
+        not converge fall back to the sequential integrator.  None when the
+        configuration needs the per-row engine (window, full trace, other modes)."""
+        from .deer import _DIVERGENCE_FACTOR, default_max_iters
+
+        if (cfg.mode != "block2x2-stochastic" or cfg.full_trace or getattr(cfg, "engine", "auto") == "host"
+                or (cfg.window_len is not None and cfg.window_len < system.T)):
+            return None
+        lib = _lib.load()
+        dt = _lib.dtype_code(self.dtype)
+        d = system.desc()
+        if not lib.cs_leapfrog_batch_supported(ctypes.byref(d), _lib.CS_MODE_BLOCK, dt):
+            return None
+        B = x.shape[0]
+        h = self.model.dim
+        s0s = torch.cat([x, v], dim=1).to(self.dtype).contiguous()
+        finals = torch.empty_like(s0s)
+        info = torch.empty((B, 4), dtype=torch.int32, device=self.device)
+        err = torch.empty(B, dtype=torch.int64, device=self.device)
+        c = _lib.cs_deer_config()
+        c.mode = _lib.CS_MODE_BLOCK
+        c.atol, c.rtol = float(cfg.atol), float(cfg.rtol)
+        c.max_iters = int(cfg.max_iters if cfg.max_iters is not None else default_max_iters(system.T))
+        c.hutchinson_samples = int(cfg.hutchinson_samples)
+        c.damping, c.clip = float(cfg.damping), float(cfg.clip)
+        pre = None if cfg.preconditioner is None else torch.as_tensor(cfg.preconditioner, dtype=torch.float64,
+                                                                       device=self.device).contiguous()
+        c.preconditioner = 0 if pre is None else pre.data_ptr()
+        _lib.check(lib.cs_leapfrog_batch_solve(ctypes.byref(d), ctypes.byref(c), dt, B, _lib.ptr(s0s), _lib.ptr(finals),
+                                               _lib.ptr(info), _lib.ptr(err), _lib.stream_ptr()))
+        info_h, err_h = info.cpu().numpy(), err.cpu().numpy()
+        ts_h = np.asarray(ts.cpu() if torch.is_tensor(ts) else ts).reshape(-1)
+        xs, vs = finals[:, :h].to(torch.float64).clone(), finals[:, h:].to(torch.float64).clone()
+        for b in range(B):
+            status, iters, kind, eit = (int(q) for q in info_h[b])
+            if status == _lib.CS_RUN_DIVERGED:
+                step = None if err_h[b] < 0 else int(err_h[b])
+                it = None if eit < 0 else eit
+                msg = {_lib.CS_DIV_STEP: f"non-finite step value at step {step} (iteration {it})",
+                       _lib.CS_DIV_JACOBIAN: f"non-finite jacobian at step {step} (iteration {it})"}.get(
+                    kind, f"fixed-point iteration diverging: delta_max exceeds {_DIVERGENCE_FACTOR:.0e} x initial")
+                raise ChainDivergedError(msg, step=step, iteration=it)
+            if status != _lib.CS_RUN_CONVERGED:
+                self.fallback_events.append((int(ts_h[b]), iters))
+                xb, vb = self._integrate_sequential(x[b:b + 1], v[b:b + 1])
+                xs[b], vs[b] = xb[0], vb[0]
         return xs, vs
 
     def _torch_step(self, ts, S, relaxed):

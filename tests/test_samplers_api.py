@@ -9,7 +9,7 @@ import pytest
 import torch
 
 import paper_2508_18413_b200 as cs
-from paper_2508_18413_b200.errors import ConfigurationError
+from paper_2508_18413_b200.errors import ChainDivergedError, ConfigurationError
 from paper_2508_18413_b200.samplers import (CLASSIC_EFFECTS, CLASSIC_SES, gibbs_sweep, hmc_chain_system, hmc_step,
                                             leapfrog_block_jacobian, leapfrog_step)
 
@@ -223,3 +223,38 @@ def test_gibbs_chain_solves_as_a_fixed_point(cuda_device):
     r = cs.run_deer(kernel, s0, cs.DeerConfig(mode="dense", max_iters=200))
     assert r.converged and r.iterations < 100
     assert np.all(np.abs(np_(r.trace) - reference) <= 1e-4 + 1e-3 * np.abs(reference))
+
+
+@pytest.mark.parametrize("target,eps,L,max_iters", [("rosen", 0.2, 16, None), ("rosen", 0.05, 16, 1),
+                                                    ("std", 0.1, 32, None), ("gauss", 0.3, 40, 3)])
+def test_batched_inner_solves_match_per_row_runs(cuda_device, target, eps, L, max_iters):
+    # cs_leapfrog_batch_solve (one CTA per proposal) against the per-row run_deer
+    # loop of samplers.py:301-320 (engine="host"): same states, same fallbacks
+    tg = {"rosen": cs.rosenbrock(), "std": cs.std_normal(2),
+          "gauss": cs.gaussian(np.zeros(2), np.array([[1.1, 0.0], [0.3, 0.8]]))}[target]
+    model = cs.model_logp_grad_hvp(tg)
+    kw = {} if max_iters is None else dict(max_iters=max_iters)
+    fast = hmc_chain_system(model, eps=eps, L=L, seed=5, T=48, leapfrog_mode="parallel",
+                            leapfrog_cfg=cs.DeerConfig(mode="block2x2-stochastic", **kw))
+    slow = hmc_chain_system(model, eps=eps, L=L, seed=5, T=48, leapfrog_mode="parallel",
+                            leapfrog_cfg=cs.DeerConfig(mode="block2x2-stochastic", engine="host", **kw))
+    x0 = np.array([0.5, -0.5])
+
+    def outcome(k):
+        try:
+            return np_(cs.sequential_evaluate(k, x0)), None
+        except ChainDivergedError as e:  # an inner solve tripping its guard propagates, as in the reference
+            return None, (e.step, e.iteration)
+
+    (a, ea), (b, eb) = outcome(fast), outcome(slow)
+    assert ea == eb
+    assert fast.fallback_events == slow.fallback_events
+    if ea is not None:
+        return
+    np.testing.assert_allclose(a, b, atol=1e-10, rtol=1e-10)
+    # and one batched step_batch over all rows equals the per-row loop
+    S = torch.as_tensor(a, device=cuda_device)
+    ts = torch.arange(1, 49, device=cuda_device)
+    fast.fallback_events.clear(), slow.fallback_events.clear()
+    np.testing.assert_allclose(np_(fast.step_batch(ts, S)), np_(slow.step_batch(ts, S)), atol=1e-10, rtol=1e-10)
+    assert fast.fallback_events == slow.fallback_events
