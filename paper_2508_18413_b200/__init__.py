@@ -40,6 +40,7 @@ from .samplers import (  # noqa: F401
 )
 from .targets import blr, gaussian, model_logp_grad_hvp, mog, rosenbrock, std_normal, synthetic_credit_like  # noqa: F401
 
+from .basis import OrthogonalBasis, orthogonal_basis, transform_system  # noqa: F401
 from .tracefile import TraceFormatError, export_csv, read_trace, write_trace  # noqa: F401
 
 __version__ = "0.1.0"

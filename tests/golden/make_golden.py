@@ -232,7 +232,39 @@ def trace_fixture():
     print("wrote trace_ref")
 
 
+def basis_fixture():
+    # orthogonal change of basis (targets.py:400-517): Jacobi eigenbasis of a random
+    # symmetric matrix, and a diag quasi-Newton MALA solve in the eigenbasis of a
+    # correlated Gaussian's precision
+    from chainscan.targets import orthogonal_basis, transform_system
+
+    out = {}
+    rng = np.random.default_rng(5)
+    M = rng.normal(size=(16, 16))
+    C = M + M.T
+    b = orthogonal_basis(C)
+    out["C"], out["Q"], out["eig"] = C, b.Q, b.eigenvalues
+    A = rng.normal(size=(4, 4))
+    P = A @ A.T + 0.5 * np.eye(4)
+    Lc = np.linalg.cholesky(P)
+    m = model_logp_grad_hvp(gaussian(np.array([0.5, -1.0, 0.0, 1.0]), Lc))
+    k = MalaKernel(m, eps=0.15, seed=9, T=400)
+    basis = orthogonal_basis(P)
+    w = transform_system(k, basis.Q)
+    s0 = np.zeros(4)
+    out["chol"], out["P"], out["Qp"] = Lc, P, basis.Q
+    r = run_deer(w, w.transform_state(s0), DeerConfig(mode="diag-stochastic", workers=WORKERS))
+    out["z_trace"], out["z_iterations"], out["z_converged"] = r.trace, np.array(r.iterations), np.array(r.converged)
+    out["seq"] = sequential_evaluate(k, s0)
+    r2 = run_deer(k, s0, DeerConfig(mode="diag-stochastic", workers=WORKERS))
+    out["plain_iterations"] = np.array(r2.iterations)
+    save("basis", **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["basis"]:
+        basis_fixture()
+        sys.exit(0)
     if sys.argv[1:] == ["blr_dense"]:
         blr_dense_fixture()
         sys.exit(0)
@@ -244,3 +276,4 @@ if __name__ == "__main__":
     chain_fixtures()
     blr_dense_fixture()
     trace_fixture()
+    basis_fixture()

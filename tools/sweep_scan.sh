@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_basis.py -m gpu -q 2>&1 | tail -15
