@@ -149,14 +149,17 @@ int cs_scan_block(int dtype, const void *a, const void *b, const void *c, const 
                   const void *u, const void *s0, void *out, int64_t T, int32_t D,
                   void *ws, size_t ws_bytes, void *stream);
 /* dense: D <= 8 single-pass register kernel; 8 < D <= 128 chunked reduce /
- * two-level f64 carry / replay (pscan.py:196-213, _scan_kernels.py:47-99). */
+ * two-level f64 carry / replay; D > 128 chunk maps composed by strided-batched
+ * library GEMMs (storage type), f64 carry, CTA-per-chunk replay
+ * (pscan.py:196-213, _scan_kernels.py:47-99; any D like the reference). */
 int cs_scan_dense(int dtype, const void *J, const void *u, const void *s0, void *out,
                   int64_t T, int32_t D, void *ws, size_t ws_bytes, void *stream);
 
 /* Composed affine map of the whole sequence (the shard carry exchanged by the
  * T-sharded driver): agg_out f64 = diag [j|u] (2D), block
- * [A|B|C|E|ux|uv] (6D), dense [M row-major | w] (D*D + D).  Same workspace as
- * the scan of that mode. */
+ * [A|B|C|E|ux|uv] (6D), dense [M row-major | w] (D*D + D; for D > 8 the chunk
+ * maps are folded as a tree of f64 GEMMs on augmented (D+1)^2 matrices).  Same
+ * workspace as the scan of that mode. */
 int cs_scan_aggregate(int mode, int dtype, const void *e0, const void *e1, const void *e2,
                       const void *e3, const void *u, int64_t T, int32_t D, double *agg_out,
                       void *ws, size_t ws_bytes, void *stream);

@@ -351,8 +351,30 @@ int cs_rademacher_fill(uint64_t seed, int64_t iteration, const int64_t *ts, int6
 // ---- scans -----------------------------------------------------------------
 size_t cs_scan_workspace_bytes(int mode, int dtype, int64_t T, int32_t D) {
   const int var = mode == CS_MODE_DIAG ? SCAN_DIAG : mode == CS_MODE_BLOCK ? SCAN_BLOCK : SCAN_DENSE;
+  if (var == SCAN_DENSE && D > 128) return dense_xl_ws_bytes(T, D, dtype == CS_F64 ? 8 : 4);
   if (var == SCAN_DENSE && D > 8) return dense_wide_ws_bytes(T, D);
   return scan_ws_bytes(var, dtype, T, D);
+}
+
+// wide dense scans (D > 8) and their whole-sequence aggregate (agg_out != null):
+// cs_dense.cu up to D = 128, cs_dense_xl.cu beyond
+static int dense_wide_call(int dtype, const void *J, const void *u, const void *s0, void *out, int64_t T, int D,
+                           void *ws, size_t ws_bytes, double *agg_out, void *stream) {
+  const size_t need = D > 128 ? dense_xl_ws_bytes(T, D, dtype == CS_F64 ? 8 : 4) : dense_wide_ws_bytes(T, D);
+  if (ws_bytes < need) return fail(CS_ERR_CONFIG, "scan workspace too small");
+  cudaError_t e;
+  if (dtype == CS_F64) {
+    ScanArgs<double> a{(const double *)J, nullptr, nullptr, nullptr, (const double *)u, (const double *)s0,
+                       (double *)out, T, D};
+    e = D > 128 ? launch_dense_xl_t<double>(a, ws, agg_out, S(stream))
+                : launch_dense_wide_t<double>(a, ws, S(stream), agg_out);
+  } else {
+    ScanArgs<float> a{(const float *)J, nullptr, nullptr, nullptr, (const float *)u, (const float *)s0,
+                      (float *)out, T, D};
+    e = D > 128 ? launch_dense_xl_t<float>(a, ws, agg_out, S(stream))
+                : launch_dense_wide_t<float>(a, ws, S(stream), agg_out);
+  }
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, agg_out ? "dense aggregate launch" : "dense scan launch");
 }
 
 static int do_scan(int var, int dtype, const void *e0, const void *e1, const void *e2, const void *e3,
@@ -360,22 +382,8 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
                    void *stream) {
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   if (T < 0 || D < 1) return fail(CS_ERR_STRUCTURAL, "bad scan shape");
-  if (var == SCAN_DENSE && D > 128) return fail(CS_ERR_CONFIG, "dense scan supports D <= 128");
   if (var != SCAN_DENSE && D > 4096) return fail(CS_ERR_CONFIG, "scan D too large");
-  if (var == SCAN_DENSE && D > 8) {  // wide dense: chunked reduce / carry / replay (cs_dense.cu)
-    if (ws_bytes < dense_wide_ws_bytes(T, D)) return fail(CS_ERR_CONFIG, "scan workspace too small");
-    cudaError_t e;
-    if (dtype == CS_F64) {
-      ScanArgs<double> a{(const double *)e0, nullptr, nullptr, nullptr, (const double *)u, (const double *)s0,
-                         (double *)out, T, D};
-      e = launch_dense_wide_t<double>(a, ws, S(stream));
-    } else {
-      ScanArgs<float> a{(const float *)e0, nullptr, nullptr, nullptr, (const float *)u, (const float *)s0,
-                        (float *)out, T, D};
-      e = launch_dense_wide_t<float>(a, ws, S(stream));
-    }
-    return e == cudaSuccess ? CS_OK : cuda_fail(e, "dense scan launch");
-  }
+  if (var == SCAN_DENSE && D > 8) return dense_wide_call(dtype, e0, u, s0, out, T, D, ws, ws_bytes, nullptr, stream);
   const ScanPlan p = scan_plan(var, dtype, T, D);
   if (ws_bytes < p.ws_bytes) return fail(CS_ERR_CONFIG, "scan workspace too small");
   if (T == 0) return CS_OK;
@@ -415,7 +423,8 @@ int cs_scan_aggregate(int mode, int dtype, const void *e0, const void *e1, const
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   if (T < 1 || D < 1) return fail(CS_ERR_STRUCTURAL, "bad aggregate shape");
   const int var = mode == CS_MODE_DIAG ? SCAN_DIAG : mode == CS_MODE_BLOCK ? SCAN_BLOCK : SCAN_DENSE;
-  if (var == SCAN_DENSE && D > 8) return fail(CS_ERR_CONFIG, "dense aggregate supports D <= 8");
+  if (var == SCAN_DENSE && D > 8)
+    return dense_wide_call(dtype, e0, u, nullptr, nullptr, T, D, ws, ws_bytes, agg_out, stream);
   const ScanPlan p = scan_plan(var, dtype, T, D);
   if (ws_bytes < p.ws_bytes) return fail(CS_ERR_CONFIG, "scan workspace too small");
   cudaError_t e;

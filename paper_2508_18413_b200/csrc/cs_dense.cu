@@ -272,7 +272,10 @@ size_t dense_wide_ws_bytes(int64_t T, int D) {
   const int c = dense_wide_chunk(T);
   const int64_t nch = (T + c - 1) / c;
   const int64_t ng = (nch + 15) / 16;
-  return (size_t)(nch + ng) * ((size_t)D * D + 2 * D) * sizeof(double) + 256;
+  // + the tree scratch of the whole-sequence aggregate (cs_scan_aggregate):
+  // the chunk aggregates when there are few, else the group aggregates
+  const int64_t nf = nch <= 64 ? nch : ng;
+  return (size_t)(nch + ng) * ((size_t)D * D + 2 * D) * sizeof(double) + 256 + dense_tree_bytes(nf, D) + 256;
 }
 
 static bool dense_tc() {  // CS_DENSE_TC=0 keeps the f32 composition on the FP32 pipes
@@ -497,7 +500,7 @@ static cudaError_t launch_tail(const ScanArgs<ST> &a, int c, int64_t nch, const 
 }
 
 template <typename ST>
-cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
+cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st, double *agg_out) {
   const int64_t T = a.T;
   const int D = a.D;
   if (T == 0) return cudaSuccess;
@@ -524,6 +527,23 @@ cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
     default: e = launch_reduce<ST, 128>(a, c, nch, aggM, aggw, st); break;
   }
   if (e != cudaSuccess) return e;
+  if (agg_out) {  // whole-sequence map: fold chunk (or group) aggregates as a tree of DGEMMs
+    double *tree = (double *)(((uintptr_t)(gM + ((nch + kDwGroup - 1) / kDwGroup) * ((int64_t)D * D + 2 * D)) + 255) &
+                              ~(uintptr_t)255);
+    if (nch <= 64) return dense_fold_aggregates(aggM, aggw, nch, D, tree, agg_out, st);
+    const int64_t ng = (nch + kDwGroup - 1) / kDwGroup;
+    double *gw = gM + ng * (int64_t)D * D;
+    ScanArgs<double> g{aggM, nullptr, nullptr, nullptr, aggw, nullptr, nullptr, nch, D};
+    switch (dense_dp(D)) {
+      case 16: e = launch_reduce<double, 16>(g, kDwGroup, ng, gM, gw, st); break;
+      case 32: e = launch_reduce<double, 32>(g, kDwGroup, ng, gM, gw, st); break;
+      case 64: e = launch_reduce<double, 64>(g, kDwGroup, ng, gM, gw, st); break;
+      case 112: e = launch_reduce<double, 112>(g, kDwGroup, ng, gM, gw, st); break;
+      default: e = launch_reduce<double, 128>(g, kDwGroup, ng, gM, gw, st); break;
+    }
+    if (e != cudaSuccess) return e;
+    return dense_fold_aggregates(gM, gw, ng, D, tree, agg_out, st);
+  }
   switch (dense_dp(D)) {
     case 16: e = launch_tail<ST, 16>(a, c, nch, aggM, aggw, entries, gM, st); break;
     case 32: e = launch_tail<ST, 32>(a, c, nch, aggM, aggw, entries, gM, st); break;
@@ -534,7 +554,7 @@ cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
   return e;
 }
 
-template cudaError_t launch_dense_wide_t<float>(ScanArgs<float>, void *, cudaStream_t);
-template cudaError_t launch_dense_wide_t<double>(ScanArgs<double>, void *, cudaStream_t);
+template cudaError_t launch_dense_wide_t<float>(ScanArgs<float>, void *, cudaStream_t, double *);
+template cudaError_t launch_dense_wide_t<double>(ScanArgs<double>, void *, cudaStream_t, double *);
 
 }  // namespace cs

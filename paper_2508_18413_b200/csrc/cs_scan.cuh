@@ -39,8 +39,16 @@ template <typename ST>
 cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update = false);
 // wide dense scans, 8 < D <= 128 (cs_dense.cu)
 size_t dense_wide_ws_bytes(int64_t T, int D);
+// agg_out != null: write the whole-sequence map [M (D x D) | w (D)] (f64) instead of scanning
 template <typename ST>
-cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st);
+cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st, double *agg_out = nullptr);
+// dense scans and aggregates for D > 128 (cs_dense_xl.cu)
+size_t dense_xl_ws_bytes(int64_t T, int D, int elem_bytes);
+template <typename ST>
+cudaError_t launch_dense_xl_t(ScanArgs<ST> a, void *ws, double *agg_out, cudaStream_t st);
+size_t dense_tree_bytes(int64_t n, int D);
+cudaError_t dense_fold_aggregates(const double *aggM, const double *aggw, int64_t n, int D, double *tree,
+                                  double *out, cudaStream_t st);
 template <typename ST>
 cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, double *out, cudaStream_t st);
 

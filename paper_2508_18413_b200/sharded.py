@@ -227,7 +227,7 @@ def run_deer_sharded(system, s0, cfg, ops: ShardOps | None = None, group=None, m
         pf = 0 if (f is None or bad_f is not None) else ops.picard_fails(guess, f, cfg.atol, cfg.rtol)
         vecA = torch.tensor([_NO_STEP if bad_prop is None else bad_prop,
                              _NO_STEP if bad_f is None else bad_f, float(pf)], dtype=torch.float64, device=dev)
-        gA = _gather(vecA, group, world) if world > 1 else vecA[None]
+        gA = _gather(vecA, group, world) if dist.is_initialized() else vecA[None]
         gbp, gbf, gpf = float(gA[:, 0].min()), float(gA[:, 1].min()), float(gA[:, 2].sum())
         if gbp < _NO_STEP:
             raise ChainDivergedError(f"non-finite {getattr(system, '_what', 'proposal')} at step {int(gbp)}",
@@ -244,7 +244,7 @@ def run_deer_sharded(system, s0, cfg, ops: ShardOps | None = None, group=None, m
         agg = ops.aggregate(el) if bad_j is None else torch.zeros(W, dtype=torch.float64, device=dev)
         vecB = torch.cat([agg.to(torch.float64),
                           torch.tensor([_NO_STEP if bad_j is None else bad_j], dtype=torch.float64, device=dev)])
-        gB = _gather(vecB, group, world) if world > 1 else vecB[None]
+        gB = _gather(vecB, group, world) if dist.is_initialized() else vecB[None]
         gbj = float(gB[:, W].min())
         if gbj < _NO_STEP:
             raise ChainDivergedError(f"non-finite jacobian at step {int(gbj)} (iteration {it + 1})",
@@ -257,7 +257,7 @@ def run_deer_sharded(system, s0, cfg, ops: ShardOps | None = None, group=None, m
         nfail, dmax = ops.bookkeeping(guess, nxt, cfg.atol, cfg.rtol, it, last_fail)
         vecC = torch.cat([torch.tensor([float(nfail), dmax], dtype=torch.float64, device=dev),
                           nxt[-1].to(torch.float64)])
-        gC = _gather(vecC, group, world) if world > 1 else vecC[None]
+        gC = _gather(vecC, group, world) if dist.is_initialized() else vecC[None]
         tot_fail = float(gC[:, 0].sum())
         dm = gC[:, 1]
         dmax_g = float("nan") if bool(torch.isnan(dm).any()) else float(dm.max())

@@ -151,10 +151,34 @@ def test_wide_dense_scan_kat_and_errors(cuda_device):
     got = np_(cs.parallel_affine_solve(cs.DenseElements(J, u), torch.ones(D, dtype=torch.float64, device=cuda_device)))
     want = 2.0 - 0.5 ** np.arange(1, T + 1)
     np.testing.assert_allclose(got, np.repeat(want[:, None], D, axis=1), rtol=1e-13, atol=1e-13)
-    with pytest.raises(Exception):
-        big = torch.zeros((2, 129, 129), device=cuda_device)
-        cs.parallel_affine_solve(cs.DenseElements(big, torch.zeros((2, 129), device=cuda_device)),
-                                 torch.zeros(129, device=cuda_device))
+    with pytest.raises(cs.StructuralError):
+        cs.parallel_affine_solve(cs.DenseElements(J, u), torch.ones(D + 1, dtype=torch.float64, device=cuda_device))
+
+
+@pytest.mark.parametrize("D,T", [(129, 1), (129, 1201), (200, 300), (257, 150)])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_xl_dense_scan_vs_oracle(cuda_device, D, T, dtype):
+    # D > 128 (cs_dense_xl.cu): batched-GEMM chunk maps, f64 carry, CTA-per-chunk
+    # replay; partial last chunks at T = 1201 (c = 9) and T = 150 (c = 8)
+    rng = np.random.default_rng(3 * D + T)
+    J = rng.normal(size=(T, D, D)) * (0.9 / (2.0 * np.sqrt(D)))
+    u = rng.normal(size=(T, D))
+    s0 = rng.normal(size=D)
+    tt = lambda x: torch.as_tensor(x, dtype=dtype, device=cuda_device)
+    Jd, ud, s0d = (np_(tt(x)).astype(np.float64) for x in (J, u, s0))
+    want = O.parallel_affine_solve(O.DenseElements(Jd, ud), s0d, workers=8)
+    got = np_(cs.parallel_affine_solve(cs.DenseElements(tt(J), tt(u)), tt(s0)))
+    tol = 1e-10 if dtype == torch.float64 else 2e-5
+    np.testing.assert_allclose(got, want, atol=tol * 10, rtol=tol)
+
+
+def test_xl_dense_scan_kat(cuda_device):
+    T, D = 333, 150
+    J = torch.eye(D, dtype=torch.float64, device=cuda_device).expand(T, D, D).contiguous() * 0.5
+    u = torch.ones((T, D), dtype=torch.float64, device=cuda_device)
+    got = np_(cs.parallel_affine_solve(cs.DenseElements(J, u), torch.ones(D, dtype=torch.float64, device=cuda_device)))
+    want = 2.0 - 0.5 ** np.arange(1, T + 1)
+    np.testing.assert_allclose(got, np.repeat(want[:, None], D, axis=1), rtol=1e-13, atol=1e-13)
 
 
 # ---------------------------------------------------------------------------
@@ -512,13 +536,45 @@ def test_sharded_driver_cuda_ops_single_rank(cuda_device, mode, kw):
     np.testing.assert_array_equal(np_(r.per_step_converged_at), np_(ref.per_step_converged_at))
 
 
-@pytest.mark.parametrize("mode", ["diag", "block", "dense"])
-def test_scan_aggregate_matches_fold(cuda_device, mode):
-    # cs_scan_aggregate = the composed map of the whole sequence (the shard carry)
+@pytest.mark.parametrize("which", ["hmc_diag", "mala_dense12"])
+def test_sharded_driver_over_nccl_single_rank(cuda_device, which):
+    # the multi-GPU driver's collectives on device tensors through NCCL (world
+    # size 1: the pool has one GPU per box; multi-rank exchange is the gloo suite)
+    import socket
+
+    import torch.distributed as dist
+    from paper_2508_18413_b200.sharded import gather_trace, run_deer_sharded
+
+    if which == "hmc_diag":
+        m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
+        k, s0, cfg = cs.HmcKernel(m, 0.5, 8, seed=0, T=4000), np.zeros(2), cs.DeerConfig(mode="diag-stochastic", clip=1.0)
+    else:
+        k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.std_normal(12)), 0.3, seed=2, T=1500)
+        s0, cfg = np.zeros(12), cs.DeerConfig(mode="dense")
+    ref = cs.run_deer(k, s0, cfg)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device(cuda_device))
+    try:
+        assert dist.get_backend() == "nccl"
+        r = run_deer_sharded(k, s0, cfg)
+        full = gather_trace(r, k.T)
+    finally:
+        dist.destroy_process_group()
+    assert r.iterations == ref.iterations and r.converged == ref.converged
+    np.testing.assert_allclose(np_(full), np_(ref.trace), atol=1e-10)
+
+
+@pytest.mark.parametrize("mode,D,T", [("diag", 4, 7001), ("block", 4, 7001), ("dense", 3, 7001), ("dense", 20, 500),
+                                       ("dense", 20, 7001), ("dense", 100, 3000), ("dense", 140, 400)])
+def test_scan_aggregate_matches_fold(cuda_device, mode, D, T):
+    # cs_scan_aggregate = the composed map of the whole sequence (the shard carry);
+    # dense D > 8 folds chunk (T = 500) or group (T = 7001) maps as a DGEMM tree
     from paper_2508_18413_b200.sharded import CudaShardOps, apply_agg
 
     rng = np.random.default_rng(5)
-    T, D = 7001, (4 if mode != "dense" else 3)
     tt = lambda x: torch.as_tensor(x, device=cuda_device)
     if mode == "diag":
         el = cs.DiagElements(tt(rng.uniform(-0.9, 0.9, (T, D))), tt(rng.normal(size=(T, D))))
