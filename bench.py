@@ -287,7 +287,7 @@ def scan_roofline(cs, dev, hbm, src):
     diag/block scans are HBM-bound; 12 B per element in fp32)."""
     import torch
 
-    T, D = 1 << 22, 18
+    T, D = 1 << 24, 18  # SURVEY.md 8d's large synthetic (3.6 GB of j, u, s): well past L2
     g = torch.Generator(device=dev).manual_seed(0)
     j = (torch.rand((T, D), generator=g, device=dev) * 1.8 - 0.9).float()
     u = torch.randn((T, D), generator=g, device=dev).float()

@@ -1615,9 +1615,11 @@ static int env_int(const char *name, int lo, int hi, int dflt) {
   const int v = e ? atoi(e) : 0;
   return v >= lo && v <= hi ? v : dflt;
 }
-static int rows_chunk_stages() {  // tuning override for experiments
-  static const int v = env_int("CS_SCAN_CHUNK_STAGES", 1, 256, 16);
-  return v;
+// cap on stages per chunk (measured, tools/sweep_scan.sh): diag 16 (T = 4M: 2.51
+// TB/s vs 2.27 at 32), block2x2 32 (T = 4M D = 18: 2.56 vs 2.38 at 16)
+static int rows_chunk_stages(int var) {
+  static const int v = env_int("CS_SCAN_CHUNK_STAGES", 1, 256, 0);  // tuning override for experiments
+  return v ? v : var == SCAN_BLOCK ? 32 : 16;
 }
 static int rows_resident_ctas(int minb) {  // persistent grid of scan_rows (launch bounds: minb CTAs per SM)
   static const int sms = [] {
@@ -1691,7 +1693,7 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update) {
       const int64_t stages = (T + p.R - 1) / p.R;
       const int64_t g = (int64_t)rows_resident_ctas(minb);
       int64_t cs = stages / (2 * g);
-      const int cmax = rows_chunk_stages();
+      const int cmax = rows_chunk_stages(var);
       if (cs > cmax) cs = cmax;
       if (rows_lbw()) {
         // the look-back is off the critical path, so chunks only need to be
