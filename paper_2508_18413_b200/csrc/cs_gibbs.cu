@@ -17,8 +17,15 @@ CS_D double team_sum(double v) {
   return v;
 }
 
+// fp32 storage: compiled for 4 resident CTAs per SM (64 registers, 4 B of
+// spill): cfg 5 T = 1M 92.8 -> 88.8 ms against the unconstrained 80-register
+// build (tools/build_gibbs_variants.sh); f64 keeps 80 (64 would spill 24 B)
+#ifndef CS_GIBBS_MINB
+#define CS_GIBBS_MINB 4
+#endif
+
 template <typename ST>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, sizeof(ST) == 4 ? CS_GIBBS_MINB : 1)
 k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout, ST *uout, cs_elem_stats *stats) {
   constexpr int S = 8, D = 18;
   constexpr double kFloor = 1e-8;
