@@ -240,6 +240,16 @@ typedef struct cs_elem_stats {
 int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtype, int64_t iteration,
                        const void *s0, const void *guess, void *e0, void *e1, void *e2, void *e3,
                        void *u, cs_elem_stats *d_stats, void *stream);
+/* cs_system_elements for the step range t0+1 .. t0+n of the chain -- one rank's
+ * T shard in the sharded driver: guess holds the shard's n rows,
+ * s0 the state before step t0+1 (the halo row); noise and probes are indexed by
+ * the absolute step, so the shard's elements equal rows t0 .. t0+n-1 of the
+ * whole chain's.  Register-kernel systems (incl. Gibbs); CS_ERR_CONFIG for the
+ * GEMM-backed builders unless the range is the whole chain.  Replaces the
+ * per-shard _iterate_range (deer.py:147-208) of a T-sharded run. */
+int cs_system_elements_range(const cs_system *sys, const cs_deer_config *cfg, int dtype, int64_t iteration,
+                             int64_t t0, int64_t n, const void *s0, const void *guess, void *e0, void *e1,
+                             void *e2, void *e3, void *u, cs_elem_stats *d_stats, void *stream);
 /* 1 when cs_system_elements can build elements for (sys, mode, dtype): the
  * register builders (narrow built-in systems); for a leapfrog system on a
  * dense Gaussian target in block2x2 mode at any dimension, the GEMM-backed

@@ -668,6 +668,39 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements");
 }
 
+int cs_system_elements_range(const cs_system *sys, const cs_deer_config *cfg, int dtype, int64_t iteration,
+                             int64_t t0, int64_t n, const void *s0, const void *guess, void *e0, void *e1, void *e2,
+                             void *e3, void *u, cs_elem_stats *d_stats, void *stream) {
+  if (!sys || !cfg || !d_stats) return fail(CS_ERR_CONFIG, "null argument");
+  if (t0 < 0 || n < 0 || t0 + n > sys->T) return fail(CS_ERR_STRUCTURAL, "step range outside [1, T]");
+  if (t0 == 0 && n == sys->T)
+    return cs_system_elements(sys, cfg, dtype, iteration, s0, guess, e0, e1, e2, e3, u, d_stats, stream);
+  if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
+  const int md = elem_width(sys);
+  if (!md) return fail(CS_ERR_CONFIG, "step ranges need a register-kernel system (GEMM-backed builders take whole chains)");
+  if (cfg->mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG)
+    return fail(CS_ERR_CONFIG, "system does not provide a block2x2 Jacobian estimate");
+  cudaStream_t st = S(stream);
+  k_init_stats<<<1, 1, 0, st>>>(d_stats);
+  if (n < 1) return CS_OK;
+  cudaError_t e;
+  if (dtype == CS_F64) {
+    SolveArgs<double> A{};
+    A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;
+    A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
+    A.pre = cfg->preconditioner; A.s0 = (const double *)s0; A.T = n; A.D = sys->dim; A.t0 = t0;
+    e = elements_dispatch(*sys, dtype, md, cfg->mode, &A, (int)iteration, guess, e0, e1, e2, e3, u, d_stats, st);
+  } else {
+    SolveArgs<float> A{};
+    A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;
+    A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
+    A.pre = cfg->preconditioner; A.s0 = (const float *)s0; A.T = n; A.D = sys->dim; A.t0 = t0;
+    e = elements_dispatch(*sys, dtype, md, cfg->mode, &A, (int)iteration, guess, e0, e1, e2, e3, u, d_stats, st);
+  }
+  if (e == cudaErrorNotSupported) return fail(CS_ERR_CONFIG, "element builder not instantiated for this system/mode");
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements_range");
+}
+
 static int do_scan_update(int var, int dtype, const void *e0, const void *e1, const void *e2, const void *e3,
                           const void *u, const void *s0, void *out, int64_t T, int D, void *ws, size_t ws_bytes,
                           const void *guess, double atol, double rtol, int it, int32_t *last_fail,

@@ -131,7 +131,7 @@ k_sys_elements(SolveArgs<ST> A, int iteration, const ST *guess, ST *e0, ST *e1, 
   long long bp = kNoStep, bf = kNoStep, bj = kNoStep;
   unsigned pf = 0;
   if (r < A.T) {
-    const int64_t t = r + 1;
+    const int64_t t = A.t0 + r + 1;
     double prev[MD], gr[MD];
     load_row_ro<Sys, MD, ST>(sys, r == 0 ? A.s0 : guess + (r - 1) * D, prev);
     load_row_ro<Sys, MD, ST>(sys, guess + r * D, gr);

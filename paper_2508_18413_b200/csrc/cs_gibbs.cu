@@ -43,7 +43,7 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
   const int64_t r = ((int64_t)blockIdx.x * 256 + threadIdx.x) >> 3;
   const bool valid = r < A.T;
   const int64_t rr = valid ? r : 0;
-  const int64_t t = rr + 1;
+  const int64_t t = A.t0 + rr + 1;
   const ST *prow = rr == 0 ? A.s0 : guess + (rr - 1) * D;
   const ST *grow = guess + rr * D;
   const ST *g_tau = (const ST *)A.sys.g_tau, *xi_mu = (const ST *)A.sys.xi_mu;

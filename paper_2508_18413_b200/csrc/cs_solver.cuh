@@ -65,6 +65,7 @@ struct SolveArgs {
   int probe_n;
   int64_t T;
   int D, seg, nblocks;
+  int64_t t0;  // element builders: rows are steps t0+1 .. t0+T (a T shard); 0 elsewhere
 };
 
 // ---------------------------------------------------------------------------

@@ -190,10 +190,26 @@ def _gather(vec: torch.Tensor, group, world):
     return torch.stack(out)
 
 
+def _streamed_shard_ok(system, cfg) -> bool:
+    """Register-kernel systems: the shard runs the streamed engine's launches."""
+    if not (getattr(system, "desc", None) is not None and getattr(system, "kernels", False) and not cfg.full_trace
+            and getattr(system, "leapfrog_mode", "sequential") != "parallel"
+            and cfg.mode in ("diag-stochastic", "block2x2-stochastic", "dense")):
+        return False
+    from . import _lib
+    from .deer import _MODE_CODE
+
+    d = system.desc()
+    return bool(_lib.load().cs_system_elements_supported(ctypes.byref(d), _MODE_CODE[cfg.mode],
+                                                         _lib.dtype_code(system.dtype)))
+
+
 def run_deer_sharded(system, s0, cfg, ops: ShardOps | None = None, group=None, max_iters=None) -> ShardResult:
     """run_deer (deer.py:230-328) with T sharded over the process group."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if ops is None and _streamed_shard_ok(system, cfg) and (cfg.window_len is None or cfg.window_len >= system.T):
+        return _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters)
     ops = ops or CudaShardOps(system)
     dev = ops.device
     dtype = getattr(system, "dtype", torch.float64)
@@ -274,6 +290,156 @@ def run_deer_sharded(system, s0, cfg, ops: ShardOps | None = None, group=None, m
             break
     return ShardResult(trace=guess, iterations=it, delta_history=np.array(hist), converged=done,
                        per_step_converged_at=last_fail + 1, lo=lo, hi=hi, stats=stats)
+
+
+def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> ShardResult:
+    """The sharded iteration of run_deer_sharded with the streamed engine's kernels
+    on this rank's steps: ONE element launch for f, the finite/Picard checks and
+    the elements of steps lo+1..hi (cs_system_elements_range: noise and probes at
+    the absolute step, the halo row as the state before step lo+1), the shard
+    aggregate, the scan from the carry with the bookkeeping fused into its
+    replay -- and the same three small all-gathers and the same error/stop order
+    as the general loop above (deer.py:261-286)."""
+    from . import _lib
+    from .deer import _MODE_CODE, _STATS_BYTES, _parse_stats, _pre_tensor, default_max_iters
+
+    lib = _lib.load()
+    dev, dtype = system.device, system.dtype
+    T, D = system.T, system.dim
+    lo, hi = shard_bounds(T, world, rank)
+    n = hi - lo
+    if n < 1:
+        raise StructuralError(f"T={T} too short for {world} shards")
+    max_iters = cfg.max_iters if cfg.max_iters is not None else (max_iters or default_max_iters(T))
+    dt = _lib.dtype_code(dtype)
+    st = _lib.stream_ptr()
+    d = system.desc()
+    c = _lib.cs_deer_config()
+    c.mode = _MODE_CODE[cfg.mode]
+    c.atol, c.rtol = float(cfg.atol), float(cfg.rtol)
+    c.max_iters = int(max_iters)
+    c.hutchinson_samples = int(cfg.hutchinson_samples)
+    c.damping, c.clip = float(cfg.damping), float(cfg.clip)
+    pre = _pre_tensor(cfg, dev)
+    c.preconditioner = 0 if pre is None else pre.data_ptr()
+    mode = cfg.mode
+    half = D // 2 if mode == "block2x2-stochastic" else D
+    if mode == "diag-stochastic":
+        E = [torch.empty((n, D), dtype=dtype, device=dev)]
+    elif mode == "dense":
+        E = [torch.empty((n, D, D), dtype=dtype, device=dev)]
+    else:
+        E = [torch.empty((n, half), dtype=dtype, device=dev) for _ in range(4)]
+    u = torch.empty((n, D), dtype=dtype, device=dev)
+    eptr = [_lib.ptr(x) for x in E] + [_lib.ptr(None)] * (4 - len(E))
+    ws_bytes = lib.cs_scan_workspace_bytes(c.mode, dt, n, half)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    stats = torch.zeros(_STATS_BYTES, dtype=torch.uint8, device=dev)
+    sptr = _lib.ptr(stats)
+    W = agg_width(mode, D)
+    agg = torch.empty(W, dtype=torch.float64, device=dev)
+    s0 = torch.as_tensor(s0, dtype=dtype, device=dev).reshape(D).contiguous()
+    np_s0 = s0.to(torch.float64).cpu()
+    guess = s0.expand(n, -1).clone()
+    nxt = torch.empty_like(guess)
+    halo = s0.clone()
+    last_fail = torch.zeros(n, dtype=torch.int32, device=dev)
+    hist, d0, it, done = [], None, 0, False
+    use_dist = dist.is_initialized()
+    stats_info = {"path": "sharded-streamed", "world": world, "rows": (lo, hi), "collectives_per_iteration": 3}
+    vB = torch.empty(W + 1, dtype=torch.float64, device=dev)
+    vC = torch.empty(2 + D, dtype=torch.float64, device=dev)
+
+    def exchange(vec):  # all-gather a small device vector -> (world, len) on the host, one sync
+        return _gather(vec, group, world).cpu().numpy()
+
+    while True:
+        rc = lib.cs_system_elements_range(ctypes.byref(d), ctypes.byref(c), dt, it, lo, n, _lib.ptr(halo),
+                                          _lib.ptr(guess), *eptr, _lib.ptr(u), sptr, st)
+        _lib.check(rc)
+        bad_prop, bad_f, bad_j, picard, _, _ = _parse_stats(stats)
+        if use_dist:
+            gA = exchange(torch.tensor([float(bad_prop), float(bad_f), float(picard)], dtype=torch.float64,
+                                       device=dev))
+        else:
+            gA = np.array([[float(bad_prop), float(bad_f), float(picard)]])
+        gbp, gbf, gpf = float(gA[:, 0].min()), float(gA[:, 1].min()), float(gA[:, 2].sum())
+        if gbp < _NO_STEP:
+            raise ChainDivergedError(f"non-finite {getattr(system, '_what', 'proposal')} at step {int(gbp)}",
+                                     step=int(gbp))
+        if gbf < _NO_STEP:
+            raise ChainDivergedError(f"non-finite step value at step {int(gbf)} (iteration {it + 1})",
+                                     step=int(gbf), iteration=it + 1)
+        if gpf == 0:
+            done = True
+            break
+        if it >= max_iters:
+            break
+        if world > 1:  # only ranks above this one need its aggregate
+            if bad_j >= 2 ** 62:  # the stats' "none" is INT64_MAX
+                rc = lib.cs_scan_aggregate(c.mode, dt, *eptr, _lib.ptr(u), n, half, _lib.ptr(agg), _lib.ptr(ws),
+                                           ws_bytes, st)
+                _lib.check(rc)
+            else:
+                agg.zero_()
+            vB[:W].copy_(agg)
+            vB[W].fill_(float(bad_j))
+            gB = exchange(vB)
+        else:
+            gB = np.zeros((1, W + 1))
+            gB[0, W] = float(bad_j)
+        gbj = float(gB[:, W].min())
+        if gbj < _NO_STEP:
+            raise ChainDivergedError(f"non-finite jacobian at step {int(gbj)} (iteration {it + 1})",
+                                     step=int(gbj), iteration=it + 1)
+        carry = torch.as_tensor(np_s0)
+        for q in range(rank):  # prefix fix-up, shard by shard (_scan_kernels.py:32-36)
+            carry = apply_agg(mode, torch.from_numpy(gB[q, :W]), carry)
+        carry = carry.to(device=dev, dtype=dtype).contiguous()
+        if mode == "diag-stochastic":
+            rc = lib.cs_scan_diag_update(dt, eptr[0], _lib.ptr(u), _lib.ptr(carry), _lib.ptr(nxt), n, D,
+                                         _lib.ptr(ws), ws_bytes, _lib.ptr(guess), c.atol, c.rtol, it + 1,
+                                         _lib.ptr(last_fail), sptr, st)
+        elif mode == "block2x2-stochastic":
+            rc = lib.cs_scan_block_update(dt, *eptr, _lib.ptr(u), _lib.ptr(carry), _lib.ptr(nxt), n, half,
+                                          _lib.ptr(ws), ws_bytes, _lib.ptr(guess), c.atol, c.rtol, it + 1,
+                                          _lib.ptr(last_fail), sptr, st)
+        else:
+            rc = lib.cs_scan_dense(dt, eptr[0], _lib.ptr(u), _lib.ptr(carry), _lib.ptr(nxt), n, D, _lib.ptr(ws),
+                                   ws_bytes, st)
+            _lib.check(rc)
+            base = stats.data_ptr()
+            rc = lib.cs_update_bookkeeping(dt, _lib.ptr(guess), _lib.ptr(nxt), n, D, c.atol, c.rtol, it + 1,
+                                           _lib.ptr(last_fail), ctypes.c_void_p(base + 28),
+                                           ctypes.c_void_p(base + 32), st)
+        _lib.check(rc)
+        it += 1
+        if use_dist:
+            vC[2:].copy_(nxt[-1])
+        _, _, _, _, nfail, dmax = _parse_stats(stats)
+        if use_dist:
+            vC[0].fill_(float(nfail))
+            vC[1].fill_(dmax)
+            gC = exchange(vC)
+        else:
+            gC = np.array([[float(nfail), dmax]])
+        tot_fail = float(gC[:, 0].sum())
+        dm = gC[:, 1]
+        dmax_g = float("nan") if bool(np.isnan(dm).any()) else float(dm.max())
+        hist.append(dmax_g)
+        guess, nxt = nxt, guess
+        if rank > 0:
+            halo = torch.as_tensor(gC[rank - 1, 2:], device=dev).to(dtype).contiguous()
+        if d0 is None:
+            d0 = dmax_g
+        if d0 > 0 and dmax_g > _GUARD * d0:
+            raise ChainDivergedError(f"fixed-point iteration diverging: delta_max {dmax_g:.3e} exceeds "
+                                     f"{_GUARD:.0e} x initial {d0:.3e}", iteration=it)
+        if tot_fail == 0:
+            done = True
+            break
+    return ShardResult(trace=guess, iterations=it, delta_history=np.array(hist), converged=done,
+                       per_step_converged_at=last_fail + 1, lo=lo, hi=hi, stats=stats_info)
 
 
 def gather_trace(res: ShardResult, T: int, group=None):

@@ -536,6 +536,78 @@ def test_sharded_driver_cuda_ops_single_rank(cuda_device, mode, kw):
     np.testing.assert_array_equal(np_(r.per_step_converged_at), np_(ref.per_step_converged_at))
 
 
+@pytest.mark.parametrize("which,mode", [("mala", "diag-stochastic"), ("mala", "dense"), ("hmc", "diag-stochastic"),
+                                        ("gibbs", "diag-stochastic"), ("leapfrog", "block2x2-stochastic")])
+def test_elements_range_equals_whole_chain_rows(cuda_device, which, mode):
+    # cs_system_elements_range (one rank's T shard): noise and probes at the
+    # absolute step, the halo row as the state before the shard -> bit-identical
+    # to rows lo..hi-1 of the whole chain's elements
+    import ctypes
+
+    from paper_2508_18413_b200 import _lib
+    from paper_2508_18413_b200.deer import _MODE_CODE, _STATS_BYTES, _parse_stats
+
+    if which == "mala":
+        k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.gaussian([1.0, -1.0], [[1.0, 0.0], [-0.6, 1.2]])), 0.4, seed=3, T=5000)
+        s0 = torch.zeros(2, dtype=torch.float64, device=cuda_device)
+    elif which == "hmc":
+        k = cs.HmcKernel(cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0)), 0.5, 8, seed=1, T=5000)
+        s0 = torch.zeros(2, dtype=torch.float64, device=cuda_device)
+    elif which == "gibbs":
+        k = cs.GibbsKernel(cs.generate_eight_schools(), seed=2, T=5000)
+        s0 = torch.as_tensor(k.initial_state(), device=cuda_device)
+    else:
+        k = cs.LeapfrogSystem(cs.model_logp_grad_hvp(cs.rosenbrock(b=0.1, scale2=1.0)), 0.1, 64, probe_seed=4)
+        s0 = torch.tensor([0.3, -0.2, 1.0, 0.5], dtype=torch.float64, device=cuda_device)
+    T, D = k.T, k.dim
+    guess = cs.sequential_evaluate(k, s0).contiguous()
+    lib = _lib.load()
+    d = k.desc()
+    c = _lib.cs_deer_config()
+    c.mode = _MODE_CODE[mode]
+    c.atol, c.rtol, c.max_iters, c.hutchinson_samples = 1e-4, 1e-3, 100, 3 if which == "gibbs" else 1
+    c.damping, c.clip, c.preconditioner = 1.0, float("inf"), 0
+    half = D // 2 if mode == "block2x2-stochastic" else D
+
+    def build(t0, n, prev, g):
+        if mode == "diag-stochastic":
+            E = [torch.empty((n, D), dtype=torch.float64, device=cuda_device)]
+        elif mode == "dense":
+            E = [torch.empty((n, D, D), dtype=torch.float64, device=cuda_device)]
+        else:
+            E = [torch.empty((n, half), dtype=torch.float64, device=cuda_device) for _ in range(4)]
+        u = torch.empty((n, D), dtype=torch.float64, device=cuda_device)
+        st = torch.zeros(_STATS_BYTES, dtype=torch.uint8, device=cuda_device)
+        ptrs = [_lib.ptr(x) for x in E] + [_lib.ptr(None)] * (4 - len(E))
+        rc = lib.cs_system_elements_range(ctypes.byref(d), ctypes.byref(c), _lib.dtype_code(torch.float64), 2, t0, n,
+                                          _lib.ptr(prev.contiguous()), _lib.ptr(g.contiguous()), *ptrs, _lib.ptr(u),
+                                          _lib.ptr(st), _lib.stream_ptr())
+        _lib.check(rc)
+        return [np_(x) for x in E] + [np_(u)], _parse_stats(st)
+
+    whole, _ = build(0, T, s0, guess)
+    for lo, hi in ((0, T // 3), (T // 3, 2 * T // 3 + 1), (T - 7, T)):
+        halo = s0 if lo == 0 else guess[lo - 1]
+        part, stats = build(lo, hi - lo, halo, guess[lo:hi])
+        for a, b in zip(part, whole):
+            np.testing.assert_array_equal(a, b[lo:hi])
+        assert stats[0] >= 2 ** 62 and stats[1] >= 2 ** 62  # no bad proposal / step inside the range
+
+
+def test_streamed_shard_path_matches_run_deer(cuda_device):
+    # the sharded driver's streamed-engine path (register systems) at world size 1
+    from paper_2508_18413_b200.sharded import run_deer_sharded
+
+    k = cs.GibbsKernel(cs.generate_eight_schools(), seed=0, T=20_000, dtype=torch.float32)
+    cfg = cs.DeerConfig(mode="diag-stochastic", hutchinson_samples=3, preconditioner=k.recommended_preconditioner())
+    ref = cs.run_deer(k, k.initial_state(), cfg)
+    r = run_deer_sharded(k, k.initial_state(), cfg)
+    assert r.stats["path"] == "sharded-streamed"
+    assert r.iterations == ref.iterations and r.converged == ref.converged
+    np.testing.assert_array_equal(np_(r.per_step_converged_at), np_(ref.per_step_converged_at))
+    np.testing.assert_allclose(np_(r.trace), np_(ref.trace), rtol=1e-5, atol=1e-5)
+
+
 @pytest.mark.parametrize("which", ["hmc_diag", "mala_dense12"])
 def test_sharded_driver_over_nccl_single_rank(cuda_device, which):
     # the multi-GPU driver's collectives on device tensors through NCCL (world
