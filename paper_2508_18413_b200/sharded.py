@@ -185,6 +185,8 @@ class CudaShardOps(ShardOps):
 
 
 def _gather(vec: torch.Tensor, group, world):
+    if vec.is_cuda and dist.get_backend(group) == "gloo":  # host-side groups (CPU tests) stage through host
+        vec = vec.cpu()
     out = [torch.empty_like(vec) for _ in range(world)]
     dist.all_gather(out, vec, group=group)
     return torch.stack(out)
