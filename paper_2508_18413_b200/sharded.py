@@ -359,11 +359,13 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
         rc = lib.cs_system_elements_range(ctypes.byref(d), ctypes.byref(c), dt, it, lo, n, _lib.ptr(halo),
                                           _lib.ptr(guess), *eptr, _lib.ptr(u), sptr, st)
         _lib.check(rc)
-        bad_prop, bad_f, bad_j, picard, _, _ = _parse_stats(stats)
-        if use_dist:
-            gA = exchange(torch.tensor([float(bad_prop), float(bad_f), float(picard)], dtype=torch.float64,
-                                       device=dev))
+        if use_dist:  # the stats go into the all-gather on the device: one host sync for both
+            i64 = stats[:24].view(torch.int64)
+            vA = torch.cat([i64[:2].double(), stats[24:28].view(torch.int32).double(), i64[2:3].double()])
+            gA = exchange(vA)
+            bad_j = int(gA[rank, 3]) if gA[rank, 3] < _NO_STEP else 2 ** 63 - 1
         else:
+            bad_prop, bad_f, bad_j, picard, _, _ = _parse_stats(stats)
             gA = np.array([[float(bad_prop), float(bad_f), float(picard)]])
         gbp, gbf, gpf = float(gA[:, 0].min()), float(gA[:, 1].min()), float(gA[:, 2].sum())
         if gbp < _NO_STEP:
@@ -417,13 +419,12 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
         _lib.check(rc)
         it += 1
         if use_dist:
+            vC[0:1].copy_(stats[28:32].view(torch.int32).double())
+            vC[1:2].copy_(stats[32:40].view(torch.float64))
             vC[2:].copy_(nxt[-1])
-        _, _, _, _, nfail, dmax = _parse_stats(stats)
-        if use_dist:
-            vC[0].fill_(float(nfail))
-            vC[1].fill_(dmax)
             gC = exchange(vC)
         else:
+            _, _, _, _, nfail, dmax = _parse_stats(stats)
             gC = np.array([[float(nfail), dmax]])
         tot_fail = float(gC[:, 0].sum())
         dm = gC[:, 1]
