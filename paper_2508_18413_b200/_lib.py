@@ -136,7 +136,9 @@ def _load_path(path):
     global _lib
     lib = ctypes.CDLL(path)
     for name, (args, res) in _SIGS.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)  # an older variant may predate an entry point
+        if fn is None:
+            continue
         fn.argtypes = args
         fn.restype = res
     _lib = lib

@@ -1,7 +1,6 @@
-# bench + scan probes + one ncu capture of the 2^24 diag row scan
-timeout 300 python bench.py > gpurun_out/bench7.json 2> gpurun_out/bench7.err; echo bench=$?
-for m in diag block; do timeout 120 python tools/probe_scan.py --mode $m --T 4194304 --D 18 --reps 20 2>&1 | tail -1; done
-timeout 120 python tools/probe_scan.py --mode diag --T 16777216 --D 18 --reps 20 2>&1 | tail -1
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "scan" 2>&1 | tail -1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:scan_rows -s 2 -c 1 -o gpurun_out/scan24 -f \
-  python tools/probe_scan.py --mode diag --T 16777216 --D 18 --reps 2 > gpurun_out/ncu24.log 2>&1; echo ncu=$?
+# round-end check: GPU suite, smoke, bench, the BASELINE config table, bench launch list
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 300 python bench.py > gpurun_out/bench12.json 2> gpurun_out/bench12.err; echo bench=$?
+timeout 900 python tools/bench_configs.py 1 1r 2 3 3d 4 5 2>&1 | grep config | cut -c1-200
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r01_final.csv python bench.py --steps 2 --warmup 1 --no-extras > gpurun_out/ncu_final.log 2>&1; echo ncu=$?
