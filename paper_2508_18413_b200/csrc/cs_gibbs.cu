@@ -10,12 +10,16 @@ namespace cs {
 // -- the same pairwise order numpy uses for 8 terms.  Each lane holds one
 // school's state, so 8x more threads carry the f64 dependency chains than in the
 // one-thread-per-step kernel, at a fraction of the registers.
-CS_D double team_sum(double v) {
+template <typename V>
+CS_D V team_sum(V v) {
   v += __shfl_xor_sync(0xffffffffu, v, 1);
   v += __shfl_xor_sync(0xffffffffu, v, 2);
   v += __shfl_xor_sync(0xffffffffu, v, 4);
   return v;
 }
+#ifndef CS_GIBBS_TT_SUMS  // tangent team sums + probe shuffles in the tangent type (fp32: 89.3 -> 87 ms at cfg 5, same 135 iterations)
+#define CS_GIBBS_TT_SUMS 1
+#endif
 
 // fp32 storage: compiled for 4 resident CTAs per SM (64 registers, 4 B of
 // spill): cfg 5 T = 1M 92.8 -> 88.8 ms against the unconstrained 80-register
@@ -109,14 +113,19 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
   TT e_tau = 0, e_mu = 0, e_th = 0, e_sg = 0;
   for (int k = 0; k < A.nsamp; ++k) {
     // z_tau / z_mu are shared by the team: lanes 0 and 1 hash them
-    const double zs = probe_sign(h3, k, sub == 0 ? 0 : (sub == 1 ? 1 : 2 + sub));
+#if CS_GIBBS_TT_SUMS
+    using SU = TT;
+#else
+    using SU = double;
+#endif
+    const SU zs = (SU)probe_sign(h3, k, sub == 0 ? 0 : (sub == 1 ? 1 : 2 + sub));
     const TT z_tau = (TT)__shfl_sync(0xffffffffu, zs, (threadIdx.x & 31) & ~7);
     const TT z_mu = (TT)__shfl_sync(0xffffffffu, zs, ((threadIdx.x & 31) & ~7) + 1);
     const TT z_th = (TT)probe_sign(h3, k, 2 + sub), z_sg = (TT)probe_sign(h3, k, 2 + S + sub);
     const TT dsg = raw_ok ? z_sg : (TT)0;
-    const TT dq = mu_c * z_mu + (TT)team_sum((double)(two_dm * (z_th - z_mu)));
+    const TT dq = mu_c * z_mu + (TT)team_sum((SU)(two_dm * (z_th - z_mu)));
     const TT dtau2 = dq * inv_gt;
-    const TT dmu = (TT)team_sum((double)z_th) * inv_kS + c_mu * dtau2;
+    const TT dmu = (TT)team_sum((SU)z_th) * inv_kS + c_mu * dtau2;
     const TT dprec = -dtau2 * inv_t2sq - n_sg2 * dsg;
     const TT damean = (dmu * inv_tau2n - mun_t * dtau2 * inv_t2sq) - xbar_t * n_sg2 * dsg;
     const TT dmean = (damean - mean_t * dprec) * inv_prec;

@@ -14,5 +14,6 @@ build() {
   $NVCC -gencode arch=compute_100a,code=sm_100a -shared -o $d/libchainscan_b200.so $OBJS $d/cs_gibbs.o -cudart static -lcublas -Xlinker -rpath=/usr/local/cuda/lib64
   echo built $name
 }
-for m in 3 4 5 6; do build gibbs_m$m -DCS_GIBBS_MINB=$m & done
+build gibbs_m4 -DCS_GIBBS_MINB=4 &
+build gibbs_m4_tt -DCS_GIBBS_MINB=4 -DCS_GIBBS_TT_SUMS=1 &
 wait
