@@ -276,7 +276,8 @@ def run_gpu(args):
                            "l2": "flushed (256 MiB write) between timed steps",
                            "solver": res.stats},
                 "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
-                        "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps},
+                        "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps,
+                        "gpu_launches": args.steps * int(res.stats.get("launches", 3))},
                 "gpu_launches": args.steps * int(res.stats.get("launches", 3)),
                 "roofline": roof, "scan_roofline": scan_roof, "cpu_baseline": cpu_base,
                 **({"t_sharded": shard} if shard is not None else {}),
