@@ -341,7 +341,6 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
     W = agg_width(mode, D)
     agg = torch.empty(W, dtype=torch.float64, device=dev)
     s0 = torch.as_tensor(s0, dtype=dtype, device=dev).reshape(D).contiguous()
-    np_s0 = s0.to(torch.float64).cpu()
     guess = s0.expand(n, -1).clone()
     nxt = torch.empty_like(guess)
     halo = s0.clone()
@@ -352,21 +351,26 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
     vB = torch.empty(W + 1, dtype=torch.float64, device=dev)
     vC = torch.empty(2 + D, dtype=torch.float64, device=dev)
 
-    def exchange(vec):  # all-gather a small device vector -> (world, len) on the host, one sync
-        return _gather(vec, group, world).cpu().numpy()
+    def build(it_, halo_):
+        rc_ = lib.cs_system_elements_range(ctypes.byref(d), ctypes.byref(c), dt, it_, lo, n, _lib.ptr(halo_),
+                                           _lib.ptr(guess), *eptr, _lib.ptr(u), sptr, st)
+        _lib.check(rc_)
 
+    def flags_dev():  # [bad_prop, bad_f, picard_fail, bad_jac] from the stats words, on the device
+        i64 = stats[:24].view(torch.int64)
+        return torch.cat([i64[:2].double(), stats[24:28].view(torch.int32).double(), i64[2:3].double()])
+
+    # With a process group, one host read per iteration: the next iteration's
+    # elements are built speculatively from the device-side halo while the
+    # convergence exchange is in flight, and both gathered vectors come back
+    # together (the speculative build is discarded when the chain stops).
+    build(0, halo)
+    if use_dist:
+        gA = _gather(flags_dev(), group, world).cpu().numpy()
+    else:
+        bp, bf, bj, pc, _, _ = _parse_stats(stats)
+        gA = np.array([[float(bp), float(bf), float(pc), float(bj)]])
     while True:
-        rc = lib.cs_system_elements_range(ctypes.byref(d), ctypes.byref(c), dt, it, lo, n, _lib.ptr(halo),
-                                          _lib.ptr(guess), *eptr, _lib.ptr(u), sptr, st)
-        _lib.check(rc)
-        if use_dist:  # the stats go into the all-gather on the device: one host sync for both
-            i64 = stats[:24].view(torch.int64)
-            vA = torch.cat([i64[:2].double(), stats[24:28].view(torch.int32).double(), i64[2:3].double()])
-            gA = exchange(vA)
-            bad_j = int(gA[rank, 3]) if gA[rank, 3] < _NO_STEP else 2 ** 63 - 1
-        else:
-            bad_prop, bad_f, bad_j, picard, _, _ = _parse_stats(stats)
-            gA = np.array([[float(bad_prop), float(bad_f), float(picard)]])
         gbp, gbf, gpf = float(gA[:, 0].min()), float(gA[:, 1].min()), float(gA[:, 2].sum())
         if gbp < _NO_STEP:
             raise ChainDivergedError(f"non-finite {getattr(system, '_what', 'proposal')} at step {int(gbp)}",
@@ -379,27 +383,23 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
             break
         if it >= max_iters:
             break
-        if world > 1:  # only ranks above this one need its aggregate
-            if bad_j >= 2 ** 62:  # the stats' "none" is INT64_MAX
-                rc = lib.cs_scan_aggregate(c.mode, dt, *eptr, _lib.ptr(u), n, half, _lib.ptr(agg), _lib.ptr(ws),
-                                           ws_bytes, st)
-                _lib.check(rc)
-            else:
-                agg.zero_()
-            vB[:W].copy_(agg)
-            vB[W].fill_(float(bad_j))
-            gB = exchange(vB)
-        else:
-            gB = np.zeros((1, W + 1))
-            gB[0, W] = float(bad_j)
-        gbj = float(gB[:, W].min())
+        gbj = float(gA[:, 3].min())
         if gbj < _NO_STEP:
             raise ChainDivergedError(f"non-finite jacobian at step {int(gbj)} (iteration {it + 1})",
                                      step=int(gbj), iteration=it + 1)
-        carry = torch.as_tensor(np_s0)
-        for q in range(rank):  # prefix fix-up, shard by shard (_scan_kernels.py:32-36)
-            carry = apply_agg(mode, torch.from_numpy(gB[q, :W]), carry)
-        carry = carry.to(device=dev, dtype=dtype).contiguous()
+        if world > 1:  # shard aggregates -> carry, on the device (only lower ranks' maps are used)
+            rc = lib.cs_scan_aggregate(c.mode, dt, *eptr, _lib.ptr(u), n, half, _lib.ptr(agg), _lib.ptr(ws),
+                                       ws_bytes, st)
+            _lib.check(rc)
+            vB[:W].copy_(agg)
+            vB[W].fill_(0.0)
+            gB = _gather(vB, group, world).to(dev)
+            carry = s0.to(torch.float64)
+            for q in range(rank):  # prefix fix-up, shard by shard (_scan_kernels.py:32-36)
+                carry = apply_agg(mode, gB[q, :W], carry)
+            carry = carry.to(dtype).contiguous()
+        else:
+            carry = s0
         if mode == "diag-stochastic":
             rc = lib.cs_scan_diag_update(dt, eptr[0], _lib.ptr(u), _lib.ptr(carry), _lib.ptr(nxt), n, D,
                                          _lib.ptr(ws), ws_bytes, _lib.ptr(guess), c.atol, c.rtol, it + 1,
@@ -418,11 +418,19 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
                                            ctypes.c_void_p(base + 32), st)
         _lib.check(rc)
         it += 1
+        guess, nxt = nxt, guess
         if use_dist:
             vC[0:1].copy_(stats[28:32].view(torch.int32).double())
             vC[1:2].copy_(stats[32:40].view(torch.float64))
-            vC[2:].copy_(nxt[-1])
-            gC = exchange(vC)
+            vC[2:].copy_(guess[-1])
+            gC_dev = _gather(vC, group, world).to(dev)
+            if rank > 0:
+                halo = gC_dev[rank - 1, 2:].to(dtype).contiguous()
+            build(it, halo)  # speculative: the next iteration's elements
+            gA_dev = _gather(flags_dev(), group, world).to(dev)
+            both = torch.cat([gC_dev[:, :2].reshape(-1), gA_dev.reshape(-1)]).cpu().numpy()
+            gC = both[:2 * world].reshape(world, 2)
+            gA = both[2 * world:].reshape(world, 4)
         else:
             _, _, _, _, nfail, dmax = _parse_stats(stats)
             gC = np.array([[float(nfail), dmax]])
@@ -430,9 +438,6 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
         dm = gC[:, 1]
         dmax_g = float("nan") if bool(np.isnan(dm).any()) else float(dm.max())
         hist.append(dmax_g)
-        guess, nxt = nxt, guess
-        if rank > 0:
-            halo = torch.as_tensor(gC[rank - 1, 2:], device=dev).to(dtype).contiguous()
         if d0 is None:
             d0 = dmax_g
         if d0 > 0 and dmax_g > _GUARD * d0:
@@ -441,6 +446,10 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
         if tot_fail == 0:
             done = True
             break
+        if not use_dist:
+            build(it, halo)
+            bp, bf, bj, pc, _, _ = _parse_stats(stats)
+            gA = np.array([[float(bp), float(bf), float(pc), float(bj)]])
     return ShardResult(trace=guess, iterations=it, delta_history=np.array(hist), converged=done,
                        per_step_converged_at=last_fail + 1, lo=lo, hi=hi, stats=stats_info)
 
