@@ -30,7 +30,16 @@ def _system(name):
         k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.gaussian([1.0, -1.0], [[1.0, 0.0], [-0.6, 1.2]])), 0.4,
                           seed=0, T=2001)
         return k, np.zeros(2), cs.DeerConfig(mode="dense")
+    if name == "explode":  # plain diag quasi-Newton diverges on this chain (clip=1 is what tames it)
+        m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
+        return cs.HmcKernel(m, 0.5, 8, seed=0, T=3001), np.zeros(2), cs.DeerConfig(mode="diag-stochastic")
     raise KeyError(name)
+
+
+def cs_errors():
+    import paper_2508_18413_b200 as cs
+
+    return cs
 
 
 def _worker(rank, world, port, name, q):
@@ -42,7 +51,11 @@ def _worker(rank, world, port, name, q):
         from paper_2508_18413_b200.sharded import gather_trace, run_deer_sharded
 
         k, s0, cfg = _system(name)
-        r = run_deer_sharded(k, s0, cfg)
+        try:
+            r = run_deer_sharded(k, s0, cfg)
+        except cs_errors().ChainDivergedError as e:
+            q.put((rank, "diverged", e.step, e.iteration))
+            return
         full = gather_trace(type(r)(trace=r.trace.cpu(), iterations=0, delta_history=None, converged=True,
                                     per_step_converged_at=None), k.T)
         psca = gather_trace(type(r)(trace=r.per_step_converged_at[:, None].to(torch.float64).cpu(), iterations=0,
@@ -79,3 +92,30 @@ def test_two_rank_streamed_shards_match_run_deer(cuda_device, name):
             np.testing.assert_allclose(full, want, atol=1e-8, rtol=1e-8)
         else:  # one more or fewer update: both within the solve's own envelope
             assert np.all(np.abs(full - want) <= 1e-4 + 1e-3 * np.abs(want))
+
+
+def test_two_rank_streamed_shards_agree_on_divergence(cuda_device):
+    import paper_2508_18413_b200 as cs
+
+    k, s0, cfg = _system("explode")
+    with pytest.raises(cs.ChainDivergedError) as ref:
+        cs.run_deer(k, s0, cfg)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, "explode", q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=600) for _ in range(2)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    # every rank raises the same error; its step / iteration match the
+    # single-process solve up to the +-1 iteration the chunk layout allows
+    assert all(o[1] == "diverged" for o in out), out
+    assert out[0][2:] == out[1][2:], out
+    if ref.value.step is not None:
+        assert out[0][2] == ref.value.step, (out, ref.value.step)
+    if ref.value.iteration is not None:
+        assert abs(out[0][3] - ref.value.iteration) <= 1, (out, ref.value.iteration)
