@@ -54,10 +54,30 @@ def peaks():
 POLL_S = float(os.environ.get("CS_BENCH_POLL_MS", "5")) / 1e3
 
 
+_POLLER = r"""
+import json, sys, time
+import pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+period = float(sys.argv[2])
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+sys.stdout.write("ready\n"); sys.stdout.flush()
+import select
+samples, bits = [], 0
+while not select.select([sys.stdin], [], [], period)[0]:
+    try:
+        samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+        bits |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    except Exception:
+        pass
+sys.stdout.write(json.dumps({"samples": samples, "bits": bits, "max": mx}) + "\n"); sys.stdout.flush()
+"""
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled (NVML, every POLL_S) during the timed
-    region.  NVML calls take driver locks, so a 1 kHz poller measurably delays the
-    solve's launches and read-back; 5 ms still yields ~10 samples per leg."""
+    region, by a child process: a poller thread in this process competes for the
+    GIL with the solve's host path (measured: 0.43 -> 0.57 ms per headline step)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
@@ -67,47 +87,38 @@ class ClockSampler:
         self.samples = []
         self.reasons = set()
         self.max_mhz = None
-        self._stop = None
+        self._p = None
 
     def __enter__(self):
-        import threading
+        import subprocess
 
         try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[self.gpu].strip().isdigit() else self.gpu
+            self._p = subprocess.Popen([sys.executable, "-c", _POLLER, str(idx), str(POLL_S)], stdin=subprocess.PIPE,
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            if self._p.stdout.readline().strip() != "ready":
+                self._p = None
         except Exception:
-            return self
-        self._stop = threading.Event()
-
-        def poll():
-            while not self._stop.is_set():
-                try:
-                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
-                    bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    for name, bit in self.REASONS.items():
-                        if bits & bit:
-                            self.reasons.add(name)
-                except Exception:
-                    pass
-                time.sleep(POLL_S)
-
-        self._t = threading.Thread(target=poll, daemon=True)
-        self._t.start()
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        if self._stop is not None:
-            self._stop.set()
-            self._t.join()
+        if self._p is None:
+            return
+        try:
+            out, _ = self._p.communicate("stop\n", timeout=30)
+            r = json.loads(out.strip().splitlines()[-1])
+            self.samples, self.max_mhz = r["samples"], r["max"]
+            self.reasons = {n for n, b in self.REASONS.items() if r["bits"] & b}
+        except Exception:
+            self._p.kill()
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
         return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "sampler": "child process (NVML)"}
 
 
 def dist_env():
