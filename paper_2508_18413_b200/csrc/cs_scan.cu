@@ -602,11 +602,11 @@ struct RowsGeom {
   int R, CS, G, j;
   int L;  // rounds between a chunk's A pass and its C pass
   bool agg_only;
-  int64_t nstages;  // ceil(T / R), so stages_in needs no division
-  CS_D int stages_in(int64_t q) const {
-    const int64_t st = nstages - q * CS;
-    return (int)(st < CS ? st : CS);
-  }
+  int64_t nstages;  // ceil(T / R)
+  // balanced partition: chunk q covers stages [c0(q), c0(q+1)), at most CS of
+  // them, so the last round of the grid is as full as the others
+  CS_D int64_t c0(int64_t q) const { return q * nstages / nchunks; }
+  CS_D int stages_in(int64_t q) const { return (int)(c0(q + 1) - c0(q)); }
   CS_D void settle(RowsJob &it) const {
     while (it.r < nr + L) {
       const int64_t rr = it.ph == 0 ? it.r : it.r - L;
@@ -785,7 +785,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
   constexpr int NA = VAR == SCAN_DIAG ? 2 : 6;
   // issue one stage's loads (this thread's KR rows of its column) into ev
   auto load_stage = [&](const RowsJob &job, CT (&ev)[NA][KR]) {
-    const int64_t row0 = (job.q * CS + job.s) * R;
+    const int64_t row0 = (geo.c0(job.q) + job.s) * R;
     const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
     const uint64_t pol = job.ph == 0 ? pol_a : pol_c;
     const int r0 = sg * KR, r1 = min(rows, r0 + KR);
@@ -826,7 +826,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
   // already in flight in the other register set)
   auto body = [&](const RowsJob &cur, int64_t n, const CT (&ev)[NA][KR]) {
     const int64_t q = cur.q;
-    const int64_t stg = q * CS + cur.s;
+    const int64_t stg = geo.c0(q) + cur.s;
     const int64_t row0 = stg * R;
     const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
     double *s_chunk = s_chunk2 + (LBW ? (ka & 1) * 64 * W : 0);
@@ -1617,6 +1617,13 @@ static int env_int(const char *name, int lo, int hi, int dflt) {
 }
 // cap on stages per chunk (measured, tools/sweep_scan.sh): diag 16 (T = 4M: 2.51
 // TB/s vs 2.27 at 32), block2x2 32 (T = 4M D = 18: 2.56 vs 2.38 at 16)
+static bool rows_balanced() {  // CS_SCAN_BALANCED=0: uniform chunks with a partial last round (A/B experiments)
+  static const bool v = [] {
+    const char *e = getenv("CS_SCAN_BALANCED");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
 static int rows_chunk_stages(int var) {
   static const int v = env_int("CS_SCAN_CHUNK_STAGES", 1, 256, 0);  // tuning override for experiments
   return v ? v : var == SCAN_BLOCK ? 32 : 16;
@@ -1708,6 +1715,17 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update) {
       p.seg = (int)cs;
     }
     p.ntiles = (T + (int64_t)p.R * p.seg - 1) / ((int64_t)p.R * p.seg);  // chunks
+    {
+      // round the chunk count up to whole rounds of the grid (chunks then hold
+      // seg or seg-1 stages): a partial last round leaves most CTAs idle while
+      // the rest finish it (T = 16M diag: 10.5 rounds -> 11 full ones)
+      const int64_t nst = (T + p.R - 1) / p.R;
+      const int64_t g = (int64_t)rows_resident_ctas(minb);
+      if (rows_balanced() && p.ntiles > g) {
+        const int64_t nb = (p.ntiles + g - 1) / g * g;
+        if (nb <= nst) p.ntiles = nb;
+      }
+    }
     p.agg_w = D * (var == SCAN_DIAG ? 2 : 6);
     p.state_w = var == SCAN_DIAG ? D : 2 * D;
     const int esz = dtype == CS_F64 ? 8 : 4;
