@@ -1626,7 +1626,12 @@ static bool rows_balanced() {  // CS_SCAN_BALANCED=0: uniform chunks with a part
 }
 static int rows_chunk_stages(int var) {
   static const int v = env_int("CS_SCAN_CHUNK_STAGES", 1, 256, 0);  // tuning override for experiments
-  return v ? v : var == SCAN_BLOCK ? 32 : 16;
+  // with whole rounds (rows_balanced) the >= 2-rounds rule sets the chunk length
+  // at every T that fills the grid; the cap only binds at very long chains
+  // (tools/sweep_chunk_stages.sh, T = 16M D = 18: diag 16 -> 64+ stages 2.85 -> 3.08 TB/s,
+  // block2x2 32 -> 128 2.53 -> 2.66)
+  (void)var;
+  return v ? v : 128;
 }
 static int rows_resident_ctas(int minb) {  // persistent grid of scan_rows (launch bounds: minb CTAs per SM)
   static const int sms = [] {
