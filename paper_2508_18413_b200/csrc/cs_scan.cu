@@ -672,6 +672,24 @@ CS_D T ld_hint(const T *p, uint64_t pol) {
     return v;
   }
 }
+// 16-byte variant for the small-D diag scan's coalesced stage loads
+CS_D float4 ld_hint_v4(const float *p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+// small-D diag (D | 256, D <= 4, fp32): each thread owns KR rows of one column, so a
+// warp's per-row loads touch 32 / D rows KR rows apart (D = 2: 8 useful bytes per
+// 32-byte sector per request, LSU-bound).  Instead the CTA loads the stage block
+// with coalesced 16-byte loads and redistributes it through shared memory
+// (segments padded by 4 floats: 16-byte stores, <= 2-way read conflicts).
+template <typename ST, int VAR, bool UPDATE, bool LBW>
+struct RowsTx {
+  static constexpr bool kOn = sizeof(ST) == 4 && VAR == SCAN_DIAG && !UPDATE && !LBW && !CS_ROWS_PREFETCH;
+};
+CS_HD bool rows_tx_dim(int D) { return D == 1 || D == 2 || D == 4; }
 
 template <typename ST, int VAR, bool AGG_ONLY = false, bool UPDATE = false, bool LBW = false>
 __global__ void __launch_bounds__(kScanThreads + (LBW ? 64 : 0),
@@ -709,6 +727,12 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
   int *s_fail = (int *)(segagg + 2 * (nseg + 1) * ncol * W);  // UPDATE: one flag per stage row
   // LBW: look-back staging buffer and the two-slot entry hand-off
   double *lb_stage = (double *)(((uintptr_t)(s_fail + R) + 15) & ~(uintptr_t)15);
+  // small-D transposition buffer (same spot as lb_stage: the two never coexist)
+  float *txb = (float *)lb_stage;
+  constexpr bool kTx = RowsTx<ST, VAR, UPDATE, LBW>::kOn;
+  static_assert(!kTx || KR % 4 == 0, "coalesced stage loads move 4 rows' floats at a time");
+  const int txw = R * ncol + 4 * nseg;  // floats per array in txb
+  const bool tx = kTx && rows_tx_dim(ncol) && ((((uintptr_t)a.e0) | ((uintptr_t)a.u)) & 15) == 0;
   __shared__ double s_lbe[2 * 128];
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], s_aggfull[2], s_aggempty[2];
   double *pub_stage = lb_stage + kLbwStage;  // kLbwPubStage doubles
@@ -789,6 +813,29 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
     const int rows = (int)(a.T - row0 < (int64_t)R ? a.T - row0 : (int64_t)R);
     const uint64_t pol = job.ph == 0 ? pol_a : pol_c;
     const int r0 = sg * KR, r1 = min(rows, r0 + KR);
+    if constexpr (kTx) {
+      if (tx) {  // ev[.][4m + e] <- float 4 * (tid + m * 256) + e of the stage block
+        const int nv = rows * ncol;
+        const float *b0 = (const float *)a.e0 + row0 * ncol, *bu = (const float *)a.u + row0 * ncol;
+#pragma unroll
+        for (int m = 0; m < KR / 4; ++m) {
+          const int f = 4 * (tid + m * kScanThreads);
+          float4 x0, xu;
+          if (f + 4 <= nv) {
+            x0 = ld_hint_v4(b0 + f, pol);
+            xu = ld_hint_v4(bu + f, pol);
+          } else {  // ragged last stage: identity past the end
+            x0.x = f + 0 < nv ? ld_hint(b0 + f + 0, pol) : 1.f; xu.x = f + 0 < nv ? ld_hint(bu + f + 0, pol) : 0.f;
+            x0.y = f + 1 < nv ? ld_hint(b0 + f + 1, pol) : 1.f; xu.y = f + 1 < nv ? ld_hint(bu + f + 1, pol) : 0.f;
+            x0.z = f + 2 < nv ? ld_hint(b0 + f + 2, pol) : 1.f; xu.z = f + 2 < nv ? ld_hint(bu + f + 2, pol) : 0.f;
+            x0.w = f + 3 < nv ? ld_hint(b0 + f + 3, pol) : 1.f; xu.w = f + 3 < nv ? ld_hint(bu + f + 3, pol) : 0.f;
+          }
+          ev[0][4 * m + 0] = (CT)x0.x; ev[0][4 * m + 1] = (CT)x0.y; ev[0][4 * m + 2] = (CT)x0.z; ev[0][4 * m + 3] = (CT)x0.w;
+          ev[1][4 * m + 0] = (CT)xu.x; ev[1][4 * m + 1] = (CT)xu.y; ev[1][4 * m + 2] = (CT)xu.z; ev[1][4 * m + 3] = (CT)xu.w;
+        }
+        return;
+      }
+    }
     if (!active) return;
     // per-stage 64-bit bases, 32-bit offsets inside the stage
     const int64_t g0 = row0 * ncol;
@@ -1078,6 +1125,26 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
   int64_t n = 0;
   for (RowsJob cur = geo.first(); geo.valid(cur); geo.next(cur)) {
     load_stage(cur, ev);
+    if constexpr (kTx) {
+      if (tx) {  // flat (coalesced) order -> this thread's KR rows of column c
+        const int KD = KR * ncol;
+#pragma unroll
+        for (int m = 0; m < KR / 4; ++m) {
+          const int f = 4 * (tid + m * kScanThreads);
+          const int pf = f + 4 * (f / KD);  // segment pad: 4 floats
+          *(float4 *)(txb + pf) = make_float4(ev[0][4 * m], ev[0][4 * m + 1], ev[0][4 * m + 2], ev[0][4 * m + 3]);
+          *(float4 *)(txb + txw + pf) = make_float4(ev[1][4 * m], ev[1][4 * m + 1], ev[1][4 * m + 2], ev[1][4 * m + 3]);
+        }
+        __syncthreads();
+        const int base = sg * (KD + 4) + c;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          ev[0][k] = txb[base + k * ncol];
+          ev[1][k] = txb[txw + base + k * ncol];
+        }
+        __syncthreads();
+      }
+    }
     body(cur, n++, ev);
   }
 #endif
@@ -1741,6 +1808,8 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update) {
     if (rows_lbw()) {
       p.smem += 16 + sizeof(double) * (kLbwStage + kLbwPubStage);
     }
+    if (!rows_lbw() && !update && var == SCAN_DIAG && dtype == CS_F32 && rows_tx_dim(D))
+      p.smem += 16 + sizeof(float) * 2 * ((size_t)p.R * D + 4 * nseg);  // small-D transposition buffer
   } else {
     p.kind = 1;
     const int ncb = (D + 31) / 32;

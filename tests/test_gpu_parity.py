@@ -699,6 +699,31 @@ def test_row_scan_multi_round_vs_oracle(cuda_device, mode, D, T, dtype):
     np.testing.assert_allclose(got, want, atol=tol * 10, rtol=tol)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("D,T", [(1, 3_000_017), (2, 1_000_003), (4, 700_001), (2, 3071), (4, 5)])
+def test_small_d_row_scan_coalesced_path(cuda_device, D, T):
+    """Small-D fp32 diag scans load stages with 16-byte loads transposed through
+    shared memory when j and u are 16-byte aligned; a one-row storage offset takes
+    the per-column path.  Same per-segment arithmetic order: bit-identical."""
+    rng = np.random.default_rng(D * 1000 + T)
+    j = rng.uniform(-0.95, 0.95, (T + 1, D))
+    u = rng.normal(size=(T + 1, D))
+    s0 = rng.normal(size=D)
+    jt = torch.as_tensor(j, dtype=torch.float32, device=cuda_device)
+    ut = torch.as_tensor(u, dtype=torch.float32, device=cuda_device)
+    s0t = torch.as_tensor(s0, dtype=torch.float32, device=cuda_device)
+    aligned = cs.parallel_affine_solve(cs.DiagElements(jt[:T].clone(), ut[:T].clone()), s0t)
+    # one-float storage offset (misaligned for 16-byte loads at every D)
+    js, us = jt.reshape(-1)[1:1 + T * D].view(T, D), ut.reshape(-1)[1:1 + T * D].view(T, D)
+    assert js.data_ptr() % 16 != 0 and us.data_ptr() % 16 != 0
+    shifted = cs.parallel_affine_solve(cs.DiagElements(js, us), s0t)
+    ref_shift = cs.parallel_affine_solve(cs.DiagElements(js.clone(), us.clone()), s0t)
+    assert torch.equal(shifted, ref_shift)
+    want = O.parallel_affine_solve(O.DiagElements(j[:T].astype(np.float32).astype(np.float64),
+                                                  u[:T].astype(np.float32).astype(np.float64)), s0.astype(np.float32), workers=16)
+    np.testing.assert_allclose(np_(aligned), want, atol=2e-4, rtol=2e-5)
+
+
 def test_update_scan_bookkeeping_multi_round(cuda_device):
     # the replay's fused bookkeeping (deer.py:273-277) at a multi-round size:
     # last_fail stamps, fail_rows and dmax against a direct evaluation
