@@ -646,10 +646,16 @@ struct RowsGeom {
 #ifndef CS_ROWS_PREFETCH
 #define CS_ROWS_PREFETCH 0  // software-pipelined stage loads (needs 2x registers)
 #endif
+#ifndef CS_ROWS_DIAG_KR
+#define CS_ROWS_DIAG_KR 24  // plain diag: fp32 rows per thread per stage (tools/build_scan_variants.sh)
+#endif
+#ifndef CS_ROWS_DIAG_MINB
+#define CS_ROWS_DIAG_MINB 2
+#endif
 template <int VAR, bool UPD>
 struct RowsTune {
-  static constexpr int kRows32 = VAR == SCAN_DIAG ? (UPD ? 16 : 24) : 6;  // fp32 rows per thread per stage
-  static constexpr int kMinBlocks = VAR == SCAN_DIAG && !UPD ? 2 : 3;
+  static constexpr int kRows32 = VAR == SCAN_DIAG ? (UPD ? 16 : CS_ROWS_DIAG_KR) : 6;  // fp32 rows per thread per stage
+  static constexpr int kMinBlocks = VAR == SCAN_DIAG && !UPD ? CS_ROWS_DIAG_MINB : 3;
 };
 template <typename ST, int VAR, bool UPD = false>
 struct RowsSeg {

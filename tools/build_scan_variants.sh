@@ -14,5 +14,9 @@ build() {
   $NVCC -gencode arch=compute_100a,code=sm_100a -shared -o $d/libchainscan_b200.so $OBJS $d/cs_scan.o -cudart static -lcublas -Xlinker -rpath=/usr/local/cuda/lib64
   echo built $name
 }
-build old_kr16_m3 -DCS_ROWS_KR=16 -DCS_ROWS_KR_BLOCK=16 -DCS_ROWS_MINB=3 &
+build kr16_m3 -DCS_ROWS_DIAG_KR=16 -DCS_ROWS_DIAG_MINB=3 &
+build kr20_m2 -DCS_ROWS_DIAG_KR=20 -DCS_ROWS_DIAG_MINB=2 &
+build kr24_m2 -DCS_ROWS_DIAG_KR=24 -DCS_ROWS_DIAG_MINB=2 &
+build kr28_m2 -DCS_ROWS_DIAG_KR=28 -DCS_ROWS_DIAG_MINB=2 &
+build kr32_m2 -DCS_ROWS_DIAG_KR=32 -DCS_ROWS_DIAG_MINB=2 &
 wait
