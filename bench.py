@@ -267,7 +267,10 @@ def run_gpu(args):
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": traffic(f"deer_persistent_hmc_rosen_T{T}") if dtype == torch.float32 else None,
             "kernel": "cs::deer_persistent<Hmc<2,f,Rosenbrock>,DIAG> (whole solve)",
-            "peak_source": src, "algorithmic_bytes_per_launch": bytes_per_launch}
+            "peak_source": src, "algorithmic_bytes_per_launch": bytes_per_launch,
+            "note": "whole-solve working set (3.6 MB) is L2-resident: the kernel is bound by the grid "
+                    "barrier and dependent f64 leapfrog chains, not HBM (profiles/r01_ncu_hmc_fused_solver.md); "
+                    "the HBM-bound scan is scan_roofline"}
 
     # the T-sharded driver on BASELINE cfg 5 whenever ranks exist
     shard = t_sharded_gibbs(cs, dev, world, rank) if (world > 1 or args.sharded) and not args.no_extras else None
