@@ -691,9 +691,12 @@ CS_D float4 ld_hint_v4(const float *p, uint64_t pol) {
 // 32-byte sector per request, LSU-bound).  Instead the CTA loads the stage block
 // with coalesced 16-byte loads and redistributes it through shared memory
 // (segments padded by 4 floats: 16-byte stores, <= 2-way read conflicts).
+#ifndef CS_ROWS_TX_UPDATE
+#define CS_ROWS_TX_UPDATE 1  // the fused-bookkeeping (streamed engine) variant too
+#endif
 template <typename ST, int VAR, bool UPDATE, bool LBW>
 struct RowsTx {
-  static constexpr bool kOn = sizeof(ST) == 4 && VAR == SCAN_DIAG && !UPDATE && !LBW && !CS_ROWS_PREFETCH;
+  static constexpr bool kOn = sizeof(ST) == 4 && VAR == SCAN_DIAG && (!UPDATE || CS_ROWS_TX_UPDATE) && !LBW && !CS_ROWS_PREFETCH;
 };
 CS_HD bool rows_tx_dim(int D) { return D == 1 || D == 2 || D == 4; }
 
@@ -1814,7 +1817,7 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update) {
     if (rows_lbw()) {
       p.smem += 16 + sizeof(double) * (kLbwStage + kLbwPubStage);
     }
-    if (!rows_lbw() && !update && var == SCAN_DIAG && dtype == CS_F32 && rows_tx_dim(D))
+    if (!rows_lbw() && (!update || CS_ROWS_TX_UPDATE) && var == SCAN_DIAG && dtype == CS_F32 && rows_tx_dim(D))
       p.smem += 16 + sizeof(float) * 2 * ((size_t)p.R * D + 4 * nseg);  // small-D transposition buffer
   } else {
     p.kind = 1;
