@@ -15,6 +15,7 @@ flushed (256 MiB write) between timed steps, outside the timed region.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -220,6 +221,10 @@ def run_gpu(args):
     iters = res.iterations
 
     def timed(fn):
+        # the collector stays off inside the timed region (a collection pause in
+        # the host path would land in one step); objects are freed at the end
+        gc.collect()
+        gc.disable()
         evs = []
         for _ in range(args.steps):
             flush.fill_(1.0)
@@ -230,6 +235,7 @@ def run_gpu(args):
             b.record()
             evs.append((a, b))
         torch.cuda.synchronize()
+        gc.enable()
         return sum(a.elapsed_time(b) for a, b in evs), out
 
     if world > 1:

@@ -115,6 +115,10 @@ typedef struct cs_deer_result {
   int32_t grid_blocks;           /* persistent CTAs used                     */
   int32_t steps_per_thread;      /* contiguous steps folded per thread       */
   int32_t kept_in_registers;     /* 1 = elements kept across the grid sync   */
+  int32_t fused_tangent;         /* 1 = f_t and its one Hutchinson tangent in
+                                    a single integrator pass (diag HMC)       */
+  double device_ms;              /* device time of the solve (CUDA events on
+                                    the caller's stream around the launch)   */
 } cs_deer_result;
 
 const char *cs_last_error(void);

@@ -56,7 +56,8 @@ class cs_deer_result(ctypes.Structure):
     _fields_ = [("iterations", i32), ("status", i32), ("err_kind", i32), ("err_step", i64),
                 ("err_iteration", i32), ("launches", i32), ("guard_dmax", f64),
                 ("guard_d0", f64), ("stop_reason", i32), ("grid_blocks", i32),
-                ("steps_per_thread", i32), ("kept_in_registers", i32)]
+                ("steps_per_thread", i32), ("kept_in_registers", i32), ("fused_tangent", i32),
+                ("device_ms", f64)]
 
 
 class cs_elem_stats(ctypes.Structure):

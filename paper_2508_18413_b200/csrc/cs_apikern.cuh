@@ -252,14 +252,15 @@ cudaError_t run_syscall(const cs_system &s, const SysCall &c, cudaStream_t st) {
 // persistent solver launch: pick register-kept vs recompute variant and the
 // co-resident grid from the occupancy calculator.
 struct SolvePick {
-  int nblocks, seg, keep;
+  int nblocks, seg, keep, fused_tangent;
 };
 
-template <class Sys, int MODE, int MD, typename ST>
-cudaError_t launch_solve(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *pick) {
+template <class Sys, int MODE, int MD, typename ST, bool FT>
+cudaError_t launch_solve_ft(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *pick) {
   // register-kept elements only pay off (and only fit) for narrow states
   constexpr bool kKeepOK = MD <= 4;
-  auto kr = deer_persistent<Sys, MODE, MD, ST, false>;
+  auto kk = deer_persistent<Sys, MODE, MD, ST, kKeepOK, FT>;
+  auto kr = deer_persistent<Sys, MODE, MD, ST, false, FT>;
   const size_t keep_smem = sizeof(double) * kSegKeep * Elem<MODE, MD>::W * kSolveThreads;
   // occupancy is a property of the instantiation: query once per device
   static int s_bk[16], s_br[16];
@@ -271,11 +272,9 @@ cudaError_t launch_solve(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *p
   if (!s_done[dev]) {
     int bk = 0, br = 0;
     if constexpr (kKeepOK) {
-      e = cudaFuncSetAttribute(deer_persistent<Sys, MODE, MD, ST, true>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)keep_smem);
+      e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)keep_smem);
       if (e != cudaSuccess) return e;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, deer_persistent<Sys, MODE, MD, ST, true>,
-                                                        kSolveThreads, keep_smem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bk, kk, kSolveThreads, keep_smem);
       if (e != cudaSuccess) return e;
     }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&br, kr, kSolveThreads, 0);
@@ -297,24 +296,38 @@ cudaError_t launch_solve(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *p
     seg = (T + cap * kSolveThreads - 1) / (cap * kSolveThreads);
   }
   if (seg < 1) seg = 1;
-  // every co-resident CTA gets an equal contiguous share (at most seg steps per thread)
+  // every co-resident CTA gets an equal contiguous share (at most seg steps per
+  // thread); once the grid spans every SM, round it up to a whole number of
+  // CTAs per SM so no SM carries an extra CTA's steps (T = 100K at 3 CTAs/SM:
+  // 444 CTAs x 225 steps instead of 391 x 256, where 95 SMs ran 3 CTAs and 53
+  // ran 2 and the grid waited on the busy ones)
   int64_t nb = (T + kSolveThreads - 1) / kSolveThreads;
+  if (nb >= sms) nb = (nb + sms - 1) / sms * sms;
   if (nb > cap) nb = cap;
   A.seg = (int)seg;
   A.nblocks = (int)(nb < 1 ? 1 : nb);
   pick->nblocks = A.nblocks;
   pick->seg = A.seg;
   pick->keep = keep;
+  pick->fused_tangent = FT;
   void *args[] = {&A};
   void *fn = (void *)kr;
   size_t smem = 0;
   if constexpr (kKeepOK) {
     if (keep) {
-      fn = (void *)deer_persistent<Sys, MODE, MD, ST, true>;
+      fn = (void *)kk;
       smem = keep_smem;
     }
   }
   return cudaLaunchCooperativeKernel(fn, dim3(A.nblocks), dim3(kSolveThreads), args, smem, st);
+}
+
+template <class Sys, int MODE, int MD, typename ST>
+cudaError_t launch_solve(SolveArgs<ST> A, int sms, cudaStream_t st, SolvePick *pick) {
+  if constexpr (MODE == CS_MODE_DIAG && HasStepTangent<Sys>::value) {
+    if (A.nsamp == 1) return launch_solve_ft<Sys, MODE, MD, ST, true>(A, sms, st, pick);
+  }
+  return launch_solve_ft<Sys, MODE, MD, ST, false>(A, sms, st, pick);
 }
 
 }  // namespace cs

@@ -80,6 +80,23 @@ CS_D int warp_sum_i(int v) {
   return v;
 }
 
+// single-instruction warp reductions (redux.sync) for the solver's flags:
+// sums of u32 counts, and min / max of NON-NEGATIVE 64-bit words (step indices
+// with the INT64_MAX sentinel; f64 bit patterns of |x|) as hi-word then lo-word
+CS_D unsigned warp_sum_u32(unsigned v) { return __reduce_add_sync(0xffffffffu, v); }
+CS_D long long warp_min_nn64(long long v) {
+  const unsigned hi = (unsigned)((unsigned long long)v >> 32), lo = (unsigned)v;
+  const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+  return (long long)(((unsigned long long)mh << 32) | ml);
+}
+CS_D unsigned long long warp_max_nn64(unsigned long long v) {
+  const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  return ((unsigned long long)mh << 32) | ml;
+}
+
 CS_D bool finite(double x) { return isfinite(x); }
 
 }  // namespace cs

@@ -33,18 +33,37 @@ constexpr int kSolveThreads = 256;
 constexpr int kSegKeep = 4;
 constexpr int kTanMax = 4;
 
-struct SolveSlot {
+// Per-iteration reduction slot.  One per group of kSlotGroup consecutive CTAs,
+// each on its own 128-byte line: the CTAs of a group combine their flags with
+// atomics (16-way, groups in parallel on different L2 slices) instead of the
+// whole grid serialising on one line, and after the barrier every CTA folds
+// the few group slots.
+struct __align__(128) SolveSlot {
   long long bad_prop, bad_f, bad_jac;
   unsigned picard_fail, any_fail;
   unsigned long long dmax_bits;
 };
+static_assert(offsetof(SolveSlot, bad_jac) == 16 && offsetof(SolveSlot, picard_fail) == 24 &&
+                  offsetof(SolveSlot, any_fail) == 28 && offsetof(SolveSlot, dmax_bits) == 32,
+              "the solver reads slots as three 16-byte words");
+constexpr int kSlotGroup = 16;
+constexpr int kMaxSlotGroups = 80;  // 8 CTAs/SM x 148 SMs / 16, rounded up
+constexpr int kReadyStride = 32;    // halo stamps one 128-byte line apart
 
+// Grid control block.  It lives in library-owned device memory (one per
+// device and stream, zeroed once) and the kernel leaves it zeroed on exit: the
+// last CTA out resets the slots, the barrier counter and the halo stamps, so a
+// solve is ONE launch (no init kernel).
 struct SolveCtl {
-  SolveSlot slot[4];
-  unsigned arrive, gen;
+  SolveSlot slot[4][kMaxSlotGroups];
+  unsigned arrive, gen, exit_count, pad0;
+};
+
+// Outcome of a solve, written by CTA 0 into host-mapped memory at exit.
+struct SolveOut {
   int iterations, status, err_kind, final_buf, stop;
+  int err_iter;
   long long err_step;
-  int err_iter, pad;
   double guard_dmax, guard_d0;
 };
 
@@ -59,6 +78,7 @@ struct SolveArgs {
   int32_t *last_fail;
   double *hist;
   SolveCtl *ctl;
+  SolveOut *out;  // host-mapped
   double *agg;  // [2][nblocks][W]
   int *ready;   // [nblocks] iterate stamp: rows of guess_it written by CTA b
   unsigned long long *probe;  // cs_debug_probe buffer or null
@@ -267,9 +287,19 @@ CS_D void probe_stamp(unsigned long long *buf, int n, int it, int k) {
 #ifndef CS_SOLVE_MIN_BLOCKS
 #define CS_SOLVE_MIN_BLOCKS 2
 #endif
-template <class Sys, int MODE, int MD, typename ST, bool KEEP>
-__global__ void __launch_bounds__(kSolveThreads, CS_SOLVE_MIN_BLOCKS)
+// Systems with a one-pass f_t + tangent (step_tangent): the diag quasi-Newton
+// solve with one Hutchinson sample runs it instead of prepare + jvp_many.
+template <class Sys> struct HasStepTangent { static constexpr bool value = false; };
+template <int MD, typename ST, int TK> struct HasStepTangent<Hmc<MD, ST, TK>> { static constexpr bool value = true; };
+
+// resident CTAs per SM the instance is compiled for: the fused-tangent HMC
+// kernels fit 3 x 256 threads (one step per thread at T = 100K)
+template <bool FT> struct SolveOcc { static constexpr int kMinBlocks = FT ? 3 : CS_SOLVE_MIN_BLOCKS; };
+
+template <class Sys, int MODE, int MD, typename ST, bool KEEP, bool FT = false>
+__global__ void __launch_bounds__(kSolveThreads, SolveOcc<FT>::kMinBlocks)
 deer_persistent(SolveArgs<ST> A) {
+  static_assert(!FT || (MODE == CS_MODE_DIAG && HasStepTangent<Sys>::value), "fused tangent: diag HMC only");
   using E = Elem<MODE, MD>;
   // KEEP: the segment's elements wait in shared memory across the grid sync,
   // laid out [k][w][thread] so every access is bank-conflict free
@@ -278,6 +308,7 @@ deer_persistent(SolveArgs<ST> A) {
   __shared__ long long s_min[3];
   __shared__ unsigned s_cnt[2];
   __shared__ unsigned long long s_dm;
+  __shared__ long long s_dec[6];  // the slot words every thread decides on, read once per CTA
 
   const Sys sys = SysFactory<Sys>::make(A.sys);
   const int b = blockIdx.x;
@@ -303,7 +334,8 @@ deer_persistent(SolveArgs<ST> A) {
   E excl;  // this thread's exclusive in-CTA prefix of the current pass
 
   for (;;) {
-    SolveSlot *S = &A.ctl->slot[it & 3];
+    SolveSlot *S = &A.ctl->slot[it & 3][b / kSlotGroup];  // this CTA's group slot
+    const int ngroups = (A.nblocks + kSlotGroup - 1) / kSlotGroup;
     const ST *Gc = cur ? A.G1 : A.G0;
     if (threadIdx.x == 0) {
       s_min[0] = s_min[1] = s_min[2] = kNoStep;
@@ -314,7 +346,7 @@ deer_persistent(SolveArgs<ST> A) {
     // the halo row guess_it[row0-1] of CTA b's first thread was written by CTA b-1
     probe_stamp(A.probe, A.probe_n, it, 0);
     if (it > 0 && threadIdx.x == 0 && b > 0) {
-      const int *rd = A.ready + (b - 1);
+      const int *rd = A.ready + (size_t)(b - 1) * kReadyStride;
       while (ld_acquire(rd) < it) {
       }
     }
@@ -344,10 +376,41 @@ deer_persistent(SolveArgs<ST> A) {
       } else {
         load_row<Sys, MD, ST>(sys, Gc + r * D, gr);
       }
-      typename Sys::Aux aux;
-      if (!sys.prepare(t, prev, aux)) bp = min(bp, (long long)t);
       double f[MD];
-      sys.f(aux, f);
+      E e;
+      bool jok = true;
+      if constexpr (FT) {
+        // f_t and the one Hutchinson tangent in a single integrator pass
+        const uint64_t h3 = hash_t(probe_prefix(A.sys.seed, it), (uint64_t)t);
+        double V[MD], O[MD];
+#pragma unroll
+        for (int i = 0; i < MD; ++i) {
+          const int m = sys.mem_index(i);
+          V[i] = m >= 0 ? probe_sign(h3, 0, m) : 0.0;
+        }
+        if (!sys.template step_tangent<ST>(t, prev, V, f, O)) bp = min(bp, (long long)t);
+        if (want_elem) {
+#pragma unroll
+          for (int i = 0; i < MD; ++i) {
+            const int m = sys.mem_index(i);
+            if (m < 0) { e.j(i) = 0.0; e.u(i) = 0.0; continue; }
+            double est = 0.0;
+            est += V[i] * O[i];
+            double d = est / 1.0;  // deer.py:131 mean over one sample, same bits as the general path
+            jok &= finite(d);
+            if (A.pre) d = d * __ldg(A.pre + m);
+            d = d * A.damping;
+            if (isfinite(A.clip)) d = clipv(d, A.clip);
+            e.j(i) = d;
+            e.u(i) = f[i] - d * prev[i];
+          }
+        }
+      } else {
+        typename Sys::Aux aux;
+        if (!sys.prepare(t, prev, aux)) bp = min(bp, (long long)t);
+        sys.f(aux, f);
+        if (want_elem) build_elem<Sys, MODE, MD, ST>(sys, aux, prev, f, t, it, A, e, jok);
+      }
       bool fin = true, pfail = false;
 #pragma unroll
       for (int i = 0; i < MD; ++i) {
@@ -358,9 +421,6 @@ deer_persistent(SolveArgs<ST> A) {
       if (!fin) bf = min(bf, (long long)t);
       pf += pfail ? 1u : 0u;
       if (want_elem) {
-        E e;
-        bool jok;
-        build_elem<Sys, MODE, MD, ST>(sys, aux, prev, f, t, it, A, e, jok);
         if (!jok) bj = min(bj, (long long)t);
         agg.after(e);
         if constexpr (KEEP) {
@@ -379,10 +439,10 @@ deer_persistent(SolveArgs<ST> A) {
 #pragma unroll
       for (int q = 0; q < E::W; ++q) g[q] = total.v[q];
     }
-    bp = warp_min_i64(bp);
-    bf = warp_min_i64(bf);
-    bj = warp_min_i64(bj);
-    pf = (unsigned)warp_sum_i((int)pf);
+    bp = warp_min_nn64(bp);
+    bf = warp_min_nn64(bf);
+    bj = warp_min_nn64(bj);
+    pf = warp_sum_u32(pf);
     if ((threadIdx.x & 31) == 0) {
       if (bp != kNoStep) atomicMin(&s_min[0], bp);
       if (bf != kNoStep) atomicMin(&s_min[1], bf);
@@ -401,18 +461,55 @@ deer_persistent(SolveArgs<ST> A) {
     probe_stamp(A.probe, A.probe_n, it, 3);
     grid_sync(A.ctl, (unsigned)A.nblocks, target);
     probe_stamp(A.probe, A.probe_n, it, 4);
-    if (b == 0 && threadIdx.x == 0) {
-      SolveSlot *O = &A.ctl->slot[(it + 2) & 3];
+    if (b == 0 && threadIdx.x < ngroups) {
+      SolveSlot *O = &A.ctl->slot[(it + 2) & 3][threadIdx.x];
       O->bad_prop = O->bad_f = O->bad_jac = kNoStep;
       O->picard_fail = O->any_fail = 0;
       O->dmax_bits = 0ull;
     }
 
     // ---------------- decisions (identical in every CTA) ------------------
+    // one thread per CTA reads the slot words (not every thread: 100K readers
+    // of one L2 line serialise at its slice and skew the grid by microseconds)
+    if (threadIdx.x < 32) {  // warp 0 folds the group slots
+      unsigned gaf = 0, gpf = 0;
+      unsigned long long gdm = 0ull;
+      long long gbp = kNoStep, gbf = kNoStep, gbj = kNoStep;
+      for (int q = threadIdx.x; q < ngroups; q += 32) {
+        // 16-byte loads: [bad_prop bad_f] [bad_jac picard|any_fail] [dmax]
+        if (it > 0) {
+          const longlong2 *P = (const longlong2 *)&A.ctl->slot[(it - 1) & 3][q];
+          const longlong2 w1 = __ldcg(P + 1), w2 = __ldcg(P + 2);
+          gaf += (unsigned)((unsigned long long)w1.y >> 32);
+          const unsigned long long d = (unsigned long long)w2.x;
+          gdm = d > gdm ? d : gdm;
+        }
+        const longlong2 *Q = (const longlong2 *)&A.ctl->slot[it & 3][q];
+        const longlong2 w0 = __ldcg(Q), w1 = __ldcg(Q + 1);
+        gbp = min(gbp, w0.x);
+        gbf = min(gbf, w0.y);
+        gbj = min(gbj, w1.x);
+        gpf += (unsigned)w1.y;
+      }
+      gaf = warp_sum_u32(gaf);
+      gpf = warp_sum_u32(gpf);
+      gdm = warp_max_nn64(gdm);
+      gbp = warp_min_nn64(gbp);
+      gbf = warp_min_nn64(gbf);
+      gbj = warp_min_nn64(gbj);
+      if (threadIdx.x == 0) {
+        s_dec[0] = (long long)gaf;
+        s_dec[1] = (long long)gdm;
+        s_dec[2] = gbp;
+        s_dec[3] = gbf;
+        s_dec[4] = gbj;
+        s_dec[5] = (long long)gpf;
+      }
+    }
+    __syncthreads();
     if (it > 0) {  // the update that produced guess_it (deer.py:273-286)
-      const SolveSlot *P = &A.ctl->slot[(it - 1) & 3];
-      const unsigned gaf = vload(&P->any_fail);
-      const double dmax = __longlong_as_double((long long)vload(&P->dmax_bits));
+      const unsigned gaf = (unsigned)s_dec[0];
+      const double dmax = __longlong_as_double(s_dec[1]);
       if (b == 0 && threadIdx.x == 0) A.hist[it - 1] = dmax;
       if (!have_d0) { d0 = dmax; have_d0 = true; }
       g_dmax = dmax;
@@ -423,8 +520,8 @@ deer_persistent(SolveArgs<ST> A) {
       if (gaf == 0) { status = CS_RUN_CONVERGED; stop = CS_STOP_NOFAIL; break; }
     }
     {
-      const long long gbp = vload(&S->bad_prop), gbf = vload(&S->bad_f), gbj = vload(&S->bad_jac);
-      const unsigned gpf = vload(&S->picard_fail);
+      const long long gbp = s_dec[2], gbf = s_dec[3], gbj = s_dec[4];
+      const unsigned gpf = (unsigned)s_dec[5];
       if (gbp != kNoStep) { status = CS_RUN_DIVERGED; stop = CS_STOP_ERROR; err_kind = CS_DIV_PROPOSAL; err_step = gbp; err_iter = -1; break; }
       if (gbf != kNoStep) { status = CS_RUN_DIVERGED; stop = CS_STOP_ERROR; err_kind = CS_DIV_STEP; err_step = gbf; err_iter = it + 1; break; }
       if (gpf == 0) { status = CS_RUN_CONVERGED; stop = CS_STOP_PICARD; break; }
@@ -442,8 +539,13 @@ deer_persistent(SolveArgs<ST> A) {
       fold.ident();
       for (int q = lo; q < hi; ++q) {
         E e;
+        const double2 *src = (const double2 *)(ag + (size_t)q * E::W);  // W is even, records 16 B aligned
 #pragma unroll
-        for (int w = 0; w < E::W; ++w) e.v[w] = __ldcg(ag + (size_t)q * E::W + w);
+        for (int w = 0; w < E::W / 2; ++w) {
+          const double2 p = __ldcg(src + w);
+          e.v[2 * w] = p.x;
+          e.v[2 * w + 1] = p.y;
+        }
         fold.after(e);
       }
       E fex, ftot;
@@ -510,8 +612,8 @@ deer_persistent(SolveArgs<ST> A) {
           ++af;
         }
       }
-      af = (unsigned)warp_sum_i((int)af);
-      dmb = warp_max_u64(dmb);
+      af = warp_sum_u32(af);
+      dmb = warp_max_nn64(dmb);
       if ((threadIdx.x & 31) == 0) {
         if (af) atomicAdd(&s_cnt[1], af);
         atomicMax(&s_dm, dmb);
@@ -523,7 +625,7 @@ deer_persistent(SolveArgs<ST> A) {
         if (s_cnt[1]) atomicAdd(&S->any_fail, s_cnt[1]);
         atomicMax(&S->dmax_bits, s_dm);
         __threadfence();
-        st_release(A.ready + b, it + 1);  // rows of guess_{it+1} from this CTA are visible
+        st_release(A.ready + (size_t)b * kReadyStride, it + 1);  // rows of guess_{it+1} from this CTA are visible
       }
     }
     probe_stamp(A.probe, A.probe_n, it, 6);
@@ -531,17 +633,54 @@ deer_persistent(SolveArgs<ST> A) {
     cur ^= 1;
   }
 
+  // trace <- final iterate, per_step_converged_at = last_fail + 1
+  // (deer.py:321-328), each CTA over its own rows (written only by itself)
+  {
+    const int fb = it == 0 ? -1 : cur;
+    for (int64_t r = lo_b + threadIdx.x; r < hi_b; r += kSolveThreads) {
+      if (fb == 1) {
+        for (int d = 0; d < D; ++d) A.G0[r * D + d] = A.G1[r * D + d];
+      } else if (fb == -1) {
+        for (int d = 0; d < D; ++d) A.G0[r * D + d] = A.s0[d];
+      }
+      A.last_fail[r] = A.last_fail[r] + 1;
+    }
+  }
   if (b == 0 && threadIdx.x == 0) {
-    SolveCtl *c = A.ctl;
-    c->iterations = it;
-    c->status = status;
-    c->stop = stop;
-    c->err_kind = err_kind;
-    c->err_step = err_step;
-    c->err_iter = err_iter;
-    c->final_buf = it == 0 ? -1 : cur;
-    c->guard_dmax = g_dmax;
-    c->guard_d0 = d0;
+    SolveOut *o = A.out;
+    o->iterations = it;
+    o->status = status;
+    o->stop = stop;
+    o->err_kind = err_kind;
+    o->err_step = err_step;
+    o->err_iter = err_iter;
+    o->final_buf = it == 0 ? -1 : cur;
+    o->guard_dmax = g_dmax;
+    o->guard_d0 = d0;
+  }
+  // leave the control block zeroed for the next solve on this stream: the last
+  // CTA out (every other CTA is past its last read of it) resets it
+  __shared__ unsigned s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&A.ctl->exit_count, 1u) == (unsigned)A.nblocks - 1u;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    for (int i = threadIdx.x; i < A.nblocks; i += kSolveThreads) A.ready[(size_t)i * kReadyStride] = 0;
+    for (int i = threadIdx.x; i < 4 * kMaxSlotGroups; i += kSolveThreads) {
+      SolveSlot *O = &A.ctl->slot[i / kMaxSlotGroups][i % kMaxSlotGroups];
+      O->bad_prop = O->bad_f = O->bad_jac = kNoStep;
+      O->picard_fail = O->any_fail = 0;
+      O->dmax_bits = 0ull;
+    }
+    if (threadIdx.x == 0) {
+      A.ctl->arrive = 0;
+      A.ctl->gen = 0;
+      A.ctl->exit_count = 0;
+    }
   }
 }
 

@@ -176,6 +176,83 @@ struct Hmc {
     for (int i = 0; i < MD; ++i) o[i] = w * a.xl[i] + (1.0 - w) * a.S[i];
   }
 
+  // f_t(s) and ONE tangent J_t V in a single pass of the integrator: prepare()
+  // followed by jvp_many<1>() with the same operations in the same order (so
+  // the same bits), minus the second primal integration and without the Aux
+  // record -- the diag quasi-Newton solve's per-step work (samplers.py:322-381).
+  // Returns false when the proposal is non-finite (like prepare()).
+  template <typename TT>
+  CS_D bool step_tangent(int64_t t, const double (&s)[MD], const double (&V)[MD], double (&fo)[MD],
+                         double (&o)[MD]) const {
+    const int D = dim();
+    double x[MD], v[MD], g[MD];
+    TT dx[MD], dv[MD], h[MD], Vk[MD];
+    const TT e = (TT)eps, he = (TT)(0.5 * eps);
+    tg.grad(s, g);
+#pragma unroll
+    for (int i = 0; i < MD; ++i) Vk[i] = (TT)V[i];
+    tg.hvpT(s, Vk, h);
+    double xx = 0.0;
+    TT sg = 0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      const double z = (i < D) ? ld(mom, t * D + i) : 0.0;
+      xx += z * z;
+      x[i] = s[i];
+      v[i] = (i < D) ? sqrt(m(i)) * z + (0.5 * eps) * g[i] : 0.0;
+      dx[i] = Vk[i];
+      dv[i] = he * h[i];
+      sg += (TT)g[i] * Vk[i];
+    }
+    const TT dh0 = -sg;
+    const double h0 = 0.5 * xx - tg.logp(s);
+#pragma unroll 1
+    for (int l = 0; l < L; ++l) {
+#pragma unroll
+      for (int i = 0; i < MD; ++i) x[i] = x[i] + divm(eps * v[i], i);
+#pragma unroll
+      for (int i = 0; i < MD; ++i) dx[i] = dx[i] + (TT)divm((double)(e * dv[i]), i);
+      tg.hvpT(x, dx, h);
+#pragma unroll
+      for (int i = 0; i < MD; ++i) dv[i] = dv[i] + e * h[i];
+      tg.grad(x, g);
+#pragma unroll
+      for (int i = 0; i < MD; ++i) v[i] = v[i] + eps * g[i];
+    }
+    // g = grad(x_L) (prepare()'s gl; the loop's last gradient, or grad(s) at L = 0)
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) ok &= (i >= D) || finite(x[i]);
+    double kin = 0.0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      v[i] = v[i] - (0.5 * eps) * g[i];  // vl
+      if (i < D) kin += divm(v[i] * v[i], i);
+    }
+    const double hl = 0.5 * kin - tg.logp(x);
+    const double delta = h0 - hl;
+    const double margin = fmin(0.0, delta) - __ldg(logu + t);
+    const bool acc = margin > 0.0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) fo[i] = acc ? x[i] : s[i];
+    const TT gate = (TT)(acc ? 1.0 : 0.0);
+    tg.hvpT(x, dx, h);
+    TT s1 = 0, s2 = 0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i) {
+      const TT dvl = dv[i] - he * h[i];
+      if (i < D) s1 += (TT)divm((double)((TT)v[i] * dvl), i);
+      s2 += (TT)g[i] * dx[i];
+    }
+    const TT ddelta = dh0 - (s1 - s2);
+    // sigmoid_prime (an f64 exp + log) only matters where delta < 0
+    const TT bend = delta < 0.0 ? (TT)sigmoid_prime(margin) * ddelta : ddelta * (TT)0;
+#pragma unroll
+    for (int i = 0; i < MD; ++i)
+      o[i] = (double)((gate * dx[i] + ((TT)1 - gate) * Vk[i]) + (TT)(x[i] - s[i]) * bend);
+    return ok;
+  }
+
   // tangents ride the forward integrator (samplers.py:353-381), all n at once,
   // in tangent precision TT; the positions they are linearised at stay f64
   template <int NT, typename TT = double>

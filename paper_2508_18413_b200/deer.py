@@ -174,10 +174,20 @@ def _check_finite(arr, what, ts, iteration):
                                  step=t, iteration=iteration + 1)
 
 
-def _pre_tensor(cfg, device):
+def _pre_tensor(cfg, device, D=None):
+    """The preconditioner as a (D,) f64 device vector.  The kernels read D
+    entries, so the length is checked here, before any launch: length D, or
+    length 1 broadcast like the reference's ``d * pre`` / ``pre[None,:]``
+    products (deer.py:163-164, :177-178); block mode slices it into x and v
+    halves (deer.py:192-195), which needs all D entries."""
     if cfg.preconditioner is None:
         return None
-    return torch.as_tensor(cfg.preconditioner, dtype=torch.float64, device=device)
+    pre = torch.as_tensor(cfg.preconditioner, dtype=torch.float64, device=device).reshape(-1)
+    if D is not None and pre.shape[0] != D:
+        if pre.shape[0] == 1 and cfg.mode != "block2x2-stochastic":
+            return pre.expand(D).contiguous()
+        raise StructuralError(f"preconditioner has length {pre.shape[0]}, the state has dimension {D}")
+    return pre
 
 
 def _build_elements(system, ts, guess, s0_local, cfg, iteration, f, on_bad=None, prev=None):
@@ -194,7 +204,7 @@ def _build_elements(system, ts, guess, s0_local, cfg, iteration, f, on_bad=None,
         prev = torch.cat([s0_local[None], guess[:-1]], dim=0)
     f = f.to(guess.dtype).contiguous()
     T, W = guess.shape
-    pre = _pre_tensor(cfg, guess.device)
+    pre = _pre_tensor(cfg, guess.device, W)
     clip = float(cfg.clip)
 
     def finite_or(arr, what):
@@ -337,18 +347,26 @@ def _run_fused(system, s0, cfg, max_iters):
     # delta history straight into pinned host memory (UVA: the kernel's one
     # store per iteration lands on the host; no second read-back after the solve)
     hist = _pinned_hist(max_iters)
-    ws_bytes = lib.cs_deer_workspace_bytes(ctypes.byref(d), _lib.dtype_code(dtype), max_iters)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    pre = _pre_tensor(cfg, dev)
-    if pre is not None and pre.shape != (D,):
-        raise StructuralError(f"preconditioner must have shape ({D},)")
-    c = _lib.cs_deer_config()
-    c.mode = _MODE_CODE[cfg.mode]
-    c.atol, c.rtol = float(cfg.atol), float(cfg.rtol)
-    c.max_iters = int(max_iters)
-    c.hutchinson_samples = int(cfg.hutchinson_samples)
-    c.damping, c.clip = float(cfg.damping), float(cfg.clip)
-    c.preconditioner = 0 if pre is None else pre.data_ptr()
+    # the solver workspace and the config record are reused across solves of
+    # this system (cs_deer_solve synchronises before returning)
+    key = (cfg.mode, dtype, max_iters, cfg.atol, cfg.rtol, cfg.hutchinson_samples, cfg.damping, cfg.clip,
+           None if cfg.preconditioner is None else cfg.preconditioner.tobytes(), T, dev)
+    cache = system.__dict__.setdefault("_fused_ws", {})
+    hit = cache.get(key)
+    if hit is None:
+        ws_bytes = lib.cs_deer_workspace_bytes(ctypes.byref(d), _lib.dtype_code(dtype), max_iters)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        pre = _pre_tensor(cfg, dev, D)
+        c = _lib.cs_deer_config()
+        c.mode = _MODE_CODE[cfg.mode]
+        c.atol, c.rtol = float(cfg.atol), float(cfg.rtol)
+        c.max_iters = int(max_iters)
+        c.hutchinson_samples = int(cfg.hutchinson_samples)
+        c.damping, c.clip = float(cfg.damping), float(cfg.clip)
+        c.preconditioner = 0 if pre is None else pre.data_ptr()
+        cache.clear()
+        hit = cache[key] = (ws, ws_bytes, pre, c)
+    ws, ws_bytes, pre, c = hit
     res = _lib.cs_deer_result()
     rc = lib.cs_deer_solve(ctypes.byref(d), ctypes.byref(c), _lib.dtype_code(dtype), _lib.ptr(s0.contiguous()),
                            _lib.ptr(trace), _lib.ptr(psca), _lib.ptr(hist), _lib.ptr(ws), ws_bytes,
@@ -375,8 +393,9 @@ def _run_fused(system, s0, cfg, max_iters):
         raise ChainDivergedError(kind, step=step, iteration=iteration)
     _lib.check(rc)
     stats = {"path": "fused", "grid_blocks": int(res.grid_blocks), "steps_per_thread": int(res.steps_per_thread),
-             "kept_in_registers": bool(res.kept_in_registers), "launches": int(res.launches),
-             "stop_reason": int(res.stop_reason)}
+             "kept_in_registers": bool(res.kept_in_registers), "fused_tangent": bool(res.fused_tangent),
+             "launches": int(res.launches), "stop_reason": int(res.stop_reason),
+             "device_ms": float(res.device_ms)}
     return DeerResult(trace=trace, iterations=it, delta_history=hist[:it].numpy().copy(),
                       converged=res.status == _lib.CS_RUN_CONVERGED, per_step_converged_at=psca,
                       full_trace=None, stats=stats)
@@ -401,6 +420,7 @@ def run_deer(system: TransitionSystem, s0, cfg: DeerConfig) -> DeerResult:
     if tuple(s0.shape) != (system.dim,):
         raise StructuralError(f"s0 must have shape ({system.dim},), got {tuple(s0.shape)}")
     T = system.T
+    _pre_tensor(cfg, system.device, system.dim)  # length check before any engine runs
     max_iters = cfg.max_iters if cfg.max_iters is not None else default_max_iters(T)
     engine = _pick_engine(system, cfg)
     if engine == "fused":
@@ -455,7 +475,7 @@ def _run_streamed(system, s0, cfg, max_iters):
     c.max_iters = int(max_iters)
     c.hutchinson_samples = int(cfg.hutchinson_samples)
     c.damping, c.clip = float(cfg.damping), float(cfg.clip)
-    pre = _pre_tensor(cfg, dev)
+    pre = _pre_tensor(cfg, dev, D)
     c.preconditioner = 0 if pre is None else pre.data_ptr()
     mode = cfg.mode
     if mode == "diag-stochastic":

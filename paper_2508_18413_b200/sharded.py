@@ -185,11 +185,14 @@ class CudaShardOps(ShardOps):
 
 
 def _gather(vec: torch.Tensor, group, world):
+    """All-gather a small vector; the result lives on ``vec``'s device (a gloo
+    group stages CUDA vectors through the host and moves the result back)."""
+    dev = vec.device
     if vec.is_cuda and dist.get_backend(group) == "gloo":  # host-side groups (CPU tests) stage through host
         vec = vec.cpu()
     out = [torch.empty_like(vec) for _ in range(world)]
     dist.all_gather(out, vec, group=group)
-    return torch.stack(out)
+    return torch.stack(out).to(dev)
 
 
 def _streamed_shard_ok(system, cfg) -> bool:
@@ -210,6 +213,9 @@ def run_deer_sharded(system, s0, cfg, ops: ShardOps | None = None, group=None, m
     """run_deer (deer.py:230-328) with T sharded over the process group."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    from .deer import _pre_tensor
+
+    _pre_tensor(cfg, "cpu", system.dim)  # length check before any launch
     if ops is None and _streamed_shard_ok(system, cfg) and (cfg.window_len is None or cfg.window_len >= system.T):
         return _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters)
     ops = ops or CudaShardOps(system)
@@ -322,7 +328,7 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
     c.max_iters = int(max_iters)
     c.hutchinson_samples = int(cfg.hutchinson_samples)
     c.damping, c.clip = float(cfg.damping), float(cfg.clip)
-    pre = _pre_tensor(cfg, dev)
+    pre = _pre_tensor(cfg, dev, D)
     c.preconditioner = 0 if pre is None else pre.data_ptr()
     mode = cfg.mode
     half = D // 2 if mode == "block2x2-stochastic" else D

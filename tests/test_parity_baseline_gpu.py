@@ -1,0 +1,203 @@
+"""Parity at the BASELINE.json sizes (not reduced ones).
+
+Anchors, in order of strength:
+* fixtures made by running the REFERENCE itself at the full sizes
+  (tests/golden/make_golden_big.py: cfg1 T=10K, cfg2 T=100K, cfg3 diag
+  T=100K, cfg5 T=1M): iteration counts, converged flags, the whole
+  delta_history and per-step convergence record, trace rows at a stride,
+  and the reference's SEQUENTIAL chain's accept/reject mask;
+* the CPU oracle's run_deer, live, on the same inputs (full trace).
+
+Bar (north_star): f32 (the bench dtype) within the reference's own
+convergence envelope |gpu - ref| <= 1e-4 + 1e-3|ref|, iterations within +-1,
+and the accept/reject decisions at the converged trace identical to the
+reference's sequential chain.  f64: the same iteration count, the same
+per-step convergence record, trace within 1e-8.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+cs = pytest.importorskip("paper_2508_18413_b200")
+
+ATOL, RTOL = 1e-4, 1e-3
+
+
+def np_(t):
+    return t.detach().cpu().numpy() if torch.is_tensor(t) else np.asarray(t)
+
+
+def outside_envelope(a, ref, atol=ATOL, rtol=RTOL):
+    return int(np.sum(np.abs(np.asarray(a, float) - ref) > atol + rtol * np.abs(ref)))
+
+
+def accept_mask(osys, s0, trace):
+    """Gate decisions of every step at a converged trace: step t accepted iff
+    f_t(s_{t-1}) != s_{t-1} (a rejection returns the state bit for bit,
+    samplers.py:120-122 / :344-346), evaluated by the oracle in f64."""
+    tr = np.asarray(trace, float)
+    prev = np.concatenate([np.asarray(s0, float)[None], tr[:-1]], axis=0)
+    ts = np.arange(1, tr.shape[0] + 1)
+    out = np.empty(tr.shape[0], bool)
+    for a in range(0, tr.shape[0], 1 << 16):
+        b = min(a + (1 << 16), tr.shape[0])
+        f = osys.step_batch(ts[a:b], prev[a:b])
+        out[a:b] = np.any(f != prev[a:b], axis=1)
+    return out
+
+
+def ref_accept(g, T):
+    return np.unpackbits(g["seq_accept_bits"])[:T].astype(bool)
+
+
+def check_record(res, g, prefix, dtype, T, exact_psca=True):
+    stride = int(g["stride"])
+    rows = np_(res.trace)[stride - 1::stride]
+    it_ref = int(g[prefix + "iterations"])
+    assert res.converged == bool(g[prefix + "converged"])
+    if dtype == torch.float64:
+        assert res.iterations == it_ref
+        np.testing.assert_allclose(rows, g[prefix + "rows"], atol=1e-8, rtol=1e-8)
+        np.testing.assert_allclose(res.delta_history, g[prefix + "delta_history"], rtol=1e-6, atol=1e-12)
+        psca = np_(res.per_step_converged_at)
+        if exact_psca:
+            np.testing.assert_array_equal(psca, g[prefix + "psca"])
+        else:  # at T = 1M a per-step test can sit within f64 rounding of its tolerance
+            assert np.mean(psca == g[prefix + "psca"]) > 0.9999
+    else:
+        assert abs(res.iterations - it_ref) <= 1, (res.iterations, it_ref)
+        assert outside_envelope(rows, g[prefix + "rows"]) == 0
+    np.testing.assert_allclose(np_(res.trace).mean(axis=0), g[prefix + "mean"],
+                               atol=1e-4 if dtype == torch.float32 else 1e-9, rtol=1e-3)
+
+
+# ---------------------------------------------------------------------------
+# cfg2: the bench's headline workload (HMC Rosenbrock, T = 100K, diag + clip)
+
+
+def _cfg2(dtype):
+    m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
+    return cs.HmcKernel(m, 0.5, 8, seed=0, T=100_000, dtype=dtype)
+
+
+def _cfg2_oracle():
+    return O.HmcKernel(O.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0), 0.5, 8, seed=0, T=100_000)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_cfg2_hmc_T100K_vs_reference(cuda_device, dtype):
+    g = golden("big_cfg2_hmc_rosen2d_T100K")
+    cfg = cs.DeerConfig(mode="diag-stochastic", clip=1.0)
+    res = cs.run_deer(_cfg2(dtype), np.zeros(2), cfg)
+    assert res.stats["path"] == "fused"          # the bench's path
+    check_record(res, g, "diagclip_", dtype, 100_000)
+    # the accept/reject decisions at the converged trace are the sequential chain's
+    acc = accept_mask(_cfg2_oracle(), np.zeros(2), np_(res.trace))
+    np.testing.assert_array_equal(acc, ref_accept(g, 100_000))
+    if dtype == torch.float32:
+        # the whole trace against the oracle's run_deer on the same noise
+        ref = O.run_deer(_cfg2_oracle(), np.zeros(2), O.DeerConfig(mode="diag-stochastic", clip=1.0))
+        assert abs(ref.iterations - res.iterations) <= 1
+        assert outside_envelope(np_(res.trace), ref.trace) == 0
+        # ... and the sequential chain itself, every 100th row
+        assert outside_envelope(np_(res.trace)[99::100], g["seq_rows"]) == 0
+
+
+@pytest.mark.parametrize("engine", ["streamed", "host"])
+def test_cfg2_hmc_T100K_other_engines(cuda_device, engine):
+    g = golden("big_cfg2_hmc_rosen2d_T100K")
+    res = cs.run_deer(_cfg2(torch.float64), np.zeros(2),
+                      cs.DeerConfig(mode="diag-stochastic", clip=1.0, engine=engine))
+    assert res.stats["path"] == engine
+    check_record(res, g, "diagclip_", torch.float64, 100_000)
+
+
+# ---------------------------------------------------------------------------
+# cfg1: MALA on the criterion-8 Gaussian, T = 10K, dense Newton
+
+
+def _cfg1(dtype=torch.float64):
+    m = cs.model_logp_grad_hvp(cs.gaussian([1.0, -1.0], [[1.0, 0.0], [-0.6, 1.2]]))
+    return cs.MalaKernel(m, 0.4, seed=0, T=10_000, dtype=dtype)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_cfg1_mala_T10K_dense_vs_reference(cuda_device, dtype):
+    g = golden("big_cfg1_mala_gauss2d_T10K")
+    om = O.gaussian(np.array([1.0, -1.0]), np.array([[1.0, 0.0], [-0.6, 1.2]]))
+    for prefix, kw in (("dense_", {}), ("tight_", dict(atol=1e-6, rtol=1e-5))):
+        res = cs.run_deer(_cfg1(dtype), np.zeros(2), cs.DeerConfig(mode="dense", **kw))
+        check_record(res, g, prefix, dtype, 10_000)
+        acc = accept_mask(O.MalaKernel(om, 0.4, seed=0, T=10_000), np.zeros(2), np_(res.trace))
+        np.testing.assert_array_equal(acc, ref_accept(g, 10_000))
+    # sequential chain on the device vs the reference's
+    seq = np_(cs.sequential_evaluate(_cfg1(dtype), np.zeros(2)))
+    tol = 1e-9 if dtype == torch.float64 else 1e-5
+    np.testing.assert_allclose(seq[19::20], g["seq_rows"], atol=tol, rtol=tol)
+    np.testing.assert_allclose(seq[-1], g["seq_last"], atol=tol, rtol=tol)
+
+
+# ---------------------------------------------------------------------------
+# cfg5: eight-schools Gibbs, T = 1M, diag x3 + preconditioner
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_cfg5_gibbs_T1M_vs_reference(cuda_device, dtype):
+    g = golden("big_cfg5_gibbs_T1M")
+    k = cs.GibbsKernel(cs.generate_eight_schools(), seed=0, T=1_000_000, dtype=dtype)
+    s0 = k.initial_state()
+    np.testing.assert_allclose(np_(s0), g["s0"], rtol=1e-10 if dtype == torch.float64 else 1e-6)
+    cfg = cs.DeerConfig(mode="diag-stochastic", hutchinson_samples=3,
+                        preconditioner=k.recommended_preconditioner(), max_iters=400)
+    res = cs.run_deer(k, g["s0"], cfg)
+    if dtype == torch.float64:
+        check_record(res, g, "diag3_", dtype, 1_000_000, exact_psca=False)
+    else:
+        # Gibbs states span 1e-8..1e2 (sigma^2 floors): iterations +-1 and the
+        # rows within the envelope of the reference run_deer rows
+        assert res.converged == bool(g["diag3_converged"])
+        assert abs(res.iterations - int(g["diag3_iterations"])) <= 1
+        rows = np_(res.trace)[int(g["stride"]) - 1::int(g["stride"])]
+        assert outside_envelope(rows, g["diag3_rows"]) == 0
+
+
+# ---------------------------------------------------------------------------
+# cfg3 diag: BLR MALA, D = 100, N = 1000, T = 100K (f64, the streamed engine)
+
+
+def test_cfg3_blr_diag_T100K_vs_reference(cuda_device):
+    g = golden("big_cfg3_mala_blr100_T100K")
+    X, y, _ = cs.synthetic_credit_like(seed=20250819, n=1000, dim=100)
+    m = cs.model_logp_grad_hvp(cs.blr(X, y, 1.0))
+    k = cs.MalaKernel(m, 0.003, seed=4, T=100_000)
+    res = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="diag-stochastic"))
+    assert res.stats["path"] == "streamed"
+    check_record(res, g, "diag_", torch.float64, 100_000, exact_psca=False)
+
+
+# ---------------------------------------------------------------------------
+# run-to-run bit identity of the scans (the reference's fixed-chunk property,
+# _scan_kernels.py:3-8, test_pscan.py:160-168): the carries are folded in a
+# fixed order, so repeated solves on the same elements agree bit for bit
+
+
+@pytest.mark.parametrize("kind", ["diag", "block"])
+@pytest.mark.parametrize("T,D", [(1 << 22, 18), (3_000_017, 2), (1 << 20, 64)])
+def test_scan_bit_identical_run_to_run(cuda_device, kind, T, D):
+    gen = torch.Generator(device=cuda_device).manual_seed(T + D)
+    r = lambda *s: torch.rand(*s, device=cuda_device, generator=gen, dtype=torch.float32)
+    s0 = r(D if kind == "diag" else 2 * D) - 0.5
+    if kind == "diag":
+        el = cs.DiagElements(1.9 * r(T, D) - 0.95, r(T, D) - 0.5)
+    else:
+        el = cs.Block2x2Elements(*(1.3 * r(T, D) - 0.65 for _ in range(4)), r(T, 2 * D) - 0.5)
+    first = cs.parallel_affine_solve(el, s0)
+    for _ in range(4):
+        again = cs.parallel_affine_solve(el, s0)
+        assert torch.equal(first, again)
