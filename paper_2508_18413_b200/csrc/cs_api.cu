@@ -630,7 +630,7 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
   }
   if (blr) {
     e = elements_blr(*sys, *cfg, dtype, iteration, s0, guess, e0, u, d_stats, st);
-    return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements (logistic-regression MALA, cuBLAS)");
+    return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements (logistic-regression MALA)");
   }
   if (dtype == CS_F64) {
     SolveArgs<double> A{};
@@ -658,13 +658,20 @@ int cs_system_elements_range(const cs_system *sys, const cs_deer_config *cfg, in
     return cs_system_elements(sys, cfg, dtype, iteration, s0, guess, e0, e1, e2, e3, u, d_stats, stream);
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   const int md = elem_width(sys);
-  if (!md) return fail(CS_ERR_CONFIG, "step ranges need a register-kernel system (GEMM-backed builders take whole chains)");
+  const bool blr = !md && blr_mala_ok(*sys, cfg->mode) && blr_fused_ok(*sys, *cfg);
+  if (!md && !blr)
+    return fail(CS_ERR_CONFIG, "step ranges need a register-kernel system or the fused logistic-regression "
+                               "builder (the other GEMM-backed builders take whole chains)");
   if (cfg->mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG)
     return fail(CS_ERR_CONFIG, "system does not provide a block2x2 Jacobian estimate");
   cudaStream_t st = S(stream);
   k_init_stats<<<1, 1, 0, st>>>(d_stats);
   if (n < 1) return CS_OK;
   cudaError_t e;
+  if (blr) {
+    e = elements_blr_fused(*sys, *cfg, dtype, iteration, t0, n, s0, guess, e0, u, d_stats, st);
+    return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements_range (logistic-regression MALA)");
+  }
   if (dtype == CS_F64) {
     SolveArgs<double> A{};
     A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;

@@ -19,6 +19,7 @@
 #include <mutex>
 
 #include "cs_apikern.cuh"
+#include "cs_dispatch.h"
 #include "cs_umma.cuh"
 
 namespace cs {
@@ -853,6 +854,10 @@ cudaError_t elements_blr(const cs_system &sys, const cs_deer_config &cfg, int dt
     return blr_dense_run<float>(sys, cfg, iteration, (const float *)s0, (const float *)guess, (float *)e0,
                                 (float *)u, stats, st);
   }
+  // diag: the fused DMMA builder (cs_blr_fused.cu); more than 7 probes per step
+  // take the GEMM pipeline below
+  if (blr_fused_ok(sys, cfg))
+    return elements_blr_fused(sys, cfg, dtype, iteration, 0, sys.T, s0, guess, e0, u, stats, st);
   if (dtype == CS_F64)
     return blr_run<double>(sys, cfg, iteration, (const double *)s0, (const double *)guess, (double *)e0,
                            (double *)u, stats, st);

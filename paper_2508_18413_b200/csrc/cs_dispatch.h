@@ -12,6 +12,10 @@ cudaError_t elements_wide(const cs_system &sys, const cs_deer_config &cfg, int d
                           const void *s0, const void *guess, void *e0, void *e1, void *e2, void *e3, void *u,
                           cs_elem_stats *stats, cudaStream_t st);
 bool blr_mala_ok(const cs_system &s, int mode);
+bool blr_fused_ok(const cs_system &s, const cs_deer_config &cfg);
+cudaError_t elements_blr_fused(const cs_system &sys, const cs_deer_config &cfg, int dtype, int64_t iteration,
+                               int64_t t0, int64_t n, const void *s0, const void *guess, void *j, void *u,
+                               cs_elem_stats *stats, cudaStream_t st);
 bool leapfrog_batch_ok(const cs_system &s, int mode);
 cudaError_t leapfrog_batch_solve(const cs_system &sys, const cs_deer_config &cfg, int dtype, int B, const void *s0s,
                                  void *finals, int32_t *info, long long *err_step, cudaStream_t st);
