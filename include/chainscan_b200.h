@@ -248,12 +248,18 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
  * T shard in the sharded driver: guess holds the shard's n rows,
  * s0 the state before step t0+1 (the halo row); noise and probes are indexed by
  * the absolute step, so the shard's elements equal rows t0 .. t0+n-1 of the
- * whole chain's.  Register-kernel systems (incl. Gibbs); CS_ERR_CONFIG for the
- * GEMM-backed builders unless the range is the whole chain.  Replaces the
+ * whole chain's.  Register-kernel systems (incl. Gibbs) and logistic-regression
+ * MALA; CS_ERR_CONFIG for the wide leapfrog builder unless the range is the
+ * whole chain.  Replaces the
  * per-shard _iterate_range (deer.py:147-208) of a T-sharded run. */
 int cs_system_elements_range(const cs_system *sys, const cs_deer_config *cfg, int dtype, int64_t iteration,
                              int64_t t0, int64_t n, const void *s0, const void *guess, void *e0, void *e1,
                              void *e2, void *e3, void *u, cs_elem_stats *d_stats, void *stream);
+/* 1 when cs_system_elements_range can build this system's elements for a step
+ * range under cfg (register-kernel systems, Gibbs, logistic-regression MALA in
+ * dense mode or diag with <= 7 probes), else 0.  The sharded driver's test for
+ * its streamed shard path (replaces the per-shard _iterate_range dispatch). */
+int cs_system_elements_range_supported(const cs_system *sys, const cs_deer_config *cfg, int dtype);
 /* 1 when cs_system_elements can build elements for (sys, mode, dtype): the
  * register builders (narrow built-in systems); for a leapfrog system on a
  * dense Gaussian target in block2x2 mode at any dimension, the GEMM-backed

@@ -98,6 +98,7 @@ _SIGS = {
     "cs_system_elements": ([SP, CP, ctypes.c_int, i64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
     "cs_system_elements_range": ([SP, CP, ctypes.c_int, i64, i64, i64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
     "cs_system_elements_supported": ([SP, i32, ctypes.c_int], ctypes.c_int),
+    "cs_system_elements_range_supported": ([SP, CP, ctypes.c_int], ctypes.c_int),
     "cs_scan_diag_update": ([ctypes.c_int, P, P, P, P, i64, i32, P, szt, P, f64, f64, i32, P, P, P], ctypes.c_int),
     "cs_scan_block_update": ([ctypes.c_int, P, P, P, P, P, P, P, i64, i32, P, szt, P, f64, f64, i32, P, P, P],
                              ctypes.c_int),

@@ -74,10 +74,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = True) ->
                 if verbose:
                     print(f"  compiled {os.path.basename(s)} ({time.time() - t0:.0f}s)", flush=True)
     if todo or not os.path.exists(LIB):
-        # cuBLAS (dynamic, CUDA's own copy; a process that already loaded torch's
-        # libcublas.so.12 resolves to that one) backs the wide leapfrog builder
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-cudart", "static", "-lcublas",
-                                                               "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+        # no vendor math libraries: every product is one of our kernels
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-cudart", "static"]
         subprocess.check_call(cmd)
         if verbose:
             print(f"linked {LIB} ({time.time() - t0:.0f}s)", flush=True)

@@ -603,6 +603,14 @@ int cs_system_elements_supported(const cs_system *sys, int32_t mode, int dtype) 
   return md > 0 || wide_leapfrog_ok(*sys, mode) || blr_mala_ok(*sys, mode) ? 1 : 0;
 }
 
+int cs_system_elements_range_supported(const cs_system *sys, const cs_deer_config *cfg, int dtype) {
+  if (!sys || !cfg || !dtype_ok(dtype)) return 0;
+  if (!cs_system_elements_supported(sys, cfg->mode, dtype)) return 0;
+  if (sys->target.kind == CS_TARGET_BLR && sys->kind == CS_SYS_MALA)
+    return blr_mala_ok(*sys, cfg->mode) && (cfg->mode == CS_MODE_DENSE || blr_fused_ok(*sys, *cfg)) ? 1 : 0;
+  return !wide_leapfrog_ok(*sys, cfg->mode) || elem_md(sys->kind, sys->target.kind, sys->dim) > 0 ? 1 : 0;
+}
+
 static int elem_width(const cs_system *sys) {
   if (sys->kind == CS_SYS_GIBBS) return sys->dim == 18 ? 18 : 0;
   if (sys->target.kind == CS_TARGET_BLR) return 0;
@@ -658,10 +666,10 @@ int cs_system_elements_range(const cs_system *sys, const cs_deer_config *cfg, in
     return cs_system_elements(sys, cfg, dtype, iteration, s0, guess, e0, e1, e2, e3, u, d_stats, stream);
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   const int md = elem_width(sys);
-  const bool blr = !md && blr_mala_ok(*sys, cfg->mode) && blr_fused_ok(*sys, *cfg);
+  const bool blr = !md && blr_mala_ok(*sys, cfg->mode);
   if (!md && !blr)
-    return fail(CS_ERR_CONFIG, "step ranges need a register-kernel system or the fused logistic-regression "
-                               "builder (the other GEMM-backed builders take whole chains)");
+    return fail(CS_ERR_CONFIG, "step ranges need a register-kernel system or the logistic-regression builders "
+                               "(the wide leapfrog builder takes whole chains)");
   if (cfg->mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG)
     return fail(CS_ERR_CONFIG, "system does not provide a block2x2 Jacobian estimate");
   cudaStream_t st = S(stream);
@@ -669,7 +677,20 @@ int cs_system_elements_range(const cs_system *sys, const cs_deer_config *cfg, in
   if (n < 1) return CS_OK;
   cudaError_t e;
   if (blr) {
-    e = elements_blr_fused(*sys, *cfg, dtype, iteration, t0, n, s0, guess, e0, u, d_stats, st);
+    if (blr_fused_ok(*sys, *cfg)) {
+      e = elements_blr_fused(*sys, *cfg, dtype, iteration, t0, n, s0, guess, e0, u, d_stats, st);
+    } else {
+      // the dense (and many-probe) pipelines index noise by local row: hand them
+      // the shard as a chain of n steps whose noise tables start at step t0 + 1
+      // (their probes, the many-probe diag case, hash the local step: refused)
+      if (cfg->mode != CS_MODE_DENSE)
+        return fail(CS_ERR_CONFIG, "step ranges of the logistic-regression diag builder need <= 7 probes");
+      cs_system loc = *sys;
+      loc.T = n;
+      loc.noise_vec = (const char *)sys->noise_vec + (size_t)t0 * sys->dim * esize(dtype);
+      loc.noise_logu = sys->noise_logu + t0;
+      e = elements_blr(loc, *cfg, dtype, iteration, s0, guess, e0, u, d_stats, st);
+    }
     return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_elements_range (logistic-regression MALA)");
   }
   if (dtype == CS_F64) {

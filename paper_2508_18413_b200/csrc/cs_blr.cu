@@ -5,21 +5,22 @@
 // One Newton update needs, at every step t, grad/logp at the current state S_t
 // and at the proposal x~_t, plus hvp(S_t, z_k) and hvp(x~_t, dx~_k) for the
 // probe tangents (samplers.py:95-145, targets.py:254-287).  All of them are
-// row blocks of four plain GEMMs against the data matrix X:
+// row blocks of four plain GEMMs against the data matrix X (the fused builder
+// in cs_blr_fused.cu does all of this in one kernel for <= 7 probes; this
+// pipeline serves more probes):
 //   E1 = [S; Z] X^T          logits eta_S and the probes' z X^T
 //   G1 = [y - p_S; w_S.(Z X^T)] X       (w = p (1 - p))
 //   E2 = [x~; dx~] X^T
 //   G2 = [y - p~; w~.(dx~ X^T)] X
-// run by cuBLAS (FP64 tensor cores); the sigmoid / weight / row-sum epilogues
+// run by our DMMA GEMM (cs_gemm.cuh, FP64 tensor cores); the sigmoid / weight / row-sum epilogues
 // and the per-step MALA gate, tangents, Hutchinson estimate and element
 // formation (deer.py:171-183) are our kernels, one warp per step.
-#include <cublas_v2.h>
-
 #include <cstdlib>
 #include <mutex>
 
 #include "cs_apikern.cuh"
 #include "cs_dispatch.h"
+#include "cs_gemm.cuh"
 #include "cs_umma.cuh"
 
 namespace cs {
@@ -31,7 +32,6 @@ constexpr int kBlrCols = kBlrMaxD / 32;
 
 struct BlrCtx {
   std::mutex mu;
-  cublasHandle_t h = nullptr;
   double *buf = nullptr;
   size_t cap = 0;
 };
@@ -695,7 +695,6 @@ static cudaError_t blr_run(const cs_system &sys, const cs_deer_config &cfg, int6
   cudaGetDevice(&dev);
   BlrCtx &ctx = g_blr[dev & 15];
   std::lock_guard<std::mutex> lock(ctx.mu);
-  if (!ctx.h && cublasCreate(&ctx.h) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   // A, A2, G (M x D), E (M x N), gS (T x D), row sums 2 x (2T)
   const size_t need = (size_t)3 * M * D + (size_t)M * N + (size_t)T * D + (size_t)4 * T;
   if (ctx.cap < need) {
@@ -709,24 +708,23 @@ static cudaError_t blr_run(const cs_system &sys, const cs_deer_config &cfg, int6
   double *A = ctx.buf, *A2 = A + (size_t)M * D, *G = A2 + (size_t)M * D, *E = G + (size_t)M * D;
   double *gS = E + (size_t)M * N, *rsS = gS + (size_t)T * D, *rsX = rsS + 2 * T;
   const double *X = sys.target.X, *y = sys.target.y;
-  const double one = 1.0, zero = 0.0;
-  if (cublasSetStream(ctx.h, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
-  auto gemm_xt = [&](const double *Ain, double *Cout) {  // row-major C (M x N) = A (M x D) X^T
-    return cublasDgemm(ctx.h, CUBLAS_OP_T, CUBLAS_OP_N, N, (int)M, D, &one, X, D, Ain, D, &zero, Cout, N);
+  // the two data products on the FP64 tensor cores (cs_gemm.cuh), row-major
+  auto gemm_xt = [&](const double *Ain, double *Cout) {  // C (M x N) = A (M x D) X^T
+    return gemm_rm<double, double, double>(true, (int)M, N, D, Ain, D, 0, X, D, 0, Cout, N, 0, 1, st);
   };
-  auto gemm_x = [&](const double *Bin, double *Cout) {  // row-major C (M x D) = B (M x N) X
-    return cublasDgemm(ctx.h, CUBLAS_OP_N, CUBLAS_OP_N, D, (int)M, N, &one, X, D, Bin, N, &zero, Cout, D);
+  auto gemm_x = [&](const double *Bin, double *Cout) {  // C (M x D) = B (M x N) X
+    return gemm_rm<double, double, double>(false, (int)M, D, N, Bin, N, 0, X, D, 0, Cout, D, 0, 1, st);
   };
   const unsigned ge = (unsigned)((T * D + 255) / 256 < 148 * 32 ? (T * D + 255) / 256 : 148 * 32);
   const unsigned gw = (unsigned)((T * 32 + 255) / 256);
   k_blr_prologue<ST><<<ge, 256, 0, st>>>(sys, s0, guess, iteration, K, A);
-  if (gemm_xt(A, E) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_xt(A, E)) return ge;
   k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, K, N, rsS);
-  if (gemm_x(E, G) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_x(E, G)) return ge;
   k_blr_propose<ST><<<gw, 256, 0, st>>>(sys, s0, guess, A, G, K, A2, gS, stats);
-  if (gemm_xt(A2, E) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_xt(A2, E)) return ge;
   k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, K, N, rsX);
-  if (gemm_x(E, G) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_x(E, G)) return ge;
   k_blr_final<ST><<<gw, 256, 0, st>>>(sys, cfg, iteration, s0, guess, A, A2, G, gS, rsS, rsX, jout, uout, stats);
   return cudaGetLastError();
 }
@@ -766,7 +764,6 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   cudaGetDevice(&dev);
   BlrCtx &ctx = g_blr[dev & 15];
   std::lock_guard<std::mutex> lock(ctx.mu);
-  if (!ctx.h && cublasCreate(&ctx.h) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   // A, A2, G, gS, GX, R, HR (T x D); E, WS, WX (T x N); row sums 2 x (2T)
   // + Xf: X as f32 (N x 128, or its transpose 128 x ldx for tcgen05)
   const size_t need = (size_t)7 * T * D + (size_t)3 * T * N + (size_t)4 * T + (size_t)64 * (N + 32);
@@ -784,28 +781,26 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   double *rsS = WX + (size_t)T * N, *rsX = rsS + 2 * T;
   float *Xf = (float *)(rsX + 2 * T);
   const double *X = sys.target.X, *y = sys.target.y;
-  const double one = 1.0, zero = 0.0;
-  if (cublasSetStream(ctx.h, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
-  auto gemm_xt = [&](const double *Ain, double *Cout) {  // row-major C (T x N) = A (T x D) X^T
-    return cublasDgemm(ctx.h, CUBLAS_OP_T, CUBLAS_OP_N, N, (int)T, D, &one, X, D, Ain, D, &zero, Cout, N);
+  auto gemm_xt = [&](const double *Ain, double *Cout) {  // C (T x N) = A (T x D) X^T
+    return gemm_rm<double, double, double>(true, (int)T, N, D, Ain, D, 0, X, D, 0, Cout, N, 0, 1, st);
   };
-  auto gemm_x = [&](const double *Bin, double *Cout) {  // row-major C (T x D) = B (T x N) X
-    return cublasDgemm(ctx.h, CUBLAS_OP_N, CUBLAS_OP_N, D, (int)T, N, &one, X, D, Bin, N, &zero, Cout, D);
+  auto gemm_x = [&](const double *Bin, double *Cout) {  // C (T x D) = B (T x N) X
+    return gemm_rm<double, double, double>(false, (int)T, D, N, Bin, N, 0, X, D, 0, Cout, D, 0, 1, st);
   };
   const unsigned ge = (unsigned)((T * D + 255) / 256 < 148 * 32 ? (T * D + 255) / 256 : 148 * 32);
   const unsigned gw = (unsigned)((T * 32 + 255) / 256);
   k_blr_prologue<ST><<<ge, 256, 0, st>>>(sys, s0, guess, iteration, 0, A);
-  if (gemm_xt(A, E) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_xt(A, E)) return ge;
   k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsS, WS);
-  if (gemm_x(E, G) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_x(E, G)) return ge;
   k_blr_propose<ST><<<gw, 256, 0, st>>>(sys, s0, guess, A, G, 0, A2, gS, stats);
-  if (gemm_xt(A2, E) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_xt(A2, E)) return ge;
   k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsX, WX);
-  if (gemm_x(E, G) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_x(E, G)) return ge;
   k_bd_resid<ST><<<ge, 256, 0, st>>>(sys, s0, guess, A2, G, GX, R);
-  if (gemm_xt(R, E) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_xt(R, E)) return ge;
   k_bd_scale<<<148 * 32, 256, 0, st>>>(E, WX, T * N);
-  if (gemm_x(E, HR) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  if (cudaError_t ge = gemm_x(E, HR)) return ge;
   if constexpr (sizeof(ST) == 4) {
     if (bd_tensor_cores() == 2) {  // f32 storage: H(S) on the 5th-gen tensor cores (tcgen05, TMEM accumulator)
       const int ldx = (N + 31) / 32 * 32;

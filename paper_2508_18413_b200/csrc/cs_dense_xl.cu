@@ -3,7 +3,8 @@
 // _scan_kernels.py:47-99; deer.py:161-170 builds these elements for any D).
 //
 // D > 128 is past the register/shared-memory tiling of cs_dense.cu, so the
-// chunk compositions -- the scan's 2 T D^3 flop -- are batched library GEMMs:
+// chunk compositions -- the scan's 2 T D^3 flop -- are batched DMMA GEMMs
+// (cs_gemm.cuh):
 //   per step k of a chunk, every chunk at once:  [M|w]_q <- J_{t0_q+k} [M|w]_q
 //     (one strided-batched GEMM over the chunks, row-major D x (D+1) operands,
 //      the affine column riding along) + u_{t0_q+k} added to the last column
@@ -17,21 +18,14 @@
 // Aggregates: chunk maps (this file's or cs_dense.cu's) are lifted to
 // augmented (D+1) x (D+1) f64 matrices [[M, w], [0, 1]], where composing two
 // affine maps is a plain product, and folded as a balanced tree of batched
-// DGEMMs (log2(n) launches).
-#include <cublas_v2.h>
-
+// DMMA GEMMs (log2(n) launches).
 #include "cs_common.cuh"
+#include "cs_gemm.cuh"
 #include "cs_scan.cuh"
 
 namespace cs {
 
 namespace {
-
-cublasHandle_t xl_handle() {
-  static thread_local cublasHandle_t h = nullptr;
-  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
-  return h;
-}
 
 constexpr int kXlThr = 512;
 
@@ -180,22 +174,17 @@ static unsigned grid1(int64_t n) {
 // fold n augmented maps (earliest first) into the flat aggregate; buf holds
 // n + ceil(n/2) augmented matrices, the first n filled
 static cudaError_t tree_fold(double *buf, int64_t n, int D, double *out, cudaStream_t st) {
-  cublasHandle_t h = xl_handle();
-  if (!h) return cudaErrorUnknown;
-  if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   const int W = D + 1;
   const long long S = (long long)W * W;
   double *a = buf, *b = buf + n * S;
-  const double one = 1.0, zero = 0.0;
   while (n > 1) {
     const int64_t pairs = n / 2;
-    // row-major C = A_{2i+1} A_{2i} (later map applied last) <=> column-major
-    // C^T = A_{2i}^T A_{2i+1}^T: the buffers in the order (2i, 2i+1)
-    if (cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, W, W, W, &one, a, W, 2 * S, a + S, W, 2 * S, &zero,
-                                  b, W, S, (int)pairs) != CUBLAS_STATUS_SUCCESS)
-      return cudaErrorUnknown;
+    // pair i: C = A_{2i+1} A_{2i} (the later map applied last), batched DMMA GEMM
+    cudaError_t e = gemm_rm<double, double, double>(false, W, W, W, a + S, W, 2 * S, a, W, 2 * S, b, W, S,
+                                                    (int)pairs, st);
+    if (e != cudaSuccess) return e;
     if (n & 1) {
-      cudaError_t e = cudaMemcpyAsync(b + pairs * S, a + (n - 1) * S, S * sizeof(double), cudaMemcpyDeviceToDevice, st);
+      e = cudaMemcpyAsync(b + pairs * S, a + (n - 1) * S, S * sizeof(double), cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) return e;
     }
     n = (n + 1) / 2;
@@ -217,26 +206,16 @@ static cudaError_t xl_reduce(const ScanArgs<ST> &a, int c, int64_t nch, ST *Ma, 
       a.e0, a.u, D, c, Ma);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  cublasHandle_t h = xl_handle();
-  if (!h) return cudaErrorUnknown;
-  if (cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   const int64_t last_len = a.T - (nch - 1) * (int64_t)c;
-  const ST one = 1, zero = 0;
   ST *cur = Ma, *nxt = Mb;
   for (int k = 1; k < c; ++k) {
     const int64_t nq = k < last_len ? nch : nch - 1;  // only the last chunk can be short
     if (nq <= 0) break;
-    // row-major [M|w]' = J_t [M|w]  <=>  column-major X'^T = X^T J_t^T
-    cublasStatus_t s;
-    if constexpr (sizeof(ST) == 8)
-      s = cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)W, D, D, (const double *)&one,
-                                    (const double *)cur, (int)W, n, (const double *)a.e0 + (int64_t)k * D * D, D,
-                                    (long long)c * D * D, (const double *)&zero, (double *)nxt, (int)W, n, (int)nq);
-    else
-      s = cublasSgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)W, D, D, (const float *)&one,
-                                    (const float *)cur, (int)W, n, (const float *)a.e0 + (int64_t)k * D * D, D,
-                                    (long long)c * D * D, (const float *)&zero, (float *)nxt, (int)W, n, (int)nq);
-    if (s != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    // [M|w]' = J_t [M|w] for every chunk at once (row-major, batched DMMA GEMM;
+    // storage-type operands widened to f64, the product rounded back)
+    e = gemm_rm<ST, ST, ST>(false, D, (int)W, D, a.e0 + (int64_t)k * D * D, D, (int64_t)c * D * D, cur, W, n, nxt,
+                            W, n, (int)nq, st);
+    if (e != cudaSuccess) return e;
     k_xl_addu<ST><<<grid1(nq * D), 256, 0, st>>>(a.u, D, c, k, nq, nxt);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (nq < nch) {  // the short last chunk keeps its finished map

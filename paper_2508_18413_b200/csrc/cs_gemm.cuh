@@ -1,0 +1,155 @@
+// Row-major strided-batched GEMM on the FP64 tensor cores (DMMA, mma.sync
+// m8n8k4 f64), the library's one dense-product building block:
+//
+//   C[b] (M x N, ldc) = A[b] (M x K, lda) . op(B[b])
+//   op(B) = B (K x N, ldb)            BT = false
+//         = B^T with B given N x K    BT = true   (e.g. X^T of a data matrix X)
+//
+// Inputs are f32 or f64 and are widened to f64 on their way into shared
+// memory; accumulation is f64, the result is rounded once to C's type.  Tiles:
+// BM x 64 outputs per CTA (BM = 64: 16 warps, BM = 32: 8 warps), each warp a
+// 16 x 16 block (2 x 2 DMMA tiles); K in steps of 16, the next step's operands
+// loaded into registers while the current one is multiplied (double-buffered
+// shared memory).  Strides of the staged tiles are chosen so every DMMA
+// fragment load is bank-conflict free.  The summation order is fixed (k
+// ascending per output), so results are reproducible bit for bit.
+//
+// Used by the wide leapfrog builder (A . P, cfg 4), the dense logistic-
+// regression builder ([S; z] X^T and P X, cfg 3 "full") and the dense affine
+// aggregates / D > 128 dense scans (products of augmented maps).
+#pragma once
+#include "cs_common.cuh"
+
+namespace cs {
+
+namespace gemm_detail {
+
+constexpr int kBK = 16, kBN = 64;
+constexpr int kLDA = kBK + 4;  // 20 doubles: A fragments conflict free
+constexpr int kLDB = kBN + 4;  // 68 doubles: B fragments conflict free
+
+CS_D void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <typename T>
+CS_D double ldg_d(const T *p) {
+  return (double)__ldg(p);
+}
+
+template <int BM, bool BT, typename TA, typename TB, typename TC>
+__global__ void __launch_bounds__(BM * 8)
+k_gemm(int M, int N, int K, const TA *__restrict__ A, int64_t lda, int64_t sA, const TB *__restrict__ B,
+       int64_t ldb, int64_t sB, TC *__restrict__ C, int64_t ldc, int64_t sC) {
+  constexpr int NT = BM * 8;                     // threads
+  constexpr int EA = BM * kBK / NT;              // A elements per thread per K step (2)
+  constexpr int EB = kBK * kBN / NT;             // B elements per thread per K step (2 or 4)
+  __shared__ __align__(16) double As[2][BM * kLDA];
+  __shared__ __align__(16) double Bs[2][kBK * kLDB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / (kBN / 16), wn = warp % (kBN / 16);  // warp grid (BM/16) x 4
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * kBN;
+  A += (int64_t)blockIdx.z * sA;
+  B += (int64_t)blockIdx.z * sB;
+  C += (int64_t)blockIdx.z * sC;
+  double ra[EA], rb[EB];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < EA; ++e) {
+      const int i = tid + e * NT, r = i / kBK, k = i % kBK;
+      const int gm = m0 + r, gk = k0 + k;
+      ra[e] = (gm < M && gk < K) ? ldg_d(A + (int64_t)gm * lda + gk) : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < EB; ++e) {
+      const int i = tid + e * NT;
+      if constexpr (BT) {  // B^T given N x K: walk k fastest (coalesced)
+        const int n = i / kBK, k = i % kBK;
+        const int gn = n0 + n, gk = k0 + k;
+        rb[e] = (gn < N && gk < K) ? ldg_d(B + (int64_t)gn * ldb + gk) : 0.0;
+      } else {
+        const int k = i / kBN, n = i % kBN;
+        const int gn = n0 + n, gk = k0 + k;
+        rb[e] = (gn < N && gk < K) ? ldg_d(B + (int64_t)gk * ldb + gn) : 0.0;
+      }
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < EA; ++e) {
+      const int i = tid + e * NT;
+      As[buf][(i / kBK) * kLDA + i % kBK] = ra[e];
+    }
+#pragma unroll
+    for (int e = 0; e < EB; ++e) {
+      const int i = tid + e * NT;
+      if constexpr (BT) Bs[buf][(i % kBK) * kLDB + i / kBK] = rb[e];
+      else Bs[buf][(i / kBN) * kLDB + i % kBN] = rb[e];
+    }
+  };
+  double c[2][2][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) c[mi][ni][0] = c[mi][ni][1] = 0.0;
+  const int nk = (K + kBK - 1) / kBK;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int s = 0; s < nk; ++s) {
+    const int buf = s & 1;
+    if (s + 1 < nk) load((s + 1) * kBK);  // in flight while this step multiplies
+    const double *as = As[buf] + (wm * 16 + (lane >> 2)) * kLDA + (lane & 3);
+    const double *bs = Bs[buf] + (lane & 3) * kLDB + wn * 16 + (lane >> 2);
+#pragma unroll
+    for (int k0 = 0; k0 < kBK; k0 += 4) {
+      const double a0 = as[k0], a1 = as[8 * kLDA + k0];
+      const double b0 = bs[k0 * kLDB], b1 = bs[k0 * kLDB + 8];
+      dmma884(c[0][0], a0, b0);
+      dmma884(c[0][1], a0, b1);
+      dmma884(c[1][0], a1, b0);
+      dmma884(c[1][1], a1, b1);
+    }
+    if (s + 1 < nk) {
+      store(buf ^ 1);  // the other buffer's last readers finished before the previous barrier
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int gm = m0 + wm * 16 + mi * 8 + (lane >> 2);
+      const int gn = n0 + wn * 16 + ni * 8 + 2 * (lane & 3);
+      if (gm >= M) continue;
+      if (gn < N) C[(int64_t)gm * ldc + gn] = (TC)c[mi][ni][0];
+      if (gn + 1 < N) C[(int64_t)gm * ldc + gn + 1] = (TC)c[mi][ni][1];
+    }
+}
+
+}  // namespace gemm_detail
+
+// C = A . op(B) for `batch` independent problems (see the header comment).
+// Small problems (fewer than ~2 waves of 64 x 64 tiles) take 32 x 64 tiles.
+template <typename TA, typename TB, typename TC>
+cudaError_t gemm_rm(bool bt, int M, int N, int K, const TA *A, int64_t lda, int64_t sA, const TB *B, int64_t ldb,
+                    int64_t sB, TC *C, int64_t ldc, int64_t sC, int batch, cudaStream_t st) {
+  using namespace gemm_detail;
+  if (M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
+  const int64_t tiles64 = (int64_t)((M + 63) / 64) * ((N + kBN - 1) / kBN) * batch;
+  const bool small = tiles64 < 2 * 148;
+  const int BM = small ? 32 : 64;
+  const dim3 grid((N + kBN - 1) / kBN, (M + BM - 1) / BM, batch);
+  if (small) {
+    if (bt) k_gemm<32, true, TA, TB, TC><<<grid, 256, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
+    else k_gemm<32, false, TA, TB, TC><<<grid, 256, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  } else {
+    if (bt) k_gemm<64, true, TA, TB, TC><<<grid, 512, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
+    else k_gemm<64, false, TA, TB, TC><<<grid, 512, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace cs

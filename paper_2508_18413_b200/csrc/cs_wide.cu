@@ -3,19 +3,19 @@
 //
 // Per Newton iteration every step t needs grad(x'_t) = -(x'_t - mu) P and the
 // Hutchinson products hvp(x'_t, z_tk) = -z_tk P (samplers.py:188-222), i.e.
-// one (T*(1+K)) x n by n x n product -- a plain dense GEMM, done by cuBLAS on
-// the FP64 tensor cores.  Two kernels wrap it:
+// one (T*(1+K)) x n by n x n product -- a plain dense GEMM, done by our DMMA
+// GEMM (cs_gemm.cuh) on the FP64 tensor cores.  Two kernels wrap it:
 //   k_wide_prologue  x'_t = x + eps v / m  (minus mu) and the +-1 probes,
 //                    written as the GEMM's row-major A operand
 //   k_wide_epilogue  v'_t, the finite / Picard checks, d_hat, the block
 //                    (a, b, c, d) with preconditioner, damping and clip, and
 //                    u = f - M prev (deer.py:184-204) -- one CTA per step
 // The result feeds cs_scan_block_update exactly like the register builders.
-#include <cublas_v2.h>
 
 #include <mutex>
 
 #include "cs_apikern.cuh"
+#include "cs_gemm.cuh"
 
 namespace cs {
 
@@ -23,7 +23,6 @@ namespace {
 
 struct WideCtx {
   std::mutex mu;
-  cublasHandle_t h = nullptr;
   double *buf = nullptr;  // A (M x n) then C (M x n), f64
   size_t cap = 0;         // doubles
 };
@@ -132,7 +131,6 @@ static cudaError_t wide_run(const cs_system &sys, const cs_deer_config &cfg, int
   cudaGetDevice(&dev);
   WideCtx &ctx = g_wide[dev & 15];
   std::lock_guard<std::mutex> lock(ctx.mu);
-  if (!ctx.h && cublasCreate(&ctx.h) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   const size_t need = (size_t)2 * M * n;
   if (ctx.cap < need) {
     if (ctx.buf) cudaFree(ctx.buf);  // cudaFree synchronises: growth happens once per shape
@@ -148,12 +146,9 @@ static cudaError_t wide_run(const cs_system &sys, const cs_deer_config &cfg, int
   k_wide_prologue<ST><<<g1 < 1 ? 1 : g1, 256, 0, st>>>(sys, s0, guess, iteration, K, A);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  // row-major C (M x n) = A (M x n) P (n x n); column-major view: C^T = P^T A^T = P A^T (P symmetric)
-  if (cublasSetStream(ctx.h, st) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
-  const double one = 1.0, zero = 0.0;
-  if (cublasDgemm(ctx.h, CUBLAS_OP_N, CUBLAS_OP_N, n, (int)M, n, &one, sys.target.prec, n, A, n, &zero, C, n) !=
-      CUBLAS_STATUS_SUCCESS)
-    return cudaErrorUnknown;
+  // C (M x n) = A (M x n) P (n x n), row-major, on the FP64 tensor cores (cs_gemm.cuh)
+  e = gemm_rm<double, double, double>(false, (int)M, n, n, A, n, 0, sys.target.prec, n, 0, C, n, 0, 1, st);
+  if (e != cudaSuccess) return e;
   const unsigned g2 = (unsigned)(T < 148 * 8 ? T : 148 * 8);
   k_wide_epilogue<ST><<<g2 < 1 ? 1 : g2, 256, 0, st>>>(sys, s0, guess, A, C, K, cfg.atol, cfg.rtol,
                                                         cfg.preconditioner, cfg.damping, cfg.clip, e0, e1, e2, e3, u,

@@ -196,8 +196,10 @@ def _gather(vec: torch.Tensor, group, world):
 
 
 def _streamed_shard_ok(system, cfg) -> bool:
-    """Register-kernel systems: the shard runs the streamed engine's launches."""
-    if not (getattr(system, "desc", None) is not None and getattr(system, "kernels", False) and not cfg.full_trace
+    """Built-in systems whose element builder takes a step range (register
+    kernels, Gibbs, logistic-regression MALA): the shard runs the streamed
+    engine's launches."""
+    if not (getattr(system, "desc", None) is not None and not cfg.full_trace
             and getattr(system, "leapfrog_mode", "sequential") != "parallel"
             and cfg.mode in ("diag-stochastic", "block2x2-stochastic", "dense")):
         return False
@@ -205,8 +207,11 @@ def _streamed_shard_ok(system, cfg) -> bool:
     from .deer import _MODE_CODE
 
     d = system.desc()
-    return bool(_lib.load().cs_system_elements_supported(ctypes.byref(d), _MODE_CODE[cfg.mode],
-                                                         _lib.dtype_code(system.dtype)))
+    c = _lib.cs_deer_config()
+    c.mode = _MODE_CODE[cfg.mode]
+    c.hutchinson_samples = int(cfg.hutchinson_samples)
+    return bool(_lib.load().cs_system_elements_range_supported(ctypes.byref(d), ctypes.byref(c),
+                                                               _lib.dtype_code(system.dtype)))
 
 
 def run_deer_sharded(system, s0, cfg, ops: ShardOps | None = None, group=None, max_iters=None) -> ShardResult:

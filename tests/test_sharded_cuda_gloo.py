@@ -30,6 +30,11 @@ def _system(name):
         k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.gaussian([1.0, -1.0], [[1.0, 0.0], [-0.6, 1.2]])), 0.4,
                           seed=0, T=2001)
         return k, np.zeros(2), cs.DeerConfig(mode="dense")
+    if name in ("blr_diag", "blr_dense"):  # BASELINE cfg 3's chain (reduced T): the logistic-regression builders
+        X, y, _ = cs.synthetic_credit_like(seed=20250819, n=1000, dim=100)
+        m = cs.model_logp_grad_hvp(cs.blr(X, y, 1.0))
+        k = cs.MalaKernel(m, 0.003, seed=4, T=601 if name == "blr_diag" else 301)
+        return k, np.zeros(100), cs.DeerConfig(mode="diag-stochastic" if name == "blr_diag" else "dense")
     if name == "explode":  # plain diag quasi-Newton diverges on this chain (clip=1 is what tames it)
         m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
         return cs.HmcKernel(m, 0.5, 8, seed=0, T=3001), np.zeros(2), cs.DeerConfig(mode="diag-stochastic")
@@ -65,7 +70,7 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["hmc", "gibbs", "mala_dense"])
+@pytest.mark.parametrize("name", ["hmc", "gibbs", "mala_dense", "blr_diag", "blr_dense"])
 def test_two_rank_streamed_shards_match_run_deer(cuda_device, name):
     import paper_2508_18413_b200 as cs
 
