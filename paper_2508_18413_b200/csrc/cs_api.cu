@@ -764,21 +764,26 @@ int cs_deer_supported(const cs_system *sys, int mode, int dtype) {
 }
 
 int cs_leapfrog_batch_supported(const cs_system *sys, int32_t mode, int dtype) {
-  return sys && dtype_ok(dtype) && leapfrog_batch_ok(*sys, mode) ? 1 : 0;
+  return sys && dtype_ok(dtype) && (leapfrog_batch_ok(*sys, mode) || wide_leapfrog_ok(*sys, mode)) ? 1 : 0;
 }
 
 int cs_leapfrog_batch_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, int32_t B, const void *s0s,
                             void *finals, int32_t *info, int64_t *err_step, void *stream) {
   if (!sys || !cfg || !info || !err_step) return fail(CS_ERR_CONFIG, "null argument");
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
-  if (!leapfrog_batch_ok(*sys, cfg->mode)) return fail(CS_ERR_CONFIG, "batched leapfrog solve: unsupported system/mode");
+  const bool narrow = leapfrog_batch_ok(*sys, cfg->mode);
+  if (!narrow && !wide_leapfrog_ok(*sys, cfg->mode))
+    return fail(CS_ERR_CONFIG, "batched leapfrog solve: unsupported system/mode");
   if (cfg->max_iters < 1 || cfg->hutchinson_samples < 1 || !(cfg->atol > 0) || !(cfg->rtol >= 0) ||
       !(cfg->damping > 0 && cfg->damping <= 1) || !(cfg->clip > 0))
     return fail(CS_ERR_CONFIG, "bad solver configuration");
   if (B < 0) return fail(CS_ERR_STRUCTURAL, "negative batch");
   if (B == 0) return CS_OK;
+  // register-width trajectories: one CTA per proposal; dense Gaussian targets
+  // of any width (cfg 4): all proposals' passes share one DMMA GEMM per iteration
   const cudaError_t e =
-      leapfrog_batch_solve(*sys, *cfg, dtype, B, s0s, finals, info, (long long *)err_step, S(stream));
+      narrow ? leapfrog_batch_solve(*sys, *cfg, dtype, B, s0s, finals, info, (long long *)err_step, S(stream))
+             : wide_batch_solve(*sys, *cfg, dtype, B, s0s, finals, info, (long long *)err_step, S(stream));
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "batched leapfrog solve");
 }
 

@@ -17,6 +17,8 @@ cudaError_t elements_blr_fused(const cs_system &sys, const cs_deer_config &cfg, 
                                int64_t t0, int64_t n, const void *s0, const void *guess, void *j, void *u,
                                cs_elem_stats *stats, cudaStream_t st);
 bool leapfrog_batch_ok(const cs_system &s, int mode);
+cudaError_t wide_batch_solve(const cs_system &sys, const cs_deer_config &cfg, int dtype, int B, const void *s0s,
+                             void *finals, int32_t *info, long long *err_step, cudaStream_t st);
 cudaError_t leapfrog_batch_solve(const cs_system &sys, const cs_deer_config &cfg, int dtype, int B, const void *s0s,
                                  void *finals, int32_t *info, long long *err_step, cudaStream_t st);
 cudaError_t debug_gram(const double *X, int N, int D, const double *W, int64_t T, float *H, cudaStream_t st);

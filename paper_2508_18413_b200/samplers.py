@@ -431,10 +431,11 @@ class HmcKernel(_Fused):
         per proposal runs its own Newton loop); rows are then taken in order with
         the reference's semantics -- the first diverged row raises, rows that did
         not converge fall back to the sequential integrator.  None when the
-        configuration needs the per-row engine (window, full trace, other modes)."""
+        configuration needs the per-row engine (window, full trace, other modes, an
+        explicitly chosen engine)."""
         from .deer import _DIVERGENCE_FACTOR, default_max_iters
 
-        if (cfg.mode != "block2x2-stochastic" or cfg.full_trace or getattr(cfg, "engine", "auto") == "host"
+        if (cfg.mode != "block2x2-stochastic" or cfg.full_trace or getattr(cfg, "engine", "auto") != "auto"
                 or (cfg.window_len is not None and cfg.window_len < system.T)):
             return None
         lib = _lib.load()

@@ -258,3 +258,44 @@ def test_batched_inner_solves_match_per_row_runs(cuda_device, target, eps, L, ma
     fast.fallback_events.clear(), slow.fallback_events.clear()
     np.testing.assert_allclose(np_(fast.step_batch(ts, S)), np_(slow.step_batch(ts, S)), atol=1e-10, rtol=1e-10)
     assert fast.fallback_events == slow.fallback_events
+
+
+def test_parallel_leapfrog_chain_matches_reference_golden(cuda_device):
+    # the reference's own HmcKernel(leapfrog_mode="parallel") chain (make_golden.py:
+    # Rosenbrock, eps 0.2, L 16, seed 5, T 40), every proposal an inner block
+    # quasi-Newton solve -- here all rows' solves batched on the device
+    g = np.load(__import__("conftest").GOLDEN + "/hmc_parallel_leapfrog.npz")
+    model = cs.model_logp_grad_hvp(cs.rosenbrock(b=0.1, scale2=1.0))
+    k = cs.HmcKernel(model, 0.2, 16, seed=5, T=40, leapfrog_mode="parallel",
+                     leapfrog_cfg=cs.DeerConfig(mode="block2x2-stochastic"))
+    np.testing.assert_allclose(np_(cs.sequential_evaluate(k, np.array([0.5, -0.5]))), g["seq"], atol=1e-8, rtol=1e-8)
+    assert [tuple(e) for e in g["fallbacks"]] == [tuple(e) for e in k.fallback_events]
+
+
+def _wide_gauss(n, seed=0):
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.normal(size=(n, n)))
+    lam = np.exp(rng.uniform(np.log(0.1), np.log(10.0), n))
+    return cs.model_logp_grad_hvp(cs.gaussian(np.zeros(n), np.linalg.cholesky((Q * lam) @ Q.T)))
+
+
+@pytest.mark.parametrize("n,L,eps,T,max_iters", [(16, 24, 0.1, 12, None), (16, 24, 0.1, 6, 2),
+                                                 (1000, 100, 0.05, 4, None)])
+def test_wide_batched_inner_solves_match_per_row_runs(cuda_device, n, L, eps, T, max_iters):
+    # BASELINE cfg 4's proposals (dense Gaussian, n up to 1000, L = 100): every
+    # row's inner solve batched (one DMMA GEMM per Newton pass for all rows)
+    # against the per-row run_deer loop of samplers.py:301-320 on the streamed
+    # engine -- same states, same fallback events
+    model = _wide_gauss(n)
+    kw = {} if max_iters is None else dict(max_iters=max_iters)
+    fast = hmc_chain_system(model, eps=eps, L=L, seed=3, T=T, leapfrog_mode="parallel",
+                            leapfrog_cfg=cs.DeerConfig(mode="block2x2-stochastic", **kw))
+    slow = hmc_chain_system(model, eps=eps, L=L, seed=3, T=T, leapfrog_mode="parallel",
+                            leapfrog_cfg=cs.DeerConfig(mode="block2x2-stochastic", engine="streamed", **kw))
+    x0 = np.random.default_rng(1).normal(size=n)
+    a = np_(cs.sequential_evaluate(fast, x0))
+    b = np_(cs.sequential_evaluate(slow, x0))
+    assert fast.fallback_events == slow.fallback_events
+    if max_iters is not None:
+        assert len(fast.fallback_events) > 0
+    np.testing.assert_allclose(a, b, atol=1e-10, rtol=1e-10)

@@ -90,6 +90,21 @@ def main():
         lf = cs.LeapfrogSystem(m, eps, L, dtype=torch.float64)
         ms, r = timed(lambda: cs.run_deer(lf, s0, cs.DeerConfig(mode="block2x2-stochastic")), 5)
         rows.append(("cfg4 leapfrog Gaussian D=1000 L=100 block (per proposal)", ms, r, L, None))
+    if "4p" in which:
+        # HMC with the parallel leapfrog inside each proposal at cfg 4's width: one
+        # batched step_batch over B chain rows (every row's inner block solve)
+        D, eps, L, B = 1000, 0.05, 100, 64
+        m = cs.model_logp_grad_hvp(cs.gaussian(np.zeros(D), cfg4_chol(D)))
+        S = torch.as_tensor(np.random.default_rng(1).normal(size=(B, D)), device="cuda")
+        ts = torch.arange(1, B + 1, device="cuda")
+        for eng in ("auto", "streamed"):
+            k = cs.HmcKernel(m, eps, L, seed=3, T=B, leapfrog_mode="parallel",
+                             leapfrog_cfg=cs.DeerConfig(mode="block2x2-stochastic", engine=eng))
+            ms, _ = timed(lambda: k.step_batch(ts, S), 2)
+            print(json.dumps({"config": f"cfg4 HMC parallel-leapfrog D=1000 L=100, step_batch over {B} rows",
+                              "inner": "batched (one GEMM per pass for all rows)" if eng == "auto" else
+                              "per-row run_deer (streamed)", "ms": round(ms, 3), "ms_per_proposal": round(ms / B, 3),
+                              "fallbacks": len(k.fallback_events)}), flush=True)
     if "5" in which:
         k = cs.GibbsKernel(cs.generate_eight_schools(), seed=0, T=1_000_000, dtype=dt)
         s0 = k.initial_state()
