@@ -5,10 +5,15 @@
 //   block2x2  a,b,c,d (T,D), u (T,2D) [x|v]   -> scan_rows<BLOCK> (D <= 64)
 //   both, wide D > 64                         -> scan_cols<...>
 //   dense     J (T,D,D), u (T,D), D <= 8      -> scan_dense_small<MD>
-// All are single-pass: each tile is read from HBM once into shared memory (or
-// registers), reduced, linked to its predecessors by decoupled look-back,
-// replayed and written once -- 12 B/element (diag, f32) of algorithmic
-// traffic.  Carries and composition run in f64 regardless of storage type.
+// The column and dense scans are single-pass: each tile is read from HBM once,
+// reduced, linked to its predecessors by decoupled look-back, replayed and
+// written once (12 B/element diag f32).  The row scan is two-pass over chunks
+// (A: reduce, C: re-read and replay a round later, see scan_rows): j, u are
+// read twice, 20 B/element of HBM traffic against the 12 B algorithmic.
+// Carries and composition run in f64 regardless of storage type; every
+// chunk's entry state is the fixed chain exit(k) = A_k(exit(k-1)) from s0
+// (lookback_cta applies aggregates one at a time), so results are bit-
+// identical run to run however the look-back races resolve.
 #include <cstdlib>
 
 #include "cs_lookback.cuh"
@@ -177,15 +182,11 @@ constexpr int kLbWindow = 32 * kLbPerLane;          // 128 predecessors per roun
 template <int VAR, class G = CtaGrp, class StatusF, class AggF, class ExitF, class ExitVF, class S0F, class S0VF>
 CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF exit_x, ExitVF exit_v,
                        S0F s0x, S0VF s0v, double *s_acc, double *s_entry, int *s_ctl) {
-  constexpr int W = ColElem<VAR>::W;
-  constexpr int NW = G::kN / 32;
+  (void)s_acc;
   const int tid = G::tid(), lane = tid & 31, wid = tid >> 5;
-  for (int c = tid; c < ncol; c += G::kN) {
-    ColElem<VAR> id;
-    id.ident();
-    id.store(s_acc + c * W);
-  }
-  int64_t hi = pos - 1;
+  // (1) the nearest published exit state at or before pos - 1, scanning back
+  // window by window; every tile between it and pos has its aggregate out
+  int64_t hi = pos - 1, pe = -1;
   for (;;) {
     G::sync();
     if (wid == 0) {
@@ -210,50 +211,40 @@ CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF ex
     }
     G::sync();
     const int stop = s_ctl[0];
-    for (int c = wid; c < ncol; c += NW) {
-      // each lane folds its K tiles (latest applied last), then an ordered tree
-      ColElem<VAR> e;
-      e.ident();
-#pragma unroll
-      for (int j = kLbPerLane - 1; j >= 0; --j) {
-        const int idx = lane * kLbPerLane + j;
-        if (idx < stop) {
-          ColElem<VAR> a;
-          a.load_cg(agg(hi - idx, c));
-          e.push(a);  // e <- a o e: tile hi-idx is later than hi-idx-1
-        }
-      }
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        ColElem<VAR> o = e.down(off);
-        if (lane + off < 32) e.pre(o);  // later lanes hold earlier tiles
-      }
-      if (lane == 0) {
-        ColElem<VAR> acc;
-        acc.load(s_acc + c * W);
-        acc.pre(e);
-        acc.store(s_acc + c * W);
-      }
-    }
     if (stop < kLbWindow) {
-      G::sync();
-      const int64_t pe = hi - stop;
-      for (int c = tid; c < ncol; c += G::kN) {
-        double x = pe < 0 ? s0x(c) : exit_x(pe, c);
-        double v = 0.0;
-        if (VAR == SCAN_BLOCK) v = pe < 0 ? s0v(c) : exit_v(pe, c);
-        ColElem<VAR> acc;
-        acc.load(s_acc + c * W);
-        if constexpr (VAR == SCAN_DIAG) acc.apply(x);
-        else acc.apply(x, v);
-        s_entry[c] = x;
-        if (VAR == SCAN_BLOCK) s_entry[ncol + c] = v;
-      }
-      G::sync();
-      return;
+      pe = hi - stop;
+      break;
     }
     hi -= kLbWindow;
   }
+  // (2) apply the aggregates pe+1 .. pos-1 to that exit ONE AT A TIME, oldest
+  // first.  Every published exit is itself exit(k) = A_k(exit(k-1)) from s0,
+  // so whichever exit the scan found, the entry is the same chain of single
+  // applications -- the same bits run to run (the reference's fixed-chunk
+  // property, _scan_kernels.py:3-8), independent of publication timing.
+  // (Composing the aggregates first and applying the product once would round
+  // differently depending on where the look-back stopped.)
+  constexpr int kB = VAR == SCAN_DIAG ? 8 : 1;  // block: 6 doubles per aggregate, keep register pressure low
+  for (int c = tid; c < ncol; c += G::kN) {
+    double x = pe < 0 ? s0x(c) : exit_x(pe, c);
+    double v = 0.0;
+    if (VAR == SCAN_BLOCK) v = pe < 0 ? s0v(c) : exit_v(pe, c);
+    for (int64_t k0 = pe + 1; k0 < pos; k0 += kB) {
+      ColElem<VAR> e[kB];
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+        if (k0 + j < pos) e[j].load_cg(agg(k0 + j, c));  // a batch of loads in flight, then the chain
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        if (k0 + j >= pos) break;
+        if constexpr (VAR == SCAN_DIAG) e[j].apply(x);
+        else e[j].apply(x, v);
+      }
+    }
+    s_entry[c] = x;
+    if (VAR == SCAN_BLOCK) s_entry[ncol + c] = v;
+  }
+  G::sync();
 }
 
 // Two-level look-back for row tiles (see cs_lookback.cuh).  On return

@@ -3,11 +3,16 @@
 
 An element (J_t, u_t) maps s -> J_t s + u_t in one of three carriers:
 Diag (j, u), Dense (J, u), Block2x2 (a, b, c, d, u) on a stacked [x, v] state
-(pscan.py:100-173).  ``parallel_affine_solve`` runs the single-pass CUDA scans
-of csrc/cs_scan.cu: tiles staged in shared memory, linked by decoupled
-look-back, f64 carries.  ``workers`` / ``chunk`` are accepted for API
-compatibility; the device tiling is fixed, so results are bit-identical run
-to run regardless of them.
+(pscan.py:100-173).  ``parallel_affine_solve`` runs the CUDA scans of
+csrc/cs_scan.cu: chunks of rows reduced and replayed with f64 carries, linked
+by look-back.  Every chunk's entry state is the fixed chain
+exit(k) = A_k(exit(k-1)) from s0 -- the look-back applies the aggregates it
+needs one at a time instead of composing them first -- so for a given shape
+the result is bit-identical run to run however the look-back races resolve
+(the reference's fixed-chunk property, _scan_kernels.py:3-8;
+tests/test_parity_baseline_gpu.py::test_scan_bit_identical_run_to_run).
+``workers`` / ``chunk`` are accepted for API compatibility; the device tiling
+depends only on the shape.
 """
 
 from __future__ import annotations
