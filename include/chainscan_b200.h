@@ -172,6 +172,10 @@ int cs_scan_aggregate(int mode, int dtype, const void *e0, const void *e1, const
 /* The three reductions below write into caller-owned DEVICE scalars (the host
  * reads them once per iteration, after the stream work it needs is queued).
  * First row (0-based) with a non-finite entry, INT64_MAX if none (deer.py:135-144). */
+/* First row r < n with last_fail[r] == iteration into *d_first (device,
+ * INT64_MAX if none): the sliding window's advance to the first step that
+ * failed the update test (deer.py:318, w = lo + argmax(fail)). */
+int cs_first_stamped_row(const int32_t *last_fail, int64_t n, int32_t iteration, int64_t *d_first, void *stream);
 int cs_first_nonfinite_row(int dtype, const void *x, int64_t n, int64_t width,
                            int64_t *d_first, void *stream);
 /* converged(prev, next): *d_notok = #entries with !(|next-prev| <= atol + rtol|next|),

@@ -81,6 +81,7 @@ _SIGS = {
     "cs_scan_dense": ([ctypes.c_int, P, P, P, P, i64, i32, P, szt, P], ctypes.c_int),
     "cs_scan_aggregate": ([ctypes.c_int, ctypes.c_int, P, P, P, P, P, i64, i32, P, P, szt, P], ctypes.c_int),
     "cs_first_nonfinite_row": ([ctypes.c_int, P, i64, i64, P, P], ctypes.c_int),
+    "cs_first_stamped_row": ([P, i64, i32, P, P], ctypes.c_int),
     "cs_converged": ([ctypes.c_int, P, P, i64, f64, f64, P, P, P], ctypes.c_int),
     "cs_update_bookkeeping": ([ctypes.c_int, P, P, i64, i32, f64, f64, i32, P, P, P, P], ctypes.c_int),
     "cs_form_diag": ([ctypes.c_int, P, P, P, P, i64, i32, P, f64, f64, P, P, P], ctypes.c_int),

@@ -259,6 +259,18 @@ __global__ void k_init_stats(cs_elem_stats *s) {
   s->dmax = 0.0;
 }
 
+// first row whose last-fail stamp is `it` (the window advance of deer.py:318)
+__global__ void k_first_stamp(const int32_t *lf, int64_t n, int32_t it, long long *out) {
+  long long best = kNoStep;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    if (lf[r] == it) {
+      best = r;
+      break;
+    }
+  best = warp_min_nn64(best);
+  if ((threadIdx.x & 31) == 0 && best != kNoStep) atomicMin(out, best);
+}
+
 // Per (device, stream) solver state that outlives a call: the grid control
 // block and halo stamps (zeroed once here, left zeroed by every solve), the
 // host-mapped outcome record and a pair of timing events.
@@ -422,6 +434,14 @@ int cs_scan_aggregate(int mode, int dtype, const void *e0, const void *e1, const
 }
 
 // ---- building blocks -------------------------------------------------------------
+int cs_first_stamped_row(const int32_t *last_fail, int64_t n, int32_t iteration, int64_t *d_first, void *stream) {
+  if (!last_fail || !d_first || n < 0) return fail(CS_ERR_CONFIG, "bad arguments");
+  k_set_i64<<<1, 1, 0, S(stream)>>>((long long *)d_first, kNoStep);
+  if (n > 0) k_first_stamp<<<grid_for(n, 256), 256, 0, S(stream)>>>(last_fail, n, iteration, (long long *)d_first);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_first_stamped_row");
+}
+
 int cs_first_nonfinite_row(int dtype, const void *x, int64_t n, int64_t width, int64_t *d_first,
                            void *stream) {
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");

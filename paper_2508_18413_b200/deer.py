@@ -422,6 +422,9 @@ def run_deer(system: TransitionSystem, s0, cfg: DeerConfig) -> DeerResult:
     T = system.T
     _pre_tensor(cfg, system.device, system.dim)  # length check before any engine runs
     max_iters = cfg.max_iters if cfg.max_iters is not None else default_max_iters(T)
+    if (cfg.window_len is not None and cfg.window_len < T and cfg.engine != "host" and not cfg.full_trace
+            and _window_ok(system, cfg)):
+        return _run_streamed_window(system, s0, cfg, max_iters)
     engine = _pick_engine(system, cfg)
     if engine == "fused":
         return _run_fused(system, s0, cfg, max_iters)
@@ -563,6 +566,140 @@ def _run_streamed(system, s0, cfg, max_iters):
     return DeerResult(trace=guess, iterations=it, delta_history=np.array(hist), converged=done,
                       per_step_converged_at=last_fail + 1, full_trace=None,
                       stats={"path": "streamed", "launches": launches})
+
+
+def _window_ok(system, cfg):
+    """Built-in systems whose element builder takes a step range."""
+    if getattr(system, "desc", None) is None or getattr(system, "leapfrog_mode", "sequential") == "parallel":
+        return False
+    cache = system.__dict__.setdefault("_range_support", {})
+    key = (cfg.mode, cfg.hutchinson_samples, system.dtype)
+    if key not in cache:
+        d = system.desc()
+        c = _lib.cs_deer_config()
+        c.mode = _MODE_CODE[cfg.mode]
+        c.hutchinson_samples = int(cfg.hutchinson_samples)
+        cache[key] = bool(_lib.load().cs_system_elements_range_supported(ctypes.byref(d), ctypes.byref(c),
+                                                                          _lib.dtype_code(system.dtype)))
+    return cache[key]
+
+
+def _run_streamed_window(system, s0, cfg, max_iters):
+    """The sliding-window solve of deer.py:287-319 on the device: each pass
+    builds f, the Picard test and the elements of the window's steps in ONE
+    launch (cs_system_elements_range: noise and probes at the absolute step,
+    the seed row guess[lo-1] as the state before the window), runs the update
+    scan with the bookkeeping fused (stamps last_fail[lo:hi] = iteration) and
+    finds the first failing step on the device; one 48-byte read decides the
+    branch and the window's advance, in the reference's order."""
+    lib = _lib.load()
+    T, D = system.T, system.dim
+    dev, dtype = system.device, system.dtype
+    dt = _lib.dtype_code(dtype)
+    st = _lib.stream_ptr()
+    d = system.desc()
+    c = _lib.cs_deer_config()
+    c.mode = _MODE_CODE[cfg.mode]
+    c.atol, c.rtol = float(cfg.atol), float(cfg.rtol)
+    c.max_iters = int(max_iters)
+    c.hutchinson_samples = int(cfg.hutchinson_samples)
+    c.damping, c.clip = float(cfg.damping), float(cfg.clip)
+    pre = _pre_tensor(cfg, dev, D)
+    c.preconditioner = 0 if pre is None else pre.data_ptr()
+    mode = cfg.mode
+    win = int(cfg.window_len)
+    if mode == "diag-stochastic":
+        E = [torch.empty((win, D), dtype=dtype, device=dev)]
+    elif mode == "dense":
+        E = [torch.empty((win, D, D), dtype=dtype, device=dev)]
+    else:
+        E = [torch.empty((win, D // 2), dtype=dtype, device=dev) for _ in range(4)]
+    u = torch.empty((win, D), dtype=dtype, device=dev)
+    eptr = [_lib.ptr(x) for x in E] + [_lib.ptr(None)] * (4 - len(E))
+    half = D // 2 if mode == "block2x2-stochastic" else D
+    ws_bytes = lib.cs_scan_workspace_bytes(c.mode, dt, win, half)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    buf = torch.zeros(_STATS_BYTES + 8, dtype=torch.uint8, device=dev)  # stats + first failing row
+    sptr = _lib.ptr(buf)
+    first_ptr = ctypes.c_void_p(buf.data_ptr() + _STATS_BYTES)
+    guess = s0.expand(T, D).clone()
+    nxt = torch.empty((win, D), dtype=dtype, device=dev)
+    last_fail = torch.zeros(T, dtype=torch.int32, device=dev)
+    backup = torch.empty(win, dtype=torch.int32, device=dev)
+    host = torch.empty(_STATS_BYTES + 8, dtype=torch.uint8).pin_memory()
+    hist, d0, it, w = [], None, 0, 0
+    step_rows, update_rows = 0, 0  # work counters as the reference accumulates them
+    while w < T:
+        lo, hi = w, min(w + win, T)
+        n = hi - lo
+        step_rows += n
+        seed = s0 if lo == 0 else guess[lo - 1]
+        gw = guess[lo:hi]
+        lf = last_fail[lo:hi]
+        _lib.check(lib.cs_system_elements_range(ctypes.byref(d), ctypes.byref(c), dt, it, lo, n, _lib.ptr(seed),
+                                                _lib.ptr(gw), *eptr, _lib.ptr(u), sptr, st))
+        counted = it < max_iters
+        if counted:  # the update, speculatively (discarded if the Picard test stops the window)
+            backup[:n].copy_(lf)
+            if mode == "diag-stochastic":
+                rc = lib.cs_scan_diag_update(dt, eptr[0], _lib.ptr(u), _lib.ptr(seed), _lib.ptr(nxt), n, D,
+                                             _lib.ptr(ws), ws_bytes, _lib.ptr(gw), c.atol, c.rtol, it + 1,
+                                             _lib.ptr(lf), sptr, st)
+            elif mode == "block2x2-stochastic":
+                rc = lib.cs_scan_block_update(dt, *eptr, _lib.ptr(u), _lib.ptr(seed), _lib.ptr(nxt), n, half,
+                                              _lib.ptr(ws), ws_bytes, _lib.ptr(gw), c.atol, c.rtol, it + 1,
+                                              _lib.ptr(lf), sptr, st)
+            else:
+                rc = lib.cs_scan_dense(dt, eptr[0], _lib.ptr(u), _lib.ptr(seed), _lib.ptr(nxt), n, D, _lib.ptr(ws),
+                                       ws_bytes, st)
+                _lib.check(rc)
+                base = buf.data_ptr()
+                rc = lib.cs_update_bookkeeping(dt, _lib.ptr(gw), _lib.ptr(nxt), n, D, c.atol, c.rtol, it + 1,
+                                               _lib.ptr(lf), ctypes.c_void_p(base + 28), ctypes.c_void_p(base + 32),
+                                               st)
+            _lib.check(rc)
+            _lib.check(lib.cs_first_stamped_row(_lib.ptr(lf), n, it + 1, first_ptr, st))
+        host.copy_(buf, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        raw = host.numpy().tobytes()
+        bad_prop, bad_step, bad_jac = np.frombuffer(raw[:24], dtype=np.int64)
+        picard, nfail = np.frombuffer(raw[24:32], dtype=np.uint32)
+        dmax = float(np.frombuffer(raw[32:40], dtype=np.float64)[0])
+        first = int(np.frombuffer(raw[40:48], dtype=np.int64)[0])
+        if bad_prop != _NO_STEP:
+            raise ChainDivergedError(f"non-finite {getattr(system, '_what', 'proposal')} at step {int(bad_prop)}",
+                                     step=int(bad_prop))
+        if bad_step != _NO_STEP:
+            raise ChainDivergedError(f"non-finite step value at step {int(bad_step)} (iteration {it + 1})",
+                                     step=int(bad_step), iteration=it + 1)
+        if picard == 0:  # deer.py:297-299: the window is already a fixed point
+            if counted:
+                lf.copy_(backup[:n])
+            w = hi
+            continue
+        if not counted:
+            break
+        if bad_jac != _NO_STEP:
+            raise ChainDivergedError(f"non-finite jacobian at step {int(bad_jac)} (iteration {it + 1})",
+                                     step=int(bad_jac), iteration=it + 1)
+        it += 1
+        update_rows += n
+        hist.append(dmax)
+        gw.copy_(nxt[:n])
+        if d0 is None:
+            d0 = dmax
+        _guard(dmax, d0, it)
+        w = lo + first if nfail else hi
+    system.n_step_evals += step_rows
+    if mode == "diag-stochastic":
+        system.n_jvp_evals += update_rows * cfg.hutchinson_samples
+    elif mode == "dense":
+        system.n_jvp_evals += update_rows * D
+    else:
+        system.n_hvp_evals += update_rows * cfg.hutchinson_samples
+    return DeerResult(trace=guess, iterations=it, delta_history=np.array(hist), converged=w >= T,
+                      per_step_converged_at=last_fail + 1, full_trace=None,
+                      stats={"path": "streamed-window", "window_len": win})
 
 
 def _run_host(system, s0, cfg, max_iters):

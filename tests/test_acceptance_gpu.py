@@ -113,6 +113,8 @@ def test_criterion_01_oracle_equivalence(cuda_device, case):
     result = cs.run_deer(k, s0, cfg)
     assert result.converged, case
     assert within_envelope(result.trace, reference), case
+    if cfg.window_len is not None:
+        assert result.stats["path"] == "streamed-window", case
 
 
 # ---------------------------------------------------------------------------
@@ -278,7 +280,7 @@ def test_criterion_09_early_stopping_quality(cuda_device):
     k, s0 = cs.MalaKernel(model, eps=0.2, seed=6, T=T), np.zeros(2)
     reference = cs.sequential_evaluate(k, s0)
     conv = cs.run_deer(k, s0, cs.DeerConfig(mode="diag-stochastic", clip=1.0, window_len=2048, max_iters=8000))
-    assert conv.converged
+    assert conv.converged and conv.stats["path"] == "streamed-window"  # the window runs on the device engine
     early = cs.run_deer(k, s0, cs.DeerConfig(mode="diag-stochastic", clip=1.0, max_iters=8))
     assert not within_envelope(early.trace, reference)  # still coarse at iteration 8
     # exact mixture draws (test_acceptance.py:66-72): equal weights, unit variances

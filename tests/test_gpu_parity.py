@@ -369,11 +369,19 @@ def test_streamed_engine_golden(cuda_device, dtype):
 def test_run_deer_leapfrog_block_and_window(cuda_device):
     g = golden("mala_window")
     k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.std_normal(2)), 0.3, seed=6, T=512)
-    _deer_cmp(cs.run_deer(k, np.array([1.0, 0.0]), cs.DeerConfig(mode="dense", window_len=64, max_iters=2000)),
-              g, "win64_", torch.float64)
+    r = cs.run_deer(k, np.array([1.0, 0.0]), cs.DeerConfig(mode="dense", window_len=64, max_iters=2000))
+    assert r.stats["path"] == "streamed-window"  # the window runs on the device engine
+    _deer_cmp(r, g, "win64_", torch.float64)
     k1 = cs.MalaKernel(cs.model_logp_grad_hvp(cs.std_normal(2)), 0.3, seed=6, T=40)
-    _deer_cmp(cs.run_deer(k1, np.array([1.0, 0.0]), cs.DeerConfig(mode="dense", window_len=1, max_iters=500)),
-              g, "win1_", torch.float64)
+    r = cs.run_deer(k1, np.array([1.0, 0.0]), cs.DeerConfig(mode="dense", window_len=1, max_iters=500))
+    assert r.stats["path"] == "streamed-window"
+    _deer_cmp(r, g, "win1_", torch.float64)
+    # and the host engine's window loop agrees on both
+    for kk, cfg, pre in ((k, cs.DeerConfig(mode="dense", window_len=64, max_iters=2000, engine="host"), "win64_"),
+                         (k1, cs.DeerConfig(mode="dense", window_len=1, max_iters=500, engine="host"), "win1_")):
+        h = cs.run_deer(kk, np.array([1.0, 0.0]), cfg)
+        assert h.stats["path"] == "host"
+        _deer_cmp(h, g, pre, torch.float64)
     # block one-shot on a Gaussian leapfrog (test_deer.py:250-261)
     lf = cs.LeapfrogSystem(cs.model_logp_grad_hvp(cs.std_normal(2)), 0.1, 64)
     s0 = np.array([1.0, -0.5, 0.3, 0.8])
@@ -829,3 +837,34 @@ def test_wide_short_update_scan_bookkeeping(cuda_device):
     raw = stats.cpu().numpy().tobytes()
     assert (int(np.frombuffer(raw[28:32], dtype=np.uint32)[0]) > 0) == bool(fail.any())
     assert float(np.frombuffer(raw[32:40], dtype=np.float64)[0]) == float(gap.max())
+
+
+@pytest.mark.parametrize("case", ["hmc-diag", "gibbs-diag3", "leapfrog-block", "mala-mog-diag"])
+def test_streamed_window_matches_host_window(cuda_device, case):
+    # deer.py:287-319 on the device engine against the host-driven window loop:
+    # same iterations, delta history, per-step records and trace
+    if case == "hmc-diag":
+        m = cs.model_logp_grad_hvp(cs.rosenbrock(a=0.0, b=0.1, scale1=1.0, scale2=1.0))
+        k, s0 = cs.HmcKernel(m, 0.5, 8, seed=0, T=3000), np.zeros(2)
+        kw = dict(mode="diag-stochastic", clip=1.0, window_len=500, max_iters=2000)
+    elif case == "gibbs-diag3":
+        k = cs.GibbsKernel(cs.generate_eight_schools(), seed=0, T=4000)
+        s0 = k.initial_state()
+        kw = dict(mode="diag-stochastic", hutchinson_samples=3, preconditioner=k.recommended_preconditioner(),
+                  window_len=1000, max_iters=4000)
+    elif case == "leapfrog-block":
+        tg = cs.gaussian(np.array([0.5, -0.5]), np.array([[1.2, 0.0], [0.7, 0.6]]))
+        k = cs.LeapfrogSystem(cs.model_logp_grad_hvp(tg), 0.1, 300)
+        s0 = np.array([0.5, -0.5, 0.2, 0.1])
+        kw = dict(mode="block2x2-stochastic", window_len=64, max_iters=500)
+    else:
+        k = cs.MalaKernel(cs.model_logp_grad_hvp(cs.mog()), 0.1, seed=1, T=4096)
+        s0 = np.zeros(2)
+        kw = dict(mode="diag-stochastic", clip=1.0, window_len=512, max_iters=4000)
+    a = cs.run_deer(k, s0, cs.DeerConfig(**kw))
+    b = cs.run_deer(k, s0, cs.DeerConfig(engine="host", **kw))
+    assert a.stats["path"] == "streamed-window" and b.stats["path"] == "host"
+    assert a.iterations == b.iterations and a.converged == b.converged
+    np.testing.assert_array_equal(np_(a.per_step_converged_at), np_(b.per_step_converged_at))
+    np.testing.assert_allclose(a.delta_history, b.delta_history, rtol=1e-5, atol=1e-12)
+    np.testing.assert_allclose(np_(a.trace), np_(b.trace), rtol=1e-6, atol=1e-8)
