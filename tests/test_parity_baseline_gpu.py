@@ -169,6 +169,15 @@ def test_cfg5_gibbs_T1M_vs_reference(cuda_device, dtype):
 
 # ---------------------------------------------------------------------------
 # cfg3 diag: BLR MALA, D = 100, N = 1000, T = 100K (f64, the streamed engine)
+#
+# The reference itself does not converge here: after max_iters = 100 diag
+# quasi-Newton updates only the first ~350 steps have converged (its own
+# per-step record), and the rest of the iterate is an unconverged, chaotic
+# intermediate whose bits depend on every rounding.  Parity therefore pins
+# what is determined: the stop (100 iterations, not converged), the exact
+# per-step convergence record of the converged prefix, the first updates'
+# delta history, the accept/reject decisions along the converged prefix, and
+# the device's own sequential chain against the reference's.
 
 
 def test_cfg3_blr_diag_T100K_vs_reference(cuda_device):
@@ -178,7 +187,22 @@ def test_cfg3_blr_diag_T100K_vs_reference(cuda_device):
     k = cs.MalaKernel(m, 0.003, seed=4, T=100_000)
     res = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="diag-stochastic"))
     assert res.stats["path"] == "streamed"
-    check_record(res, g, "diag_", torch.float64, 100_000, exact_psca=False)
+    assert res.iterations == int(g["diag_iterations"]) == 100
+    assert res.converged == bool(g["diag_converged"]) is False
+    ref_psca = g["diag_psca"]
+    prefix = int(np.nonzero(ref_psca > int(g["diag_iterations"]))[0][0])  # steps converged within the run
+    assert prefix > 100
+    psca = np_(res.per_step_converged_at)
+    np.testing.assert_array_equal(psca[:prefix], ref_psca[:prefix])
+    np.testing.assert_allclose(res.delta_history[:5], g["diag_delta_history"][:5], rtol=1e-6)
+    # accept/reject along the converged prefix = the reference's sequential chain
+    Xo, yo, _ = O.synthetic_credit_like(seed=20250819, n=1000, dim=100)
+    ok = O.MalaKernel(O.blr(Xo, yo, 1.0), 0.003, seed=4, T=100_000)
+    acc = accept_mask(ok, np.zeros(100), np_(res.trace)[:prefix])
+    np.testing.assert_array_equal(acc, ref_accept(g, 100_000)[:prefix])
+    # the device's sequential chain against the reference's (rows 500 and 1000)
+    seq = np_(cs.sequential_evaluate(k, np.zeros(100), 1000))
+    np.testing.assert_allclose(seq[[499, 999]], g["seq_rows"][:2], rtol=1e-9, atol=1e-9)
 
 
 # ---------------------------------------------------------------------------
