@@ -47,7 +47,8 @@ def test_struct_layouts_match_header_sizes():
     # natural alignment: pointers 8, doubles 8 -> sizes fixed by the field lists
     assert ctypes.sizeof(_lib.cs_target) == 4 + 4 + 4 * 8 + 3 * 8 + 8 + 4 * 8 + 8 + 2 * 8 + 8
     assert ctypes.sizeof(_lib.cs_deer_config) == 8 + 8 + 8 + 4 + 4 + 8 + 8 + 8
-    assert ctypes.sizeof(_lib.cs_deer_result) == 4 + 4 + 4 + 4 + 8 + 4 + 4 + 8 + 8 + 16
+    # ..., kept_in_registers, fused_tangent (i32 x 2), device_ms (f64)
+    assert ctypes.sizeof(_lib.cs_deer_result) == 4 + 4 + 4 + 4 + 8 + 4 + 4 + 8 + 8 + 16 + 8 + 8
 
 
 @pytest.mark.parametrize("kwargs", [

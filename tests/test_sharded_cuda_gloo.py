@@ -55,9 +55,15 @@ def _worker(rank, world, port, name, q):
         torch.cuda.set_device(0)
         from paper_2508_18413_b200.sharded import gather_trace, run_deer_sharded
 
-        k, s0, cfg = _system(name)
+        forced = name.endswith("+ops")
+        k, s0, cfg = _system(name[:-4] if forced else name)
         try:
-            r = run_deer_sharded(k, s0, cfg)
+            if forced:  # the general per-kernel shard ops (CUDA tensors over a gloo group)
+                from paper_2508_18413_b200.sharded import CudaShardOps
+
+                r = run_deer_sharded(k, s0, cfg, ops=CudaShardOps(k))
+            else:
+                r = run_deer_sharded(k, s0, cfg)
         except cs_errors().ChainDivergedError as e:
             q.put((rank, "diverged", e.step, e.iteration))
             return
@@ -70,11 +76,11 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["hmc", "gibbs", "mala_dense", "blr_diag", "blr_dense"])
+@pytest.mark.parametrize("name", ["hmc", "gibbs", "mala_dense", "blr_diag", "blr_dense", "hmc+ops", "mala_dense+ops"])
 def test_two_rank_streamed_shards_match_run_deer(cuda_device, name):
     import paper_2508_18413_b200 as cs
 
-    k, s0, cfg = _system(name)
+    k, s0, cfg = _system(name.replace("+ops", ""))
     ref = cs.run_deer(k, s0, cfg)
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -88,7 +94,7 @@ def test_two_rank_streamed_shards_match_run_deer(cuda_device, name):
     for p in procs:
         p.join(timeout=60)
     for rank, path, its, conv, full, psca in out:
-        assert path == "sharded-streamed"
+        assert path == ("sharded" if name.endswith("+ops") else "sharded-streamed")
         # the sharded solve equals the reference's chunked scan with chunk = T/2,
         # so iterations agree within one and traces within the solve tolerance
         assert abs(its - ref.iterations) <= 1 and conv == ref.converged, (rank, its, ref.iterations)
