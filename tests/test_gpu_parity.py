@@ -732,16 +732,21 @@ def test_small_d_row_scan_coalesced_path(cuda_device, D, T):
     np.testing.assert_allclose(np_(aligned), want, atol=2e-4, rtol=2e-5)
 
 
-def test_update_scan_bookkeeping_multi_round(cuda_device):
+@pytest.mark.parametrize("D,misalign", [(18, False), (1, False), (2, False), (4, False), (2, True), (4, True)])
+def test_update_scan_bookkeeping_multi_round(cuda_device, D, misalign):
     # the replay's fused bookkeeping (deer.py:273-277) at a multi-round size:
-    # last_fail stamps, fail_rows and dmax against a direct evaluation
+    # last_fail stamps, fail_rows and dmax against a direct evaluation.  D = 1,
+    # 2, 4 take the coalesced 16-byte stage loads; a one-float offset of j and
+    # u forces the per-column fallback, ragged last stage included
     from paper_2508_18413_b200 import _lib
 
     lib = _lib.load()
-    T, D, it = 3_000_001, 18, 7
-    g = torch.Generator(device=cuda_device).manual_seed(3)
-    j = (torch.rand((T, D), generator=g, device=cuda_device) * 1.9 - 0.95).float()
-    u = torch.randn((T, D), generator=g, device=cuda_device).float()
+    T, it = 3_000_001, 7
+    g = torch.Generator(device=cuda_device).manual_seed(3 + D)
+    off = 1 if misalign else 0
+    jb = (torch.rand((T * D + off,), generator=g, device=cuda_device) * 1.9 - 0.95).float()
+    ub = torch.randn((T * D + off,), generator=g, device=cuda_device).float()
+    j, u = jb[off:].view(T, D), ub[off:].view(T, D)
     s0 = torch.zeros(D, device=cuda_device)
     ref = cs.parallel_affine_solve(cs.DiagElements(j, u), s0)
     guess = ref + torch.randn((T, D), generator=g, device=cuda_device) * 1e-4 * (torch.rand((T, 1), generator=g, device=cuda_device) < 0.3)
@@ -755,7 +760,7 @@ def test_update_scan_bookkeeping_multi_round(cuda_device):
                                        _lib.ptr(ws), wsb, _lib.ptr(guess), atol, rtol, it, _lib.ptr(last_fail),
                                        _lib.ptr(stats), _lib.stream_ptr()))
     torch.cuda.synchronize()
-    torch.testing.assert_close(out, ref, atol=1e-5, rtol=1e-5)  # look-back fold order may differ run to run
+    torch.testing.assert_close(out, ref, atol=1e-5, rtol=1e-5)
     gap = (out.double() - guess.double()).abs()
     fail = (gap > atol + rtol * out.double().abs()).any(dim=1)
     want_lf = torch.where(fail, torch.tensor(it, dtype=torch.int32, device=cuda_device), torch.tensor(2, dtype=torch.int32, device=cuda_device))
