@@ -90,6 +90,12 @@ typedef struct cs_system {
   const double *noise_logu;
   const void *g_tau, *xi_mu, *xi_theta, *g_sigma;
   const double *gibbs;
+  const double *basis;           /* NULL, or an orthogonal Q (dim x dim, row-
+                                    major, device f64): the system runs in z =
+                                    Q' s coordinates, z -> Q' f(Q z), jvp
+                                    V -> Q' J Q V (targets.py:473-517
+                                    transform_system), fused into the MALA /
+                                    HMC kernels                               */
 } cs_system;
 
 /* DeerConfig (deer.py:55-93), validated on the host. */

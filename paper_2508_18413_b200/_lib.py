@@ -43,7 +43,7 @@ class cs_system(ctypes.Structure):
     _fields_ = [("kind", i32), ("dim", i32), ("target", cs_target), ("eps", f64), ("L", i32),
                 ("mass", P), ("seed", u64), ("probe_seed", u64), ("T", i64),
                 ("noise_vec", P), ("noise_logu", P), ("g_tau", P), ("xi_mu", P),
-                ("xi_theta", P), ("g_sigma", P), ("gibbs", P)]
+                ("xi_theta", P), ("g_sigma", P), ("gibbs", P), ("basis", P)]
 
 
 class cs_deer_config(ctypes.Structure):

@@ -9,7 +9,11 @@ reference's to rounding.  ``transform_system(system, Q)`` conjugates a system
 into z = Q' s coordinates, z -> Q' f(Q z), with jvp and dense Jacobian
 conjugated alike; solving it from Q' s0 and mapping back through Q reproduces
 the original trace (quasi-Newton solves converge faster on correlated targets
-in the eigenbasis).
+in the eigenbasis).  For the built-in MALA / HMC systems Q
+is fused into the CUDA kernels (the system descriptor carries it; f_t,
+tangents, the sequential walk and the streamed engine's element builder
+conjugate in registers); other systems get the conjugation as batched GEMMs
+around their step / jvp calls.
 """
 
 from __future__ import annotations
@@ -94,6 +98,68 @@ class _TransformedSystem(TransitionSystem):
         return self.Q.T @ J @ self.Q
 
 
+class _FusedTransformed(_TransformedSystem):
+    """A built-in MALA / HMC system in z = Q' s coordinates with Q fused into its
+    CUDA kernels: the descriptor carries Q, so f_t, the tangents, the sequential
+    walk and the streamed engine's element builder conjugate in registers
+    (x = Q z on the way in, Q' on the way out) -- no extra passes over T."""
+
+    def __init__(self, base, Q):
+        super().__init__(base, Q)
+        from .samplers import _Fused
+
+        self._Qd = Q.to(dtype=torch.float64, device=base.device).contiguous()
+        self._kind = base._kind
+        self._what = base._what
+        self._call_step = _Fused._call_step.__get__(self)
+        self._call_jvp = _Fused._call_jvp.__get__(self)
+        self._sequential_kernel = _Fused._sequential_kernel.__get__(self)
+
+    def desc(self):
+        d = self.base.desc()
+        d.basis = self._Qd.data_ptr()
+        return d
+
+    @property
+    def kernels(self) -> bool:
+        return True
+
+    @property
+    def _sequential(self):
+        return self._sequential_kernel
+
+    def _step_batch(self, ts, Z):
+        return self._call_step(ts, Z)
+
+    def _jvp_batch(self, ts, Z, V):
+        return self._call_jvp(ts, Z, V)
+
+    def relaxed_step_batch(self, ts, Z):
+        return self._call_step(as_steps(ts, self.device), self._state(Z), relaxed=True)
+
+    def relaxed_jvp_batch(self, ts, Z, V):
+        return self._call_jvp(as_steps(ts, self.device), self._state(Z), self._state(V), relaxed=True)
+
+    def dense_jacobian_batch(self, ts, Z):
+        return TransitionSystem.dense_jacobian_batch(self, ts, Z)
+
+
+def _fusable(system) -> bool:
+    from . import _lib
+    from .samplers import HmcKernel, MalaKernel
+
+    if not isinstance(system, (MalaKernel, HmcKernel)) or not getattr(system, "kernels", False):
+        return False
+    if getattr(system, "leapfrog_mode", "sequential") == "parallel":
+        return False
+    import ctypes
+
+    d = system.desc()
+    probe = torch.eye(system.dim, dtype=torch.float64, device=system.device)
+    d.basis = probe.data_ptr()
+    return bool(_lib.load().cs_system_supported(ctypes.byref(d), _lib.dtype_code(system.dtype)))
+
+
 def transform_system(system: TransitionSystem, Q) -> TransitionSystem:
     """Rewrite a system in the orthogonal coordinates z = Q' s (targets.py:504-517)."""
     Q = torch.as_tensor(np.asarray(Q, float) if not torch.is_tensor(Q) else Q, dtype=torch.float64,
@@ -103,4 +169,6 @@ def transform_system(system: TransitionSystem, Q) -> TransitionSystem:
         raise StructuralError(f"Q must be {d}x{d} to match the system, got {tuple(Q.shape)}")
     if float((Q.T @ Q - torch.eye(d, dtype=Q.dtype, device=Q.device)).abs().max()) > 1e-10:
         raise StructuralError("Q is not orthogonal")
+    if _fusable(system):
+        return _FusedTransformed(system, Q)
     return _TransformedSystem(system, Q)

@@ -549,9 +549,15 @@ int cs_hutchinson_accumulate(int dtype, void *est, const void *z, const void *jz
 }
 
 // ---- transition systems -------------------------------------------------------------
+// a change of basis is fused into the MALA and HMC register kernels only
+static bool basis_ok(const cs_system *sys) {
+  return !sys->basis || sys->kind == CS_SYS_MALA || sys->kind == CS_SYS_HMC;
+}
+
 static int check_sys(const cs_system *sys, int dtype, int *md_out) {
   if (!sys) return fail(CS_ERR_CONFIG, "null system");
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
+  if (!basis_ok(sys)) return fail(CS_ERR_CONFIG, "a change of basis is fused into the MALA and HMC kernels only");
   int md = 0;
   if (sys->kind == CS_SYS_GIBBS) {
     md = sys->dim == 18 ? 18 : 0;
@@ -567,7 +573,7 @@ static int check_sys(const cs_system *sys, int dtype, int *md_out) {
 }
 
 int cs_system_supported(const cs_system *sys, int dtype) {
-  if (!sys || !dtype_ok(dtype)) return 0;
+  if (!sys || !dtype_ok(dtype) || !basis_ok(sys)) return 0;
   if (sys->kind == CS_SYS_GIBBS) return sys->dim == 18 ? 1 : 0;
   if (sys->target.kind == CS_TARGET_BLR) return 0;
   return api_md(sys->kind, sys->target.kind, sys->dim) ? 1 : 0;
@@ -616,6 +622,7 @@ int cs_system_sequential(const cs_system *sys, int dtype, const void *s0, int64_
 // ---- fused element builder + update scans (the streamed solver path) ---------------
 int cs_system_elements_supported(const cs_system *sys, int32_t mode, int dtype) {
   if (!sys || !dtype_ok(dtype)) return 0;
+  if (sys->basis && (!basis_ok(sys) || mode == CS_MODE_BLOCK || sys->target.kind == CS_TARGET_BLR)) return 0;
   if (mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG) return 0;
   int md = 0;
   if (sys->kind == CS_SYS_GIBBS) md = (sys->dim == 18 && mode == CS_MODE_DIAG) ? 18 : 0;
@@ -642,6 +649,8 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
                        cs_elem_stats *d_stats, void *stream) {
   if (!sys || !cfg || !d_stats) return fail(CS_ERR_CONFIG, "null argument");
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
+  if (sys->basis && !cs_system_elements_supported(sys, cfg->mode, dtype))
+    return fail(CS_ERR_CONFIG, "a change of basis is fused into the MALA / HMC diag and dense builders only");
   const int md = elem_width(sys);
   const bool wide = !md && wide_leapfrog_ok(*sys, cfg->mode);
   const bool blr = !md && !wide && blr_mala_ok(*sys, cfg->mode);
@@ -684,6 +693,8 @@ int cs_system_elements_range(const cs_system *sys, const cs_deer_config *cfg, in
   if (t0 < 0 || n < 0 || t0 + n > sys->T) return fail(CS_ERR_STRUCTURAL, "step range outside [1, T]");
   if (t0 == 0 && n == sys->T)
     return cs_system_elements(sys, cfg, dtype, iteration, s0, guess, e0, e1, e2, e3, u, d_stats, stream);
+  if (sys->basis && !cs_system_elements_supported(sys, cfg->mode, dtype))
+    return fail(CS_ERR_CONFIG, "a change of basis is fused into the MALA / HMC diag and dense builders only");
   if (!dtype_ok(dtype)) return fail(CS_ERR_CONFIG, "bad dtype");
   const int md = elem_width(sys);
   const bool blr = !md && blr_mala_ok(*sys, cfg->mode);
@@ -776,7 +787,7 @@ static int solver_width(const cs_system *sys) {
 }
 
 int cs_deer_supported(const cs_system *sys, int mode, int dtype) {
-  if (!sys || !dtype_ok(dtype)) return 0;
+  if (!sys || !dtype_ok(dtype) || sys->basis) return 0;  // bases run on the streamed engine
   const int md = solver_width(sys);
   if (!md) return 0;
   if (mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG) return 0;

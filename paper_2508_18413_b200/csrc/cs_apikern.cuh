@@ -36,11 +36,23 @@ k_sys_step(cs_system s, const int64_t *ts, int64_t t0, int64_t n, const ST *S, S
   const int64_t t = ts ? ts[i] : t0 + i;
   double x[MD], f[MD];
   load_row_ro<Sys, MD, ST>(sys, S + i * D, x);
+  if (s.basis) {  // z -> Q' f(Q z)
+    double z[MD];
+#pragma unroll
+    for (int k = 0; k < MD; ++k) z[k] = x[k];
+    basis_in<Sys, MD>(sys, s.basis, D, z, x);
+  }
   typename Sys::Aux aux;
   const bool ok = sys.prepare(t, x, aux);
   if (!ok && bad) atomicMin(bad, (long long)t);
   if (relaxed) sys.relaxed_f(aux, f);
   else sys.f(aux, f);
+  if (s.basis) {
+    double fx[MD];
+#pragma unroll
+    for (int k = 0; k < MD; ++k) fx[k] = f[k];
+    basis_out<Sys, MD>(sys, s.basis, D, fx, f);
+  }
   store_row<Sys, MD, ST>(sys, out + i * D, f);
 }
 
@@ -56,9 +68,15 @@ k_sys_jvp(cs_system s, const int64_t *ts, int64_t t0, int64_t n, const ST *S, co
   double x[MD], v[1][MD], o[1][MD];
   load_row_ro<Sys, MD, ST>(sys, S + i * D, x);
   load_row_ro<Sys, MD, ST>(sys, V + i * D, v[0]);
+  if (s.basis) {
+    double z[MD];
+#pragma unroll
+    for (int k = 0; k < MD; ++k) z[k] = x[k];
+    basis_in<Sys, MD>(sys, s.basis, D, z, x);
+  }
   typename Sys::Aux aux;
   sys.prepare(t, x, aux);
-  sys.template jvp_many<1>(aux, v, o, 1, relaxed != 0);
+  jvp_basis<1, double>(sys, s.basis, D, aux, v, o, 1, relaxed != 0);
   store_row<Sys, MD, ST>(sys, out + i * D, o[0]);
 }
 
@@ -101,8 +119,17 @@ __global__ void k_sys_seq(cs_system s, const ST *s0, int64_t T, ST *out, long lo
   load_row_ro<Sys, MD, ST>(sys, s0, x);
   for (int64_t t = 1; t <= T; ++t) {
     typename Sys::Aux aux;
-    bool ok = sys.prepare(t, x, aux);
-    sys.f(aux, x);
+    bool ok;
+    if (s.basis) {  // the chain in z coordinates: z_t = Q' f(Q z_{t-1})
+      double xs[MD], fx[MD];
+      basis_in<Sys, MD>(sys, s.basis, D, x, xs);
+      ok = sys.prepare(t, xs, aux);
+      sys.f(aux, fx);
+      basis_out<Sys, MD>(sys, s.basis, D, fx, x);
+    } else {
+      ok = sys.prepare(t, x, aux);
+      sys.f(aux, x);
+    }
 #pragma unroll
     for (int k = 0; k < MD; ++k)
       if (sys.mem_index(k) >= 0) ok &= finite(x[k]);
@@ -136,9 +163,17 @@ k_sys_elements(SolveArgs<ST> A, int iteration, const ST *guess, ST *e0, ST *e1, 
     load_row_ro<Sys, MD, ST>(sys, r == 0 ? A.s0 : guess + (r - 1) * D, prev);
     load_row_ro<Sys, MD, ST>(sys, guess + r * D, gr);
     typename Sys::Aux aux;
-    if (!sys.prepare(t, prev, aux)) bp = t;
     double f[MD];
-    sys.f(aux, f);
+    if (A.sys.basis) {  // z coordinates: prepare at Q z, f -> Q' f (build_elem conjugates the tangents)
+      double xs[MD], fx[MD];
+      basis_in<Sys, MD>(sys, A.sys.basis, D, prev, xs);
+      if (!sys.prepare(t, xs, aux)) bp = t;
+      sys.f(aux, fx);
+      basis_out<Sys, MD>(sys, A.sys.basis, D, fx, f);
+    } else {
+      if (!sys.prepare(t, prev, aux)) bp = t;
+      sys.f(aux, f);
+    }
     bool fin = true, pfail = false;
 #pragma unroll
     for (int i = 0; i < MD; ++i) {

@@ -115,6 +115,49 @@ CS_D void load_row(const Sys &sys, const ST *row, double (&x)[MD]) {
   }
 }
 
+// Orthogonal change of basis (targets.py:473-517): a system in z = Q' s
+// coordinates steps z -> Q' f(Q z).  Q is dim x dim row-major f64; registers
+// past dim (mem_index < 0) stay zero.  x = Q z, and z = Q' x.
+template <class Sys, int MD>
+CS_D void basis_in(const Sys &sys, const double *Q, int D, const double (&z)[MD], double (&x)[MD]) {
+#pragma unroll
+  for (int i = 0; i < MD; ++i) {
+    double a = 0.0;
+    if (sys.mem_index(i) >= 0)
+#pragma unroll
+      for (int j = 0; j < MD; ++j)
+        if (sys.mem_index(j) >= 0) a += __ldg(Q + i * D + j) * z[j];
+    x[i] = a;
+  }
+}
+template <class Sys, int MD>
+CS_D void basis_out(const Sys &sys, const double *Q, int D, const double (&x)[MD], double (&z)[MD]) {
+#pragma unroll
+  for (int j = 0; j < MD; ++j) {
+    double a = 0.0;
+    if (sys.mem_index(j) >= 0)
+#pragma unroll
+      for (int i = 0; i < MD; ++i)
+        if (sys.mem_index(i) >= 0) a += x[i] * __ldg(Q + i * D + j);
+    z[j] = a;
+  }
+}
+// NT tangents through the system, conjugated by the basis when one is set
+template <int NT, typename TT, class Sys, int MD>
+CS_D void jvp_basis(const Sys &sys, const double *Q, int D, const typename Sys::Aux &aux,
+                    const double (&V)[NT][MD], double (&O)[NT][MD], int n, bool relaxed) {
+  if (!Q) {
+    sys.template jvp_many<NT, TT>(aux, V, O, n, relaxed);
+    return;
+  }
+  double Vx[NT][MD], Ox[NT][MD];
+#pragma unroll
+  for (int k = 0; k < NT; ++k) basis_in<Sys, MD>(sys, Q, D, V[k], Vx[k]);
+  sys.template jvp_many<NT, TT>(aux, Vx, Ox, n, relaxed);
+#pragma unroll
+  for (int k = 0; k < NT; ++k) basis_out<Sys, MD>(sys, Q, D, Ox[k], O[k]);
+}
+
 // Element for one step from the forward pass (deer.py:161-204).
 template <class Sys, int MODE, int MD, typename ST>
 CS_D void build_elem(const Sys &sys, const typename Sys::Aux &aux, const double (&prev)[MD],
@@ -135,7 +178,7 @@ CS_D void build_elem(const Sys &sys, const typename Sys::Aux &aux, const double 
         const int m = sys.mem_index(i);
         V[0][i] = m >= 0 ? probe_sign(h3, k, m) : 0.0;
       }
-      sys.template jvp_many<1, ST>(aux, V, O, 1, false);
+      jvp_basis<1, ST>(sys, A.sys.basis, A.D, aux, V, O, 1, false);
 #pragma unroll
       for (int i = 0; i < MD; ++i) est[i] += V[0][i] * O[0][i];
     }
@@ -161,7 +204,7 @@ CS_D void build_elem(const Sys &sys, const typename Sys::Aux &aux, const double 
 #pragma unroll
       for (int i = 0; i < MD; ++i) V[c][i] = (i == c && sys.mem_index(c) >= 0) ? 1.0 : 0.0;
     }
-    sys.template jvp_many<MD, ST>(aux, V, O, nk, false);
+    jvp_basis<MD, ST>(sys, A.sys.basis, A.D, aux, V, O, nk, false);
 #pragma unroll
     for (int a = 0; a < MD; ++a) {
       const int ma = sys.mem_index(a);

@@ -127,6 +127,36 @@ def test_eigenbasis_solve_matches_the_reference(cuda_device):
     k = cs.MalaKernel(m, 0.15, seed=9, T=400)
     w = cs.transform_system(k, cs.orthogonal_basis(g["P"]).Q)
     r = cs.run_deer(w, w.transform_state(np.zeros(4)), cs.DeerConfig(mode="diag-stochastic"))
+    assert r.stats["path"] == "streamed"  # Q fused into the element builder, no eager conjugation
     assert r.converged == bool(g["z_converged"]) and r.iterations == int(g["z_iterations"])
     np.testing.assert_allclose(np_(r.trace), g["z_trace"], atol=1e-8, rtol=1e-8)
     np.testing.assert_allclose(np_(w.untransform_state(r.trace)), g["seq"], atol=1e-3, rtol=1e-3)
+
+
+@pytest.mark.parametrize("kind", ["mala", "hmc"])
+def test_fused_basis_matches_eager_conjugation(cuda_device, kind):
+    # Q fused into the MALA / HMC kernels against the same conjugation done as
+    # batched matmuls around the plain system (targets.py:487-501)
+    from paper_2508_18413_b200.basis import _FusedTransformed, _TransformedSystem
+
+    g = golden("basis")
+    m = cs.model_logp_grad_hvp(cs.gaussian(np.array([0.5, -1.0, 0.0, 1.0]), g["chol"]))
+    k = cs.MalaKernel(m, 0.15, seed=9, T=400) if kind == "mala" else cs.HmcKernel(m, 0.2, 5, seed=9, T=400)
+    Q = cs.orthogonal_basis(g["P"]).Q
+    fused, eager = cs.transform_system(k, Q), _TransformedSystem(k, Q)
+    assert isinstance(fused, _FusedTransformed) and not isinstance(eager, _FusedTransformed)
+    rng = np.random.default_rng(4)
+    Z = torch.as_tensor(rng.normal(size=(64, 4)), device=cuda_device)
+    V = torch.as_tensor(rng.normal(size=(64, 4)), device=cuda_device)
+    ts = torch.arange(1, 65, device=cuda_device)
+    torch.testing.assert_close(fused.step_batch(ts, Z), eager.step_batch(ts, Z), atol=1e-12, rtol=1e-12)
+    torch.testing.assert_close(fused.jvp_batch(ts, Z, V), eager.jvp_batch(ts, Z, V), atol=1e-12, rtol=1e-12)
+    z0 = fused.transform_state(np.zeros(4))
+    torch.testing.assert_close(cs.sequential_evaluate(fused, z0), cs.sequential_evaluate(eager, z0), atol=1e-10,
+                               rtol=1e-10)
+    for mode in ("diag-stochastic", "dense"):
+        a = cs.run_deer(fused, z0, cs.DeerConfig(mode=mode))
+        b = cs.run_deer(eager, z0, cs.DeerConfig(mode=mode))
+        assert a.stats["path"] == "streamed" and b.stats["path"] == "host"
+        assert a.iterations == b.iterations and a.converged == b.converged
+        torch.testing.assert_close(a.trace, b.trace, atol=1e-9, rtol=1e-9)
