@@ -33,6 +33,11 @@ EPS, LSTEPS = 0.5, 8
 ROSEN = dict(a=0.0, b=0.1, scale1=1.0, scale2=1.0)
 
 
+def workload(T):
+    """The one workload description both arms print (same_config)."""
+    return f"HMC Rosenbrock(b=0.1,s2=1) eps={EPS} L={LSTEPS} T={T}, diag quasi-Newton clip=1, s0=0"
+
+
 def traffic(key):
     """DRAM bytes per launch of a kernel at a bench workload, from its committed
     ncu capture (profiles/r01_traffic.json); None when not captured."""
@@ -164,8 +169,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-RNG noise)",
             "impl": "reference",
-            "config": {"workload": f"HMC Rosenbrock(b=0.1,s2=1) eps={EPS} L={LSTEPS} T={T}, diag quasi-Newton clip=1",
-                       "T": T, "newton_iterations": int(np.median(iters))},
+            "config": {"workload": workload(T), "T": T, "newton_iterations": int(np.median(iters))},
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
                              "sample": f"full T={T} chain solve per step (oracle/: numpy f_t + pthread C scan)"},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -187,7 +191,7 @@ def run_gpu(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1 or args.sharded:
+    if world > 1 or not args.no_extras:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
@@ -220,6 +224,13 @@ def run_gpu(args):
     torch.cuda.synchronize()
     iters = res.iterations
 
+    kernel_ms = []
+
+    def solve_rec():
+        r = solve()
+        kernel_ms.append(r.stats.get("device_ms", float("nan")))
+        return r
+
     def timed(fn):
         # the collector stays off inside the timed region (a collection pause in
         # the host path would land in one step); objects are freed at the end
@@ -242,7 +253,8 @@ def run_gpu(args):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        ms_dev, res = timed(solve)
+        ms_dev, res = timed(solve_rec)
+        kernel_step_ms = float(np.mean(kernel_ms[-args.steps:]))
 
         def e2e_step():
             kern.noise.load("momentum", mom_host, dtype=dtype)
@@ -278,8 +290,11 @@ def run_gpu(args):
                     "barrier and dependent f64 leapfrog chains, not HBM (profiles/r01_ncu_hmc_fused_solver.md); "
                     "the HBM-bound scan is scan_roofline"}
 
-    # the T-sharded driver on BASELINE cfg 5 whenever ranks exist
-    shard = t_sharded_gibbs(cs, dev, world, rank) if (world > 1 or args.sharded) and not args.no_extras else None
+    # f64 companion (the reference computes in f64): the same solve, device-resident
+    f64 = f64_companion(cs, dev, T, args) if not args.no_extras and dtype == torch.float32 else None
+
+    # the T-sharded driver on BASELINE cfg 5
+    shard = t_sharded_gibbs(cs, dev, world, rank) if not args.no_extras else None
     scan_roof = None
     cpu_base = None
     if rank == 0 and not args.no_extras:
@@ -290,8 +305,7 @@ def run_gpu(args):
                 "warmup": args.warmup, "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
                 "data": "synthetic (counter-RNG noise, reference seed 0 per rank)",
-                "config": {"workload": f"HMC Rosenbrock(b=0.1,s2=1) eps={EPS} L={LSTEPS} T={T}, "
-                                       f"diag quasi-Newton clip=1, s0=0",
+                "config": {"workload": workload(T),
                            "T": T, "newton_iterations": iters, "parallelism": f"replicas x{world}",
                            "l2": "flushed (256 MiB write) between timed steps",
                            "solver": res.stats},
@@ -299,13 +313,44 @@ def run_gpu(args):
                         "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps,
                         "gpu_launches": args.steps * int(res.stats.get("launches", 3))},
                 "gpu_launches": args.steps * int(res.stats.get("launches", 3)),
+                "kernel_ms_per_step": kernel_step_ms,
                 "roofline": roof, "scan_roofline": scan_roof, "cpu_baseline": cpu_base,
                 **({"t_sharded": shard} if shard is not None else {}),
+                **({"f64": f64} if f64 is not None else {}),
                 "clocks": clk.summary()}
         emit(line)
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
+
+
+def f64_companion(cs, dev, T, args):
+    """The headline solve with states and elements in f64 (the reference's
+    dtype): device-resident timing like ``value``; reported beside it."""
+    import torch
+
+    try:
+        k = cs.HmcKernel(cs.model_logp_grad_hvp(cs.rosenbrock(**ROSEN)), EPS, LSTEPS, seed=0, T=T,
+                         dtype=torch.float64)
+        cfg = cs.DeerConfig(mode="diag-stochastic", clip=1.0)
+        s0 = torch.zeros(2, dtype=torch.float64, device=dev)
+        for _ in range(max(3, args.warmup)):
+            r = cs.run_deer(k, s0, cfg)
+        n = max(5, min(args.steps, 20))
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ker = []
+        a.record()
+        for _ in range(n):
+            r = cs.run_deer(k, s0, cfg)
+            ker.append(r.stats.get("device_ms", float("nan")))
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / n
+        return {"value": T / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms, "kernel_ms_per_step": float(np.mean(ker)),
+                "newton_iterations": r.iterations, "steps": n, "dtype": "f64", "solver": r.stats}
+    except Exception as e:  # reported, never required
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def t_sharded_gibbs(cs, dev, world, rank, reps=3):
@@ -418,8 +463,7 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--T", type=int, default=T_DEFAULT)
     ap.add_argument("--no-extras", action="store_true")
-    ap.add_argument("--sharded", action="store_true",
-                    help="also run the T-sharded cfg5 solve at N=1 (an NCCL group of one); automatic for N>1")
+    ap.add_argument("--sharded", action="store_true", help="(kept for compatibility: t_sharded always runs)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
