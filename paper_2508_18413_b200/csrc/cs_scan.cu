@@ -179,7 +179,8 @@ template <typename T> struct SegE<SCAN_BLOCK, T> {
 constexpr int kLbPerLane = 4;                    // tiles per lane in a look-back window
 constexpr int kLbWindow = 32 * kLbPerLane;          // 128 predecessors per round trip
 
-template <int VAR, class G = CtaGrp, class StatusF, class AggF, class ExitF, class ExitVF, class S0F, class S0VF>
+template <int VAR, class G = CtaGrp, int KB = 8, class StatusF, class AggF, class ExitF, class ExitVF, class S0F,
+          class S0VF>
 CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF exit_x, ExitVF exit_v,
                        S0F s0x, S0VF s0v, double *s_acc, double *s_entry, int *s_ctl) {
   (void)s_acc;
@@ -224,7 +225,7 @@ CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF ex
   // property, _scan_kernels.py:3-8), independent of publication timing.
   // (Composing the aggregates first and applying the product once would round
   // differently depending on where the look-back stopped.)
-  constexpr int kB = VAR == SCAN_DIAG ? 8 : 1;  // block: 6 doubles per aggregate, keep register pressure low
+  constexpr int kB = KB;  // aggregates in flight per round trip (a register budget, set by the caller)
   for (int c = tid; c < ncol; c += G::kN) {
     double x = pe < 0 ? s0x(c) : exit_x(pe, c);
     double v = 0.0;
@@ -249,7 +250,7 @@ CS_D void lookback_cta(int64_t pos, int ncol, StatusF status, AggF agg, ExitF ex
 
 // Two-level look-back for row tiles (see cs_lookback.cuh).  On return
 // s_entry holds the chain state entering tile b.
-template <int VAR, class G = CtaGrp, class S0F, class S0VF, class StampF>
+template <int VAR, class G = CtaGrp, int KB = 8, class S0F, class S0VF, class StampF>
 CS_D void lookback_grouped(int64_t b, int ncol, const LookbackWs &ws, S0F s0x, S0VF s0v, double *s_acc,
                            double *s_acc2, double *s_entry, double *s_gentry, int *s_ctl, StampF stamp) {
   constexpr int W = ColElem<VAR>::W;
@@ -284,7 +285,7 @@ CS_D void lookback_grouped(int64_t b, int ncol, const LookbackWs &ws, S0F s0x, S
     if (ht == 0) stamp(6);
   } else {
     // (2) state entering the group: decoupled look-back over group aggregates
-    lookback_cta<VAR, H1>(
+    lookback_cta<VAR, H1, KB>(
         g, ncol, [&](int64_t p) { return ws.gstatus + p; },
         [&](int64_t p, int cc) { return ws.gagg + (p * ncol + cc) * W; },
         [&](int64_t p, int cc) { return ld_cg(ws.exit + p * SW + cc); },
@@ -896,7 +897,9 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
           mbar_wait(&s_full[kc & 1], (unsigned)((kc >> 1) & 1));
           for (int cc = tid; cc < SW; cc += kScanThreads) s_run[(n & 1) * 2 * 64 + cc] = s_lbe[(kc & 1) * 128 + cc];
         } else {
-          lookback_grouped<VAR, CtaGrp>(
+          // the 80-register instances (block2x2, the bookkeeping scan) fetch fewer
+          // aggregates per round trip so the look-back does not spill the stage loop
+          lookback_grouped<VAR, CtaGrp, (VAR == SCAN_BLOCK ? 1 : UPDATE ? 2 : 8)>(
               q, ncol, ws, [&](int cc) { return (double)a.s0[cc]; },
               [&](int cc) { return (double)a.s0[ncol + cc]; }, s_acc, s_acc2, s_entry, s_gentry, s_ctl,
               [&](int k) { scan_stamp(a, q, k); });

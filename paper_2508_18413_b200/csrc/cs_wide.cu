@@ -346,9 +346,24 @@ static cudaError_t wide_batch_chunk(const cs_system &sys, const cs_deer_config &
   const size_t bA = sizeof(double) * (size_t)M * n, bG = sizeof(ST) * (size_t)rows * D;
   const size_t bE = sizeof(ST) * (size_t)rows * n;
   const size_t need = 2 * bA + 2 * bG + 4 * bE + sizeof(WbCtl) * (size_t)B + 256;
-  char *w = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)&w, need, st);
-  if (e != cudaSuccess) return e;
+  // one grow-only scratch buffer per device (the solve synchronises every pass,
+  // so the next call may reuse it; a stream-ordered malloc/free pair per call
+  // returned the memory to the driver at every sync and re-mapped it)
+  static std::mutex mu;
+  static char *bufs[16];
+  static size_t caps[16];
+  int dv = 0;
+  cudaGetDevice(&dv);
+  std::lock_guard<std::mutex> lock(mu);
+  cudaError_t e = cudaSuccess;
+  if (caps[dv & 15] < need) {
+    if (bufs[dv & 15]) cudaFree(bufs[dv & 15]);
+    bufs[dv & 15] = nullptr;
+    caps[dv & 15] = 0;
+    if ((e = cudaMalloc((void **)&bufs[dv & 15], need)) != cudaSuccess) return e;
+    caps[dv & 15] = need;
+  }
+  char *w = bufs[dv & 15];
   double *A = (double *)w, *C = (double *)(w + bA);
   ST *G = (ST *)(w + 2 * bA), *U = (ST *)(w + 2 * bA + bG);
   ST *ea = (ST *)(w + 2 * bA + 2 * bG), *eb = (ST *)((char *)ea + bE), *ec = (ST *)((char *)eb + bE),
@@ -384,7 +399,6 @@ static cudaError_t wide_batch_chunk(const cs_system &sys, const cs_deer_config &
     k_wb_finish<ST><<<g_for((int64_t)B * D), 256, 0, st>>>(B, L, D, G, ctl, finals, info, err_step);
     e = cudaGetLastError();
   }
-  cudaFreeAsync(w, st);
   return e;
 }
 
