@@ -1,10 +1,10 @@
 """Reference fixtures at the BASELINE.json sizes (cfg1 T=10K, cfg2 T=100K,
-cfg3 diag T=100K, cfg5 T=1M), made by running the REFERENCE itself.
+cfg3 diag T=100K, cfg4 D=1000 L=100, cfg5 T=1M), made by running the REFERENCE itself.
 
 Run in the build container (the only place /root/reference exists):
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
-        CHAINSCAN_THREADS=8 python tests/golden/make_golden_big.py [cfg1 cfg2 cfg3 cfg5]
+        CHAINSCAN_THREADS=8 python tests/golden/make_golden_big.py [cfg1 cfg2 cfg3 cfg4 cfg5]
 
 The full traces are too large to commit, so each fixture keeps a compact but
 size-independent record of the run: iterations, converged, the whole
@@ -109,6 +109,31 @@ def cfg3():
     save("big_cfg3_mala_blr100_T100K", out)
 
 
+def cfg4():
+    # the leapfrog trajectory inside one HMC proposal at full width: D = 1000
+    # correlated Gaussian, L = 100, eps = 0.05, block vs diag
+    from chainscan.samplers import LeapfrogSystem
+
+    out = {"stride": np.array(10)}
+    D = 1000
+    rng = np.random.default_rng(0)
+    Q, _ = np.linalg.qr(rng.normal(size=(D, D)))
+    lam = np.exp(rng.uniform(np.log(0.1), np.log(10.0), D))
+    Lc = np.linalg.cholesky((Q * lam) @ Q.T)
+    m = model_logp_grad_hvp(gaussian(np.zeros(D), Lc))
+    x0 = np.random.default_rng(1).normal(size=D)
+    v0 = np.random.default_rng(2).normal(size=D)
+    s0 = np.concatenate([x0, v0 + 0.5 * 0.05 * m.grad(x0)])
+    lf = LeapfrogSystem(m, eps=0.05, L=100, probe_seed=0)
+    out["s0"] = s0
+    seq = sequential_evaluate(lf, s0)
+    out["seq_rows"] = seq[9::10].copy()
+    for mode, pre in (("block2x2-stochastic", "block_"), ("diag-stochastic", "diag_")):
+        r, w = timed_deer(LeapfrogSystem(m, eps=0.05, L=100, probe_seed=0), s0, DeerConfig(mode=mode, workers=WORKERS))
+        record(out, pre, r, 10, w)
+    save("big_cfg4_leapfrog_gauss1000", out)
+
+
 def cfg5():
     out = {"stride": np.array(2000)}
     data = generate_eight_schools()
@@ -124,7 +149,7 @@ def cfg5():
 
 
 if __name__ == "__main__":
-    todo = sys.argv[1:] or ["cfg1", "cfg2", "cfg5", "cfg3"]
+    todo = sys.argv[1:] or ["cfg1", "cfg2", "cfg4", "cfg5", "cfg3"]
     for name in todo:
         t0 = time.perf_counter()
         globals()[name]()
