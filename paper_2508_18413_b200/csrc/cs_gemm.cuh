@@ -7,8 +7,8 @@
 //
 // Inputs are f32 or f64 and are widened to f64 on their way into shared
 // memory; accumulation is f64, the result is rounded once to C's type.  Tiles:
-// BM x 64 outputs per CTA (BM = 64: 16 warps, BM = 32: 8 warps), each warp a
-// 16 x 16 block (2 x 2 DMMA tiles); K in steps of 16, the next step's operands
+// BM x 64 outputs per CTA -- BM = 128: 8 warps of 32 x 32 (4 x 4 DMMA tiles);
+// BM = 64 / 32: 16 / 8 warps of 16 x 16 for smaller problems; K in steps of 16, the next step's operands
 // loaded into registers while the current one is multiplied (double-buffered
 // shared memory).  Strides of the staged tiles are chosen so every DMMA
 // fragment load is bank-conflict free.  The summation order is fixed (k
@@ -24,8 +24,7 @@ namespace cs {
 
 namespace gemm_detail {
 
-constexpr int kBK = 16, kBN = 64;
-constexpr int kLDA = kBK + 4;  // 20 doubles: A fragments conflict free
+constexpr int kBN = 64;
 constexpr int kLDB = kBN + 4;  // 68 doubles: B fragments conflict free
 
 CS_D void dmma884(double (&c)[2], double a, double b) {
@@ -39,17 +38,31 @@ CS_D double ldg_d(const T *p) {
   return (double)__ldg(p);
 }
 
+// BM = 32 / 64: 16 x 16 warp tiles (BM/16 x 4 warps); BM = 128: 32 x 32 warp
+// tiles (4 x 2 warps), twice the DMMAs per fragment load for large products
+template <int BM> struct GemmWarps {
+  static constexpr int WT = BM == 128 ? 32 : 16;  // warp tile edge
+  static constexpr int WN = kBN / WT;             // warps across N
+  static constexpr int NT = (BM / WT) * WN * 32;  // threads
+  static constexpr int MI = WT / 8;               // DMMA tiles per warp edge
+  static constexpr int BK = BM == 128 ? 8 : 16;   // K per staged step (48 KB of static smem)
+  static constexpr int LDA = BK + 4;              // 12 / 20 doubles: A fragments conflict free
+};
+
 template <int BM, bool BT, typename TA, typename TB, typename TC>
-__global__ void __launch_bounds__(BM * 8)
+__global__ void __launch_bounds__(GemmWarps<BM>::NT)
 k_gemm(int M, int N, int K, const TA *__restrict__ A, int64_t lda, int64_t sA, const TB *__restrict__ B,
        int64_t ldb, int64_t sB, TC *__restrict__ C, int64_t ldc, int64_t sC) {
-  constexpr int NT = BM * 8;                     // threads
-  constexpr int EA = BM * kBK / NT;              // A elements per thread per K step (2)
-  constexpr int EB = kBK * kBN / NT;             // B elements per thread per K step (2 or 4)
+  using GW = GemmWarps<BM>;
+  constexpr int kBK = GW::BK, kLDA = GW::LDA;
+  constexpr int NT = GW::NT;                     // threads
+  constexpr int MI = GW::MI;
+  constexpr int EA = BM * kBK / NT;              // A elements per thread per K step
+  constexpr int EB = kBK * kBN / NT;             // B elements per thread per K step
   __shared__ __align__(16) double As[2][BM * kLDA];
   __shared__ __align__(16) double Bs[2][kBK * kLDB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / (kBN / 16), wn = warp % (kBN / 16);  // warp grid (BM/16) x 4
+  const int wm = warp / GW::WN, wn = warp % GW::WN;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * kBN;
   A += (int64_t)blockIdx.z * sA;
   B += (int64_t)blockIdx.z * sB;
@@ -89,11 +102,11 @@ k_gemm(int M, int N, int K, const TA *__restrict__ A, int64_t lda, int64_t sA, c
       else Bs[buf][(i / kBN) * kLDB + i % kBN] = rb[e];
     }
   };
-  double c[2][2][2];
+  double c[MI][MI][2];
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni) c[mi][ni][0] = c[mi][ni][1] = 0.0;
+    for (int ni = 0; ni < MI; ++ni) c[mi][ni][0] = c[mi][ni][1] = 0.0;
   const int nk = (K + kBK - 1) / kBK;
   load(0);
   store(0);
@@ -101,16 +114,20 @@ k_gemm(int M, int N, int K, const TA *__restrict__ A, int64_t lda, int64_t sA, c
   for (int s = 0; s < nk; ++s) {
     const int buf = s & 1;
     if (s + 1 < nk) load((s + 1) * kBK);  // in flight while this step multiplies
-    const double *as = As[buf] + (wm * 16 + (lane >> 2)) * kLDA + (lane & 3);
-    const double *bs = Bs[buf] + (lane & 3) * kLDB + wn * 16 + (lane >> 2);
+    const double *as = As[buf] + (wm * GW::WT + (lane >> 2)) * kLDA + (lane & 3);
+    const double *bs = Bs[buf] + (lane & 3) * kLDB + wn * GW::WT + (lane >> 2);
 #pragma unroll
     for (int k0 = 0; k0 < kBK; k0 += 4) {
-      const double a0 = as[k0], a1 = as[8 * kLDA + k0];
-      const double b0 = bs[k0 * kLDB], b1 = bs[k0 * kLDB + 8];
-      dmma884(c[0][0], a0, b0);
-      dmma884(c[0][1], a0, b1);
-      dmma884(c[1][0], a1, b0);
-      dmma884(c[1][1], a1, b1);
+      double av[MI], bv[MI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        av[i] = as[i * 8 * kLDA + k0];
+        bv[i] = bs[k0 * kLDB + i * 8];
+      }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < MI; ++ni) dmma884(c[mi][ni], av[mi], bv[ni]);
     }
     if (s + 1 < nk) {
       store(buf ^ 1);  // the other buffer's last readers finished before the previous barrier
@@ -118,11 +135,11 @@ k_gemm(int M, int N, int K, const TA *__restrict__ A, int64_t lda, int64_t sA, c
     }
   }
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni) {
-      const int gm = m0 + wm * 16 + mi * 8 + (lane >> 2);
-      const int gn = n0 + wn * 16 + ni * 8 + 2 * (lane & 3);
+    for (int ni = 0; ni < MI; ++ni) {
+      const int gm = m0 + wm * GW::WT + mi * 8 + (lane >> 2);
+      const int gn = n0 + wn * GW::WT + ni * 8 + 2 * (lane & 3);
       if (gm >= M) continue;
       if (gn < N) C[(int64_t)gm * ldc + gn] = (TC)c[mi][ni][0];
       if (gn + 1 < N) C[(int64_t)gm * ldc + gn + 1] = (TC)c[mi][ni][1];
@@ -138,16 +155,21 @@ cudaError_t gemm_rm(bool bt, int M, int N, int K, const TA *A, int64_t lda, int6
                     int64_t sB, TC *C, int64_t ldc, int64_t sC, int batch, cudaStream_t st) {
   using namespace gemm_detail;
   if (M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
-  const int64_t tiles64 = (int64_t)((M + 63) / 64) * ((N + kBN - 1) / kBN) * batch;
-  const bool small = tiles64 < 2 * 148;
-  const int BM = small ? 32 : 64;
-  const dim3 grid((N + kBN - 1) / kBN, (M + BM - 1) / BM, batch);
-  if (small) {
-    if (bt) k_gemm<32, true, TA, TB, TC><<<grid, 256, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
-    else k_gemm<32, false, TA, TB, TC><<<grid, 256, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  const int64_t nt = (N + kBN - 1) / kBN;
+  const int64_t tiles128 = (int64_t)((M + 127) / 128) * nt * batch, tiles64 = (int64_t)((M + 63) / 64) * nt * batch;
+  // the largest tile that still gives every SM a couple of CTAs
+  const int BM = tiles128 >= 4 * 148 ? 128 : tiles64 >= 2 * 148 ? 64 : 32;
+  const dim3 grid((unsigned)nt, (M + BM - 1) / BM, batch);
+  auto go = [&](auto kern, int threads) { kern<<<grid, threads, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC); };
+  if (BM == 128) {
+    if (bt) go(k_gemm<128, true, TA, TB, TC>, GemmWarps<128>::NT);
+    else go(k_gemm<128, false, TA, TB, TC>, GemmWarps<128>::NT);
+  } else if (BM == 64) {
+    if (bt) go(k_gemm<64, true, TA, TB, TC>, GemmWarps<64>::NT);
+    else go(k_gemm<64, false, TA, TB, TC>, GemmWarps<64>::NT);
   } else {
-    if (bt) k_gemm<64, true, TA, TB, TC><<<grid, 512, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
-    else k_gemm<64, false, TA, TB, TC><<<grid, 512, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
+    if (bt) go(k_gemm<32, true, TA, TB, TC>, GemmWarps<32>::NT);
+    else go(k_gemm<32, false, TA, TB, TC>, GemmWarps<32>::NT);
   }
   return cudaGetLastError();
 }

@@ -32,6 +32,11 @@ def main():
         cfg = cs.DeerConfig(mode="diag-stochastic", hutchinson_samples=3, preconditioner=k.recommended_preconditioner(),
                             max_iters=400)
         r = cs.run_deer(k, s0, cfg)
+    elif which == "3d":  # cfg3 "full": dense Newton, f32 states (the tcgen05 Hessian path)
+        X, y, _ = cs.synthetic_credit_like(seed=20250819, n=1000, dim=100)
+        m = cs.model_logp_grad_hvp(cs.blr(X, y, 1.0))
+        k = cs.MalaKernel(m, 0.003, seed=4, T=100_000, dtype=torch.float32)
+        r = cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode="dense", max_iters=int(sys.argv[2]) if len(sys.argv) > 2 else None))
     elif which == "3":
         X, y, _ = cs.synthetic_credit_like(seed=20250819, n=1000, dim=100)
         m = cs.model_logp_grad_hvp(cs.blr(X, y, 1.0))
