@@ -615,6 +615,15 @@ int cs_system_block_jacobian(const cs_system *sys, int dtype, const int64_t *ts,
 }
 int cs_system_sequential(const cs_system *sys, int dtype, const void *s0, int64_t T, void *out, int64_t *bad_step,
                          void *stream) {
+  if (sys && dtype_ok(dtype) && !sys->basis && blr_mala_ok(*sys, CS_MODE_DIAG)) {
+    // logistic-regression MALA: one CTA walks the chain with the target's data
+    // products in the CTA (not the register path)
+    k_set_i64<<<1, 1, 0, S(stream)>>>((long long *)bad_step, kNoStep);
+    if (T < 1) return CS_OK;
+    const cudaError_t e = blr_sequential(*sys, dtype, s0, T, out, (long long *)bad_step, S(stream));
+    if (e == cudaErrorNotSupported) return fail(CS_ERR_CONFIG, "sequential walk: D <= 128 and N <= 4096 data rows");
+    return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_system_sequential (logistic regression)");
+  }
   SysCall c{3, nullptr, 1, T, s0, nullptr, out, nullptr, nullptr, nullptr, (long long *)bad_step, 0, 0, 0};
   return syscall(sys, dtype, c, stream, "cs_system_sequential");
 }

@@ -465,6 +465,126 @@ k_blr_fused(cs_system sys, cs_deer_config cfg, int64_t iteration, int64_t t0, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// sequential_evaluate (core.py:163-184) for BLR MALA: one CTA walks the chain
+// in order, f64.  The state's logits, gradient and log density are carried from
+// step to step (the next state is either the proposal or the state itself), so
+// each step evaluates the target once, at the proposal: eta = X x~ (a warp per
+// data row, lanes across D), p = sigmoid(eta), g = (y - p) X - prec x~ (a thread
+// per column over a slice of the rows, slices summed in order), the MALA gate
+// (samplers.py:95-122).  X (800 KB at cfg 3) is read from L2 every step.
+constexpr int kSeqThr = 1024;
+constexpr int kSeqMaxN = 4096;
+
+CS_D double seq_eval(const double *X, const double *y, int N, int D, double prec, const double *xs, double *eta,
+                     double *P, double *part, double *g, double *red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kSeqThr / 32;
+  // eta_n = X[n] . x  and the log-density terms eta.y, logaddexp(0, eta)
+  double a = 0.0, b = 0.0;
+  for (int n = warp; n < N; n += nw) {
+    double e = 0.0;
+    for (int d = lane; d < D; d += 32) e += __ldg(X + (size_t)n * D + d) * xs[d];
+    e = warp_sum(e);
+    if (lane == 0) {
+      const double em = exp(-e), p = 1.0 / (1.0 + em), yn = __ldg(y + n);
+      eta[n] = e;
+      P[n] = yn - p;
+      a += e * yn;
+      b += e != e ? e : fmax(e, 0.0) + log1p(e >= 0.0 ? em : exp(e));
+    }
+  }
+  if (lane == 0) {
+    red[2 * warp] = a;
+    red[2 * warp + 1] = b;
+  }
+  __syncthreads();
+  // g_d = sum_n P_n X[n][d] - prec x_d: column d, rows split into kSeqThr / 128 slices
+  const int ns = kSeqThr / 128, d = tid & 127, sl = tid >> 7;
+  if (d < D) {
+    double acc = 0.0;
+    const int n0 = sl * ((N + ns - 1) / ns), n1 = min(N, n0 + (N + ns - 1) / ns);
+#pragma unroll 4
+    for (int n = n0; n < n1; ++n) acc += P[n] * __ldg(X + (size_t)n * D + d);
+    part[sl * 128 + d] = acc;
+  }
+  __syncthreads();
+  double lp = 0.0;
+  if (tid < D) {
+    double acc = 0.0;
+    for (int q = 0; q < ns; ++q) acc += part[q * 128 + tid];
+    g[tid] = acc - prec * xs[tid];
+  }
+  if (tid == 0) {
+    double aa = 0.0, bb = 0.0, ss = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      aa += red[2 * w];
+      bb += red[2 * w + 1];
+    }
+    for (int k = 0; k < D; ++k) ss += xs[k] * xs[k];
+    red[2 * nw] = (aa - bb) - 0.5 * prec * ss;  // logp = eta.y - sum logaddexp - prec/2 |x|^2
+  }
+  __syncthreads();
+  lp = red[2 * nw];
+  return lp;
+}
+
+template <typename ST>
+__global__ void __launch_bounds__(kSeqThr, 1)
+k_blr_sequential(cs_system sys, const ST *s0, int64_t T, ST *out, long long *bad) {
+  __shared__ double xs[128], xp[128], gS[128], gX[128], part[kSeqThr], red[2 * (kSeqThr / 32) + 2];
+  __shared__ int s_bad;
+  extern __shared__ double seq_dyn[];  // eta[N], P[N]
+  const int D = sys.dim, N = (int)sys.target.n_data;
+  const double prec = sys.target.prior_precision, eps = sys.eps, sq = sqrt(2.0 * eps);
+  const double *X = sys.target.X, *y = sys.target.y;
+  const ST *xi = (const ST *)sys.noise_vec;
+  double *eta = seq_dyn, *P = seq_dyn + N;
+  const int tid = threadIdx.x;
+  if (tid < D) xs[tid] = (double)s0[tid];
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  double lpS = seq_eval(X, y, N, D, prec, xs, eta, P, part, gS, red);
+  for (int64_t t = 1; t <= T; ++t) {
+    // proposal x~ = S + eps g(S) + sqrt(2 eps) xi_t  (samplers.py:206)
+    if (tid < D) {
+      const double xv = (xs[tid] + eps * gS[tid]) + sq * (double)xi[t * D + tid];
+      xp[tid] = xv;
+      if (!isfinite(xv)) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (tid == 0) *bad = t;
+      return;
+    }
+    const double lpX = seq_eval(X, y, N, D, prec, xp, eta, P, part, gX, red);
+    // gate: delta = logp(x~) - logp(S) - |r|^2/(4 eps) + |xi|^2/2, r = S - x~ - eps g(x~)
+    if (tid == 0) {
+      double srb = 0.0, sxi = 0.0;
+      for (int k = 0; k < D; ++k) {
+        const double r = (xs[k] - xp[k]) - eps * gX[k];
+        const double z = (double)xi[t * D + k];
+        srb += r * r;
+        sxi += z * z;
+      }
+      const double delta = lpX - lpS - srb / (4.0 * eps) + 0.5 * sxi;
+      const double margin = fmin(0.0, delta) - __ldg(sys.noise_logu + t);
+      red[2 * (kSeqThr / 32) + 1] = margin > 0.0 ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    const bool acc = red[2 * (kSeqThr / 32) + 1] > 0.0;
+    if (acc) {
+      if (tid < D) {
+        xs[tid] = xp[tid];
+        gS[tid] = gX[tid];
+      }
+      lpS = lpX;
+    }
+    __syncthreads();
+    if (tid < D) out[(t - 1) * D + tid] = (ST)xs[tid];  // the walk itself stays f64 (as k_sys_seq)
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 bool blr_fused_ok(const cs_system &s, const cs_deer_config &cfg) {
@@ -494,6 +614,25 @@ cudaError_t elements_blr_fused(const cs_system &sys, const cs_deer_config &cfg, 
     if (e != cudaSuccess) return e;
     k<<<grid, kFThr, kFSmem, st>>>(sys, cfg, iteration, t0, n, (const float *)s0, (const float *)guess,
                                    (float *)j, (float *)u, stats);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace cs
+
+namespace cs {
+
+cudaError_t blr_sequential(const cs_system &sys, int dtype, const void *s0, int64_t T, void *out, long long *bad,
+                           cudaStream_t st) {
+  const int N = (int)sys.target.n_data;
+  if (sys.dim > 128 || N > kSeqMaxN) return cudaErrorNotSupported;
+  const size_t smem = sizeof(double) * 2 * (size_t)N;
+  if (dtype == CS_F64) {
+    cudaFuncSetAttribute(k_blr_sequential<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_blr_sequential<double><<<1, kSeqThr, smem, st>>>(sys, (const double *)s0, T, (double *)out, bad);
+  } else {
+    cudaFuncSetAttribute(k_blr_sequential<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_blr_sequential<float><<<1, kSeqThr, smem, st>>>(sys, (const float *)s0, T, (float *)out, bad);
   }
   return cudaGetLastError();
 }

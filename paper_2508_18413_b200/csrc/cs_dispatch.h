@@ -13,6 +13,8 @@ cudaError_t elements_wide(const cs_system &sys, const cs_deer_config &cfg, int d
                           cs_elem_stats *stats, cudaStream_t st);
 bool blr_mala_ok(const cs_system &s, int mode);
 bool blr_fused_ok(const cs_system &s, const cs_deer_config &cfg);
+cudaError_t blr_sequential(const cs_system &sys, int dtype, const void *s0, int64_t T, void *out, long long *bad,
+                           cudaStream_t st);
 cudaError_t elements_blr_fused(const cs_system &sys, const cs_deer_config &cfg, int dtype, int64_t iteration,
                                int64_t t0, int64_t n, const void *s0, const void *guess, void *j, void *u,
                                cs_elem_stats *stats, cudaStream_t st);

@@ -127,7 +127,13 @@ class _Fused(TransitionSystem):
 
     @property
     def _sequential(self):
-        return self._sequential_kernel if self.kernels else None
+        if self.kernels:
+            return self._sequential_kernel
+        # logistic-regression MALA walks on the device too (one CTA per chain)
+        if self._kind == _lib.CS_SYS_MALA and getattr(self, "_blr_walk", None) is None:
+            d = self.desc()
+            self._blr_walk = bool(d.target.kind == _lib.CS_TARGET_BLR and d.dim <= 128 and d.target.n_data <= 4096)
+        return self._sequential_kernel if getattr(self, "_blr_walk", False) else None
 
     def _sequential_kernel(self, s0, T):
         out = torch.empty((T, self.dim), dtype=self.dtype, device=self.device)

@@ -200,9 +200,12 @@ def test_cfg3_blr_diag_T100K_vs_reference(cuda_device):
     ok = O.MalaKernel(O.blr(Xo, yo, 1.0), 0.003, seed=4, T=100_000)
     acc = accept_mask(ok, np.zeros(100), np_(res.trace)[:prefix])
     np.testing.assert_array_equal(acc, ref_accept(g, 100_000)[:prefix])
-    # the device's sequential chain against the reference's (rows 500 and 1000)
-    seq = np_(cs.sequential_evaluate(k, np.zeros(100), 1000))
-    np.testing.assert_allclose(seq[[499, 999]], g["seq_rows"][:2], rtol=1e-9, atol=1e-9)
+    # the device's sequential chain (one CTA walking all 100K steps) against the
+    # reference's: every 500th row and all accept / reject decisions
+    seq = np_(cs.sequential_evaluate(k, np.zeros(100)))
+    np.testing.assert_allclose(seq[499::500], g["seq_rows"], rtol=1e-9, atol=1e-9)
+    moved = np.any(np.diff(np.vstack([np.zeros(100), seq]), axis=0) != 0, axis=1)
+    np.testing.assert_array_equal(moved, ref_accept(g, 100_000))
 
 
 # ---------------------------------------------------------------------------
