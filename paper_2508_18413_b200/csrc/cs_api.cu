@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "cs_dispatch.h"
@@ -277,6 +278,7 @@ __global__ void k_first_stamp(const int32_t *lf, int64_t n, int32_t it, long lon
 struct SolveState {
   int dev;
   cudaStream_t st;
+  std::thread::id host;  // per host thread too: two threads sharing a stream get separate outcome records
   SolveCtl *ctl;
   int *ready;
   SolveOut *out;  // host-mapped (UVA: the same pointer on the device)
@@ -865,12 +867,14 @@ int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, co
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
+    const std::thread::id me = std::this_thread::get_id();
     for (SolveState *x : states)
-      if (x->dev == dev && x->st == st) ss = x;
+      if (x->dev == dev && x->st == st && x->host == me) ss = x;
     if (!ss) {
       SolveState n{};
       n.dev = dev;
       n.st = st;
+      n.host = me;
       cudaError_t e = cudaMalloc(&n.ctl, sizeof(SolveCtl) + sizeof(int) * kReadyStride * 8 * (size_t)sms);
       if (e == cudaSuccess) e = cudaHostAlloc(&n.out, sizeof(SolveOut), cudaHostAllocMapped);
       if (e == cudaSuccess) e = cudaEventCreate(&n.ev0);
