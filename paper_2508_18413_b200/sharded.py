@@ -184,15 +184,21 @@ class CudaShardOps(ShardOps):
         return _bookkeeping(guess.contiguous(), nxt, atol, rtol, iteration, last_fail, _scratch(guess.device))
 
 
-def _gather(vec: torch.Tensor, group, world):
-    """All-gather a small vector; the result lives on ``vec``'s device (a gloo
-    group stages CUDA vectors through the host and moves the result back)."""
+def _gather(vec: torch.Tensor, group, world, out: torch.Tensor | None = None):
+    """All-gather a small vector into a (world, n) tensor on ``vec``'s device (a
+    gloo group stages CUDA vectors through the host and moves the result back).
+    NCCL groups gather straight into ``out`` when given (one collective, no
+    list of per-rank buffers)."""
     dev = vec.device
-    if vec.is_cuda and dist.get_backend(group) == "gloo":  # host-side groups (CPU tests) stage through host
+    if dist.get_backend(group) != "nccl":  # gloo (CPU tests): host tensors, per-rank list
         vec = vec.cpu()
-    out = [torch.empty_like(vec) for _ in range(world)]
-    dist.all_gather(out, vec, group=group)
-    return torch.stack(out).to(dev)
+        res = [torch.empty_like(vec) for _ in range(world)]
+        dist.all_gather(res, vec, group=group)
+        return torch.stack(res).to(dev)
+    if out is None:
+        out = torch.empty((world, vec.numel()), dtype=vec.dtype, device=vec.device)
+    dist.all_gather_into_tensor(out, vec.contiguous(), group=group)
+    return out
 
 
 def _streamed_shard_ok(system, cfg) -> bool:
@@ -361,6 +367,11 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
     stats_info = {"path": "sharded-streamed", "world": world, "rows": (lo, hi), "collectives_per_iteration": 3}
     vB = torch.empty(W + 1, dtype=torch.float64, device=dev)
     vC = torch.empty(2 + D, dtype=torch.float64, device=dev)
+    oA = torch.empty((world, 4), dtype=torch.float64, device=dev)
+    oB = torch.empty((world, W + 1), dtype=torch.float64, device=dev)
+    oC = torch.empty((world, 2 + D), dtype=torch.float64, device=dev)
+    both = torch.empty(2 * world + 4 * world, dtype=torch.float64, device=dev)
+    both_h = torch.empty(both.numel(), dtype=torch.float64).pin_memory() if dev.type == "cuda" else None
 
     def build(it_, halo_):
         rc_ = lib.cs_system_elements_range(ctypes.byref(d), ctypes.byref(c), dt, it_, lo, n, _lib.ptr(halo_),
@@ -404,7 +415,7 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
             _lib.check(rc)
             vB[:W].copy_(agg)
             vB[W].fill_(0.0)
-            gB = _gather(vB, group, world).to(dev)
+            gB = _gather(vB, group, world, oB)
             carry = s0.to(torch.float64)
             for q in range(rank):  # prefix fix-up, shard by shard (_scan_kernels.py:32-36)
                 carry = apply_agg(mode, gB[q, :W], carry)
@@ -434,14 +445,21 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
             vC[0:1].copy_(stats[28:32].view(torch.int32).double())
             vC[1:2].copy_(stats[32:40].view(torch.float64))
             vC[2:].copy_(guess[-1])
-            gC_dev = _gather(vC, group, world).to(dev)
+            gC_dev = _gather(vC, group, world, oC)
             if rank > 0:
                 halo = gC_dev[rank - 1, 2:].to(dtype).contiguous()
             build(it, halo)  # speculative: the next iteration's elements
-            gA_dev = _gather(flags_dev(), group, world).to(dev)
-            both = torch.cat([gC_dev[:, :2].reshape(-1), gA_dev.reshape(-1)]).cpu().numpy()
-            gC = both[:2 * world].reshape(world, 2)
-            gA = both[2 * world:].reshape(world, 4)
+            gA_dev = _gather(flags_dev(), group, world, oA)
+            both[:2 * world].view(world, 2).copy_(gC_dev[:, :2])
+            both[2 * world:].view(world, 4).copy_(gA_dev)
+            if both_h is not None:  # one pinned read for both gathered vectors
+                both_h.copy_(both, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+                bh = both_h.numpy()
+            else:
+                bh = both.cpu().numpy()
+            gC = bh[:2 * world].reshape(world, 2)
+            gA = bh[2 * world:].reshape(world, 4)
         else:
             _, _, _, _, nfail, dmax = _parse_stats(stats)
             gC = np.array([[float(nfail), dmax]])
