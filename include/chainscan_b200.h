@@ -137,6 +137,11 @@ int cs_debug_probe(unsigned long long *dev_buf, int n);
  * device inputs.  The Hessian term of the dense logistic-regression builder. */
 int cs_debug_gram(const double *X, int32_t N, int32_t D, const double *W, int64_t T, float *H_out,
                   void *stream);
+/* The same product through the pair-Gram GEMM (all steps at once: W Q^T over
+ * the data-row pairs, tcgen05 + bulk-copy operand tiles), unpacked into the
+ * same 128 x 128 zero-padded layout. */
+int cs_debug_pair_gram(const double *X, int32_t N, int32_t D, const double *W, int64_t T, float *H_out,
+                       void *stream);
 int cs_device_sm_count(int *out);
 
 /* ---- counter-based noise (noise.py:50-80, 140-156, 159-171) ------------- */

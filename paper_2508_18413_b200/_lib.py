@@ -72,6 +72,7 @@ _SIGS = {
     "cs_version": ([], ctypes.c_int),
     "cs_debug_probe": ([P, ctypes.c_int], ctypes.c_int),
     "cs_debug_gram": ([P, i32, i32, P, i64, P, P], ctypes.c_int),
+    "cs_debug_pair_gram": ([P, i32, i32, P, i64, P, P], ctypes.c_int),
     "cs_device_sm_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "cs_noise_fill": ([ctypes.c_int, u64, u64, i64, i64, i32, f64, ctypes.c_int, P, P], ctypes.c_int),
     "cs_rademacher_fill": ([u64, i64, P, i64, i64, i32, i32, ctypes.c_int, P, P], ctypes.c_int),

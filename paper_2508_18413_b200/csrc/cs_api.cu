@@ -299,6 +299,12 @@ int cs_debug_gram(const double *X, int32_t N, int32_t D, const double *W, int64_
   const cudaError_t e = debug_gram(X, N, D, W, T, H_out, S(stream));
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_debug_gram");
 }
+int cs_debug_pair_gram(const double *X, int32_t N, int32_t D, const double *W, int64_t T, float *H_out,
+                       void *stream) {
+  if (!X || !W || !H_out || N < 1 || D < 1 || D > 128 || T < 0) return fail(CS_ERR_CONFIG, "bad gram arguments");
+  const cudaError_t e = debug_pair_gram(X, N, D, W, T, H_out, S(stream));
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_debug_pair_gram");
+}
 
 int cs_debug_probe(unsigned long long *dev_buf, int n) {
   h_probe = dev_buf;

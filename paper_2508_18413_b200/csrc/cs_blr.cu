@@ -54,12 +54,26 @@ __global__ void k_blr_prologue(cs_system sys, const ST *s0, const ST *guess, int
   }
 }
 
+// float offset of element (row, k) in the tiled operand layout: tile (row / 128,
+// k / 32) is 128 rows x 128 B, 16-byte chunk c of row rr stored at c ^ (rr & 7)
+CS_D int64_t swz_index(int64_t row, int k, int nkb) {
+  const int rr = (int)(row & 127), c = (k & 31) >> 2;
+  return (((row >> 7) * nkb + (k >> 5)) * 128 + rr) * 32 + ((c ^ (rr & 7)) << 2) + (k & 3);
+}
+
+// first packed index of triangle row i (pairs (i, j >= i), row-major)
+CS_D int pair_row_start(int i, int D) { return i * D - i * (i - 1) / 2; }
+
 // per step r (one warp, lanes across the N data rows): p = sigmoid(eta),
 // E[r] <- y - p, probe rows <- p(1-p) . (z X^T), and the two log-density row
 // sums eta.y and sum logaddexp(0, eta).  exp(-eta) serves both the sigmoid and,
 // for eta >= 0, logaddexp's exp(-|eta|).
+// wsw (optional): the weights again as f32 in the tiled tcgen05 operand layout
+// of the pair-Gram GEMM (k_pair_gram): 128-step x 32-row tiles, K-major,
+// SWIZZLE_128B, zero past N (nkb = padded data rows / 32)
 __global__ void __launch_bounds__(256) k_blr_epilogue(double *E, const double *y, int64_t T, int K, int N,
-                                                       double *rowsum, double *wout = nullptr) {
+                                                       double *rowsum, double *wout = nullptr,
+                                                       float *wsw = nullptr, int nkb = 0) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < T; r += nw) {
@@ -75,8 +89,11 @@ __global__ void __launch_bounds__(256) k_blr_epilogue(double *E, const double *y
       er[n] = yn - p;
       const double w = p * (1.0 - p);
       if (wout) wout[r * N + n] = w;
+      if (wsw) wsw[swz_index(r, n, nkb)] = (float)w;
       for (int k = 0; k < K; ++k) E[((int64_t)(k + 1) * T + r) * N + n] *= w;
     }
+    if (wsw)
+      for (int n = N + lane; n < 32 * nkb; n += 32) wsw[swz_index(r, n, nkb)] = 0.0f;
     a = warp_sum(a);
     b = warp_sum(b);
     if (lane == 0) {
@@ -299,7 +316,9 @@ __global__ void k_bd_xf(const double *X, int N, int D, float *Xf) {
 
 constexpr int kTcKB = 32, kTcLD = 136;  // n rows per staged block; padded row stride (conflict-free fragments)
 
-// TCM: 0 = FP32/FP64 pipes, 1 = mma.sync TF32, 2 = tcgen05 (UMMA, TMEM accumulator)
+// TCM: 0 = FP32/FP64 pipes, 1 = mma.sync TF32, 2 = tcgen05 (UMMA, TMEM accumulator),
+// 3 = H_raw read from the pair-Gram GEMM's output (Xf = Hp, ldx = its row stride;
+// the next step's packed triangle is copied in by cp.async behind this step)
 template <typename ST, int DP, int TCM>
 __global__ void __launch_bounds__(kBdThr)
 k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, const double *A2, const double *GX,
@@ -319,7 +338,7 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
   constexpr int HLD = DP + 1;  // Hessian tile row stride: row and column walks are both bank-conflict free
   constexpr int HS = TCM == 2 && 2 * kUmmaStages * kUmmaTile > DP * HLD ? 2 * kUmmaStages * kUmmaTile : DP * HLD;
   CT *Xs = Hs + HS;  // SIMT: 2 x SL x DP; mma.sync: 2 x kTcKB x kTcLD + 2 x kTcKB weights; tcgen05: ldx weights
-  double *vS = TCM == 2 ? (double *)(((uintptr_t)(Xs + ldx) + 15) & ~(uintptr_t)15)
+  double *vS = TCM >= 2 ? (double *)(((uintptr_t)(Xs + ldx) + 15) & ~(uintptr_t)15)
                         : (double *)(Xs + XS + ((XS & 1) ? 1 : 0));
   double *vX = vS + DP, *vG = vX + DP, *vR = vG + DP, *vW = vR + DP, *vH = vW + DP, *vP = vH + DP;
   __shared__ double red[4][kBdThr / 32];
@@ -352,6 +371,13 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     }
   };
   if constexpr (TCM == 2) wload(blockIdx.x);
+  static_assert(TCM != 3 || sizeof(ST) == 4, "pair-Gram Hessian: f32");
+  const int hp_chunks = (D * (D + 1) / 2 + 3) / 4;
+  auto hp_fetch = [&](int64_t rr) {  // step rr's packed triangle -> the staging row Xs
+    if (rr < sys.T)
+      for (int q = tid; q < hp_chunks; q += kBdThr) cp_async16(Xs + 4 * q, Xf + rr * ldx + 4 * q);
+  };
+  if constexpr (TCM == 3) hp_fetch(blockIdx.x);
   for (int64_t r = blockIdx.x; r < sys.T; r += gridDim.x) {
     const int64_t t = r + 1;
     const double *w = WS + r * N;
@@ -379,6 +405,18 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
       __syncthreads();
       gram_tcgen05<kBdThr>(pipe, Xf, ldx, N, wbuf, (float *)Hs, (float *)Hs, HLD);
       wload(r + gridDim.x);
+    } else if constexpr (TCM == 3) {
+      cp_async_wait_all();
+      __syncthreads();
+      // unpack: warp per triangle row, both halves of the symmetric tile
+      for (int i = wid; i < D; i += kBdThr / 32) {
+        const float *src = (const float *)Xs + pair_row_start(i, D) - i;
+        for (int j = i + lane; j < D; j += 32) {
+          const float v = src[j];
+          Hs[i * HLD + j] = v;
+          Hs[j * HLD + i] = v;
+        }
+      }
     } else if constexpr (TC) {
       // H_raw on the tensor cores (mma.sync m16n8k8 TF32, f32 accumulate):
       // warp wid owns output rows 16 wid .. 16 wid + 15, all 16 column blocks
@@ -528,6 +566,7 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
     }
     if (tid < 3) flags[tid] = 0;
     __syncthreads();  // Hs, vectors, partial sums
+    if constexpr (TCM == 3) hp_fetch(r + gridDim.x);  // the staging row is free again
     ss = sx = sr = sxi = 0.0;
 #pragma unroll
     for (int k = 0; k < kBdThr / 32; ++k) {
@@ -650,6 +689,111 @@ __global__ void k_bd_xt(const double *X, int N, int D, int ldx, float *XT) {
   }
 }
 
+// ---- H_t for every step as ONE GEMM over data-row pairs ---------------------
+// H_raw,t[i][j] = sum_n w_t[n] X[n][i] X[n][j] = (W Q^T)[t][p(i, j)] with
+// Q[p(i, j)][n] = X[n][i] X[n][j] over the upper-triangle pairs p (row-major,
+// p(i, j) = i D - i (i - 1) / 2 + j - i).  The per-step weights become the A
+// operand and the data products a fixed B operand, so the tensor cores stream
+// TMA-loaded tiles instead of re-forming w . X^T per step (k_bd_final TCM 2).
+
+// Q in the tiled operand layout (see swz_index), pairs >= P and data rows >= N zero
+__global__ void k_pair_operand(const double *X, int N, int D, int nkb, int P, int64_t total, float *Qt) {
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(o & 3), sc = (int)((o >> 2) & 7), rr = (int)((o >> 5) & 127);
+    const int64_t tile = o >> 12;
+    const int kb = (int)(tile % nkb), nt = (int)(tile / nkb);
+    const int p = nt * 128 + rr, n = kb * 32 + ((sc ^ (rr & 7)) << 2) + e;
+    float v = 0.0f;
+    if (p < P && n < N) {
+      const double b = 2.0 * D + 1.0;
+      int i = (int)floor((b - sqrt(b * b - 8.0 * p)) * 0.5);
+      i = i < 0 ? 0 : (i >= D ? D - 1 : i);
+      while (i + 1 < D && pair_row_start(i + 1, D) <= p) ++i;
+      while (i > 0 && pair_row_start(i, D) > p) --i;
+      const int j = i + p - pair_row_start(i, D);
+      v = (float)(X[(int64_t)n * D + i] * X[(int64_t)n * D + j]);
+    }
+    Qt[o] = v;
+  }
+}
+
+// Hp (f32, row stride ldp) = W Q^T: one 128-step x 128-pair tile per CTA, K =
+// the data rows in blocks of 32.  Warp 0 lane 0 moves the pre-tiled operand
+// blocks with 1-D bulk copies (TMA engine), warp 1 lane 0 issues kind::tf32
+// MMAs into a TMEM accumulator; all four warps then drain TMEM through shared
+// memory and write the tile rows back with bulk stores.  Two CTAs per SM: one's
+// epilogue overlaps the other's MMAs.
+constexpr int kPgStages = 3;
+constexpr int kPgLd = 132;  // staged output row stride (floats): conflict-free v4 stores, 16-byte rows
+static_assert(128 * kPgLd <= kPgStages * 2 * kUmmaTile, "output staging fits the operand stages");
+
+__global__ void __launch_bounds__(128) k_pair_gram(const float *__restrict__ Wt, const float *__restrict__ Qt, int nkb,
+                                                  float *Hp, int64_t ldp) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  float *tiles = (float *)(((uintptr_t)psm + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[kPgStages], empty[kPgStages], done;
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int nt = blockIdx.x;
+  const int64_t mt = blockIdx.y;
+  if (tid == 0) {
+    for (int s = 0; s < kPgStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&done, 1);
+    fence_mbar_init();
+  }
+  const uint32_t tmem = tmem_alloc128(&s_tmem);  // its barrier also publishes the mbarrier inits
+  const float *Ab = Wt + mt * nkb * kUmmaTile, *Bb = Qt + (int64_t)nt * nkb * kUmmaTile;
+  if (wid == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kPgStages;
+        if (kb >= kPgStages) mbar_wait(&empty[s], ((kb / kPgStages) - 1) & 1);
+        float *A = tiles + s * 2 * kUmmaTile;
+        mbar_expect_tx(&full[s], 2 * kUmmaTile * sizeof(float));
+        bulk_g2s(A, Ab + (int64_t)kb * kUmmaTile, kUmmaTile * sizeof(float), &full[s]);
+        bulk_g2s(A + kUmmaTile, Bb + (int64_t)kb * kUmmaTile, kUmmaTile * sizeof(float), &full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (wid == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kPgStages;
+        mbar_wait(&full[s], (kb / kPgStages) & 1);
+        tc_fence_after();
+        const float *A = tiles + s * 2 * kUmmaTile;
+        const uint64_t da = umma_desc_sw128(A), db = umma_desc_sw128(A + kUmmaTile);
+#pragma unroll
+        for (int k = 0; k < kUmmaKB / 8; ++k)
+          umma_tf32(tmem, da + 2 * k, db + 2 * k, kIdescTf32_128x128, (kb | k) != 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(&done);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&done, 0);
+  tc_fence_after();
+  // TMEM lanes 32 w .. 32 w + 31 = this warp's tile rows -> staged rows -> bulk stores
+  const int row = 32 * wid + lane;
+  float *srow = tiles + row * kPgLd;
+#pragma unroll
+  for (int cc = 0; cc < 128; cc += 16) {
+    float v[16];
+    tmem_ld16(tmem + ((uint32_t)(32 * wid) << 16) + (uint32_t)cc, v);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) *(float4 *)(srow + cc + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+  fence_proxy_async_smem();
+  bulk_s2g(Hp + (mt * 128 + row) * ldp + (int64_t)nt * 128, srow, 128 * sizeof(float));
+  bulk_commit();
+  bulk_wait_read();
+  tmem_free128(tmem);
+}
+
 }  // namespace
 
 // test hook: H_t = X^T diag(W_t) X through the tcgen05 path, one CTA per t
@@ -729,10 +873,12 @@ static cudaError_t blr_run(const cs_system &sys, const cs_deer_config &cfg, int6
   return cudaGetLastError();
 }
 
-static int bd_tensor_cores() {  // f32 Hessian: 2 tcgen05 (default), 1 mma.sync, 0 FP32 pipes (CS_BLR_DENSE_TC)
+// f32 Hessian (CS_BLR_DENSE_TC): 3 pair-Gram GEMM on tcgen05 (default), 2 per-step
+// tcgen05 Gram, 1 mma.sync, 0 FP32 pipes
+static int bd_tensor_cores() {
   static const int v = [] {
     const char *e = getenv("CS_BLR_DENSE_TC");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 3;
   }();
   return v;
 }
@@ -743,7 +889,7 @@ static cudaError_t bd_final_launch(const cs_system &sys, const cs_deer_config &c
                                    const double *HR, const double *WS, const double *rsS, const double *rsX,
                                    const float *Xf, ST *J, ST *u, cs_elem_stats *stats, cudaStream_t st,
                                    int ldx = 0) {
-  const size_t xs = TCM == 1 ? 2 * kTcKB * kTcLD + 2 * kTcKB : TCM == 2 ? (size_t)ldx + 4 : 2 * 16 * DP;
+  const size_t xs = TCM == 1 ? 2 * kTcKB * kTcLD + 2 * kTcKB : TCM >= 2 ? (size_t)ldx + 4 : 2 * 16 * DP;
   const size_t hs = TCM == 2 && 2 * kUmmaStages * kUmmaTile > DP * (DP + 1) ? 2 * kUmmaStages * kUmmaTile : DP * (DP + 1);
   const size_t smem = sizeof(ST) * (hs + xs) + 8 + 7 * DP * sizeof(double) + (TCM == 2 ? 1024 : 0);
   auto k = k_bd_final<ST, DP, TCM>;
@@ -766,7 +912,13 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   std::lock_guard<std::mutex> lock(ctx.mu);
   // A, A2, G, gS, GX, R, HR (T x D); E, WS, WX (T x N); row sums 2 x (2T)
   // + Xf: X as f32 (N x 128, or its transpose 128 x ldx for tcgen05)
-  const size_t need = (size_t)7 * T * D + (size_t)3 * T * N + (size_t)4 * T + (size_t)64 * (N + 32);
+  // pair-Gram path: W tiles (Tpad x 32 nkb), Q tiles (ldp x 32 nkb), Hp (Tpad x ldp), f32
+  const bool pg = sizeof(ST) == 4 && bd_tensor_cores() == 3;
+  const int nkb = (N + 31) / 32, npairs = D * (D + 1) / 2;
+  const int64_t Tpad = (T + 127) / 128 * 128, ldp = (int64_t)(npairs + 127) / 128 * 128;
+  const size_t pg_floats = pg ? (size_t)(Tpad * 32 * nkb + ldp * 32 * nkb + Tpad * ldp) : 0;
+  const size_t need = (size_t)7 * T * D + (size_t)3 * T * N + (size_t)4 * T + (size_t)64 * (N + 32) +
+                      (pg_floats + 1) / 2 + 64;
   if (ctx.cap < need) {
     if (ctx.buf) cudaFree(ctx.buf);
     ctx.buf = nullptr;
@@ -780,6 +932,8 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   double *E = HR + (size_t)T * D, *WS = E + (size_t)T * N, *WX = WS + (size_t)T * N;
   double *rsS = WX + (size_t)T * N, *rsX = rsS + 2 * T;
   float *Xf = (float *)(rsX + 2 * T);
+  float *Wt = (float *)(((uintptr_t)(rsX + 2 * T + 64 * (N + 32)) + 255) & ~(uintptr_t)255);
+  float *Qt = Wt + Tpad * 32 * nkb, *Hp = Qt + ldp * 32 * nkb;
   const double *X = sys.target.X, *y = sys.target.y;
   auto gemm_xt = [&](const double *Ain, double *Cout) {  // C (T x N) = A (T x D) X^T
     return gemm_rm<double, double, double>(true, (int)T, N, D, Ain, D, 0, X, D, 0, Cout, N, 0, 1, st);
@@ -791,7 +945,22 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   const unsigned gw = (unsigned)((T * 32 + 255) / 256);
   k_blr_prologue<ST><<<ge, 256, 0, st>>>(sys, s0, guess, iteration, 0, A);
   if (cudaError_t ge = gemm_xt(A, E)) return ge;
-  k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsS, WS);
+  if (pg) {  // the weights go straight into the GEMM's operand tiles; H_raw for every step in one GEMM
+    k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsS, nullptr, Wt, nkb);
+    const int64_t qn = ldp * 32 * nkb;
+    k_pair_operand<<<(unsigned)((qn + 255) / 256 < 148 * 64 ? (qn + 255) / 256 : 148 * 64), 256, 0, st>>>(
+        X, N, D, nkb, npairs, qn, Qt);
+    const size_t smem = 1024 + (size_t)kPgStages * 2 * kUmmaTile * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_pair_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    k_pair_gram<<<dim3((unsigned)(ldp / 128), (unsigned)(Tpad / 128)), 128, smem, st>>>(Wt, Qt, nkb, Hp, ldp);
+  } else {
+    k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsS, WS);
+  }
   if (cudaError_t ge = gemm_x(E, G)) return ge;
   k_blr_propose<ST><<<gw, 256, 0, st>>>(sys, s0, guess, A, G, 0, A2, gS, stats);
   if (cudaError_t ge = gemm_xt(A2, E)) return ge;
@@ -802,6 +971,13 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   k_bd_scale<<<148 * 32, 256, 0, st>>>(E, WX, T * N);
   if (cudaError_t ge = gemm_x(E, HR)) return ge;
   if constexpr (sizeof(ST) == 4) {
+    if (pg) {
+      if (D <= 112)
+        return bd_final_launch<ST, 112, 3>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Hp, J, uout, stats,
+                                           st, (int)ldp);
+      return bd_final_launch<ST, 128, 3>(sys, cfg, s0, guess, A2, GX, gS, R, HR, WS, rsS, rsX, Hp, J, uout, stats,
+                                         st, (int)ldp);
+    }
     if (bd_tensor_cores() == 2) {  // f32 storage: H(S) on the 5th-gen tensor cores (tcgen05, TMEM accumulator)
       const int ldx = (N + 31) / 32 * 32;
       k_bd_xt<<<(128 * ldx + 255) / 256, 256, 0, st>>>(X, N, D, ldx, Xf);
@@ -836,6 +1012,45 @@ cudaError_t debug_gram(const double *X, int N, int D, const double *W, int64_t T
   k_gram_debug<<<(unsigned)(T < 148 ? T : 148), kBdThr, smem, st>>>(XT, ldx, N, W, T, H);
   e = cudaGetLastError();
   cudaFreeAsync(XT, st);
+  return e;
+}
+
+namespace {
+__global__ void k_w_tiles(const double *W, int64_t T, int N, int nkb, float *Wt) {  // W (T x N) -> operand tiles
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T * 32 * nkb; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / (32 * nkb);
+    const int n = (int)(i - r * 32 * nkb);
+    Wt[swz_index(r, n, nkb)] = n < N ? (float)W[r * N + n] : 0.0f;
+  }
+}
+__global__ void k_pair_unpack(const float *Hp, int64_t ldp, int64_t T, int D, float *H) {  // -> T x 128 x 128
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T * 128 * 128; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i >> 14;
+    const int a = (int)((i >> 7) & 127), b = (int)(i & 127);
+    const int lo = a < b ? a : b, hi = a < b ? b : a;
+    H[i] = (a < D && b < D) ? Hp[t * ldp + pair_row_start(lo, D) + hi - lo] : 0.0f;
+  }
+}
+}  // namespace
+
+cudaError_t debug_pair_gram(const double *X, int N, int D, const double *W, int64_t T, float *H, cudaStream_t st) {
+  const int nkb = (N + 31) / 32, npairs = D * (D + 1) / 2;
+  const int64_t Tpad = (T + 127) / 128 * 128, ldp = (int64_t)(npairs + 127) / 128 * 128;
+  if (T == 0) return cudaSuccess;
+  float *buf = nullptr;
+  const size_t nf = (size_t)(Tpad * 32 * nkb + ldp * 32 * nkb + Tpad * ldp);
+  cudaError_t e = cudaMallocAsync(&buf, sizeof(float) * nf, st);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(buf, 0, sizeof(float) * Tpad * 32 * nkb, st);
+  float *Wt = buf, *Qt = Wt + Tpad * 32 * nkb, *Hp = Qt + ldp * 32 * nkb;
+  k_w_tiles<<<148 * 8, 256, 0, st>>>(W, T, N, nkb, Wt);
+  k_pair_operand<<<148 * 8, 256, 0, st>>>(X, N, D, nkb, npairs, ldp * 32 * nkb, Qt);
+  const size_t smem = 1024 + (size_t)kPgStages * 2 * kUmmaTile * sizeof(float);
+  cudaFuncSetAttribute(k_pair_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_pair_gram<<<dim3((unsigned)(ldp / 128), (unsigned)(Tpad / 128)), 128, smem, st>>>(Wt, Qt, nkb, Hp, ldp);
+  k_pair_unpack<<<148 * 8, 256, 0, st>>>(Hp, ldp, T, D, H);
+  e = cudaGetLastError();
+  cudaFreeAsync(buf, st);
   return e;
 }
 

@@ -419,17 +419,20 @@ def test_run_deer_blr_gemm_path(cuda_device):
     _deer_cmp(h, g, "diag_", torch.float64)
 
 
-@pytest.mark.parametrize("N,D,T", [(1000, 100, 37), (77, 9, 5), (512, 128, 3), (33, 64, 300)])
-def test_tcgen05_weighted_gram(cuda_device, N, D, T):
+@pytest.mark.parametrize("N,D,T", [(1000, 100, 37), (77, 9, 5), (512, 128, 3), (33, 64, 300), (1000, 100, 1000)])
+@pytest.mark.parametrize("hook", ["cs_debug_gram", "cs_debug_pair_gram"])
+def test_tcgen05_weighted_gram(cuda_device, N, D, T, hook):
     # the 5th-gen tensor-core (tcgen05/TMEM) Hessian term X^T diag(w_t) X against
-    # an f64 evaluation; TF32 operands -> relative error ~1e-3 of the term scale
+    # an f64 evaluation -- per step (cs_debug_gram) and as one pair-Gram GEMM over
+    # all steps (cs_debug_pair_gram); TF32 operands -> relative error ~1e-3 of the
+    # term scale
     from paper_2508_18413_b200 import _lib
 
     g = torch.Generator(device=cuda_device).manual_seed(N + D)
     X = torch.randn((N, D), generator=g, device=cuda_device, dtype=torch.float64)
     W = torch.rand((T, N), generator=g, device=cuda_device, dtype=torch.float64) * 0.25
     H = torch.empty((T, 128, 128), device=cuda_device, dtype=torch.float32)
-    _lib.check(_lib.load().cs_debug_gram(_lib.ptr(X), N, D, _lib.ptr(W), T, _lib.ptr(H), _lib.stream_ptr()))
+    _lib.check(getattr(_lib.load(), hook)(_lib.ptr(X), N, D, _lib.ptr(W), T, _lib.ptr(H), _lib.stream_ptr()))
     torch.cuda.synchronize()
     want = torch.einsum("nd,tn,ne->tde", X, W, X)
     got = H[:, :D, :D].double()
