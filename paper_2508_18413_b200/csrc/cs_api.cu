@@ -353,7 +353,7 @@ int cs_rademacher_fill(uint64_t seed, int64_t iteration, const int64_t *ts, int6
 size_t cs_scan_workspace_bytes(int mode, int dtype, int64_t T, int32_t D) {
   const int var = mode == CS_MODE_DIAG ? SCAN_DIAG : mode == CS_MODE_BLOCK ? SCAN_BLOCK : SCAN_DENSE;
   if (var == SCAN_DENSE && D > 128) return dense_xl_ws_bytes(T, D, dtype == CS_F64 ? 8 : 4);
-  if (var == SCAN_DENSE && D > 8) return dense_wide_ws_bytes(T, D);
+  if (var == SCAN_DENSE && D > 8) return dense_wide_ws_bytes(T, D, dtype == CS_F64 ? 8 : 4);
   return scan_ws_bytes(var, dtype, T, D);
 }
 
@@ -361,7 +361,7 @@ size_t cs_scan_workspace_bytes(int mode, int dtype, int64_t T, int32_t D) {
 // cs_dense.cu up to D = 128, cs_dense_xl.cu beyond
 static int dense_wide_call(int dtype, const void *J, const void *u, const void *s0, void *out, int64_t T, int D,
                            void *ws, size_t ws_bytes, double *agg_out, void *stream) {
-  const size_t need = D > 128 ? dense_xl_ws_bytes(T, D, dtype == CS_F64 ? 8 : 4) : dense_wide_ws_bytes(T, D);
+  const size_t need = D > 128 ? dense_xl_ws_bytes(T, D, dtype == CS_F64 ? 8 : 4) : dense_wide_ws_bytes(T, D, dtype == CS_F64 ? 8 : 4);
   if (ws_bytes < need) return fail(CS_ERR_CONFIG, "scan workspace too small");
   cudaError_t e;
   if (dtype == CS_F64) {

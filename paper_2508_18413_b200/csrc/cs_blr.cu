@@ -334,11 +334,11 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
   const ST *xi = (const ST *)sys.noise_vec;
   extern __shared__ __align__(16) unsigned char bsm[];
   // TCM 2: the UMMA operand stages (1024-aligned) alias the Hessian tile
-  CT *Hs = TCM == 2 ? (CT *)(((uintptr_t)bsm + 1023) & ~(uintptr_t)1023) : (CT *)bsm;  // DP x DP
+  CT *Hs = TCM == 2 ? smem_align<CT, 1024>(bsm) : (CT *)bsm;  // DP x DP
   constexpr int HLD = DP + 1;  // Hessian tile row stride: row and column walks are both bank-conflict free
   constexpr int HS = TCM == 2 && 2 * kUmmaStages * kUmmaTile > DP * HLD ? 2 * kUmmaStages * kUmmaTile : DP * HLD;
   CT *Xs = Hs + HS;  // SIMT: 2 x SL x DP; mma.sync: 2 x kTcKB x kTcLD + 2 x kTcKB weights; tcgen05: ldx weights
-  double *vS = TCM >= 2 ? (double *)(((uintptr_t)(Xs + ldx) + 15) & ~(uintptr_t)15)
+  double *vS = TCM >= 2 ? smem_align<double, 16>(Xs + ldx)
                         : (double *)(Xs + XS + ((XS & 1) ? 1 : 0));
   double *vX = vS + DP, *vG = vX + DP, *vR = vG + DP, *vW = vR + DP, *vH = vW + DP, *vP = vH + DP;
   __shared__ double red[4][kBdThr / 32];
@@ -730,7 +730,7 @@ static_assert(128 * kPgLd <= kPgStages * 2 * kUmmaTile, "output staging fits the
 __global__ void __launch_bounds__(128) k_pair_gram(const float *__restrict__ Wt, const float *__restrict__ Qt, int nkb,
                                                   float *Hp, int64_t ldp) {
   extern __shared__ __align__(16) unsigned char psm[];
-  float *tiles = (float *)(((uintptr_t)psm + 1023) & ~(uintptr_t)1023);
+  float *tiles = smem_align<float, 1024>(psm);
   __shared__ __align__(8) uint64_t full[kPgStages], empty[kPgStages], done;
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(128) k_pair_gram(const float *__restrict__ Wt,
 __global__ void __launch_bounds__(kBdThr) k_gram_debug(const float *XT, int ldx, int N, const double *W, int64_t T,
                                                        float *Hout) {
   extern __shared__ __align__(16) unsigned char gsm[];
-  float *tiles = (float *)(((uintptr_t)gsm + 1023) & ~(uintptr_t)1023);
+  float *tiles = smem_align<float, 1024>(gsm);
   constexpr int kHs = 2 * kUmmaStages * kUmmaTile > 128 * 129 ? 2 * kUmmaStages * kUmmaTile : 128 * 129;
   float *wbuf = tiles + kHs;  // after the operand stages / the (aliased) Hessian tile
   __shared__ __align__(8) uint64_t bars[2 * kUmmaStages + 1];

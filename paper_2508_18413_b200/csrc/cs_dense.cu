@@ -260,22 +260,13 @@ k_dense_replay(const ST *__restrict__ J, const ST *__restrict__ u, const double 
 int dense_wide_chunk(int64_t T) {
   const char *e = getenv("CS_DENSE_CHUNK");
   if (e && atoi(e) > 0) return atoi(e);
-  // enough chunks to fill the machine with reduce CTAs, few enough that the
-  // serial carry stays short: ~128 steps per chunk at T = 1e5
-  int64_t c = T / 768;
-  if (c < 8) c = 8;
-  if (c > 512) c = 512;
-  return (int)c;
-}
-
-size_t dense_wide_ws_bytes(int64_t T, int D) {
-  const int c = dense_wide_chunk(T);
-  const int64_t nch = (T + c - 1) / c;
-  const int64_t ng = (nch + 15) / 16;
-  // + the tree scratch of the whole-sequence aggregate (cs_scan_aggregate):
-  // the chunk aggregates when there are few, else the group aggregates
-  const int64_t nf = nch <= 64 ? nch : ng;
-  return (size_t)(nch + ng) * ((size_t)D * D + 2 * D) * sizeof(double) + 256 + dense_tree_bytes(nf, D) + 256;
+  // enough chunks to fill the machine with replay CTAs, few enough that the
+  // serial carry stays short: the power of two nearest T / 768 (128 steps per
+  // chunk at T = 1e5), so the tree composition covers whole chunks
+  const double want = (double)T / 768.0;
+  int c = 8;
+  while (c < 512 && (double)c * 1.4142135623730951 < want) c *= 2;
+  return c;
 }
 
 static bool dense_tc() {  // CS_DENSE_TC=0 keeps the f32 composition on the FP32 pipes
@@ -321,6 +312,13 @@ CS_D void tf32_split(float x, float &hi, float &lo) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
   lo = __uint_as_float(l);
 }
+// x = hi + lo with hi = x rounded to TF32 (nearest, ties away -- cvt.rna for
+// finite x) by integer arithmetic; lo is left in f32 (the tensor core reads its
+// top 19 bits)
+CS_D void tf32_split_fast(float x, float &hi, float &lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  lo = x - hi;
+}
 // float offset of element (row, k) in a K-major SW128 operand of 128 rows whose
 // K extent is split into 32-column atoms of 128 x 32 floats
 CS_D int sw128_off(int row, int k) {
@@ -331,7 +329,7 @@ __global__ void __launch_bounds__(kDrtThr, 1)
 k_dense_reduce_tc(const float *__restrict__ J, const float *__restrict__ u, int64_t T, int D, int c, double *aggM,
                   double *aggw) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  float *Bh = (float *)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);  // 4 atoms: M_aug^T hi
+  float *Bh = smem_align<float, 1024>(dsm);  // 4 atoms: M_aug^T hi
   float *Bl = Bh + 4 * kUmmaTile;                                      // lo
   float *As = Bl + 4 * kUmmaTile;                                      // 2 stages x (hi, lo) of J_t K-blocks
   __shared__ __align__(8) uint64_t bars[2 * kUmmaStages + 1];
@@ -474,6 +472,297 @@ k_dense_reduce_tc(const float *__restrict__ J, const float *__restrict__ u, int6
   tmem_free128(pipe.tmem);
 }
 
+// ---------------------------------------------------------------------------
+// Tree-ordered composition (f32 storage, D < 128, D % 4 == 0): chunk aggregates
+// over chunks of c = 2^L steps as L levels of INDEPENDENT pair products,
+//   (M, w)_p <- (M_{2p+1} M_{2p}, M_{2p+1} w_{2p} + w_{2p+1})
+// (an odd tail is carried through as I . (M, w)), so every level is one
+// throughput-bound batched product instead of a dependent chain per chunk.
+// Persistent CTAs walk the level's products; per product, K (= D padded to
+// 128) streams in four 32-row blocks through a 3-stage ring:
+//   warps 5..11   stage A = M_{2p+1} (K-major SW128) and B = [M_{2p} | w_{2p}]
+//                 (MN-major, SWIZZLE_128B_BASE32B: rows k, the 128 columns j
+//                 contiguous -- the maps' own row-major order, so no
+//                 transposition), both split
+//                 hi + lo in TF32
+//   warp 4        issues 4 x 3 kind::tf32 MMAs per block (hi.hi + hi.lo +
+//                 lo.hi) into one of two TMEM accumulators
+//   warps 0..3    drain the other accumulator (tcgen05.ld, row per lane), add
+//                 w_{2p+1}, store the product (f32, or f64 at the last level)
+// so staging, MMAs and the epilogue of consecutive products overlap.
+constexpr int kDtThr = 384;
+constexpr int kDtStages = 3;
+constexpr int kDtStaging = kDtThr - 160;  // warps 5..11
+// MN-major tf32 operand descriptor (the only MN-major layout tf32 takes:
+// SWIZZLE_128B_BASE32B, layout type 1): rows (K) of 128 B = 32 columns, the
+// four 32-byte granules of row k stored at granule ^ (k & 3); 4-row atoms
+// `sbo` bytes apart, 32-column groups `lbo` bytes apart
+CS_D uint64_t umma_desc_sw128_mn(const void *smem_tile, uint32_t lbo, uint32_t sbo = 512) {
+  const uint64_t a = (uint64_t)smem_u32(smem_tile);
+  return ((a & 0x3FFFFull) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) | (1ull << 46) |
+         (1ull << 61);
+}
+// D f32, A/B tf32, A K-major, B MN-major (bit 16), N = 128, M = 128
+constexpr uint32_t kIdescTf32_128x128_BMN = kIdescTf32_128x128 | (1u << 16);
+
+__global__ void __launch_bounds__(kDtThr, 1)
+k_dense_tree_tc(const float *__restrict__ Min, const float *__restrict__ win, int64_t K, int D, float *Mout,
+                float *wout, double *Mout64, double *wout64) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  // stage s: A hi, A lo (128 rows x 32 k), B hi, B lo (4 column groups x 32 k-rows x 32)
+  float *stg = smem_align<float, 1024>(dsm);
+  __shared__ __align__(8) uint64_t full[kDtStages], empty[kDtStages], accf[2], acce[2];
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int64_t nprod = (K + 1) / 2;
+  const int64_t DD = (int64_t)D * D;
+  if (tid == 0) {
+    for (int s = 0; s < kDtStages; ++s) {
+      mbar_init(&full[s], kDtStaging);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 128);
+    }
+    fence_mbar_init();
+  }
+  if (wid == 0) {  // two 128-column accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  if (wid >= 5) {
+    // ---- staging: 2 x 1024 16-byte chunks per block (A: row i, k chunk; B: k-row, j chunk).
+    // Block g's in-range chunks are copied raw by cp.async straight to their
+    // swizzled places in the hi tiles, two blocks ahead; when they land, the
+    // thread that copied a chunk rewrites it as (rna hi, lo) -- no cross-thread
+    // hand-off, no register staging.  Chunks out of range (zero), the identity
+    // of an odd tail and the affine column are formed at conversion.
+    constexpr int PER = (2048 + kDtStaging - 1) / kDtStaging;
+    const int st = tid - 160;
+    float *wS = (float *)(stg + kDtStages * 4 * kUmmaTile);  // [stage][32]: w_{2p} rows of the block
+    const int64_t nloc = nprod > blockIdx.x ? (nprod - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t nblk = 4 * nloc;
+    // per slot e (chunk q = st + 224 e, fixed for the whole kernel): its place in
+    // the stage (floats past A hi), its offset in the source map at kb = 0, the
+    // row / column it covers (validity per kb), A or B
+    int dsto[PER], soff[PER], rc[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int q = st + e * kDtStaging;
+      if (q < 1024) {
+        const int r = q >> 3, c = q & 7;
+        dsto[e] = r * 32 + ((c ^ (r & 7)) << 2);
+        soff[e] = r * D + 4 * c;
+        rc[e] = (r << 8) | (4 * c);  // i, k0
+      } else {
+        const int qb = q < 2048 ? q - 1024 : 0, r = qb >> 5, j4 = qb & 31, grp = j4 >> 3, c = j4 & 7;
+        dsto[e] = 2 * kUmmaTile + grp * 1024 + r * 32 + ((((c >> 1) ^ (r & 3)) << 3) | ((c & 1) << 2));
+        soff[e] = r * D + 4 * j4;
+        rc[e] = (r << 8) | (4 * j4);  // k0, j
+      }
+    }
+    const int stepB = 32 * D;
+    auto issue = [&](int64_t g) {
+      const int s = (int)(g % kDtStages);
+      const int64_t p = blockIdx.x + (g >> 2) * gridDim.x;
+      const int kb = (int)(g & 3);
+      float *Ah = stg + s * 4 * kUmmaTile;
+      const bool tail = 2 * p + 1 >= K;
+      const float *M1 = Min + (2 * p + 1) * DD + 32 * kb, *M0 = Min + 2 * p * DD + (int64_t)stepB * kb;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        const int q = st + e * kDtStaging;
+        const int a = rc[e] >> 8, b = rc[e] & 255;
+        if (q < 1024) {
+          if (!tail && a < D && b + 32 * kb < D) cp_async16(Ah + dsto[e], M1 + soff[e]);
+        } else if (q < 2048 && a + 32 * kb < D) {
+          if (b < D) cp_async16(Ah + dsto[e], M0 + soff[e]);
+          else if (b == D)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(wS + s * 32 + a)),
+                         "l"(win + 2 * p * D + 32 * kb + a)
+                         : "memory");
+        }
+      }
+    };
+    auto convert = [&](int64_t g) {
+      const int s = (int)(g % kDtStages);
+      const int64_t p = blockIdx.x + (g >> 2) * gridDim.x;
+      const int kb = (int)(g & 3);
+      float *Ah = stg + s * 4 * kUmmaTile;
+      const bool tail = 2 * p + 1 >= K;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        const int q = st + e * kDtStaging;
+        if (q < 2048) {
+          const int a = rc[e] >> 8, b = rc[e] & 255;
+          float *dh = Ah + dsto[e], *dl = dh + kUmmaTile;  // lo tiles sit one tile past their hi tiles
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q < 1024) {
+            const int k = b + 32 * kb;
+            if (a < D && k < D) {
+              if (!tail) x = *(const float4 *)dh;
+              else x = make_float4(a == k, a == k + 1, a == k + 2, a == k + 3);
+            }
+          } else if (a + 32 * kb < D) {
+            if (b < D) x = *(const float4 *)dh;
+            else if (b == D) x.x = wS[s * 32 + a];
+          }
+          float4 h, l;
+          tf32_split_fast(x.x, h.x, l.x);
+          tf32_split_fast(x.y, h.y, l.y);
+          tf32_split_fast(x.z, h.z, l.z);
+          tf32_split_fast(x.w, h.w, l.w);
+          *(float4 *)dh = h;
+          *(float4 *)dl = l;
+        }
+      }
+    };
+    // block g: converted (and handed to the MMA) two iterations after its copies
+    // were issued, before this iteration's wait for a free stage
+    for (int64_t g = 0; g < nblk + 2; ++g) {
+      if (g >= 2) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        convert(g - 2);
+        fence_proxy_async_smem();
+        mbar_arrive(&full[(g - 2) % kDtStages]);
+      }
+      if (g < nblk) {
+        const uint32_t use = (uint32_t)(g / kDtStages);
+        if (use > 0) mbar_wait(&empty[g % kDtStages], (use - 1) & 1);
+        issue(g);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  } else if (wid == 4) {
+    // ---- MMA issue
+    if (lane == 0) {
+      uint32_t g = 0, n = 0;
+      for (int64_t p = blockIdx.x; p < nprod; p += gridDim.x, ++n) {
+        const uint32_t b = n & 1;
+        if (n >= 2) mbar_wait(&acce[b], ((n >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + 128 * b;
+        for (int kb = 0; kb < 4; ++kb, ++g) {
+          const int s = (int)(g % kDtStages);
+          mbar_wait(&full[s], (g / kDtStages) & 1);
+          tc_fence_after();
+          const float *Ah = stg + s * 4 * kUmmaTile, *Al = Ah + kUmmaTile, *Bh = Al + kUmmaTile, *Bl = Bh + kUmmaTile;
+          const uint64_t dah = umma_desc_sw128(Ah), dal = umma_desc_sw128(Al);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {  // 8 k-rows per MMA: A start + 32 B, B start + 8 rows (1 KB)
+            const uint64_t dbh = umma_desc_sw128_mn(Bh + kk * 256, 4096), dbl = umma_desc_sw128_mn(Bl + kk * 256, 4096);
+            constexpr uint32_t idesc = kIdescTf32_128x128_BMN;
+            umma_tf32(acc, dah + 2 * kk, dbh, idesc, (kb | kk) != 0);
+            umma_tf32(acc, dah + 2 * kk, dbl, idesc, 1);
+            umma_tf32(acc, dal + 2 * kk, dbh, idesc, 1);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&accf[b]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- epilogue: warp w drains TMEM lanes 32 w .. (row i = 32 w + lane)
+    const int i = 32 * wid + lane;
+    uint32_t n = 0;
+    for (int64_t p = blockIdx.x; p < nprod; p += gridDim.x, ++n) {
+      const uint32_t b = n & 1;
+      const bool tail = 2 * p + 1 >= K;
+      const float w1 = (!tail && i < D) ? __ldcs(win + (2 * p + 1) * D + i) : 0.0f;
+      mbar_wait(&accf[b], (n >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int cc = 0; cc < 128; cc += 16) {
+        float v[16];
+        tmem_ld16(tmem + 128 * b + ((uint32_t)(32 * wid) << 16) + (uint32_t)cc, v);
+        if (i >= D || cc > D) continue;
+        if (Mout64) {
+          double *row = Mout64 + p * DD + (int64_t)i * D;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int j = cc + e;
+            if (j < D) row[j] = (double)v[e];
+            else if (j == D) wout64[p * D + i] = (double)v[e] + (double)w1;
+          }
+        } else {
+          float *row = Mout + p * DD + (int64_t)i * D;
+#pragma unroll
+          for (int e = 0; e < 16; e += 4) {
+            const int j = cc + e;
+            if (j + 4 <= D) *(float4 *)(row + j) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+            else if (j == D) wout[p * D + i] = v[e] + w1;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acce[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
+static bool dense_tree() {  // CS_DENSE_TREE=0 keeps the per-chunk product chain (k_dense_reduce_tc)
+  static const bool v = [] {
+    const char *e = getenv("CS_DENSE_TREE");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
+static bool tree_ok(int D, int esize) { return esize == 4 && D % 4 == 0 && D < 128 && dense_tree(); }
+
+// f32 scratch of the tree levels: ceil(T/2) + ceil(T/4) maps (ping-pong)
+static size_t tree_scratch_floats(int64_t T, int D) {
+  return (size_t)(((T + 1) / 2) + ((T + 3) / 4)) * ((size_t)D * D + D) + 64;
+}
+
+// chunk aggregates over chunks of c = 2^L steps (c from dense_wide_chunk)
+static cudaError_t launch_tree(const float *J, const float *u, int64_t T, int D, int c, double *aggM, double *aggw,
+                               float *scratch, cudaStream_t st) {
+  int L = 0;
+  while ((1 << L) < c) ++L;
+  const size_t smem = 1024 + sizeof(float) * ((size_t)kDtStages * 4 * kUmmaTile + kDtStages * 32);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_dense_tree_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t DD = (int64_t)D * D;
+  float *bufA = scratch, *bufB = scratch + ((T + 1) / 2) * (DD + D);
+  const float *inM = J, *inw = u;
+  int64_t K = T;
+  for (int l = 1; l <= L; ++l) {
+    const int64_t np = (K + 1) / 2;
+    float *o = (l & 1) ? bufA : bufB;
+    float *oM = o, *ow = o + np * DD;
+    const bool last = l == L;
+    const unsigned grid = (unsigned)(np < sms ? np : sms);
+    k_dense_tree_tc<<<grid, kDtThr, smem, st>>>(inM, inw, K, D, last ? nullptr : oM, last ? nullptr : ow,
+                                                last ? aggM : nullptr, last ? aggw : nullptr);
+    inM = oM;
+    inw = ow;
+    K = np;
+  }
+  return cudaGetLastError();
+}
+
 // Chunk entries: one serial walk over the chunk aggregates when they are few;
 // otherwise two levels -- groups of kDwGroup chunk aggregates are composed in
 // parallel (the reduce kernel again, on f64 aggregates), one CTA walks the
@@ -511,7 +800,14 @@ cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st, doubl
   double *entries = aggw + nch * (int64_t)D;
   double *gM = entries + nch * (int64_t)D;  // group level: ng x (D*D + 2D)
   cudaError_t e;
-  if (sizeof(ST) == 4 && dense_tc() && D % 4 == 0 && D < 128) {
+  const int64_t ngt = (nch + kDwGroup - 1) / kDwGroup;
+  double *tree_end = (double *)(((uintptr_t)(gM + ngt * ((int64_t)D * D + 2 * D)) + 255) & ~(uintptr_t)255);
+  if (tree_ok(D, (int)sizeof(ST)) && (c & (c - 1)) == 0) {
+    // scratch past the aggregate-fold tree (see dense_wide_ws_bytes)
+    const int64_t nf = nch <= 64 ? nch : ngt;
+    float *scratch = (float *)(((uintptr_t)tree_end + dense_tree_bytes(nf, D) + 255) & ~(uintptr_t)255);
+    e = launch_tree((const float *)a.e0, (const float *)a.u, T, D, c, aggM, aggw, scratch, st);
+  } else if (sizeof(ST) == 4 && dense_tc() && D % 4 == 0 && D < 128) {
     const size_t smem = 1024 + sizeof(float) * (8 + 2 * kUmmaStages) * kUmmaTile;  // B hi/lo + A stages
     e = cudaFuncSetAttribute(k_dense_reduce_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -552,6 +848,18 @@ cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st, doubl
     default: e = launch_tail<ST, 128>(a, c, nch, aggM, aggw, entries, gM, st); break;
   }
   return e;
+}
+
+size_t dense_wide_ws_bytes(int64_t T, int D, int esize) {
+  const int c = dense_wide_chunk(T);
+  const int64_t nch = (T + c - 1) / c;
+  const int64_t ng = (nch + 15) / 16;
+  // + the tree scratch of the whole-sequence aggregate (cs_scan_aggregate):
+  // the chunk aggregates when there are few, else the group aggregates;
+  // + the f32 levels of the tree-ordered chunk composition
+  const int64_t nf = nch <= 64 ? nch : ng;
+  return (size_t)(nch + ng) * ((size_t)D * D + 2 * D) * sizeof(double) + 256 + dense_tree_bytes(nf, D) + 256 +
+         (tree_ok(D, esize) ? tree_scratch_floats(T, D) * sizeof(float) + 256 : 0);
 }
 
 template cudaError_t launch_dense_wide_t<float>(ScanArgs<float>, void *, cudaStream_t, double *);

@@ -38,7 +38,7 @@ size_t scan_ws_bytes(int var, int dtype, int64_t T, int D);
 template <typename ST>
 cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update = false);
 // wide dense scans, 8 < D <= 128 (cs_dense.cu)
-size_t dense_wide_ws_bytes(int64_t T, int D);
+size_t dense_wide_ws_bytes(int64_t T, int D, int esize);  // esize: storage bytes (4 adds the f32 tree levels)
 // agg_out != null: write the whole-sequence map [M (D x D) | w (D)] (f64) instead of scanning
 template <typename ST>
 cudaError_t launch_dense_wide_t(ScanArgs<ST> a, void *ws, cudaStream_t st, double *agg_out = nullptr);

@@ -68,6 +68,16 @@ CS_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta
 
 CS_D bool aligned16(const void *p) { return (((uintptr_t)p) & 15u) == 0; }
 
+// p rounded up to an A-byte boundary of the shared window.  Pointer arithmetic
+// (not an integer round trip) keeps the compiler's knowledge that the result
+// is shared memory, so accesses through it compile to LDS/STS rather than
+// generic LD/ST.
+template <typename T, unsigned A>
+CS_D T *smem_align(void *p) {
+  unsigned char *c = (unsigned char *)p;
+  return (T *)(c + ((A - (smem_u32(c) & (A - 1))) & (A - 1)));
+}
+
 // plain arrive (release at CTA scope): producer/consumer hand-offs inside a CTA
 CS_D void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");

@@ -127,10 +127,13 @@ def test_dense_scan_vs_oracle(cuda_device, D):
     np.testing.assert_allclose(got, want, atol=1e-10, rtol=1e-10)
 
 
-@pytest.mark.parametrize("D,T", [(9, 1), (9, 3001), (16, 2000), (33, 777), (100, 1), (100, 2049), (128, 1500)])
+@pytest.mark.parametrize("D,T", [(9, 1), (9, 3001), (16, 2000), (33, 777), (100, 1), (100, 2049), (128, 1500),
+                                 (64, 5001), (100, 20001)])
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 def test_wide_dense_scan_vs_oracle(cuda_device, D, T, dtype):
-    # chunked reduce / carry / replay for 8 < D <= 128 (cs_dense.cu; A12 at cfg 3's D = 100)
+    # chunked reduce / carry / replay for 8 < D <= 128 (cs_dense.cu; A12 at cfg 3's D = 100);
+    # f32 with D % 4 == 0, D < 128: chunk aggregates by the tree-ordered tcgen05
+    # composition (odd tails at several levels for T = 5001, 20001)
     rng = np.random.default_rng(7 * D + T)
     J = rng.normal(size=(T, D, D)) * (0.9 / (2.0 * np.sqrt(D)))  # spectral radius ~0.45
     u = rng.normal(size=(T, D))
