@@ -335,13 +335,16 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
   extern __shared__ __align__(16) unsigned char bsm[];
   // TCM 2: the UMMA operand stages (1024-aligned) alias the Hessian tile
   CT *Hs = TCM == 2 ? smem_align<CT, 1024>(bsm) : (CT *)bsm;  // DP x DP
-  constexpr int HLD = DP + 1;  // Hessian tile row stride: row and column walks are both bank-conflict free
+  // Hessian tile row stride: DP + 1 makes row and column walks bank-conflict
+  // free; TCM 3 takes DP + 4 so the element rows are read as 16-byte vectors
+  constexpr int HLD = TCM == 3 ? DP + 4 : DP + 1;
   constexpr int HS = TCM == 2 && 2 * kUmmaStages * kUmmaTile > DP * HLD ? 2 * kUmmaStages * kUmmaTile : DP * HLD;
   CT *Xs = Hs + HS;  // SIMT: 2 x SL x DP; mma.sync: 2 x kTcKB x kTcLD + 2 x kTcKB weights; tcgen05: ldx weights
   double *vS = TCM >= 2 ? smem_align<double, 16>(Xs + ldx)
                         : (double *)(Xs + XS + ((XS & 1) ? 1 : 0));
   double *vX = vS + DP, *vG = vX + DP, *vR = vG + DP, *vW = vR + DP, *vH = vW + DP, *vP = vH + DP;
   __shared__ double red[4][kBdThr / 32];
+  __shared__ __align__(16) CT s_vwf[128], s_pcol[128];  // w_j in the storage type, p_j (the element rows)
   // matvec partials [4][2][128]: for TCM 2 in the stage region past the Hessian tile
   __shared__ double mpart_s[TCM == 2 ? 1 : 4 * 2 * 128];
   double(*mpart)[2][128] = (double(*)[2][128])(TCM == 2 ? (double *)(Hs + ((DP * HLD + 1) & ~1)) : mpart_s);
@@ -610,6 +613,8 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
       const double wv = (vG[tid] + eps * hg) - pgS + 0.5 * (hr + (hxr + eps * hh));
       vW[tid] = wv;
       wps = wv * vP[tid];
+      s_vwf[tid] = (CT)wv;
+      s_pcol[tid] = cfg.preconditioner ? (CT)__ldg(cfg.preconditioner + tid) : CT(1);
     }
     wps = warp_sum(wps);
     if (lane == 0) red[0][wid] = wps;
@@ -633,20 +638,48 @@ k_bd_final(cs_system sys, cs_deer_config cfg, const ST *s0, const ST *guess, con
       const CT g1 = (CT)gate, g0 = (CT)(1.0 - gate), ce = (CT)(gate * eps), lam = (CT)cfg.damping;
       const CT cl = (CT)cfg.clip;
       const CT pdiag = (CT)prec;
-      for (int i = wid; i < D; i += kBdThr / 32) {
-        const CT ci = (CT)(cb * (vX[i] - vS[i]));
-        const CT pinv = cfg.preconditioner ? (CT)(1.0 / __ldg(cfg.preconditioner + i)) : CT(1);
-        const CT *hrow = Hs + i * HLD;
-        ST *jrow = Jr + (int64_t)i * D;
-        for (int j = lane; j < D; j += 32) {
-          const CT hij = -hrow[j] - (i == j ? pdiag : CT(0));
-          CT v = ce * hij + ci * (CT)vW[j] + (i == j ? g1 + g0 : CT(0));
-          if (cfg.preconditioner) v = v * ((CT)__ldg(cfg.preconditioner + j) * pinv);
-          v = v * lam;
-          if (do_clip) v = v < -cl ? -cl : (v > cl ? cl : v);
-          jok &= isfinite((double)v);
-          jrow[j] = (ST)v;
+      const bool pre = cfg.preconditioner != nullptr;
+      auto elem = [&](int i, int j, CT h, CT ci, CT pinv) {
+        const CT hij = -h - (i == j ? pdiag : CT(0));
+        CT v = ce * hij + ci * s_vwf[j] + (i == j ? g1 + g0 : CT(0));
+        if (pre) v = v * (s_pcol[j] * pinv);
+        v = v * lam;
+        if (do_clip) v = v < -cl ? -cl : (v > cl ? cl : v);
+        jok &= isfinite(v);
+        return v;
+      };
+      auto rows_scalar = [&]() {
+        for (int i = wid; i < D; i += kBdThr / 32) {
+          const CT ci = (CT)(cb * (vX[i] - vS[i]));
+          const CT pinv = pre ? (CT)(1.0 / __ldg(cfg.preconditioner + i)) : CT(1);
+          const CT *hrow = Hs + i * HLD;
+          ST *jrow = Jr + (int64_t)i * D;
+          for (int j = lane; j < D; j += 32) jrow[j] = (ST)elem(i, j, hrow[j], ci, pinv);
         }
+      };
+      if constexpr (TCM == 3) {
+        if ((D & 3) == 0) {
+          // four columns per lane: 16-byte Hessian reads and J stores
+          for (int i = wid; i < D; i += kBdThr / 32) {
+            const CT ci = (CT)(cb * (vX[i] - vS[i]));
+            const CT pinv = pre ? (CT)(1.0 / __ldg(cfg.preconditioner + i)) : CT(1);
+            const CT *hrow = Hs + i * HLD;
+            ST *jrow = Jr + (int64_t)i * D;
+            for (int j = 4 * lane; j < D; j += 128) {
+              const float4 h = *(const float4 *)(hrow + j);
+              float4 o;
+              o.x = elem(i, j, h.x, ci, pinv);
+              o.y = elem(i, j + 1, h.y, ci, pinv);
+              o.z = elem(i, j + 2, h.z, ci, pinv);
+              o.w = elem(i, j + 3, h.w, ci, pinv);
+              *(float4 *)(jrow + j) = o;
+            }
+          }
+        } else {
+          rows_scalar();
+        }
+      } else {
+        rows_scalar();
       }
     }
     if (!jok) flags[1] = 1;
@@ -890,7 +923,8 @@ static cudaError_t bd_final_launch(const cs_system &sys, const cs_deer_config &c
                                    const float *Xf, ST *J, ST *u, cs_elem_stats *stats, cudaStream_t st,
                                    int ldx = 0) {
   const size_t xs = TCM == 1 ? 2 * kTcKB * kTcLD + 2 * kTcKB : TCM >= 2 ? (size_t)ldx + 4 : 2 * 16 * DP;
-  const size_t hs = TCM == 2 && 2 * kUmmaStages * kUmmaTile > DP * (DP + 1) ? 2 * kUmmaStages * kUmmaTile : DP * (DP + 1);
+  const size_t hld = TCM == 3 ? DP + 4 : DP + 1;
+  const size_t hs = TCM == 2 && 2 * kUmmaStages * kUmmaTile > DP * hld ? 2 * kUmmaStages * kUmmaTile : DP * hld;
   const size_t smem = sizeof(ST) * (hs + xs) + 8 + 7 * DP * sizeof(double) + (TCM == 2 ? 1024 : 0);
   auto k = k_bd_final<ST, DP, TCM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
