@@ -1858,16 +1858,31 @@ static unsigned rows_grid(const ScanPlan &p, const void *k, int threads = kScanT
   return (unsigned)(p.ntiles < cap ? p.ntiles : cap);
 }
 
+// scan_rows maps chunks to CTAs statically and its look-back waits on chunks of
+// other CTAs, so the whole grid must be resident at once: launched cooperative,
+// the launch waits for (or fails without) co-residency instead of hanging when
+// another stream or process holds part of the device
+template <typename ST, int VAR, bool AGG, bool UPD, bool LBW>
+static void launch_rows_coop(const ScanPlan &p, const ScanArgs<ST> &a, LookbackWs w, int md, cudaStream_t st) {
+  auto k = scan_rows<ST, VAR, AGG, UPD, LBW>;
+  const int threads = LBW ? kScanThreads + 64 : kScanThreads;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(rows_grid(p, (const void *)k, threads));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, a, w, p.R, p.seg, p.ntiles, p.win, md);
+}
+
 template <typename ST, int VAR, bool UPD>
 static void launch_rows(const ScanPlan &p, const ScanArgs<ST> &a, LookbackWs w, cudaStream_t st) {
-  if (rows_lbw()) {
-    auto k = scan_rows<ST, VAR, false, UPD, true>;
-    k<<<rows_grid(p, (const void *)k, kScanThreads + 64), kScanThreads + 64, p.smem, st>>>(a, w, p.R, p.seg,
-                                                                                            p.ntiles, p.win, 0);
-  } else {
-    auto k = scan_rows<ST, VAR, false, UPD>;
-    k<<<rows_grid(p, (const void *)k), kScanThreads, p.smem, st>>>(a, w, p.R, p.seg, p.ntiles, p.win, p.md);
-  }
+  if (rows_lbw()) launch_rows_coop<ST, VAR, false, UPD, true>(p, a, w, 0, st);
+  else launch_rows_coop<ST, VAR, false, UPD, false>(p, a, w, p.md, st);
 }
 
 template <typename ST>
@@ -1922,12 +1937,10 @@ cudaError_t launch_aggregate_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, doub
   const unsigned grid = (unsigned)p.ntiles;
   if (p.kind == 0) {
     if (p.var == SCAN_DIAG) {
-      const void *kf = (const void *)scan_rows<ST, SCAN_DIAG, true>;
-      scan_rows<ST, SCAN_DIAG, true><<<rows_grid(p, kf), kScanThreads, p.smem, st>>>(a, w, p.R, p.seg, p.ntiles, p.win, p.md);
+      launch_rows_coop<ST, SCAN_DIAG, true, false, false>(p, a, w, p.md, st);
       k_agg_compose_cols<SCAN_DIAG><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
     } else {
-      const void *kf = (const void *)scan_rows<ST, SCAN_BLOCK, true>;
-      scan_rows<ST, SCAN_BLOCK, true><<<rows_grid(p, kf), kScanThreads, p.smem, st>>>(a, w, p.R, p.seg, p.ntiles, p.win, p.md);
+      launch_rows_coop<ST, SCAN_BLOCK, true, false, false>(p, a, w, p.md, st);
       k_agg_compose_cols<SCAN_BLOCK><<<1, kScanThreads, 0, st>>>(w.agg, p.ntiles, a.D, 0, out);
     }
   } else if (p.kind == 1) {
