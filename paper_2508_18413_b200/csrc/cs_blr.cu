@@ -32,6 +32,7 @@ constexpr int kBlrCols = kBlrMaxD / 32;
 
 struct BlrCtx {
   std::mutex mu;
+  ScratchFence fence;
   double *buf = nullptr;
   size_t cap = 0;
 };
@@ -872,6 +873,7 @@ static cudaError_t blr_run(const cs_system &sys, const cs_deer_config &cfg, int6
   cudaGetDevice(&dev);
   BlrCtx &ctx = g_blr[dev & 15];
   std::lock_guard<std::mutex> lock(ctx.mu);
+  ScratchScope scope(ctx.fence, st);
   // A, A2, G (M x D), E (M x N), gS (T x D), row sums 2 x (2T)
   const size_t need = (size_t)3 * M * D + (size_t)M * N + (size_t)T * D + (size_t)4 * T;
   if (ctx.cap < need) {
@@ -944,6 +946,7 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   cudaGetDevice(&dev);
   BlrCtx &ctx = g_blr[dev & 15];
   std::lock_guard<std::mutex> lock(ctx.mu);
+  ScratchScope scope(ctx.fence, st);
   // A, A2, G, gS, GX, R, HR (T x D); E, WS, WX (T x N); row sums 2 x (2T)
   // + Xf: X as f32 (N x 128, or its transpose 128 x ldx for tcgen05)
   // pair-Gram path: W tiles (Tpad x 32 nkb), Q tiles (ldp x 32 nkb), Hp (Tpad x ldp), f32

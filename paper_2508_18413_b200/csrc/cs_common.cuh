@@ -15,6 +15,31 @@ namespace cs {
 
 constexpr int64_t kNoStep = INT64_MAX;   // "no offending step" sentinel for atomicMin
 
+// Stream-ordered hand-off of a scratch buffer shared by all streams of a
+// device (the host mutex only orders the enqueueing): a user's stream first
+// waits for the previous user's queued work on the buffer, and on scope exit
+// records its own, so a call on another stream cannot overwrite it mid-flight.
+struct ScratchFence {
+  cudaEvent_t ev = nullptr;
+  void acquire(cudaStream_t st) {
+    if (ev) cudaStreamWaitEvent(st, ev, 0);
+  }
+  void release(cudaStream_t st) {
+    if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+      ev = nullptr;
+      cudaDeviceSynchronize();  // no event: fall back to draining the device
+      return;
+    }
+    cudaEventRecord(ev, st);
+  }
+};
+struct ScratchScope {  // acquire now, release when the enqueueing function returns
+  ScratchFence &f;
+  cudaStream_t st;
+  ScratchScope(ScratchFence &fence, cudaStream_t s) : f(fence), st(s) { f.acquire(st); }
+  ~ScratchScope() { f.release(st); }
+};
+
 // ---- storage <-> f64 ------------------------------------------------------
 template <typename ST> CS_D double ld(const ST *p, int64_t i) { return (double)__ldg(p + i); }
 template <typename ST> CS_D void st(ST *p, int64_t i, double v) { p[i] = (ST)v; }

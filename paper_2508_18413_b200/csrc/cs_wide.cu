@@ -23,6 +23,7 @@ namespace {
 
 struct WideCtx {
   std::mutex mu;
+  ScratchFence fence;
   double *buf = nullptr;  // A (M x n) then C (M x n), f64
   size_t cap = 0;         // doubles
 };
@@ -352,9 +353,11 @@ static cudaError_t wide_batch_chunk(const cs_system &sys, const cs_deer_config &
   static std::mutex mu;
   static char *bufs[16];
   static size_t caps[16];
+  static ScratchFence fences[16];
   int dv = 0;
   cudaGetDevice(&dv);
   std::lock_guard<std::mutex> lock(mu);
+  ScratchScope scope(fences[dv & 15], st);
   cudaError_t e = cudaSuccess;
   if (caps[dv & 15] < need) {
     if (bufs[dv & 15]) cudaFree(bufs[dv & 15]);
@@ -421,6 +424,7 @@ static cudaError_t wide_run(const cs_system &sys, const cs_deer_config &cfg, int
   cudaGetDevice(&dev);
   WideCtx &ctx = g_wide[dev & 15];
   std::lock_guard<std::mutex> lock(ctx.mu);
+  ScratchScope scope(ctx.fence, st);
   const size_t need = (size_t)2 * M * n;
   if (ctx.cap < need) {
     if (ctx.buf) cudaFree(ctx.buf);  // cudaFree synchronises: growth happens once per shape

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -401,17 +402,22 @@ def _run_fused(system, s0, cfg, max_iters):
                       full_trace=None, stats=stats)
 
 
-_PINNED_HIST: dict = {}
+_PINNED = threading.local()  # per-thread pinned read-back buffers (threads solve concurrently)
+
+
+def _pinned(kind, n, dtype):
+    d = _PINNED.__dict__.setdefault(kind, {})
+    buf = d.get(n)
+    if buf is None:
+        buf = torch.empty(n, dtype=dtype).pin_memory()
+        d[n] = buf
+    return buf
 
 
 def _pinned_hist(n):
     # reused across solves on this thread's stream: cs_deer_solve synchronises
     # before returning, and the result copies out of it
-    buf = _PINNED_HIST.get(n)
-    if buf is None:
-        buf = torch.empty(n, dtype=torch.float64).pin_memory()
-        _PINNED_HIST[n] = buf
-    return buf
+    return _pinned("hist", n, torch.float64)
 
 
 def run_deer(system: TransitionSystem, s0, cfg: DeerConfig) -> DeerResult:
@@ -443,16 +449,10 @@ class _NotInstantiated(Exception):
 _STATS_BYTES = 40
 
 
-_PINNED_STATS: dict = {}
-
-
 def _parse_stats(buf):
-    # one 40-byte read-back per iteration into a reused pinned buffer (no
-    # pageable allocation, one stream sync)
-    host = _PINNED_STATS.get(buf.numel())
-    if host is None:
-        host = torch.empty(buf.numel(), dtype=torch.uint8).pin_memory()
-        _PINNED_STATS[buf.numel()] = host
+    # one 40-byte read-back per iteration into a reused (per-thread) pinned
+    # buffer: no pageable allocation, one stream sync
+    host = _pinned("stats", buf.numel(), torch.uint8)
     host.copy_(buf, non_blocking=True)
     torch.cuda.current_stream(buf.device).synchronize()
     raw = host.numpy().tobytes()

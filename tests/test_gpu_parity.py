@@ -462,6 +462,43 @@ def test_run_deer_blr_dense_wide(cuda_device, dtype):
     _deer_cmp(h, g, "dense_", dtype)
 
 
+@pytest.mark.parametrize("mode", ["dense", "diag-stochastic"])
+def test_blr_concurrent_streams_match_serial(cuda_device, mode):
+    # the logistic-regression builders share per-device scratch: solves from two
+    # threads on two streams must see it handed off in stream order (no
+    # overwrite mid-flight) and reproduce the serial traces bit for bit
+    import threading
+
+    g0 = golden("mala_blr100")
+    m = cs.model_logp_grad_hvp(cs.blr(g0["X"], g0["y"], 1.0))
+
+    def solve(seed):
+        k = cs.MalaKernel(m, 0.003, seed=seed, T=400, dtype=torch.float32)
+        return cs.run_deer(k, np.zeros(100), cs.DeerConfig(mode=mode, max_iters=30))
+
+    want = {sd: solve(sd).trace.cpu() for sd in (4, 5)}
+    out, errs = {}, []
+
+    def worker(sd):
+        try:
+            s = torch.cuda.Stream(device=cuda_device)
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    r = solve(sd)
+                    out.setdefault(sd, []).append(r.trace.cpu())
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    ths = [threading.Thread(target=worker, args=(sd,)) for sd in (4, 5)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    for sd in (4, 5):
+        assert all(torch.equal(x, want[sd]) for x in out[sd])
+
+
 @pytest.mark.parametrize("kw", [dict(damping=0.7), dict(preconditioner="ramp"), dict(clip=0.5),
                                 dict(damping=0.8, preconditioner="ramp", clip=2.0)])
 def test_blr_dense_builder_options_match_host_engine(cuda_device, kw):
