@@ -67,6 +67,11 @@ pynvml.nvmlInit()
 h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
 period = float(sys.argv[2])
 mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+# the first queries of a process are slow (and hold the driver's lock): make
+# them here, before the parent starts its timed region
+for _ in range(3):
+    pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+    pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
 sys.stdout.write("ready\n"); sys.stdout.flush()
 import select
 samples, bits = [], 0
@@ -236,17 +241,35 @@ def run_gpu(args):
         # the host path would land in one step); objects are freed at the end
         gc.collect()
         gc.disable()
+        # untimed pre-roll, results held at once: the timed loop keeps one step's
+        # result alive while the next allocates, and the allocator must already
+        # own blocks for both (otherwise step 2 pays a cudaMalloc: 2-100 ms)
+        keep = []
+        for _ in range(3):
+            flush.fill_(1.0)
+            keep.append(fn())
+        torch.cuda.synchronize()
+        del keep
         evs = []
+        host = []
         for _ in range(args.steps):
+            h0 = time.perf_counter()
             flush.fill_(1.0)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
+            h1 = time.perf_counter()
             a.record()
             out = fn()
             b.record()
+            h2 = time.perf_counter()
             evs.append((a, b))
+            host.append((round((h1 - h0) * 1e3, 3), round((h2 - h1) * 1e3, 3)))
         torch.cuda.synchronize()
         gc.enable()
+        if os.environ.get("CS_BENCH_STEPS"):
+            print("steps", [round(a.elapsed_time(b), 3) for a, b in evs], file=sys.stderr)
+            print("host", host[:4], file=sys.stderr)
+            print("kernel", [round(x, 3) for x in kernel_ms[-args.steps:]][:4], file=sys.stderr)
         return sum(a.elapsed_time(b) for a, b in evs), out
 
     if world > 1:

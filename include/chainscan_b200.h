@@ -143,6 +143,8 @@ int cs_debug_gram(const double *X, int32_t N, int32_t D, const double *W, int64_
 int cs_debug_pair_gram(const double *X, int32_t N, int32_t D, const double *W, int64_t T, float *H_out,
                        void *stream);
 int cs_device_sm_count(int *out);
+/* Wait for the work queued on `stream` (the host-engine read-backs). */
+int cs_stream_sync(void *stream);
 
 /* ---- counter-based noise (noise.py:50-80, 140-156, 159-171) ------------- */
 /* out[(i*count + k)] = value k of the slot at step t0+i; f64 always except

@@ -313,6 +313,11 @@ int cs_debug_probe(unsigned long long *dev_buf, int n) {
 }
 int cs_version(void) { return 1; }
 
+int cs_stream_sync(void *stream) {
+  const cudaError_t e = cudaStreamSynchronize(S(stream));
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_stream_sync");
+}
+
 int cs_device_sm_count(int *out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);

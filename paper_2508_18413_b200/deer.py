@@ -454,7 +454,7 @@ def _parse_stats(buf):
     # buffer: no pageable allocation, one stream sync
     host = _pinned("stats", buf.numel(), torch.uint8)
     host.copy_(buf, non_blocking=True)
-    torch.cuda.current_stream(buf.device).synchronize()
+    _lib.sync_current()
     raw = host.numpy().tobytes()
     bad_prop, bad_step, bad_jac = np.frombuffer(raw[:24], dtype=np.int64)
     picard, fail_rows = np.frombuffer(raw[24:32], dtype=np.uint32)
@@ -660,7 +660,7 @@ def _run_streamed_window(system, s0, cfg, max_iters):
             _lib.check(rc)
             _lib.check(lib.cs_first_stamped_row(_lib.ptr(lf), n, it + 1, first_ptr, st))
         host.copy_(buf, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
+        _lib.sync_current()
         raw = host.numpy().tobytes()
         bad_prop, bad_step, bad_jac = np.frombuffer(raw[:24], dtype=np.int64)
         picard, nfail = np.frombuffer(raw[24:32], dtype=np.uint32)

@@ -454,7 +454,7 @@ def _run_streamed_shard(system, s0, cfg, group, world, rank, max_iters) -> Shard
             both[2 * world:].view(world, 4).copy_(gA_dev)
             if both_h is not None:  # one pinned read for both gathered vectors
                 both_h.copy_(both, non_blocking=True)
-                torch.cuda.current_stream(dev).synchronize()
+                _lib.sync_current()
                 bh = both_h.numpy()
             else:
                 bh = both.cpu().numpy()
