@@ -393,19 +393,25 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
   const ScanPlan p = scan_plan(var, dtype, T, D);
   if (ws_bytes < p.ws_bytes) return fail(CS_ERR_CONFIG, "scan workspace too small");
   if (T == 0) return CS_OK;
+  // plain diag scans take the single-pass kernel when the workspace covers its
+  // tile records and the element / output arrays are 16-byte aligned (bulk copies)
+  const bool a16 = ((((uintptr_t)e0) | ((uintptr_t)u) | ((uintptr_t)out)) & 15) == 0;
+  const bool one_pass = a16 && scan_1p_eligible(var, T, D) && ws_bytes >= scan_plan_1p(var, dtype, T, D).ws_bytes;
   cudaError_t e;
   if (dtype == CS_F64) {
     ScanArgs<double> a{(const double *)e0, (const double *)e1, (const double *)e2, (const double *)e3,
                        (const double *)u, (const double *)s0, (double *)out, T, D};
     a.probe = h_probe;
     a.probe_n = h_probe_n;
-    e = launch_scan_t<double>(p, a, ws, S(stream));
+    e = one_pass ? launch_scan_1p_t<double>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
+                 : launch_scan_t<double>(p, a, ws, S(stream));
   } else {
     ScanArgs<float> a{(const float *)e0, (const float *)e1, (const float *)e2, (const float *)e3,
                       (const float *)u, (const float *)s0, (float *)out, T, D};
     a.probe = h_probe;
     a.probe_n = h_probe_n;
-    e = launch_scan_t<float>(p, a, ws, S(stream));
+    e = one_pass ? launch_scan_1p_t<float>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
+                 : launch_scan_t<float>(p, a, ws, S(stream));
   }
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "scan launch");
 }

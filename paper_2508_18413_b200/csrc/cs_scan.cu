@@ -1678,6 +1678,165 @@ __global__ void k_agg_compose_dense(const double *agg, int64_t ntiles, int D, do
 
 // ---------------------------------------------------------------------------
 // host launchers
+// ---------------------------------------------------------------------------
+// Single-pass row scan (plain diag, D <= 64).  Persistent CTAs claim tiles of
+// R rows in order through the ticket (every predecessor of a claimed tile has
+// been claimed, and its aggregate is published before its claimer waits on
+// anything: forward progress without co-residency).  A tile's j and u arrive
+// in shared memory by two 1-D bulk copies (TMA engine); each thread reduces its
+// column segment (storage precision) and the tile aggregate (f64, fixed fold)
+// is published and counted into its group.  The tile's look-back (two-level,
+// the same fixed chain of single applications as scan_rows: bit-identical run
+// to run), replay in place and bulk store run one claim later, while the next
+// tile's copies are in flight -- the look-back is a round behind its
+// predecessors instead of racing them.  HBM traffic is the algorithmic 12 B per
+// f32 element: j and u read once, s written once.
+constexpr int kRows1pMinB = 2;
+
+template <typename ST>
+__global__ void __launch_bounds__(kScanThreads, kRows1pMinB)
+scan_rows_1p(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles) {
+  using CT = ST;
+  constexpr int W = 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double s_acc[64 * W];
+  __shared__ double s_acc2[64 * W];
+  __shared__ double s_entry[2 * 64];
+  __shared__ double s_gentry[2 * 64];
+  __shared__ int s_ctl[1];
+  __shared__ int s_gflag;
+  __shared__ unsigned s_tile;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  const int D = a.D, tid = threadIdx.x;
+  const size_t tile_elems = (size_t)R * D;
+  ST *buf = (ST *)smem_raw;  // [2][j | u] tiles
+  const int nseg = kScanThreads / D, c = tid % D, sg = tid / D;
+  const bool active = sg < nseg;
+  CT *sa_base = (CT *)(buf + 4 * tile_elems);  // [2][nseg][D][2] segment aggregates
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  unsigned use[2] = {0u, 0u};  // mbarrier phases per buffer
+  auto claim = [&]() -> int64_t {
+    if (tid == 0) s_tile = atomicAdd(ws.ticket, 1u);
+    __syncthreads();
+    const int64_t t = s_tile;
+    __syncthreads();  // s_tile is rewritten by the next claim
+    return t;
+  };
+  auto rows_of = [&](int64_t t) { return (int)(a.T - t * R < R ? a.T - t * R : R); };
+  auto bulk_of = [&](int64_t t) { return (unsigned)(((size_t)rows_of(t) * D * sizeof(ST)) & ~(size_t)15); };
+  // issue tile t's copies into buffer k (thread 0) and the ragged tail (all)
+  auto load = [&](int64_t t, int k) {
+    ST *jt = buf + (size_t)k * 2 * tile_elems, *ut = jt + tile_elems;
+    const int64_t row0 = t * R;
+    const unsigned bulk = bulk_of(t);
+    if (tid == 0) {
+      bulk_wait_read();  // the previous store out of this buffer has read it
+      if (bulk) {
+        mbar_expect_tx(&s_bar[k], 2 * bulk);
+        bulk_g2s(jt, a.e0 + row0 * D, bulk, &s_bar[k]);
+        bulk_g2s(ut, a.u + row0 * D, bulk, &s_bar[k]);
+      }
+    }
+    const int n = rows_of(t) * D, nb = (int)(bulk / sizeof(ST));
+    for (int i = nb + tid; i < n; i += kScanThreads) {
+      jt[i] = a.e0[row0 * D + i];
+      ut[i] = a.u[row0 * D + i];
+    }
+  };
+  // wait for buffer k, reduce its segments, publish the tile aggregate
+  auto reduce_publish = [&](int64_t t, int k) {
+    ST *jt = buf + (size_t)k * 2 * tile_elems, *ut = jt + tile_elems;
+    CT *sa = sa_base + (size_t)k * nseg * D * W;
+    if (bulk_of(t)) mbar_wait(&s_bar[k], use[k]++ & 1);
+    __syncthreads();
+    const int rows = rows_of(t), rs = (rows + nseg - 1) / nseg, r0 = sg * rs, r1 = min(rows, r0 + rs);
+    if (active) {
+      SegE<SCAN_DIAG, CT> run;
+      run.ident();
+      for (int r = r0; r < r1; ++r) {
+        SegE<SCAN_DIAG, CT> e;
+        e.j = jt[r * D + c];
+        e.u = ut[r * D + c];
+        run.push(e);
+      }
+      run.store(sa + (sg * D + c) * W);
+    }
+    __syncthreads();
+    if (tid < D) {
+      ColElem<SCAN_DIAG> ch;
+      ch.ident();
+      for (int q = 0; q < nseg; ++q) {
+        SegE<SCAN_DIAG, CT> x;
+        x.load(sa + (q * D + tid) * W);
+        ch.push(x.wide());
+      }
+      ch.store(ws.agg + (t * D + tid) * W);
+      __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) st_release(ws.status + t, 1);
+    group_aggregate_publish<SCAN_DIAG, CtaGrp>(t, D, ws, &s_gflag);
+  };
+  // look back for tile t's entry, replay buffer k in place, store it
+  auto finish = [&](int64_t t, int k) {
+    ST *jt = buf + (size_t)k * 2 * tile_elems, *ut = jt + tile_elems;
+    CT *sa = sa_base + (size_t)k * nseg * D * W;
+    lookback_grouped<SCAN_DIAG, CtaGrp, 4>(
+        t, D, ws, [&](int cc) { return (double)a.s0[cc]; }, [&](int) { return 0.0; }, s_acc, s_acc2, s_entry,
+        s_gentry, s_ctl, [&](int) {});
+    const int rows = rows_of(t), rs = (rows + nseg - 1) / nseg, r0 = sg * rs, r1 = min(rows, r0 + rs);
+    if (active) {
+      SegE<SCAN_DIAG, CT> pre;
+      pre.ident();
+      for (int q = 0; q < sg; ++q) {
+        SegE<SCAN_DIAG, CT> x;
+        x.load(sa + (q * D + c) * W);
+        pre.push(x);
+      }
+      double xe = s_entry[c];
+      pre.apply(xe);
+      CT x = (CT)xe;
+      for (int r = r0; r < r1; ++r) {
+        x = jt[r * D + c] * x + ut[r * D + c];
+        ut[r * D + c] = (ST)x;
+      }
+    }
+    fence_proxy_async_smem();  // every thread's writes -> visible to the bulk store
+    __syncthreads();
+    const int64_t row0 = t * R;
+    const unsigned bulk = bulk_of(t);
+    if (tid == 0 && bulk) {
+      bulk_s2g(a.out + row0 * D, ut, bulk);
+      bulk_commit();
+    }
+    const int n = rows * D, nb = (int)(bulk / sizeof(ST));
+    for (int i = nb + tid; i < n; i += kScanThreads) a.out[row0 * D + i] = ut[i];
+  };
+  int64_t cur = claim();
+  if (cur >= ntiles) return;
+  int kc = 0;
+  load(cur, kc);
+  reduce_publish(cur, kc);
+  for (;;) {
+    const int64_t nxt = claim();
+    if (nxt < ntiles) {
+      // the next tile's aggregate goes out before this tile's look-back, so
+      // aggregates never wait on look-backs; the look-back then runs a tile behind
+      load(nxt, kc ^ 1);
+      reduce_publish(nxt, kc ^ 1);
+    }
+    finish(cur, kc);
+    if (nxt >= ntiles) break;
+    cur = nxt;
+    kc ^= 1;
+  }
+  if (tid == 0) bulk_wait_read();
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static int env_int(const char *name, int lo, int hi, int dflt) {
@@ -1740,10 +1899,71 @@ static int rows_per_tile(int var, int dtype, int D) {
   return R;
 }
 
+// CS_SCAN_1P=1 selects the single-pass kernel for plain diag scans.  Off by
+// default: at T = 2^24, D = 18 it measured 1.50 ms (36.8 % of HBM) against the
+// two-pass scan's 1.21 ms -- with j, u moved once (0.83 ms without the
+// look-back, 67 %), each tile's look-back (~5 L2 round trips) is exposed per
+// CTA; see DESIGN.md section 8.
+static bool scan_1p() {
+  static const bool v = [] {
+    const char *e = getenv("CS_SCAN_1P");
+    return e ? atoi(e) != 0 : false;
+  }();
+  return v;
+}
+
+bool scan_1p_eligible(int var, int64_t T, int D) { return scan_1p() && var == SCAN_DIAG && D >= 1 && D <= 64 && T > 0; }
+
+// tiles of ~kB KB of j + u, R a multiple of 4 so every full tile is whole 16-byte lines
+ScanPlan scan_plan_1p(int var, int dtype, int64_t T, int D) {
+  ScanPlan p{};
+  p.var = var;
+  p.kind = 3;
+  const int esz = dtype == CS_F64 ? 8 : 4;
+  static const int kb = env_int("CS_SCAN_1P_KB", 8, 100, 48);
+  int R = (kb * 1024) / (2 * esz * D);
+  R = R / 4 * 4;
+  if (R < 4) R = 4;
+  p.R = R;
+  p.ntiles = (T + R - 1) / R;
+  p.agg_w = 2 * D;
+  p.state_w = D;
+  const int nseg = kScanThreads / D;
+  p.smem = (size_t)4 * R * D * esz + (size_t)2 * nseg * D * 2 * esz;  // two tiles in flight
+  const int64_t ngroups = (p.ntiles + kGroupTiles - 1) / kGroupTiles;
+  p.ws_bytes = align_up(sizeof(unsigned)) + align_up(sizeof(int) * (p.ntiles + 2 * ngroups)) +
+               align_up(sizeof(double) * (p.ntiles + ngroups) * p.agg_w) + align_up(sizeof(double) * p.ntiles * p.state_w);
+  return p;
+}
+
 size_t scan_ws_bytes(int var, int dtype, int64_t T, int D) {
-  const size_t a = scan_plan(var, dtype, T, D, false).ws_bytes, b = scan_plan(var, dtype, T, D, true).ws_bytes;
+  size_t a = scan_plan(var, dtype, T, D, false).ws_bytes, b = scan_plan(var, dtype, T, D, true).ws_bytes;
+  if (scan_1p_eligible(var, T, D)) {
+    const size_t c = scan_plan_1p(var, dtype, T, D).ws_bytes;
+    a = a > c ? a : c;
+  }
   return a > b ? a : b;
 }
+
+template <typename ST>
+cudaError_t launch_scan_1p_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st) {
+  LookbackWs w = carve_ws(p, ws, a.D);
+  cudaError_t e = cudaMemsetAsync(ws, 0, (unsigned char *)w.agg - (unsigned char *)ws, st);
+  if (e != cudaSuccess) return e;
+  if (p.ntiles == 0) return cudaSuccess;
+  e = cudaFuncSetAttribute(scan_rows_1p<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_rows_1p<ST>, kScanThreads, p.smem);
+  if (occ < 1) occ = 1;
+  const int64_t g = (int64_t)occ * sms;
+  scan_rows_1p<ST><<<(unsigned)(p.ntiles < g ? p.ntiles : g), kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles);
+  return cudaGetLastError();
+}
+template cudaError_t launch_scan_1p_t<float>(const ScanPlan &, ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_scan_1p_t<double>(const ScanPlan &, ScanArgs<double>, void *, cudaStream_t);
 
 ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update) {
   ScanPlan p{};
@@ -1820,7 +2040,7 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update) {
     p.agg_w = 32 * (var == SCAN_DIAG ? 2 : 6);
     p.state_w = var == SCAN_DIAG ? D : 2 * D;
   }
-  const int64_t ngroups = p.kind == 0 ? (p.ntiles + kGroupTiles - 1) / kGroupTiles : 0;
+  const int64_t ngroups = (p.kind == 0 || p.kind == 3) ? (p.ntiles + kGroupTiles - 1) / kGroupTiles : 0;
   p.ws_bytes = align_up(sizeof(unsigned)) + align_up(sizeof(int) * (p.ntiles + 2 * ngroups)) +
                align_up(sizeof(double) * (p.ntiles + ngroups) * p.agg_w) +
                align_up(sizeof(double) * (p.kind == 1 ? (p.ntiles / ((D + 31) / 32) + 1) : p.ntiles) * p.state_w);
@@ -1832,7 +2052,7 @@ LookbackWs carve_ws(const ScanPlan &p, void *ws, int D) {
   LookbackWs w;
   w.ticket = (unsigned *)b;
   b += align_up(sizeof(unsigned));
-  const int64_t ngroups = p.kind == 0 ? (p.ntiles + kGroupTiles - 1) / kGroupTiles : 0;
+  const int64_t ngroups = (p.kind == 0 || p.kind == 3) ? (p.ntiles + kGroupTiles - 1) / kGroupTiles : 0;
   w.status = (int *)b;
   w.gstatus = w.status + p.ntiles;
   w.gcount = w.gstatus + ngroups;

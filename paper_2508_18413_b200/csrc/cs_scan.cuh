@@ -35,6 +35,11 @@ struct ScanPlan {
 ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update = false);
 // workspace for either the plain or the bookkeeping (update) scan of a shape
 size_t scan_ws_bytes(int var, int dtype, int64_t T, int D);
+// single-pass row scan for plain diag scans (scan_rows_1p): eligibility, plan, launch
+bool scan_1p_eligible(int var, int64_t T, int D);
+ScanPlan scan_plan_1p(int var, int dtype, int64_t T, int D);
+template <typename ST>
+cudaError_t launch_scan_1p_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st);
 template <typename ST>
 cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update = false);
 // wide dense scans, 8 < D <= 128 (cs_dense.cu)
