@@ -4,6 +4,7 @@
 // call launches hand-written sm_100a kernels on the caller's stream.
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -283,6 +284,7 @@ struct SolveState {
   int *ready;
   SolveOut *out;  // host-mapped (UVA: the same pointer on the device)
   cudaEvent_t ev0, ev1;
+  unsigned seq;   // solves launched on this state
 };
 
 }  // namespace cs
@@ -894,6 +896,7 @@ int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, co
       n.host = me;
       cudaError_t e = cudaMalloc(&n.ctl, sizeof(SolveCtl) + sizeof(int) * kReadyStride * 8 * (size_t)sms);
       if (e == cudaSuccess) e = cudaHostAlloc(&n.out, sizeof(SolveOut), cudaHostAllocMapped);
+      if (e == cudaSuccess) memset((void *)n.out, 0, sizeof(SolveOut));  // seq 0: no solve signalled yet
       if (e == cudaSuccess) e = cudaEventCreate(&n.ev0);
       if (e == cudaSuccess) e = cudaEventCreate(&n.ev1);
       if (e != cudaSuccess) return cuda_fail(e, "solver state");
@@ -917,13 +920,14 @@ int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, co
   double *agg = (double *)w;
   SolvePick pick{};
   cudaError_t e;
-  cudaEventRecord(ss->ev0, st);
+  const unsigned seq = ++ss->seq;
   if (dtype == CS_F64) {
     SolveArgs<double> A{};
     A.sys = *sys; A.mode = cfg->mode; A.max_iters = cfg->max_iters; A.nsamp = cfg->hutchinson_samples;
     A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
     A.pre = cfg->preconditioner; A.s0 = (const double *)s0; A.G0 = (double *)trace; A.G1 = (double *)G1;
     A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ss->ctl; A.out = ss->out; A.agg = agg;
+    A.seq = seq;
     A.ready = ss->ready; A.probe = h_probe; A.probe_n = h_probe_n; A.T = T; A.D = D;
     e = solve_dispatch(*sys, dtype, md, cfg->mode, &A, sms, st, &pick);
   } else {
@@ -932,19 +936,30 @@ int cs_deer_solve(const cs_system *sys, const cs_deer_config *cfg, int dtype, co
     A.atol = cfg->atol; A.rtol = cfg->rtol; A.damping = cfg->damping; A.clip = cfg->clip;
     A.pre = cfg->preconditioner; A.s0 = (const float *)s0; A.G0 = (float *)trace; A.G1 = (float *)G1;
     A.last_fail = per_step_converged_at; A.hist = delta_history; A.ctl = ss->ctl; A.out = ss->out; A.agg = agg;
+    A.seq = seq;
     A.ready = ss->ready; A.probe = h_probe; A.probe_n = h_probe_n; A.T = T; A.D = D;
     e = solve_dispatch(*sys, dtype, md, cfg->mode, &A, sms, st, &pick);
   }
   if (e == cudaErrorNotSupported) return fail(CS_ERR_CONFIG, "fused solver not instantiated for this system");
   if (e != cudaSuccess) return cuda_fail(e, "cooperative solve launch");
   cudaEventRecord(ss->ev1, st);
-  // the kernel writes its outcome straight into host-mapped memory: one sync
-  e = cudaEventSynchronize(ss->ev1);
-  if (e != cudaSuccess) return cuda_fail(e, "solve");
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, ss->ev0, ss->ev1);
+  // the kernel writes its outcome straight into host-mapped memory and signals
+  // it with the sequence number: spin on that word (it lands before the grid's
+  // last CTAs retire; everything after is stream-ordered), polling the event
+  // now and then so a failed launch cannot hang the host
+  const volatile unsigned *sig = (const volatile unsigned *)&ss->out->seq;
+  for (unsigned n = 1; *sig != seq; ++n) {
+    if ((n & 1023u) == 0u) {
+      e = cudaEventQuery(ss->ev1);
+      if (e == cudaErrorNotReady) continue;
+      if (e != cudaSuccess) return cuda_fail(e, "solve");
+      if (*sig != seq) return fail(CS_ERR_CUDA, "solve finished without its outcome record");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   SolveOut h;
   memcpy(&h, (const void *)ss->out, sizeof h);
+  const float ms = (float)((double)(h.t_end - h.t_start) * 1e-6);
   res->iterations = h.iterations;
   res->status = h.status;
   res->err_kind = h.err_kind;

@@ -65,6 +65,8 @@ struct SolveOut {
   int err_iter;
   long long err_step;
   double guard_dmax, guard_d0;
+  unsigned long long t_start, t_end;  // %globaltimer (ns) at CTA 0's entry and at the outcome write
+  unsigned seq;                       // written last: the host's completion signal for solve `seq`
 };
 
 template <typename ST>
@@ -79,6 +81,7 @@ struct SolveArgs {
   double *hist;
   SolveCtl *ctl;
   SolveOut *out;  // host-mapped
+  unsigned seq;   // this solve's sequence number (SolveOut::seq on completion)
   double *agg;  // [2][nblocks][W]
   int *ready;   // [nblocks] iterate stamp: rows of guess_it written by CTA b
   unsigned long long *probe;  // cs_debug_probe buffer or null
@@ -356,6 +359,11 @@ deer_persistent(SolveArgs<ST> A) {
   const Sys sys = SysFactory<Sys>::make(A.sys);
   const int b = blockIdx.x;
   const int D = A.D;
+  if (b == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.out->t_start = t;
+  }
   // balanced contiguous ranges: CTA b owns rows [lo_b, hi_b), thread i the
   // segment starting at lo_b + i * seg (every SM gets the same share of steps)
   const int64_t lo_b = (int64_t)b * A.T / A.nblocks, hi_b = (int64_t)(b + 1) * A.T / A.nblocks;
@@ -700,6 +708,11 @@ deer_persistent(SolveArgs<ST> A) {
     o->final_buf = it == 0 ? -1 : cur;
     o->guard_dmax = g_dmax;
     o->guard_d0 = d0;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    o->t_end = t;
+    __threadfence_system();  // the record and the delta history before the signal
+    *(volatile unsigned *)&o->seq = A.seq;
   }
   // leave the control block zeroed for the next solve on this stream: the last
   // CTA out (every other CTA is past its last read of it) resets it
