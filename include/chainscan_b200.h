@@ -143,6 +143,13 @@ int cs_debug_gram(const double *X, int32_t N, int32_t D, const double *W, int64_
 int cs_debug_pair_gram(const double *X, int32_t N, int32_t D, const double *W, int64_t T, float *H_out,
                        void *stream);
 int cs_device_sm_count(int *out);
+/* Target model functions for a batch of n states (targets.py:160-287, the
+ * ModelFns a model_logp_grad_hvp returns), f64 device arrays: what = 0 log
+ * density (out: n), 1 gradient (out: n x dim), 2 Hessian-vector product with
+ * v (out: n x dim).  Logistic regression and dense Gaussians (any dim) run on
+ * the library's DMMA GEMM; other kinds return CS_ERR_CONFIG. */
+int cs_target_eval(const cs_target *target, int what, int64_t n, const double *x, const double *v, double *out,
+                   void *stream);
 /* Wait for the work queued on `stream` (the host-engine read-backs). */
 int cs_stream_sync(void *stream);
 

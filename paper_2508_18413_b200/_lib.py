@@ -75,6 +75,7 @@ _SIGS = {
     "cs_debug_pair_gram": ([P, i32, i32, P, i64, P, P], ctypes.c_int),
     "cs_device_sm_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "cs_stream_sync": ([P], ctypes.c_int),
+    "cs_target_eval": ([ctypes.POINTER(cs_target), ctypes.c_int, i64, P, P, P, P], ctypes.c_int),
     "cs_noise_fill": ([ctypes.c_int, u64, u64, i64, i64, i32, f64, ctypes.c_int, P, P], ctypes.c_int),
     "cs_rademacher_fill": ([u64, i64, P, i64, i64, i32, i32, ctypes.c_int, P, P], ctypes.c_int),
     "cs_scan_workspace_bytes": ([ctypes.c_int, ctypes.c_int, i64, i32], szt),

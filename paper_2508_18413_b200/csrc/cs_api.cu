@@ -315,6 +315,20 @@ int cs_debug_probe(unsigned long long *dev_buf, int n) {
 }
 int cs_version(void) { return 1; }
 
+int cs_target_eval(const cs_target *target, int what, int64_t n, const double *x, const double *v, double *out,
+                   void *stream) {
+  if (!target || !x || !out || n < 0 || what < 0 || what > 2 || (what == 2 && !v))
+    return fail(CS_ERR_CONFIG, "bad target_eval arguments");
+  if (target->dim < 1) return fail(CS_ERR_CONFIG, "bad target dimension");
+  if (target->kind == CS_TARGET_BLR && (!target->X || !target->y || target->n_data < 1))
+    return fail(CS_ERR_CONFIG, "logistic-regression target without data");
+  if (target->kind == CS_TARGET_GAUSSIAN && (!target->mu || !target->chol || !target->prec))
+    return fail(CS_ERR_CONFIG, "gaussian target without mean / factors");
+  const cudaError_t e = target_eval_gemm(*target, what, n, x, v, out, S(stream));
+  if (e == cudaErrorNotSupported) return fail(CS_ERR_CONFIG, "target_eval: logistic regression and gaussian only");
+  return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_target_eval");
+}
+
 int cs_stream_sync(void *stream) {
   const cudaError_t e = cudaStreamSynchronize(S(stream));
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "cs_stream_sync");

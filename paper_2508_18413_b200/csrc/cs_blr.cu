@@ -1070,6 +1070,121 @@ __global__ void k_pair_unpack(const float *Hp, int64_t ldp, int64_t T, int D, fl
 }
 }  // namespace
 
+// ---- target model functions on the device (targets.py:160-287 ModelFns) -------
+// The GEMM-shaped targets -- logistic regression and dense Gaussians of any
+// width -- evaluated for a batch of n states with our DMMA GEMM and small row
+// kernels: log density (n), gradient (n x D), Hessian-vector product (n x D).
+namespace {
+// rows of E (n x N): logp partials eta.y - sum logaddexp(0, eta) - prec/2 |x|^2 (warp per row)
+__global__ void k_tgt_blr_logp(const double *E, const double *y, const double *x, int64_t n, int N, int D,
+                               double prec, double *out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    double a = 0.0, b = 0.0, q = 0.0;
+    for (int k = lane; k < N; k += 32) {
+      const double eta = E[r * N + k];
+      a += eta * __ldg(y + k);
+      b += logaddexp0(eta);
+    }
+    for (int d = lane; d < D; d += 32) q += x[r * D + d] * x[r * D + d];
+    a = warp_sum(a);
+    b = warp_sum(b);
+    q = warp_sum(q);
+    if (lane == 0) out[r] = (a - b) - 0.5 * prec * q;
+  }
+}
+// E <- y - sigmoid(E)  (what 1), or T <- sigmoid'(E) . T (what 2)
+__global__ void k_tgt_blr_map(double *E, const double *y, double *T, int64_t total, int N, int what) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const double eta = E[i];
+    const double p = expit(eta);
+    if (what == 1) E[i] = __ldg(y + i % N) - p;
+    else T[i] *= p * (1.0 - p);
+  }
+}
+// out = sgn * G - c * z (the prior / precision terms), elementwise
+__global__ void k_tgt_axpy(double *out, const double *G, const double *z, int64_t total, double sgn, double c) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = sgn * G[i] - (z ? c * z[i] : 0.0);
+}
+__global__ void k_tgt_diff(const double *x, const double *mu, int64_t n, int D, double *out) {  // x - mu
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * D; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = x[i] - __ldg(mu + i % D);
+}
+__global__ void k_tgt_halfsq(const double *H, int64_t n, int D, double *out) {  // -|h|^2 / 2 per row
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    double q = 0.0;
+    for (int d = lane; d < D; d += 32) q += H[r * D + d] * H[r * D + d];
+    q = warp_sum(q);
+    if (lane == 0) out[r] = -0.5 * q;
+  }
+}
+unsigned egrid(int64_t total) { return (unsigned)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16); }
+}  // namespace
+
+cudaError_t target_eval_gemm(const cs_target &tg, int what, int64_t n, const double *x, const double *v,
+                             double *out, cudaStream_t st) {
+  const int D = tg.dim;
+  if (n <= 0) return cudaSuccess;
+  const unsigned gw = (unsigned)((n * 32 + 255) / 256 < 148 * 16 ? (n * 32 + 255) / 256 : 148 * 16);
+  if (tg.kind == CS_TARGET_BLR) {
+    const int N = (int)tg.n_data;
+    double *E = nullptr, *Tm = nullptr;
+    const size_t eb = sizeof(double) * (size_t)n * N;
+    cudaError_t e = cudaMallocAsync(&E, what == 2 ? 2 * eb : eb, st);
+    if (e != cudaSuccess) return e;
+    Tm = what == 2 ? E + (size_t)n * N : nullptr;
+    // eta = x X^T
+    e = gemm_rm<double, double, double>(true, (int)n, N, D, x, D, 0, tg.X, D, 0, E, N, 0, 1, st);
+    if (e == cudaSuccess) {
+      if (what == 0) {
+        k_tgt_blr_logp<<<gw, 256, 0, st>>>(E, tg.y, x, n, N, D, tg.prior_precision, out);
+      } else if (what == 1) {  // (y - p) X - prec x
+        k_tgt_blr_map<<<egrid(n * N), 256, 0, st>>>(E, tg.y, nullptr, n * N, N, 1);
+        e = gemm_rm<double, double, double>(false, (int)n, D, N, E, N, 0, tg.X, D, 0, out, D, 0, 1, st);
+        if (e == cudaSuccess) k_tgt_axpy<<<egrid(n * D), 256, 0, st>>>(out, out, x, n * D, 1.0, tg.prior_precision);
+      } else {  // -((p (1 - p)) . (v X^T)) X - prec v
+        e = gemm_rm<double, double, double>(true, (int)n, N, D, v, D, 0, tg.X, D, 0, Tm, N, 0, 1, st);
+        if (e == cudaSuccess) {
+          k_tgt_blr_map<<<egrid(n * N), 256, 0, st>>>(E, nullptr, Tm, n * N, N, 2);
+          e = gemm_rm<double, double, double>(false, (int)n, D, N, Tm, N, 0, tg.X, D, 0, out, D, 0, 1, st);
+          if (e == cudaSuccess)
+            k_tgt_axpy<<<egrid(n * D), 256, 0, st>>>(out, out, v, n * D, -1.0, tg.prior_precision);
+        }
+      }
+    }
+    cudaFreeAsync(E, st);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
+  if (tg.kind == CS_TARGET_GAUSSIAN) {
+    double *W = nullptr;
+    cudaError_t e = cudaMallocAsync(&W, sizeof(double) * (size_t)n * D * 2, st);
+    if (e != cudaSuccess) return e;
+    double *Z = W, *H = W + (size_t)n * D;
+    if (what == 2) {  // -(v P)
+      e = gemm_rm<double, double, double>(false, (int)n, D, D, v, D, 0, tg.prec, D, 0, H, D, 0, 1, st);
+      if (e == cudaSuccess) k_tgt_axpy<<<egrid(n * D), 256, 0, st>>>(out, H, nullptr, n * D, -1.0, 0.0);
+    } else {
+      k_tgt_diff<<<egrid(n * D), 256, 0, st>>>(x, tg.mu, n, D, Z);
+      if (what == 1) {  // -((x - mu) P)
+        e = gemm_rm<double, double, double>(false, (int)n, D, D, Z, D, 0, tg.prec, D, 0, H, D, 0, 1, st);
+        if (e == cudaSuccess) k_tgt_axpy<<<egrid(n * D), 256, 0, st>>>(out, H, nullptr, n * D, -1.0, 0.0);
+      } else {  // -|(x - mu) L|^2 / 2
+        e = gemm_rm<double, double, double>(false, (int)n, D, D, Z, D, 0, tg.chol, D, 0, H, D, 0, 1, st);
+        if (e == cudaSuccess) k_tgt_halfsq<<<gw, 256, 0, st>>>(H, n, D, out);
+      }
+    }
+    cudaFreeAsync(W, st);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
+  return cudaErrorNotSupported;
+}
+
 cudaError_t debug_pair_gram(const double *X, int N, int D, const double *W, int64_t T, float *H, cudaStream_t st) {
   const int nkb = (N + 31) / 32, npairs = D * (D + 1) / 2;
   const int64_t Tpad = (T + 127) / 128 * 128, ldp = (int64_t)(npairs + 127) / 128 * 128;

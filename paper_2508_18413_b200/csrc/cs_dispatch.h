@@ -25,6 +25,8 @@ cudaError_t leapfrog_batch_solve(const cs_system &sys, const cs_deer_config &cfg
                                  void *finals, int32_t *info, long long *err_step, cudaStream_t st);
 cudaError_t debug_gram(const double *X, int N, int D, const double *W, int64_t T, float *H, cudaStream_t st);
 cudaError_t debug_pair_gram(const double *X, int N, int D, const double *W, int64_t T, float *H, cudaStream_t st);
+cudaError_t target_eval_gemm(const cs_target &tg, int what, int64_t n, const double *x, const double *v,
+                             double *out, cudaStream_t st);
 cudaError_t elements_blr(const cs_system &sys, const cs_deer_config &cfg, int dtype, int64_t iteration,
                          const void *s0, const void *guess, void *e0, void *u, cs_elem_stats *stats,
                          cudaStream_t st);

@@ -12,7 +12,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import weakref
 from dataclasses import dataclass, field
 from typing import Any
 
@@ -122,6 +121,21 @@ def _flat(x, dim):
     return x.reshape(-1, dim), x.shape[:-1]
 
 
+def _native(desc, what, dim, x, v=None):
+    """log density (what 0), gradient (1) or Hessian-vector product (2) of a
+    GEMM-shaped target for a batch of states, through cs_target_eval."""
+    flat, lead = _flat(x, dim)
+    flat = flat.contiguous()
+    n = flat.shape[0]
+    vflat = None
+    if v is not None:
+        vflat = _flat(v.expand(x.shape), dim)[0].contiguous()
+    out = torch.empty((n,) if what == 0 else (n, dim), dtype=torch.float64, device=flat.device)
+    _lib.check(_lib.load().cs_target_eval(ctypes.byref(desc), what, n, _lib.ptr(flat), _lib.ptr(vflat),
+                                          _lib.ptr(out), _lib.stream_ptr()))
+    return out.reshape(lead) if what == 0 else out.reshape(tuple(lead) + (dim,))
+
+
 def model_logp_grad_hvp(spec: ModelSpec) -> TargetModel:
     """Compile a ModelSpec (targets.py:290-308): device parameters + cs_target."""
     dev = _dev()
@@ -145,12 +159,11 @@ def model_logp_grad_hvp(spec: ModelSpec) -> TargetModel:
         keep.update(mu=mu, L=L, P=P)
         desc.mu, desc.chol, desc.prec = mu.data_ptr(), L.data_ptr(), P.data_ptr()
 
-        def logp(x):
-            h = (f64(x) - mu) @ L
-            return -0.5 * torch.sum(h * h, dim=-1)
-
-        grad = lambda x: -((f64(x) - mu) @ P)
-        hvp = lambda x, v: -(f64(v) @ P)
+        # the library's DMMA GEMM (cs_target_eval): same arithmetic as
+        # targets.py:168-180, no vendor BLAS
+        logp = lambda x: _native(desc, 0, spec.dim, f64(x))
+        grad = lambda x: _native(desc, 1, spec.dim, f64(x))
+        hvp = lambda x, v: _native(desc, 2, spec.dim, f64(x), f64(v))
     elif spec.kind == "rosenbrock":
         a, b, s1, s2 = p["a"], p["b"], p["scale1"], p["scale2"]
         desc.a, desc.b, desc.scale1, desc.scale2 = a, b, s1, s2
@@ -213,49 +226,14 @@ def model_logp_grad_hvp(spec: ModelSpec) -> TargetModel:
             term = torch.sum((r * gv)[..., None] * gk, dim=-2)
             curv = torch.sum(r / var, dim=-1)
             return term - curv[..., None] * v - gbar * torch.sum(gbar * v, dim=-1)[..., None]
-    else:  # blr: eta = beta X^T as a cuBLAS GEMM, shared by logp / grad / hvp
+    else:  # blr (targets.py:254-287): eta = beta X^T and the products against X on the library's DMMA GEMM
         X, y, prec = _t(p["X"], dev), _t(p["y"], dev), p["prior_precision"]
         keep.update(X=X, y=y)
         desc.n_data = X.shape[0]
         desc.X, desc.y, desc.prior_precision = X.data_ptr(), y.data_ptr(), prec
-        dim = spec.dim
-        etas = []  # [(weakref(beta), version, eta, sigmoid(eta))], two most recent batches
-
-        def eta_of(beta, flat):
-            # MALA evaluates logp, grad and hvp at the current states and at the
-            # proposals; each batch's logits are formed once (weakref identity +
-            # version key, so a recycled allocation never hits)
-            for ref, ver, eta, pr in etas:
-                if ref() is beta and ver == beta._version:
-                    return eta, pr
-            eta = flat @ X.T
-            pr = torch.sigmoid(eta)
-            etas.insert(0, (weakref.ref(beta), beta._version, eta, pr))
-            del etas[2:]
-            return eta, pr
-
-        def logp(beta):
-            beta = f64(beta)
-            flat, lead = _flat(beta, dim)
-            eta, _ = eta_of(beta, flat)
-            out = eta @ y - torch.logaddexp(torch.zeros((), dtype=eta.dtype, device=dev), eta).sum(dim=-1)
-            out = out - 0.5 * prec * torch.sum(flat * flat, dim=-1)
-            return out.reshape(lead)
-
-        def grad(beta):
-            beta = f64(beta)
-            flat, lead = _flat(beta, dim)
-            _, pr = eta_of(beta, flat)
-            out = (y - pr) @ X - prec * flat
-            return out.reshape(lead + (dim,))
-
-        def hvp(beta, v):
-            beta = f64(beta)
-            flat, lead = _flat(beta, dim)
-            vflat, _ = _flat(f64(v).expand(beta.shape), dim)
-            _, pr = eta_of(beta, flat)
-            out = -(((pr * (1.0 - pr)) * (vflat @ X.T)) @ X) - prec * vflat
-            return out.reshape(lead + (dim,))
+        logp = lambda beta: _native(desc, 0, spec.dim, f64(beta))
+        grad = lambda beta: _native(desc, 1, spec.dim, f64(beta))
+        hvp = lambda beta, v: _native(desc, 2, spec.dim, f64(beta), f64(v))
 
     tm = DeviceTarget(dim=spec.dim, logp=logp, grad=grad, hvp=hvp, spec=spec)
     object.__setattr__(tm, "_keep", keep)

@@ -117,6 +117,36 @@ def test_blr_large_batch_matches_one_shot_formula(cuda_device):  # test_targets.
     np.testing.assert_allclose(np_(model.grad(B)), gwant, atol=1e-10)
 
 
+@pytest.mark.parametrize("D", [3, 100, 300])
+def test_gemm_targets_native_match_numpy(cuda_device, D):
+    # logistic regression and dense Gaussians evaluate on the library's DMMA GEMM
+    # (cs_target_eval): logp / grad / hvp against the numpy formulas
+    # (targets.py:160-287), including a broadcast tangent and a leading batch shape
+    rng = np.random.default_rng(D)
+    X = rng.normal(size=(257, D)) / np.sqrt(D)
+    y = (rng.uniform(size=257) < 0.5).astype(float)
+    blr = T_.model_logp_grad_hvp(T_.blr(X, y, prior_precision=0.7))
+    B = rng.normal(size=(2, 33, D))
+    V = rng.normal(size=D)
+    eta = B @ X.T
+    p = 1.0 / (1.0 + np.exp(-eta))
+    np.testing.assert_allclose(np_(blr.logp(B)), eta @ y - np.logaddexp(0.0, eta).sum(-1) - 0.35 * np.sum(B * B, -1),
+                               rtol=1e-12, atol=1e-10)
+    np.testing.assert_allclose(np_(blr.grad(B)), (y - p) @ X - 0.7 * B, rtol=1e-12, atol=1e-10)
+    np.testing.assert_allclose(np_(blr.hvp(B, V)), -(((p * (1 - p)) * (V @ X.T)) @ X) - 0.7 * V,
+                               rtol=1e-12, atol=1e-10)
+    Q, _ = np.linalg.qr(rng.normal(size=(D, D)))
+    Lc = np.linalg.cholesky((Q * np.exp(rng.uniform(-1, 1, D))) @ Q.T)
+    mu = rng.normal(size=D)
+    g = T_.model_logp_grad_hvp(T_.gaussian(mu, Lc))
+    P = Lc @ Lc.T
+    h = (B - mu) @ Lc
+    np.testing.assert_allclose(np_(g.logp(B)), -0.5 * np.sum(h * h, -1), rtol=1e-12, atol=1e-9)
+    np.testing.assert_allclose(np_(g.grad(B)), -((B - mu) @ P), rtol=1e-12, atol=1e-9)
+    np.testing.assert_allclose(np_(g.hvp(B, V)), np.broadcast_to(-(V @ P), B.shape), rtol=1e-12, atol=1e-9)
+    assert g.logp(B[0, 0]).shape == () and g.grad(B[0, 0]).shape == (D,)
+
+
 def test_invalid_specs_rejected(cuda_device):  # test_targets.py:151-164
     with pytest.raises(cs.ConfigurationError):
         T_.mog(weights=[0.5, 0.6], means=[[0.0], [1.0]])
