@@ -65,6 +65,13 @@ CS_D int64_t swz_index(int64_t row, int k, int nkb) {
 // first packed index of triangle row i (pairs (i, j >= i), row-major)
 CS_D int pair_row_start(int i, int D) { return i * D - i * (i - 1) / 2; }
 
+// zero the K padding (data rows N .. 32 nkb) of the tiled weight operand
+__global__ void k_wt_pad(float *wsw, int64_t T, int N, int nkb) {
+  const int pad = 32 * nkb - N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T * pad; i += (int64_t)gridDim.x * blockDim.x)
+    wsw[swz_index(i / pad, N + (int)(i % pad), nkb)] = 0.0f;
+}
+
 // per step r (one warp, lanes across the N data rows): p = sigmoid(eta),
 // E[r] <- y - p, probe rows <- p(1-p) . (z X^T), and the two log-density row
 // sums eta.y and sum logaddexp(0, eta).  exp(-eta) serves both the sigmoid and,
@@ -278,11 +285,6 @@ __global__ void k_bd_resid(cs_system sys, const ST *s0, const ST *guess, const d
     GX[idx] = gt;
     R[idx] = (s - xt) - eps * gt;
   }
-}
-
-__global__ void k_bd_scale(double *E, const double *W, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    E[i] *= W[i];
 }
 
 constexpr int kBdThr = 256;
@@ -954,8 +956,10 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   const int nkb = (N + 31) / 32, npairs = D * (D + 1) / 2;
   const int64_t Tpad = (T + 127) / 128 * 128, ldp = (int64_t)(npairs + 127) / 128 * 128;
   const size_t pg_floats = pg ? (size_t)(Tpad * 32 * nkb + ldp * 32 * nkb + Tpad * ldp) : 0;
+  // + the fused GEMM epilogue's row partials (T x npart x 2)
+  const int npart = (N + 63) / 64 * 2;
   const size_t need = (size_t)7 * T * D + (size_t)3 * T * N + (size_t)4 * T + (size_t)64 * (N + 32) +
-                      (pg_floats + 1) / 2 + 64;
+                      (pg_floats + 1) / 2 + 64 + (size_t)2 * T * npart + 64;
   if (ctx.cap < need) {
     if (ctx.buf) cudaFree(ctx.buf);
     ctx.buf = nullptr;
@@ -971,9 +975,14 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   float *Xf = (float *)(rsX + 2 * T);
   float *Wt = (float *)(((uintptr_t)(rsX + 2 * T + 64 * (N + 32)) + 255) & ~(uintptr_t)255);
   float *Qt = Wt + Tpad * 32 * nkb, *Hp = Qt + ldp * 32 * nkb;
+  double *part = (double *)(((uintptr_t)(pg ? Hp + Tpad * ldp : Wt) + 255) & ~(uintptr_t)255);
   const double *X = sys.target.X, *y = sys.target.y;
   auto gemm_xt = [&](const double *Ain, double *Cout) {  // C (T x N) = A (T x D) X^T
     return gemm_rm<double, double, double>(true, (int)T, N, D, Ain, D, 0, X, D, 0, Cout, N, 0, 1, st);
+  };
+  // the same product with the logistic epilogue fused into its tile stores
+  auto gemm_xt_logit = [&](const double *Ain, double *wout, float *wsw, double *rowsum) {
+    return gemm_xt_logistic((int)T, N, D, Ain, D, X, D, E, N, y, wout, wsw, nkb, part, rowsum, st);
   };
   auto gemm_x = [&](const double *Bin, double *Cout) {  // C (T x D) = B (T x N) X
     return gemm_rm<double, double, double>(false, (int)T, D, N, Bin, N, 0, X, D, 0, Cout, D, 0, 1, st);
@@ -981,9 +990,9 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
   const unsigned ge = (unsigned)((T * D + 255) / 256 < 148 * 32 ? (T * D + 255) / 256 : 148 * 32);
   const unsigned gw = (unsigned)((T * 32 + 255) / 256);
   k_blr_prologue<ST><<<ge, 256, 0, st>>>(sys, s0, guess, iteration, 0, A);
-  if (cudaError_t ge = gemm_xt(A, E)) return ge;
   if (pg) {  // the weights go straight into the GEMM's operand tiles; H_raw for every step in one GEMM
-    k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsS, nullptr, Wt, nkb);
+    if (cudaError_t ge = gemm_xt_logit(A, nullptr, Wt, rsS)) return ge;
+    if (N < 32 * nkb) k_wt_pad<<<(unsigned)((T * 32 + 255) / 256), 256, 0, st>>>(Wt, T, N, nkb);
     const int64_t qn = ldp * 32 * nkb;
     k_pair_operand<<<(unsigned)((qn + 255) / 256 < 148 * 64 ? (qn + 255) / 256 : 148 * 64), 256, 0, st>>>(
         X, N, D, nkb, npairs, qn, Qt);
@@ -996,16 +1005,15 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
     }
     k_pair_gram<<<dim3((unsigned)(ldp / 128), (unsigned)(Tpad / 128)), 128, smem, st>>>(Wt, Qt, nkb, Hp, ldp);
   } else {
-    k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsS, WS);
+    if (cudaError_t ge = gemm_xt_logit(A, WS, nullptr, rsS)) return ge;
   }
   if (cudaError_t ge = gemm_x(E, G)) return ge;
   k_blr_propose<ST><<<gw, 256, 0, st>>>(sys, s0, guess, A, G, 0, A2, gS, stats);
-  if (cudaError_t ge = gemm_xt(A2, E)) return ge;
-  k_blr_epilogue<<<gw, 256, 0, st>>>(E, y, T, 0, N, rsX, WX);
+  if (cudaError_t ge = gemm_xt_logit(A2, WX, nullptr, rsX)) return ge;
   if (cudaError_t ge = gemm_x(E, G)) return ge;
   k_bd_resid<ST><<<ge, 256, 0, st>>>(sys, s0, guess, A2, G, GX, R);
-  if (cudaError_t ge = gemm_xt(R, E)) return ge;
-  k_bd_scale<<<148 * 32, 256, 0, st>>>(E, WX, T * N);
+  // H(x~) r: (r X^T) . w~ straight out of the GEMM, then against X
+  if (cudaError_t ge = gemm_xt_scaled((int)T, N, D, R, D, X, D, E, N, WX, st)) return ge;
   if (cudaError_t ge = gemm_x(E, HR)) return ge;
   if constexpr (sizeof(ST) == 4) {
     if (pg) {

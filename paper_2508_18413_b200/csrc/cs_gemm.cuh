@@ -22,6 +22,24 @@
 
 namespace cs {
 
+// Optional fused epilogue on the C tile (mode 0: plain store):
+//   1 logistic: eta = the product; C <- y[col] - sigmoid(eta); weights
+//     p (1 - p) to `wout` (f64, C's layout) and / or `wsw` (f32 tcgen05 operand
+//     tiles, see swz_index in cs_blr.cu); per-row partial sums
+//     (eta . y, sum logaddexp(0, eta)) over this warp's 32 columns to
+//     part[row][npart] -- folded in a fixed order afterwards (deterministic)
+//   2 scale: C <- product . S[row][col]
+struct GemmEpi {
+  int mode = 0;
+  const double *y = nullptr;
+  double *part = nullptr;
+  int npart = 0;
+  double *wout = nullptr;
+  float *wsw = nullptr;
+  int nkb = 0;
+  const double *S = nullptr;
+};
+
 namespace gemm_detail {
 
 constexpr int kBN = 64;
@@ -49,10 +67,10 @@ template <int BM> struct GemmWarps {
   static constexpr int LDA = BK + 4;              // 12 / 20 doubles: A fragments conflict free
 };
 
-template <int BM, bool BT, typename TA, typename TB, typename TC>
+template <int BM, bool BT, typename TA, typename TB, typename TC, int EPI = 0>
 __global__ void __launch_bounds__(GemmWarps<BM>::NT)
 k_gemm(int M, int N, int K, const TA *__restrict__ A, int64_t lda, int64_t sA, const TB *__restrict__ B,
-       int64_t ldb, int64_t sB, TC *__restrict__ C, int64_t ldc, int64_t sC) {
+       int64_t ldb, int64_t sB, TC *__restrict__ C, int64_t ldc, int64_t sC, GemmEpi ep = GemmEpi()) {
   using GW = GemmWarps<BM>;
   constexpr int kBK = GW::BK, kLDA = GW::LDA;
   constexpr int NT = GW::NT;                     // threads
@@ -134,19 +152,127 @@ k_gemm(int M, int N, int K, const TA *__restrict__ A, int64_t lda, int64_t sA, c
       __syncthreads();
     }
   }
+  if constexpr (EPI == 0) {
 #pragma unroll
-  for (int mi = 0; mi < MI; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < MI; ++ni) {
+      for (int ni = 0; ni < MI; ++ni) {
+        const int gm = m0 + wm * GW::WT + mi * 8 + (lane >> 2);
+        const int gn = n0 + wn * GW::WT + ni * 8 + 2 * (lane & 3);
+        if (gm >= M) continue;
+        if (gn < N) C[(int64_t)gm * ldc + gn] = (TC)c[mi][ni][0];
+        if (gn + 1 < N) C[(int64_t)gm * ldc + gn + 1] = (TC)c[mi][ni][1];
+      }
+  } else {
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
       const int gm = m0 + wm * GW::WT + mi * 8 + (lane >> 2);
-      const int gn = n0 + wn * GW::WT + ni * 8 + 2 * (lane & 3);
-      if (gm >= M) continue;
-      if (gn < N) C[(int64_t)gm * ldc + gn] = (TC)c[mi][ni][0];
-      if (gn + 1 < N) C[(int64_t)gm * ldc + gn + 1] = (TC)c[mi][ni][1];
+      double pa = 0.0, pb = 0.0;
+#pragma unroll
+      for (int ni = 0; ni < MI; ++ni)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = n0 + wn * GW::WT + ni * 8 + 2 * (lane & 3) + h;
+          if (gm >= M || gn >= N) continue;
+          const int64_t o = (int64_t)gm * ldc + gn;
+          const double v = c[mi][ni][h];
+          if constexpr (EPI == 1) {
+            const double yn = __ldg(ep.y + gn);
+            const double em = exp(-v);
+            const double p = 1.0 / (1.0 + em);  // expit
+            pa += v * yn;
+            pb += v != v ? v : fmax(v, 0.0) + log1p(v >= 0.0 ? em : exp(v));  // logaddexp(0, eta)
+            C[o] = (TC)(yn - p);
+            const double w = p * (1.0 - p);
+            if (ep.wout) ep.wout[o] = w;
+            if (ep.wsw) {
+              const int rr = gm & 127, cc = (gn & 31) >> 2;
+              ep.wsw[((((int64_t)gm >> 7) * ep.nkb + (gn >> 5)) * 128 + rr) * 32 + ((cc ^ (rr & 7)) << 2) + (gn & 3)] =
+                  (float)w;
+            }
+          } else {
+            C[o] = (TC)(v * ep.S[o]);
+          }
+        }
+      if constexpr (EPI == 1) {
+        // the 4 lanes of a row (lane & 3), then one partial per (row, warp column)
+        pa += __shfl_xor_sync(0xffffffffu, pa, 1);
+        pb += __shfl_xor_sync(0xffffffffu, pb, 1);
+        pa += __shfl_xor_sync(0xffffffffu, pa, 2);
+        pb += __shfl_xor_sync(0xffffffffu, pb, 2);
+        if ((lane & 3) == 0 && gm < M) {
+          double *q = ep.part + ((int64_t)gm * ep.npart + (int64_t)blockIdx.x * GW::WN + wn) * 2;
+          q[0] = pa;
+          q[1] = pb;
+        }
+      }
     }
+  }
+}
+
+// fixed-order fold of the logistic epilogue's row partials (warp per row)
+static __global__ void k_gemm_rowfold(const double *part, int64_t M, int npart, double *rowsum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < M; r += nw) {
+    double a = 0.0, b = 0.0;
+    for (int j = lane; j < npart; j += 32) {  // lane-sequential, then a fixed butterfly
+      a += part[(r * npart + j) * 2];
+      b += part[(r * npart + j) * 2 + 1];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, off);
+      b += __shfl_xor_sync(0xffffffffu, b, off);
+    }
+    if (lane == 0) {
+      rowsum[2 * r] = a;
+      rowsum[2 * r + 1] = b;
+    }
+  }
 }
 
 }  // namespace gemm_detail
+
+// C = eta = A X^T (M x N, f64) with the logistic epilogue fused (GemmEpi mode 1):
+// C <- y - sigmoid(eta), weights to wout / wsw, row sums (eta . y, sum
+// logaddexp(0, eta)) to rowsum[2 M].  part: scratch of M * ceil(N / 32) * 2
+// doubles.  One batch, 128-row tiles.
+inline cudaError_t gemm_xt_logistic(int M, int N, int K, const double *A, int64_t lda, const double *X, int64_t ldx,
+                                    double *C, int64_t ldc, const double *y, double *wout, float *wsw, int nkb,
+                                    double *part, double *rowsum, cudaStream_t st) {
+  using namespace gemm_detail;
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  GemmEpi ep;
+  ep.mode = 1;
+  ep.y = y;
+  ep.wout = wout;
+  ep.wsw = wsw;
+  ep.nkb = nkb;
+  ep.part = part;
+  ep.npart = (int)((N + kBN - 1) / kBN) * GemmWarps<128>::WN;
+  const dim3 grid((unsigned)((N + kBN - 1) / kBN), (M + 127) / 128, 1);
+  k_gemm<128, true, double, double, double, 1><<<grid, GemmWarps<128>::NT, 0, st>>>(M, N, K, A, lda, 0, X, ldx, 0, C,
+                                                                                    ldc, 0, ep);
+  const int64_t wr = (int64_t)M * 32;
+  k_gemm_rowfold<<<(unsigned)((wr + 255) / 256 < 148 * 16 ? (wr + 255) / 256 : 148 * 16), 256, 0, st>>>(
+      part, M, ep.npart, rowsum);
+  return cudaGetLastError();
+}
+
+// C = (A X^T) . S elementwise (GemmEpi mode 2), 128-row tiles, one batch
+inline cudaError_t gemm_xt_scaled(int M, int N, int K, const double *A, int64_t lda, const double *X, int64_t ldx,
+                                  double *C, int64_t ldc, const double *S, cudaStream_t st) {
+  using namespace gemm_detail;
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  GemmEpi ep;
+  ep.mode = 2;
+  ep.S = S;
+  const dim3 grid((unsigned)((N + kBN - 1) / kBN), (M + 127) / 128, 1);
+  k_gemm<128, true, double, double, double, 2><<<grid, GemmWarps<128>::NT, 0, st>>>(M, N, K, A, lda, 0, X, ldx, 0, C,
+                                                                                    ldc, 0, ep);
+  return cudaGetLastError();
+}
 
 // C = A . op(B) for `batch` independent problems (see the header comment).
 // Small problems (fewer than ~2 waves of 64 x 64 tiles) take 32 x 64 tiles.
@@ -160,7 +286,9 @@ cudaError_t gemm_rm(bool bt, int M, int N, int K, const TA *A, int64_t lda, int6
   // the largest tile that still gives every SM a couple of CTAs
   const int BM = tiles128 >= 4 * 148 ? 128 : tiles64 >= 2 * 148 ? 64 : 32;
   const dim3 grid((unsigned)nt, (M + BM - 1) / BM, batch);
-  auto go = [&](auto kern, int threads) { kern<<<grid, threads, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC); };
+  auto go = [&](auto kern, int threads) {
+    kern<<<grid, threads, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, GemmEpi());
+  };
   if (BM == 128) {
     if (bt) go(k_gemm<128, true, TA, TB, TC>, GemmWarps<128>::NT);
     else go(k_gemm<128, false, TA, TB, TC>, GemmWarps<128>::NT);
