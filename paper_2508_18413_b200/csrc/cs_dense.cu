@@ -256,6 +256,83 @@ k_dense_replay(const ST *__restrict__ J, const ST *__restrict__ u, const double 
   }
 }
 
+// f32 replay with the step maps streamed through shared memory: J_t and u_t of
+// the next kRpStages steps are in flight as 1-D bulk copies (TMA engine) while
+// step t is applied, so a chunk's walk runs at its HBM rate instead of one
+// exposed load latency per step (D % 4 == 0: every map is whole 16-byte lines)
+constexpr int kRpStages = 2;
+
+template <int DP>
+__global__ void __launch_bounds__(kDwThr, 1)
+k_dense_replay_tma(const float *__restrict__ J, const float *__restrict__ u, const double *entries, int64_t T, int D,
+                   int c, float *out) {
+  constexpr int NW = kDwThr / 32, RPW = DP / NW, KL = (DP + 31) / 32;
+  extern __shared__ __align__(16) unsigned char rsm[];
+  __shared__ double s[2][128];
+  __shared__ __align__(8) uint64_t bar[kRpStages];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t q = blockIdx.x, t0 = q * (int64_t)c;
+  const int64_t t1 = t0 + c < T ? t0 + c : T;
+  const int64_t DD = (int64_t)D * D;
+  const int slot = (int)(((size_t)DD + D + 3) / 4 * 4);  // floats per stage (16-byte multiple)
+  float *ring = (float *)rsm;
+  if (tid == 0) {
+    for (int k = 0; k < kRpStages; ++k) mbar_init(&bar[k], 1);
+    fence_mbar_init();
+  }
+  if (tid < D) s[0][tid] = entries[q * D + tid];
+  __syncthreads();
+  auto issue = [&](int64_t t) {  // thread 0: step t's J_t and u_t into its stage
+    const int k = (int)((t - t0) % kRpStages);
+    float *dst = ring + (size_t)k * slot;
+    mbar_expect_tx(&bar[k], (unsigned)((DD + D) * sizeof(float)));
+    bulk_g2s(dst, J + t * DD, (unsigned)(DD * sizeof(float)), &bar[k]);
+    bulk_g2s(dst + DD, u + t * D, (unsigned)(D * sizeof(float)), &bar[k]);
+  };
+  if (tid == 0)
+    for (int64_t t = t0; t < t1 && t < t0 + kRpStages; ++t) issue(t);
+  int par = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int k = (int)((t - t0) % kRpStages);
+    mbar_wait(&bar[k], (unsigned)(((t - t0) / kRpStages) & 1));
+    const float *Js = ring + (size_t)k * slot, *us = Js + DD;
+    const double *cur = s[par];
+    double acc[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int i = w + NW * r;
+      acc[r] = 0.0;
+#pragma unroll
+      for (int m = 0; m < KL; ++m) {
+        const int kk = lane + 32 * m;
+        if (i < D && kk < D) acc[r] = fma((double)Js[i * D + kk], cur[kk], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
+      const int i = w + NW * r;
+      if (lane == 0 && i < D) {
+        const float v = (float)(acc[r] + (double)us[i]);
+        s[par ^ 1][i] = (double)v;
+        out[t * D + i] = v;
+      }
+    }
+    __syncthreads();  // every read of stage k and of s[par] is done
+    if (tid == 0 && t + kRpStages < t1) issue(t + kRpStages);
+    par ^= 1;
+  }
+}
+
+static bool dense_replay_tma() {  // CS_DENSE_REPLAY_TMA=0 keeps the register-prefetch replay
+  static const bool v = [] {
+    const char *e = getenv("CS_DENSE_REPLAY_TMA");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 int dense_wide_chunk(int64_t T) {
   const char *e = getenv("CS_DENSE_CHUNK");
@@ -783,6 +860,18 @@ static cudaError_t launch_tail(const ScanArgs<ST> &a, int c, int64_t nch, const 
     if (e != cudaSuccess) return e;
     k_dense_carry<ST, DP><<<1, kDwThr, 0, st>>>(gM, gw, a.s0, nullptr, ng, D, ng, gent);
     k_dense_carry<ST, DP><<<(unsigned)ng, kDwThr, 0, st>>>(aggM, aggw, a.s0, gent, nch, D, kDwGroup, entries);
+  }
+  if constexpr (sizeof(ST) == 4) {
+    if (dense_replay_tma() && D % 4 == 0 && ((((uintptr_t)a.e0) | ((uintptr_t)a.u)) & 15) == 0) {
+      const size_t slot = ((size_t)D * D + D + 3) / 4 * 4;
+      const size_t smem = sizeof(float) * slot * kRpStages;
+      cudaError_t e = cudaFuncSetAttribute(k_dense_replay_tma<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      k_dense_replay_tma<DP><<<(unsigned)nch, kDwThr, smem, st>>>((const float *)a.e0, (const float *)a.u, entries,
+                                                                  a.T, D, c, (float *)a.out);
+      return cudaGetLastError();
+    }
   }
   k_dense_replay<ST, DP><<<(unsigned)nch, kDwThr, 0, st>>>(a.e0, a.u, entries, a.T, D, c, a.out);
   return cudaGetLastError();
