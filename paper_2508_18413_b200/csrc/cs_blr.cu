@@ -1048,7 +1048,7 @@ static cudaError_t blr_dense_run(const cs_system &sys, const cs_deer_config &cfg
 cudaError_t debug_gram(const double *X, int N, int D, const double *W, int64_t T, float *H, cudaStream_t st) {
   const int ldx = (N + 31) / 32 * 32;
   float *XT = nullptr;
-  cudaError_t e = cudaMallocAsync(&XT, sizeof(float) * 128 * ldx, st);
+  cudaError_t e = scratch_alloc((void **)&XT, sizeof(float) * 128 * ldx, st);
   if (e != cudaSuccess) return e;
   k_bd_xt<<<(128 * ldx + 255) / 256, 256, 0, st>>>(X, N, D, ldx, XT);
   const size_t hs = 2 * kUmmaStages * kUmmaTile > 128 * 129 ? 2 * kUmmaStages * kUmmaTile : 128 * 129;
@@ -1142,7 +1142,7 @@ cudaError_t target_eval_gemm(const cs_target &tg, int what, int64_t n, const dou
     const int N = (int)tg.n_data;
     double *E = nullptr, *Tm = nullptr;
     const size_t eb = sizeof(double) * (size_t)n * N;
-    cudaError_t e = cudaMallocAsync(&E, what == 2 ? 2 * eb : eb, st);
+    cudaError_t e = scratch_alloc((void **)&E, what == 2 ? 2 * eb : eb, st);
     if (e != cudaSuccess) return e;
     Tm = what == 2 ? E + (size_t)n * N : nullptr;
     // eta = x X^T
@@ -1170,7 +1170,7 @@ cudaError_t target_eval_gemm(const cs_target &tg, int what, int64_t n, const dou
   }
   if (tg.kind == CS_TARGET_GAUSSIAN) {
     double *W = nullptr;
-    cudaError_t e = cudaMallocAsync(&W, sizeof(double) * (size_t)n * D * 2, st);
+    cudaError_t e = scratch_alloc((void **)&W, sizeof(double) * (size_t)n * D * 2, st);
     if (e != cudaSuccess) return e;
     double *Z = W, *H = W + (size_t)n * D;
     if (what == 2) {  // -(v P)
@@ -1199,7 +1199,7 @@ cudaError_t debug_pair_gram(const double *X, int N, int D, const double *W, int6
   if (T == 0) return cudaSuccess;
   float *buf = nullptr;
   const size_t nf = (size_t)(Tpad * 32 * nkb + ldp * 32 * nkb + Tpad * ldp);
-  cudaError_t e = cudaMallocAsync(&buf, sizeof(float) * nf, st);
+  cudaError_t e = scratch_alloc((void **)&buf, sizeof(float) * nf, st);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(buf, 0, sizeof(float) * Tpad * 32 * nkb, st);
   float *Wt = buf, *Qt = Wt + Tpad * 32 * nkb, *Hp = Qt + ldp * 32 * nkb;

@@ -33,6 +33,24 @@ struct ScratchFence {
     cudaEventRecord(ev, st);
   }
 };
+// Stream-ordered scratch (cudaMallocAsync) from the device's default pool, which
+// keeps freed blocks instead of returning them at every synchronisation (the
+// default release threshold of 0 re-maps memory on each call: milliseconds).
+inline cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st) {
+  static bool done[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!done[dev & 15]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done[dev & 15] = true;
+  }
+  return cudaMallocAsync(p, bytes, st);
+}
+
 struct ScratchScope {  // acquire now, release when the enqueueing function returns
   ScratchFence &f;
   cudaStream_t st;
