@@ -175,12 +175,19 @@ def require_cuda():
         raise RuntimeError("paper_2508_18413_b200 needs a CUDA device (B200); no CPU fallback")
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_CUR_DEVICE = getattr(torch._C, "_cuda_getDevice", None)
+
+
 def stream_ptr(stream=None):
     # the current stream's raw handle without building a torch.cuda.Stream
-    # object (15 us per call through torch.cuda.current_stream())
+    # object (15 us per call through torch.cuda.current_stream()); the public
+    # path when this torch build lacks the private accessors
     if stream is not None:
         return ctypes.c_void_p(stream.cuda_stream)
-    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
+    if _RAW_STREAM is not None and _CUR_DEVICE is not None:
+        return ctypes.c_void_p(_RAW_STREAM(_CUR_DEVICE()))
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def sync_current():
