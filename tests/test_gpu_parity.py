@@ -520,6 +520,24 @@ def test_blr_dense_builder_options_match_host_engine(cuda_device, kw):
     np.testing.assert_array_equal(np_(r.per_step_converged_at), np_(h.per_step_converged_at))
 
 
+@pytest.mark.parametrize("D", [9, 100, 128])
+def test_blr_dense_f32_builder_widths(cuda_device, D):
+    # the f32 dense builder (pair-Gram tcgen05 Hessian + element kernel: scalar J
+    # rows at D % 4 != 0, 16-byte rows otherwise, DP = 112 / 128 tiles) converges
+    # to the sequential chain, like the host engine's jvp-built Jacobians
+    X, y, _ = cs.synthetic_credit_like(seed=7 + D, n=400, dim=D)
+    m = cs.model_logp_grad_hvp(cs.blr(X, y, 1.0))
+    k = cs.MalaKernel(m, 0.002, seed=3, T=257, dtype=torch.float32)
+    seq = np_(cs.sequential_evaluate(k, np.zeros(D)))
+    r = cs.run_deer(k, np.zeros(D), cs.DeerConfig(mode="dense", atol=1e-6, rtol=1e-5, max_iters=120))
+    h = cs.run_deer(k, np.zeros(D), cs.DeerConfig(mode="dense", atol=1e-6, rtol=1e-5, max_iters=120, engine="host"))
+    assert r.stats["path"] == "streamed" and h.stats["path"] == "host"
+    assert r.converged and h.converged
+    assert abs(r.iterations - h.iterations) <= 3
+    np.testing.assert_allclose(np_(r.trace), seq, atol=2e-4, rtol=2e-4)
+    np.testing.assert_allclose(np_(h.trace), seq, atol=2e-4, rtol=2e-4)
+
+
 def test_run_deer_leapfrog_gauss200(cuda_device):
     g = golden("leapfrog_gauss200")
     m = cs.model_logp_grad_hvp(cs.gaussian(np.zeros(200), g["chol"]))
