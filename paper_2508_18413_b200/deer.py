@@ -449,12 +449,17 @@ class _NotInstantiated(Exception):
 _STATS_BYTES = 40
 
 
-def _parse_stats(buf):
+def _parse_stats(buf, host=None, event=None):
     # one 40-byte read-back per iteration into a reused (per-thread) pinned
-    # buffer: no pageable allocation, one stream sync
-    host = _pinned("stats", buf.numel(), torch.uint8)
-    host.copy_(buf, non_blocking=True)
-    _lib.sync_current()
+    # buffer: no pageable allocation, one stream sync -- or, with `host` and
+    # `event`, a copy already queued: wait for that event only (work queued
+    # after it keeps the device busy while the host decides)
+    if host is None:
+        host = _pinned("stats", buf.numel(), torch.uint8)
+        host.copy_(buf, non_blocking=True)
+        _lib.sync_current()
+    else:
+        event.synchronize()
     raw = host.numpy().tobytes()
     bad_prop, bad_step, bad_jac = np.frombuffer(raw[:24], dtype=np.int64)
     picard, fail_rows = np.frombuffer(raw[24:32], dtype=np.uint32)
@@ -492,8 +497,14 @@ def _run_streamed(system, s0, cfg, max_iters):
     half = D // 2 if mode == "block2x2-stochastic" else D
     ws_bytes = lib.cs_scan_workspace_bytes(c.mode, dt, T, half)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
-    stats = torch.zeros(_STATS_BYTES, dtype=torch.uint8, device=dev)
-    sptr = _lib.ptr(stats)
+    # two stats records: while the host reads iteration it's, iteration it+1's
+    # elements are already being built (speculatively: they depend only on the
+    # new iterate and it+1, so they are exact whenever the loop goes on)
+    stats2 = [torch.zeros(_STATS_BYTES, dtype=torch.uint8, device=dev) for _ in range(2)]
+    hosts = [_pinned("stats_a", _STATS_BYTES, torch.uint8), _pinned("stats_b", _STATS_BYTES, torch.uint8)]
+    ready = torch.cuda.Event()
+    sb = 0
+    stats, sptr = stats2[0], _lib.ptr(stats2[0])
     guess = s0.expand(T, D).clone()
     nxt = torch.empty_like(guess)
     last_fail = torch.zeros(T, dtype=torch.int32, device=dev)
@@ -501,12 +512,18 @@ def _run_streamed(system, s0, cfg, max_iters):
     hist, d0, it, done = [], None, 0, False
     launches = 0
     nfail, picard = 1, 1
-    while True:
-        rc = lib.cs_system_elements(ctypes.byref(d), ctypes.byref(c), dt, it, _lib.ptr(s0), _lib.ptr(guess),
-                                    *eptr, _lib.ptr(u), sptr, st)
-        if rc == _lib.CS_ERR_CONFIG and it == 0:
+    built = False  # this iteration's elements already queued (speculation)
+
+    def build(it_, g_, sp_):
+        rc_ = lib.cs_system_elements(ctypes.byref(d), ctypes.byref(c), dt, it_, _lib.ptr(s0), _lib.ptr(g_),
+                                     *eptr, _lib.ptr(u), sp_, st)
+        if rc_ == _lib.CS_ERR_CONFIG and it_ == 0:
             raise _NotInstantiated()
-        _lib.check(rc)
+        _lib.check(rc_)
+
+    while True:
+        if not built:
+            build(it, guess, sptr)
         launches += 2
         counted = it < max_iters
         if counted:
@@ -529,7 +546,12 @@ def _run_streamed(system, s0, cfg, max_iters):
                                                ctypes.c_void_p(base + 32), st)
             _lib.check(rc)
             launches += 2
-        bad_prop, bad_step, bad_jac, picard, nfail, dmax = _parse_stats(stats)
+        hosts[sb].copy_(stats, non_blocking=True)
+        ready.record()
+        built = counted  # the next iteration's elements, queued before the host decides
+        if built:
+            build(it + 1, nxt, _lib.ptr(stats2[sb ^ 1]))
+        bad_prop, bad_step, bad_jac, picard, nfail, dmax = _parse_stats(stats, hosts[sb], ready)
         if bad_prop != _NO_STEP:
             raise ChainDivergedError(f"non-finite {getattr(system, '_what', 'proposal')} at step {bad_prop}",
                                      step=bad_prop)
@@ -549,6 +571,8 @@ def _run_streamed(system, s0, cfg, max_iters):
         it += 1
         hist.append(dmax)
         guess, nxt = nxt, guess
+        sb ^= 1
+        stats, sptr = stats2[sb], _lib.ptr(stats2[sb])
         if d0 is None:
             d0 = dmax
         _guard(dmax, d0, it)
