@@ -413,21 +413,25 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
   // tile records and the element / output arrays are 16-byte aligned (bulk copies)
   const bool a16 = ((((uintptr_t)e0) | ((uintptr_t)u) | ((uintptr_t)out)) & 15) == 0;
   const bool one_pass = a16 && scan_1p_eligible(var, T, D) && ws_bytes >= scan_plan_1p(var, dtype, T, D).ws_bytes;
+  // (any alignment: the local scan falls back to plain loads for unaligned arrays)
+  const bool local = scan_local_eligible(var, T, D) && ws_bytes >= scan_local_ws_bytes(dtype, T, D);
   cudaError_t e;
   if (dtype == CS_F64) {
     ScanArgs<double> a{(const double *)e0, (const double *)e1, (const double *)e2, (const double *)e3,
                        (const double *)u, (const double *)s0, (double *)out, T, D};
     a.probe = h_probe;
     a.probe_n = h_probe_n;
-    e = one_pass ? launch_scan_1p_t<double>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
-                 : launch_scan_t<double>(p, a, ws, S(stream));
+    e = local      ? launch_scan_local_t<double>(a, ws, S(stream))
+        : one_pass ? launch_scan_1p_t<double>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
+                   : launch_scan_t<double>(p, a, ws, S(stream));
   } else {
     ScanArgs<float> a{(const float *)e0, (const float *)e1, (const float *)e2, (const float *)e3,
                       (const float *)u, (const float *)s0, (float *)out, T, D};
     a.probe = h_probe;
     a.probe_n = h_probe_n;
-    e = one_pass ? launch_scan_1p_t<float>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
-                 : launch_scan_t<float>(p, a, ws, S(stream));
+    e = local      ? launch_scan_local_t<float>(a, ws, S(stream))
+        : one_pass ? launch_scan_1p_t<float>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
+                   : launch_scan_t<float>(p, a, ws, S(stream));
   }
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "scan launch");
 }

@@ -1837,6 +1837,248 @@ scan_rows_1p(ScanArgs<ST> a, LookbackWs ws, int R, int64_t ntiles) {
   if (tid == 0) bulk_wait_read();
 }
 
+// ---------------------------------------------------------------------------
+// Local-scan + fix-up row scan (plain diag, D <= 64; CS_SCAN_1P=3).  Every CTA
+// owns one contiguous range of rows and scans it from a zero state in one
+// streaming pass (j, u in by bulk copy, the local states s~ out by bulk
+// store), recording the range aggregate (P = prod a, s~ at the end) and, per
+// tile while P is not yet exactly zero, P at the tile start.  One CTA chains
+// the ranges' entries (e_g, a fixed sequential walk), and a fix-up pass adds
+// P_t e_g to the rows of each range's leading tiles: x_t = s~_t + P_t e_g.  P
+// is carried in f64, so for a contracting map it reaches exactly zero after a
+// few thousand rows and every later row is already final -- HBM moves j, u
+// once and s once plus the fixed-up prefix of each range.
+struct LocalWs {
+  double *ragg;    // [G][D][2]  (P, s~ at the range end)
+  double *rentry;  // [G][D]
+  int *nfix;       // [G]       leading tiles with some P != 0
+  double *tileP;   // [G][tmax][D]  P at each such tile's start
+};
+
+template <typename ST>
+struct LocalStream {  // double-buffered bulk-copy stream of row tiles through shared memory
+  ST *buf;
+  size_t be;
+  uint64_t *bar;
+  unsigned use[2];
+  int D;
+  bool aligned;  // 16-byte aligned arrays: bulk copies, else plain loads / stores
+  CS_D ST *jt(int k) const { return buf + (size_t)k * 2 * be; }
+  CS_D ST *ut(int k) const { return buf + (size_t)k * 2 * be + be; }
+  CS_D unsigned issue(const ST *j, const ST *u, int64_t row0, int rows, int k) const {
+    const unsigned bulk = aligned ? (unsigned)(((size_t)rows * D * sizeof(ST)) & ~(size_t)15) : 0u;
+    if (threadIdx.x == 0 && bulk) {
+      mbar_expect_tx(&bar[k], 2 * bulk);
+      bulk_g2s(jt(k), j + row0 * D, bulk, &bar[k]);
+      bulk_g2s(ut(k), u + row0 * D, bulk, &bar[k]);
+    }
+    return bulk;
+  }
+  CS_D void land(const ST *j, const ST *u, int64_t row0, int rows, int k, unsigned bulk) {
+    const int n = rows * D, nb = (int)(bulk / sizeof(ST));
+    for (int i = nb + threadIdx.x; i < n; i += kScanThreads) {
+      jt(k)[i] = j[row0 * D + i];
+      ut(k)[i] = u[row0 * D + i];
+    }
+    if (bulk) mbar_wait(&bar[k], use[k]++ & 1);
+    __syncthreads();
+  }
+  CS_D void store(ST *out, int64_t row0, int rows, int k, unsigned bulk) const {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0 && bulk) {
+      bulk_s2g(out + row0 * D, ut(k), bulk);
+      bulk_commit();
+    }
+    const int n = rows * D, nb = (int)(bulk / sizeof(ST));
+    for (int i = nb + threadIdx.x; i < n; i += kScanThreads) out[row0 * D + i] = ut(k)[i];
+  }
+};
+
+CS_D void local_range(int64_t T, int G, int g, int64_t &lo, int64_t &hi) {  // 4-row aligned balanced split
+  lo = (T * g / G) & ~(int64_t)3;
+  hi = g == G - 1 ? T : (T * (g + 1) / G) & ~(int64_t)3;
+}
+
+template <typename ST>
+__global__ void __launch_bounds__(kScanThreads, 2)
+scan_local(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
+  using CT = ST;
+  constexpr int W = 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double s_x[64], s_P[64];
+  __shared__ int s_nz;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  const int D = a.D, tid = threadIdx.x, G = gridDim.x, g = blockIdx.x;
+  const size_t be = (size_t)B * D;
+  LocalStream<ST> S{(ST *)smem_raw, be, s_bar, {0u, 0u}, D, aligned};
+  double *sa = (double *)(S.buf + 4 * be);  // f64 segment aggregates: P and the range exits stay exact products
+  const int nseg = kScanThreads / D, c = tid % D, sg = tid / D;
+  const bool active = sg < nseg;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  if (tid < D) {
+    s_x[tid] = 0.0;
+    s_P[tid] = 1.0;
+  }
+  __syncthreads();
+  int64_t lo, hi;
+  local_range(a.T, G, g, lo, hi);
+  const int nblk = (int)((hi - lo + B - 1) / B);
+  int nfix = 0;
+  bool nz = true;  // some column's P is still nonzero
+  unsigned bk[2] = {0u, 0u};
+  if (nblk > 0) bk[0] = S.issue(a.e0, a.u, lo, (int)(hi - lo < B ? hi - lo : B), 0);
+  for (int k = 0; k < nblk; ++k) {
+    const int64_t row0 = lo + (int64_t)k * B;
+    const int rows = (int)(hi - row0 < B ? hi - row0 : B);
+    const int kb = k & 1;
+    if (k + 1 < nblk) {
+      if (tid == 0) bulk_wait_read();
+      __syncthreads();
+      const int64_t rn = row0 + B;
+      bk[kb ^ 1] = S.issue(a.e0, a.u, rn, (int)(hi - rn < B ? hi - rn : B), kb ^ 1);
+    }
+    if (nz) {
+      if (tid < D) ws.tileP[((size_t)g * tmax + k) * D + tid] = s_P[tid];
+      nfix = k + 1;
+    }
+    S.land(a.e0, a.u, row0, rows, kb, bk[kb]);
+    ST *jt = S.jt(kb), *ut = S.ut(kb);
+    const int rs = (rows + nseg - 1) / nseg, r0 = sg * rs, r1 = min(rows, r0 + rs);
+    if (active) {
+      SegE<SCAN_DIAG, double> run;
+      run.ident();
+      for (int r = r0; r < r1; ++r) {
+        SegE<SCAN_DIAG, double> e;
+        e.j = (double)jt[r * D + c];
+        e.u = (double)ut[r * D + c];
+        run.push(e);
+      }
+      run.store(sa + (sg * D + c) * W);
+    }
+    __syncthreads();
+    if (active) {  // replay from the local running state
+      double xe = s_x[c];
+      for (int q = 0; q < sg; ++q) {  // the segments before this one, in order (f64)
+        SegE<SCAN_DIAG, double> x;
+        x.load(sa + (q * D + c) * W);
+        x.apply(xe);
+      }
+      CT x = (CT)xe;
+      for (int r = r0; r < r1; ++r) {
+        x = jt[r * D + c] * x + ut[r * D + c];
+        ut[r * D + c] = (ST)x;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) s_nz = 0;
+    __syncthreads();
+    if (tid < D) {  // the tile's exit (segments in order, f64) and P through it
+      double xv = s_x[tid], P = s_P[tid];
+      for (int q = 0; q < nseg; ++q) {
+        SegE<SCAN_DIAG, double> e;
+        e.load(sa + (q * D + tid) * W);
+        e.apply(xv);
+        P *= e.j;
+      }
+      s_x[tid] = xv;
+      s_P[tid] = P;
+      if (P != 0.0) s_nz = 1;
+    }
+    S.store(a.out, row0, rows, kb, bk[kb]);
+    __syncthreads();
+    nz = s_nz != 0;
+  }
+  if (tid == 0) bulk_wait_read();
+  if (tid < D) {
+    ws.ragg[((size_t)g * D + tid) * W] = s_P[tid];
+    ws.ragg[((size_t)g * D + tid) * W + 1] = s_x[tid];
+  }
+  if (tid == 0) ws.nfix[g] = nfix;
+}
+
+// entries of the ranges: e_0 = s0, e_{g+1} = P_g e_g + s~_g (one thread per column, in order)
+template <typename ST>
+__global__ void scan_local_carry(const ST *s0, LocalWs ws, int G, int D) {
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    double e = (double)s0[c];
+    for (int g = 0; g < G; ++g) {
+      ws.rentry[(size_t)g * D + c] = e;
+      e = ws.ragg[((size_t)g * D + c) * 2] * e + ws.ragg[((size_t)g * D + c) * 2 + 1];
+    }
+  }
+}
+
+// x_t = s~_t + P_t e_g over each range's leading tiles (P_t = P at the tile start
+// times the a's of the rows up to t, f64)
+template <typename ST>
+__global__ void __launch_bounds__(kScanThreads, 2)
+scan_local_fixup(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ double s_pre[kScanThreads];  // [seg][col] P at the segment start (nseg * D <= 256)
+  const int D = a.D, tid = threadIdx.x, G = gridDim.x, g = blockIdx.x;
+  const size_t be = (size_t)B * D;
+  LocalStream<ST> S{(ST *)smem_raw, be, s_bar, {0u, 0u}, D, aligned};
+  const int nseg = kScanThreads / D, c = tid % D, sg = tid / D;
+  const bool active = sg < nseg;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int64_t lo, hi;
+  local_range(a.T, G, g, lo, hi);
+  const int nblk = ws.nfix[g];
+  const double e = active ? ws.rentry[(size_t)g * D + c] : 0.0;
+  unsigned bk[2] = {0u, 0u};
+  // j in, the local states (a.out) in the u slot, fixed states back out
+  if (nblk > 0) bk[0] = S.issue(a.e0, a.out, lo, (int)(hi - lo < B ? hi - lo : B), 0);
+  for (int k = 0; k < nblk; ++k) {
+    const int64_t row0 = lo + (int64_t)k * B;
+    const int rows = (int)(hi - row0 < B ? hi - row0 : B);
+    const int kb = k & 1;
+    if (k + 1 < nblk) {
+      if (tid == 0) bulk_wait_read();
+      __syncthreads();
+      const int64_t rn = row0 + B;
+      bk[kb ^ 1] = S.issue(a.e0, a.out, rn, (int)(hi - rn < B ? hi - rn : B), kb ^ 1);
+    }
+    S.land(a.e0, a.out, row0, rows, kb, bk[kb]);
+    ST *jt = S.jt(kb), *xt = S.ut(kb);
+    const int rs = (rows + nseg - 1) / nseg, r0 = sg * rs, r1 = min(rows, r0 + rs);
+    double pseg = 1.0;
+    if (active)
+      for (int r = r0; r < r1; ++r) pseg *= (double)jt[r * D + c];
+    if (active) s_pre[sg * D + c] = pseg;
+    __syncthreads();
+    if (tid < D) {  // exclusive products over the segments, from the tile's recorded start
+      double P = ws.tileP[((size_t)g * tmax + k) * D + tid];
+      for (int q = 0; q < nseg; ++q) {
+        const double v = s_pre[q * D + tid];
+        s_pre[q * D + tid] = P;
+        P *= v;
+      }
+    }
+    __syncthreads();
+    if (active) {
+      double P = s_pre[sg * D + c];
+      for (int r = r0; r < r1; ++r) {
+        P *= (double)jt[r * D + c];
+        if (e != 0.0) xt[r * D + c] = (ST)((double)xt[r * D + c] + P * e);  // e = 0: nothing to add (even if P overflowed)
+      }
+    }
+    S.store(a.out, row0, rows, kb, bk[kb]);
+    __syncthreads();
+  }
+  if (tid == 0) bulk_wait_read();
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static int env_int(const char *name, int lo, int hi, int dflt) {
@@ -1904,15 +2146,9 @@ static int rows_per_tile(int var, int dtype, int D) {
 // two-pass scan's 1.21 ms -- with j, u moved once (0.83 ms without the
 // look-back, 67 %), each tile's look-back (~5 L2 round trips) is exposed per
 // CTA; see DESIGN.md section 8.
-static bool scan_1p() {
-  static const bool v = [] {
-    const char *e = getenv("CS_SCAN_1P");
-    return e ? atoi(e) != 0 : false;
-  }();
-  return v;
-}
-
-bool scan_1p_eligible(int var, int64_t T, int D) { return scan_1p() && var == SCAN_DIAG && D >= 1 && D <= 64 && T > 0; }
+size_t scan_local_ws_bytes(int dtype, int64_t T, int D);
+bool scan_1p_eligible(int var, int64_t T, int D) { return scan_1p_mode() == 1 && var == SCAN_DIAG && D >= 1 && D <= 64 && T > 0; }
+bool scan_local_eligible(int var, int64_t T, int D) { return scan_1p_mode() == 3 && var == SCAN_DIAG && D >= 1 && D <= 64 && T > 0; }
 
 // tiles of ~kB KB of j + u, R a multiple of 4 so every full tile is whole 16-byte lines
 ScanPlan scan_plan_1p(int var, int dtype, int64_t T, int D) {
@@ -1942,6 +2178,10 @@ size_t scan_ws_bytes(int var, int dtype, int64_t T, int D) {
     const size_t c = scan_plan_1p(var, dtype, T, D).ws_bytes;
     a = a > c ? a : c;
   }
+  if (scan_local_eligible(var, T, D)) {
+    const size_t c = scan_local_ws_bytes(dtype, T, D);
+    a = a > c ? a : c;
+  }
   return a > b ? a : b;
 }
 
@@ -1962,6 +2202,65 @@ cudaError_t launch_scan_1p_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaSt
   scan_rows_1p<ST><<<(unsigned)(p.ntiles < g ? p.ntiles : g), kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles);
   return cudaGetLastError();
 }
+static void local_geom(int dtype, int64_t T, int D, int &G, int &B, int &tmax, size_t &smem) {
+  const int esz = dtype == CS_F64 ? 8 : 4;
+  static const int blk_kb = env_int("CS_SCAN_BLOCK_KB", 4, 48, 48);  // j + u per tile (T = 2^24, D = 18: 24 KB 0.92 ms, 40-48 KB 0.74-0.77 ms)
+  B = (blk_kb * 1024) / (2 * esz * D);
+  B = B / 4 * 4;
+  if (B < 4) B = 4;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // two ranges per SM, each at least four tiles long (short scans: fewer, longer ranges)
+  G = 2 * sms;
+  if ((int64_t)G * 4 * B > T) G = (int)(T / (4 * (int64_t)B));
+  if (G < 1) G = 1;
+  const int64_t maxrows = T / G + 8;
+  tmax = (int)((maxrows + B - 1) / B) + 1;
+  const int nseg = kScanThreads / D;
+  smem = (size_t)4 * B * D * esz + (size_t)nseg * D * 2 * sizeof(double);
+}
+size_t scan_local_ws_bytes(int dtype, int64_t T, int D) {
+  int G, B, tmax;
+  size_t smem;
+  local_geom(dtype, T, D, G, B, tmax, smem);
+  return align_up(sizeof(double) * (size_t)G * D * 2) + align_up(sizeof(double) * (size_t)G * D) +
+         align_up(sizeof(int) * (size_t)G) + align_up(sizeof(double) * (size_t)G * tmax * D);
+}
+template <typename ST>
+cudaError_t launch_scan_local_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
+  int G, B, tmax;
+  size_t smem;
+  local_geom(sizeof(ST) == 8 ? CS_F64 : CS_F32, a.T, a.D, G, B, tmax, smem);
+  unsigned char *b = (unsigned char *)ws;
+  LocalWs w;
+  w.ragg = (double *)b;
+  b += align_up(sizeof(double) * (size_t)G * a.D * 2);
+  w.rentry = (double *)b;
+  b += align_up(sizeof(double) * (size_t)G * a.D);
+  w.nfix = (int *)b;
+  b += align_up(sizeof(int) * (size_t)G);
+  w.tileP = (double *)b;
+  for (auto k : {(const void *)scan_local<ST>, (const void *)scan_local_fixup<ST>}) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const bool al = ((((uintptr_t)a.e0) | ((uintptr_t)a.u) | ((uintptr_t)a.out)) & 15) == 0;
+  scan_local<ST><<<G, kScanThreads, smem, st>>>(a, w, B, tmax, al);
+  scan_local_carry<ST><<<1, 64, 0, st>>>(a.s0, w, G, a.D);
+  scan_local_fixup<ST><<<G, kScanThreads, smem, st>>>(a, w, B, tmax, al);
+  return cudaGetLastError();
+}
+template cudaError_t launch_scan_local_t<float>(ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_scan_local_t<double>(ScanArgs<double>, void *, cudaStream_t);
+int scan_1p_mode() {  // plain diag scans: 3 local scan + fix-up (default), 1 single-pass tiles, 0 two-pass chunks
+  static const int v = [] {
+    const char *e = getenv("CS_SCAN_1P");
+    return e ? atoi(e) : 3;
+  }();
+  return v;
+}
+
 template cudaError_t launch_scan_1p_t<float>(const ScanPlan &, ScanArgs<float>, void *, cudaStream_t);
 template cudaError_t launch_scan_1p_t<double>(const ScanPlan &, ScanArgs<double>, void *, cudaStream_t);
 

@@ -37,9 +37,15 @@ ScanPlan scan_plan(int var, int dtype, int64_t T, int D, bool update = false);
 size_t scan_ws_bytes(int var, int dtype, int64_t T, int D);
 // single-pass row scan for plain diag scans (scan_rows_1p): eligibility, plan, launch
 bool scan_1p_eligible(int var, int64_t T, int D);
+bool scan_local_eligible(int var, int64_t T, int D);
 ScanPlan scan_plan_1p(int var, int dtype, int64_t T, int D);
 template <typename ST>
 cudaError_t launch_scan_1p_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st);
+// local-scan + fix-up row scan (CS_SCAN_1P=3)
+int scan_1p_mode();
+size_t scan_local_ws_bytes(int dtype, int64_t T, int D);
+template <typename ST>
+cudaError_t launch_scan_local_t(ScanArgs<ST> a, void *ws, cudaStream_t st);
 template <typename ST>
 cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update = false);
 // wide dense scans, 8 < D <= 128 (cs_dense.cu)

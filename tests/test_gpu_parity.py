@@ -768,6 +768,40 @@ def test_row_scan_multi_round_vs_oracle(cuda_device, mode, D, T, dtype):
     np.testing.assert_allclose(got, want, atol=tol * 10, rtol=tol)
 
 
+@pytest.mark.parametrize("case", ["unit", "near_unit", "growing", "zero_entry"])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_diag_scan_local_fixup_extremes(cuda_device, case, dtype):
+    # the default plain diag scan scans each CTA range from zero and adds
+    # P_t e_g while P = prod a is nonzero: maps that never contract (j = 1, j
+    # near 1, |j| > 1 in stretches) fix up whole ranges; e = 0 must not turn an
+    # overflowing P into NaN.  Against the sequential recursion in f64.
+    T, D = 600_011, 3
+    rng = np.random.default_rng(11)
+    if case == "unit":
+        j = np.ones((T, D))
+    elif case == "near_unit":
+        j = rng.uniform(0.9995, 1.0, (T, D))
+    elif case == "growing":
+        j = np.where(rng.uniform(size=(T, D)) < 0.5, 1.0005, 0.9995)
+    else:
+        j = rng.uniform(-0.9, 0.9, (T, D))
+    u = rng.normal(size=(T, D)) * (1e-3 if case != "zero_entry" else 1.0)
+    s0 = np.zeros(D) if case == "zero_entry" else rng.normal(size=D)
+    tt = lambda x: torch.as_tensor(x, dtype=dtype, device=cuda_device)
+    jd, ud, sd = (np_(tt(x)).astype(np.float64) for x in (j, u, s0))
+    want = np.empty((T, D))
+    x = sd.copy()
+    for t in range(T):  # numpy row loop over D = 3 columns
+        x = jd[t] * x + ud[t]
+        want[t] = x
+    got = np_(cs.parallel_affine_solve(cs.DiagElements(tt(j), tt(u)), tt(s0)))
+    assert np.all(np.isfinite(got))
+    tol = 1e-9 if dtype == torch.float64 else 2e-4
+    np.testing.assert_allclose(got, want, rtol=tol, atol=tol * max(1.0, float(np.abs(want).max())))
+    again = cs.parallel_affine_solve(cs.DiagElements(tt(j), tt(u)), tt(s0))
+    assert torch.equal(again, tt(got)) or np.array_equal(np_(again), got)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("D,T", [(1, 3_000_017), (2, 1_000_003), (4, 700_001), (2, 3071), (4, 5)])
 def test_small_d_row_scan_coalesced_path(cuda_device, D, T):
