@@ -421,7 +421,7 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
                        (const double *)u, (const double *)s0, (double *)out, T, D};
     a.probe = h_probe;
     a.probe_n = h_probe_n;
-    e = local      ? launch_scan_local_t<double>(a, ws, S(stream))
+    e = local      ? launch_scan_local_t<double, false>(a, ws, S(stream))
         : one_pass ? launch_scan_1p_t<double>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
                    : launch_scan_t<double>(p, a, ws, S(stream));
   } else {
@@ -429,7 +429,7 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
                       (const float *)u, (const float *)s0, (float *)out, T, D};
     a.probe = h_probe;
     a.probe_n = h_probe_n;
-    e = local      ? launch_scan_local_t<float>(a, ws, S(stream))
+    e = local      ? launch_scan_local_t<float, false>(a, ws, S(stream))
         : one_pass ? launch_scan_1p_t<float>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
                    : launch_scan_t<float>(p, a, ws, S(stream));
   }
@@ -798,17 +798,23 @@ static int do_scan_update(int var, int dtype, const void *e0, const void *e1, co
   const ScanPlan p = scan_plan(var, dtype, T, D, true);
   if (ws_bytes < p.ws_bytes) return fail(CS_ERR_CONFIG, "scan workspace too small");
   if (T == 0) return CS_OK;
+  // very long diag scans: the local scan + fix-up with the bookkeeping on each tile's
+  // final states.  Newton iterates' maps often contract slowly, so the fix-up covers
+  // much of each range and the two-pass scan stays ahead at moderate T (cfg 5, T = 1M:
+  // 79.0 -> 83.9 ms per solve with the local scan)
+  const bool local = T >= ((int64_t)1 << 22) && scan_local_eligible(var, T, D) &&
+                     ws_bytes >= scan_local_ws_bytes(dtype, T, D);
   cudaError_t e;
   if (dtype == CS_F64) {
     ScanArgs<double> a{(const double *)e0, (const double *)e1, (const double *)e2, (const double *)e3,
                        (const double *)u, (const double *)s0, (double *)out, T, D, (const double *)guess,
                        atol, rtol, it, last_fail, stats};
-    e = launch_scan_t<double>(p, a, ws, S(stream), true);
+    e = local ? launch_scan_local_t<double, true>(a, ws, S(stream)) : launch_scan_t<double>(p, a, ws, S(stream), true);
   } else {
     ScanArgs<float> a{(const float *)e0, (const float *)e1, (const float *)e2, (const float *)e3,
                       (const float *)u, (const float *)s0, (float *)out, T, D, (const float *)guess,
                       atol, rtol, it, last_fail, stats};
-    e = launch_scan_t<float>(p, a, ws, S(stream), true);
+    e = local ? launch_scan_local_t<float, true>(a, ws, S(stream)) : launch_scan_t<float>(p, a, ws, S(stream), true);
   }
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "scan update launch");
 }

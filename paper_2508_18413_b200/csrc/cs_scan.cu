@@ -1895,12 +1895,46 @@ struct LocalStream {  // double-buffered bulk-copy stream of row tiles through s
   }
 };
 
+// fused Newton bookkeeping (deer.py:273-277) on a tile whose states are final:
+// rows with any |x - guess| > atol + rtol |x| get last_fail = it; fail-row count
+// and max gap into the stats record (the scan_rows UPDATE semantics)
+template <typename ST>
+CS_D void local_bookkeep(const ScanArgs<ST> &a, const ST *xt, int64_t row0, int rows, int *s_fail,
+                         unsigned long long *s_dm) {
+  const int D = a.D, tid = threadIdx.x, lane = tid & 31;
+  for (int r = tid; r < rows; r += kScanThreads) s_fail[r] = 0;
+  if (tid == 0) *s_dm = 0ull;
+  __syncthreads();
+  unsigned long long dmb = 0ull;
+  const ST *gb = a.guess + row0 * D;
+  for (int i = tid; i < rows * D; i += kScanThreads) {
+    const double xv = (double)xt[i];
+    const double gap = fabs(xv - (double)gb[i]);
+    if (gap > a.atol + a.rtol * fabs(xv)) s_fail[i / D] = 1;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(gap);
+    dmb = bits > dmb ? bits : dmb;
+  }
+  dmb = warp_max_u64(dmb);
+  if (lane == 0) atomicMax(s_dm, dmb);
+  __syncthreads();
+  unsigned nf = 0;
+  for (int r = tid; r < rows; r += kScanThreads)
+    if (s_fail[r]) {
+      a.last_fail[row0 + r] = a.it;
+      ++nf;
+    }
+  nf = (unsigned)warp_sum_i((int)nf);
+  if (lane == 0 && nf) atomicAdd(&a.stats->fail_rows, nf);
+  if (tid == 0) atomicMax((unsigned long long *)&a.stats->dmax, *s_dm);
+  __syncthreads();
+}
+
 CS_D void local_range(int64_t T, int G, int g, int64_t &lo, int64_t &hi) {  // 4-row aligned balanced split
   lo = (T * g / G) & ~(int64_t)3;
   hi = g == G - 1 ? T : (T * (g + 1) / G) & ~(int64_t)3;
 }
 
-template <typename ST>
+template <typename ST, bool UPD = false>
 __global__ void __launch_bounds__(kScanThreads, 2)
 scan_local(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
   using CT = ST;
@@ -1908,11 +1942,13 @@ scan_local(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double s_x[64], s_P[64];
   __shared__ int s_nz;
+  __shared__ unsigned long long s_dm;
   __shared__ __align__(8) uint64_t s_bar[2];
   const int D = a.D, tid = threadIdx.x, G = gridDim.x, g = blockIdx.x;
   const size_t be = (size_t)B * D;
   LocalStream<ST> S{(ST *)smem_raw, be, s_bar, {0u, 0u}, D, aligned};
   double *sa = (double *)(S.buf + 4 * be);  // f64 segment aggregates: P and the range exits stay exact products
+  int *s_fail = (int *)(sa + 2 * (kScanThreads / D) * D);  // UPD: one flag per tile row
   const int nseg = kScanThreads / D, c = tid % D, sg = tid / D;
   const bool active = sg < nseg;
   if (tid == 0) {
@@ -1942,6 +1978,7 @@ scan_local(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
       const int64_t rn = row0 + B;
       bk[kb ^ 1] = S.issue(a.e0, a.u, rn, (int)(hi - rn < B ? hi - rn : B), kb ^ 1);
     }
+    const bool fixed_later = nz;  // this tile's states get P e added by the fix-up pass
     if (nz) {
       if (tid < D) ws.tileP[((size_t)g * tmax + k) * D + tid] = s_P[tid];
       nfix = k + 1;
@@ -1989,6 +2026,9 @@ scan_local(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
       s_P[tid] = P;
       if (P != 0.0) s_nz = 1;
     }
+    if constexpr (UPD) {
+      if (!fixed_later) local_bookkeep(a, (const ST *)ut, row0, rows, s_fail, &s_dm);  // these states are final
+    }
     S.store(a.out, row0, rows, kb, bk[kb]);
     __syncthreads();
     nz = s_nz != 0;
@@ -2004,22 +2044,35 @@ scan_local(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
 // entries of the ranges: e_0 = s0, e_{g+1} = P_g e_g + s~_g (one thread per column, in order)
 template <typename ST>
 __global__ void scan_local_carry(const ST *s0, LocalWs ws, int G, int D) {
+  constexpr int KB = 32;  // range aggregates in flight per round trip, then applied in order
   for (int c = threadIdx.x; c < D; c += blockDim.x) {
     double e = (double)s0[c];
-    for (int g = 0; g < G; ++g) {
-      ws.rentry[(size_t)g * D + c] = e;
-      e = ws.ragg[((size_t)g * D + c) * 2] * e + ws.ragg[((size_t)g * D + c) * 2 + 1];
+    for (int g0 = 0; g0 < G; g0 += KB) {
+      double A[KB], Bv[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k)
+        if (g0 + k < G) {
+          A[k] = ws.ragg[((size_t)(g0 + k) * D + c) * 2];
+          Bv[k] = ws.ragg[((size_t)(g0 + k) * D + c) * 2 + 1];
+        }
+#pragma unroll
+      for (int k = 0; k < KB; ++k)
+        if (g0 + k < G) {
+          ws.rentry[(size_t)(g0 + k) * D + c] = e;
+          e = A[k] * e + Bv[k];
+        }
     }
   }
 }
 
 // x_t = s~_t + P_t e_g over each range's leading tiles (P_t = P at the tile start
 // times the a's of the rows up to t, f64)
-template <typename ST>
+template <typename ST, bool UPD = false>
 __global__ void __launch_bounds__(kScanThreads, 2)
 scan_local_fixup(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ unsigned long long s_dm;
   __shared__ double s_pre[kScanThreads];  // [seg][col] P at the segment start (nseg * D <= 256)
   const int D = a.D, tid = threadIdx.x, G = gridDim.x, g = blockIdx.x;
   const size_t be = (size_t)B * D;
@@ -2072,6 +2125,10 @@ scan_local_fixup(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
         P *= (double)jt[r * D + c];
         if (e != 0.0) xt[r * D + c] = (ST)((double)xt[r * D + c] + P * e);  // e = 0: nothing to add (even if P overflowed)
       }
+    }
+    if constexpr (UPD) {
+      __syncthreads();
+      local_bookkeep(a, (const ST *)xt, row0, rows, (int *)(S.buf + 4 * be), &s_dm);
     }
     S.store(a.out, row0, rows, kb, bk[kb]);
     __syncthreads();
@@ -2148,7 +2205,16 @@ static int rows_per_tile(int var, int dtype, int D) {
 // CTA; see DESIGN.md section 8.
 size_t scan_local_ws_bytes(int dtype, int64_t T, int D);
 bool scan_1p_eligible(int var, int64_t T, int D) { return scan_1p_mode() == 1 && var == SCAN_DIAG && D >= 1 && D <= 64 && T > 0; }
-bool scan_local_eligible(int var, int64_t T, int D) { return scan_1p_mode() == 3 && var == SCAN_DIAG && D >= 1 && D <= 64 && T > 0; }
+// long scans only: each range's fixed-up prefix (until P underflows) and the
+// three launches are amortised from ~2M steps on (T = 1M, D = 18: two-pass
+// 0.127 ms vs 0.164; T = 4M: 0.344 vs 0.287; T = 16M: 1.21 vs 0.77)
+bool scan_local_eligible(int var, int64_t T, int D) {
+  static const int64_t min_t = [] {
+    const char *e = getenv("CS_SCAN_LOCAL_MIN_T");
+    return e ? (int64_t)atoll(e) : ((int64_t)1 << 19);
+  }();
+  return scan_1p_mode() == 3 && var == SCAN_DIAG && D >= 1 && D <= 64 && T >= min_t && T > 0;
+}
 
 // tiles of ~kB KB of j + u, R a multiple of 4 so every full tile is whole 16-byte lines
 ScanPlan scan_plan_1p(int var, int dtype, int64_t T, int D) {
@@ -2218,7 +2284,7 @@ static void local_geom(int dtype, int64_t T, int D, int &G, int &B, int &tmax, s
   const int64_t maxrows = T / G + 8;
   tmax = (int)((maxrows + B - 1) / B) + 1;
   const int nseg = kScanThreads / D;
-  smem = (size_t)4 * B * D * esz + (size_t)nseg * D * 2 * sizeof(double);
+  smem = (size_t)4 * B * D * esz + (size_t)nseg * D * 2 * sizeof(double) + sizeof(int) * (size_t)B;  // + UPD row flags
 }
 size_t scan_local_ws_bytes(int dtype, int64_t T, int D) {
   int G, B, tmax;
@@ -2227,7 +2293,7 @@ size_t scan_local_ws_bytes(int dtype, int64_t T, int D) {
   return align_up(sizeof(double) * (size_t)G * D * 2) + align_up(sizeof(double) * (size_t)G * D) +
          align_up(sizeof(int) * (size_t)G) + align_up(sizeof(double) * (size_t)G * tmax * D);
 }
-template <typename ST>
+template <typename ST, bool UPD>
 cudaError_t launch_scan_local_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
   int G, B, tmax;
   size_t smem;
@@ -2241,18 +2307,20 @@ cudaError_t launch_scan_local_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
   w.nfix = (int *)b;
   b += align_up(sizeof(int) * (size_t)G);
   w.tileP = (double *)b;
-  for (auto k : {(const void *)scan_local<ST>, (const void *)scan_local_fixup<ST>}) {
+  for (auto k : {(const void *)scan_local<ST, UPD>, (const void *)scan_local_fixup<ST, UPD>}) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   const bool al = ((((uintptr_t)a.e0) | ((uintptr_t)a.u) | ((uintptr_t)a.out)) & 15) == 0;
-  scan_local<ST><<<G, kScanThreads, smem, st>>>(a, w, B, tmax, al);
+  scan_local<ST, UPD><<<G, kScanThreads, smem, st>>>(a, w, B, tmax, al);
   scan_local_carry<ST><<<1, 64, 0, st>>>(a.s0, w, G, a.D);
-  scan_local_fixup<ST><<<G, kScanThreads, smem, st>>>(a, w, B, tmax, al);
+  scan_local_fixup<ST, UPD><<<G, kScanThreads, smem, st>>>(a, w, B, tmax, al);
   return cudaGetLastError();
 }
-template cudaError_t launch_scan_local_t<float>(ScanArgs<float>, void *, cudaStream_t);
-template cudaError_t launch_scan_local_t<double>(ScanArgs<double>, void *, cudaStream_t);
+template cudaError_t launch_scan_local_t<float, false>(ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_scan_local_t<double, false>(ScanArgs<double>, void *, cudaStream_t);
+template cudaError_t launch_scan_local_t<float, true>(ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_scan_local_t<double, true>(ScanArgs<double>, void *, cudaStream_t);
 int scan_1p_mode() {  // plain diag scans: 3 local scan + fix-up (default), 1 single-pass tiles, 0 two-pass chunks
   static const int v = [] {
     const char *e = getenv("CS_SCAN_1P");

@@ -44,7 +44,7 @@ cudaError_t launch_scan_1p_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaSt
 // local-scan + fix-up row scan (CS_SCAN_1P=3)
 int scan_1p_mode();
 size_t scan_local_ws_bytes(int dtype, int64_t T, int D);
-template <typename ST>
+template <typename ST, bool UPD>
 cudaError_t launch_scan_local_t(ScanArgs<ST> a, void *ws, cudaStream_t st);
 template <typename ST>
 cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update = false);

@@ -775,7 +775,7 @@ def test_diag_scan_local_fixup_extremes(cuda_device, case, dtype):
     # P_t e_g while P = prod a is nonzero: maps that never contract (j = 1, j
     # near 1, |j| > 1 in stretches) fix up whole ranges; e = 0 must not turn an
     # overflowing P into NaN.  Against the sequential recursion in f64.
-    T, D = 600_011, 3
+    T, D = 2_200_011, 3  # above the local scan's 2^21 threshold
     rng = np.random.default_rng(11)
     if case == "unit":
         j = np.ones((T, D))
@@ -789,11 +789,7 @@ def test_diag_scan_local_fixup_extremes(cuda_device, case, dtype):
     s0 = np.zeros(D) if case == "zero_entry" else rng.normal(size=D)
     tt = lambda x: torch.as_tensor(x, dtype=dtype, device=cuda_device)
     jd, ud, sd = (np_(tt(x)).astype(np.float64) for x in (j, u, s0))
-    want = np.empty((T, D))
-    x = sd.copy()
-    for t in range(T):  # numpy row loop over D = 3 columns
-        x = jd[t] * x + ud[t]
-        want[t] = x
+    want = O.parallel_affine_solve(O.DiagElements(jd, ud), sd, workers=8)
     got = np_(cs.parallel_affine_solve(cs.DiagElements(tt(j), tt(u)), tt(s0)))
     assert np.all(np.isfinite(got))
     tol = 1e-9 if dtype == torch.float64 else 2e-4
