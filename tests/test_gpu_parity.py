@@ -823,16 +823,19 @@ def test_small_d_row_scan_coalesced_path(cuda_device, D, T):
     np.testing.assert_allclose(np_(aligned), want, atol=2e-4, rtol=2e-5)
 
 
-@pytest.mark.parametrize("D,misalign", [(18, False), (1, False), (2, False), (4, False), (2, True), (4, True)])
-def test_update_scan_bookkeeping_multi_round(cuda_device, D, misalign):
+@pytest.mark.parametrize("D,misalign,T", [(18, False, 3_000_001), (1, False, 3_000_001), (2, False, 3_000_001),
+                                         (4, False, 3_000_001), (2, True, 3_000_001), (4, True, 3_000_001),
+                                         (18, False, 4_200_001), (2, True, 4_200_001)])
+def test_update_scan_bookkeeping_multi_round(cuda_device, D, misalign, T):
     # the replay's fused bookkeeping (deer.py:273-277) at a multi-round size:
     # last_fail stamps, fail_rows and dmax against a direct evaluation.  D = 1,
     # 2, 4 take the coalesced 16-byte stage loads; a one-float offset of j and
-    # u forces the per-column fallback, ragged last stage included
+    # u forces the per-column fallback, ragged last stage included.  T > 2^22:
+    # the local scan + fix-up with the bookkeeping on each tile's final states
     from paper_2508_18413_b200 import _lib
 
     lib = _lib.load()
-    T, it = 3_000_001, 7
+    it = 7
     g = torch.Generator(device=cuda_device).manual_seed(3 + D)
     off = 1 if misalign else 0
     jb = (torch.rand((T * D + off,), generator=g, device=cuda_device) * 1.9 - 0.95).float()
