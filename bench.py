@@ -443,9 +443,11 @@ def scan_roofline(cs, dev, hbm, src):
     byts = 12 * T * D
     ach = byts / (ms / 1e3) / 1e9
     return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-            "traffic": traffic(f"scan_rows_diag_f32_T{T}_D{D}"),
-            "kernel": "cs::scan_rows<float,DIAG>", "T": T, "D": D, "ms": ms, "peak_source": src,
-            "algorithmic_bytes": byts}
+            "traffic": traffic(f"scan_local_diag_f32_T{T}_D{D}"),
+            "kernel": "cs::scan_local<float> + scan_local_carry + scan_local_fixup (one scan)", "T": T, "D": D,
+            "ms": ms, "peak_source": src, "algorithmic_bytes": byts,
+            "note": "local scan per CTA range (j, u read once, s written once) + f64-exact fix-up of each "
+                    "range's leading tiles while prod a != 0; profiles/r02_ncu_scan_local_T16M_D18.md"}
 
 
 def cpu_baseline_sample(args):
