@@ -90,10 +90,10 @@ __global__ void __launch_bounds__(256) k_blr_epilogue(double *E, const double *y
 #pragma unroll 4
     for (int n = lane; n < N; n += 32) {
       const double eta = er[n], yn = __ldg(y + n);
-      const double em = exp(-eta);
-      const double p = 1.0 / (1.0 + em);  // expit / torch.sigmoid
+      double p, lae;
+      sigmoid_logaddexp(eta, p, lae);  // expit, logaddexp(0, eta)
       a += eta * yn;
-      b += eta != eta ? eta : fmax(eta, 0.0) + log1p(eta >= 0.0 ? em : exp(eta));  // logaddexp(0, eta)
+      b += lae;
       er[n] = yn - p;
       const double w = p * (1.0 - p);
       if (wout) wout[r * N + n] = w;

@@ -158,10 +158,10 @@ CS_D void blr_pass(const double *Qs, double *Xs, double *Ps, const double *X, co
           continue;
         }
         const double eta = *ps;
-        const double em = exp(-eta);
-        const double p = 1.0 / (1.0 + em);  // expit / torch.sigmoid
+        double p, lae;
+        sigmoid_logaddexp(eta, p, lae);  // expit, logaddexp(0, eta)
         ra[q] += eta * yn;
-        rb[q] += eta != eta ? eta : fmax(eta, 0.0) + log1p(eta >= 0.0 ? em : exp(eta));  // logaddexp(0, eta)
+        rb[q] += lae;
         *ps = yn - p;
         const double w = p * (1.0 - p);
         for (int k = 0; k < K; ++k) ps[(size_t)(k + 1) * TS * kFPL] *= w;

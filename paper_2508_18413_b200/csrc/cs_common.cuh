@@ -79,7 +79,21 @@ CS_D double sigmoid_prime(double z) {
   const double q = 1.0 + e;
   return e / (q * q);
 }
-CS_D double expit(double x) { return 1.0 / (1.0 + exp(-x)); }             // scipy.special.expit
+CS_D double expit(double x) { return 1.0 / (1.0 + exp(-x)); }
+// sigmoid(x) and logaddexp(0, x) from ONE exponential, t = e^{-|x|}:
+// p = 1 / (1 + t) for x >= 0 and t / (1 + t) below (expit to within an ulp),
+// logaddexp(0, x) = max(x, 0) + log1p(t), numpy's own form (same bits)
+CS_D void sigmoid_logaddexp(double x, double &p, double &lae) {
+  if (x != x) {
+    p = x;
+    lae = x;
+    return;
+  }
+  const double t = exp(-fabs(x));
+  const double r = 1.0 / (1.0 + t);
+  p = x >= 0.0 ? r : t * r;
+  lae = fmax(x, 0.0) + log1p(t);
+}             // scipy.special.expit
 CS_D double clipv(double x, double c) { return fmin(fmax(x, -c), c); }    // np.clip
 
 // ---- atomics ------------------------------------------------------------------

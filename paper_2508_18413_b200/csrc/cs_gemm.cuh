@@ -178,10 +178,10 @@ k_gemm(int M, int N, int K, const TA *__restrict__ A, int64_t lda, int64_t sA, c
           const double v = c[mi][ni][h];
           if constexpr (EPI == 1) {
             const double yn = __ldg(ep.y + gn);
-            const double em = exp(-v);
-            const double p = 1.0 / (1.0 + em);  // expit
+            double p, lae;
+            sigmoid_logaddexp(v, p, lae);  // expit, logaddexp(0, eta)
             pa += v * yn;
-            pb += v != v ? v : fmax(v, 0.0) + log1p(v >= 0.0 ? em : exp(v));  // logaddexp(0, eta)
+            pb += lae;
             C[o] = (TC)(yn - p);
             const double w = p * (1.0 - p);
             if (ep.wout) ep.wout[o] = w;
