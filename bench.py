@@ -310,7 +310,7 @@ def run_gpu(args):
             "kernel": "cs::deer_persistent<Hmc<2,f,Rosenbrock>,DIAG> (whole solve)",
             "peak_source": src, "algorithmic_bytes_per_launch": bytes_per_launch,
             "note": "whole-solve working set (3.6 MB) is L2-resident: the kernel is bound by the grid "
-                    "barrier and dependent f64 leapfrog chains, not HBM (profiles/r01_ncu_hmc_fused_solver.md); "
+                    "barrier and dependent f64 leapfrog chains, not HBM (profiles/r02_ncu_hmc_fused_solver.md); "
                     "the HBM-bound scan is scan_roofline"}
 
     # f64 companion (the reference computes in f64): the same solve, device-resident
