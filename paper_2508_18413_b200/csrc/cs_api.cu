@@ -414,14 +414,17 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
   const bool a16 = ((((uintptr_t)e0) | ((uintptr_t)u) | ((uintptr_t)out)) & 15) == 0;
   const bool one_pass = a16 && scan_1p_eligible(var, T, D) && ws_bytes >= scan_plan_1p(var, dtype, T, D).ws_bytes;
   // (any alignment: the local scan falls back to plain loads for unaligned arrays)
-  const bool local = scan_local_eligible(var, T, D) && ws_bytes >= scan_local_ws_bytes(dtype, T, D);
+  const bool local = scan_local_eligible(var, T, D) &&
+                     ws_bytes >= (var == SCAN_BLOCK ? scan_local_blk_ws_bytes(dtype, T, D)
+                                                    : scan_local_ws_bytes(dtype, T, D));
   cudaError_t e;
   if (dtype == CS_F64) {
     ScanArgs<double> a{(const double *)e0, (const double *)e1, (const double *)e2, (const double *)e3,
                        (const double *)u, (const double *)s0, (double *)out, T, D};
     a.probe = h_probe;
     a.probe_n = h_probe_n;
-    e = local      ? launch_scan_local_t<double, false>(a, ws, S(stream))
+    e = local      ? (var == SCAN_BLOCK ? launch_scan_local_blk_t<double>(a, ws, S(stream))
+                                        : launch_scan_local_t<double, false>(a, ws, S(stream)))
         : one_pass ? launch_scan_1p_t<double>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
                    : launch_scan_t<double>(p, a, ws, S(stream));
   } else {
@@ -429,7 +432,8 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
                       (const float *)u, (const float *)s0, (float *)out, T, D};
     a.probe = h_probe;
     a.probe_n = h_probe_n;
-    e = local      ? launch_scan_local_t<float, false>(a, ws, S(stream))
+    e = local      ? (var == SCAN_BLOCK ? launch_scan_local_blk_t<float>(a, ws, S(stream))
+                                        : launch_scan_local_t<float, false>(a, ws, S(stream)))
         : one_pass ? launch_scan_1p_t<float>(scan_plan_1p(var, dtype, T, D), a, ws, S(stream))
                    : launch_scan_t<float>(p, a, ws, S(stream));
   }
@@ -802,7 +806,7 @@ static int do_scan_update(int var, int dtype, const void *e0, const void *e1, co
   // final states.  Newton iterates' maps often contract slowly, so the fix-up covers
   // much of each range and the two-pass scan stays ahead at moderate T (cfg 5, T = 1M:
   // 79.0 -> 83.9 ms per solve with the local scan)
-  const bool local = T >= ((int64_t)1 << 22) && scan_local_eligible(var, T, D) &&
+  const bool local = T >= ((int64_t)1 << 22) && var == SCAN_DIAG && scan_local_eligible(var, T, D) &&
                      ws_bytes >= scan_local_ws_bytes(dtype, T, D);
   cudaError_t e;
   if (dtype == CS_F64) {

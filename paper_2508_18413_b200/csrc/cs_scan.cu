@@ -2136,6 +2136,324 @@ scan_local_fixup(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
   if (tid == 0) bulk_wait_read();
 }
 
+// ---------------------------------------------------------------------------
+// Block2x2 version of the local scan + fix-up (plain block scans): per column
+// the state is (x, v), the map M_t = (a b; c d) with u_t = (ux, uv); P is the
+// 2 x 2 product of the range's maps (f64), x_t = s~_t + P_t e_g.  Tiles carry
+// a, b, c, d (B x D each) and u (B x 2D, rows [x | v]); the states replace u.
+template <typename ST>
+struct BlkTile {  // the five input slots of one ring buffer
+  ST *a, *b, *c, *d, *u;
+};
+
+template <typename ST>
+CS_D BlkTile<ST> blk_tile(ST *buf, size_t be, int k) {
+  ST *base = buf + (size_t)k * 6 * be;
+  return BlkTile<ST>{base, base + be, base + 2 * be, base + 3 * be, base + 4 * be};
+}
+
+template <typename ST>
+CS_D unsigned blk_issue(const ScanArgs<ST> &a, BlkTile<ST> t, int64_t row0, int rows, uint64_t *bar, bool aligned,
+                        const ST *usrc) {
+  const int D = a.D;
+  const unsigned bh = aligned ? (unsigned)(((size_t)rows * D * sizeof(ST)) & ~(size_t)15) : 0u;
+  const unsigned bu = aligned ? (unsigned)(((size_t)rows * 2 * D * sizeof(ST)) & ~(size_t)15) : 0u;
+  if (threadIdx.x == 0 && bh) {
+    mbar_expect_tx(bar, 4 * bh + bu);
+    bulk_g2s(t.a, a.e0 + row0 * D, bh, bar);
+    bulk_g2s(t.b, a.e1 + row0 * D, bh, bar);
+    bulk_g2s(t.c, a.e2 + row0 * D, bh, bar);
+    bulk_g2s(t.d, a.e3 + row0 * D, bh, bar);
+    bulk_g2s(t.u, usrc + row0 * 2 * D, bu, bar);
+  }
+  return bh;
+}
+
+template <typename ST>
+CS_D void blk_land(const ScanArgs<ST> &a, BlkTile<ST> t, int64_t row0, int rows, unsigned bh, uint64_t *bar,
+                   unsigned &use, const ST *usrc) {
+  const int D = a.D;
+  const int n = rows * D, nb = (int)(bh / sizeof(ST));
+  const int nbu = bh ? (int)((((size_t)rows * 2 * D * sizeof(ST)) & ~(size_t)15) / sizeof(ST)) : 0;
+  for (int i = nb + threadIdx.x; i < n; i += kScanThreads) {
+    t.a[i] = a.e0[row0 * D + i];
+    t.b[i] = a.e1[row0 * D + i];
+    t.c[i] = a.e2[row0 * D + i];
+    t.d[i] = a.e3[row0 * D + i];
+  }
+  for (int i = nbu + threadIdx.x; i < 2 * n; i += kScanThreads) t.u[i] = usrc[row0 * 2 * D + i];
+  if (bh) mbar_wait(bar, use++ & 1);
+  __syncthreads();
+}
+
+template <typename ST>
+CS_D void blk_store(const ScanArgs<ST> &a, BlkTile<ST> t, int64_t row0, int rows, bool aligned) {
+  const int D = a.D;
+  const unsigned bu = aligned ? (unsigned)(((size_t)rows * 2 * D * sizeof(ST)) & ~(size_t)15) : 0u;
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0 && bu) {
+    bulk_s2g(a.out + row0 * 2 * D, t.u, bu);
+    bulk_commit();
+  }
+  const int nb = (int)(bu / sizeof(ST));
+  for (int i = nb + threadIdx.x; i < rows * 2 * D; i += kScanThreads) a.out[row0 * 2 * D + i] = t.u[i];
+}
+
+template <typename ST>
+__global__ void __launch_bounds__(kScanThreads, 2)
+scan_local_blk(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
+  using CT = ST;
+  constexpr int W = 6;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double s_x[64], s_v[64], s_P[4 * 64];
+  __shared__ int s_nz;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  const int D = a.D, tid = threadIdx.x, G = gridDim.x, g = blockIdx.x;
+  const size_t be = (size_t)B * D;
+  ST *buf = (ST *)smem_raw;
+  double *sa = (double *)(buf + 12 * be);  // [nseg][D][6] f64
+  const int nseg = kScanThreads / D, c = tid % D, sg = tid / D;
+  const bool active = sg < nseg;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  if (tid < D) {
+    s_x[tid] = 0.0;
+    s_v[tid] = 0.0;
+    s_P[4 * tid] = 1.0;
+    s_P[4 * tid + 1] = 0.0;
+    s_P[4 * tid + 2] = 0.0;
+    s_P[4 * tid + 3] = 1.0;
+  }
+  __syncthreads();
+  unsigned use[2] = {0u, 0u};
+  int64_t lo, hi;
+  local_range(a.T, G, g, lo, hi);
+  const int nblk = (int)((hi - lo + B - 1) / B);
+  int nfix = 0;
+  bool nz = true;
+  unsigned bk[2] = {0u, 0u};
+  if (nblk > 0) bk[0] = blk_issue(a, blk_tile(buf, be, 0), lo, (int)(hi - lo < B ? hi - lo : B), &s_bar[0], aligned, a.u);
+  for (int k = 0; k < nblk; ++k) {
+    const int64_t row0 = lo + (int64_t)k * B;
+    const int rows = (int)(hi - row0 < B ? hi - row0 : B);
+    const int kb = k & 1;
+    if (k + 1 < nblk) {
+      if (tid == 0) bulk_wait_read();
+      __syncthreads();
+      const int64_t rn = row0 + B;
+      bk[kb ^ 1] = blk_issue(a, blk_tile(buf, be, kb ^ 1), rn, (int)(hi - rn < B ? hi - rn : B), &s_bar[kb ^ 1],
+                             aligned, a.u);
+    }
+    if (nz) {
+      if (tid < 4 * D) ws.tileP[((size_t)g * tmax + k) * 4 * D + tid] = s_P[tid];
+      nfix = k + 1;
+    }
+    BlkTile<ST> t = blk_tile(buf, be, kb);
+    blk_land(a, t, row0, rows, bk[kb], &s_bar[kb], use[kb], a.u);
+    const int rs = (rows + nseg - 1) / nseg, r0 = sg * rs, r1 = min(rows, r0 + rs);
+    if (active) {
+      SegE<SCAN_BLOCK, double> run;
+      run.ident();
+      for (int r = r0; r < r1; ++r) {
+        SegE<SCAN_BLOCK, double> e;
+        e.A = (double)t.a[r * D + c];
+        e.B = (double)t.b[r * D + c];
+        e.C = (double)t.c[r * D + c];
+        e.E = (double)t.d[r * D + c];
+        e.ux = (double)t.u[r * 2 * D + c];
+        e.uv = (double)t.u[r * 2 * D + D + c];
+        run.push(e);
+      }
+      run.store(sa + (sg * D + c) * W);
+    }
+    __syncthreads();
+    if (active) {
+      double xe = s_x[c], ve = s_v[c];
+      for (int q = 0; q < sg; ++q) {
+        SegE<SCAN_BLOCK, double> e;
+        e.load(sa + (q * D + c) * W);
+        e.apply(xe, ve);
+      }
+      CT x = (CT)xe, v = (CT)ve;
+      for (int r = r0; r < r1; ++r) {
+        const CT xa = t.a[r * D + c] * x + t.b[r * D + c] * v + t.u[r * 2 * D + c];
+        const CT va = t.c[r * D + c] * x + t.d[r * D + c] * v + t.u[r * 2 * D + D + c];
+        x = xa;
+        v = va;
+        t.u[r * 2 * D + c] = (ST)x;
+        t.u[r * 2 * D + D + c] = (ST)v;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) s_nz = 0;
+    __syncthreads();
+    if (tid < D) {
+      double xv = s_x[tid], vv = s_v[tid];
+      double p0 = s_P[4 * tid], p1 = s_P[4 * tid + 1], p2 = s_P[4 * tid + 2], p3 = s_P[4 * tid + 3];
+      for (int q = 0; q < nseg; ++q) {
+        SegE<SCAN_BLOCK, double> e;
+        e.load(sa + (q * D + tid) * W);
+        e.apply(xv, vv);
+        const double n0 = e.A * p0 + e.B * p2, n1 = e.A * p1 + e.B * p3;
+        const double n2 = e.C * p0 + e.E * p2, n3 = e.C * p1 + e.E * p3;
+        p0 = n0;
+        p1 = n1;
+        p2 = n2;
+        p3 = n3;
+      }
+      s_x[tid] = xv;
+      s_v[tid] = vv;
+      s_P[4 * tid] = p0;
+      s_P[4 * tid + 1] = p1;
+      s_P[4 * tid + 2] = p2;
+      s_P[4 * tid + 3] = p3;
+      if (p0 != 0.0 || p1 != 0.0 || p2 != 0.0 || p3 != 0.0) s_nz = 1;
+    }
+    blk_store(a, t, row0, rows, aligned);
+    __syncthreads();
+    nz = s_nz != 0;
+  }
+  if (tid == 0) bulk_wait_read();
+  if (tid < D) {
+    double *o = ws.ragg + ((size_t)g * D + tid) * 6;
+    o[0] = s_P[4 * tid];
+    o[1] = s_P[4 * tid + 1];
+    o[2] = s_P[4 * tid + 2];
+    o[3] = s_P[4 * tid + 3];
+    o[4] = s_x[tid];
+    o[5] = s_v[tid];
+  }
+  if (tid == 0) ws.nfix[g] = nfix;
+}
+
+template <typename ST>
+__global__ void scan_local_carry_blk(const ST *s0, LocalWs ws, int G, int D) {
+  constexpr int KB = 8;  // range aggregates in flight per round trip, then applied in order
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    double ex = (double)s0[c], ev = (double)s0[D + c];
+    for (int g0 = 0; g0 < G; g0 += KB) {
+      double r[KB][6];
+#pragma unroll
+      for (int k = 0; k < KB; ++k)
+        if (g0 + k < G)
+#pragma unroll
+          for (int q = 0; q < 6; ++q) r[k][q] = ws.ragg[((size_t)(g0 + k) * D + c) * 6 + q];
+#pragma unroll
+      for (int k = 0; k < KB; ++k)
+        if (g0 + k < G) {
+          ws.rentry[((size_t)(g0 + k) * D + c) * 2] = ex;
+          ws.rentry[((size_t)(g0 + k) * D + c) * 2 + 1] = ev;
+          const double nx = r[k][0] * ex + r[k][1] * ev + r[k][4], nv = r[k][2] * ex + r[k][3] * ev + r[k][5];
+          ex = nx;
+          ev = nv;
+        }
+    }
+  }
+}
+
+template <typename ST>
+__global__ void __launch_bounds__(kScanThreads, 2)
+scan_local_fixup_blk(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ double s_pre[4 * kScanThreads];  // [seg][col][4] P at the segment start
+  const int D = a.D, tid = threadIdx.x, G = gridDim.x, g = blockIdx.x;
+  const size_t be = (size_t)B * D;
+  ST *buf = (ST *)smem_raw;
+  const int nseg = kScanThreads / D, c = tid % D, sg = tid / D;
+  const bool active = sg < nseg;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  unsigned use[2] = {0u, 0u};
+  int64_t lo, hi;
+  local_range(a.T, G, g, lo, hi);
+  const int nblk = ws.nfix[g];
+  const double ex = active ? ws.rentry[((size_t)g * D + c) * 2] : 0.0;
+  const double ev = active ? ws.rentry[((size_t)g * D + c) * 2 + 1] : 0.0;
+  unsigned bk[2] = {0u, 0u};
+  // the local states (a.out) ride in the u slot
+  if (nblk > 0)
+    bk[0] = blk_issue(a, blk_tile(buf, be, 0), lo, (int)(hi - lo < B ? hi - lo : B), &s_bar[0], aligned,
+                      (const ST *)a.out);
+  for (int k = 0; k < nblk; ++k) {
+    const int64_t row0 = lo + (int64_t)k * B;
+    const int rows = (int)(hi - row0 < B ? hi - row0 : B);
+    const int kb = k & 1;
+    if (k + 1 < nblk) {
+      if (tid == 0) bulk_wait_read();
+      __syncthreads();
+      const int64_t rn = row0 + B;
+      bk[kb ^ 1] = blk_issue(a, blk_tile(buf, be, kb ^ 1), rn, (int)(hi - rn < B ? hi - rn : B), &s_bar[kb ^ 1],
+                             aligned, (const ST *)a.out);
+    }
+    BlkTile<ST> t = blk_tile(buf, be, kb);
+    blk_land(a, t, row0, rows, bk[kb], &s_bar[kb], use[kb], (const ST *)a.out);
+    const int rs = (rows + nseg - 1) / nseg, r0 = sg * rs, r1 = min(rows, r0 + rs);
+    double m0 = 1.0, m1 = 0.0, m2 = 0.0, m3 = 1.0;  // the segment's map product
+    if (active) {
+      for (int r = r0; r < r1; ++r) {
+        const double A = (double)t.a[r * D + c], Bq = (double)t.b[r * D + c];
+        const double C = (double)t.c[r * D + c], E = (double)t.d[r * D + c];
+        const double n0 = A * m0 + Bq * m2, n1 = A * m1 + Bq * m3, n2 = C * m0 + E * m2, n3 = C * m1 + E * m3;
+        m0 = n0;
+        m1 = n1;
+        m2 = n2;
+        m3 = n3;
+      }
+      double *sp = s_pre + (sg * D + c) * 4;
+      sp[0] = m0;
+      sp[1] = m1;
+      sp[2] = m2;
+      sp[3] = m3;
+    }
+    __syncthreads();
+    if (tid < D) {  // exclusive products over the segments, from the tile's recorded start
+      const double *tp = ws.tileP + ((size_t)g * tmax + k) * 4 * D + 4 * tid;
+      double p0 = tp[0], p1 = tp[1], p2 = tp[2], p3 = tp[3];
+      for (int q = 0; q < nseg; ++q) {
+        double *sp = s_pre + (q * D + tid) * 4;
+        const double a0 = sp[0], a1 = sp[1], a2 = sp[2], a3 = sp[3];
+        sp[0] = p0;
+        sp[1] = p1;
+        sp[2] = p2;
+        sp[3] = p3;
+        const double n0 = a0 * p0 + a1 * p2, n1 = a0 * p1 + a1 * p3, n2 = a2 * p0 + a3 * p2, n3 = a2 * p1 + a3 * p3;
+        p0 = n0;
+        p1 = n1;
+        p2 = n2;
+        p3 = n3;
+      }
+    }
+    __syncthreads();
+    if (active && (ex != 0.0 || ev != 0.0)) {
+      const double *sp = s_pre + (sg * D + c) * 4;
+      double p0 = sp[0], p1 = sp[1], p2 = sp[2], p3 = sp[3];
+      for (int r = r0; r < r1; ++r) {
+        const double A = (double)t.a[r * D + c], Bq = (double)t.b[r * D + c];
+        const double C = (double)t.c[r * D + c], E = (double)t.d[r * D + c];
+        const double n0 = A * p0 + Bq * p2, n1 = A * p1 + Bq * p3, n2 = C * p0 + E * p2, n3 = C * p1 + E * p3;
+        p0 = n0;
+        p1 = n1;
+        p2 = n2;
+        p3 = n3;
+        t.u[r * 2 * D + c] = (ST)((double)t.u[r * 2 * D + c] + p0 * ex + p1 * ev);
+        t.u[r * 2 * D + D + c] = (ST)((double)t.u[r * 2 * D + D + c] + p2 * ex + p3 * ev);
+      }
+    }
+    blk_store(a, t, row0, rows, aligned);
+    __syncthreads();
+  }
+  if (tid == 0) bulk_wait_read();
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static int env_int(const char *name, int lo, int hi, int dflt) {
@@ -2213,7 +2531,7 @@ bool scan_local_eligible(int var, int64_t T, int D) {
     const char *e = getenv("CS_SCAN_LOCAL_MIN_T");
     return e ? (int64_t)atoll(e) : ((int64_t)1 << 19);
   }();
-  return scan_1p_mode() == 3 && var == SCAN_DIAG && D >= 1 && D <= 64 && T >= min_t && T > 0;
+  return scan_1p_mode() == 3 && (var == SCAN_DIAG || var == SCAN_BLOCK) && D >= 1 && D <= 64 && T >= min_t && T > 0;
 }
 
 // tiles of ~kB KB of j + u, R a multiple of 4 so every full tile is whole 16-byte lines
@@ -2245,7 +2563,7 @@ size_t scan_ws_bytes(int var, int dtype, int64_t T, int D) {
     a = a > c ? a : c;
   }
   if (scan_local_eligible(var, T, D)) {
-    const size_t c = scan_local_ws_bytes(dtype, T, D);
+    const size_t c = var == SCAN_BLOCK ? scan_local_blk_ws_bytes(dtype, T, D) : scan_local_ws_bytes(dtype, T, D);
     a = a > c ? a : c;
   }
   return a > b ? a : b;
@@ -2317,6 +2635,57 @@ cudaError_t launch_scan_local_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
   scan_local_fixup<ST, UPD><<<G, kScanThreads, smem, st>>>(a, w, B, tmax, al);
   return cudaGetLastError();
 }
+static void local_geom_blk(int dtype, int64_t T, int D, int &G, int &B, int &tmax, size_t &smem) {
+  const int esz = dtype == CS_F64 ? 8 : 4;
+  static const int blk_kb = env_int("CS_SCAN_BLOCK_KB", 4, 48, 48);
+  B = (blk_kb * 1024) / (6 * esz * D);  // a, b, c, d, u (2 D): 6 D values per row
+  B = B / 4 * 4;
+  if (B < 4) B = 4;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  G = 2 * sms;
+  if ((int64_t)G * 4 * B > T) G = (int)(T / (4 * (int64_t)B));
+  if (G < 1) G = 1;
+  tmax = (int)((T / G + 8 + B - 1) / B) + 1;
+  const int nseg = kScanThreads / D;
+  smem = (size_t)12 * B * D * esz + (size_t)nseg * D * 6 * sizeof(double);
+}
+size_t scan_local_blk_ws_bytes(int dtype, int64_t T, int D) {
+  int G, B, tmax;
+  size_t smem;
+  local_geom_blk(dtype, T, D, G, B, tmax, smem);
+  return align_up(sizeof(double) * (size_t)G * D * 6) + align_up(sizeof(double) * (size_t)G * D * 2) +
+         align_up(sizeof(int) * (size_t)G) + align_up(sizeof(double) * (size_t)G * tmax * D * 4);
+}
+template <typename ST>
+cudaError_t launch_scan_local_blk_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
+  int G, B, tmax;
+  size_t smem;
+  local_geom_blk(sizeof(ST) == 8 ? CS_F64 : CS_F32, a.T, a.D, G, B, tmax, smem);
+  unsigned char *b = (unsigned char *)ws;
+  LocalWs w;
+  w.ragg = (double *)b;
+  b += align_up(sizeof(double) * (size_t)G * a.D * 6);
+  w.rentry = (double *)b;
+  b += align_up(sizeof(double) * (size_t)G * a.D * 2);
+  w.nfix = (int *)b;
+  b += align_up(sizeof(int) * (size_t)G);
+  w.tileP = (double *)b;
+  for (auto k : {(const void *)scan_local_blk<ST>, (const void *)scan_local_fixup_blk<ST>}) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const bool al = ((((uintptr_t)a.e0) | ((uintptr_t)a.e1) | ((uintptr_t)a.e2) | ((uintptr_t)a.e3) |
+                    ((uintptr_t)a.u) | ((uintptr_t)a.out)) & 15) == 0;
+  scan_local_blk<ST><<<G, kScanThreads, smem, st>>>(a, w, B, tmax, al);
+  scan_local_carry_blk<ST><<<1, 64, 0, st>>>(a.s0, w, G, a.D);
+  scan_local_fixup_blk<ST><<<G, kScanThreads, smem, st>>>(a, w, B, tmax, al);
+  return cudaGetLastError();
+}
+template cudaError_t launch_scan_local_blk_t<float>(ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_scan_local_blk_t<double>(ScanArgs<double>, void *, cudaStream_t);
+
 template cudaError_t launch_scan_local_t<float, false>(ScanArgs<float>, void *, cudaStream_t);
 template cudaError_t launch_scan_local_t<double, false>(ScanArgs<double>, void *, cudaStream_t);
 template cudaError_t launch_scan_local_t<float, true>(ScanArgs<float>, void *, cudaStream_t);

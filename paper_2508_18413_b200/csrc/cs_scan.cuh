@@ -46,6 +46,9 @@ int scan_1p_mode();
 size_t scan_local_ws_bytes(int dtype, int64_t T, int D);
 template <typename ST, bool UPD>
 cudaError_t launch_scan_local_t(ScanArgs<ST> a, void *ws, cudaStream_t st);
+size_t scan_local_blk_ws_bytes(int dtype, int64_t T, int D);
+template <typename ST>
+cudaError_t launch_scan_local_blk_t(ScanArgs<ST> a, void *ws, cudaStream_t st);
 template <typename ST>
 cudaError_t launch_scan_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaStream_t st, bool update = false);
 // wide dense scans, 8 < D <= 128 (cs_dense.cu)

@@ -798,6 +798,24 @@ def test_diag_scan_local_fixup_extremes(cuda_device, case, dtype):
     assert torch.equal(again, tt(got)) or np.array_equal(np_(again), got)
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_block_scan_local_fixup_rotation(cuda_device, dtype):
+    # block2x2 local scan + fix-up with maps that never contract (rotations,
+    # |det| = 1, like a leapfrog step): every range is fixed up end to end
+    T, D = 1_100_003, 2
+    rng = np.random.default_rng(5)
+    th = rng.uniform(-0.05, 0.05, (T, D))
+    a, b, c, d = np.cos(th), -np.sin(th), np.sin(th), np.cos(th)
+    u = rng.normal(size=(T, 2 * D)) * 1e-3
+    s0 = rng.normal(size=2 * D)
+    tt = lambda x: torch.as_tensor(x, dtype=dtype, device=cuda_device)
+    ad, bd, cd, dd, ud, sd = (np_(tt(x)).astype(np.float64) for x in (a, b, c, d, u, s0))
+    want = O.parallel_affine_solve(O.Block2x2Elements(ad, bd, cd, dd, ud), sd, workers=8)
+    got = np_(cs.parallel_affine_solve(cs.Block2x2Elements(tt(a), tt(b), tt(c), tt(d), tt(u)), tt(s0)))
+    tol = 1e-9 if dtype == torch.float64 else 5e-4
+    np.testing.assert_allclose(got, want, rtol=tol, atol=tol * max(1.0, float(np.abs(want).max())))
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("D,T", [(1, 3_000_017), (2, 1_000_003), (4, 700_001), (2, 3071), (4, 5)])
 def test_small_d_row_scan_coalesced_path(cuda_device, D, T):
