@@ -7,9 +7,12 @@
 //   dense     J (T,D,D), u (T,D), D <= 8      -> scan_dense_small<MD>
 // The column and dense scans are single-pass: each tile is read from HBM once,
 // reduced, linked to its predecessors by decoupled look-back, replayed and
-// written once (12 B/element diag f32).  The row scan is two-pass over chunks
-// (A: reduce, C: re-read and replay a round later, see scan_rows): j, u are
-// read twice, 20 B/element of HBM traffic against the 12 B algorithmic.
+// written once (12 B/element diag f32).  Long plain row scans (T >= 2^19) take
+// the local scan + fix-up (scan_local / scan_local_blk): every CTA scans its own
+// range from zero in one streaming pass and only each range's leading tiles are
+// corrected by P e -- j, u read once.  The bookkeeping update scans below 2^22
+// and short scans use the two-pass chunk scan (A: reduce, C: re-read and replay
+// a round later, see scan_rows): 20 B/element of HBM traffic.
 // Carries and composition run in f64 regardless of storage type; every
 // chunk's entry state is the fixed chain exit(k) = A_k(exit(k-1)) from s0
 // (lookback_cta applies aggregates one at a time), so results are bit-
