@@ -18,6 +18,9 @@
 // regression builder ([S; z] X^T and P X, cfg 3 "full") and the dense affine
 // aggregates / D > 128 dense scans (products of augmented maps).
 #pragma once
+#include <cstdlib>
+#include <type_traits>
+
 #include "cs_common.cuh"
 
 namespace cs {
@@ -210,6 +213,91 @@ k_gemm(int M, int N, int K, const TA *__restrict__ A, int64_t lda, int64_t sA, c
   }
 }
 
+// f64, non-transposed operands: the same tiles fed by a 3-stage cp.async ring
+// (global -> shared without a register round trip, two K-steps in flight)
+constexpr int kCpStages = 3;
+CS_D void cp_async8_zfill(void *dst, const void *src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+template <int BM, typename TC>
+__global__ void __launch_bounds__(GemmWarps<BM>::NT)
+k_gemm_cp(int M, int N, int K, const double *__restrict__ A, int64_t lda, int64_t sA, const double *__restrict__ B,
+          int64_t ldb, int64_t sB, TC *__restrict__ C, int64_t ldc, int64_t sC) {
+  using GW = GemmWarps<BM>;
+  constexpr int kBK = GW::BK, kLDA = GW::LDA, NT = GW::NT, MI = GW::MI;
+  constexpr int EA = BM * kBK / NT, EB = kBK * kBN / NT;
+  constexpr int SA = BM * kLDA, SB = kBK * kLDB;
+  extern __shared__ __align__(16) double cp_sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / GW::WN, wn = warp % GW::WN;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * kBN;
+  A += (int64_t)blockIdx.z * sA;
+  B += (int64_t)blockIdx.z * sB;
+  C += (int64_t)blockIdx.z * sC;
+  const int nk = (K + kBK - 1) / kBK;
+  auto issue = [&](int st) {
+    if (st < nk) {
+      double *As = cp_sm + (st % kCpStages) * (SA + SB), *Bs = As + SA;
+      const int k0 = st * kBK;
+#pragma unroll
+      for (int e = 0; e < EA; ++e) {
+        const int i = tid + e * NT, r = i / kBK, k = i % kBK;
+        const int gm = m0 + r, gk = k0 + k;
+        const bool ok = gm < M && gk < K;
+        cp_async8_zfill(As + r * kLDA + k, ok ? A + (int64_t)gm * lda + gk : A, ok);
+      }
+#pragma unroll
+      for (int e = 0; e < EB; ++e) {
+        const int i = tid + e * NT, k = i / kBN, n = i % kBN;
+        const int gn = n0 + n, gk = k0 + k;
+        const bool ok = gn < N && gk < K;
+        cp_async8_zfill(Bs + k * kLDB + n, ok ? B + (int64_t)gk * ldb + gn : B, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double c[MI][MI][2];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < MI; ++ni) c[mi][ni][0] = c[mi][ni][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < kCpStages - 1; ++st) issue(st);
+  for (int s = 0; s < nk; ++s) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kCpStages - 2) : "memory");
+    __syncthreads();  // stage s landed everywhere; stage s-1's readers are done
+    issue(s + kCpStages - 1);
+    const double *As = cp_sm + (s % kCpStages) * (SA + SB), *Bs = As + SA;
+    const double *as = As + (wm * GW::WT + (lane >> 2)) * kLDA + (lane & 3);
+    const double *bs = Bs + (lane & 3) * kLDB + wn * GW::WT + (lane >> 2);
+#pragma unroll
+    for (int k0 = 0; k0 < kBK; k0 += 4) {
+      double av[MI], bv[MI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        av[i] = as[i * 8 * kLDA + k0];
+        bv[i] = bs[k0 * kLDB + i * 8];
+      }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < MI; ++ni) dmma884(c[mi][ni], av[mi], bv[ni]);
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < MI; ++ni) {
+      const int gm = m0 + wm * GW::WT + mi * 8 + (lane >> 2);
+      const int gn = n0 + wn * GW::WT + ni * 8 + 2 * (lane & 3);
+      if (gm >= M) continue;
+      if (gn < N) C[(int64_t)gm * ldc + gn] = (TC)c[mi][ni][0];
+      if (gn + 1 < N) C[(int64_t)gm * ldc + gn + 1] = (TC)c[mi][ni][1];
+    }
+}
+
 // fixed-order fold of the logistic epilogue's row partials (warp per row)
 static __global__ void k_gemm_rowfold(const double *part, int64_t M, int npart, double *rowsum) {
   const int lane = threadIdx.x & 31;
@@ -286,6 +374,27 @@ cudaError_t gemm_rm(bool bt, int M, int N, int K, const TA *A, int64_t lda, int6
   // the largest tile that still gives every SM a couple of CTAs
   const int BM = tiles128 >= 4 * 148 ? 128 : tiles64 >= 2 * 148 ? 64 : 32;
   const dim3 grid((unsigned)nt, (M + BM - 1) / BM, batch);
+  if constexpr (std::is_same<TA, double>::value && std::is_same<TB, double>::value) {
+    static const bool use_cp = [] {
+      const char *e = getenv("CS_GEMM_CP");
+      return e ? atoi(e) != 0 : true;
+    }();
+    if (!bt && use_cp) {  // f64 operands as stored: the cp.async ring
+      auto cp = [&](auto bm) -> cudaError_t {
+        constexpr int kBM = decltype(bm)::value;
+        using GW = GemmWarps<kBM>;
+        constexpr size_t smem = sizeof(double) * kCpStages * ((size_t)kBM * GW::LDA + (size_t)GW::BK * kLDB);
+        static const cudaError_t attr =  // once per tile shape (each kBM is its own lambda body)
+            cudaFuncSetAttribute(k_gemm_cp<kBM, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (attr != cudaSuccess) return attr;
+        k_gemm_cp<kBM, TC><<<grid, GW::NT, smem, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
+        return cudaGetLastError();
+      };
+      if (BM == 128) return cp(std::integral_constant<int, 128>());
+      if (BM == 64) return cp(std::integral_constant<int, 64>());
+      return cp(std::integral_constant<int, 32>());
+    }
+  }
   auto go = [&](auto kern, int threads) {
     kern<<<grid, threads, 0, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, GemmEpi());
   };
