@@ -221,12 +221,12 @@ CS_D void cp_async8_zfill(void *dst, const void *src, bool valid) {
                "r"(valid ? 8 : 0)
                : "memory");
 }
-template <int BM, typename TC>
+template <int BM, typename TC, int CBK = GemmWarps<BM>::BK>
 __global__ void __launch_bounds__(GemmWarps<BM>::NT)
 k_gemm_cp(int M, int N, int K, const double *__restrict__ A, int64_t lda, int64_t sA, const double *__restrict__ B,
           int64_t ldb, int64_t sB, TC *__restrict__ C, int64_t ldc, int64_t sC) {
   using GW = GemmWarps<BM>;
-  constexpr int kBK = GW::BK, kLDA = GW::LDA, NT = GW::NT, MI = GW::MI;
+  constexpr int kBK = CBK, kLDA = CBK + 4, NT = GW::NT, MI = GW::MI;
   constexpr int EA = BM * kBK / NT, EB = kBK * kBN / NT;
   constexpr int SA = BM * kLDA, SB = kBK * kLDB;
   extern __shared__ __align__(16) double cp_sm[];
@@ -381,13 +381,13 @@ cudaError_t gemm_rm(bool bt, int M, int N, int K, const TA *A, int64_t lda, int6
     }();
     if (!bt && use_cp) {  // f64 operands as stored: the cp.async ring
       auto cp = [&](auto bm) -> cudaError_t {
-        constexpr int kBM = decltype(bm)::value;
+        constexpr int kBM = decltype(bm)::value, kBK = 16;
         using GW = GemmWarps<kBM>;
-        constexpr size_t smem = sizeof(double) * kCpStages * ((size_t)kBM * GW::LDA + (size_t)GW::BK * kLDB);
+        constexpr size_t smem = sizeof(double) * kCpStages * ((size_t)kBM * (kBK + 4) + (size_t)kBK * kLDB);
         static const cudaError_t attr =  // once per tile shape (each kBM is its own lambda body)
-            cudaFuncSetAttribute(k_gemm_cp<kBM, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(k_gemm_cp<kBM, TC, kBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (attr != cudaSuccess) return attr;
-        k_gemm_cp<kBM, TC><<<grid, GW::NT, smem, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
+        k_gemm_cp<kBM, TC, kBK><<<grid, GW::NT, smem, st>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC);
         return cudaGetLastError();
       };
       if (BM == 128) return cp(std::integral_constant<int, 128>());
