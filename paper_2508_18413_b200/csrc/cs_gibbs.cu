@@ -111,17 +111,18 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
   const TT mun_t = (TT)mun, mean_t = (TT)mean;
   const TT xbar_t = (TT)xbar, two_dm = (TT)(2.0 * (th - mu)), mu_c = (TT)(2.0 * kappa0 * (mu - mu0));
   TT e_tau = 0, e_mu = 0, e_th = 0, e_sg = 0;
-  for (int k = 0; k < A.nsamp; ++k) {
-    // z_tau / z_mu are shared by the team: lanes 0 and 1 hash them
 #if CS_GIBBS_TT_SUMS
-    using SU = TT;
+  using SU = TT;
 #else
-    using SU = double;
+  using SU = double;
 #endif
-    const SU zs = (SU)probe_sign(h3, k, sub == 0 ? 0 : (sub == 1 ? 1 : 2 + sub));
-    const TT z_tau = (TT)__shfl_sync(0xffffffffu, zs, (threadIdx.x & 31) & ~7);
-    const TT z_mu = (TT)__shfl_sync(0xffffffffu, zs, ((threadIdx.x & 31) & ~7) + 1);
-    const TT z_th = (TT)probe_sign(h3, k, 2 + sub), z_sg = (TT)probe_sign(h3, k, 2 + S + sub);
+  const int team0 = (threadIdx.x & 31) & ~7;
+  SU zpre = 0;  // z_tau / z_mu are shared by the team: lane j hashes (probe j/2, coordinate j%2) of 4 probes
+  for (int k = 0; k < A.nsamp; ++k) {
+    if ((k & 3) == 0) zpre = (SU)probe_sign_fast(h3, k + (sub >> 1), sub & 1);
+    const TT z_tau = (TT)__shfl_sync(0xffffffffu, zpre, team0 + 2 * (k & 3));
+    const TT z_mu = (TT)__shfl_sync(0xffffffffu, zpre, team0 + 2 * (k & 3) + 1);
+    const TT z_th = (TT)probe_sign_fast(h3, k, 2 + sub), z_sg = (TT)probe_sign_fast(h3, k, 2 + S + sub);
     const TT dsg = raw_ok ? z_sg : (TT)0;
     const TT dq = mu_c * z_mu + (TT)team_sum((SU)(two_dm * (z_th - z_mu)));
     const TT dtau2 = dq * inv_gt;
@@ -136,10 +137,12 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
     e_th += z_th * dth;
     e_sg += z_sg * dsgo;
   }
-  const double ns = (double)A.nsamp;
+  const double ns = (double)A.nsamp, inv_ns = 1.0 / ns;
   bool jok = true;
   auto elem = [&](int d, double est, double f, double p, int64_t off) {
-    double v = est / ns;  // est / n_samples as deer.py:131
+    // est / n_samples as deer.py:131 (fp32 storage: times the reciprocal -- the
+    // f64 quotient is rounded to fp32 anyway)
+    double v = sizeof(ST) == 4 ? est * inv_ns : est / ns;
     jok &= isfinite(v);
     if (A.pre) v = v * __ldg(A.pre + d);
     v = v * A.damping;
@@ -151,10 +154,9 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
   };
   elem(2 + sub, (double)e_th, thn, th, rr * D + 2 + sub);
   elem(2 + S + sub, (double)e_sg, sgn, sgraw, rr * D + 2 + S + sub);
-  if (sub == 0) {
-    elem(0, (double)e_tau, tau2n, (double)prow[0], rr * D);
-    elem(1, (double)e_mu, mun, mu, rr * D + 1);
-  }
+  if (sub < 2)  // tau^2 on lane 0, mu on lane 1 (every lane holds both team values)
+    elem(sub, sub == 0 ? (double)e_tau : (double)e_mu, sub == 0 ? tau2n : mun, sub == 0 ? (double)prow[0] : mu,
+         rr * D + sub);
   // team flags -> block -> stats
   const unsigned bad_fin = __ballot_sync(0xffffffffu, valid && !fin);
   const unsigned bad_jac = __ballot_sync(0xffffffffu, valid && !jok);
