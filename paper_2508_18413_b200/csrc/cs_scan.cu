@@ -1011,6 +1011,21 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
     // ---- C: entry state of each segment = (segments before it) o running state
     double *run_in = s_run + (n & 1) * 2 * 64, *run_out = s_run + ((n + 1) & 1) * 2 * 64;
     if (active) {
+      // UPDATE: this thread's previous-guess values, loaded before the entry
+      // fold (the replay's stores may alias them, so loads issued at the point
+      // of use would serialise behind every store)
+      constexpr int NG = UPDATE ? (VAR == SCAN_BLOCK ? 2 : 1) : 0;
+      ST gv[NG > 0 ? NG : 1][UPDATE ? KR : 1];
+      if constexpr (UPDATE) {
+        const ST *gb0 = a.guess + row0 * SW + c;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          if (r0 + k < r1) {
+            gv[0][k] = gb0[(r0 + k) * SW];
+            if constexpr (NG == 2) gv[NG - 1][k] = gb0[(r0 + k) * SW + ncol];
+          }
+        }
+      }
       SegE<VAR, CT> pre;
       pre.ident();
       if (nseg <= 32) {
@@ -1044,10 +1059,9 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
       // ---- replay from registers; states stream straight out (lanes of a warp
       // cover whole rows, so each store instruction writes contiguous runs)
       unsigned long long dmb = 0ull;
-      const ST *gbase = UPDATE ? a.guess + row0 * SW : nullptr;
-      auto check = [&](int r, int col, double xv) {  // deer.py:273-275 on the stored value
+      auto check = [&](int r, double g, double xv) {  // deer.py:273-275 on the stored value
         if constexpr (UPDATE) {
-          const double gap = fabs(xv - (double)gbase[r * SW + col]);
+          const double gap = fabs(xv - g);
           if (gap > a.atol + a.rtol * fabs(xv)) s_fail[r] = 1;
           const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
           dmb = gb > dmb ? gb : dmb;
@@ -1061,7 +1075,7 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
           x = ev[0][k] * x + ev[1][k];
           if (r0 + k < r1) {
             __stcs(o + (r0 + k) * SW, (ST)x);
-            check(r0 + k, c, (double)x);
+            check(r0 + k, (double)gv[0][k], (double)x);
           }
         }
       } else {
@@ -1075,8 +1089,8 @@ scan_rows(ScanArgs<ST> a, LookbackWs ws, int R, int CS, int64_t nchunks, int lag
           if (r0 + k < r1) {
             __stcs(o + (r0 + k) * SW, (ST)x);
             __stcs(o + (r0 + k) * SW + ncol, (ST)v);
-            check(r0 + k, c, (double)x);
-            check(r0 + k, ncol + c, (double)v);
+            check(r0 + k, (double)gv[0][k], (double)x);
+            check(r0 + k, (double)gv[NG > 1 ? 1 : 0][k], (double)v);
           }
         }
       }
@@ -1866,14 +1880,18 @@ struct LocalStream {  // double-buffered bulk-copy stream of row tiles through s
   unsigned use[2];
   int D;
   bool aligned;  // 16-byte aligned arrays: bulk copies, else plain loads / stores
+  const ST *gsrc = nullptr;  // optional third stream (the previous guess), two slots at gbuf
+  ST *gbuf = nullptr;
   CS_D ST *jt(int k) const { return buf + (size_t)k * 2 * be; }
   CS_D ST *ut(int k) const { return buf + (size_t)k * 2 * be + be; }
+  CS_D ST *gt(int k) const { return gbuf + (size_t)k * be; }
   CS_D unsigned issue(const ST *j, const ST *u, int64_t row0, int rows, int k) const {
     const unsigned bulk = aligned ? (unsigned)(((size_t)rows * D * sizeof(ST)) & ~(size_t)15) : 0u;
     if (threadIdx.x == 0 && bulk) {
-      mbar_expect_tx(&bar[k], 2 * bulk);
+      mbar_expect_tx(&bar[k], (gsrc ? 3 : 2) * bulk);
       bulk_g2s(jt(k), j + row0 * D, bulk, &bar[k]);
       bulk_g2s(ut(k), u + row0 * D, bulk, &bar[k]);
+      if (gsrc) bulk_g2s(gt(k), gsrc + row0 * D, bulk, &bar[k]);
     }
     return bulk;
   }
@@ -1882,6 +1900,7 @@ struct LocalStream {  // double-buffered bulk-copy stream of row tiles through s
     for (int i = nb + threadIdx.x; i < n; i += kScanThreads) {
       jt(k)[i] = j[row0 * D + i];
       ut(k)[i] = u[row0 * D + i];
+      if (gsrc) gt(k)[i] = gsrc[row0 * D + i];
     }
     if (bulk) mbar_wait(&bar[k], use[k]++ & 1);
     __syncthreads();
@@ -1903,13 +1922,13 @@ struct LocalStream {  // double-buffered bulk-copy stream of row tiles through s
 // and max gap into the stats record (the scan_rows UPDATE semantics)
 template <typename ST>
 CS_D void local_bookkeep(const ScanArgs<ST> &a, const ST *xt, int64_t row0, int rows, int *s_fail,
-                         unsigned long long *s_dm) {
+                         unsigned long long *s_dm, const ST *gtile = nullptr) {  // gtile: the guess rows staged in smem
   const int D = a.D, tid = threadIdx.x, lane = tid & 31;
   for (int r = tid; r < rows; r += kScanThreads) s_fail[r] = 0;
   if (tid == 0) *s_dm = 0ull;
   __syncthreads();
   unsigned long long dmb = 0ull;
-  const ST *gb = a.guess + row0 * D;
+  const ST *gb = gtile ? gtile : a.guess + row0 * D;
   for (int i = tid; i < rows * D; i += kScanThreads) {
     const double xv = (double)xt[i];
     const double gap = fabs(xv - (double)gb[i]);
@@ -2135,6 +2154,246 @@ scan_local_fixup(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
     }
     S.store(a.out, row0, rows, kb, bk[kb]);
     __syncthreads();
+  }
+  if (tid == 0) bulk_wait_read();
+}
+
+// ---------------------------------------------------------------------------
+// Reduce-then-replay row scan with the fused Newton bookkeeping (diag, moderate
+// T): the local scan's ranges, but the first pass only forms each range's map
+// (tiles walked last to first, so the replay's first tiles are the ones still
+// in L2), and the replay scans every
+// range from its true entry (each CTA folds the maps of the ranges before its
+// own while its first tile lands).  No fix-up, however slowly the maps contract (the
+// Newton iterates of cfg 5 do): j, u are read twice, guess once, s written once.
+CS_HD size_t rr_guess_off(int B, int D, size_t esz) {  // after the j/u slots, segment aggregates, row flags
+  const size_t o = 4 * (size_t)B * D * esz + (size_t)(kScanThreads / D) * D * 2 * sizeof(double) + sizeof(int) * (size_t)B;
+  return (o + 127) & ~(size_t)127;
+}
+template <typename ST>
+__global__ void __launch_bounds__(kScanThreads, 2)
+scan_rr_reduce(ScanArgs<ST> a, LocalWs ws, int B, bool aligned) {
+  constexpr int W = 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double s_x[64], s_P[64];  // map of the tiles after the current one
+  __shared__ __align__(8) uint64_t s_bar[2];
+  const int D = a.D, tid = threadIdx.x, G = gridDim.x, g = blockIdx.x;
+  const size_t be = (size_t)B * D;
+  LocalStream<ST> S{(ST *)smem_raw, be, s_bar, {0u, 0u}, D, aligned};
+  double *sa = (double *)(S.buf + 4 * be);
+  const int nseg = kScanThreads / D, c = tid % D, sg = tid / D;
+  const bool active = sg < nseg;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  if (tid < D) {
+    s_x[tid] = 0.0;
+    s_P[tid] = 1.0;
+  }
+  __syncthreads();
+  int64_t lo, hi;
+  local_range(a.T, G, g, lo, hi);
+  const int nblk = (int)((hi - lo + B - 1) / B);
+  unsigned bk[2] = {0u, 0u};
+  if (nblk > 0) {
+    const int64_t rl = lo + (int64_t)(nblk - 1) * B;
+    bk[(nblk - 1) & 1] = S.issue(a.e0, a.u, rl, (int)(hi - rl), (nblk - 1) & 1);
+  }
+  for (int k = nblk - 1; k >= 0; --k) {
+    const int64_t row0 = lo + (int64_t)k * B;
+    const int rows = (int)(hi - row0 < B ? hi - row0 : B);
+    const int kb = k & 1;
+    if (k > 0) {
+      __syncthreads();  // the slot the previous tile lands in is free
+      bk[kb ^ 1] = S.issue(a.e0, a.u, row0 - B, B, kb ^ 1);
+    }
+    S.land(a.e0, a.u, row0, rows, kb, bk[kb]);
+    const ST *jt = S.jt(kb), *ut = S.ut(kb);
+    const int rs = (rows + nseg - 1) / nseg, r0 = sg * rs, r1 = min(rows, r0 + rs);
+    if (active) {
+      SegE<SCAN_DIAG, double> run;
+      run.ident();
+      for (int r = r0; r < r1; ++r) {
+        SegE<SCAN_DIAG, double> e;
+        e.j = (double)jt[r * D + c];
+        e.u = (double)ut[r * D + c];
+        run.push(e);
+      }
+      run.store(sa + (sg * D + c) * W);
+    }
+    __syncthreads();
+    if (tid < D) {  // (tiles after) o (this tile), the tile's segments in order
+      double xv = 0.0, P = 1.0;
+      for (int q = 0; q < nseg; ++q) {
+        SegE<SCAN_DIAG, double> e;
+        e.load(sa + (q * D + tid) * W);
+        e.apply(xv);
+        P *= e.j;
+      }
+      const double Pl = s_P[tid];
+      s_x[tid] = (xv != 0.0 ? Pl * xv : 0.0) + s_x[tid];
+      s_P[tid] = Pl * P;
+    }
+  }
+  __syncthreads();
+  if (tid < D) {
+    ws.ragg[((size_t)g * D + tid) * W] = s_P[tid];
+    ws.ragg[((size_t)g * D + tid) * W + 1] = s_x[tid];
+  }
+}
+
+template <typename ST, bool UPD>
+__global__ void __launch_bounds__(kScanThreads, 2)
+scan_rr_replay(ScanArgs<ST> a, LocalWs ws, int B, bool aligned) {
+  using CT = ST;
+  constexpr int W = 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ double s_x[64];
+  __shared__ unsigned long long s_dm;
+  __shared__ unsigned s_nf;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  const int D = a.D, tid = threadIdx.x, lane = tid & 31, G = gridDim.x, g = blockIdx.x;
+  const size_t be = (size_t)B * D;
+  LocalStream<ST> S{(ST *)smem_raw, be, s_bar, {0u, 0u}, D, aligned};
+  double *sa = (double *)(S.buf + 4 * be);
+  int *s_fail = (int *)(sa + 2 * (kScanThreads / D) * D);
+  if constexpr (UPD) {  // the guess rows ride the same bulk copies (two more slots after the row flags)
+    S.gsrc = a.guess;
+    S.gbuf = (ST *)((unsigned char *)smem_raw + rr_guess_off(B, D, sizeof(ST)));
+  }
+  const int nseg = kScanThreads / D, c = tid % D, sg = tid / D;
+  const bool active = sg < nseg;
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+    s_dm = 0ull;
+    s_nf = 0u;
+  }
+  for (int r = tid; r < B; r += kScanThreads) s_fail[r] = 0;
+  __syncthreads();
+  int64_t lo, hi;
+  local_range(a.T, G, g, lo, hi);
+  const int nblk = (int)((hi - lo + B - 1) / B);
+  unsigned bk[2] = {0u, 0u};
+  if (nblk > 0) bk[0] = S.issue(a.e0, a.u, lo, (int)(hi - lo < B ? hi - lo : B), 0);
+  // this range's entry while the first tile lands: s0 through ranges 0..g-1 in
+  // order (f64) -- each of a column's threads composes a contiguous run of the
+  // range maps, then one thread per column chains the runs
+  if (active) {
+    constexpr int KP = 8;
+    const int per = (g + nseg - 1) / nseg, q0 = min(g, sg * per), q1 = min(g, q0 + per);
+    double P = 1.0, X = 0.0;
+    for (int qb = q0; qb < q1; qb += KP) {
+      double pa[KP], xa[KP];
+#pragma unroll
+      for (int i = 0; i < KP; ++i)
+        if (qb + i < q1) {
+          pa[i] = ws.ragg[((size_t)(qb + i) * D + c) * 2];
+          xa[i] = ws.ragg[((size_t)(qb + i) * D + c) * 2 + 1];
+        }
+#pragma unroll
+      for (int i = 0; i < KP; ++i)
+        if (qb + i < q1) {
+          X = (X != 0.0 ? pa[i] * X : 0.0) + xa[i];
+          P *= pa[i];
+        }
+    }
+    sa[(sg * D + c) * W] = P;
+    sa[(sg * D + c) * W + 1] = X;
+  }
+  __syncthreads();
+  if (tid < D) {
+    double e = (double)a.s0[tid];
+    for (int q = 0; q < nseg; ++q) {
+      const double P = sa[(q * D + tid) * W], X = sa[(q * D + tid) * W + 1];
+      e = (e != 0.0 ? P * e : 0.0) + X;
+    }
+    s_x[tid] = e;
+  }
+  __syncthreads();
+  unsigned long long dmb = 0ull;  // bookkeeping partials over all of this thread's rows
+  unsigned nf = 0;
+  for (int k = 0; k < nblk; ++k) {
+    const int64_t row0 = lo + (int64_t)k * B;
+    const int rows = (int)(hi - row0 < B ? hi - row0 : B);
+    const int kb = k & 1;
+    if (k + 1 < nblk) {
+      if (tid == 0) bulk_wait_read();
+      __syncthreads();
+      const int64_t rn = row0 + B;
+      bk[kb ^ 1] = S.issue(a.e0, a.u, rn, (int)(hi - rn < B ? hi - rn : B), kb ^ 1);
+    }
+    S.land(a.e0, a.u, row0, rows, kb, bk[kb]);
+    ST *jt = S.jt(kb), *ut = S.ut(kb);
+    const int rs = (rows + nseg - 1) / nseg, r0 = sg * rs, r1 = min(rows, r0 + rs);
+    if (active) {
+      SegE<SCAN_DIAG, double> run;
+      run.ident();
+      for (int r = r0; r < r1; ++r) {
+        SegE<SCAN_DIAG, double> e;
+        e.j = (double)jt[r * D + c];
+        e.u = (double)ut[r * D + c];
+        run.push(e);
+      }
+      run.store(sa + (sg * D + c) * W);
+    }
+    __syncthreads();
+    if (active) {  // replay from the tile's entry and the segments before this one (f64)
+      double xe = s_x[c];
+      for (int q = 0; q < sg; ++q) {
+        SegE<SCAN_DIAG, double> x;
+        x.load(sa + (q * D + c) * W);
+        x.apply(xe);
+      }
+      CT x = (CT)xe;
+      const ST *gt = UPD ? S.gt(kb) : nullptr;
+      for (int r = r0; r < r1; ++r) {
+        x = jt[r * D + c] * x + ut[r * D + c];
+        ut[r * D + c] = (ST)x;
+        if constexpr (UPD) {  // deer.py:273-275 on the stored value
+          const double xv = (double)(ST)x, gap = fabs(xv - (double)gt[r * D + c]);
+          if (gap > a.atol + a.rtol * fabs(xv)) s_fail[r] = 1;
+          const unsigned long long bits = (unsigned long long)__double_as_longlong(gap);
+          dmb = bits > dmb ? bits : dmb;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < D) {  // the tile's exit
+      double xv = s_x[tid];
+      for (int q = 0; q < nseg; ++q) {
+        SegE<SCAN_DIAG, double> e;
+        e.load(sa + (q * D + tid) * W);
+        e.apply(xv);
+      }
+      s_x[tid] = xv;
+    }
+    if constexpr (UPD) {
+      for (int r = tid; r < rows; r += kScanThreads)
+        if (s_fail[r]) {
+          a.last_fail[row0 + r] = a.it;
+          s_fail[r] = 0;
+          ++nf;
+        }
+    }
+    S.store(a.out, row0, rows, kb, bk[kb]);
+    __syncthreads();
+  }
+  if constexpr (UPD) {
+    dmb = warp_max_u64(dmb);
+    nf = (unsigned)warp_sum_i((int)nf);
+    if (lane == 0) {
+      atomicMax(&s_dm, dmb);
+      if (nf) atomicAdd(&s_nf, nf);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (s_nf) atomicAdd(&a.stats->fail_rows, s_nf);
+      atomicMax((unsigned long long *)&a.stats->dmax, s_dm);
+    }
   }
   if (tid == 0) bulk_wait_read();
 }
@@ -2525,6 +2784,8 @@ static int rows_per_tile(int var, int dtype, int D) {
 // look-back, 67 %), each tile's look-back (~5 L2 round trips) is exposed per
 // CTA; see DESIGN.md section 8.
 size_t scan_local_ws_bytes(int dtype, int64_t T, int D);
+bool scan_rr_eligible(int var, int64_t T, int D);
+size_t scan_rr_ws_bytes(int dtype, int64_t T, int D);
 bool scan_1p_eligible(int var, int64_t T, int D) { return scan_1p_mode() == 1 && var == SCAN_DIAG && D >= 1 && D <= 64 && T > 0; }
 // long scans only: each range's fixed-up prefix (until P underflows) and the
 // three launches are amortised from ~2M steps on (T = 1M, D = 18: two-pass
@@ -2567,6 +2828,10 @@ size_t scan_ws_bytes(int var, int dtype, int64_t T, int D) {
   }
   if (scan_local_eligible(var, T, D)) {
     const size_t c = var == SCAN_BLOCK ? scan_local_blk_ws_bytes(dtype, T, D) : scan_local_ws_bytes(dtype, T, D);
+    a = a > c ? a : c;
+  }
+  if (scan_rr_eligible(var, T, D)) {
+    const size_t c = scan_rr_ws_bytes(dtype, T, D);
     a = a > c ? a : c;
   }
   return a > b ? a : b;
@@ -2688,6 +2953,46 @@ cudaError_t launch_scan_local_blk_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
 }
 template cudaError_t launch_scan_local_blk_t<float>(ScanArgs<float>, void *, cudaStream_t);
 template cudaError_t launch_scan_local_blk_t<double>(ScanArgs<double>, void *, cudaStream_t);
+
+// reduce-then-replay (scan_rr_*): the local scan's ranges, no tile records
+bool scan_rr_eligible(int var, int64_t T, int D) {
+  static const int64_t min_t = [] {
+    const char *e = getenv("CS_SCAN_RR_MIN_T");
+    return e ? (int64_t)atoll(e) : ((int64_t)1 << 16);
+  }();
+  return var == SCAN_DIAG && D >= 1 && D <= 64 && T >= min_t;
+}
+size_t scan_rr_ws_bytes(int dtype, int64_t T, int D) {
+  int G, B, tmax;
+  size_t smem;
+  local_geom(dtype, T, D, G, B, tmax, smem);
+  return align_up(sizeof(double) * (size_t)G * D * 2) + align_up(sizeof(double) * (size_t)G * D);
+}
+template <typename ST, bool UPD>
+cudaError_t launch_scan_rr_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
+  int G, B, tmax;
+  size_t smem;
+  local_geom(sizeof(ST) == 8 ? CS_F64 : CS_F32, a.T, a.D, G, B, tmax, smem);
+  unsigned char *b = (unsigned char *)ws;
+  LocalWs w{};
+  w.ragg = (double *)b;
+  b += align_up(sizeof(double) * (size_t)G * a.D * 2);
+  w.rentry = (double *)b;
+  const size_t smem_r = UPD ? rr_guess_off(B, a.D, sizeof(ST)) + 2 * (size_t)B * a.D * sizeof(ST) : smem;
+  cudaError_t e = cudaFuncSetAttribute(scan_rr_reduce<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(scan_rr_replay<ST, UPD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r);
+  if (e != cudaSuccess) return e;
+  const bool al = ((((uintptr_t)a.e0) | ((uintptr_t)a.u) | ((uintptr_t)a.out)) & 15) == 0 &&
+                  (!UPD || (((uintptr_t)a.guess) & 15) == 0);
+  scan_rr_reduce<ST><<<G, kScanThreads, smem, st>>>(a, w, B, al);
+  scan_rr_replay<ST, UPD><<<G, kScanThreads, smem_r, st>>>(a, w, B, al);
+  return cudaGetLastError();
+}
+template cudaError_t launch_scan_rr_t<float, true>(ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_scan_rr_t<double, true>(ScanArgs<double>, void *, cudaStream_t);
+template cudaError_t launch_scan_rr_t<float, false>(ScanArgs<float>, void *, cudaStream_t);
+template cudaError_t launch_scan_rr_t<double, false>(ScanArgs<double>, void *, cudaStream_t);
 
 template cudaError_t launch_scan_local_t<float, false>(ScanArgs<float>, void *, cudaStream_t);
 template cudaError_t launch_scan_local_t<double, false>(ScanArgs<double>, void *, cudaStream_t);

@@ -46,6 +46,11 @@ int scan_1p_mode();
 size_t scan_local_ws_bytes(int dtype, int64_t T, int D);
 template <typename ST, bool UPD>
 cudaError_t launch_scan_local_t(ScanArgs<ST> a, void *ws, cudaStream_t st);
+// reduce-then-replay row scan (diag; the update scans at moderate T)
+bool scan_rr_eligible(int var, int64_t T, int D);
+size_t scan_rr_ws_bytes(int dtype, int64_t T, int D);
+template <typename ST, bool UPD>
+cudaError_t launch_scan_rr_t(ScanArgs<ST> a, void *ws, cudaStream_t st);
 size_t scan_local_blk_ws_bytes(int dtype, int64_t T, int D);
 template <typename ST>
 cudaError_t launch_scan_local_blk_t(ScanArgs<ST> a, void *ws, cudaStream_t st);

@@ -884,6 +884,70 @@ def test_update_scan_bookkeeping_multi_round(cuda_device, D, misalign, T):
     assert dmax == float(gap.max())
 
 
+@pytest.mark.parametrize("kind,T", [("slow", 1_000_003), ("slow", 70_001), ("unit", 300_001), ("growing", 250_001),
+                                    ("zero_entry", 500_001), ("mixed", 2_000_003)])
+def test_update_scan_reduce_replay_extremes(cuda_device, kind, T):
+    # the reduce-then-replay update scan (2^16 <= T < 2^22): maps that contract
+    # slowly (the Newton iterates of cfg 5), not at all, grow for a stretch or
+    # hold an exact zero -- states against the f64 oracle scan, bookkeeping
+    # against a direct evaluation
+    from paper_2508_18413_b200 import _lib
+
+    lib = _lib.load()
+    D, it = 18, 4
+    rng = np.random.default_rng(T % 1000 + len(kind))
+    if kind == "slow":
+        j = rng.uniform(0.9990, 0.99999, (T, D))
+    elif kind == "unit":
+        j = np.ones((T, D))
+    elif kind == "growing":
+        j = rng.uniform(0.5, 0.95, (T, D))
+        j[T // 3:T // 3 + 300] = 1.02
+    elif kind == "zero_entry":
+        j = rng.uniform(-0.99, 0.99, (T, D))
+        j[T // 2, 3] = 0.0
+    else:
+        j = np.where(rng.uniform(size=(T, D)) < 0.5, rng.uniform(0.999, 1.0, (T, D)), rng.uniform(-0.9, 0.9, (T, D)))
+    u = rng.normal(size=(T, D)) * (1e-3 if kind in ("unit", "slow") else 1.0)
+    j32, u32 = j.astype(np.float32), u.astype(np.float32)
+    s0 = rng.normal(size=D).astype(np.float32)
+    want = O.parallel_affine_solve(O.DiagElements(j32.astype(np.float64), u32.astype(np.float64)),
+                                   s0.astype(np.float64), workers=16)
+    jt, ut = torch.as_tensor(j32, device=cuda_device), torch.as_tensor(u32, device=cuda_device)
+    s0t = torch.as_tensor(s0, device=cuda_device)
+    wt = torch.as_tensor(want, device=cuda_device)
+    g = torch.Generator(device=cuda_device).manual_seed(T)
+    guess = (wt + torch.randn((T, D), generator=g, device=cuda_device, dtype=torch.float64) * 1e-4 *
+             (torch.rand((T, 1), generator=g, device=cuda_device) < 0.3)).float()
+    out = torch.empty_like(jt)
+    last_fail = torch.full((T,), 1, dtype=torch.int32, device=cuda_device)
+    stats = torch.zeros(40, dtype=torch.uint8, device=cuda_device)
+    wsb = lib.cs_scan_workspace_bytes(_lib.CS_MODE_DIAG, _lib.CS_F32, T, D)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=cuda_device)
+    atol, rtol = 1e-5, 1e-5
+    _lib.check(lib.cs_scan_diag_update(_lib.CS_F32, _lib.ptr(jt), _lib.ptr(ut), _lib.ptr(s0t), _lib.ptr(out), T, D,
+                                       _lib.ptr(ws), wsb, _lib.ptr(guess), atol, rtol, it, _lib.ptr(last_fail),
+                                       _lib.ptr(stats), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    scale = np.abs(want).max()
+    np.testing.assert_allclose(np_(out), want, atol=2e-5 * max(scale, 1.0) * (30 if kind == "unit" else 1), rtol=1e-4)
+    gap = (out.double() - guess.double()).abs()
+    fail = (gap > atol + rtol * out.double().abs()).any(dim=1)
+    want_lf = torch.where(fail, torch.tensor(it, dtype=torch.int32, device=cuda_device),
+                          torch.tensor(1, dtype=torch.int32, device=cuda_device))
+    assert torch.equal(last_fail, want_lf)
+    raw = stats.cpu().numpy().tobytes()
+    assert int(np.frombuffer(raw[28:32], dtype=np.uint32)[0]) == int(fail.sum())
+    assert float(np.frombuffer(raw[32:40], dtype=np.float64)[0]) == float(gap.max())
+    # run to run: bit-identical
+    out2 = torch.empty_like(out)
+    _lib.check(lib.cs_scan_diag_update(_lib.CS_F32, _lib.ptr(jt), _lib.ptr(ut), _lib.ptr(s0t), _lib.ptr(out2), T, D,
+                                       _lib.ptr(ws), wsb, _lib.ptr(guess), atol, rtol, it, _lib.ptr(last_fail),
+                                       _lib.ptr(stats), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
+
+
 @pytest.mark.skipif(bool(__import__("os").environ.get("CS_SCAN_LBW")), reason="already the variant run")
 @pytest.mark.parametrize("lag,round_kb", [(1, 4096), (2, 16384)])
 def test_row_scan_lookback_warp_variant(cuda_device, lag, round_kb):
@@ -894,7 +958,8 @@ def test_row_scan_lookback_warp_variant(cuda_device, lag, round_kb):
     import subprocess
     import sys
 
-    env = dict(os.environ, CS_SCAN_LBW="1", CS_SCAN_LAG=str(lag), CS_SCAN_ROUND_KB=str(round_kb))
+    # (CS_SCAN_RR=0: the update cases below 2^22 take this two-pass kernel too)
+    env = dict(os.environ, CS_SCAN_LBW="1", CS_SCAN_LAG=str(lag), CS_SCAN_ROUND_KB=str(round_kb), CS_SCAN_RR="0")
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-x", "-q", "-m", "gpu", "-p",
                         "no:cacheprovider", "-k", "multi_round or update_scan_bookkeeping or scan_kats or diag_and_block"],
                        env=env, capture_output=True, text=True, timeout=600)
