@@ -417,7 +417,25 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
   const bool local = scan_local_eligible(var, T, D) &&
                      ws_bytes >= (var == SCAN_BLOCK ? scan_local_blk_ws_bytes(dtype, T, D)
                                                     : scan_local_ws_bytes(dtype, T, D));
+  // reduce-then-replay for plain diag scans up to CS_SCAN_RR_PLAIN_MAX_T
+  static const int64_t rr_max = [] {
+    const char *e = getenv("CS_SCAN_RR_PLAIN_MAX_T");
+    return e ? (int64_t)atoll(e) : ((int64_t)1 << 20);  // D = 18: 2^17 0.053 -> 0.046 ms, 2^18 0.069 -> 0.051, 2^19 0.085 -> 0.070; even at 2^20; local ahead above (tools/sweep_rr_plain.sh)
+  }();
+  const bool rr = T < rr_max && scan_rr_eligible(var, T, D) && ws_bytes >= scan_rr_ws_bytes(dtype, T, D);
   cudaError_t e;
+  if (rr) {
+    if (dtype == CS_F64) {
+      ScanArgs<double> a{(const double *)e0, nullptr, nullptr, nullptr, (const double *)u, (const double *)s0,
+                         (double *)out, T, D};
+      e = launch_scan_rr_t<double, false>(a, ws, S(stream));
+    } else {
+      ScanArgs<float> a{(const float *)e0, nullptr, nullptr, nullptr, (const float *)u, (const float *)s0,
+                        (float *)out, T, D};
+      e = launch_scan_rr_t<float, false>(a, ws, S(stream));
+    }
+    return e == cudaSuccess ? CS_OK : cuda_fail(e, "scan launch");
+  }
   if (dtype == CS_F64) {
     ScanArgs<double> a{(const double *)e0, (const double *)e1, (const double *)e2, (const double *)e3,
                        (const double *)u, (const double *)s0, (double *)out, T, D};

@@ -2854,17 +2854,17 @@ cudaError_t launch_scan_1p_t(const ScanPlan &p, ScanArgs<ST> a, void *ws, cudaSt
   scan_rows_1p<ST><<<(unsigned)(p.ntiles < g ? p.ntiles : g), kScanThreads, p.smem, st>>>(a, w, p.R, p.ntiles);
   return cudaGetLastError();
 }
-static void local_geom(int dtype, int64_t T, int D, int &G, int &B, int &tmax, size_t &smem) {
+static void local_geom(int dtype, int64_t T, int D, int &G, int &B, int &tmax, size_t &smem, int kb = 0, int cps = 2) {
   const int esz = dtype == CS_F64 ? 8 : 4;
   static const int blk_kb = env_int("CS_SCAN_BLOCK_KB", 4, 48, 48);  // j + u per tile (T = 2^24, D = 18: 24 KB 0.92 ms, 40-48 KB 0.74-0.77 ms)
-  B = (blk_kb * 1024) / (2 * esz * D);
+  B = ((kb ? kb : blk_kb) * 1024) / (2 * esz * D);
   B = B / 4 * 4;
   if (B < 4) B = 4;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // two ranges per SM, each at least four tiles long (short scans: fewer, longer ranges)
-  G = 2 * sms;
+  G = cps * sms;
   if ((int64_t)G * 4 * B > T) G = (int)(T / (4 * (int64_t)B));
   if (G < 1) G = 1;
   const int64_t maxrows = T / G + 8;
@@ -2962,17 +2962,25 @@ bool scan_rr_eligible(int var, int64_t T, int D) {
   }();
   return var == SCAN_DIAG && D >= 1 && D <= 64 && T >= min_t;
 }
+static int rr_kb() {  // j + u per tile
+  static const int v = env_int("CS_SCAN_RR_KB", 4, 48, 32);  // cfg 5: 48 KB 64.5 ms, 32 KB 59.6 (tools/sweep_rr.sh)
+  return v;
+}
+static int rr_cps() {  // ranges (CTAs) per SM
+  static const int v = env_int("CS_SCAN_RR_CPS", 1, 8, 2);
+  return v;
+}
 size_t scan_rr_ws_bytes(int dtype, int64_t T, int D) {
   int G, B, tmax;
   size_t smem;
-  local_geom(dtype, T, D, G, B, tmax, smem);
+  local_geom(dtype, T, D, G, B, tmax, smem, rr_kb(), rr_cps());
   return align_up(sizeof(double) * (size_t)G * D * 2) + align_up(sizeof(double) * (size_t)G * D);
 }
 template <typename ST, bool UPD>
 cudaError_t launch_scan_rr_t(ScanArgs<ST> a, void *ws, cudaStream_t st) {
   int G, B, tmax;
   size_t smem;
-  local_geom(sizeof(ST) == 8 ? CS_F64 : CS_F32, a.T, a.D, G, B, tmax, smem);
+  local_geom(sizeof(ST) == 8 ? CS_F64 : CS_F32, a.T, a.D, G, B, tmax, smem, rr_kb(), rr_cps());
   unsigned char *b = (unsigned char *)ws;
   LocalWs w{};
   w.ragg = (double *)b;

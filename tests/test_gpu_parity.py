@@ -885,7 +885,7 @@ def test_update_scan_bookkeeping_multi_round(cuda_device, D, misalign, T):
 
 
 @pytest.mark.parametrize("kind,T", [("slow", 1_000_003), ("slow", 70_001), ("unit", 300_001), ("growing", 250_001),
-                                    ("zero_entry", 500_001), ("mixed", 2_000_003)])
+                                    ("zero_entry", 500_001), ("mixed", 2_000_003), ("mixed", 65_537)])
 def test_update_scan_reduce_replay_extremes(cuda_device, kind, T):
     # the reduce-then-replay update scan (2^16 <= T < 2^22): maps that contract
     # slowly (the Newton iterates of cfg 5), not at all, grow for a stretch or
@@ -939,6 +939,9 @@ def test_update_scan_reduce_replay_extremes(cuda_device, kind, T):
     raw = stats.cpu().numpy().tobytes()
     assert int(np.frombuffer(raw[28:32], dtype=np.uint32)[0]) == int(fail.sum())
     assert float(np.frombuffer(raw[32:40], dtype=np.float64)[0]) == float(gap.max())
+    # the plain scan of the same maps (below 2^20 the reduce-then-replay kernels, above the local scan)
+    plain = cs.parallel_affine_solve(cs.DiagElements(jt, ut), s0t)
+    np.testing.assert_allclose(np_(plain), want, atol=2e-5 * max(scale, 1.0) * (30 if kind == "unit" else 1), rtol=1e-4)
     # run to run: bit-identical
     out2 = torch.empty_like(out)
     _lib.check(lib.cs_scan_diag_update(_lib.CS_F32, _lib.ptr(jt), _lib.ptr(ut), _lib.ptr(s0t), _lib.ptr(out2), T, D,
