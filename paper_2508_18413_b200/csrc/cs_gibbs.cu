@@ -67,11 +67,26 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
   const double q_tau = (nu0 * tau0_sq + kappa0 * (dmu0 * dmu0)) + q;
   const double tau2n = q_tau / gt;
   const double kS = kappa0 + (double)S;
-  const double mun = (kappa0 * mu0 + sth) / kS + sqrt(tau2n / kS) * xm;
-  const double prec = 1.0 / tau2n + n / sg;
-  const double mean = (mun / tau2n + (n * xbar) / sg) / prec;
-  const double rsq = sqrt(prec);
-  const double thn = mean + xt / rsq;
+  double mun, prec, mean, thn, inv_t = 0, inv_sg = 0, rq = 0, rsq = 0;
+  if constexpr (sizeof(ST) == 4) {
+    // fp32 storage: the f64 sweep with shared reciprocals (1/tau^2, 1/sigma^2,
+    // 1/kS, rsqrt(prec)) -- a few f64 ulps against the quotients, far below the
+    // fp32 rounding of the stored states; f64 storage keeps the exact quotients
+    const double inv_kS = 1.0 / kS;
+    inv_t = 1.0 / tau2n;
+    inv_sg = 1.0 / sg;
+    mun = (kappa0 * mu0 + sth) * inv_kS + sqrt(tau2n * inv_kS) * xm;
+    prec = inv_t + n * inv_sg;
+    rq = rsqrt(prec);
+    mean = (mun * inv_t + (n * xbar) * inv_sg) * (rq * rq);
+    thn = mean + xt * rq;
+  } else {
+    mun = (kappa0 * mu0 + sth) / kS + sqrt(tau2n / kS) * xm;
+    prec = 1.0 / tau2n + n / sg;
+    mean = (mun / tau2n + (n * xbar) / sg) / prec;
+    rsq = sqrt(prec);
+    thn = mean + xt / rsq;
+  }
   const double res = xbar - thn;
   const double sgn = ((alpha0 * sigma0_sq + ss) + n * (res * res)) / gs;
   // finite / Picard on the coordinates this lane owns (lane 0 also tau^2, mu)
@@ -92,15 +107,15 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
   // are fp32 reciprocals (the f64 forward values above are only rounded once)
   TT inv_gt, inv_kS, inv_tau2n, inv_t2sq, n_sg2, inv_prec, c_mu, c_th, c_sg;
   if constexpr (sizeof(TT) == 4) {
-    const float gt_t = (float)gt, kS_t = (float)kS, t2_t = (float)tau2n, sg_t = (float)sg, n_t = (float)n;
+    const float gt_t = (float)gt, kS_t = (float)kS, t2_t = (float)tau2n, n_t = (float)n;
     inv_gt = 1.0f / gt_t;
     inv_kS = 1.0f / kS_t;
-    inv_tau2n = 1.0f / t2_t;
+    inv_tau2n = (float)inv_t;
     inv_t2sq = inv_tau2n * inv_tau2n;
-    n_sg2 = n_t / (sg_t * sg_t);
-    inv_prec = 1.0f / (float)prec;
+    n_sg2 = (float)(n * inv_sg * inv_sg);
+    inv_prec = (float)(rq * rq);
     c_mu = (float)xm / (2.0f * sqrtf(t2_t * kS_t));
-    c_th = 0.5f * (float)xt * inv_prec / (float)rsq;
+    c_th = 0.5f * (float)xt * inv_prec * (float)rq;
     c_sg = (-2.0f * n_t * (float)(xbar - thn)) / (float)gs;
   } else {
     inv_gt = 1.0 / gt; inv_kS = 1.0 / kS; inv_tau2n = 1.0 / tau2n;
