@@ -826,26 +826,29 @@ static int do_scan_update(int var, int dtype, const void *e0, const void *e1, co
   // 79.0 -> 83.9 ms per solve with the local scan)
   const bool local = T >= ((int64_t)1 << 22) && var == SCAN_DIAG && scan_local_eligible(var, T, D) &&
                      ws_bytes >= scan_local_ws_bytes(dtype, T, D);
-  // moderate T: reduce-then-replay (no fix-up, j / u re-read partly from L2)
-  static const bool rr_on = [] {
+  // reduce-then-replay (default everywhere from 2^16): the local scan's per-tile
+  // bookkeeping is latency-bound on its guess loads -- T = 2^22 / 2^24, D = 18:
+  // 0.89 / 3.40 ms local vs 0.35 / 1.30 ms (tools/update_scan_time.py)
+  static const int rr_mode = [] {  // 0 off, 1 below the local scan's range, 2 everywhere
     const char *e = getenv("CS_SCAN_RR");
-    return e ? atoi(e) != 0 : true;
+    return e ? atoi(e) : 2;
   }();
-  const bool rr = !local && rr_on && scan_rr_eligible(var, T, D) && ws_bytes >= scan_rr_ws_bytes(dtype, T, D);
+  const bool rr = (rr_mode == 2 || (rr_mode == 1 && !local)) && scan_rr_eligible(var, T, D) &&
+                  ws_bytes >= scan_rr_ws_bytes(dtype, T, D);
   cudaError_t e;
   if (dtype == CS_F64) {
     ScanArgs<double> a{(const double *)e0, (const double *)e1, (const double *)e2, (const double *)e3,
                        (const double *)u, (const double *)s0, (double *)out, T, D, (const double *)guess,
                        atol, rtol, it, last_fail, stats};
-    e = local ? launch_scan_local_t<double, true>(a, ws, S(stream))
-        : rr  ? launch_scan_rr_t<double, true>(a, ws, S(stream))
+    e = rr      ? launch_scan_rr_t<double, true>(a, ws, S(stream))
+        : local ? launch_scan_local_t<double, true>(a, ws, S(stream))
               : launch_scan_t<double>(p, a, ws, S(stream), true);
   } else {
     ScanArgs<float> a{(const float *)e0, (const float *)e1, (const float *)e2, (const float *)e3,
                       (const float *)u, (const float *)s0, (float *)out, T, D, (const float *)guess,
                       atol, rtol, it, last_fail, stats};
-    e = local ? launch_scan_local_t<float, true>(a, ws, S(stream))
-        : rr  ? launch_scan_rr_t<float, true>(a, ws, S(stream))
+    e = rr      ? launch_scan_rr_t<float, true>(a, ws, S(stream))
+        : local ? launch_scan_local_t<float, true>(a, ws, S(stream))
               : launch_scan_t<float>(p, a, ws, S(stream), true);
   }
   return e == cudaSuccess ? CS_OK : cuda_fail(e, "scan update launch");

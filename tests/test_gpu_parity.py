@@ -848,8 +848,9 @@ def test_update_scan_bookkeeping_multi_round(cuda_device, D, misalign, T):
     # the replay's fused bookkeeping (deer.py:273-277) at a multi-round size:
     # last_fail stamps, fail_rows and dmax against a direct evaluation.  D = 1,
     # 2, 4 take the coalesced 16-byte stage loads; a one-float offset of j and
-    # u forces the per-column fallback, ragged last stage included.  T > 2^22:
-    # the local scan + fix-up with the bookkeeping on each tile's final states
+    # u forces the per-column fallback, ragged last stage included.  By default
+    # these run the reduce-then-replay kernels (the variant run below covers the
+    # two-pass and local-scan kernels)
     from paper_2508_18413_b200 import _lib
 
     lib = _lib.load()
@@ -961,7 +962,8 @@ def test_row_scan_lookback_warp_variant(cuda_device, lag, round_kb):
     import subprocess
     import sys
 
-    # (CS_SCAN_RR=0: the update cases below 2^22 take this two-pass kernel too)
+    # (CS_SCAN_RR=0: the update cases take the two-pass kernel below 2^22 and the
+    # local scan + fix-up with per-tile bookkeeping above)
     env = dict(os.environ, CS_SCAN_LBW="1", CS_SCAN_LAG=str(lag), CS_SCAN_ROUND_KB=str(round_kb), CS_SCAN_RR="0")
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-x", "-q", "-m", "gpu", "-p",
                         "no:cacheprovider", "-k", "multi_round or update_scan_bookkeeping or scan_kats or diag_and_block"],
