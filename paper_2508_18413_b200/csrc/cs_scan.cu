@@ -2329,16 +2329,17 @@ scan_rr_replay(ScanArgs<ST> a, LocalWs ws, int B, bool aligned) {
     S.land(a.e0, a.u, row0, rows, kb, bk[kb]);
     ST *jt = S.jt(kb), *ut = S.ut(kb);
     const int rs = (rows + nseg - 1) / nseg, r0 = sg * rs, r1 = min(rows, r0 + rs);
-    if (active) {
-      SegE<SCAN_DIAG, double> run;
+    if (active) {  // segment maps in the storage precision (no exact-zero P needed here)
+      SegE<SCAN_DIAG, CT> run;
       run.ident();
       for (int r = r0; r < r1; ++r) {
-        SegE<SCAN_DIAG, double> e;
-        e.j = (double)jt[r * D + c];
-        e.u = (double)ut[r * D + c];
+        SegE<SCAN_DIAG, CT> e;
+        e.j = jt[r * D + c];
+        e.u = ut[r * D + c];
         run.push(e);
       }
-      run.store(sa + (sg * D + c) * W);
+      sa[(sg * D + c) * W] = (double)run.j;
+      sa[(sg * D + c) * W + 1] = (double)run.u;
     }
     __syncthreads();
     if (active) {  // replay from the tile's entry and the segments before this one (f64)

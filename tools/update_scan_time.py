@@ -44,5 +44,5 @@ for _ in range(10):
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
 ms = float(np.median(ts))
-print(f"update scan T={T} D={D} {'slow' if slow else 'fast'} CS_SCAN_RR={os.environ.get('CS_SCAN_RR', '1')}: {ms:.3f} ms "
+print(f"update scan T={T} D={D} {'slow' if slow else 'fast'} CS_SCAN_RR={os.environ.get('CS_SCAN_RR', '2')}: {ms:.3f} ms "
       f"({20 * T * D / ms / 1e6:.0f} GB/s at 20 B/element)", flush=True)
