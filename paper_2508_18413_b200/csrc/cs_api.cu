@@ -913,7 +913,7 @@ size_t cs_deer_workspace_bytes(const cs_system *sys, int dtype, int32_t max_iter
   const int md = solver_width(sys);
   const int W = md * md + md;
   const size_t T = (size_t)sys->T, D = (size_t)sys->dim;
-  return al(T * D * esize(dtype)) + al(sizeof(SolveCtl)) + al(sizeof(double) * 2 * 8 * (size_t)sm_count() * (W > 0 ? W : 1)) +
+  return al(T * D * esize(dtype)) + al(sizeof(SolveCtl)) + al(sizeof(double) * 2 * kAggReplicas * 8 * (size_t)sm_count() * (W > 0 ? W : 1)) +
          al(sizeof(int) * 8 * (size_t)sm_count());
 }
 

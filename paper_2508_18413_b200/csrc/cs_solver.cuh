@@ -298,6 +298,15 @@ CS_D void block_scan(const E &x, E &excl, E &total, E *s_warp) {
   __syncthreads();
 }
 
+// Every CTA's aggregate is written kAggReplicas times and CTA b folds copy
+// b % kAggReplicas: right after the barrier all CTAs read the low CTAs'
+// records at once, and one copy per line serialised those reads at its L2
+// slice (the high CTAs, which read the most records, finished the fold last).
+#ifndef CS_AGG_REPLICAS
+#define CS_AGG_REPLICAS 4
+#endif
+constexpr int kAggReplicas = CS_AGG_REPLICAS;
+
 // Grid barrier on a monotone arrival counter: every CTA adds 1 with release
 // semantics and waits (acquire) until the counter reaches nblocks * generation.
 // No reset and no last-arriver hand-off, so one L2 round trip per barrier.
@@ -485,8 +494,8 @@ deer_persistent(SolveArgs<ST> A) {
     probe_stamp(A.probe, A.probe_n, it, 2);
     E total;
     block_scan(agg, excl, total, s_warp);
-    if (threadIdx.x == 0) {
-      double *g = A.agg + ((size_t)(it & 1) * A.nblocks + b) * E::W;
+    if (threadIdx.x < kAggReplicas) {  // one copy per replica: readers spread over kAggReplicas lines
+      double *g = A.agg + (((size_t)(it & 1) * kAggReplicas + threadIdx.x) * A.nblocks + b) * E::W;
 #pragma unroll
       for (int q = 0; q < E::W; ++q) g[q] = total.v[q];
     }
@@ -583,7 +592,7 @@ deer_persistent(SolveArgs<ST> A) {
     // ---------------- phase B(it): carry-in, replay, bookkeeping ----------
     ST *Gn = cur ? A.G0 : A.G1;
     {
-      const double *ag = A.agg + (size_t)(it & 1) * A.nblocks * E::W;
+      const double *ag = A.agg + ((size_t)(it & 1) * kAggReplicas + (b % kAggReplicas)) * A.nblocks * E::W;
       const int per = (b + kSolveThreads - 1) / kSolveThreads;
       const int lo = threadIdx.x * per, hi = min(b, lo + per);
       E fold;
