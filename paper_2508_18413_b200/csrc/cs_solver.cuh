@@ -528,6 +528,27 @@ deer_persistent(SolveArgs<ST> A) {
       O->dmax_bits = 0ull;
     }
 
+    // the predecessors' aggregates, loaded now so this L2 round trip overlaps
+    // the decision reads below (used by phase B's carry-in)
+    E fold;
+    fold.ident();
+    {
+      const double *ag = A.agg + ((size_t)(it & 1) * kAggReplicas + (b % kAggReplicas)) * A.nblocks * E::W;
+      const int per = (b + kSolveThreads - 1) / kSolveThreads;
+      const int lo = threadIdx.x * per, hi = min(b, lo + per);
+      for (int q = lo; q < hi; ++q) {
+        E e;
+        const double2 *src = (const double2 *)(ag + (size_t)q * E::W);  // W is even, records 16 B aligned
+#pragma unroll
+        for (int w = 0; w < E::W / 2; ++w) {
+          const double2 p = __ldcg(src + w);
+          e.v[2 * w] = p.x;
+          e.v[2 * w + 1] = p.y;
+        }
+        fold.after(e);
+      }
+    }
+
     // ---------------- decisions (identical in every CTA) ------------------
     // one thread per CTA reads the slot words (not every thread: 100K readers
     // of one L2 line serialise at its slice and skew the grid by microseconds)
@@ -592,22 +613,6 @@ deer_persistent(SolveArgs<ST> A) {
     // ---------------- phase B(it): carry-in, replay, bookkeeping ----------
     ST *Gn = cur ? A.G0 : A.G1;
     {
-      const double *ag = A.agg + ((size_t)(it & 1) * kAggReplicas + (b % kAggReplicas)) * A.nblocks * E::W;
-      const int per = (b + kSolveThreads - 1) / kSolveThreads;
-      const int lo = threadIdx.x * per, hi = min(b, lo + per);
-      E fold;
-      fold.ident();
-      for (int q = lo; q < hi; ++q) {
-        E e;
-        const double2 *src = (const double2 *)(ag + (size_t)q * E::W);  // W is even, records 16 B aligned
-#pragma unroll
-        for (int w = 0; w < E::W / 2; ++w) {
-          const double2 p = __ldcg(src + w);
-          e.v[2 * w] = p.x;
-          e.v[2 * w + 1] = p.y;
-        }
-        fold.after(e);
-      }
       E fex, ftot;
       block_scan(fold, fex, ftot, s_warp);
       probe_stamp(A.probe, A.probe_n, it, 5);
