@@ -32,3 +32,20 @@ t("DeerResult(...)", lambda: deer.DeerResult(trace=s0, iterations=14, delta_hist
                                              per_step_converged_at=s0, full_trace=None, stats={}))
 t("key tuple", lambda: (cfg.mode, k.dtype, 400, cfg.atol, cfg.rtol, cfg.hutchinson_samples, cfg.damping, cfg.clip,
                          None if cfg.preconditioner is None else cfg.preconditioner.tobytes(), k.T, k.device))
+# whole calls
+t("run_deer (fused, full solve)", lambda: cs.run_deer(k, s0, cfg), n=300)
+d = k.desc()
+c = k._fused_ws[next(iter(k._fused_ws))][3]
+lib = _lib.load()
+tr = torch.empty((100_000, 2), dtype=torch.float32, device="cuda")
+ps = torch.empty(100_000, dtype=torch.int32, device="cuda")
+ws, wsb = k._fused_ws[next(iter(k._fused_ws))][0], k._fused_ws[next(iter(k._fused_ws))][1]
+
+
+def raw():
+    res = _lib.cs_deer_result()
+    lib.cs_deer_solve(ctypes.byref(d), ctypes.byref(c), _lib.dtype_code(k.dtype), _lib.ptr(s0), _lib.ptr(tr),
+                      _lib.ptr(ps), _lib.ptr(hist), _lib.ptr(ws), wsb, ctypes.byref(res), _lib.stream_ptr())
+
+
+t("cs_deer_solve via ctypes only", raw, n=300)
