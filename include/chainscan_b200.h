@@ -307,7 +307,9 @@ int cs_leapfrog_batch_solve(const cs_system *sys, const cs_deer_config *cfg, int
                             void *stream);
 /* Scans with the post-update bookkeeping fused into the replay (deer.py:273-277):
  * rows of `out` that moved more than atol + rtol|out| from `guess` get
- * last_fail[t] = iteration; d_stats->fail_rows / dmax are accumulated. */
+ * last_fail[t] = iteration; d_stats->fail_rows / dmax are accumulated.
+ * `out` must not overlap `guess` (CS_ERR_CONFIG otherwise): the kernels read
+ * guess through the read-only path while they write out. */
 int cs_scan_diag_update(int dtype, const void *j, const void *u, const void *s0, void *out, int64_t T,
                         int32_t D, void *ws, size_t ws_bytes, const void *guess, double atol, double rtol,
                         int32_t iteration, int32_t *last_fail, cs_elem_stats *d_stats, void *stream);

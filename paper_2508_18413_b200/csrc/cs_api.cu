@@ -820,6 +820,11 @@ static int do_scan_update(int var, int dtype, const void *e0, const void *e1, co
   const ScanPlan p = scan_plan(var, dtype, T, D, true);
   if (ws_bytes < p.ws_bytes) return fail(CS_ERR_CONFIG, "scan workspace too small");
   if (T == 0) return CS_OK;
+  {  // out and guess must not overlap (guess is read through the read-only path)
+    const size_t nb = (size_t)T * (size_t)D * (var == SCAN_BLOCK ? 2 : 1) * (size_t)esize(dtype);
+    const uintptr_t o0 = (uintptr_t)out, g0 = (uintptr_t)guess;
+    if (guess && o0 < g0 + nb && g0 < o0 + nb) return fail(CS_ERR_CONFIG, "scan update: out overlaps guess");
+  }
   // very long diag scans: the local scan + fix-up with the bookkeeping on each tile's
   // final states.  Newton iterates' maps often contract slowly, so the fix-up covers
   // much of each range and the two-pass scan stays ahead at moderate T (cfg 5, T = 1M:

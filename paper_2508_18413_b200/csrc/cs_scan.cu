@@ -1272,7 +1272,7 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
   auto check = [&](int k, int64_t r, int64_t idx, double xv) {
     if constexpr (UPDATE) {
       const double xd = (double)(ST)xv;
-      const double gap = fabs(xd - (double)a.guess[idx]);
+      const double gap = fabs(xd - (double)__ldg(a.guess + idx));  // guess never aliases out (API contract): not ordered behind the stores
       if (gap > a.atol + a.rtol * fabs(xd)) s_fail[s * kWideSeg + k] = 1;
       const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
       dmb = gb > dmb ? gb : dmb;
@@ -1386,7 +1386,7 @@ scan_cols_small(ScanArgs<ST> a) {
   auto check = [&](int k, int64_t idx, double xv) {
     if constexpr (UPDATE) {
       const double xd = (double)(ST)xv;
-      const double gap = fabs(xd - (double)a.guess[idx]);
+      const double gap = fabs(xd - (double)__ldg(a.guess + idx));  // guess never aliases out (API contract): not ordered behind the stores
       if (gap > a.atol + a.rtol * fabs(xd)) s_fail[s * rpt + k] = 1;
       const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
       dmb = gb > dmb ? gb : dmb;

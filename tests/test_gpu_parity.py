@@ -885,6 +885,25 @@ def test_update_scan_bookkeeping_multi_round(cuda_device, D, misalign, T):
     assert dmax == float(gap.max())
 
 
+def test_update_scan_rejects_out_overlapping_guess(cuda_device):
+    # the update kernels read guess through the read-only path while writing out
+    from paper_2508_18413_b200 import _lib
+
+    lib = _lib.load()
+    T, D = 1000, 4
+    j = torch.full((T, D), 0.5, device=cuda_device)
+    u = torch.ones((T, D), device=cuda_device)
+    s0 = torch.zeros(D, device=cuda_device)
+    g = torch.zeros((T, D), device=cuda_device)
+    lf = torch.zeros(T, dtype=torch.int32, device=cuda_device)
+    st = torch.zeros(40, dtype=torch.uint8, device=cuda_device)
+    wsb = lib.cs_scan_workspace_bytes(_lib.CS_MODE_DIAG, _lib.CS_F32, T, D)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=cuda_device)
+    rc = lib.cs_scan_diag_update(_lib.CS_F32, _lib.ptr(j), _lib.ptr(u), _lib.ptr(s0), _lib.ptr(g), T, D, _lib.ptr(ws),
+                                 wsb, _lib.ptr(g), 1e-5, 1e-5, 1, _lib.ptr(lf), _lib.ptr(st), _lib.stream_ptr())
+    assert rc == _lib.CS_ERR_CONFIG
+
+
 @pytest.mark.parametrize("kind,T", [("slow", 1_000_003), ("slow", 70_001), ("unit", 300_001), ("growing", 250_001),
                                     ("zero_entry", 500_001), ("mixed", 2_000_003), ("mixed", 65_537)])
 def test_update_scan_reduce_replay_extremes(cuda_device, kind, T):
