@@ -728,7 +728,7 @@ int cs_system_elements(const cs_system *sys, const cs_deer_config *cfg, int dtyp
   if (cfg->mode == CS_MODE_BLOCK && sys->kind != CS_SYS_LEAPFROG)
     return fail(CS_ERR_CONFIG, "system does not provide a block2x2 Jacobian estimate");
   cudaStream_t st = S(stream);
-  k_init_stats<<<1, 1, 0, st>>>(d_stats);
+  if (!wide || sys->T < 1) k_init_stats<<<1, 1, 0, st>>>(d_stats);  // (the wide prologue resets it itself)
   if (sys->T < 1) return CS_OK;
   cudaError_t e;
   if (wide) {

@@ -31,7 +31,13 @@ WideCtx g_wide[16];
 
 template <typename ST>
 __global__ void k_wide_prologue(cs_system sys, const ST *s0, const ST *guess, int64_t iteration, int nsamp,
-                                double *A) {
+                                double *A, cs_elem_stats *stats) {
+  if (stats && blockIdx.x == 0 && threadIdx.x == 0) {  // this update's stats record (the epilogue adds to it)
+    stats->bad_proposal = stats->bad_step = stats->bad_jacobian = kNoStep;
+    stats->picard_fail = 0;
+    stats->fail_rows = 0;
+    stats->dmax = 0.0;
+  }
   const int n = sys.dim / 2;
   const int64_t T = sys.T;
   const int64_t total = T * n;
@@ -437,7 +443,7 @@ static cudaError_t wide_run(const cs_system &sys, const cs_deer_config &cfg, int
   double *A = ctx.buf, *C = ctx.buf + (size_t)M * n;
   const int64_t tot = T * n;
   const unsigned g1 = (unsigned)((tot + 255) / 256 < 148 * 16 ? (tot + 255) / 256 : 148 * 16);
-  k_wide_prologue<ST><<<g1 < 1 ? 1 : g1, 256, 0, st>>>(sys, s0, guess, iteration, K, A);
+  k_wide_prologue<ST><<<g1 < 1 ? 1 : g1, 256, 0, st>>>(sys, s0, guess, iteration, K, A, stats);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // C (M x n) = A (M x n) P (n x n), row-major, on the FP64 tensor cores (cs_gemm.cuh)
