@@ -1196,6 +1196,17 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
   const bool colok = c < ncol;
   const int64_t rbase = rb * 64 + s * kWideSeg;
   double ej[kWideSeg], eu[kWideSeg], eb[kWideSeg], ec[kWideSeg], ed[kWideSeg], ev[kWideSeg];
+  // UPDATE: the previous guess of this thread's rows, loaded up front so the
+  // look-back hides them (loaded at the check they cost a round trip per row)
+  // (diag only: the block variant has no registers to spare and reads them at the check)
+  ST gx[(UPDATE && VAR == SCAN_DIAG) ? kWideSeg : 1];
+  if constexpr (UPDATE && VAR == SCAN_DIAG) {
+#pragma unroll
+    for (int k = 0; k < kWideSeg; ++k) {
+      const int64_t r = rbase + k;
+      gx[k] = (colok && r < a.T) ? __ldg(a.guess + r * ncol + c) : (ST)0;
+    }
+  }
   ColElem<VAR> run;
   run.ident();
 #pragma unroll
@@ -1269,10 +1280,10 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
     __syncthreads();
   }
   unsigned long long dmb = 0ull;
-  auto check = [&](int k, int64_t r, int64_t idx, double xv) {
+  auto check = [&](int k, double g, double xv) {
     if constexpr (UPDATE) {
       const double xd = (double)(ST)xv;
-      const double gap = fabs(xd - (double)__ldg(a.guess + idx));  // guess never aliases out (API contract): not ordered behind the stores
+      const double gap = fabs(xd - g);
       if (gap > a.atol + a.rtol * fabs(xd)) s_fail[s * kWideSeg + k] = 1;
       const unsigned long long gb = (unsigned long long)__double_as_longlong(gap);
       dmb = gb > dmb ? gb : dmb;
@@ -1290,7 +1301,7 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
     if constexpr (VAR == SCAN_DIAG) {
       x = ej[k] * x + eu[k];
       a.out[r * ncol + c] = (ST)x;
-      check(k, r, r * ncol + c, x);
+      check(k, (double)gx[k], x);
     } else {
       const double xa = ej[k] * x + eb[k] * v + eu[k];
       const double va = ec[k] * x + ed[k] * v + ev[k];
@@ -1298,8 +1309,10 @@ scan_cols(ScanArgs<ST> a, LookbackWs ws) {
       v = va;
       a.out[r * 2 * ncol + c] = (ST)x;
       a.out[r * 2 * ncol + ncol + c] = (ST)v;
-      check(k, r, r * 2 * ncol + c, x);
-      check(k, r, r * 2 * ncol + ncol + c, v);
+      if constexpr (UPDATE) {
+        check(k, (double)__ldg(a.guess + r * 2 * ncol + c), x);
+        check(k, (double)__ldg(a.guess + r * 2 * ncol + ncol + c), v);
+      }
     }
   }
   if constexpr (UPDATE) {
