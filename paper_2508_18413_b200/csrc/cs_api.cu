@@ -422,7 +422,8 @@ static int do_scan(int var, int dtype, const void *e0, const void *e1, const voi
     const char *e = getenv("CS_SCAN_RR_PLAIN_MAX_T");
     return e ? (int64_t)atoll(e) : ((int64_t)1 << 20);  // D = 18: 2^17 0.053 -> 0.046 ms, 2^18 0.069 -> 0.051, 2^19 0.085 -> 0.070; even at 2^20; local ahead above (tools/sweep_rr_plain.sh)
   }();
-  const bool rr = T < rr_max && scan_rr_eligible(var, T, D) && ws_bytes >= scan_rr_ws_bytes(dtype, T, D);
+  // (D > 64: every T from 2^16 -- the column scan's tile chain is latency-bound there)
+  const bool rr = (T < rr_max || D > 64) && scan_rr_eligible(var, T, D) && ws_bytes >= scan_rr_ws_bytes(dtype, T, D);
   cudaError_t e;
   if (rr) {
     if (dtype == CS_F64) {

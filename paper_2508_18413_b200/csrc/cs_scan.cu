@@ -2205,6 +2205,7 @@ scan_local_fixup(ScanArgs<ST> a, LocalWs ws, int B, int tmax, bool aligned) {
 // range from its true entry (each CTA folds the maps of the ranges before its
 // own while its first tile lands).  No fix-up, however slowly the maps contract (the
 // Newton iterates of cfg 5 do): j, u are read twice, guess once, s written once.
+constexpr int kRrMaxD = 256;  // one thread per column at least (nseg = 256 / D >= 1)
 CS_HD size_t rr_guess_off(int B, int D, size_t esz) {  // after the j/u slots, segment aggregates, row flags
   const size_t o = 4 * (size_t)B * D * esz + (size_t)(kScanThreads / D) * D * 2 * sizeof(double) + sizeof(int) * (size_t)B;
   return (o + 127) & ~(size_t)127;
@@ -2214,7 +2215,7 @@ __global__ void __launch_bounds__(kScanThreads, 2)
 scan_rr_reduce(ScanArgs<ST> a, LocalWs ws, int B, bool aligned) {
   constexpr int W = 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ double s_x[64], s_P[64];  // map of the tiles after the current one
+  __shared__ double s_x[kRrMaxD], s_P[kRrMaxD];  // map of the tiles after the current one
   __shared__ __align__(8) uint64_t s_bar[2];
   const int D = a.D, tid = threadIdx.x, G = gridDim.x, g = blockIdx.x;
   const size_t be = (size_t)B * D;
@@ -2289,7 +2290,7 @@ scan_rr_replay(ScanArgs<ST> a, LocalWs ws, int B, bool aligned) {
   using CT = ST;
   constexpr int W = 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ double s_x[64];
+  __shared__ double s_x[kRrMaxD];
   __shared__ unsigned long long s_dm;
   __shared__ unsigned s_nf;
   __shared__ __align__(8) uint64_t s_bar[2];
@@ -3000,7 +3001,7 @@ bool scan_rr_eligible(int var, int64_t T, int D) {
     const char *e = getenv("CS_SCAN_RR_MIN_T");
     return e ? (int64_t)atoll(e) : ((int64_t)1 << 16);
   }();
-  return var == SCAN_DIAG && D >= 1 && D <= 64 && T >= min_t;
+  return var == SCAN_DIAG && D >= 1 && D <= kRrMaxD && T >= min_t;
 }
 static int rr_kb() {  // j + u per tile
   static const int v = env_int("CS_SCAN_RR_KB", 4, 48, 32);  // cfg 5: 48 KB 64.5 ms, 32 KB 59.6 (tools/sweep_rr.sh)

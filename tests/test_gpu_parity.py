@@ -885,6 +885,52 @@ def test_update_scan_bookkeeping_multi_round(cuda_device, D, misalign, T):
     assert dmax == float(gap.max())
 
 
+@pytest.mark.parametrize("D,T,dtype", [(100, 100_000, torch.float64), (100, 70_001, torch.float32),
+                                       (256, 65_537, torch.float64), (65, 131_075, torch.float32)])
+def test_wide_reduce_replay_scans(cuda_device, D, T, dtype):
+    # 64 < D <= 256: reduce-then-replay for plain and update scans (one to four
+    # threads per column; cfg 3 diag's update scan is D = 100, f64) against the
+    # oracle scan and a direct evaluation of the bookkeeping
+    from paper_2508_18413_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(D + T)
+    j = rng.uniform(-0.999, 0.999, (T, D))
+    u = rng.normal(size=(T, D))
+    s0 = rng.normal(size=D)
+    cast = (lambda x: x.astype(np.float32).astype(np.float64)) if dtype == torch.float32 else (lambda x: x)
+    want = O.parallel_affine_solve(O.DiagElements(cast(j), cast(u)), cast(s0), workers=16)
+    tt = lambda x: torch.as_tensor(x, dtype=dtype, device=cuda_device)
+    jt, ut, s0t = tt(j), tt(u), tt(s0)
+    tol = dict(atol=1e-9, rtol=1e-9) if dtype == torch.float64 else dict(atol=3e-4, rtol=1e-4)
+    plain = cs.parallel_affine_solve(cs.DiagElements(jt, ut), s0t)
+    np.testing.assert_allclose(np_(plain), want, **tol)
+    g = torch.Generator(device=cuda_device).manual_seed(D)
+    wt = torch.as_tensor(want, device=cuda_device)
+    guess = (wt + torch.randn((T, D), generator=g, device=cuda_device, dtype=torch.float64) * 1e-4 *
+             (torch.rand((T, 1), generator=g, device=cuda_device) < 0.3)).to(dtype)
+    out = torch.empty_like(jt)
+    lf = torch.full((T,), 1, dtype=torch.int32, device=cuda_device)
+    st = torch.zeros(40, dtype=torch.uint8, device=cuda_device)
+    code = _lib.CS_F64 if dtype == torch.float64 else _lib.CS_F32
+    wsb = lib.cs_scan_workspace_bytes(_lib.CS_MODE_DIAG, code, T, D)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=cuda_device)
+    atol, rtol = 1e-5, 1e-5
+    _lib.check(lib.cs_scan_diag_update(code, _lib.ptr(jt), _lib.ptr(ut), _lib.ptr(s0t), _lib.ptr(out), T, D,
+                                       _lib.ptr(ws), wsb, _lib.ptr(guess), atol, rtol, 6, _lib.ptr(lf),
+                                       _lib.ptr(st), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(np_(out), want, **tol)
+    gap = (out.double() - guess.double()).abs()
+    fail = (gap > atol + rtol * out.double().abs()).any(dim=1)
+    want_lf = torch.where(fail, torch.tensor(6, dtype=torch.int32, device=cuda_device),
+                          torch.tensor(1, dtype=torch.int32, device=cuda_device))
+    assert torch.equal(lf, want_lf)
+    raw = st.cpu().numpy().tobytes()
+    assert int(np.frombuffer(raw[28:32], dtype=np.uint32)[0]) == int(fail.sum())
+    assert float(np.frombuffer(raw[32:40], dtype=np.float64)[0]) == float(gap.max())
+
+
 def test_update_scan_rejects_out_overlapping_guess(cuda_device):
     # the update kernels read guess through the read-only path while writing out
     from paper_2508_18413_b200 import _lib
