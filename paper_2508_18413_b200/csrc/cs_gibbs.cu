@@ -35,9 +35,11 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
   constexpr double kFloor = 1e-8;
   __shared__ long long smin[3];
   __shared__ unsigned scnt;
+  __shared__ uint64_t s_h2;  // the iteration's probe prefix (two hash rounds), once per CTA
   if (threadIdx.x == 0) {
     smin[0] = smin[1] = smin[2] = kNoStep;
     scnt = 0;
+    s_h2 = probe_prefix(A.sys.seed, iteration);
   }
   __syncthreads();
   const double *prm = A.sys.gibbs;
@@ -102,7 +104,7 @@ k_gibbs_elements_team(SolveArgs<ST> A, int iteration, const ST *guess, ST *jout,
   // reciprocal once; the tangents run in the storage precision TT (the estimate
   // only steers convergence, the step values above stay f64).
   using TT = ST;
-  const uint64_t h3 = hash_t(probe_prefix(A.sys.seed, iteration), (uint64_t)t);
+  const uint64_t h3 = hash_t(s_h2, (uint64_t)t);
   // coefficients of the tangent map, formed in TT: in fp32 storage mode these
   // are fp32 reciprocals (the f64 forward values above are only rounded once)
   TT inv_gt, inv_kS, inv_tau2n, inv_t2sq, n_sg2, inv_prec, c_mu, c_th, c_sg;
